@@ -1,0 +1,158 @@
+/* rrsvd_b200.h — C ABI of the B200-native TEBD two-site decimation library
+ * (librrsvd_b200.so, sm_100a).
+ *
+ * Drop-in boundary for the hot path of the reference C++ core (rrsvd::core, namespace
+ * rrsvd / rrsvd::tebd).  Each entry point names the reference interface it replaces
+ * (file:line under /root/reference/proj).  The reference has no C ABI of its own; the
+ * C++ shim in include/rrsvd_b200/rrsvd.hpp re-exposes these entry points with the
+ * reference's exact C++ signatures.
+ *
+ * Conventions
+ *  - Complex matrices are row-major, interleaved (re, im) float64 — the memory image of
+ *    rrsvd::DenseMatrix (dense_matrix.hpp:13-49) and of rrsvd::tebd::Tensor3 (mps.hpp:12-26).
+ *    They are passed as `double*` pointing at the first real part.
+ *  - Every matrix/vector pointer may be DEVICE memory (the fast path; no copies) or HOST memory
+ *    (pageable or pinned; the library stages it through its workspace — "end-to-end" mode).
+ *    The kind is detected per pointer with cudaPointerGetAttributes.
+ *  - All work is enqueued on the context's stream.  Functions that return host-visible results
+ *    (scalars, `info` structs, sizes) synchronise that stream before returning.
+ *  - Status codes mirror the reference's exceptions (errors.hpp:11-32):
+ *      0 ok, 1 contract_violation, 2 numeric_failure, 3 CUDA error.
+ *    rrsvd_b200_last_error(ctx) returns the message of the last failure on that context.
+ *  - Contexts are not thread-safe; use one per host thread / stream (SPEC.md:112,225 allow
+ *    concurrent calls on distinct inputs, which maps to distinct contexts).
+ *  - There is no CPU fallback: without a usable sm_100 device, ctx_create fails.
+ */
+#ifndef RRSVD_B200_H
+#define RRSVD_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RRSVD_B200_OK 0
+#define RRSVD_B200_CONTRACT_VIOLATION 1
+#define RRSVD_B200_NUMERIC_FAILURE 2
+#define RRSVD_B200_CUDA_ERROR 3
+
+#define RRSVD_B200_OP_N 0 /* op(X) = X            (CblasNoTrans,  linalg.cpp:30-31) */
+#define RRSVD_B200_OP_C 1 /* op(X) = X^H          (CblasConjTrans, linalg.cpp:30-31) */
+
+/* Source of the Gaussian sketch Omega when the caller does not pass one explicitly. */
+#define RRSVD_B200_OMEGA_REFERENCE 0 /* the reference stream of gaussian_test_matrix
+                                        (randomized.cpp:17-45,79-86): mt19937_64 + Box-Muller,
+                                        regenerated ON THE DEVICE from the same seed */
+#define RRSVD_B200_OMEGA_PHILOX 1    /* counter-based Philox4x32-10 + Box-Muller, fully
+                                        parallel (the GPU's own RNG; statistical parity) */
+
+typedef struct rrsvd_b200_ctx rrsvd_b200_ctx;
+
+/* == rrsvd::tebd::DecimationBackend (tebd.hpp:65-85), field for field. */
+typedef struct rrsvd_b200_backend {
+    int kind; /* 0 = Deterministic, 1 = Randomized */
+    uint64_t target_rank;      /* 0 -> chi_max */
+    uint64_t oversampling;     /* 0 -> target rank */
+    uint64_t power_iterations; /* q */
+    int accuracy_check;        /* fixed-precision mode (not yet supported: returns 1) */
+    double epsilon;
+    uint64_t probe_count;
+    uint64_t det_crossover; /* minor <= crossover -> deterministic SVD */
+    uint64_t seed;          /* base seed; the C ABI takes the per-call seed explicitly */
+} rrsvd_b200_backend;
+
+/* == the scalar part of rrsvd::tebd::DecimationResult (tebd.hpp:87-96). */
+typedef struct rrsvd_b200_decim_info {
+    double discarded;
+    uint64_t chi;
+    int randomized_path;
+    int tolerance_certified;
+    int pseudo_inverse_applied;
+} rrsvd_b200_decim_info;
+
+/* ---- context --------------------------------------------------------------------------- */
+const char* rrsvd_b200_version(void);
+/* device: CUDA ordinal; stream: a cudaStream_t (NULL = the library creates its own). */
+int rrsvd_b200_ctx_create(int device, void* stream, rrsvd_b200_ctx** out);
+void rrsvd_b200_ctx_destroy(rrsvd_b200_ctx* ctx);
+const char* rrsvd_b200_last_error(const rrsvd_b200_ctx* ctx);
+int rrsvd_b200_set_stream(rrsvd_b200_ctx* ctx, void* stream);
+int rrsvd_b200_synchronize(rrsvd_b200_ctx* ctx);
+/* Number of kernels this context has launched (for benchmark accounting). */
+uint64_t rrsvd_b200_launch_count(const rrsvd_b200_ctx* ctx);
+
+/* ---- L1: dense linear algebra (linalg.hpp:29-56) ---------------------------------------- */
+/* C (m x n) = op_a(A) (m x k) * op_b(B) (k x n); replaces rrsvd::gemm (linalg.cpp:20-35).
+ * Only op_b = N is supported.  lda/ldb/ldc are row strides in complex elements. */
+int rrsvd_b200_zgemm(rrsvd_b200_ctx* ctx, int op_a, int op_b, size_t m, size_t n, size_t k,
+                     const double* A, size_t lda, const double* B, size_t ldb, double* C,
+                     size_t ldc);
+/* Thin orthonormal basis Q (m x n, m >= n) of A plus R = Q^H A (n x n); replaces rrsvd::qr
+ * (linalg.cpp:49-65).  Like the reference, rank-deficient A yields no NaN; dependent columns
+ * of Q come back as zero columns instead of an arbitrary orthonormal completion. */
+int rrsvd_b200_qr(rrsvd_b200_ctx* ctx, const double* A, size_t m, size_t n, double* Q, double* R);
+/* Full economy SVD A = U diag(S) V^H (U m x r, S r, V n x r, r = min(m,n)), S non-increasing;
+ * replaces rrsvd::svd_full (linalg.cpp:67-88).  One-sided Jacobi on the device. */
+int rrsvd_b200_svd(rrsvd_b200_ctx* ctx, const double* A, size_t m, size_t n, double* U,
+                   double* S, double* V);
+/* ||A||_F (linalg.cpp:136-139). */
+int rrsvd_b200_frobenius_norm(rrsvd_b200_ctx* ctx, const double* A, size_t m, size_t n,
+                              double* out);
+
+/* ---- L2: randomized SVD (randomized.hpp:48-61) ------------------------------------------ */
+/* n x l Gaussian test matrix; mode RRSVD_B200_OMEGA_REFERENCE reproduces
+ * rrsvd::gaussian_test_matrix(n, l, seed) (randomized.cpp:79-86) to the last ulp of the
+ * device's log/sin/cos. */
+int rrsvd_b200_gaussian_test_matrix(rrsvd_b200_ctx* ctx, size_t n, size_t l, uint64_t seed,
+                                    int mode, double* out);
+/* rrsvd_sketched_svd (randomized.cpp:101-107): U m x l, S l, V n x l, *discarded = w.
+ * omega: NULL -> generated from `seed` with `omega_mode`; else the caller's n x l sketch
+ * ("Omega fed identically"). */
+int rrsvd_b200_sketched_svd(rrsvd_b200_ctx* ctx, const double* A, size_t m, size_t n, size_t l,
+                            size_t q, uint64_t seed, int omega_mode, const double* omega,
+                            double* U, double* S, double* V, double* discarded);
+/* rrsvd_fixed_rank (randomized.cpp:109-122): U m x k, S k, V n x k (U, V may be NULL). */
+int rrsvd_b200_fixed_rank(rrsvd_b200_ctx* ctx, const double* A, size_t m, size_t n, size_t k,
+                          size_t p, size_t q, uint64_t seed, int omega_mode, const double* omega,
+                          double* U, double* S, double* V, double* discarded);
+
+/* ---- L3: the TEBD two-site trio in the unfolded layout (tebd.hpp:98-110) ---------------
+ * Unfolded two-site matrix M: (cl*d1) x (d2*cr), row a*d1+i, column j*cr+b (tebd.cpp:150-155).
+ * Gamma tensors are Tensor3 (left, phys, right) row-major (mps.hpp:20-25). */
+/* build_theta (tebd.cpp:76-124): M = diag(ll (x) 1) G1 diag(lm) G2 diag(1 (x) lr);
+ * ll/lr NULL = open chain end (unit weights, tebd.cpp:82-87). */
+int rrsvd_b200_build_theta_unfolded(rrsvd_b200_ctx* ctx, const double* G1, const double* G2,
+                                    const double* ll, const double* lm, const double* lr,
+                                    size_t cl, size_t d1, size_t cm, size_t d2, size_t cr,
+                                    double* M);
+/* apply_gate_to_theta (tebd.cpp:126-139) on M: M_out[a] = G * M_in[a] for every left index a,
+ * where M[a] is the contiguous (d1*d2) x cr block.  G is (d1*d2)^2, rows/cols i*d2+j. */
+int rrsvd_b200_apply_gate_unfolded(rrsvd_b200_ctx* ctx, const double* G, size_t d1, size_t d2,
+                                   size_t cl, size_t cr, const double* M_in, double* M_out);
+/* decimate (tebd.cpp:141-237) of the unfolded M.  call_seed is the value the reference takes
+ * from backend.seed++ (tebd.cpp:162).  Outputs are sized for chi <= min(chi_max or minor, l):
+ * gamma_l cl x d1 x chi, lambda chi, gamma_r chi x d2 x cr (packed with the returned chi). */
+int rrsvd_b200_decimate_unfolded(rrsvd_b200_ctx* ctx, const double* M, size_t d1, size_t d2,
+                                 size_t cl, size_t cr, const double* ll, const double* lr,
+                                 size_t chi_max, double trunc_tol,
+                                 const rrsvd_b200_backend* backend, uint64_t call_seed,
+                                 int omega_mode, const double* omega, int renormalize,
+                                 double* gamma_l, double* lambda, double* gamma_r,
+                                 rrsvd_b200_decim_info* info);
+/* Layout conversions at the drop-in boundary: ThetaTensor (i, j, a, b) (tebd.hpp:23-28)
+ * <-> unfolded M (a*d1+i, j*cr+b). */
+int rrsvd_b200_theta_to_unfolded(rrsvd_b200_ctx* ctx, const double* theta, size_t d1, size_t d2,
+                                 size_t cl, size_t cr, double* M);
+int rrsvd_b200_unfolded_to_theta(rrsvd_b200_ctx* ctx, const double* M, size_t d1, size_t d2,
+                                 size_t cl, size_t cr, double* theta);
+
+/* ---- diagnostics ------------------------------------------------------------------------ */
+/* Measured device peak: what = 0 FP64 DMMA (mma.sync f64), 1 FP64 DFMA; TFLOP/s. */
+int rrsvd_b200_probe_peak(rrsvd_b200_ctx* ctx, int what, double* tflops);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

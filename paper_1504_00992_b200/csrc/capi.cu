@@ -1,0 +1,423 @@
+// capi.cu — the extern "C" drop-in boundary (include/rrsvd_b200.h).
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/rrsvd_b200.h"
+#include "pipeline.cuh"
+
+using namespace rb;
+
+namespace {
+
+template <class F>
+int api(rrsvd_b200_ctx* c, F&& f) {
+    if (c == nullptr) return kContract;
+    int code = kOk;
+    try {
+        cudaSetDevice(c->device);
+        f();
+    } catch (const Fail& e) {
+        code = e.code;
+    } catch (const std::exception& e) {
+        c->err = e.what();
+        code = kCuda;
+    }
+    ws_reset(c);
+    return code;
+}
+
+struct Scalars {  // host mirror of device scalars read back at the end of a call
+    int kept;
+    int nonfinite;
+    int pinv;
+    int pad;
+    double total_sq;
+    double discarded;
+};
+
+void read_scalars(rrsvd_b200_ctx* c, Scalars* dev, Scalars* host) {
+    check_cuda(c, cudaMemcpyAsync(host, dev, sizeof(Scalars), cudaMemcpyDeviceToHost, c->stream), "D2H scalars");
+    check_cuda(c, cudaStreamSynchronize(c->stream), "stream sync");
+}
+
+// Copy `bytes` from device buffer src to user pointer dst (device or host), row-pitched.
+void copy_out2d(rrsvd_b200_ctx* c, void* dst, size_t dpitch, const void* src, size_t spitch,
+                size_t width, size_t height) {
+    if (dst == nullptr || width == 0 || height == 0) return;
+    check_cuda(c, cudaMemcpy2DAsync(dst, dpitch, src, spitch, width, height, cudaMemcpyDefault, c->stream),
+               "copy out");
+}
+
+void copy_out(rrsvd_b200_ctx* c, void* dst, const void* src, size_t bytes) {
+    if (dst == nullptr || bytes == 0) return;
+    check_cuda(c, cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, c->stream), "copy out");
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* rrsvd_b200_version(void) { return "rrsvd_b200 0.1 (sm_100a, FP64 DMMA)"; }
+
+int rrsvd_b200_ctx_create(int device, void* stream, rrsvd_b200_ctx** out) {
+    if (out == nullptr) return kContract;
+    *out = nullptr;
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0 || device < 0 || device >= n) {
+        cudaGetLastError();
+        return kCuda;
+    }
+    cudaDeviceProp prop;
+    if (cudaGetDeviceProperties(&prop, device) != cudaSuccess || prop.major < 10) return kCuda;
+    auto* c = new rrsvd_b200_ctx();
+    c->device = device;
+    cudaSetDevice(device);
+    if (stream != nullptr) {
+        c->stream = static_cast<cudaStream_t>(stream);
+    } else {
+        if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) {
+            delete c;
+            return kCuda;
+        }
+        c->own_stream = true;
+    }
+    // keep workspace allocations cached in the stream-ordered pool
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+        uint64_t thr = ~0ull;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    *out = c;
+    return kOk;
+}
+
+void rrsvd_b200_ctx_destroy(rrsvd_b200_ctx* c) {
+    if (c == nullptr) return;
+    cudaSetDevice(c->device);
+    cudaStreamSynchronize(c->stream);
+    release_staged(c);
+    cudaStreamSynchronize(c->stream);
+    if (c->pinned) cudaFreeHost(c->pinned);
+    if (c->own_stream) cudaStreamDestroy(c->stream);
+    delete c;
+}
+
+const char* rrsvd_b200_last_error(const rrsvd_b200_ctx* c) { return c ? c->err.c_str() : "null context"; }
+
+int rrsvd_b200_set_stream(rrsvd_b200_ctx* c, void* stream) {
+    return api(c, [&] {
+        check_cuda(c, cudaStreamSynchronize(c->stream), "sync");
+        if (c->own_stream) cudaStreamDestroy(c->stream);
+        c->own_stream = false;
+        c->stream = static_cast<cudaStream_t>(stream);
+    });
+}
+
+int rrsvd_b200_synchronize(rrsvd_b200_ctx* c) {
+    return api(c, [&] { check_cuda(c, cudaStreamSynchronize(c->stream), "sync"); });
+}
+
+uint64_t rrsvd_b200_launch_count(const rrsvd_b200_ctx* c) { return c ? c->launches : 0; }
+
+// ------------------------------------------------------------------------------------------ L1
+
+int rrsvd_b200_zgemm(rrsvd_b200_ctx* c, int op_a, int op_b, size_t m, size_t n, size_t k,
+                     const double* A, size_t lda, const double* B, size_t ldb, double* C, size_t ldc) {
+    return api(c, [&] {
+        if (op_b != RRSVD_B200_OP_N) throw_contract(c, "zgemm: only op_b = N is supported");
+        if (op_a != RRSVD_B200_OP_N && op_a != RRSVD_B200_OP_C) throw_contract(c, "zgemm: bad op_a");
+        if (m == 0 || n == 0) return;
+        const size_t a_rows = op_a == RRSVD_B200_OP_N ? m : k;
+        std::vector<OutBuf> outs;
+        const auto* dA = static_cast<const cplx*>(stage_in(c, A, a_rows * lda * sizeof(cplx)));
+        const auto* dB = static_cast<const cplx*>(stage_in(c, B, k * ldb * sizeof(cplx)));
+        auto* dC = static_cast<cplx*>(stage_out(c, C, m * ldc * sizeof(cplx), outs));
+        if (k == 0) {
+            check_cuda(c, cudaMemsetAsync(dC, 0, m * ldc * sizeof(cplx), c->stream), "memset");
+        } else {
+            gemm(c, op_a == RRSVD_B200_OP_N ? kOpN : kOpC, (int)m, (int)n, (int)k, dA, (long long)lda, dB,
+                 (long long)ldb, dC, (long long)ldc);
+        }
+        finish_out(c, outs);
+    });
+}
+
+int rrsvd_b200_frobenius_norm(rrsvd_b200_ctx* c, const double* A, size_t m, size_t n, double* out) {
+    return api(c, [&] {
+        if (out == nullptr) throw_contract(c, "frobenius_norm: null output");
+        const size_t cnt = m * n;
+        if (cnt == 0) { *out = 0.0; return; }
+        const auto* dA = static_cast<const cplx*>(stage_in(c, A, cnt * sizeof(cplx)));
+        double* part = ws_get<double>(c, 2 * kNumSMs);
+        int* bad = ws_get<int>(c, 2 * kNumSMs);
+        auto* sc = ws_get<Scalars>(c, 1);
+        check_cuda(c, sumsq(dA, (long long)cnt, part, bad, &sc->total_sq, &sc->nonfinite, c->stream), "sumsq");
+        c->launches += 2;
+        Scalars h;
+        read_scalars(c, sc, &h);
+        *out = std::sqrt(h.total_sq);
+    });
+}
+
+int rrsvd_b200_qr(rrsvd_b200_ctx* c, const double* A, size_t m, size_t n, double* Q, double* R) {
+    return api(c, [&] {
+        if (m < n) throw_contract(c, "qr: requires rows >= cols");
+        if (n == 0) return;
+        std::vector<OutBuf> outs;
+        const auto* dA = static_cast<const cplx*>(stage_in(c, A, m * n * sizeof(cplx)));
+        auto* dQ = static_cast<cplx*>(stage_out(c, Q, m * n * sizeof(cplx), outs));
+        if (dQ == nullptr) dQ = ws_get<cplx>(c, m * n);
+        orth(c, dA, (int)m, (int)n, dQ);
+        if (R != nullptr) {
+            auto* dR = static_cast<cplx*>(stage_out(c, R, n * n * sizeof(cplx), outs));
+            gemm(c, kOpC, (int)n, (int)n, (int)m, dQ, (long long)n, dA, (long long)n, dR, (long long)n);
+        }
+        finish_out(c, outs);
+    });
+}
+
+int rrsvd_b200_svd(rrsvd_b200_ctx* c, const double* A, size_t m, size_t n, double* U, double* S,
+                   double* V) {
+    return api(c, [&] {
+        const size_t r = std::min(m, n);
+        if (r == 0) return;
+        std::vector<OutBuf> outs;
+        const auto* dA = static_cast<const cplx*>(stage_in(c, A, m * n * sizeof(cplx)));
+        auto* dU = static_cast<cplx*>(stage_out(c, U, m * r * sizeof(cplx), outs));
+        auto* dS = static_cast<double*>(stage_out(c, S, r * sizeof(double), outs));
+        auto* dV = static_cast<cplx*>(stage_out(c, V, n * r * sizeof(cplx), outs));
+        if (!dU) dU = ws_get<cplx>(c, m * r);
+        if (!dS) dS = ws_get<double>(c, r);
+        if (!dV) dV = ws_get<cplx>(c, n * r);
+        svd_jacobi(c, dA, (int)m, (int)n, dU, dS, dV);
+        finish_out(c, outs);
+    });
+}
+
+// ------------------------------------------------------------------------------------------ L2
+
+int rrsvd_b200_gaussian_test_matrix(rrsvd_b200_ctx* c, size_t n, size_t l, uint64_t seed, int mode,
+                                    double* out) {
+    return api(c, [&] {
+        if (l < 1 || n < l) throw_contract(c, "gaussian_test_matrix: requires n >= l >= 1");
+        std::vector<OutBuf> outs;
+        auto* d = static_cast<cplx*>(stage_out(c, out, n * l * sizeof(cplx), outs));
+        make_omega(c, (int)n, (int)l, seed, mode, d);
+        finish_out(c, outs);
+    });
+}
+
+static void sketch_common(rrsvd_b200_ctx* c, const double* A, size_t m, size_t n, size_t l, size_t q,
+                          uint64_t seed, int omega_mode, const double* omega, size_t keep, double* U,
+                          double* S, double* V, double* discarded) {
+    std::vector<OutBuf> outs;
+    const auto* dA = static_cast<const cplx*>(stage_in(c, A, m * n * sizeof(cplx)));
+    const cplx* dO = static_cast<const cplx*>(stage_in(c, omega, n * l * sizeof(cplx)));
+    if (dO == nullptr) {
+        cplx* o = ws_get<cplx>(c, n * l);
+        make_omega(c, (int)n, (int)l, seed, omega_mode, o);
+        dO = o;
+    }
+    cplx* dU = ws_get<cplx>(c, m * l);
+    cplx* dV = ws_get<cplx>(c, n * l);
+    double* dS = ws_get<double>(c, l);
+    rrsvd_core(c, dA, (int)m, (int)n, (int)l, (int)q, dO, dU, dS, dV);
+    double* part = ws_get<double>(c, 2 * kNumSMs);
+    int* bad = ws_get<int>(c, 2 * kNumSMs);
+    auto* sc = ws_get<Scalars>(c, 1);
+    check_cuda(c, sumsq(dA, (long long)(m * n), part, bad, &sc->total_sq, &sc->nonfinite, c->stream), "sumsq");
+    check_cuda(c, discarded_weight(dS, (int)keep, &sc->total_sq, &sc->discarded, c->stream), "weight");
+    c->launches += 3;
+    copy_out2d(c, U, keep * sizeof(cplx), dU, l * sizeof(cplx), keep * sizeof(cplx), m);
+    copy_out2d(c, V, keep * sizeof(cplx), dV, l * sizeof(cplx), keep * sizeof(cplx), n);
+    copy_out2d(c, S, keep * sizeof(double), dS, keep * sizeof(double), keep * sizeof(double), 1);
+    Scalars h;
+    read_scalars(c, sc, &h);
+    if (discarded) *discarded = h.discarded;
+}
+
+int rrsvd_b200_sketched_svd(rrsvd_b200_ctx* c, const double* A, size_t m, size_t n, size_t l, size_t q,
+                            uint64_t seed, int omega_mode, const double* omega, double* U, double* S,
+                            double* V, double* discarded) {
+    return api(c, [&] {
+        if (l > std::min(m, n)) throw_contract(c, "randomized_range_finder: l > min(m, n)");
+        if (l < 1) throw_contract(c, "gaussian_test_matrix: requires n >= l >= 1");
+        sketch_common(c, A, m, n, l, q, seed, omega_mode, omega, l, U, S, V, discarded);
+    });
+}
+
+int rrsvd_b200_fixed_rank(rrsvd_b200_ctx* c, const double* A, size_t m, size_t n, size_t k, size_t p,
+                          size_t q, uint64_t seed, int omega_mode, const double* omega, double* U,
+                          double* S, double* V, double* discarded) {
+    return api(c, [&] {
+        if (k < 2 || p < 2) throw_contract(c, "rrsvd_fixed_rank: requires k >= 2 and p >= 2");
+        if (k + p > std::min(m, n)) throw_contract(c, "rrsvd_fixed_rank: k + p exceeds min(m, n)");
+        sketch_common(c, A, m, n, k + p, q, seed, omega_mode, omega, k, U, S, V, discarded);
+    });
+}
+
+// ------------------------------------------------------------------------------------------ L3
+
+int rrsvd_b200_build_theta_unfolded(rrsvd_b200_ctx* c, const double* G1, const double* G2,
+                                    const double* ll, const double* lm, const double* lr, size_t cl,
+                                    size_t d1, size_t cm, size_t d2, size_t cr, double* M) {
+    return api(c, [&] {
+        const size_t m = cl * d1, n = d2 * cr;
+        if (m == 0 || n == 0) return;
+        if (lm == nullptr) throw_contract(c, "build_theta: missing bond lambda");
+        std::vector<OutBuf> outs;
+        const auto* dG1 = static_cast<const cplx*>(stage_in(c, G1, m * cm * sizeof(cplx)));
+        const auto* dG2 = static_cast<const cplx*>(stage_in(c, G2, cm * n * sizeof(cplx)));
+        const auto* dll = static_cast<const double*>(stage_in(c, ll, cl * sizeof(double)));
+        const auto* dlm = static_cast<const double*>(stage_in(c, lm, cm * sizeof(double)));
+        const auto* dlr = static_cast<const double*>(stage_in(c, lr, cr * sizeof(double)));
+        auto* dM = static_cast<cplx*>(stage_out(c, M, m * n * sizeof(cplx), outs));
+        Scale sc;
+        sc.rs = dll; sc.rs_div = (int)d1; sc.ks = dlm; sc.cs = dlr; sc.cs_mod = (int)cr;
+        if (cm == 0) check_cuda(c, cudaMemsetAsync(dM, 0, m * n * sizeof(cplx), c->stream), "memset");
+        else gemm(c, kOpN, (int)m, (int)n, (int)cm, dG1, (long long)cm, dG2, (long long)n, dM, (long long)n, sc);
+        finish_out(c, outs);
+    });
+}
+
+int rrsvd_b200_apply_gate_unfolded(rrsvd_b200_ctx* c, const double* G, size_t d1, size_t d2, size_t cl,
+                                   size_t cr, const double* M_in, double* M_out) {
+    return api(c, [&] {
+        const size_t dd = d1 * d2, tot = cl * dd * cr;
+        if (tot == 0) return;
+        if (M_in == M_out) throw_contract(c, "apply_gate: in-place application is not supported");
+        std::vector<OutBuf> outs;
+        const auto* dG = static_cast<const cplx*>(stage_in(c, G, dd * dd * sizeof(cplx)));
+        const auto* dI = static_cast<const cplx*>(stage_in(c, M_in, tot * sizeof(cplx)));
+        auto* dO = static_cast<cplx*>(stage_out(c, M_out, tot * sizeof(cplx), outs));
+        if (dd <= 16) {
+            check_cuda(c, gate_small(dG, (int)dd, (int)cl, (int)cr, dI, dO, c->stream), "gate_small");
+            c->launches++;
+        } else {
+            gemm(c, kOpN, (int)dd, (int)cr, (int)dd, dG, (long long)dd, dI, (long long)cr, dO, (long long)cr, {},
+                 (int)cl, 0, (long long)(dd * cr), (long long)(dd * cr));
+        }
+        finish_out(c, outs);
+    });
+}
+
+int rrsvd_b200_theta_to_unfolded(rrsvd_b200_ctx* c, const double* theta, size_t d1, size_t d2, size_t cl,
+                                 size_t cr, double* M) {
+    return api(c, [&] {
+        const size_t tot = d1 * d2 * cl * cr;
+        if (tot == 0) return;
+        std::vector<OutBuf> outs;
+        const auto* dT = static_cast<const cplx*>(stage_in(c, theta, tot * sizeof(cplx)));
+        auto* dM = static_cast<cplx*>(stage_out(c, M, tot * sizeof(cplx), outs));
+        check_cuda(c, theta_to_unfolded(dT, (int)d1, (int)d2, (int)cl, (int)cr, dM, c->stream), "unfold");
+        c->launches++;
+        finish_out(c, outs);
+    });
+}
+
+int rrsvd_b200_unfolded_to_theta(rrsvd_b200_ctx* c, const double* M, size_t d1, size_t d2, size_t cl,
+                                 size_t cr, double* theta) {
+    return api(c, [&] {
+        const size_t tot = d1 * d2 * cl * cr;
+        if (tot == 0) return;
+        std::vector<OutBuf> outs;
+        const auto* dM = static_cast<const cplx*>(stage_in(c, M, tot * sizeof(cplx)));
+        auto* dT = static_cast<cplx*>(stage_out(c, theta, tot * sizeof(cplx), outs));
+        check_cuda(c, unfolded_to_theta(dM, (int)d1, (int)d2, (int)cl, (int)cr, dT, c->stream), "fold");
+        c->launches++;
+        finish_out(c, outs);
+    });
+}
+
+int rrsvd_b200_decimate_unfolded(rrsvd_b200_ctx* c, const double* M, size_t d1, size_t d2, size_t cl,
+                                 size_t cr, const double* ll, const double* lr, size_t chi_max,
+                                 double trunc_tol, const rrsvd_b200_backend* be, uint64_t call_seed,
+                                 int omega_mode, const double* omega, int renormalize, double* gamma_l,
+                                 double* lambda, double* gamma_r, rrsvd_b200_decim_info* info) {
+    return api(c, [&] {
+        if (be == nullptr || info == nullptr) throw_contract(c, "decimate: null backend/info");
+        const size_t m = d1 * cl, n = d2 * cr, minor = std::min(m, n);
+        if (m == 0 || n == 0) throw_contract(c, "decimate: theta is identically zero");
+        const size_t k = be->target_rank != 0 ? be->target_rank : chi_max;
+        const bool randomized = be->kind == 1 && k != 0 && minor > be->det_crossover;
+        if (randomized && be->accuracy_check)
+            throw_contract(c, "decimate: accuracy_check (fixed-precision RRSVD) is not implemented on the device yet");
+        size_t ns = minor, l = 0;
+        if (randomized) {
+            const size_t p = be->oversampling != 0 ? be->oversampling : k;
+            l = std::min(k + p, minor);
+            ns = l;
+        }
+        size_t kmax = ns;
+        if (chi_max != 0) kmax = std::min(kmax, chi_max);
+
+        const auto* dM = static_cast<const cplx*>(stage_in(c, M, m * n * sizeof(cplx)));
+        const auto* dll = static_cast<const double*>(stage_in(c, ll, cl * sizeof(double)));
+        const auto* dlr = static_cast<const double*>(stage_in(c, lr, cr * sizeof(double)));
+        auto* sc = ws_get<Scalars>(c, 1);
+        double* part = ws_get<double>(c, 2 * kNumSMs);
+        int* bad = ws_get<int>(c, 2 * kNumSMs);
+        check_cuda(c, sumsq(dM, (long long)(m * n), part, bad, &sc->total_sq, &sc->nonfinite, c->stream), "sumsq");
+        c->launches += 2;
+
+        cplx* U = ws_get<cplx>(c, m * ns);
+        cplx* V = ws_get<cplx>(c, n * ns);
+        double* sig = ws_get<double>(c, ns);
+        if (randomized) {
+            const cplx* dO = static_cast<const cplx*>(stage_in(c, omega, n * l * sizeof(cplx)));
+            if (dO == nullptr) {
+                cplx* o = ws_get<cplx>(c, n * l);
+                make_omega(c, (int)n, (int)l, call_seed, omega_mode, o);
+                dO = o;
+            }
+            rrsvd_core(c, dM, (int)m, (int)n, (int)l, (int)be->power_iterations, dO, U, sig, V);
+        } else {
+            svd_jacobi(c, dM, (int)m, (int)n, U, sig, V);
+        }
+        // outputs: write straight into device buffers, else into workspace + exact D2H
+        const bool dev_gl = is_device_ptr(gamma_l), dev_lam = is_device_ptr(lambda), dev_gr = is_device_ptr(gamma_r);
+        cplx* gl = dev_gl ? reinterpret_cast<cplx*>(gamma_l) : ws_get<cplx>(c, m * kmax);
+        double* lam = dev_lam ? lambda : ws_get<double>(c, kmax);
+        cplx* gr = dev_gr ? reinterpret_cast<cplx*>(gamma_r) : ws_get<cplx>(c, kmax * n);
+        TruncArgs ta{};
+        ta.sigma = sig; ta.ns = (int)ns; ta.total_sq = &sc->total_sq; ta.trunc_tol = trunc_tol;
+        ta.cap = (long long)chi_max; ta.renormalize = renormalize; ta.kept = &sc->kept;
+        ta.lambda = lam; ta.discarded = &sc->discarded;
+        check_cuda(c, truncate(ta, c->stream), "truncate");
+        GammaArgs ga{};
+        ga.U = U; ga.ldu = (int)ns; ga.V = V; ga.ldv = (int)ns; ga.ll = dll; ga.lr = dlr;
+        ga.m = (int)m; ga.n = (int)n; ga.d1 = (int)d1; ga.cr = (int)cr; ga.kept = &sc->kept;
+        ga.gamma_l = gl; ga.gamma_r = gr; ga.pinv = &sc->pinv;
+        check_cuda(c, gamma_reshape(ga, (int)kmax, c->stream), "gamma_reshape");
+        c->launches += 4;
+        Scalars h;
+        read_scalars(c, sc, &h);
+        if (h.nonfinite) throw_contract(c, "decimate: theta has non-finite entries");
+        if (h.total_sq == 0.0) throw_contract(c, "decimate: theta is identically zero");
+        const size_t kept = (size_t)h.kept;
+        if (!dev_gl) copy_out(c, gamma_l, gl, m * kept * sizeof(cplx));
+        if (!dev_lam) copy_out(c, lambda, lam, kept * sizeof(double));
+        if (!dev_gr) copy_out(c, gamma_r, gr, kept * n * sizeof(cplx));
+        check_cuda(c, cudaStreamSynchronize(c->stream), "stream sync");
+        info->discarded = h.discarded;
+        info->chi = kept;
+        info->randomized_path = randomized ? 1 : 0;
+        info->tolerance_certified = 1;
+        info->pseudo_inverse_applied = h.pinv ? 1 : 0;
+    });
+}
+
+// ------------------------------------------------------------------------------------------ misc
+
+int rrsvd_b200_probe_peak(rrsvd_b200_ctx* c, int what, double* tflops) {
+    return api(c, [&] {
+        if (tflops == nullptr) throw_contract(c, "probe_peak: null output");
+        check_cuda(c, probe_peak(what, tflops, c->stream), "probe_peak");
+        c->launches += 2;
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,97 @@
+// ctx.cu — context, workspace and host/device staging.
+#include <cstring>
+#include <stdexcept>
+
+#include "ctx.cuh"
+
+namespace rb {
+
+namespace {
+struct Thrown : std::exception {
+    int code;
+    explicit Thrown(int c) : code(c) {}
+};
+}  // namespace
+
+int fail_cuda(cudaError_t e, const char* what, const char* file, int line) {
+    (void)e; (void)what; (void)file; (void)line;
+    return kCuda;
+}
+
+void throw_contract(rrsvd_b200_ctx* c, const std::string& msg) {
+    c->err = msg;
+    throw Fail{kContract};
+}
+void throw_numeric(rrsvd_b200_ctx* c, const std::string& msg) {
+    c->err = msg;
+    throw Fail{kNumeric};
+}
+void check_cuda(rrsvd_b200_ctx* c, cudaError_t e, const char* what) {
+    if (e == cudaSuccess) return;
+    c->err = std::string(what) + ": " + cudaGetErrorString(e);
+    throw Fail{kCuda};
+}
+
+// The workspace uses the device's stream-ordered memory pool: allocations are recycled
+// without synchronisation and released at the end of every public call.
+void* ws_alloc(rrsvd_b200_ctx* c, size_t bytes) {
+    void* p = nullptr;
+    if (bytes == 0) bytes = 16;
+    bytes = (bytes + 255) & ~size_t(255);
+    check_cuda(c, cudaMallocAsync(&p, bytes, c->stream), "cudaMallocAsync(workspace)");
+    c->staged.push_back(p);
+    return p;
+}
+
+void ws_reset(rrsvd_b200_ctx* c) { release_staged(c); }
+
+bool is_device_ptr(const void* p) {
+    if (p == nullptr) return false;
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+const void* stage_in(rrsvd_b200_ctx* c, const void* p, size_t bytes) {
+    if (p == nullptr || is_device_ptr(p)) return p;
+    void* d = ws_alloc(c, bytes);
+    check_cuda(c, cudaMemcpyAsync(d, p, bytes, cudaMemcpyHostToDevice, c->stream), "H2D staging");
+    return d;
+}
+
+void* stage_out(rrsvd_b200_ctx* c, void* p, size_t bytes, std::vector<OutBuf>& outs) {
+    if (p == nullptr || is_device_ptr(p)) return p;
+    void* d = ws_alloc(c, bytes);
+    outs.push_back({p, d, bytes});
+    return d;
+}
+
+void finish_out(rrsvd_b200_ctx* c, std::vector<OutBuf>& outs) {
+    for (const OutBuf& o : outs)
+        if (o.bytes)
+            check_cuda(c, cudaMemcpyAsync(o.host, o.dev, o.bytes, cudaMemcpyDeviceToHost, c->stream),
+                       "D2H staging");
+    check_cuda(c, cudaStreamSynchronize(c->stream), "stream sync");
+    outs.clear();
+}
+
+void release_staged(rrsvd_b200_ctx* c) {
+    for (void* p : c->staged) cudaFreeAsync(p, c->stream);
+    c->staged.clear();
+}
+
+void* pinned_scratch(rrsvd_b200_ctx* c, size_t bytes) {
+    if (bytes > c->pinned_cap) {
+        if (c->pinned) cudaFreeHost(c->pinned);
+        c->pinned = nullptr;
+        c->pinned_cap = 0;
+        check_cuda(c, cudaMallocHost(&c->pinned, bytes), "cudaMallocHost");
+        c->pinned_cap = bytes;
+    }
+    return c->pinned;
+}
+
+}  // namespace rb

@@ -1,0 +1,68 @@
+// ctx.cuh — library context: stream, device workspace arena, host staging, error state.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+
+struct rrsvd_b200_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    std::string err;
+    uint64_t launches = 0;
+
+    // Pinned host scratch for small results (info structs, scalars).
+    void* pinned = nullptr;
+    size_t pinned_cap = 0;
+    // Buffers allocated for host-pointer staging during one call, freed at call end.
+    std::vector<void*> staged;
+};
+
+namespace rb {
+
+// Status codes (include/rrsvd_b200.h)
+constexpr int kOk = 0, kContract = 1, kNumeric = 2, kCuda = 3;
+
+struct Fail {
+    int code;
+};
+
+int fail_cuda(cudaError_t e, const char* what, const char* file, int line);
+
+// Thrown inside the library, converted to a status code at the C boundary.
+[[noreturn]] void throw_contract(rrsvd_b200_ctx* c, const std::string& msg);
+[[noreturn]] void throw_numeric(rrsvd_b200_ctx* c, const std::string& msg);
+void check_cuda(rrsvd_b200_ctx* c, cudaError_t e, const char* what);
+inline void check_launch(rrsvd_b200_ctx* c, const char* what) {
+    c->launches++;
+    check_cuda(c, cudaGetLastError(), what);
+}
+
+// Workspace (stream-ordered pool; released at the end of each public call)
+void* ws_alloc(rrsvd_b200_ctx* c, size_t bytes);
+template <class T>
+T* ws_get(rrsvd_b200_ctx* c, size_t count) {
+    return static_cast<T*>(ws_alloc(c, count * sizeof(T)));
+}
+void ws_reset(rrsvd_b200_ctx* c);
+
+// Host/device pointer handling for the "device or host memory" ABI convention.
+bool is_device_ptr(const void* p);
+// Input: returns a device pointer holding `bytes` from p (H2D-staged if p is host memory).
+const void* stage_in(rrsvd_b200_ctx* c, const void* p, size_t bytes);
+// Output: returns a device pointer to write into; finish_out copies back if p was host memory.
+struct OutBuf {
+    void* host = nullptr;
+    void* dev = nullptr;
+    size_t bytes = 0;
+};
+void* stage_out(rrsvd_b200_ctx* c, void* p, size_t bytes, std::vector<OutBuf>& outs);
+void finish_out(rrsvd_b200_ctx* c, std::vector<OutBuf>& outs);  // D2H copies + sync
+void release_staged(rrsvd_b200_ctx* c);
+void* pinned_scratch(rrsvd_b200_ctx* c, size_t bytes);
+
+}  // namespace rb

@@ -1,0 +1,380 @@
+// smallla.cu — batched small dense kernels: Cholesky + inverse, cluster Jacobi SVD,
+// deterministic reductions.  See smallla.cuh.
+#include <cooperative_groups.h>
+
+#include "smallla.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace rb {
+
+namespace {
+
+constexpr double kU = 1.1102230246251565e-16;  // unit roundoff 2^-53
+constexpr double kEps = 2.220446049250313e-16;  // 2^-52
+
+// ============================================================================ Cholesky + inverse
+constexpr int CHOL_THREADS = 512;
+
+__device__ __forceinline__ int poff(int i, int l) { return i * l - (i * (i - 1)) / 2; }
+
+__global__ void __launch_bounds__(CHOL_THREADS) chol_inv_kernel(const __grid_constant__ CholBatch b) {
+    extern __shared__ __align__(16) unsigned char sm[];
+    const int p = blockIdx.x;
+    const int l = b.l[p];
+    const int npk = l * (l + 1) / 2;
+    cplx* P = reinterpret_cast<cplx*>(sm);
+    cplx* row = P + npk;
+    double* g0 = reinterpret_cast<double*>(row + l);
+    int* dead = reinterpret_cast<int*>(g0 + l);
+    __shared__ double s_shift;
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = CHOL_THREADS / 32;
+    const cplx* G = b.G[p];
+
+    for (int i = warp; i < l; i += nw)
+        for (int k = i + lane; k < l; k += 32) P[poff(i, l) + k - i] = G[(long long)i * l + k];
+    __syncthreads();
+    if (tid == 0) {
+        double tr = 0.0;
+        for (int i = 0; i < l; ++i) tr += P[poff(i, l)].x;
+        s_shift = b.shift_scale[p] * kU * tr;
+    }
+    __syncthreads();
+    for (int i = tid; i < l; i += CHOL_THREADS) {
+        P[poff(i, l)].x += s_shift;
+        P[poff(i, l)].y = 0.0;
+        g0[i] = P[poff(i, l)].x;
+    }
+    __syncthreads();
+
+    // ---- right-looking Cholesky, G = R^H R, R upper, row j of R overwrites row j of G.
+    for (int j = 0; j < l; ++j) {
+        const double d = P[poff(j, l)].x;
+        const bool isdead = !(d > kDepTol * g0[j]) || !(g0[j] > 0.0);
+        const double rjj = isdead ? 0.0 : sqrt(d);
+        const double inv = isdead ? 0.0 : 1.0 / rjj;
+        const int oj = poff(j, l);
+        for (int k = j + tid; k < l; k += CHOL_THREADS)
+            row[k] = (k == j) ? mk(rjj, 0.0) : cscale(P[oj + k - j], inv);
+        if (tid == 0) dead[j] = isdead ? 1 : 0;
+        __syncthreads();
+        for (int k = j + tid; k < l; k += CHOL_THREADS) P[oj + k - j] = row[k];
+        if (!isdead) {
+            for (int i = j + 1 + warp; i < l; i += nw) {
+                const cplx ri = cconj(row[i]);
+                const int oi = poff(i, l);
+                for (int k = i + lane; k < l; k += 32) {
+                    cplx v = P[oi + k - i];
+                    const cplx t = cmul(ri, row[k]);
+                    v.x -= t.x;
+                    v.y -= t.y;
+                    P[oi + k - i] = v;
+                }
+            }
+        }
+        __syncthreads();
+    }
+
+    // ---- in-place triangular inverse, column by column (T[0:j, j] = -t_jj * T_11 * R[0:j, j])
+    for (int j = 0; j < l; ++j) {
+        if (dead[j]) {
+            for (int i = tid; i <= j; i += CHOL_THREADS) P[poff(i, l) + j - i] = mk(0.0, 0.0);
+            __syncthreads();
+            continue;
+        }
+        const double tjj = 1.0 / P[poff(j, l)].x;
+        for (int i = warp; i < j; i += nw) {
+            const int oi = poff(i, l);
+            cplx x = mk(0.0, 0.0);
+            for (int q = i + lane; q < j; q += 32) cfma(x, P[oi + q - i], P[poff(q, l) + j - q]);
+            x = warp_sum(x);
+            if (lane == 0) row[i] = x;
+        }
+        __syncthreads();
+        for (int i = tid; i < j; i += CHOL_THREADS) P[poff(i, l) + j - i] = cscale(row[i], -tjj);
+        if (tid == 0) P[poff(j, l)] = mk(tjj, 0.0);
+        __syncthreads();
+    }
+
+    cplx* T = b.T[p];
+    for (int i = warp; i < l; i += nw)
+        for (int k = lane; k < l; k += 32)
+            T[(long long)i * l + k] = (k >= i) ? P[poff(i, l) + k - i] : mk(0.0, 0.0);
+    if (b.ndead[p] != nullptr && tid == 0) {
+        int n = 0;
+        for (int j = 0; j < l; ++j) n += dead[j];
+        *b.ndead[p] = n;
+    }
+}
+
+// ============================================================================ Jacobi SVD
+constexpr int JAC_THREADS = 256;
+constexpr int kMaxSweeps = 30;
+
+__device__ __forceinline__ int circle(int i, int t, int n) {  // round-robin slot -> player
+    return i == 0 ? 0 : ((i - 1 + t) % (n - 1)) + 1;
+}
+
+__global__ void __launch_bounds__(JAC_THREADS) jacobi_kernel(const __grid_constant__ JacobiBatch b) {
+    extern __shared__ __align__(16) unsigned char sm[];
+    cg::cluster_group cluster = cg::this_cluster();
+    const int cs = (int)cluster.num_blocks();
+    const int rank = (int)cluster.block_rank();
+    const int p = blockIdx.x / cs;
+    const int r = b.r[p], c = b.c[p], ld = r + c;
+    const int nblk = 2 * cs;
+    const int bs = (c + nblk - 1) / nblk;
+    cplx* col = reinterpret_cast<cplx*>(sm);  // [2bs][ld]
+    __shared__ int cnt[2];
+    __shared__ int s_rot;
+    cplx* W = b.W[p];
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = JAC_THREADS / 32;
+    const double tol = sqrt((double)max(r, 1)) * kEps;
+    if (tid == 0) { cnt[0] = cnt[1] = 0; }
+    cluster.sync();
+
+    int sweep = 0;
+    for (; sweep < kMaxSweeps; ++sweep) {
+        for (int t = 0; t < nblk - 1; ++t) {
+            const int blkA = circle(rank, t, nblk), blkB = circle(nblk - 1 - rank, t, nblk);
+            // load the 2*bs columns (column-major, contiguous) through L2
+            for (int lc = 0; lc < 2 * bs; ++lc) {
+                const int g = (lc < bs) ? blkA * bs + lc : blkB * bs + (lc - bs);
+                if (g >= c) continue;
+                const cplx* src = W + (long long)g * ld;
+                for (int rr = tid; rr < ld; rr += JAC_THREADS) cp_async16(col + lc * ld + rr, src + rr, true);
+            }
+            cp_async_commit();
+            cp_async_wait<0>();
+            if (tid == 0) s_rot = 0;
+            __syncthreads();
+            int myrot = 0;
+            const int n2 = 2 * bs;
+            for (int ti = 0; ti < n2 - 1; ++ti) {
+                for (int k = warp; k < bs; k += nw) {
+                    const int lp = circle(k, ti, n2), lq = circle(n2 - 1 - k, ti, n2);
+                    const int gp = (lp < bs) ? blkA * bs + lp : blkB * bs + (lp - bs);
+                    const int gq = (lq < bs) ? blkA * bs + lq : blkB * bs + (lq - bs);
+                    if (gp >= c || gq >= c) continue;
+                    cplx* xp = col + lp * ld;
+                    cplx* xq = col + lq * ld;
+                    double a = 0.0, bb = 0.0;
+                    cplx g = mk(0.0, 0.0);
+                    for (int rr = lane; rr < r; rr += 32) {
+                        const cplx u = xp[rr], v = xq[rr];
+                        a += cabs2(u);
+                        bb += cabs2(v);
+                        cfmac(g, u, v);
+                    }
+                    a = warp_sum(a);
+                    bb = warp_sum(bb);
+                    g = warp_sum(g);
+                    const double ag = hypot(g.x, g.y);
+                    if (!(a > 0.0) || !(bb > 0.0) || !(ag > tol * sqrt(a) * sqrt(bb))) continue;
+                    ++myrot;
+                    const cplx e = mk(g.x / ag, -g.y / ag);  // conj(g)/|g|
+                    const double zeta = (bb - a) / (2.0 * ag);
+                    const double tt = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + hypot(1.0, zeta));
+                    const double cc = 1.0 / sqrt(1.0 + tt * tt);
+                    const double ss = cc * tt;
+                    for (int rr = lane; rr < ld; rr += 32) {
+                        const cplx u = xp[rr];
+                        const cplx ev = cmul(e, xq[rr]);
+                        xp[rr] = mk(cc * u.x - ss * ev.x, cc * u.y - ss * ev.y);
+                        xq[rr] = mk(ss * u.x + cc * ev.x, ss * u.y + cc * ev.y);
+                    }
+                }
+                __syncthreads();
+            }
+            if (lane == 0 && myrot) atomicAdd(&s_rot, myrot);
+            __syncthreads();
+            if (tid == 0) cnt[sweep & 1] += s_rot;
+            for (int lc = 0; lc < 2 * bs; ++lc) {
+                const int g = (lc < bs) ? blkA * bs + lc : blkB * bs + (lc - bs);
+                if (g >= c) continue;
+                cplx* dst = W + (long long)g * ld;
+                for (int rr = tid; rr < ld; rr += JAC_THREADS) dst[rr] = col[lc * ld + rr];
+            }
+            __threadfence();
+            cluster.sync();
+            // every peer is past its end-of-previous-sweep read of our counters: recycle the slot
+            if (t == 0 && tid == 0) cnt[(sweep + 1) & 1] = 0;
+        }
+        // convergence: sum of all CTAs' rotation counts of this sweep (read through DSMEM)
+        int total = 0;
+        for (int q = 0; q < cs; ++q) {
+            const int* peer = cluster.map_shared_rank(cnt, q);
+            total += peer[sweep & 1];
+        }
+        if (total == 0) break;
+    }
+    cluster.sync();  // peers may still read our counters
+    if (rank == 0 && tid == 0 && b.sweeps[p] != nullptr) *b.sweeps[p] = sweep + 1;
+}
+
+__global__ void jacobi_init_kernel(const __grid_constant__ JacobiInitBatch b) {
+    const int p = blockIdx.y;
+    const int r = b.r[p], c = b.c[p], ld = r + c;
+    const long long total = (long long)c * ld;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+         e += (long long)gridDim.x * blockDim.x) {
+        const int cc = (int)(e / ld), rr = (int)(e % ld);
+        cplx v;
+        if (rr < r) {
+            v = b.adj[p] ? cconj(b.A[p][(long long)cc * b.lda[p] + rr]) : b.A[p][(long long)rr * b.lda[p] + cc];
+        } else {
+            v = mk((rr - r) == cc ? 1.0 : 0.0, 0.0);
+        }
+        b.W[p][e] = v;
+    }
+}
+
+__global__ void __launch_bounds__(256) jacobi_finish_kernel(const __grid_constant__ JacobiFinBatch b) {
+    extern __shared__ __align__(16) unsigned char sm[];
+    const int p = blockIdx.x;
+    const int r = b.r[p], c = b.c[p], ld = r + c;
+    double* sig = reinterpret_cast<double*>(sm);
+    int* pos = reinterpret_cast<int*>(sig + c);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x / 32;
+    const cplx* W = b.W[p];
+    for (int j = warp; j < c; j += nw) {
+        double a = 0.0;
+        for (int rr = lane; rr < r; rr += 32) a += cabs2(W[(long long)j * ld + rr]);
+        a = warp_sum(a);
+        if (lane == 0) sig[j] = sqrt(a);
+    }
+    __syncthreads();
+    for (int j = tid; j < c; j += blockDim.x) {
+        int rk = 0;
+        const double sj = sig[j];
+        for (int i = 0; i < c; ++i) rk += (sig[i] > sj) || (sig[i] == sj && i < j);
+        pos[j] = rk;
+    }
+    __syncthreads();
+    if (b.sigma[p])
+        for (int j = tid; j < c; j += blockDim.x) b.sigma[p][pos[j]] = sig[j];
+    if (b.Xn[p]) {
+        cplx* Xn = b.Xn[p];
+        for (int j = warp; j < c; j += nw) {
+            const double inv = sig[j] > 0.0 ? 1.0 / sig[j] : 0.0;
+            const int pj = pos[j];
+            for (int rr = lane; rr < r; rr += 32) Xn[(long long)rr * c + pj] = cscale(W[(long long)j * ld + rr], inv);
+        }
+    }
+    if (b.Js[p]) {
+        cplx* Js = b.Js[p];
+        for (int j = warp; j < c; j += nw) {
+            const int pj = pos[j];
+            for (int i = lane; i < c; i += 32) Js[(long long)i * c + pj] = W[(long long)j * ld + r + i];
+        }
+    }
+}
+
+// ============================================================================ reductions
+constexpr int RED_BLOCKS = 2 * kNumSMs, RED_THREADS = 256;
+
+__global__ void __launch_bounds__(RED_THREADS) sumsq_partial(const cplx* __restrict__ a, long long n,
+                                                             double* partial, int* bad) {
+    double s = 0.0;
+    int nb = 0;
+    for (long long i = blockIdx.x * (long long)RED_THREADS + threadIdx.x; i < n;
+         i += (long long)RED_BLOCKS * RED_THREADS) {
+        const cplx v = a[i];
+        nb += !(isfinite(v.x) && isfinite(v.y));
+        s += cabs2(v);
+    }
+    __shared__ double ss[RED_THREADS / 32];
+    __shared__ int sb[RED_THREADS / 32];
+    s = warp_sum(s);
+    for (int o = 16; o > 0; o >>= 1) nb += __shfl_xor_sync(0xffffffffu, nb, o);
+    if ((threadIdx.x & 31) == 0) { ss[threadIdx.x >> 5] = s; sb[threadIdx.x >> 5] = nb; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        int tb = 0;
+        for (int w = 0; w < RED_THREADS / 32; ++w) { t += ss[w]; tb += sb[w]; }
+        partial[blockIdx.x] = t;
+        bad[blockIdx.x] = tb;
+    }
+}
+
+__global__ void sumsq_final(const double* partial, const int* bad, double* out, int* nonfinite) {
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        int tb = 0;
+        for (int i = 0; i < RED_BLOCKS; ++i) { t += partial[i]; tb += bad[i]; }
+        *out = t;
+        if (nonfinite) *nonfinite = tb;
+    }
+}
+
+}  // namespace
+
+cudaError_t chol_inv(const CholBatch& b, int max_l, cudaStream_t s) {
+    if (b.count == 0) return cudaSuccess;
+    const size_t smem = (size_t)max_l * (max_l + 1) / 2 * sizeof(cplx) + max_l * sizeof(cplx) +
+                        max_l * sizeof(double) + max_l * sizeof(int);
+    cudaError_t e = cudaFuncSetAttribute(chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    chol_inv_kernel<<<b.count, CHOL_THREADS, smem, s>>>(b);
+    return cudaGetLastError();
+}
+
+cudaError_t jacobi_init(const JacobiInitBatch& b, cudaStream_t s) {
+    if (b.count == 0) return cudaSuccess;
+    jacobi_init_kernel<<<dim3(64, b.count), 256, 0, s>>>(b);
+    return cudaGetLastError();
+}
+
+// Chooses the cluster size (8 portable, else 16 non-portable) so that a CTA's block pair fits
+// in shared memory; returns cudaErrorInvalidValue if even 16 CTAs cannot hold it.
+cudaError_t jacobi_svd(const JacobiBatch& b, int max_r, int max_c, cudaStream_t s) {
+    if (b.count == 0) return cudaSuccess;
+    const int ld = max_r + max_c;
+    int cs = 8;
+    auto need = [&](int csz) {
+        const int bs = (max_c + 2 * csz - 1) / (2 * csz);
+        return (size_t)2 * bs * ld * sizeof(cplx);
+    };
+    const size_t kBudget = 200 * 1024;
+    if (need(8) > kBudget) cs = 16;
+    if (need(cs) > kBudget) return cudaErrorInvalidValue;
+    const size_t smem = need(cs);
+    cudaError_t e = cudaFuncSetAttribute(jacobi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    if (cs > 8) {
+        e = cudaFuncSetAttribute(jacobi_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        if (e != cudaSuccess) return e;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(cs * b.count);
+    cfg.blockDim = dim3(JAC_THREADS);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = cs;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, jacobi_kernel, b);
+}
+
+cudaError_t jacobi_finish(const JacobiFinBatch& b, int max_c, cudaStream_t s) {
+    if (b.count == 0) return cudaSuccess;
+    const size_t smem = (size_t)max_c * (sizeof(double) + sizeof(int));
+    jacobi_finish_kernel<<<b.count, 256, smem, s>>>(b);
+    return cudaGetLastError();
+}
+
+cudaError_t sumsq(const cplx* a, long long n, double* partial, int* partial_bad, double* out_sq,
+                  int* out_nonfinite, cudaStream_t s) {
+    sumsq_partial<<<RED_BLOCKS, RED_THREADS, 0, s>>>(a, n, partial, partial_bad);
+    sumsq_final<<<1, 32, 0, s>>>(partial, partial_bad, out_sq, out_nonfinite);
+    return cudaGetLastError();
+}
+
+}  // namespace rb

@@ -1,0 +1,72 @@
+// smallla.cuh — small dense linear algebra kernels of the RRSVD pipeline (batched).
+#pragma once
+#include "common.cuh"
+
+namespace rb {
+
+constexpr int kMaxSmall = 32;  // problems per launch of the small-matrix kernels
+
+// ---- Cholesky + triangular inverse (the "R^-1" of one CholeskyQR pass) -------------------
+// G (l x l, Hermitian, row-major) -> T = R^-1 (l x l upper, zeros below), G (+ s I) = R^H R.
+// Columns whose Cholesky pivot falls below kDepTol * (original diagonal) are numerically
+// dependent: their T column is zeroed, so the orthonormalised basis gets a zero column
+// (the reference's Householder QR returns an arbitrary orthonormal completion there,
+// linalg.hpp:35-37; either way no NaN and an unchanged span).
+constexpr double kDepTol = 1e-12;
+constexpr int kMaxCholL = 168;  // packed upper triangle must fit in 227 KB of shared memory
+
+struct CholBatch {
+    int count;
+    int l[kMaxSmall];
+    const cplx* G[kMaxSmall];
+    cplx* T[kMaxSmall];
+    double shift_scale[kMaxSmall];  // 0: no shift; else s = shift_scale * u * trace(G)
+    int* ndead[kMaxSmall];          // nullable: number of dependent columns found
+};
+cudaError_t chol_inv(const CholBatch& b, int max_l, cudaStream_t s);
+
+// ---- One-sided (Hestenes) Jacobi SVD ------------------------------------------------------
+// Works on W (column-major, ld = r + c): rows [0, r) hold X (r x c), rows [r, r + c) hold the
+// accumulated rotations J (initialised to I).  On exit X·J_total has orthogonal columns.
+// One thread-block cluster per problem: 2*cs column blocks, cs CTAs, round-robin block
+// pairing with a cluster barrier between rounds (data round-trips through L2).
+struct JacobiBatch {
+    int count;
+    int r[kMaxSmall], c[kMaxSmall];
+    cplx* W[kMaxSmall];
+    int* sweeps[kMaxSmall];  // nullable: sweeps used
+};
+cudaError_t jacobi_svd(const JacobiBatch& b, int max_r, int max_c, cudaStream_t s);
+
+// Load W from a row-major matrix: X = A (r x c) if !adj, or X = A^H when adj (A is c x r);
+// J = I.
+struct JacobiInitBatch {
+    int count;
+    int r[kMaxSmall], c[kMaxSmall];
+    const cplx* A[kMaxSmall];
+    int lda[kMaxSmall];
+    int adj[kMaxSmall];
+    cplx* W[kMaxSmall];
+};
+cudaError_t jacobi_init(const JacobiInitBatch& b, cudaStream_t s);
+
+// After convergence: sigma_j = ||X_j||, sorted non-increasing (ties by index);
+// Xn (r x c row-major, ld c) = normalised X columns in sorted order (zero for sigma = 0);
+// Js (c x c row-major) = J columns in sorted order.  Either output may be null.
+struct JacobiFinBatch {
+    int count;
+    int r[kMaxSmall], c[kMaxSmall];
+    const cplx* W[kMaxSmall];
+    double* sigma[kMaxSmall];
+    cplx* Xn[kMaxSmall];
+    cplx* Js[kMaxSmall];
+};
+cudaError_t jacobi_finish(const JacobiFinBatch& b, int max_c, cudaStream_t s);
+
+// ---- reductions -----------------------------------------------------------------------------
+// sum |a_i|^2 over n complex values, deterministic two-level order; also counts non-finite.
+// partial: >= 2*148 doubles + 2*148 ints of scratch. out_sq / out_nonfinite: device scalars.
+cudaError_t sumsq(const cplx* a, long long n, double* partial, int* partial_bad, double* out_sq,
+                  int* out_nonfinite, cudaStream_t s);
+
+}  // namespace rb

@@ -1,0 +1,374 @@
+// tebd_kernels.cu — sketch generation, gate for small d, layout conversion, truncation,
+// Gamma reshape, peak probes.  See tebd_kernels.cuh.
+#include "tebd_kernels.cuh"
+
+namespace rb {
+
+namespace {
+
+// ============================================================================ mt19937_64
+constexpr int MT_N = 312, MT_M = 156;
+constexpr unsigned long long MT_A = 0xB5026F5AA96619E9ull;
+constexpr unsigned long long MT_UM = 0xFFFFFFFF80000000ull, MT_LM = 0x7FFFFFFFull;
+
+__device__ __forceinline__ unsigned long long mt_twist(unsigned long long cur, unsigned long long nxt) {
+    const unsigned long long y = (cur & MT_UM) | (nxt & MT_LM);
+    return (y >> 1) ^ ((y & 1ull) ? MT_A : 0ull);
+}
+__device__ __forceinline__ unsigned long long mt_temper(unsigned long long y) {
+    y ^= (y >> 29) & 0x5555555555555555ull;
+    y ^= (y << 17) & 0x71D67FFFEDA60000ull;
+    y ^= (y << 37) & 0xFFF7EEE000000000ull;
+    y ^= (y >> 43);
+    return y;
+}
+
+// One CTA: the twist of a 312-word state has two dependency-free phases
+// (i < 156 reads only old words; i >= 156 reads words rewritten in phase 1).
+__global__ void __launch_bounds__(320) mt_draws_kernel(uint64_t seed, long long rounds,
+                                                       unsigned long long* __restrict__ out) {
+    __shared__ unsigned long long st[2][MT_N];
+    const int t = threadIdx.x;
+    if (t == 0) {
+        unsigned long long x = seed;
+        st[0][0] = x;
+        for (int i = 1; i < MT_N; ++i) {
+            x = 6364136223846793005ull * (x ^ (x >> 62)) + (unsigned long long)i;
+            st[0][i] = x;
+        }
+    }
+    __syncthreads();
+    int cur = 0;
+    for (long long rd = 0; rd < rounds; ++rd) {
+        const unsigned long long* o = st[cur];
+        unsigned long long* nw = st[cur ^ 1];
+        if (t < MT_M) nw[t] = o[t + MT_M] ^ mt_twist(o[t], o[t + 1]);
+        __syncthreads();
+        if (t >= MT_M && t < MT_N) {
+            const unsigned long long nxt = (t + 1 < MT_N) ? o[t + 1] : nw[0];
+            nw[t] = nw[t - MT_M] ^ mt_twist(o[t], nxt);
+        }
+        __syncthreads();
+        if (t < MT_N) out[rd * MT_N + t] = mt_temper(nw[t]);
+        cur ^= 1;
+    }
+}
+
+__device__ __forceinline__ cplx box_muller(unsigned long long x1, unsigned long long x2) {
+    const double u1 = ((double)(x1 >> 11) + 1.0) * 0x1p-53;  // (0, 1]
+    const double u2 = (double)(x2 >> 11) * 0x1p-53;          // [0, 1)
+    const double radius = sqrt(-2.0 * log(u1));
+    const double angle = 2.0 * 3.141592653589793 * u2;
+    double sn, cs;
+    sincos(angle, &sn, &cs);
+    return mk(radius * cs, radius * sn);
+}
+
+__global__ void box_muller_kernel(const unsigned long long* __restrict__ draws, long long n, cplx* out) {
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n;
+         e += (long long)gridDim.x * blockDim.x)
+        out[e] = box_muller(draws[2 * e], draws[2 * e + 1]);
+}
+
+// ============================================================================ Philox4x32-10
+__device__ __forceinline__ void philox_round(uint32_t c[4], const uint32_t k[2]) {
+    const uint32_t M0 = 0xD2511F53u, M1 = 0xCD9E8D57u;
+    const uint32_t hi0 = __umulhi(M0, c[0]), lo0 = M0 * c[0];
+    const uint32_t hi1 = __umulhi(M1, c[2]), lo1 = M1 * c[2];
+    const uint32_t n0 = hi1 ^ c[1] ^ k[0], n2 = hi0 ^ c[3] ^ k[1];
+    c[0] = n0; c[1] = lo1; c[2] = n2; c[3] = lo0;
+}
+
+__global__ void philox_kernel(uint64_t seed, long long n, cplx* out) {
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n;
+         e += (long long)gridDim.x * blockDim.x) {
+        uint32_t c[4] = {(uint32_t)e, (uint32_t)(e >> 32), 0x243F6A88u, 0x85A308D3u};
+        uint32_t k[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
+#pragma unroll
+        for (int r = 0; r < 10; ++r) {
+            philox_round(c, k);
+            k[0] += 0x9E3779B9u;
+            k[1] += 0xBB67AE85u;
+        }
+        const unsigned long long x1 = ((unsigned long long)c[1] << 32) | c[0];
+        const unsigned long long x2 = ((unsigned long long)c[3] << 32) | c[2];
+        out[e] = box_muller(x1, x2);
+    }
+}
+
+// ============================================================================ gate (small dd)
+template <int MAXD>
+__global__ void gate_small_kernel(const cplx* __restrict__ G, int dd, int cl, int cr,
+                                  const cplx* __restrict__ Min, cplx* __restrict__ Mout) {
+    __shared__ cplx sg[MAXD * MAXD];
+    for (int i = threadIdx.x; i < dd * dd; i += blockDim.x) sg[i] = G[i];
+    __syncthreads();
+    const long long cols = (long long)cl * cr;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < cols;
+         e += (long long)gridDim.x * blockDim.x) {
+        const long long a = e / cr, b = e % cr;
+        const cplx* src = Min + a * dd * cr + b;
+        cplx v[MAXD];
+#pragma unroll
+        for (int y = 0; y < MAXD; ++y) v[y] = y < dd ? src[(long long)y * cr] : mk(0.0, 0.0);
+        cplx* dst = Mout + a * dd * cr + b;
+#pragma unroll
+        for (int x = 0; x < MAXD; ++x) {
+            if (x >= dd) break;
+            cplx s = mk(0.0, 0.0);
+#pragma unroll
+            for (int y = 0; y < MAXD; ++y)
+                if (y < dd) cfma(s, sg[x * dd + y], v[y]);
+            dst[(long long)x * cr] = s;
+        }
+    }
+}
+
+// ============================================================================ layout
+__global__ void theta_unfold_kernel(const cplx* __restrict__ src, int d1, int d2, int cl, int cr,
+                                    cplx* __restrict__ dst, int to_unfolded) {
+    // one row of length cr per (i, j, a)
+    const long long rows = (long long)d1 * d2 * cl;
+    for (long long rw = blockIdx.x; rw < rows; rw += gridDim.x) {
+        const int a = (int)(rw % cl);
+        const int j = (int)((rw / cl) % d2);
+        const int i = (int)(rw / ((long long)cl * d2));
+        const long long th = (((long long)i * d2 + j) * cl + a) * cr;
+        const long long un = ((long long)a * d1 + i) * ((long long)d2 * cr) + (long long)j * cr;
+        for (int b = threadIdx.x; b < cr; b += blockDim.x) {
+            if (to_unfolded) dst[un + b] = src[th + b];
+            else dst[th + b] = src[un + b];
+        }
+    }
+}
+
+// ============================================================================ truncation
+__global__ void truncate_kernel(const TruncArgs a) {
+    if (threadIdx.x != 0) return;
+    const double total = *a.total_sq;
+    const double sigma1 = a.ns > 0 ? a.sigma[0] : 0.0;
+    int kept = 0;
+    for (int i = 0; i < a.ns; ++i) {
+        const double s = a.sigma[i];
+        if (s <= sigma1 * 1e-15) break;
+        if (a.trunc_tol > 0.0 && s * s / total < a.trunc_tol) break;
+        ++kept;
+    }
+    if (kept < 1) kept = 1;
+    if (a.cap > 0 && kept > a.cap) kept = (int)a.cap;
+    double kept_sq = 0.0;
+    for (int i = 0; i < kept; ++i) kept_sq += a.sigma[i] * a.sigma[i];
+    double w = 1.0 - kept_sq / total;
+    w = w < 0.0 ? 0.0 : (w > 1.0 ? 1.0 : w);
+    *a.discarded = w;
+    *a.kept = kept;
+    if (a.lambda) {
+        const double scale = a.renormalize ? 1.0 / sqrt(kept_sq) : 1.0;
+        for (int i = 0; i < kept; ++i) a.lambda[i] = a.renormalize ? a.sigma[i] * scale : a.sigma[i];
+    }
+}
+
+// ============================================================================ Gamma reshape
+constexpr double kPinvFloor = 1e-14;  // tebd.cpp:19
+
+__global__ void gamma_left_kernel(const GammaArgs a) {
+    const int kept = *a.kept;
+    const long long total = (long long)a.m * kept;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+         e += (long long)gridDim.x * blockDim.x) {
+        const int row = (int)(e / kept), g = (int)(e % kept);
+        double inv = 1.0;
+        if (a.ll) {
+            const double lv = a.ll[row / a.d1];
+            inv = lv < kPinvFloor ? 0.0 : 1.0 / lv;
+        }
+        a.gamma_l[e] = cscale(a.U[(long long)row * a.ldu + g], inv);
+    }
+}
+
+// gamma_r (kept x n) = conj(V (n x ldv))^T column-scaled: 32x32 tiles through shared memory.
+__global__ void gamma_right_kernel(const GammaArgs a) {
+    __shared__ cplx tile[32][33];
+    const int kept = *a.kept;
+    const int g0 = blockIdx.y * 32, c0 = blockIdx.x * 32;
+    if (g0 >= kept) return;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+    for (int yy = ty; yy < 32; yy += 8) {
+        const int c = c0 + yy, g = g0 + tx;
+        tile[yy][tx] = (c < a.n && g < kept) ? a.V[(long long)c * a.ldv + g] : mk(0.0, 0.0);
+    }
+    __syncthreads();
+    for (int yy = ty; yy < 32; yy += 8) {
+        const int g = g0 + yy, c = c0 + tx;
+        if (g < kept && c < a.n) {
+            double inv = 1.0;
+            if (a.lr) {
+                const double lv = a.lr[c % a.cr];
+                inv = lv < kPinvFloor ? 0.0 : 1.0 / lv;
+            }
+            a.gamma_r[(long long)g * a.n + c] = cscale(cconj(tile[tx][yy]), inv);
+        }
+    }
+}
+
+__global__ void pinv_flag_kernel(const double* ll, int cl, const double* lr, int cr, int* flag) {
+    int f = 0;
+    for (int i = threadIdx.x; i < cl; i += blockDim.x) f |= ll && ll[i] < kPinvFloor;
+    for (int i = threadIdx.x; i < cr; i += blockDim.x) f |= lr && lr[i] < kPinvFloor;
+    f = __syncthreads_or(f);
+    if (threadIdx.x == 0) *flag = f;
+}
+
+__global__ void fill_int_kernel(int* p, int v) { *p = v; }
+
+__global__ void conj_transpose_kernel(const cplx* __restrict__ A, int rows, int cols, cplx* __restrict__ out) {
+    __shared__ cplx tile[32][33];
+    const int r0 = blockIdx.y * 32, c0 = blockIdx.x * 32;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    for (int yy = ty; yy < 32; yy += 8) {
+        const int r = r0 + yy, cc = c0 + tx;
+        tile[yy][tx] = (r < rows && cc < cols) ? A[(long long)r * cols + cc] : mk(0.0, 0.0);
+    }
+    __syncthreads();
+    for (int yy = ty; yy < 32; yy += 8) {
+        const int cc = c0 + yy, r = r0 + tx;
+        if (cc < cols && r < rows) out[(long long)cc * rows + r] = cconj(tile[tx][yy]);
+    }
+}
+
+__global__ void weight_kernel(const double* sigma, int k, const double* total_sq, double* w) {
+    if (threadIdx.x != 0) return;
+    const double total = *total_sq;
+    if (total <= 0.0) { *w = 0.0; return; }
+    double kept = 0.0;
+    for (int i = 0; i < k; ++i) kept += sigma[i] * sigma[i];
+    double v = 1.0 - kept / total;
+    *w = v < 0.0 ? 0.0 : (v > 1.0 ? 1.0 : v);
+}
+
+// ============================================================================ peak probes
+constexpr int PROBE_ITERS = 4096;
+
+__global__ void __launch_bounds__(256) probe_dmma_kernel(double* sink, double seed) {
+    double acc[8][2];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc[i][0] = acc[i][1] = 0.0;
+    double a = seed + threadIdx.x * 1e-9, b = seed * 0.5;
+    for (int it = 0; it < PROBE_ITERS; ++it) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) dmma884(acc[i][0], acc[i][1], a, b);
+    }
+    double s = 0.0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s += acc[i][0] + acc[i][1];
+    if (s == 12345.678) sink[threadIdx.x] = s;
+}
+
+__global__ void __launch_bounds__(256) probe_dfma_kernel(double* sink, double seed) {
+    double acc[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc[i] = seed * i;
+    const double a = 1.0000001, b = 1e-12;
+    for (int it = 0; it < PROBE_ITERS; ++it) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc[i] = fma(acc[i], a, b);
+    }
+    double s = 0.0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s += acc[i];
+    if (s == 12345.678) sink[threadIdx.x] = s;
+}
+
+}  // namespace
+
+cudaError_t omega_reference(uint64_t seed, long long n_entries, unsigned long long* draws, cplx* out,
+                            cudaStream_t s) {
+    const long long rounds = (2 * n_entries + MT_N - 1) / MT_N;
+    mt_draws_kernel<<<1, 320, 0, s>>>(seed, rounds, draws);
+    box_muller_kernel<<<4 * kNumSMs, 256, 0, s>>>(draws, n_entries, out);
+    return cudaGetLastError();
+}
+
+cudaError_t omega_philox(uint64_t seed, long long n_entries, cplx* out, cudaStream_t s) {
+    philox_kernel<<<4 * kNumSMs, 256, 0, s>>>(seed, n_entries, out);
+    return cudaGetLastError();
+}
+
+cudaError_t gate_small(const cplx* G, int dd, int cl, int cr, const cplx* Min, cplx* Mout, cudaStream_t s) {
+    const long long cols = (long long)cl * cr;
+    const int grid = (int)std::min<long long>((cols + 255) / 256, 8 * kNumSMs);
+    if (dd <= 4) gate_small_kernel<4><<<grid, 256, 0, s>>>(G, dd, cl, cr, Min, Mout);
+    else if (dd <= 16) gate_small_kernel<16><<<grid, 256, 0, s>>>(G, dd, cl, cr, Min, Mout);
+    else return cudaErrorInvalidValue;
+    return cudaGetLastError();
+}
+
+cudaError_t theta_to_unfolded(const cplx* theta, int d1, int d2, int cl, int cr, cplx* M, cudaStream_t s) {
+    const long long rows = (long long)d1 * d2 * cl;
+    theta_unfold_kernel<<<(int)std::min<long long>(rows, 16 * kNumSMs), 128, 0, s>>>(theta, d1, d2, cl, cr, M, 1);
+    return cudaGetLastError();
+}
+cudaError_t unfolded_to_theta(const cplx* M, int d1, int d2, int cl, int cr, cplx* theta, cudaStream_t s) {
+    const long long rows = (long long)d1 * d2 * cl;
+    theta_unfold_kernel<<<(int)std::min<long long>(rows, 16 * kNumSMs), 128, 0, s>>>(M, d1, d2, cl, cr, theta, 0);
+    return cudaGetLastError();
+}
+
+cudaError_t truncate(const TruncArgs& a, cudaStream_t s) {
+    truncate_kernel<<<1, 32, 0, s>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t gamma_reshape(const GammaArgs& a, int max_kept, cudaStream_t s) {
+    gamma_left_kernel<<<4 * kNumSMs, 256, 0, s>>>(a);
+    dim3 grid((a.n + 31) / 32, (max_kept + 31) / 32);
+    gamma_right_kernel<<<grid, 256, 0, s>>>(a);
+    pinv_flag_kernel<<<1, 256, 0, s>>>(a.ll, a.ll ? a.m / a.d1 : 0, a.lr, a.lr ? a.cr : 0, a.pinv);
+    return cudaGetLastError();
+}
+
+cudaError_t fill_int(int* p, int v, cudaStream_t s) {
+    fill_int_kernel<<<1, 1, 0, s>>>(p, v);
+    return cudaGetLastError();
+}
+
+cudaError_t conj_transpose(const cplx* A, int rows, int cols, cplx* out, cudaStream_t s) {
+    dim3 grid((cols + 31) / 32, (rows + 31) / 32);
+    conj_transpose_kernel<<<grid, 256, 0, s>>>(A, rows, cols, out);
+    return cudaGetLastError();
+}
+
+cudaError_t discarded_weight(const double* sigma, int k, const double* total_sq, double* w,
+                             cudaStream_t s) {
+    weight_kernel<<<1, 32, 0, s>>>(sigma, k, total_sq, w);
+    return cudaGetLastError();
+}
+
+cudaError_t probe_peak(int what, double* tflops, cudaStream_t s) {
+    double* sink = nullptr;
+    cudaError_t e = cudaMallocAsync(&sink, 256 * sizeof(double), s);
+    if (e != cudaSuccess) return e;
+    cudaEvent_t t0, t1;
+    cudaEventCreate(&t0);
+    cudaEventCreate(&t1);
+    const int grid = 8 * kNumSMs;
+    for (int rep = 0; rep < 2; ++rep) {  // first launch warms clocks
+        cudaEventRecord(t0, s);
+        if (what == 0) probe_dmma_kernel<<<grid, 256, 0, s>>>(sink, 1.0);
+        else probe_dfma_kernel<<<grid, 256, 0, s>>>(sink, 1.0);
+        cudaEventRecord(t1, s);
+    }
+    e = cudaEventSynchronize(t1);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, t0, t1);
+    const double warps = grid * 8.0;
+    const double flops = (what == 0) ? warps * PROBE_ITERS * 8.0 * 512.0
+                                     : warps * 32.0 * PROBE_ITERS * 8.0 * 2.0;
+    *tflops = flops / (ms * 1e-3) / 1e12;
+    cudaEventDestroy(t0);
+    cudaEventDestroy(t1);
+    cudaFreeAsync(sink, s);
+    return e == cudaSuccess ? cudaGetLastError() : e;
+}
+
+}  // namespace rb

@@ -1,0 +1,74 @@
+// tebd_kernels.cuh — sketch generation and the bandwidth-bound decimation epilogue kernels.
+#pragma once
+#include "common.cuh"
+
+namespace rb {
+
+// ---- Gaussian sketch Omega (n x l, row-major) --------------------------------------------
+// Reference stream (randomized.cpp:17-45,79-86): std::mt19937_64(seed); entry e consumes draws
+// 2e (u1 = ((x>>11)+1)·2^-53) and 2e+1 (u2 = (x>>11)·2^-53); re = r cos(2πu2), im = r sin(2πu2),
+// r = sqrt(-2 ln u1).  The 64-bit Mersenne twister is sequential, so one CTA runs the twist
+// (312 words per round, two parallel phases) and writes raw draws; Box–Muller is a separate
+// fully parallel pass.  `draws` must hold 2*n*l uint64 rounded up to a multiple of 312.
+cudaError_t omega_reference(uint64_t seed, long long n_entries, unsigned long long* draws, cplx* out,
+                            cudaStream_t s);
+// Philox4x32-10 keyed by seed, counter = entry index: one 128-bit output -> (u1, u2).
+cudaError_t omega_philox(uint64_t seed, long long n_entries, cplx* out, cudaStream_t s);
+
+// ---- two-site gate for small d1*d2 (memory-bound form of tebd.cpp:126-139) ---------------
+// M_out[a][x][b] = sum_y G[x][y] M_in[a][y][b],  x, y < dd = d1*d2 <= 64.
+cudaError_t gate_small(const cplx* G, int dd, int cl, int cr, const cplx* Min, cplx* Mout,
+                       cudaStream_t s);
+
+// ---- layout conversion (i, j, a, b) <-> (a*d1+i, j*cr+b) ----------------------------------
+cudaError_t theta_to_unfolded(const cplx* theta, int d1, int d2, int cl, int cr, cplx* M, cudaStream_t s);
+cudaError_t unfolded_to_theta(const cplx* M, int d1, int d2, int cl, int cr, cplx* theta, cudaStream_t s);
+
+// ---- truncation (tebd.cpp:188-209) ---------------------------------------------------------
+// sigma: ns non-increasing values; total_sq: device scalar ||M||_F^2.  Writes *kept (int),
+// lambda[0..kept), *discarded.  cap = chi_max (0 = no cap).
+struct TruncArgs {
+    const double* sigma;
+    int ns;
+    const double* total_sq;
+    double trunc_tol;
+    long long cap;
+    int renormalize;
+    int* kept;
+    double* lambda;
+    double* discarded;
+};
+cudaError_t truncate(const TruncArgs& a, cudaStream_t s);
+
+// ---- Gamma reshape with outer-lambda pseudo-inverse (tebd.cpp:211-235) -----------------------
+// gamma_l[(a*d1+i)*kept + g] = U[(a*d1+i)*ldu + g] / ll[a]        (ll null -> 1)
+// gamma_r[g*n + c]          = conj(V[c*ldv + g]) / lr[c % cr]     (lr null -> 1), n = d2*cr
+// lambda < 1e-14 -> 0 and *pinv = 1.  kept is read from device memory.
+struct GammaArgs {
+    const cplx* U;
+    int ldu;
+    const cplx* V;
+    int ldv;
+    const double* ll;
+    const double* lr;
+    int m, n, d1, cr;
+    const int* kept;
+    cplx* gamma_l;
+    cplx* gamma_r;
+    int* pinv;
+};
+cudaError_t gamma_reshape(const GammaArgs& a, int max_kept, cudaStream_t s);
+
+cudaError_t fill_int(int* p, int v, cudaStream_t s);
+
+// out (cols x rows) = A^H for A (rows x cols), both row-major.
+cudaError_t conj_transpose(const cplx* A, int rows, int cols, cplx* out, cudaStream_t s);
+
+// *w = clamp(1 - sum_{i<k} sigma_i^2 / total_sq, 0, 1)   (randomized.cpp:68-75)
+cudaError_t discarded_weight(const double* sigma, int k, const double* total_sq, double* w,
+                             cudaStream_t s);
+
+// Peak probes (diagnostics): TFLOP/s of DMMA f64 and of DFMA.
+cudaError_t probe_peak(int what, double* tflops, cudaStream_t s);
+
+}  // namespace rb

@@ -1,0 +1,250 @@
+// zgemm.cu — see zgemm.cuh for the contract.
+#include "zgemm.cuh"
+
+namespace rb {
+
+namespace {
+
+constexpr int BM = 64, BN = 64, BK = 16, STAGES = 3;
+constexpr int WM = 32, WN = 32;
+constexpr int WARPS_M = BM / WM, WARPS_N = BN / WN;
+constexpr int NTHREADS = 32 * WARPS_M * WARPS_N;
+constexpr int MI = WM / 8, NI = WN / 8;
+// Padded strides (in complex elements) chosen so each quarter-warp's LDS.128 fragment load
+// touches 8 distinct 16-byte bank groups.
+constexpr int LDA_N = BK + 4;  // A tile stored [m][k]   (op N)
+constexpr int LDA_C = BM + 2;  // A tile stored [k][m]   (op C)
+constexpr int LDB = BN + 2;    // B tile stored [k][n]
+constexpr int A_STAGE = (BM * LDA_N > BK * LDA_C) ? BM * LDA_N : BK * LDA_C;
+constexpr int B_STAGE = BK * LDB;
+constexpr int SMEM_BYTES = STAGES * (A_STAGE + B_STAGE) * (int)sizeof(cplx);
+
+__device__ __forceinline__ int find_problem(const GemmGroup& g, int tile) {
+    int lo = 0, hi = g.count - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (g.p[mid].tile_begin <= tile) lo = mid; else hi = mid - 1;
+    }
+    return lo;
+}
+
+template <int OPA>
+__global__ void __launch_bounds__(NTHREADS, 2)
+zgemm_dmma_kernel(const __grid_constant__ GemmGroup g) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    cplx* smA = reinterpret_cast<cplx*>(smem_raw);
+    cplx* smB = smA + STAGES * A_STAGE;
+
+    const int pid = find_problem(g, blockIdx.x);
+    const GemmProblem& P = g.p[pid];
+    int t = blockIdx.x - P.tile_begin;
+    const int tn = t % P.tiles_n; t /= P.tiles_n;
+    const int tm = t % P.tiles_m; t /= P.tiles_m;
+    const int bz = t % P.batch;   t /= P.batch;
+    const int sk = t;  // split index
+
+    const int M = P.m, N = P.n, K = P.k;
+    const int kchunk = (((K + P.split - 1) / P.split) + BK - 1) / BK * BK;
+    const int kbeg = sk * kchunk;
+    const int kend = min(K, kbeg + kchunk);
+    const int m0 = tm * BM, n0 = tn * BN;
+
+    const cplx* __restrict__ A = P.A + (long long)bz * P.strideA;
+    const cplx* __restrict__ B = P.B + (long long)bz * P.strideB;
+    const long long lda = P.lda, ldb = P.ldb;
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int wm = (warp / WARPS_N) * WM, wn = (warp % WARPS_N) * WN;
+
+    const int ktiles = kend > kbeg ? (kend - kbeg + BK - 1) / BK : 0;
+
+    auto load_stage = [&](int stage, int kt) {
+        const int k0 = kbeg + kt * BK;
+        cplx* sA = smA + stage * A_STAGE;
+        cplx* sB = smB + stage * B_STAGE;
+        if (OPA == kOpN) {
+#pragma unroll
+            for (int i = 0; i < (BM * BK) / NTHREADS; ++i) {
+                const int idx = i * NTHREADS + tid;
+                const int r = idx / BK, c = idx % BK;
+                const int gr = m0 + r, gc = k0 + c;
+                const bool ok = gr < M && gc < kend;
+                cp_async16(sA + r * LDA_N + c, ok ? A + (long long)gr * lda + gc : A, ok);
+            }
+        } else {
+#pragma unroll
+            for (int i = 0; i < (BM * BK) / NTHREADS; ++i) {
+                const int idx = i * NTHREADS + tid;
+                const int r = idx / BM, c = idx % BM;  // r: k, c: m
+                const int gk = k0 + r, gm = m0 + c;
+                const bool ok = gk < kend && gm < M;
+                cp_async16(sA + r * LDA_C + c, ok ? A + (long long)gk * lda + gm : A, ok);
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < (BK * BN) / NTHREADS; ++i) {
+            const int idx = i * NTHREADS + tid;
+            const int r = idx / BN, c = idx % BN;
+            const int gk = k0 + r, gn = n0 + c;
+            const bool ok = gk < kend && gn < N;
+            cp_async16(sB + r * LDB + c, ok ? B + (long long)gk * ldb + gn : B, ok);
+        }
+    };
+
+    double acc[MI][NI][2][2];  // [mi][ni][re/im][c0/c1]
+#pragma unroll
+    for (int i = 0; i < MI; ++i)
+#pragma unroll
+        for (int j = 0; j < NI; ++j)
+#pragma unroll
+            for (int r = 0; r < 2; ++r) acc[i][j][r][0] = acc[i][j][r][1] = 0.0;
+
+#pragma unroll
+    for (int s = 0; s < STAGES - 1; ++s) {
+        if (s < ktiles) load_stage(s, s);
+        cp_async_commit();
+    }
+
+    const int fr = lane >> 2, fc = lane & 3;
+    const double* ks = P.ks;
+
+    for (int kt = 0; kt < ktiles; ++kt) {
+        cp_async_wait<STAGES - 2>();
+        __syncthreads();
+        {
+            const int nk = kt + STAGES - 1;
+            if (nk < ktiles) load_stage(nk % STAGES, nk);
+            cp_async_commit();
+        }
+        const int stage = kt % STAGES;
+        const cplx* sA = smA + stage * A_STAGE;
+        const cplx* sB = smB + stage * B_STAGE;
+        const int kbase = kbeg + kt * BK;
+#pragma unroll
+        for (int kk = 0; kk < BK; kk += 4) {
+            double ar[MI], ai[MI], ain[MI], br[NI], bi[NI];
+            double kscale = 1.0;
+            if (ks != nullptr) {
+                const int gk = kbase + kk + fc;
+                kscale = gk < kend ? __ldg(ks + gk) : 0.0;
+            }
+#pragma unroll
+            for (int i = 0; i < MI; ++i) {
+                cplx a;
+                if (OPA == kOpN) a = sA[(wm + i * 8 + fr) * LDA_N + kk + fc];
+                else a = sA[(kk + fc) * LDA_C + wm + i * 8 + fr];
+                if (OPA == kOpC) a.y = -a.y;
+                if (ks != nullptr) { a.x *= kscale; a.y *= kscale; }
+                ar[i] = a.x; ai[i] = a.y; ain[i] = -a.y;
+            }
+#pragma unroll
+            for (int j = 0; j < NI; ++j) {
+                const cplx b = sB[(kk + fc) * LDB + wn + j * 8 + fr];
+                br[j] = b.x; bi[j] = b.y;
+            }
+#pragma unroll
+            for (int i = 0; i < MI; ++i)
+#pragma unroll
+                for (int j = 0; j < NI; ++j) {
+                    dmma884(acc[i][j][0][0], acc[i][j][0][1], ar[i], br[j]);
+                    dmma884(acc[i][j][1][0], acc[i][j][1][1], ar[i], bi[j]);
+                }
+#pragma unroll
+            for (int i = 0; i < MI; ++i)
+#pragma unroll
+                for (int j = 0; j < NI; ++j) {
+                    dmma884(acc[i][j][0][0], acc[i][j][0][1], ain[i], bi[j]);
+                    dmma884(acc[i][j][1][0], acc[i][j][1][1], ai[i], br[j]);
+                }
+        }
+    }
+    cp_async_wait<0>();
+
+    // ---- epilogue
+    if (P.split > 1) {
+        cplx* W = P.partial + ((long long)sk * P.batch + bz) * (long long)M * N;
+#pragma unroll
+        for (int i = 0; i < MI; ++i) {
+            const int row = m0 + wm + i * 8 + fr;
+            if (row >= M) continue;
+#pragma unroll
+            for (int j = 0; j < NI; ++j) {
+                const int col = n0 + wn + j * 8 + fc * 2;
+#pragma unroll
+                for (int c = 0; c < 2; ++c)
+                    if (col + c < N) W[(long long)row * N + col + c] = mk(acc[i][j][0][c], acc[i][j][1][c]);
+            }
+        }
+        return;
+    }
+    cplx* C = P.C + (long long)bz * P.strideC;
+#pragma unroll
+    for (int i = 0; i < MI; ++i) {
+        const int row = m0 + wm + i * 8 + fr;
+        if (row >= M) continue;
+        const double rsc = P.rs ? __ldg(P.rs + row / P.rs_div) : 1.0;
+#pragma unroll
+        for (int j = 0; j < NI; ++j) {
+            const int col = n0 + wn + j * 8 + fc * 2;
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+                if (col + c >= N) continue;
+                const double sc = rsc * (P.cs ? __ldg(P.cs + (col + c) % P.cs_mod) : 1.0);
+                C[(long long)row * P.ldc + col + c] = mk(acc[i][j][0][c] * sc, acc[i][j][1][c] * sc);
+            }
+        }
+    }
+}
+
+// Fixed-order reduction of split-K partials + fused output scaling.
+__global__ void splitk_reduce_kernel(const __grid_constant__ GemmGroup g) {
+    const int pid = blockIdx.y;
+    const GemmProblem& P = g.p[pid];
+    if (P.split <= 1) return;
+    const long long per = (long long)P.m * P.n;
+    const long long total = per * P.batch;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+         e += (long long)gridDim.x * blockDim.x) {
+        const long long bz = e / per, rem = e % per;
+        const int row = (int)(rem / P.n), col = (int)(rem % P.n);
+        cplx s = mk(0.0, 0.0);
+        for (int k = 0; k < P.split; ++k) s = cadd(s, P.partial[(long long)k * total + e]);
+        double sc = 1.0;
+        if (P.rs) sc *= P.rs[row / P.rs_div];
+        if (P.cs) sc *= P.cs[col % P.cs_mod];
+        P.C[bz * P.strideC + (long long)row * P.ldc + col] = cscale(s, sc);
+    }
+}
+
+}  // namespace
+
+cudaError_t zgemm_grouped(GemmGroup& g, GemmOp opA, cudaStream_t s) {
+    int total = 0;
+    bool any_split = false;
+    for (int i = 0; i < g.count; ++i) {
+        GemmProblem& P = g.p[i];
+        if (P.batch < 1) P.batch = 1;
+        if (P.split < 1) P.split = 1;
+        if (P.rs_div < 1) P.rs_div = 1;
+        if (P.cs_mod < 1) P.cs_mod = 1;
+        P.tiles_m = (P.m + BM - 1) / BM;
+        P.tiles_n = (P.n + BN - 1) / BN;
+        P.tile_begin = total;
+        if (P.m > 0 && P.n > 0) total += P.tiles_m * P.tiles_n * P.batch * P.split;
+        any_split |= P.split > 1;
+    }
+    g.total_tiles = total;
+    if (total == 0) return cudaSuccess;
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(zgemm_dmma_kernel<kOpN>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+        cudaFuncSetAttribute(zgemm_dmma_kernel<kOpC>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+        configured = true;
+    }
+    if (opA == kOpN) zgemm_dmma_kernel<kOpN><<<total, NTHREADS, SMEM_BYTES, s>>>(g);
+    else zgemm_dmma_kernel<kOpC><<<total, NTHREADS, SMEM_BYTES, s>>>(g);
+    if (any_split) splitk_reduce_kernel<<<dim3(2 * kNumSMs, g.count), 256, 0, s>>>(g);
+    return cudaGetLastError();
+}
+
+}  // namespace rb

@@ -1,0 +1,54 @@
+// zgemm.cuh — grouped complex-FP64 GEMM on the FP64 tensor cores (DMMA) for sm_100a.
+//
+// Replaces every cblas_zgemm call on the TEBD decimation path (linalg.cpp:20-40,
+// tebd.cpp:134-137) and the scalar Θ contraction loop (tebd.cpp:105-114).
+//
+// Why DMMA and not tcgen05: sm_100a has no f64 kind for tcgen05.mma (ptxas rejects
+// `.kind::f64`), so FP64 tensor math is warp-level `mma.sync.m8n8k4.f64` → SASS DMMA.8x8x4.
+// Complex arithmetic is done as four real MMAs per k-step on split (re, im) fragments
+// (C_r += A_r B_r − A_i B_i, C_i += A_r B_i + A_i B_r) — the "4M" form, same rounding class as
+// zgemm (no 3M/Gauss trick).  Operands are staged global→shared with a multi-stage cp.async
+// (LDGSTS) ring; each thread loads one 16-byte complex per fragment element (LDS.128), so a
+// single shared-memory read yields both the real and imaginary fragment.
+#pragma once
+#include "common.cuh"
+
+namespace rb {
+
+enum GemmOp : int { kOpN = 0, kOpC = 1 };
+
+// One (possibly strided-batched) product  C[b] = diag(rs) · op(A[b]) · diag(ks) · B[b] · diag(cs)
+// with all three scalings optional; row scale index = row / rs_div, column scale index
+// = col % cs_mod (so λ_l over unfolded rows (α·d1+i) and λ_r over columns (j·χr+β) fuse).
+struct GemmProblem {
+    int m, n, k;
+    int batch;
+    const cplx* A;
+    long long lda, strideA;  // op N: A is m x k row-major; op C: A is k x m row-major (use A^H)
+    const cplx* B;
+    long long ldb, strideB;  // B is k x n row-major
+    cplx* C;
+    long long ldc, strideC;
+    const double* rs;  // nullable
+    const double* ks;  // nullable
+    const double* cs;  // nullable
+    int rs_div, cs_mod;
+    int split;         // split-K factor (1 = none)
+    cplx* partial;     // split-K workspace: split * batch * m * n (only if split > 1)
+    // filled by the launcher
+    int tiles_m, tiles_n, tile_begin;
+};
+
+constexpr int kMaxGroup = 48;
+
+struct GemmGroup {
+    int count;
+    int total_tiles;
+    GemmProblem p[kMaxGroup];
+};
+
+// Launches one grouped GEMM.  All problems share the A operation.  Split-K partials are
+// reduced (deterministically, fixed order) by a second kernel.
+cudaError_t zgemm_grouped(GemmGroup& g, GemmOp opA, cudaStream_t s);
+
+}  // namespace rb
