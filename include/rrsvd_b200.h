@@ -148,7 +148,70 @@ int rrsvd_b200_theta_to_unfolded(rrsvd_b200_ctx* ctx, const double* theta, size_
 int rrsvd_b200_unfolded_to_theta(rrsvd_b200_ctx* ctx, const double* M, size_t d1, size_t d2,
                                  size_t cl, size_t cr, double* theta);
 
+/* ---- device-resident MPS and TEBD evolution (mps.hpp:31-41, tebd.hpp:52-144) ----------- */
+typedef struct rrsvd_b200_mps rrsvd_b200_mps;
+
+/* == rrsvd::tebd::TrotterPlan::Sweep (tebd.hpp:52-62). */
+typedef struct rrsvd_b200_sweep {
+    int bond_parity;
+    double coefficient;
+} rrsvd_b200_sweep;
+
+/* == rrsvd::tebd::EvolveOptions (tebd.hpp:126-130) + the sketch source. */
+typedef struct rrsvd_b200_evolve_options {
+    double abort_discarded_threshold; /* cumulative fraction; 1 never aborts */
+    int renormalize;
+    int omega_mode; /* RRSVD_B200_OMEGA_REFERENCE or _PHILOX */
+} rrsvd_b200_evolve_options;
+
+/* == rrsvd::tebd::EvolveDiagnostics scalars (tebd.hpp:132-138). */
+typedef struct rrsvd_b200_evolve_diag {
+    double kept_fraction;
+    uint64_t max_bond_dim;
+    int aborted;
+    uint64_t abort_step;
+    uint64_t n_updates;
+} rrsvd_b200_evolve_diag;
+
+/* == rrsvd::tebd::UpdateRecord (tebd.hpp:115-124); times are CUDA-event device times (us). */
+typedef struct rrsvd_b200_update_record {
+    uint64_t step, bond, chi;
+    double discarded_weight;
+    double t_theta_us, t_gate_us, t_svd_us;
+    int randomized_path;
+} rrsvd_b200_update_record;
+
+/* MpsState on the device (mps.hpp:31-41), initialised to the product state |0...0>
+ * (mps_product_state, mps.cpp:15-38, with every local state e_0).  chi_max 0 = unbounded. */
+int rrsvd_b200_mps_create(rrsvd_b200_ctx* ctx, size_t n_sites, const size_t* site_dims,
+                          size_t chi_max, double trunc_tolerance, rrsvd_b200_mps** out);
+void rrsvd_b200_mps_destroy(rrsvd_b200_mps* mps);
+/* Γ of `site` (dim_left x d x dim_right) and, unless `site` is the last one, the λ of bond
+ * `site` (dim_right values).  dim_left must equal the right dimension of site-1. */
+int rrsvd_b200_mps_set_site(rrsvd_b200_mps* mps, size_t site, size_t dim_left, size_t dim_right,
+                            const double* gamma, const double* lambda_right);
+/* dims3 <- (left, phys, right); gamma / lambda_right copied out when non-NULL. */
+int rrsvd_b200_mps_get_site(rrsvd_b200_mps* mps, size_t site, size_t* dims3, double* gamma,
+                            double* lambda_right);
+/* evolve (tebd.cpp:260-326): n_steps x sweeps x (bonds of the sweep's parity, ascending):
+ * build_theta -> gate -> decimate on the device, state resident in HBM.  gates[s*(n_sites-1)+b]
+ * is the (d_b d_{b+1})^2 gate exp(-i c_s dt h_b) for sweep s (NULL = no term on that bond); the
+ * caller builds it (bond_gate, tebd.cpp:239-258).  backend->seed advances once per update, like
+ * the reference (tebd.cpp:162).  records (may be NULL) receives up to max_records updates. */
+int rrsvd_b200_evolve(rrsvd_b200_mps* mps, size_t n_sweeps, const rrsvd_b200_sweep* sweeps,
+                      const double* const* gates, size_t n_steps, rrsvd_b200_backend* backend,
+                      const rrsvd_b200_evolve_options* options, rrsvd_b200_evolve_diag* diag,
+                      rrsvd_b200_update_record* records, size_t max_records);
+/* <psi| O_site |psi> (mps.cpp:50-70) -> out2 = (re, im); S = -sum λ² ln λ² (mps.cpp:40-48). */
+int rrsvd_b200_expectation_local(rrsvd_b200_mps* mps, size_t site, const double* op, double* out2);
+int rrsvd_b200_schmidt_entropy(rrsvd_b200_mps* mps, size_t bond, double* out);
+
 /* ---- diagnostics ------------------------------------------------------------------------ */
+/* Event-time every zgemm launch (with its split-K reduction) on this context; on = 1 also
+ * resets the counters.  Stats are cumulative algorithmic flops (8 m n k per complex GEMM),
+ * device milliseconds and launch count. */
+int rrsvd_b200_set_gemm_timing(rrsvd_b200_ctx* ctx, int on);
+int rrsvd_b200_gemm_stats(rrsvd_b200_ctx* ctx, double* flops, double* ms, uint64_t* calls);
 /* Measured device peak: what = 0 FP64 DMMA (mma.sync f64), 1 FP64 DFMA; TFLOP/s. */
 int rrsvd_b200_probe_peak(rrsvd_b200_ctx* ctx, int what, double* tflops);
 

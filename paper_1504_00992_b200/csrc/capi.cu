@@ -275,10 +275,8 @@ int rrsvd_b200_build_theta_unfolded(rrsvd_b200_ctx* c, const double* G1, const d
         const auto* dlm = static_cast<const double*>(stage_in(c, lm, cm * sizeof(double)));
         const auto* dlr = static_cast<const double*>(stage_in(c, lr, cr * sizeof(double)));
         auto* dM = static_cast<cplx*>(stage_out(c, M, m * n * sizeof(cplx), outs));
-        Scale sc;
-        sc.rs = dll; sc.rs_div = (int)d1; sc.ks = dlm; sc.cs = dlr; sc.cs_mod = (int)cr;
         if (cm == 0) check_cuda(c, cudaMemsetAsync(dM, 0, m * n * sizeof(cplx), c->stream), "memset");
-        else gemm(c, kOpN, (int)m, (int)n, (int)cm, dG1, (long long)cm, dG2, (long long)n, dM, (long long)n, sc);
+        else build_theta_device(c, dG1, dG2, dll, dlm, dlr, (int)cl, (int)d1, (int)cm, (int)d2, (int)cr, dM);
         finish_out(c, outs);
     });
 }
@@ -293,13 +291,7 @@ int rrsvd_b200_apply_gate_unfolded(rrsvd_b200_ctx* c, const double* G, size_t d1
         const auto* dG = static_cast<const cplx*>(stage_in(c, G, dd * dd * sizeof(cplx)));
         const auto* dI = static_cast<const cplx*>(stage_in(c, M_in, tot * sizeof(cplx)));
         auto* dO = static_cast<cplx*>(stage_out(c, M_out, tot * sizeof(cplx), outs));
-        if (dd <= 16) {
-            check_cuda(c, gate_small(dG, (int)dd, (int)cl, (int)cr, dI, dO, c->stream), "gate_small");
-            c->launches++;
-        } else {
-            gemm(c, kOpN, (int)dd, (int)cr, (int)dd, dG, (long long)dd, dI, (long long)cr, dO, (long long)cr, {},
-                 (int)cl, 0, (long long)(dd * cr), (long long)(dd * cr));
-        }
+        apply_gate_device(c, dG, (int)d1, (int)d2, (int)cl, (int)cr, dI, dO);
         finish_out(c, outs);
     });
 }
@@ -339,60 +331,28 @@ int rrsvd_b200_decimate_unfolded(rrsvd_b200_ctx* c, const double* M, size_t d1, 
                                  double* lambda, double* gamma_r, rrsvd_b200_decim_info* info) {
     return api(c, [&] {
         if (be == nullptr || info == nullptr) throw_contract(c, "decimate: null backend/info");
-        const size_t m = d1 * cl, n = d2 * cr, minor = std::min(m, n);
+        const size_t m = d1 * cl, n = d2 * cr;
         if (m == 0 || n == 0) throw_contract(c, "decimate: theta is identically zero");
-        const size_t k = be->target_rank != 0 ? be->target_rank : chi_max;
-        const bool randomized = be->kind == 1 && k != 0 && minor > be->det_crossover;
+        const DecimPlan pl = plan_decimation((int)d1, (int)d2, (int)cl, (int)cr, chi_max, be->kind,
+                                             be->target_rank, be->oversampling, be->det_crossover);
+        const bool randomized = pl.randomized;
         if (randomized && be->accuracy_check)
             throw_contract(c, "decimate: accuracy_check (fixed-precision RRSVD) is not implemented on the device yet");
-        size_t ns = minor, l = 0;
-        if (randomized) {
-            const size_t p = be->oversampling != 0 ? be->oversampling : k;
-            l = std::min(k + p, minor);
-            ns = l;
-        }
-        size_t kmax = ns;
-        if (chi_max != 0) kmax = std::min(kmax, chi_max);
-
+        const size_t kmax = (size_t)pl.kmax;
         const auto* dM = static_cast<const cplx*>(stage_in(c, M, m * n * sizeof(cplx)));
         const auto* dll = static_cast<const double*>(stage_in(c, ll, cl * sizeof(double)));
         const auto* dlr = static_cast<const double*>(stage_in(c, lr, cr * sizeof(double)));
+        const cplx* dO = randomized ? static_cast<const cplx*>(stage_in(c, omega, n * pl.l * sizeof(cplx)))
+                                    : nullptr;
         auto* sc = ws_get<Scalars>(c, 1);
-        double* part = ws_get<double>(c, 2 * kNumSMs);
-        int* bad = ws_get<int>(c, 2 * kNumSMs);
-        check_cuda(c, sumsq(dM, (long long)(m * n), part, bad, &sc->total_sq, &sc->nonfinite, c->stream), "sumsq");
-        c->launches += 2;
-
-        cplx* U = ws_get<cplx>(c, m * ns);
-        cplx* V = ws_get<cplx>(c, n * ns);
-        double* sig = ws_get<double>(c, ns);
-        if (randomized) {
-            const cplx* dO = static_cast<const cplx*>(stage_in(c, omega, n * l * sizeof(cplx)));
-            if (dO == nullptr) {
-                cplx* o = ws_get<cplx>(c, n * l);
-                make_omega(c, (int)n, (int)l, call_seed, omega_mode, o);
-                dO = o;
-            }
-            rrsvd_core(c, dM, (int)m, (int)n, (int)l, (int)be->power_iterations, dO, U, sig, V);
-        } else {
-            svd_jacobi(c, dM, (int)m, (int)n, U, sig, V);
-        }
         // outputs: write straight into device buffers, else into workspace + exact D2H
         const bool dev_gl = is_device_ptr(gamma_l), dev_lam = is_device_ptr(lambda), dev_gr = is_device_ptr(gamma_r);
         cplx* gl = dev_gl ? reinterpret_cast<cplx*>(gamma_l) : ws_get<cplx>(c, m * kmax);
         double* lam = dev_lam ? lambda : ws_get<double>(c, kmax);
         cplx* gr = dev_gr ? reinterpret_cast<cplx*>(gamma_r) : ws_get<cplx>(c, kmax * n);
-        TruncArgs ta{};
-        ta.sigma = sig; ta.ns = (int)ns; ta.total_sq = &sc->total_sq; ta.trunc_tol = trunc_tol;
-        ta.cap = (long long)chi_max; ta.renormalize = renormalize; ta.kept = &sc->kept;
-        ta.lambda = lam; ta.discarded = &sc->discarded;
-        check_cuda(c, truncate(ta, c->stream), "truncate");
-        GammaArgs ga{};
-        ga.U = U; ga.ldu = (int)ns; ga.V = V; ga.ldv = (int)ns; ga.ll = dll; ga.lr = dlr;
-        ga.m = (int)m; ga.n = (int)n; ga.d1 = (int)d1; ga.cr = (int)cr; ga.kept = &sc->kept;
-        ga.gamma_l = gl; ga.gamma_r = gr; ga.pinv = &sc->pinv;
-        check_cuda(c, gamma_reshape(ga, (int)kmax, c->stream), "gamma_reshape");
-        c->launches += 4;
+        decimate_device(c, pl, dM, (int)d1, (int)cr, dll, dlr, chi_max, trunc_tol, (int)be->power_iterations,
+                        call_seed, omega_mode, dO, renormalize, gl, lam, gr,
+                        reinterpret_cast<DecimScalars*>(sc));
         Scalars h;
         read_scalars(c, sc, &h);
         if (h.nonfinite) throw_contract(c, "decimate: theta has non-finite entries");
@@ -411,6 +371,27 @@ int rrsvd_b200_decimate_unfolded(rrsvd_b200_ctx* c, const double* M, size_t d1, 
 }
 
 // ------------------------------------------------------------------------------------------ misc
+
+int rrsvd_b200_set_gemm_timing(rrsvd_b200_ctx* c, int on) {
+    return api(c, [&] {
+        flush_gemm_timing(c);
+        c->gemm_timing = on != 0;
+        if (on) {
+            c->gemm_ms = 0.0;
+            c->gemm_flops = 0.0;
+            c->gemm_calls = 0;
+        }
+    });
+}
+
+int rrsvd_b200_gemm_stats(rrsvd_b200_ctx* c, double* flops, double* ms, uint64_t* calls) {
+    return api(c, [&] {
+        flush_gemm_timing(c);
+        if (flops) *flops = c->gemm_flops;
+        if (ms) *ms = c->gemm_ms;
+        if (calls) *calls = c->gemm_calls;
+    });
+}
 
 int rrsvd_b200_probe_peak(rrsvd_b200_ctx* c, int what, double* tflops) {
     return api(c, [&] {

@@ -83,6 +83,31 @@ void release_staged(rrsvd_b200_ctx* c) {
     c->staged.clear();
 }
 
+cudaEvent_t pooled_event(rrsvd_b200_ctx* c) {
+    if (!c->event_pool.empty()) {
+        cudaEvent_t e = c->event_pool.back();
+        c->event_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e;
+    check_cuda(c, cudaEventCreate(&e), "cudaEventCreate");
+    return e;
+}
+
+void flush_gemm_timing(rrsvd_b200_ctx* c) {
+    for (auto& p : c->pending) {
+        check_cuda(c, cudaEventSynchronize(p.b), "event sync");
+        float ms = 0.f;
+        check_cuda(c, cudaEventElapsedTime(&ms, p.a, p.b), "event elapsed");
+        c->gemm_ms += ms;
+        c->gemm_flops += p.flops;
+        c->gemm_calls++;
+        c->event_pool.push_back(p.a);
+        c->event_pool.push_back(p.b);
+    }
+    c->pending.clear();
+}
+
 void* pinned_scratch(rrsvd_b200_ctx* c, size_t bytes) {
     if (bytes > c->pinned_cap) {
         if (c->pinned) cudaFreeHost(c->pinned);

@@ -20,6 +20,17 @@ struct rrsvd_b200_ctx {
     size_t pinned_cap = 0;
     // Buffers allocated for host-pointer staging during one call, freed at call end.
     std::vector<void*> staged;
+
+    // Optional per-launch timing of the zgemm stage (CUDA events on the context stream).
+    struct PendingGemm {
+        cudaEvent_t a, b;
+        double flops;
+    };
+    bool gemm_timing = false;
+    std::vector<PendingGemm> pending;
+    std::vector<cudaEvent_t> event_pool;
+    double gemm_ms = 0.0, gemm_flops = 0.0;
+    uint64_t gemm_calls = 0;
 };
 
 namespace rb {
@@ -63,6 +74,10 @@ struct OutBuf {
 void* stage_out(rrsvd_b200_ctx* c, void* p, size_t bytes, std::vector<OutBuf>& outs);
 void finish_out(rrsvd_b200_ctx* c, std::vector<OutBuf>& outs);  // D2H copies + sync
 void release_staged(rrsvd_b200_ctx* c);
+
+// zgemm timing: events around each GEMM launch (incl. its split-K reduction) while enabled.
+cudaEvent_t pooled_event(rrsvd_b200_ctx* c);
+void flush_gemm_timing(rrsvd_b200_ctx* c);  // waits for pending events, accumulates
 void* pinned_scratch(rrsvd_b200_ctx* c, size_t bytes);
 
 }  // namespace rb

@@ -1,0 +1,315 @@
+// evolve.cu — device-resident MpsState and the TEBD sweep driver (tebd.cpp:260-326).
+#include <algorithm>
+#include <cmath>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "../../include/rrsvd_b200.h"
+#include "pipeline.cuh"
+
+using namespace rb;
+
+struct rrsvd_b200_mps {
+    rrsvd_b200_ctx* c = nullptr;
+    int n = 0;
+    std::vector<int> d, dl, dr;
+    size_t chi_max = 0;
+    double tol = 0.0;
+    std::vector<cplx*> g;       // Γ per site (device), dl x d x dr
+    std::vector<size_t> gcap;   // capacity in elements
+    std::vector<double*> lam;   // λ per bond (device)
+    std::vector<size_t> lcap;
+};
+
+namespace {
+
+template <class F>
+int mps_api(rrsvd_b200_mps* s, F&& f) {
+    if (s == nullptr || s->c == nullptr) return kContract;
+    rrsvd_b200_ctx* c = s->c;
+    int code = kOk;
+    try {
+        cudaSetDevice(c->device);
+        f(c);
+    } catch (const Fail& e) {
+        code = e.code;
+    } catch (const std::exception& e) {
+        c->err = e.what();
+        code = kCuda;
+    }
+    ws_reset(c);
+    return code;
+}
+
+// Persistent (not per-call) device buffers, stream-ordered.
+void ensure_gamma(rrsvd_b200_mps* s, int site, size_t elems) {
+    if (s->gcap[site] >= elems) return;
+    rrsvd_b200_ctx* c = s->c;
+    if (s->g[site]) cudaFreeAsync(s->g[site], c->stream);
+    s->g[site] = nullptr;
+    check_cuda(c, cudaMallocAsync(reinterpret_cast<void**>(&s->g[site]), elems * sizeof(cplx), c->stream), "alloc gamma");
+    s->gcap[site] = elems;
+}
+void ensure_lambda(rrsvd_b200_mps* s, int bond, size_t elems) {
+    if (s->lcap[bond] >= elems) return;
+    rrsvd_b200_ctx* c = s->c;
+    if (s->lam[bond]) cudaFreeAsync(s->lam[bond], c->stream);
+    s->lam[bond] = nullptr;
+    check_cuda(c, cudaMallocAsync(reinterpret_cast<void**>(&s->lam[bond]), elems * sizeof(double), c->stream), "alloc lambda");
+    s->lcap[bond] = elems;
+}
+
+struct HostScalars {
+    DecimScalars s;
+};
+
+}  // namespace
+
+extern "C" {
+
+int rrsvd_b200_mps_create(rrsvd_b200_ctx* c, size_t n_sites, const size_t* site_dims, size_t chi_max,
+                          double trunc_tolerance, rrsvd_b200_mps** out) {
+    if (c == nullptr || out == nullptr) return kContract;
+    *out = nullptr;
+    auto* s = new rrsvd_b200_mps();
+    s->c = c;
+    const int rc = mps_api(s, [&](rrsvd_b200_ctx* cc) {
+        if (n_sites < 1 || site_dims == nullptr) throw_contract(cc, "mps_product_state: one local state per site required");
+        s->n = (int)n_sites;
+        s->chi_max = chi_max;
+        s->tol = trunc_tolerance;
+        s->d.assign(site_dims, site_dims + n_sites);
+        for (int x : s->d)
+            if (x < 1) throw_contract(cc, "mps_product_state: local state dimension mismatch");
+        s->dl.assign(n_sites, 1);
+        s->dr.assign(n_sites, 1);
+        s->g.assign(n_sites, nullptr);
+        s->gcap.assign(n_sites, 0);
+        s->lam.assign(n_sites > 1 ? n_sites - 1 : 0, nullptr);
+        s->lcap.assign(s->lam.size(), 0);
+        std::vector<cplx> e0;
+        for (int site = 0; site < s->n; ++site) {
+            ensure_gamma(s, site, (size_t)s->d[site]);
+            e0.assign(s->d[site], mk(0.0, 0.0));
+            e0[0] = mk(1.0, 0.0);
+            check_cuda(cc, cudaMemcpyAsync(s->g[site], e0.data(), e0.size() * sizeof(cplx), cudaMemcpyHostToDevice, cc->stream), "H2D");
+            check_cuda(cc, cudaStreamSynchronize(cc->stream), "sync");
+        }
+        const double one = 1.0;
+        for (size_t b = 0; b < s->lam.size(); ++b) {
+            ensure_lambda(s, (int)b, 1);
+            check_cuda(cc, cudaMemcpyAsync(s->lam[b], &one, sizeof(double), cudaMemcpyHostToDevice, cc->stream), "H2D");
+        }
+        check_cuda(cc, cudaStreamSynchronize(cc->stream), "sync");
+    });
+    if (rc != kOk) {
+        rrsvd_b200_mps_destroy(s);
+        return rc;
+    }
+    *out = s;
+    return kOk;
+}
+
+void rrsvd_b200_mps_destroy(rrsvd_b200_mps* s) {
+    if (s == nullptr) return;
+    if (s->c) {
+        cudaSetDevice(s->c->device);
+        for (cplx* p : s->g)
+            if (p) cudaFreeAsync(p, s->c->stream);
+        for (double* p : s->lam)
+            if (p) cudaFreeAsync(p, s->c->stream);
+        cudaStreamSynchronize(s->c->stream);
+    }
+    delete s;
+}
+
+int rrsvd_b200_mps_set_site(rrsvd_b200_mps* s, size_t site, size_t dim_left, size_t dim_right,
+                            const double* gamma, const double* lambda_right) {
+    return mps_api(s, [&](rrsvd_b200_ctx* c) {
+        if (site >= (size_t)s->n) throw_contract(c, "mps_set_site: bad site");
+        if (dim_left < 1 || dim_right < 1) throw_contract(c, "mps_set_site: bond dimensions must be >= 1");
+        if (site == 0 && dim_left != 1) throw_contract(c, "mps_set_site: open left end needs dim_left = 1");
+        if (site + 1 == (size_t)s->n && dim_right != 1) throw_contract(c, "mps_set_site: open right end needs dim_right = 1");
+        const size_t elems = dim_left * s->d[site] * dim_right;
+        ensure_gamma(s, (int)site, elems);
+        check_cuda(c, cudaMemcpyAsync(s->g[site], gamma, elems * sizeof(cplx), cudaMemcpyDefault, c->stream), "set gamma");
+        if (lambda_right != nullptr && site + 1 < (size_t)s->n) {
+            ensure_lambda(s, (int)site, dim_right);
+            check_cuda(c, cudaMemcpyAsync(s->lam[site], lambda_right, dim_right * sizeof(double), cudaMemcpyDefault, c->stream),
+                       "set lambda");
+        }
+        s->dl[site] = (int)dim_left;
+        s->dr[site] = (int)dim_right;
+        check_cuda(c, cudaStreamSynchronize(c->stream), "sync");
+    });
+}
+
+int rrsvd_b200_mps_get_site(rrsvd_b200_mps* s, size_t site, size_t* dims3, double* gamma, double* lambda_right) {
+    return mps_api(s, [&](rrsvd_b200_ctx* c) {
+        if (site >= (size_t)s->n) throw_contract(c, "mps_get_site: bad site");
+        if (dims3) {
+            dims3[0] = s->dl[site];
+            dims3[1] = s->d[site];
+            dims3[2] = s->dr[site];
+        }
+        const size_t elems = (size_t)s->dl[site] * s->d[site] * s->dr[site];
+        if (gamma) check_cuda(c, cudaMemcpyAsync(gamma, s->g[site], elems * sizeof(cplx), cudaMemcpyDefault, c->stream), "get gamma");
+        if (lambda_right && site + 1 < (size_t)s->n)
+            check_cuda(c, cudaMemcpyAsync(lambda_right, s->lam[site], s->dr[site] * sizeof(double), cudaMemcpyDefault, c->stream),
+                       "get lambda");
+        check_cuda(c, cudaStreamSynchronize(c->stream), "sync");
+    });
+}
+
+int rrsvd_b200_evolve(rrsvd_b200_mps* s, size_t n_sweeps, const rrsvd_b200_sweep* sweeps, const double* const* gates,
+                      size_t n_steps, rrsvd_b200_backend* be, const rrsvd_b200_evolve_options* opt,
+                      rrsvd_b200_evolve_diag* diag, rrsvd_b200_update_record* records, size_t max_records) {
+    return mps_api(s, [&](rrsvd_b200_ctx* c) {
+        if (be == nullptr || diag == nullptr || (n_sweeps && (sweeps == nullptr || gates == nullptr)))
+            throw_contract(c, "evolve: null argument");
+        const int n = s->n, nb = n - 1;
+        const double abort_thr = opt ? opt->abort_discarded_threshold : 1.0;
+        const int renorm = opt ? opt->renormalize : 1;
+        const int omode = opt ? opt->omega_mode : RRSVD_B200_OMEGA_REFERENCE;
+        // Stage each distinct gate once (the reference builds one per (bond, coefficient),
+        // tebd.cpp:276-285).
+        std::map<const double*, const cplx*> staged;
+        std::vector<void*> gate_bufs;
+        for (size_t sw = 0; sw < n_sweeps; ++sw)
+            for (int b = 0; b < nb; ++b) {
+                const double* gp = gates[sw * nb + b];
+                if (gp == nullptr || staged.count(gp)) continue;
+                const size_t dd = (size_t)s->d[b] * s->d[b + 1];
+                if (is_device_ptr(gp)) {
+                    staged[gp] = reinterpret_cast<const cplx*>(gp);
+                } else {
+                    void* buf = nullptr;
+                    check_cuda(c, cudaMallocAsync(&buf, dd * dd * sizeof(cplx), c->stream), "alloc gate");
+                    check_cuda(c, cudaMemcpyAsync(buf, gp, dd * dd * sizeof(cplx), cudaMemcpyHostToDevice, c->stream), "H2D gate");
+                    gate_bufs.push_back(buf);
+                    staged[gp] = static_cast<const cplx*>(buf);
+                }
+            }
+        struct GateGuard {
+            rrsvd_b200_ctx* c;
+            std::vector<void*>& v;
+            ~GateGuard() { for (void* p : v) cudaFreeAsync(p, c->stream); }
+        } guard{c, gate_bufs};
+
+        auto* sc_dev = static_cast<DecimScalars*>(nullptr);
+        check_cuda(c, cudaMallocAsync(reinterpret_cast<void**>(&sc_dev), sizeof(DecimScalars), c->stream), "alloc scalars");
+        struct ScGuard {
+            rrsvd_b200_ctx* c;
+            void* p;
+            ~ScGuard() { cudaFreeAsync(p, c->stream); }
+        } scg{c, sc_dev};
+        auto* sc_host = static_cast<DecimScalars*>(pinned_scratch(c, sizeof(DecimScalars)));
+        cudaEvent_t ev[4];
+        for (auto& e : ev) e = pooled_event(c);
+        struct EvGuard {
+            rrsvd_b200_ctx* c;
+            cudaEvent_t* e;
+            ~EvGuard() { for (int i = 0; i < 4; ++i) c->event_pool.push_back(e[i]); }
+        } evg{c, ev};
+
+        diag->kept_fraction = 1.0;
+        diag->aborted = 0;
+        diag->abort_step = 0;
+        diag->n_updates = 0;
+        uint64_t maxb = 1;
+        for (int b = 0; b < nb; ++b) maxb = std::max<uint64_t>(maxb, (uint64_t)s->dr[b]);
+        diag->max_bond_dim = maxb;
+
+        for (size_t step = 0; step < n_steps; ++step) {
+            for (size_t sw = 0; sw < n_sweeps; ++sw) {
+                for (int b = sweeps[sw].bond_parity; b < nb; b += 2) {
+                    const double* gp = gates[sw * nb + b];
+                    if (gp == nullptr) continue;
+                    const cplx* G = staged[gp];
+                    const int d1 = s->d[b], d2 = s->d[b + 1];
+                    const int cl = s->dl[b], cm = s->dr[b], cr = s->dr[b + 1];
+                    const double* ll = b > 0 ? s->lam[b - 1] : nullptr;
+                    const double* lm = s->lam[b];
+                    const double* lr = b + 2 < n ? s->lam[b + 1] : nullptr;
+                    const DecimPlan pl = plan_decimation(d1, d2, cl, cr, s->chi_max, be->kind, be->target_rank,
+                                                         be->oversampling, be->det_crossover);
+                    if (pl.randomized && be->accuracy_check)
+                        throw_contract(c, "evolve: accuracy_check (fixed-precision RRSVD) is not implemented on the device yet");
+                    const uint64_t call_seed = be->seed++;
+                    cplx* M1 = ws_get<cplx>(c, (size_t)pl.m * pl.n);
+                    cplx* M2 = ws_get<cplx>(c, (size_t)pl.m * pl.n);
+                    check_cuda(c, cudaEventRecord(ev[0], c->stream), "event");
+                    build_theta_device(c, s->g[b], s->g[b + 1], ll, lm, lr, cl, d1, cm, d2, cr, M1);
+                    check_cuda(c, cudaEventRecord(ev[1], c->stream), "event");
+                    apply_gate_device(c, G, d1, d2, cl, cr, M1, M2);
+                    check_cuda(c, cudaEventRecord(ev[2], c->stream), "event");
+                    ensure_gamma(s, b, (size_t)pl.m * pl.kmax);
+                    ensure_gamma(s, b + 1, (size_t)pl.kmax * pl.n);
+                    ensure_lambda(s, b, (size_t)pl.kmax);
+                    decimate_device(c, pl, M2, d1, cr, ll, lr, s->chi_max, s->tol, (int)be->power_iterations,
+                                    call_seed, omode, nullptr, renorm, s->g[b], s->lam[b], s->g[b + 1], sc_dev);
+                    check_cuda(c, cudaEventRecord(ev[3], c->stream), "event");
+                    check_cuda(c, cudaMemcpyAsync(sc_host, sc_dev, sizeof(DecimScalars), cudaMemcpyDeviceToHost, c->stream), "D2H");
+                    check_cuda(c, cudaStreamSynchronize(c->stream), "sync");
+                    if (c->gemm_timing) flush_gemm_timing(c);
+                    ws_reset(c);
+                    if (sc_host->nonfinite) throw_contract(c, "decimate: theta has non-finite entries");
+                    if (sc_host->total_sq == 0.0) throw_contract(c, "decimate: theta is identically zero");
+                    const int kept = sc_host->kept;
+                    s->dr[b] = kept;
+                    s->dl[b + 1] = kept;
+                    diag->kept_fraction *= 1.0 - sc_host->discarded;
+                    diag->max_bond_dim = std::max<uint64_t>(diag->max_bond_dim, (uint64_t)kept);
+                    if (records && diag->n_updates < max_records) {
+                        float t01 = 0, t12 = 0, t23 = 0;
+                        cudaEventElapsedTime(&t01, ev[0], ev[1]);
+                        cudaEventElapsedTime(&t12, ev[1], ev[2]);
+                        cudaEventElapsedTime(&t23, ev[2], ev[3]);
+                        records[diag->n_updates] = {step, (uint64_t)b, (uint64_t)kept, sc_host->discarded,
+                                                    1e3 * t01, 1e3 * t12, 1e3 * t23, pl.randomized ? 1 : 0};
+                    }
+                    diag->n_updates++;
+                    if (1.0 - diag->kept_fraction > abort_thr) {  // tebd.cpp:317-321
+                        diag->aborted = 1;
+                        diag->abort_step = step;
+                        return;
+                    }
+                }
+            }
+        }
+    });
+}
+
+int rrsvd_b200_expectation_local(rrsvd_b200_mps* s, size_t site, const double* op, double* out2) {
+    return mps_api(s, [&](rrsvd_b200_ctx* c) {
+        if (site >= (size_t)s->n) throw_contract(c, "expectation_local: bad site");
+        if (op == nullptr || out2 == nullptr) throw_contract(c, "expectation_local: null argument");
+        const int d = s->d[site];
+        const auto* dop = static_cast<const cplx*>(stage_in(c, op, (size_t)d * d * sizeof(cplx)));
+        const double* ll = site > 0 ? s->lam[site - 1] : nullptr;
+        const double* lr = site + 1 < (size_t)s->n ? s->lam[site] : nullptr;
+        double* res = ws_get<double>(c, 2 * kNumSMs * 2 + 2);
+        check_cuda(c, expectation_local_dev(s->g[site], s->dl[site], d, s->dr[site], ll, lr, dop, res, c->stream),
+                   "expectation_local");
+        c->launches += 2;
+        double h[2];
+        check_cuda(c, cudaMemcpyAsync(h, res + 4 * kNumSMs, 2 * sizeof(double), cudaMemcpyDeviceToHost, c->stream), "D2H");
+        check_cuda(c, cudaStreamSynchronize(c->stream), "sync");
+        out2[0] = h[0];
+        out2[1] = h[1];
+    });
+}
+
+int rrsvd_b200_schmidt_entropy(rrsvd_b200_mps* s, size_t bond, double* out) {
+    return mps_api(s, [&](rrsvd_b200_ctx* c) {
+        if (bond + 1 >= (size_t)s->n) throw_contract(c, "schmidt_entropy: bad bond");
+        double* res = ws_get<double>(c, 1);
+        check_cuda(c, schmidt_entropy_dev(s->lam[bond], s->dr[bond], res, c->stream), "schmidt_entropy");
+        c->launches++;
+        check_cuda(c, cudaMemcpyAsync(out, res, sizeof(double), cudaMemcpyDeviceToHost, c->stream), "D2H");
+        check_cuda(c, cudaStreamSynchronize(c->stream), "sync");
+    });
+}
+
+}  // extern "C"

@@ -36,4 +36,38 @@ void rrsvd_core(rrsvd_b200_ctx* c, const cplx* A, int m, int n, int l, int q, co
 // Full SVD by one-sided Jacobi (linalg.cpp:67-88): U (m x r), sigma (r), V (n x r), r = min(m,n).
 void svd_jacobi(rrsvd_b200_ctx* c, const cplx* A, int m, int n, cplx* U, double* sigma, cplx* V);
 
+// Device scalars of one decimation, read back by the host at the end of an update.
+struct DecimScalars {
+    int kept;
+    int nonfinite;
+    int pinv;
+    int pad;
+    double total_sq;
+    double discarded;
+};
+
+struct DecimPlan {  // host-side decisions of decimate (tebd.cpp:144-186)
+    int m, n, minor;
+    bool randomized;
+    int l;      // sketch width (randomized) ; ns = l or minor
+    int ns;
+    int kmax;   // upper bound on the kept rank
+};
+DecimPlan plan_decimation(int d1, int d2, int cl, int cr, size_t chi_max, int kind, size_t target_rank,
+                          size_t oversampling, size_t det_crossover);
+
+// The whole decimation of an unfolded M on the device: norm, factorization (RRSVD or Jacobi),
+// truncation, λ renormalisation, Γ reshape.  Writes gamma_l (m x kept), lambda (kept),
+// gamma_r (kept x n) packed with the device-side kept; scalars into *sc (device).
+void decimate_device(rrsvd_b200_ctx* c, const DecimPlan& pl, const cplx* M, int d1, int cr,
+                     const double* ll, const double* lr, size_t chi_max, double trunc_tol, int q,
+                     uint64_t call_seed, int omega_mode, const cplx* omega, int renormalize,
+                     cplx* gamma_l, double* lambda, cplx* gamma_r, DecimScalars* sc);
+
+// Θ = λΓλΓλ in the unfolded layout (tebd.cpp:76-124) and the gate (tebd.cpp:126-139).
+void build_theta_device(rrsvd_b200_ctx* c, const cplx* G1, const cplx* G2, const double* ll,
+                        const double* lm, const double* lr, int cl, int d1, int cm, int d2, int cr, cplx* M);
+void apply_gate_device(rrsvd_b200_ctx* c, const cplx* G, int d1, int d2, int cl, int cr,
+                       const cplx* Min, cplx* Mout);
+
 }  // namespace rb

@@ -51,7 +51,7 @@ __global__ void __launch_bounds__(CHOL_THREADS) chol_inv_kernel(const __grid_con
     // ---- right-looking Cholesky, G = R^H R, R upper, row j of R overwrites row j of G.
     for (int j = 0; j < l; ++j) {
         const double d = P[poff(j, l)].x;
-        const bool isdead = !(d > kDepTol * g0[j]) || !(g0[j] > 0.0);
+        const bool isdead = !(d > b.dep_tol[p] * g0[j]) || !(d > 0.0) || !(g0[j] > 0.0);
         const double rjj = isdead ? 0.0 : sqrt(d);
         const double inv = isdead ? 0.0 : 1.0 / rjj;
         const int oj = poff(j, l);
@@ -110,7 +110,7 @@ __global__ void __launch_bounds__(CHOL_THREADS) chol_inv_kernel(const __grid_con
 
 // ============================================================================ Jacobi SVD
 constexpr int JAC_THREADS = 256;
-constexpr int kMaxSweeps = 30;
+constexpr int kMaxSweeps = 60;
 
 __device__ __forceinline__ int circle(int i, int t, int n) {  // round-robin slot -> player
     return i == 0 ? 0 : ((i - 1 + t) % (n - 1)) + 1;

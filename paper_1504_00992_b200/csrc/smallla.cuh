@@ -8,11 +8,13 @@ constexpr int kMaxSmall = 32;  // problems per launch of the small-matrix kernel
 
 // ---- Cholesky + triangular inverse (the "R^-1" of one CholeskyQR pass) -------------------
 // G (l x l, Hermitian, row-major) -> T = R^-1 (l x l upper, zeros below), G (+ s I) = R^H R.
-// Columns whose Cholesky pivot falls below kDepTol * (original diagonal) are numerically
-// dependent: their T column is zeroed, so the orthonormalised basis gets a zero column
-// (the reference's Householder QR returns an arbitrary orthonormal completion there,
-// linalg.hpp:35-37; either way no NaN and an unchanged span).
-constexpr double kDepTol = 1e-12;
+// Columns whose Cholesky pivot falls to <= dep_tol * (original diagonal) (or to <= 0) are
+// numerically dependent: their T column is zeroed, so the orthonormalised basis gets a zero
+// column (the reference's Householder QR returns an arbitrary orthonormal completion there,
+// linalg.hpp:35-37; either way no NaN and an unchanged span).  The shifted first pass uses
+// dep_tol = 0 (its pivots are >= the shift, so only exactly-zero columns die — anything else
+// would discard genuine small-σ directions); the refinement passes use kDepTol.
+constexpr double kDepTol = 1e-14;
 constexpr int kMaxCholL = 168;  // packed upper triangle must fit in 227 KB of shared memory
 
 struct CholBatch {
@@ -21,6 +23,7 @@ struct CholBatch {
     const cplx* G[kMaxSmall];
     cplx* T[kMaxSmall];
     double shift_scale[kMaxSmall];  // 0: no shift; else s = shift_scale * u * trace(G)
+    double dep_tol[kMaxSmall];      // relative pivot floor for "dependent"
     int* ndead[kMaxSmall];          // nullable: number of dependent columns found
 };
 cudaError_t chol_inv(const CholBatch& b, int max_l, cudaStream_t s);

@@ -246,6 +246,65 @@ __global__ void weight_kernel(const double* sigma, int k, const double* total_sq
     *w = v < 0.0 ? 0.0 : (v > 1.0 ? 1.0 : v);
 }
 
+// ============================================================================ observables
+constexpr int OBS_BLOCKS = 2 * kNumSMs;
+
+__global__ void __launch_bounds__(256) expect_partial(const cplx* __restrict__ G, int dl, int d, int dr,
+                                                      const double* ll, const double* lr,
+                                                      const cplx* __restrict__ op, double* part) {
+    __shared__ cplx so[32 * 32];
+    for (int i = threadIdx.x; i < d * d; i += blockDim.x) so[i] = op[i];
+    __syncthreads();
+    cplx acc = mk(0.0, 0.0);
+    const long long pairs = (long long)dl * dr;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < pairs;
+         e += (long long)gridDim.x * blockDim.x) {
+        const int a = (int)(e / dr), b = (int)(e % dr);
+        const double wa = ll ? ll[a] * ll[a] : 1.0;
+        const double w = wa * (lr ? lr[b] * lr[b] : 1.0);
+        const cplx* g = G + (long long)a * d * dr + b;
+        cplx s = mk(0.0, 0.0);
+        for (int ip = 0; ip < d; ++ip) {
+            cplx t = mk(0.0, 0.0);
+            for (int i = 0; i < d; ++i) cfma(t, so[ip * d + i], g[(long long)i * dr]);
+            cfmac(s, g[(long long)ip * dr], t);
+        }
+        acc.x += w * s.x;
+        acc.y += w * s.y;
+    }
+    __shared__ cplx red[8];
+    acc = warp_sum(acc);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        cplx t = mk(0.0, 0.0);
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t = cadd(t, red[w]);
+        part[2 * blockIdx.x] = t.x;
+        part[2 * blockIdx.x + 1] = t.y;
+    }
+}
+
+__global__ void expect_final(const double* part, double* out) {
+    if (threadIdx.x != 0) return;
+    double re = 0.0, im = 0.0;
+    for (int i = 0; i < OBS_BLOCKS; ++i) {
+        re += part[2 * i];
+        im += part[2 * i + 1];
+    }
+    out[0] = re;
+    out[1] = im;
+}
+
+__global__ void entropy_kernel(const double* lam, int n, double* out) {
+    if (threadIdx.x != 0) return;
+    double s = 0.0;
+    for (int i = 0; i < n; ++i) {
+        const double p = lam[i] * lam[i];
+        if (p > 0.0) s -= p * log(p);
+    }
+    *out = s;
+}
+
 // ============================================================================ peak probes
 constexpr int PROBE_ITERS = 4096;
 
@@ -341,6 +400,19 @@ cudaError_t conj_transpose(const cplx* A, int rows, int cols, cplx* out, cudaStr
 cudaError_t discarded_weight(const double* sigma, int k, const double* total_sq, double* w,
                              cudaStream_t s) {
     weight_kernel<<<1, 32, 0, s>>>(sigma, k, total_sq, w);
+    return cudaGetLastError();
+}
+
+cudaError_t expectation_local_dev(const cplx* G, int dl, int d, int dr, const double* ll,
+                                  const double* lr, const cplx* op, double* res, cudaStream_t s) {
+    if (d > 32) return cudaErrorInvalidValue;
+    expect_partial<<<OBS_BLOCKS, 256, 0, s>>>(G, dl, d, dr, ll, lr, op, res);
+    expect_final<<<1, 32, 0, s>>>(res, res + 2 * OBS_BLOCKS);
+    return cudaGetLastError();
+}
+
+cudaError_t schmidt_entropy_dev(const double* lam, int n, double* out, cudaStream_t s) {
+    entropy_kernel<<<1, 32, 0, s>>>(lam, n, out);
     return cudaGetLastError();
 }
 

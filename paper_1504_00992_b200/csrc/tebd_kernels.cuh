@@ -68,6 +68,14 @@ cudaError_t conj_transpose(const cplx* A, int rows, int cols, cplx* out, cudaStr
 cudaError_t discarded_weight(const double* sigma, int k, const double* total_sq, double* w,
                              cudaStream_t s);
 
+// <psi|O|psi> at one site in canonical form (mps.cpp:50-70):
+//   sum_{a,b} ll[a]^2 lr[b]^2 sum_{i',i} conj(G[a,i',b]) O[i',i] G[a,i,b]   (ll/lr null -> 1).
+// res: scratch of >= 4*148+2 doubles; the result (re, im) lands in res[4*148..4*148+1].
+cudaError_t expectation_local_dev(const cplx* G, int dl, int d, int dr, const double* ll,
+                                  const double* lr, const cplx* op, double* res, cudaStream_t s);
+// -sum λ² ln λ² (mps.cpp:40-48), sequential order.
+cudaError_t schmidt_entropy_dev(const double* lam, int n, double* out, cudaStream_t s);
+
 // Peak probes (diagnostics): TFLOP/s of DMMA f64 and of DFMA.
 cudaError_t probe_peak(int what, double* tflops, cudaStream_t s);
 

@@ -1,0 +1,160 @@
+"""Host-side model builders for the benchmarks and parity runs (off the hot path).
+
+Restatements of the reference's CPU-cheap preprocessing, which the survey marks out of scope
+for the device: bond Hamiltonians (tebd.cpp:375-404), the TEDOPA chain
+map (chainmap.cpp:58-68,108-153,197-252), the 3rd-order Trotter plan (tebd.cpp:67-74) and
+bond gates exp(-i·s·h) (tebd.cpp:239-258).  They produce INPUTS for the device path; the
+CPU tests pin them against the reference library.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+SX = np.array([[0, 1], [1, 0]], np.complex128)
+SY = np.array([[0, -1j], [1j, 0]], np.complex128)
+SZ = np.array([[1, 0], [0, -1]], np.complex128)
+
+
+def trotter_plan_3rd(dt: float):
+    """tebd.cpp:67-74: sweeps (bond parity, coefficient) = (1, ½), (0, 1), (1, ½)."""
+    if dt == 0.0:
+        raise ValueError("trotter_plan_3rd: dt must be nonzero")
+    return [(1, 0.5), (0, 1.0), (1, 0.5)]
+
+
+def ising_terms(n: int, coupling: float, field: float) -> list[np.ndarray]:
+    """tebd.cpp:375-388: H = -J Σ σzσz - g Σ σx, fields split between neighbouring bonds."""
+    if n < 2:
+        raise ValueError("ising_terms: need at least two sites")
+    i2 = np.eye(2)
+    terms = []
+    for b in range(n - 1):
+        h = -coupling * np.kron(SZ, SZ)
+        h = h - field * (1.0 if b == 0 else 0.5) * np.kron(SX, i2)
+        h = h - field * (1.0 if b + 2 == n else 0.5) * np.kron(i2, SX)
+        terms.append(h.astype(np.complex128))
+    return terms
+
+
+def heisenberg_terms(n: int, coupling: float) -> list[np.ndarray]:
+    """tebd.cpp:390-404."""
+    h = coupling * (np.kron(SX, SX) + np.kron(SY, SY) + np.kron(SZ, SZ))
+    return [h.astype(np.complex128) for _ in range(n - 1)]
+
+
+def bond_gate(h: np.ndarray, scale: float) -> np.ndarray:
+    """exp(-i·scale·h) of a Hermitian term via its eigendecomposition (tebd.cpp:239-258)."""
+    w, v = np.linalg.eigh(h)
+    return (v * np.exp(-1j * scale * w)) @ v.conj().T
+
+
+def trapezoid_measure(nodes: np.ndarray, h2: np.ndarray):
+    """chainmap.cpp:58-68."""
+    n = nodes.size
+    w = np.empty(n)
+    w[0] = 0.5 * (nodes[1] - nodes[0])
+    w[-1] = 0.5 * (nodes[-1] - nodes[-2])
+    w[1:-1] = 0.5 * (nodes[2:] - nodes[:-2])
+    return nodes, w * h2
+
+
+def stieltjes_coefficients(nodes: np.ndarray, weights: np.ndarray, n_chain: int):
+    """Discretised Stieltjes with full reorthogonalisation (chainmap.cpp:108-153).
+    Returns (t0, omegas[n_chain], hoppings[n_chain-1])."""
+    x, w = nodes, weights
+    beta0 = float(np.sum(w))
+    polys = [np.full(x.size, 1.0 / np.sqrt(beta0))]
+    alpha = np.zeros(n_chain)
+    beta = np.zeros(n_chain)
+    for j in range(n_chain):
+        pj = polys[j]
+        u = x * pj
+        alpha[j] = np.dot(w * u, pj)
+        if j + 1 == n_chain:
+            break
+        u = u - alpha[j] * pj
+        if j > 0:
+            u = u - np.sqrt(beta[j - 1]) * polys[j - 1]
+        for _ in range(2):
+            for pk in polys:
+                u = u - np.dot(w * u, pk) * pk
+        b = np.dot(w * u, u)
+        if not (b > 0.0 and np.isfinite(b)):
+            raise ArithmeticError(f"recurrence breakdown at coefficient {j + 1}")
+        beta[j] = b
+        polys.append(u / np.sqrt(b))
+    return np.sqrt(beta0), alpha, np.sqrt(beta[:n_chain - 1])
+
+
+def ohmic_chain(n_chain: int = 100, n_nodes: int = 20001):
+    """The config-3 bath: h²(x) = x on [0, 1] with 20001 trapezoid nodes."""
+    x = np.linspace(0.0, 1.0, n_nodes)
+    nodes, w = trapezoid_measure(x, x.copy())
+    return stieltjes_coefficients(nodes, w, n_chain)
+
+
+def build_chain_terms(t0, omegas, hoppings, boson_dim: int, h_sys: np.ndarray,
+                      coupling: np.ndarray) -> tuple[list[int], list[np.ndarray]]:
+    """chainmap.cpp:197-252: system ⊗ boson bond plus boson-boson bonds; on-site ω split evenly
+    between the two bonds of a site (full share on the last bond).  Returns (site_dims, terms)."""
+    n_chain = len(omegas)
+    d_sys = h_sys.shape[0]
+    b = np.diag(np.sqrt(np.arange(1, boson_dim, dtype=float)), 1).astype(np.complex128)
+    bd = b.conj().T
+    num = np.diag(np.arange(boson_dim, dtype=float)).astype(np.complex128)
+    ib = np.eye(boson_dim, dtype=np.complex128)
+    isys = np.eye(d_sys, dtype=np.complex128)
+
+    def left_share(n):
+        return 1.0 if n + 1 == n_chain else 0.5
+
+    terms = []
+    h = np.kron(h_sys, ib) + t0 * np.kron(coupling, b + bd) + left_share(0) * omegas[0] * np.kron(isys, num)
+    terms.append(h)
+    for n in range(1, n_chain):
+        h = hoppings[n - 1] * np.kron(bd, b) + hoppings[n - 1] * np.kron(b, bd)
+        h = h + (1.0 - left_share(n - 1)) * omegas[n - 1] * np.kron(num, ib)
+        h = h + left_share(n) * omegas[n] * np.kron(ib, num)
+        terms.append(h)
+    return [d_sys] + [boson_dim] * n_chain, terms
+
+
+def tedopa_system(n_chain: int = 100, boson_dim: int = 20, eps: float = 1.0, delta: float = 1.0):
+    """Spin-boson TEDOPA chain of config 3: h_sys = ½ε σz + ½Δ σx, A = σz (experiments.cpp
+    tedopa-chain branch), ohmic bath mapped to n_chain oscillators of dimension boson_dim."""
+    t0, om, hop = ohmic_chain(n_chain)
+    h_sys = 0.5 * eps * SZ + 0.5 * delta * SX
+    return build_chain_terms(t0, om, hop, boson_dim, h_sys, SZ)
+
+
+def saturated_bond_dims(site_dims, chi: int) -> list[int]:
+    """χ_b = min(χ, Π_{s≤b} d_s, Π_{s>b} d_s): the largest canonical bond dimensions."""
+    n = len(site_dims)
+    out = []
+    for b in range(n - 1):
+        left = 1
+        for s in range(b + 1):
+            left = min(left * site_dims[s], chi)
+        right = 1
+        for s in range(b + 1, n):
+            right = min(right * site_dims[s], chi)
+        out.append(min(chi, left, right))
+    return out
+
+
+def synthetic_saturated_mps(site_dims, chi: int, seed: int = 0, decay: float = 0.9):
+    """The timing state of SURVEY §8(d) C2/C3: χ-saturated bonds, Gaussian Γ/√(χ_l d), λ ∝ decay^i
+    normalised.  Returns (gammas, lambdas) as numpy arrays."""
+    rng = np.random.default_rng(seed)
+    bonds = saturated_bond_dims(site_dims, chi)
+    n = len(site_dims)
+    gammas, lambdas = [], []
+    for s in range(n):
+        cl = 1 if s == 0 else bonds[s - 1]
+        cr = 1 if s == n - 1 else bonds[s]
+        g = (rng.standard_normal((cl, site_dims[s], cr)) + 1j * rng.standard_normal((cl, site_dims[s], cr)))
+        gammas.append(g / np.sqrt(cl * site_dims[s]))
+    for b in range(n - 1):
+        v = decay ** np.arange(bonds[b])
+        lambdas.append(v / np.linalg.norm(v))
+    return gammas, lambdas
