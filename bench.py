@@ -1,0 +1,336 @@
+#!/usr/bin/env python
+"""Benchmark of the B200-native TEBD two-site decimation path (BASELINE.json metric).
+
+Headline workload (north star, BASELINE.json configs[2]): TEDOPA spin-boson chain, spin + 100
+oscillators (d=20), χ=100 (n = d·χ = 2000 at interior bonds), RRSVD decimation p=10, q=2,
+3rd-order Trotter (150 two-site updates per step).  A "step" is one TEBD step on a χ-saturated
+synthetic MPS (Gaussian Γ, λ ∝ 0.9^i) held in HBM; the gates are the real
+TEDOPA bond gates.  Inputs are larger than L2 (MPS ≈ 320 MB > 126 MB) so no L2 flush is needed.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload c3|c2|c1]
+
+Under torchrun (N > 1) every rank evolves its own chain (weak scaling, replicas) and rank 0 prints
+the max-over-ranks timing.  `--impl reference` times the reference C++ core (oracle/_ref, built
+from /root/reference) on the host cores on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "TEBD steps/s at n=d·χ (RRSVD decimation; FP64 tensor-core roofline of the zgemm stages)"
+
+
+# ----------------------------------------------------------------------------- workloads
+
+def workload(name: str):
+    from paper_1504_00992_b200 import models as M
+    if name == "c3":
+        site_dims, terms = M.tedopa_system(n_chain=100, boson_dim=20)
+        return dict(name="tedopa_spin_boson_101sites_d20_chi100", site_dims=site_dims,
+                    terms={b: t for b, t in enumerate(terms)}, chi=100, dt=0.01,
+                    backend=dict(randomized=True, target_rank=0, oversampling=10, power_iterations=2,
+                                 det_crossover=256, seed=7),
+                    desc="TEDOPA spin-boson, spin + 100 bosons (d=20), chi=100, n=2000, RRSVD p=10 q=2")
+    if name == "c2":
+        n = 64
+        return dict(name="ising_L64_d2_chi128", site_dims=[2] * n,
+                    terms={b: t for b, t in enumerate(M.ising_terms(n, 1.0, 1.0))}, chi=128, dt=0.01,
+                    backend=dict(randomized=False, det_crossover=256, seed=7),
+                    desc="Ising L=64, d=2, chi=128 (n=256), deterministic (reference default crossover)")
+    raise SystemExit(f"unknown workload {name}")
+
+
+def updates_per_step(site_dims, terms):
+    nb = len(site_dims) - 1
+    return sum(1 for par, _ in [(1, .5), (0, 1.), (1, .5)] for b in range(par, nb, 2) if b in terms)
+
+
+def state_bytes(gammas, lambdas):
+    return int(sum(g.size * 16 for g in gammas) + sum(l.size * 8 for l in lambdas))
+
+
+# ----------------------------------------------------------------------------- clocks
+
+class ClockSampler:
+    """nvidia-smi sampling DURING the timed region (B200_PROFILING.md clocks line)."""
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = float(f[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- our arm
+
+def run_ours(args, rank, world, local_rank):
+    import torch
+    import paper_1504_00992_b200 as P
+    from paper_1504_00992_b200 import models as M
+    from paper_1504_00992_b200.tebd import DeviceMps, build_gates, evolve
+
+    torch.cuda.set_device(local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl")
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
+    ctx = P.Context(local_rank, stream=stream.cuda_stream)  # library work and events share one stream
+    peak_dmma = P.probe_peak(0, ctx=ctx)
+    wl = workload(args.workload)
+    site_dims, terms, chi = wl["site_dims"], wl["terms"], wl["chi"]
+    plan, gates = build_gates(site_dims, terms, wl["dt"])
+    gammas, lambdas = M.synthetic_saturated_mps(site_dims, chi, seed=1 + rank)
+    mps = DeviceMps(site_dims, chi, 0.0, ctx=ctx)
+    mps.load(gammas, lambdas)
+    be = P.DecimationBackend(omega_mode=P.OMEGA_PHILOX, **wl["backend"])
+    ups = updates_per_step(site_dims, terms)
+
+    def one_step():
+        return evolve(mps, terms, wl["dt"], 1, be, record_updates=False, gates=gates, plan=plan)
+
+    for _ in range(args.warmup):
+        one_step()
+        mps.load(gammas, lambdas)  # keep the saturated timing state (χ stays at the cap)
+
+    # ---- device-resident timed region
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    lib = P.lib()
+    launches0 = ctx.launches
+    ctx.check(lib.rrsvd_b200_set_gemm_timing(ctx.h, 1))
+    if dist:
+        dist.barrier()
+    ctx.synchronize()
+    torch.cuda.synchronize()
+    with ClockSampler(local_rank) as clk:
+        t0 = time.perf_counter()
+        ev0.record(stream)
+        diag = evolve(mps, terms, wl["dt"], args.steps, be, record_updates=True, gates=gates, plan=plan)
+        ev1.record(stream)
+        ev1.synchronize()
+        t1 = time.perf_counter()
+    elapsed = ev0.elapsed_time(ev1) / 1e3  # device time (CUDA events on the launching stream)
+    wall = t1 - t0
+    gpu_launches = ctx.launches - launches0
+    import ctypes as C
+    fl, ms, calls = C.c_double(), C.c_double(), C.c_uint64()
+    ctx.check(lib.rrsvd_b200_gemm_stats(ctx.h, C.byref(fl), C.byref(ms), C.byref(calls)))
+    ctx.check(lib.rrsvd_b200_set_gemm_timing(ctx.h, 0))
+    dev_update_us = sum(u["t_theta_us"] + u["t_gate_us"] + u["t_svd_us"] for u in diag.updates)
+    if dist:
+        t = torch.tensor([elapsed], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        elapsed = float(t.item())
+    steps_per_s = world * args.steps / elapsed
+
+    # ---- end-to-end through the C ABI with HOST buffers (pinned), H2D + D2H inside the region
+    pin_g = [torch.from_numpy(g).pin_memory() for g in gammas]
+    pin_l = [torch.from_numpy(l).pin_memory() for l in lambdas]
+    h2d = state_bytes(gammas, lambdas)
+    e2e_steps = max(1, min(args.steps, 3))
+    out_g = [torch.empty(g.shape, dtype=torch.complex128).pin_memory() for g in gammas]
+    if dist:
+        dist.barrier()
+    te0 = time.perf_counter()
+    d2h = 0
+    for _ in range(e2e_steps):
+        for s in range(len(site_dims)):
+            mps.set_site(s, pin_g[s], pin_l[s] if s < len(pin_l) else None)
+        one_step()
+        d2h = 0
+        for s in range(len(site_dims)):
+            dims = mps.dims(s)
+            buf = out_g[s] if tuple(out_g[s].shape) == dims else torch.empty(dims, dtype=torch.complex128).pin_memory()
+            ctx.check(lib.rrsvd_b200_mps_get_site(mps.h, s, None, C.c_void_p(buf.data_ptr()), None))
+            d2h += buf.numel() * 16
+        for b in range(len(site_dims) - 1):
+            d2h += mps.dims(b)[2] * 8
+    te1 = time.perf_counter()
+    e2e = world * e2e_steps / (te1 - te0)
+
+    clocks = clk.summary()
+    achieved = fl.value / (ms.value * 1e-3) / 1e12 if ms.value > 0 else 0.0
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(steps_per_s, 6), "unit": "steps/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * elapsed / args.steps, 3),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128 (fp64)",
+            "data": "synthetic χ-saturated MPS (Gaussian Γ, λ∝0.9^i) + real TEDOPA bond gates",
+            "config": {"workload": wl["name"], "desc": wl["desc"], "sites": len(site_dims), "chi": chi,
+                       "updates_per_step": ups, "sketch": "Philox in-kernel",
+                       "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
+                       "l2": "inputs larger than L2 (MPS %.0f MB)" % (h2d / 1e6)},
+            "decimations_per_s": round(world * ups * args.steps / elapsed, 3),
+            "roofline": {"bound": "tensor", "kernel": "zgemm_dmma (all zgemm-stage launches)",
+                         "achieved": round(achieved, 3), "peak": round(peak_dmma, 3), "unit": "TFLOP/s",
+                         "frac": round(achieved / peak_dmma, 4) if peak_dmma else None,
+                         "peak_source": "measured live: DMMA probe (mma.sync m8n8k4 f64) on this GPU;"
+                                        " MEASURED_PEAKS.json has no FP64 entry",
+                         "frac_of_40tf_nominal": round(achieved / 40.0, 4),
+                         "gemm_time_share": round(ms.value / (1e3 * elapsed), 4),
+                         "gemm_launches": int(calls.value), "traffic": None},
+            "e2e": {"value": round(e2e, 6), "unit": "steps/s", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": int(d2h)},
+            "gpu_launches": int(gpu_launches),
+            "clocks": clocks,
+            "device_time_per_step_ms": round(dev_update_us / 1e3 / args.steps, 3),
+            "wall_ms_per_step": round(1e3 * wall / args.steps, 3),
+        }
+        if not args.no_cpu_baseline and world == 1:
+            line["cpu_baseline"] = cpu_baseline(args, wl, gammas, lambdas, gates, plan, samples=2)
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+# ----------------------------------------------------------------------------- CPU reference
+
+def ref_update_sample(ref, wl, gammas, lambdas, gates, plan, bonds, seed):
+    """Times the reference's build_theta → apply_gate_to_theta → decimate on the given bonds of
+    the same synthetic state (tebd.cpp:296-306), returns seconds per update."""
+    be = ref.Backend(**wl["backend"])
+    be.seed = seed
+    n = len(wl["site_dims"])
+    t = 0.0
+    for b in bonds:
+        s = 0 if (b % 2 == 1) else 1  # a sweep of this bond's parity
+        g = gates[(s, b)]
+        ll = lambdas[b - 1] if b > 0 else None
+        lr = lambdas[b + 1] if b + 2 < n else None
+        t0 = time.perf_counter()
+        th = ref.apply_gate(ref.build_theta(gammas[b], gammas[b + 1], ll, lambdas[b], lr), g)
+        ref.decimate(th, ll, lr, wl["chi"], 0.0, be)
+        t += time.perf_counter() - t0
+    return t / len(bonds)
+
+
+def cpu_baseline(args, wl, gammas, lambdas, gates, plan, samples=2):
+    from oracle import ref
+    cores = os.cpu_count() or 1
+    ref.set_threads(cores)
+    nb = len(wl["site_dims"]) - 1
+    bonds = [nb // 2 - 1 + i for i in range(samples)]
+    sec = ref_update_sample(ref, wl, gammas, lambdas, gates, plan, bonds, 7)
+    ups = updates_per_step(wl["site_dims"], wl["terms"])
+    return {"value": round(1.0 / (sec * ups), 8), "unit": "steps/s", "cores": cores, "kind": "reference",
+            "sample": f"{samples} interior bond updates (build_theta+apply_gate+decimate, RRSVD) of the "
+                      f"same state, {sec:.3f} s/update, extrapolated x{ups} updates/step",
+            "blas": ref.blas_info()["core"]}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    from oracle import ref
+    from paper_1504_00992_b200 import models as M
+    from paper_1504_00992_b200.tebd import build_gates
+    if not ref.available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/librrsvd_ref.so not built"}))
+        return
+    cores = os.cpu_count() or 1
+    ref.set_threads(cores)
+    wl = workload(args.workload)
+    plan, gates = build_gates(wl["site_dims"], wl["terms"], wl["dt"])
+    gammas, lambdas = M.synthetic_saturated_mps(wl["site_dims"], wl["chi"], seed=1)
+    nb = len(wl["site_dims"]) - 1
+    ups = updates_per_step(wl["site_dims"], wl["terms"])
+    for w in range(args.warmup):
+        ref_update_sample(ref, wl, gammas, lambdas, gates, plan, [nb // 2], 100 + w)
+    secs = []
+    for k in range(args.steps):
+        secs.append(ref_update_sample(ref, wl, gammas, lambdas, gates, plan, [nb // 2 - 1 + (k % 2)], 7 + k))
+    per_update = sum(secs) / len(secs)
+    v = 1.0 / (per_update * ups)
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": round(v, 8), "unit": "steps/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * per_update * ups, 1),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128 (fp64)",
+        "data": "synthetic χ-saturated MPS + real TEDOPA bond gates",
+        "config": {"workload": wl["name"], "desc": wl["desc"]},
+        "cpu_baseline": {"value": round(v, 8), "unit": "steps/s", "cores": cores, "kind": "reference",
+                         "sample": f"each step = 1 interior bond update (build_theta+apply_gate+decimate) "
+                                   f"timed on the host, extrapolated x{ups} updates/step",
+                         "blas": ref.blas_info()["core"]},
+        "e2e": {"value": round(v, 8), "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="c3", choices=["c3", "c2"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+    else:
+        run_ours(args, rank, world, local_rank)
+
+
+if __name__ == "__main__":
+    main()

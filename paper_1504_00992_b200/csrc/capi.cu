@@ -276,7 +276,7 @@ int rrsvd_b200_build_theta_unfolded(rrsvd_b200_ctx* c, const double* G1, const d
         const auto* dlr = static_cast<const double*>(stage_in(c, lr, cr * sizeof(double)));
         auto* dM = static_cast<cplx*>(stage_out(c, M, m * n * sizeof(cplx), outs));
         if (cm == 0) check_cuda(c, cudaMemsetAsync(dM, 0, m * n * sizeof(cplx), c->stream), "memset");
-        else build_theta_device(c, dG1, dG2, dll, dlm, dlr, (int)cl, (int)d1, (int)cm, (int)d2, (int)cr, dM);
+        else build_theta_many(c, {ThetaJob{dG1, dG2, dll, dlm, dlr, (int)cl, (int)d1, (int)cm, (int)d2, (int)cr, dM}});
         finish_out(c, outs);
     });
 }
@@ -291,7 +291,7 @@ int rrsvd_b200_apply_gate_unfolded(rrsvd_b200_ctx* c, const double* G, size_t d1
         const auto* dG = static_cast<const cplx*>(stage_in(c, G, dd * dd * sizeof(cplx)));
         const auto* dI = static_cast<const cplx*>(stage_in(c, M_in, tot * sizeof(cplx)));
         auto* dO = static_cast<cplx*>(stage_out(c, M_out, tot * sizeof(cplx), outs));
-        apply_gate_device(c, dG, (int)d1, (int)d2, (int)cl, (int)cr, dI, dO);
+        apply_gate_many(c, {GateJob{dG, (int)d1, (int)d2, (int)cl, (int)cr, dI, dO}});
         finish_out(c, outs);
     });
 }
@@ -350,9 +350,9 @@ int rrsvd_b200_decimate_unfolded(rrsvd_b200_ctx* c, const double* M, size_t d1, 
         cplx* gl = dev_gl ? reinterpret_cast<cplx*>(gamma_l) : ws_get<cplx>(c, m * kmax);
         double* lam = dev_lam ? lambda : ws_get<double>(c, kmax);
         cplx* gr = dev_gr ? reinterpret_cast<cplx*>(gamma_r) : ws_get<cplx>(c, kmax * n);
-        decimate_device(c, pl, dM, (int)d1, (int)cr, dll, dlr, chi_max, trunc_tol, (int)be->power_iterations,
-                        call_seed, omega_mode, dO, renormalize, gl, lam, gr,
-                        reinterpret_cast<DecimScalars*>(sc));
+        decimate_many(c, {DecimJob{pl, dM, (int)d1, (int)cr, dll, dlr, chi_max, trunc_tol,
+                                   (int)be->power_iterations, call_seed, omega_mode, dO, renormalize, gl, lam, gr,
+                                   reinterpret_cast<DecimScalars*>(sc)}});
         Scalars h;
         read_scalars(c, sc, &h);
         if (h.nonfinite) throw_contract(c, "decimate: theta has non-finite entries");

@@ -197,14 +197,15 @@ int rrsvd_b200_evolve(rrsvd_b200_mps* s, size_t n_sweeps, const rrsvd_b200_sweep
             ~GateGuard() { for (void* p : v) cudaFreeAsync(p, c->stream); }
         } guard{c, gate_bufs};
 
-        auto* sc_dev = static_cast<DecimScalars*>(nullptr);
-        check_cuda(c, cudaMallocAsync(reinterpret_cast<void**>(&sc_dev), sizeof(DecimScalars), c->stream), "alloc scalars");
+        DecimScalars* sc_dev = nullptr;
+        size_t sc_cap = 0;
         struct ScGuard {
             rrsvd_b200_ctx* c;
             void* p;
-            ~ScGuard() { cudaFreeAsync(p, c->stream); }
-        } scg{c, sc_dev};
-        auto* sc_host = static_cast<DecimScalars*>(pinned_scratch(c, sizeof(DecimScalars)));
+            ~ScGuard() {
+                if (p) cudaFreeAsync(p, c->stream);
+            }
+        } scg{c, nullptr};
         cudaEvent_t ev[4];
         for (auto& e : ev) e = pooled_event(c);
         struct EvGuard {
@@ -221,54 +222,83 @@ int rrsvd_b200_evolve(rrsvd_b200_mps* s, size_t n_sweeps, const rrsvd_b200_sweep
         for (int b = 0; b < nb; ++b) maxb = std::max<uint64_t>(maxb, (uint64_t)s->dr[b]);
         diag->max_bond_dim = maxb;
 
+        // All bonds of one sweep share a parity, hence no site: they are independent
+        // and go through every stage of the pipeline as ONE batch.  The results
+        // equal the reference's bond-by-bond order (tebd.cpp:291-306), including the per-call
+        // seeds, which are assigned in ascending bond order.
         for (size_t step = 0; step < n_steps; ++step) {
             for (size_t sw = 0; sw < n_sweeps; ++sw) {
-                for (int b = sweeps[sw].bond_parity; b < nb; b += 2) {
-                    const double* gp = gates[sw * nb + b];
-                    if (gp == nullptr) continue;
-                    const cplx* G = staged[gp];
+                std::vector<int> bonds;
+                for (int b = sweeps[sw].bond_parity; b < nb; b += 2)
+                    if (gates[sw * nb + b] != nullptr) bonds.push_back(b);
+                if (bonds.empty()) continue;
+                const size_t nbnd = bonds.size();
+                if (sc_cap < nbnd) {
+                    if (sc_dev) cudaFreeAsync(sc_dev, c->stream);
+                    check_cuda(c, cudaMallocAsync(reinterpret_cast<void**>(&sc_dev), nbnd * sizeof(DecimScalars), c->stream),
+                               "alloc scalars");
+                    sc_cap = nbnd;
+                    scg.p = sc_dev;
+                }
+                auto* sc_host = static_cast<DecimScalars*>(pinned_scratch(c, nbnd * sizeof(DecimScalars)));
+                std::vector<DecimPlan> plans(nbnd);
+                std::vector<ThetaJob> tj;
+                std::vector<GateJob> gj;
+                std::vector<DecimJob> dj;
+                std::vector<cplx*> M2(nbnd);
+                for (size_t i = 0; i < nbnd; ++i) {
+                    const int b = bonds[i];
                     const int d1 = s->d[b], d2 = s->d[b + 1];
                     const int cl = s->dl[b], cm = s->dr[b], cr = s->dr[b + 1];
-                    const double* ll = b > 0 ? s->lam[b - 1] : nullptr;
-                    const double* lm = s->lam[b];
-                    const double* lr = b + 2 < n ? s->lam[b + 1] : nullptr;
-                    const DecimPlan pl = plan_decimation(d1, d2, cl, cr, s->chi_max, be->kind, be->target_rank,
-                                                         be->oversampling, be->det_crossover);
-                    if (pl.randomized && be->accuracy_check)
+                    plans[i] = plan_decimation(d1, d2, cl, cr, s->chi_max, be->kind, be->target_rank,
+                                               be->oversampling, be->det_crossover);
+                    if (plans[i].randomized && be->accuracy_check)
                         throw_contract(c, "evolve: accuracy_check (fixed-precision RRSVD) is not implemented on the device yet");
-                    const uint64_t call_seed = be->seed++;
-                    cplx* M1 = ws_get<cplx>(c, (size_t)pl.m * pl.n);
-                    cplx* M2 = ws_get<cplx>(c, (size_t)pl.m * pl.n);
-                    check_cuda(c, cudaEventRecord(ev[0], c->stream), "event");
-                    build_theta_device(c, s->g[b], s->g[b + 1], ll, lm, lr, cl, d1, cm, d2, cr, M1);
-                    check_cuda(c, cudaEventRecord(ev[1], c->stream), "event");
-                    apply_gate_device(c, G, d1, d2, cl, cr, M1, M2);
-                    check_cuda(c, cudaEventRecord(ev[2], c->stream), "event");
+                    cplx* M1 = ws_get<cplx>(c, (size_t)plans[i].m * plans[i].n);
+                    M2[i] = ws_get<cplx>(c, (size_t)plans[i].m * plans[i].n);
+                    tj.push_back({s->g[b], s->g[b + 1], b > 0 ? s->lam[b - 1] : nullptr, s->lam[b],
+                                  b + 2 < n ? s->lam[b + 1] : nullptr, cl, d1, cm, d2, cr, M1});
+                    gj.push_back({staged[gates[sw * nb + b]], d1, d2, cl, cr, M1, M2[i]});
+                }
+                check_cuda(c, cudaEventRecord(ev[0], c->stream), "event");
+                build_theta_many(c, tj);
+                check_cuda(c, cudaEventRecord(ev[1], c->stream), "event");
+                apply_gate_many(c, gj);
+                check_cuda(c, cudaEventRecord(ev[2], c->stream), "event");
+                for (size_t i = 0; i < nbnd; ++i) {  // after Θ is enqueued: outputs may reallocate
+                    const int b = bonds[i];
+                    const DecimPlan& pl = plans[i];
                     ensure_gamma(s, b, (size_t)pl.m * pl.kmax);
                     ensure_gamma(s, b + 1, (size_t)pl.kmax * pl.n);
                     ensure_lambda(s, b, (size_t)pl.kmax);
-                    decimate_device(c, pl, M2, d1, cr, ll, lr, s->chi_max, s->tol, (int)be->power_iterations,
-                                    call_seed, omode, nullptr, renorm, s->g[b], s->lam[b], s->g[b + 1], sc_dev);
-                    check_cuda(c, cudaEventRecord(ev[3], c->stream), "event");
-                    check_cuda(c, cudaMemcpyAsync(sc_host, sc_dev, sizeof(DecimScalars), cudaMemcpyDeviceToHost, c->stream), "D2H");
-                    check_cuda(c, cudaStreamSynchronize(c->stream), "sync");
-                    if (c->gemm_timing) flush_gemm_timing(c);
-                    ws_reset(c);
-                    if (sc_host->nonfinite) throw_contract(c, "decimate: theta has non-finite entries");
-                    if (sc_host->total_sq == 0.0) throw_contract(c, "decimate: theta is identically zero");
-                    const int kept = sc_host->kept;
-                    s->dr[b] = kept;
-                    s->dl[b + 1] = kept;
-                    diag->kept_fraction *= 1.0 - sc_host->discarded;
-                    diag->max_bond_dim = std::max<uint64_t>(diag->max_bond_dim, (uint64_t)kept);
-                    if (records && diag->n_updates < max_records) {
-                        float t01 = 0, t12 = 0, t23 = 0;
-                        cudaEventElapsedTime(&t01, ev[0], ev[1]);
-                        cudaEventElapsedTime(&t12, ev[1], ev[2]);
-                        cudaEventElapsedTime(&t23, ev[2], ev[3]);
-                        records[diag->n_updates] = {step, (uint64_t)b, (uint64_t)kept, sc_host->discarded,
-                                                    1e3 * t01, 1e3 * t12, 1e3 * t23, pl.randomized ? 1 : 0};
-                    }
+                    dj.push_back({pl, M2[i], s->d[b], s->dr[b + 1], b > 0 ? s->lam[b - 1] : nullptr,
+                                  b + 2 < n ? s->lam[b + 1] : nullptr, s->chi_max, s->tol, (int)be->power_iterations,
+                                  be->seed++, omode, nullptr, renorm, s->g[b], s->lam[b], s->g[b + 1], sc_dev + i});
+                }
+                decimate_many(c, dj);
+                check_cuda(c, cudaEventRecord(ev[3], c->stream), "event");
+                check_cuda(c, cudaMemcpyAsync(sc_host, sc_dev, nbnd * sizeof(DecimScalars), cudaMemcpyDeviceToHost,
+                                              c->stream), "D2H");
+                check_cuda(c, cudaStreamSynchronize(c->stream), "sync");
+                if (c->gemm_timing) flush_gemm_timing(c);
+                ws_reset(c);
+                float t01 = 0, t12 = 0, t23 = 0;
+                cudaEventElapsedTime(&t01, ev[0], ev[1]);
+                cudaEventElapsedTime(&t12, ev[1], ev[2]);
+                cudaEventElapsedTime(&t23, ev[2], ev[3]);
+                for (size_t i = 0; i < nbnd; ++i) {
+                    const int b = bonds[i];
+                    const DecimScalars& h = sc_host[i];
+                    if (h.nonfinite) throw_contract(c, "decimate: theta has non-finite entries");
+                    if (h.total_sq == 0.0) throw_contract(c, "decimate: theta is identically zero");
+                    s->dr[b] = h.kept;
+                    s->dl[b + 1] = h.kept;
+                    diag->kept_fraction *= 1.0 - h.discarded;
+                    diag->max_bond_dim = std::max<uint64_t>(diag->max_bond_dim, (uint64_t)h.kept);
+                    if (records && diag->n_updates < max_records)  // batched: stage times shared evenly
+                        records[diag->n_updates] = {step, (uint64_t)b, (uint64_t)h.kept, h.discarded,
+                                                    1e3 * t01 / nbnd, 1e3 * t12 / nbnd, 1e3 * t23 / nbnd,
+                                                    plans[i].randomized ? 1 : 0};
                     diag->n_updates++;
                     if (1.0 - diag->kept_fraction > abort_thr) {  // tebd.cpp:317-321
                         diag->aborted = 1;

@@ -1,4 +1,4 @@
-// pipeline.cu — see pipeline.cuh.
+// pipeline.cu — batched orchestration of the decimation pipeline.  See pipeline.cuh.
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
@@ -8,69 +8,134 @@
 
 namespace rb {
 
+namespace {
+
+bool debug_enabled() {
+    static const bool d = std::getenv("RRSVD_B200_DEBUG") != nullptr;
+    return d;
+}
+
+long long gemm_tiles(const GemmSpec& s) {
+    return (long long)((s.m + 63) / 64) * ((s.n + 63) / 64) * s.batch;
+}
+
+}  // namespace
+
+// ================================================================================== GEMM
+
+void gemm_many(rrsvd_b200_ctx* c, GemmOp opA, const std::vector<GemmSpec>& specs) {
+    long long total = 0;
+    for (const GemmSpec& s : specs)
+        if (s.m > 0 && s.n > 0) total += gemm_tiles(s);
+    if (total == 0) return;
+    const long long target = 2 * kNumSMs;  // two CTAs per SM
+    for (size_t base = 0; base < specs.size(); base += kMaxGroup) {
+        GemmGroup g;
+        g.count = 0;
+        double flops = 0.0;
+        bool any_split = false;
+        for (size_t i = base; i < std::min(specs.size(), base + kMaxGroup); ++i) {
+            const GemmSpec& s = specs[i];
+            if (s.m <= 0 || s.n <= 0) continue;
+            GemmProblem& P = g.p[g.count++];
+            P = GemmProblem{};
+            P.m = s.m; P.n = s.n; P.k = s.k; P.batch = s.batch;
+            P.A = s.A; P.lda = s.lda; P.strideA = s.sA;
+            P.B = s.B; P.ldb = s.ldb; P.strideB = s.sB;
+            P.C = s.C; P.ldc = s.ldc; P.strideC = s.sC;
+            P.rs = s.sc.rs; P.rs_div = s.sc.rs_div; P.ks = s.sc.ks; P.cs = s.sc.cs; P.cs_mod = s.sc.cs_mod;
+            int split = 1;
+            if (total < target && s.k > 128) {
+                split = (int)std::min<long long>((target + total - 1) / total, (s.k + 63) / 64);
+                split = std::max(split, 1);
+            }
+            P.split = split;
+            if (split > 1) {
+                P.partial = ws_get<cplx>(c, (size_t)split * s.batch * s.m * s.n);
+                any_split = true;
+            }
+            flops += 8.0 * s.m * s.n * (double)s.k * s.batch;
+        }
+        if (g.count == 0) continue;
+        cudaEvent_t ea = nullptr, eb = nullptr;
+        if (c->gemm_timing) {
+            ea = pooled_event(c);
+            eb = pooled_event(c);
+            check_cuda(c, cudaEventRecord(ea, c->stream), "event record");
+        }
+        check_cuda(c, zgemm_grouped(g, opA, c->stream), "zgemm");
+        c->launches += any_split ? 2 : 1;
+        if (c->gemm_timing) {
+            check_cuda(c, cudaEventRecord(eb, c->stream), "event record");
+            c->pending.push_back({ea, eb, flops});
+        }
+    }
+}
+
 void gemm(rrsvd_b200_ctx* c, GemmOp opA, int m, int n, int k, const cplx* A, long long lda,
           const cplx* B, long long ldb, cplx* C, long long ldc, const Scale& sc, int batch,
           long long sA, long long sB, long long sC) {
-    if (m <= 0 || n <= 0) return;
-    GemmGroup g;
-    g.count = 1;
-    GemmProblem& P = g.p[0];
-    P = GemmProblem{};
-    P.m = m; P.n = n; P.k = k; P.batch = batch;
-    P.A = A; P.lda = lda; P.strideA = sA;
-    P.B = B; P.ldb = ldb; P.strideB = sB;
-    P.C = C; P.ldc = ldc; P.strideC = sC;
-    P.rs = sc.rs; P.rs_div = sc.rs_div; P.ks = sc.ks; P.cs = sc.cs; P.cs_mod = sc.cs_mod;
-    const long long tiles = (long long)((m + 63) / 64) * ((n + 63) / 64) * batch;
-    int split = 1;
-    const long long target = 2 * kNumSMs;
-    if (tiles < target && k > 128) {
-        split = (int)std::min<long long>((target + tiles - 1) / tiles, (k + 63) / 64);
-        split = std::max(split, 1);
+    GemmSpec s{m, n, k, A, lda, B, ldb, C, ldc, sc, batch, sA, sB, sC};
+    gemm_many(c, opA, {s});
+}
+
+// ================================================================================== orth
+
+void orth_many(rrsvd_b200_ctx* c, const std::vector<OrthSpec>& specs) {
+    if (specs.empty()) return;
+    struct Buf {
+        cplx *G, *T, *a, *b;
+    };
+    std::vector<Buf> bufs(specs.size());
+    for (size_t i = 0; i < specs.size(); ++i) {
+        const OrthSpec& s = specs[i];
+        if (s.l > kMaxCholL)
+            throw_contract(c, "orth: sketch width l = " + std::to_string(s.l) + " exceeds the supported " +
+                                  std::to_string(kMaxCholL));
+        if (s.m < s.l) throw_contract(c, "qr: requires rows >= cols");
+        bufs[i] = {ws_get<cplx>(c, (size_t)s.l * s.l), ws_get<cplx>(c, (size_t)s.l * s.l),
+                   ws_get<cplx>(c, (size_t)s.m * s.l), ws_get<cplx>(c, (size_t)s.m * s.l)};
     }
-    P.split = split;
-    if (split > 1) P.partial = ws_get<cplx>(c, (size_t)split * batch * m * n);
-    cudaEvent_t ea = nullptr, eb = nullptr;
-    if (c->gemm_timing) {
-        ea = pooled_event(c);
-        eb = pooled_event(c);
-        check_cuda(c, cudaEventRecord(ea, c->stream), "event record");
-    }
-    check_cuda(c, zgemm_grouped(g, opA, c->stream), "zgemm");
-    c->launches += split > 1 ? 2 : 1;
-    if (c->gemm_timing) {
-        check_cuda(c, cudaEventRecord(eb, c->stream), "event record");
-        c->pending.push_back({ea, eb, 8.0 * m * n * (double)k * batch});
+    std::vector<const cplx*> cur(specs.size());
+    for (size_t i = 0; i < specs.size(); ++i) cur[i] = specs[i].Y;
+    for (int pass = 0; pass < 3; ++pass) {
+        std::vector<GemmSpec> gram, apply;
+        for (size_t i = 0; i < specs.size(); ++i) {
+            const OrthSpec& s = specs[i];
+            gram.push_back({s.l, s.l, s.m, cur[i], s.l, cur[i], s.l, bufs[i].G, s.l});
+        }
+        gemm_many(c, kOpC, gram);
+        for (size_t base = 0; base < specs.size(); base += kMaxSmall) {
+            CholBatch cb{};
+            int max_l = 0;
+            for (size_t i = base; i < std::min(specs.size(), base + kMaxSmall); ++i) {
+                const int k = cb.count++;
+                cb.l[k] = specs[i].l;
+                cb.G[k] = bufs[i].G;
+                cb.T[k] = bufs[i].T;
+                cb.shift_scale[k] = pass == 0 ? 10.0 * (specs[i].m + specs[i].l) : 0.0;
+                cb.dep_tol[k] = pass == 0 ? 0.0 : kDepTol;
+                cb.ndead[k] = pass == 2 ? specs[i].ndead : nullptr;
+                max_l = std::max(max_l, specs[i].l);
+            }
+            check_cuda(c, chol_inv(cb, max_l, c->stream), "chol_inv");
+            c->launches++;
+        }
+        for (size_t i = 0; i < specs.size(); ++i) {
+            const OrthSpec& s = specs[i];
+            cplx* dst = pass == 2 ? s.Q : (pass == 0 ? bufs[i].a : bufs[i].b);
+            apply.push_back({s.m, s.l, s.l, cur[i], s.l, bufs[i].T, s.l, dst, s.l});
+            cur[i] = dst;
+        }
+        gemm_many(c, kOpN, apply);
     }
 }
 
 void orth(rrsvd_b200_ctx* c, const cplx* Y, int m, int l, cplx* Q, int* ndead) {
-    if (l > kMaxCholL)
-        throw_contract(c, "orth: sketch width l = " + std::to_string(l) + " exceeds the supported " +
-                              std::to_string(kMaxCholL));
-    if (m < l) throw_contract(c, "qr: requires rows >= cols");
-    cplx* G = ws_get<cplx>(c, (size_t)l * l);
-    cplx* T = ws_get<cplx>(c, (size_t)l * l);
-    cplx* bufA = ws_get<cplx>(c, (size_t)m * l);
-    cplx* bufB = ws_get<cplx>(c, (size_t)m * l);
-    const cplx* cur = Y;
-    for (int pass = 0; pass < 3; ++pass) {
-        gemm(c, kOpC, l, l, m, cur, l, cur, l, G, l);
-        CholBatch cb{};
-        cb.count = 1;
-        cb.l[0] = l;
-        cb.G[0] = G;
-        cb.T[0] = T;
-        cb.shift_scale[0] = pass == 0 ? 10.0 * (m + l) : 0.0;
-        cb.dep_tol[0] = pass == 0 ? 0.0 : kDepTol;
-        cb.ndead[0] = pass == 2 ? ndead : nullptr;
-        check_cuda(c, chol_inv(cb, l, c->stream), "chol_inv");
-        c->launches++;
-        cplx* dst = pass == 2 ? Q : (pass == 0 ? bufA : bufB);
-        gemm(c, kOpN, m, l, l, cur, l, T, l, dst, l);
-        cur = dst;
-    }
+    orth_many(c, {OrthSpec{Y, m, l, Q, ndead}});
 }
+
+// ================================================================================== sketch
 
 void make_omega(rrsvd_b200_ctx* c, int n, int l, uint64_t seed, int mode, cplx* out) {
     const long long entries = (long long)n * l;
@@ -87,68 +152,202 @@ void make_omega(rrsvd_b200_ctx* c, int n, int l, uint64_t seed, int mode, cplx* 
     }
 }
 
-static void small_svd(rrsvd_b200_ctx* c, const cplx* X, int r, int cc, int adj, int lda,
-                      double* sigma, cplx* Xn, cplx* Js) {
-    cplx* W = ws_get<cplx>(c, (size_t)(r + cc) * cc);
-    JacobiInitBatch ib{};
-    ib.count = 1;
-    ib.r[0] = r; ib.c[0] = cc; ib.A[0] = X; ib.lda[0] = lda; ib.adj[0] = adj; ib.W[0] = W;
-    check_cuda(c, jacobi_init(ib, c->stream), "jacobi_init");
-    JacobiBatch jb{};
-    jb.count = 1;
-    jb.r[0] = r; jb.c[0] = cc; jb.W[0] = W; jb.sweeps[0] = nullptr;
-    static const bool debug = std::getenv("RRSVD_B200_DEBUG") != nullptr;
-    int* dsweeps = nullptr;
-    if (debug) {
-        dsweeps = ws_get<int>(c, 1);
-        jb.sweeps[0] = dsweeps;
+// ================================================================================== small SVD
+
+namespace {
+
+struct SmallSvdSpec {
+    const cplx* X;
+    int r, cc, adj, lda;
+    double* sigma;
+    cplx* Xn;
+    cplx* Js;
+};
+
+void small_svd_many(rrsvd_b200_ctx* c, const std::vector<SmallSvdSpec>& specs) {
+    std::vector<cplx*> W(specs.size());
+    std::vector<int*> dsweeps(specs.size(), nullptr);
+    for (size_t i = 0; i < specs.size(); ++i) {
+        W[i] = ws_get<cplx>(c, (size_t)(specs[i].r + specs[i].cc) * specs[i].cc);
+        if (debug_enabled()) dsweeps[i] = ws_get<int>(c, 1);
     }
-    const cudaError_t e = jacobi_svd(jb, r, cc, c->stream);
-    if (e == cudaErrorInvalidValue)
-        throw_contract(c, "jacobi: matrix " + std::to_string(r) + "x" + std::to_string(cc) +
-                              " exceeds the on-chip Jacobi capacity");
-    check_cuda(c, e, "jacobi_svd");
-    if (debug) {
-        int h = -1;
-        cudaMemcpyAsync(&h, dsweeps, sizeof(int), cudaMemcpyDeviceToHost, c->stream);
-        cudaStreamSynchronize(c->stream);
-        std::fprintf(stderr, "[rrsvd_b200] jacobi %dx%d: %d sweeps\n", r, cc, h);
+    for (size_t base = 0; base < specs.size(); base += kMaxSmall) {
+        const size_t end = std::min(specs.size(), base + kMaxSmall);
+        JacobiInitBatch ib{};
+        JacobiBatch jb{};
+        JacobiFinBatch fb{};
+        int max_r = 0, max_c = 0;
+        for (size_t i = base; i < end; ++i) {
+            const SmallSvdSpec& s = specs[i];
+            const int k = ib.count++;
+            ib.r[k] = s.r; ib.c[k] = s.cc; ib.A[k] = s.X; ib.lda[k] = s.lda; ib.adj[k] = s.adj; ib.W[k] = W[i];
+            jb.count++;
+            jb.r[k] = s.r; jb.c[k] = s.cc; jb.W[k] = W[i]; jb.sweeps[k] = dsweeps[i];
+            fb.count++;
+            fb.r[k] = s.r; fb.c[k] = s.cc; fb.W[k] = W[i]; fb.sigma[k] = s.sigma; fb.Xn[k] = s.Xn; fb.Js[k] = s.Js;
+            max_r = std::max(max_r, s.r);
+            max_c = std::max(max_c, s.cc);
+        }
+        check_cuda(c, jacobi_init(ib, c->stream), "jacobi_init");
+        const cudaError_t e = jacobi_svd(jb, max_r, max_c, c->stream);
+        if (e == cudaErrorInvalidValue)
+            throw_contract(c, "jacobi: matrix " + std::to_string(max_r) + "x" + std::to_string(max_c) +
+                                  " exceeds the on-chip Jacobi capacity");
+        check_cuda(c, e, "jacobi_svd");
+        check_cuda(c, jacobi_finish(fb, max_c, c->stream), "jacobi_finish");
+        c->launches += 3;
     }
-    JacobiFinBatch fb{};
-    fb.count = 1;
-    fb.r[0] = r; fb.c[0] = cc; fb.W[0] = W; fb.sigma[0] = sigma; fb.Xn[0] = Xn; fb.Js[0] = Js;
-    check_cuda(c, jacobi_finish(fb, cc, c->stream), "jacobi_finish");
-    c->launches += 3;
+    if (debug_enabled()) {
+        for (size_t i = 0; i < specs.size(); ++i) {
+            int h = -1;
+            cudaMemcpyAsync(&h, dsweeps[i], sizeof(int), cudaMemcpyDeviceToHost, c->stream);
+            cudaStreamSynchronize(c->stream);
+            std::fprintf(stderr, "[rrsvd_b200] jacobi %dx%d: %d sweeps\n", specs[i].r, specs[i].cc, h);
+        }
+    }
+}
+
+}  // namespace
+
+// ================================================================================== RRSVD
+
+void rrsvd_core_many(rrsvd_b200_ctx* c, const std::vector<RrsvdSpec>& specs) {
+    if (specs.empty()) return;
+    struct Buf {
+        cplx *Y, *Q, *Z, *Qb, *X, *Xn, *Js;
+    };
+    std::vector<Buf> b(specs.size());
+    int max_q = 0;
+    for (size_t i = 0; i < specs.size(); ++i) {
+        const RrsvdSpec& s = specs[i];
+        b[i] = {ws_get<cplx>(c, (size_t)s.m * s.l), ws_get<cplx>(c, (size_t)s.m * s.l),
+                ws_get<cplx>(c, (size_t)s.n * s.l), ws_get<cplx>(c, (size_t)s.n * s.l),
+                ws_get<cplx>(c, (size_t)s.l * s.l), ws_get<cplx>(c, (size_t)s.l * s.l),
+                ws_get<cplx>(c, (size_t)s.l * s.l)};
+        max_q = std::max(max_q, s.q);
+    }
+    std::vector<GemmSpec> gs;
+    std::vector<OrthSpec> os;
+    // range finder, Algorithm 1 (randomized.cpp:88-99): Y = A Omega, QR
+    for (size_t i = 0; i < specs.size(); ++i) {
+        const RrsvdSpec& s = specs[i];
+        gs.push_back({s.m, s.l, s.n, s.A, s.n, s.omega, s.l, b[i].Y, s.l});
+        os.push_back({b[i].Y, s.m, s.l, b[i].Q});
+    }
+    gemm_many(c, kOpN, gs);
+    orth_many(c, os);
+    for (int j = 0; j < max_q; ++j) {
+        gs.clear(); os.clear();
+        for (size_t i = 0; i < specs.size(); ++i) {  // Z = A^H Q, QR
+            const RrsvdSpec& s = specs[i];
+            if (j >= s.q) continue;
+            gs.push_back({s.n, s.l, s.m, s.A, s.n, b[i].Q, s.l, b[i].Z, s.l});
+            os.push_back({b[i].Z, s.n, s.l, b[i].Qb});
+        }
+        gemm_many(c, kOpC, gs);
+        orth_many(c, os);
+        gs.clear(); os.clear();
+        for (size_t i = 0; i < specs.size(); ++i) {  // Y = A Q~, QR
+            const RrsvdSpec& s = specs[i];
+            if (j >= s.q) continue;
+            gs.push_back({s.m, s.l, s.n, s.A, s.n, b[i].Qb, s.l, b[i].Y, s.l});
+            os.push_back({b[i].Y, s.m, s.l, b[i].Q});
+        }
+        gemm_many(c, kOpN, gs);
+        orth_many(c, os);
+    }
+    // B = Q^H A held as B^H = A^H Q = Qb X  (assemble_from_basis, randomized.cpp:57-66)
+    gs.clear(); os.clear();
+    for (size_t i = 0; i < specs.size(); ++i) {
+        const RrsvdSpec& s = specs[i];
+        gs.push_back({s.n, s.l, s.m, s.A, s.n, b[i].Q, s.l, b[i].Z, s.l});
+        os.push_back({b[i].Z, s.n, s.l, b[i].Qb});
+    }
+    gemm_many(c, kOpC, gs);
+    orth_many(c, os);
+    gs.clear();
+    for (size_t i = 0; i < specs.size(); ++i) {  // X = Qb^H B^H  (l x l, ~upper triangular)
+        const RrsvdSpec& s = specs[i];
+        gs.push_back({s.l, s.l, s.n, b[i].Qb, s.l, b[i].Z, s.l, b[i].X, s.l});
+    }
+    gemm_many(c, kOpC, gs);
+    // B = X^H Qb^H.  One-sided Jacobi on X^H (the R^H of a QR converges in a few sweeps,
+    // Drmac-Veselic): X^H K = Z Sigma  =>  B = Z Sigma (Qb K)^H, so U_B = Z, V = Qb K.
+    std::vector<SmallSvdSpec> ss;
+    for (size_t i = 0; i < specs.size(); ++i) {
+        const RrsvdSpec& s = specs[i];
+        ss.push_back({b[i].X, s.l, s.l, 1, s.l, s.sigma, b[i].Xn, b[i].Js});
+    }
+    small_svd_many(c, ss);
+    gs.clear();
+    for (size_t i = 0; i < specs.size(); ++i) {
+        const RrsvdSpec& s = specs[i];
+        gs.push_back({s.m, s.l, s.l, b[i].Q, s.l, b[i].Xn, s.l, s.U, s.l});   // U = Q U_B
+        gs.push_back({s.n, s.l, s.l, b[i].Qb, s.l, b[i].Js, s.l, s.V, s.l});  // V = Qb K
+    }
+    gemm_many(c, kOpN, gs);
 }
 
 void rrsvd_core(rrsvd_b200_ctx* c, const cplx* A, int m, int n, int l, int q, const cplx* omega,
                 cplx* U, double* sigma, cplx* V) {
-    cplx* Y = ws_get<cplx>(c, (size_t)m * l);
-    cplx* Q = ws_get<cplx>(c, (size_t)m * l);
-    cplx* Z = ws_get<cplx>(c, (size_t)n * l);
-    cplx* Qb = ws_get<cplx>(c, (size_t)n * l);
-    cplx* X = ws_get<cplx>(c, (size_t)l * l);
-    cplx* Xn = ws_get<cplx>(c, (size_t)l * l);
-    cplx* Js = ws_get<cplx>(c, (size_t)l * l);
-    // range finder, Algorithm 1 (randomized.cpp:88-99)
-    gemm(c, kOpN, m, l, n, A, n, omega, l, Y, l);            // Y = A Omega
-    orth(c, Y, m, l, Q);
-    for (int j = 0; j < q; ++j) {
-        gemm(c, kOpC, n, l, m, A, n, Q, l, Z, l);            // Z = A^H Q
-        orth(c, Z, n, l, Qb);
-        gemm(c, kOpN, m, l, n, A, n, Qb, l, Y, l);           // Y = A Q~
-        orth(c, Y, m, l, Q);
-    }
-    // B = Q^H A, held as B^H = A^H Q = Qb X  (assemble_from_basis, randomized.cpp:57-66)
-    gemm(c, kOpC, n, l, m, A, n, Q, l, Z, l);
-    orth(c, Z, n, l, Qb);
-    gemm(c, kOpC, l, l, n, Qb, l, Z, l, X, l);               // X = Qb^H B^H  (l x l, ~upper)
-    // B = X^H Qb^H.  One-sided Jacobi on X^H (the R^H of a QR converges in a few sweeps,
-    // Drmac-Veselic): X^H K = Z Sigma  =>  B = Z Sigma (Qb K)^H, so U_B = Z, V = Qb K.
-    small_svd(c, X, l, l, 1, l, sigma, Xn, Js);
-    gemm(c, kOpN, m, l, l, Q, l, Xn, l, U, l);               // U = Q U_B
-    gemm(c, kOpN, n, l, l, Qb, l, Js, l, V, l);              // V = Qb K
+    rrsvd_core_many(c, {RrsvdSpec{A, m, n, l, q, omega, U, sigma, V}});
 }
+
+// ================================================================================== full SVD
+
+void svd_jacobi_many(rrsvd_b200_ctx* c, const std::vector<SvdSpec>& specs) {
+    if (specs.empty()) return;
+    std::vector<SmallSvdSpec> direct, pre;
+    struct Pre {
+        const cplx* X;
+        int r, cc;
+        bool tall;
+        cplx *Qr, *R, *K;
+        const SvdSpec* s;
+    };
+    std::vector<Pre> pres;
+    for (const SvdSpec& s : specs) {
+        const bool tall = s.m >= s.n;
+        const int r = tall ? s.m : s.n, cc = tall ? s.n : s.m;
+        if (cc > kMaxCholL) {
+            // Unpreconditioned one-sided Jacobi (converges, in more sweeps).
+            // tall: X = A, X J = U S -> U = Xn, V = J.   wide: X = A^H -> V = Xn, U = J.
+            direct.push_back({s.A, r, cc, tall ? 0 : 1, s.n, s.sigma, tall ? s.U : s.V, tall ? s.V : s.U});
+            continue;
+        }
+        const cplx* X = s.A;
+        if (!tall) {
+            cplx* Xt = ws_get<cplx>(c, (size_t)r * cc);
+            check_cuda(c, conj_transpose(s.A, s.m, s.n, Xt, c->stream), "conj_transpose");
+            c->launches++;
+            X = Xt;
+        }
+        pres.push_back({X, r, cc, tall, ws_get<cplx>(c, (size_t)r * cc), ws_get<cplx>(c, (size_t)cc * cc),
+                        ws_get<cplx>(c, (size_t)cc * cc), &s});
+    }
+    // QR-preconditioned Jacobi: X (r x cc) = A or A^H, X = Qr R, R^H K = Z S
+    //   =>  X = (Qr K) S Z^H : left vectors Qr K, right vectors Z.
+    std::vector<OrthSpec> os;
+    std::vector<GemmSpec> gs;
+    for (const Pre& p : pres) os.push_back({p.X, p.r, p.cc, p.Qr});
+    orth_many(c, os);
+    for (const Pre& p : pres) gs.push_back({p.cc, p.cc, p.r, p.Qr, p.cc, p.X, p.cc, p.R, p.cc});
+    gemm_many(c, kOpC, gs);
+    for (const Pre& p : pres)
+        pre.push_back({p.R, p.cc, p.cc, 1, p.cc, p.s->sigma, p.tall ? p.s->V : p.s->U, p.K});
+    std::vector<SmallSvdSpec> all = direct;
+    all.insert(all.end(), pre.begin(), pre.end());
+    small_svd_many(c, all);
+    gs.clear();
+    for (const Pre& p : pres) gs.push_back({p.r, p.cc, p.cc, p.Qr, p.cc, p.K, p.cc, p.tall ? p.s->U : p.s->V, p.cc});
+    gemm_many(c, kOpN, gs);
+}
+
+void svd_jacobi(rrsvd_b200_ctx* c, const cplx* A, int m, int n, cplx* U, double* sigma, cplx* V) {
+    svd_jacobi_many(c, {SvdSpec{A, m, n, U, sigma, V}});
+}
+
+// ================================================================================== TEBD trio
 
 DecimPlan plan_decimation(int d1, int d2, int cl, int cr, size_t chi_max, int kind, size_t target_rank,
                           size_t oversampling, size_t det_crossover) {
@@ -170,87 +369,79 @@ DecimPlan plan_decimation(int d1, int d2, int cl, int cr, size_t chi_max, int ki
     return p;
 }
 
-void build_theta_device(rrsvd_b200_ctx* c, const cplx* G1, const cplx* G2, const double* ll,
-                        const double* lm, const double* lr, int cl, int d1, int cm, int d2, int cr, cplx* M) {
-    const int m = cl * d1, n = d2 * cr;
-    Scale sc;
-    sc.rs = ll; sc.rs_div = d1; sc.ks = lm; sc.cs = lr; sc.cs_mod = cr;
-    gemm(c, kOpN, m, n, cm, G1, cm, G2, n, M, n, sc);
-}
-
-void apply_gate_device(rrsvd_b200_ctx* c, const cplx* G, int d1, int d2, int cl, int cr,
-                       const cplx* Min, cplx* Mout) {
-    const int dd = d1 * d2;
-    if (dd <= 16) {
-        check_cuda(c, gate_small(G, dd, cl, cr, Min, Mout, c->stream), "gate_small");
-        c->launches++;
-    } else {
-        gemm(c, kOpN, dd, cr, dd, G, dd, Min, cr, Mout, cr, {}, cl, 0, (long long)dd * cr,
-             (long long)dd * cr);
+void build_theta_many(rrsvd_b200_ctx* c, const std::vector<ThetaJob>& jobs) {
+    std::vector<GemmSpec> gs;
+    for (const ThetaJob& j : jobs) {
+        const int m = j.cl * j.d1, n = j.d2 * j.cr;
+        Scale sc;
+        sc.rs = j.ll; sc.rs_div = j.d1; sc.ks = j.lm; sc.cs = j.lr; sc.cs_mod = j.cr;
+        gs.push_back({m, n, j.cm, j.G1, j.cm, j.G2, n, j.M, n, sc});
     }
+    gemm_many(c, kOpN, gs);
 }
 
-void decimate_device(rrsvd_b200_ctx* c, const DecimPlan& pl, const cplx* M, int d1, int cr,
-                     const double* ll, const double* lr, size_t chi_max, double trunc_tol, int q,
-                     uint64_t call_seed, int omega_mode, const cplx* omega, int renormalize,
-                     cplx* gamma_l, double* lambda, cplx* gamma_r, DecimScalars* sc) {
-    const int m = pl.m, n = pl.n, ns = pl.ns;
-    double* part = ws_get<double>(c, 2 * kNumSMs);
-    int* bad = ws_get<int>(c, 2 * kNumSMs);
-    check_cuda(c, sumsq(M, (long long)m * n, part, bad, &sc->total_sq, &sc->nonfinite, c->stream), "sumsq");
-    c->launches += 2;
-    cplx* U = ws_get<cplx>(c, (size_t)m * ns);
-    cplx* V = ws_get<cplx>(c, (size_t)n * ns);
-    double* sig = ws_get<double>(c, ns);
-    if (pl.randomized) {
-        const cplx* om = omega;
-        if (om == nullptr) {
-            cplx* o = ws_get<cplx>(c, (size_t)n * pl.l);
-            make_omega(c, n, pl.l, call_seed, omega_mode, o);
-            om = o;
+void apply_gate_many(rrsvd_b200_ctx* c, const std::vector<GateJob>& jobs) {
+    std::vector<GemmSpec> gs;
+    for (const GateJob& j : jobs) {
+        const int dd = j.d1 * j.d2;
+        if (dd <= 16) {
+            check_cuda(c, gate_small(j.G, dd, j.cl, j.cr, j.Min, j.Mout, c->stream), "gate_small");
+            c->launches++;
+        } else {
+            gs.push_back({dd, j.cr, dd, j.G, dd, j.Min, j.cr, j.Mout, j.cr, {}, j.cl, 0, (long long)dd * j.cr,
+                          (long long)dd * j.cr});
         }
-        rrsvd_core(c, M, m, n, pl.l, q, om, U, sig, V);
-    } else {
-        svd_jacobi(c, M, m, n, U, sig, V);
     }
-    TruncArgs ta{};
-    ta.sigma = sig; ta.ns = ns; ta.total_sq = &sc->total_sq; ta.trunc_tol = trunc_tol;
-    ta.cap = (long long)chi_max; ta.renormalize = renormalize; ta.kept = &sc->kept;
-    ta.lambda = lambda; ta.discarded = &sc->discarded;
-    check_cuda(c, truncate(ta, c->stream), "truncate");
-    GammaArgs ga{};
-    ga.U = U; ga.ldu = ns; ga.V = V; ga.ldv = ns; ga.ll = ll; ga.lr = lr;
-    ga.m = m; ga.n = n; ga.d1 = d1; ga.cr = cr; ga.kept = &sc->kept;
-    ga.gamma_l = gamma_l; ga.gamma_r = gamma_r; ga.pinv = &sc->pinv;
-    check_cuda(c, gamma_reshape(ga, pl.kmax, c->stream), "gamma_reshape");
-    c->launches += 4;
+    gemm_many(c, kOpN, gs);
 }
 
-void svd_jacobi(rrsvd_b200_ctx* c, const cplx* A, int m, int n, cplx* U, double* sigma, cplx* V) {
-    const bool tall = m >= n;
-    const int r = tall ? m : n, cc = tall ? n : m;
-    if (cc > kMaxCholL) {
-        // Unpreconditioned one-sided Jacobi (converges, but in more sweeps).
-        // tall: X = A, X J = U S -> U = Xn, V = J.   wide: X = A^H -> V = Xn, U = J.
-        small_svd(c, A, r, cc, tall ? 0 : 1, n, sigma, tall ? U : V, tall ? V : U);
-        return;
+void decimate_many(rrsvd_b200_ctx* c, const std::vector<DecimJob>& jobs) {
+    struct Out {
+        cplx *U, *V;
+        double* sig;
+    };
+    std::vector<Out> outs(jobs.size());
+    std::vector<RrsvdSpec> rs;
+    std::vector<SvdSpec> ds;
+    for (size_t i = 0; i < jobs.size(); ++i) {
+        const DecimJob& j = jobs[i];
+        const DecimPlan& pl = j.pl;
+        double* part = ws_get<double>(c, 2 * kNumSMs);
+        int* bad = ws_get<int>(c, 2 * kNumSMs);
+        check_cuda(c, sumsq(j.M, (long long)pl.m * pl.n, part, bad, &j.sc->total_sq, &j.sc->nonfinite, c->stream),
+                   "sumsq");
+        c->launches += 2;
+        outs[i] = {ws_get<cplx>(c, (size_t)pl.m * pl.ns), ws_get<cplx>(c, (size_t)pl.n * pl.ns),
+                   ws_get<double>(c, pl.ns)};
+        if (pl.randomized) {
+            const cplx* om = j.omega;
+            if (om == nullptr) {
+                cplx* o = ws_get<cplx>(c, (size_t)pl.n * pl.l);
+                make_omega(c, pl.n, pl.l, j.seed, j.omega_mode, o);
+                om = o;
+            }
+            rs.push_back({j.M, pl.m, pl.n, pl.l, j.q, om, outs[i].U, outs[i].sig, outs[i].V});
+        } else {
+            ds.push_back({j.M, pl.m, pl.n, outs[i].U, outs[i].sig, outs[i].V});
+        }
     }
-    // QR-preconditioned Jacobi: X (r x cc) = A or A^H, X = Qr R, R^H K = Z S
-    //   =>  X = (Qr K) S Z^H : left vectors Qr K, right vectors Z.
-    const cplx* X = A;
-    if (!tall) {
-        cplx* Xt = ws_get<cplx>(c, (size_t)r * cc);
-        check_cuda(c, conj_transpose(A, m, n, Xt, c->stream), "conj_transpose");
-        c->launches++;
-        X = Xt;
+    rrsvd_core_many(c, rs);
+    svd_jacobi_many(c, ds);
+    for (size_t i = 0; i < jobs.size(); ++i) {
+        const DecimJob& j = jobs[i];
+        const DecimPlan& pl = j.pl;
+        TruncArgs ta{};
+        ta.sigma = outs[i].sig; ta.ns = pl.ns; ta.total_sq = &j.sc->total_sq; ta.trunc_tol = j.trunc_tol;
+        ta.cap = (long long)j.chi_max; ta.renormalize = j.renormalize; ta.kept = &j.sc->kept;
+        ta.lambda = j.lambda; ta.discarded = &j.sc->discarded;
+        check_cuda(c, truncate(ta, c->stream), "truncate");
+        GammaArgs ga{};
+        ga.U = outs[i].U; ga.ldu = pl.ns; ga.V = outs[i].V; ga.ldv = pl.ns; ga.ll = j.ll; ga.lr = j.lr;
+        ga.m = pl.m; ga.n = pl.n; ga.d1 = j.d1; ga.cr = j.cr; ga.kept = &j.sc->kept;
+        ga.gamma_l = j.gamma_l; ga.gamma_r = j.gamma_r; ga.pinv = &j.sc->pinv;
+        check_cuda(c, gamma_reshape(ga, pl.kmax, c->stream), "gamma_reshape");
+        c->launches += 4;
     }
-    cplx* Qr = ws_get<cplx>(c, (size_t)r * cc);
-    cplx* R = ws_get<cplx>(c, (size_t)cc * cc);
-    cplx* K = ws_get<cplx>(c, (size_t)cc * cc);
-    orth(c, X, r, cc, Qr);
-    gemm(c, kOpC, cc, cc, r, Qr, cc, X, cc, R, cc);
-    small_svd(c, R, cc, cc, 1, cc, sigma, tall ? V : U, K);
-    gemm(c, kOpN, r, cc, cc, Qr, cc, K, cc, tall ? U : V, cc);
 }
 
 }  // namespace rb

@@ -1,6 +1,11 @@
-// pipeline.cuh — device-side orchestration of the decimation pipeline (host C++, enqueues
-// kernels on the context stream).  Used by the C ABI (capi.cu) and the sweep engine.
+// pipeline.cuh — host orchestration of the decimation pipeline (enqueues kernels on the context
+// stream).  Every stage is BATCHED: a vector of independent problems (e.g. all same-parity bonds
+// of a TEBD sweep, which the reference processes one by one, tebd.cpp:291-306) goes through each
+// stage as a grouped launch, so the latency-bound small-matrix kernels (Cholesky, Jacobi) run
+// side by side on different SMs and the GEMM grids fill the 148 SMs.
 #pragma once
+#include <vector>
+
 #include "ctx.cuh"
 #include "smallla.cuh"
 #include "tebd_kernels.cuh"
@@ -16,13 +21,34 @@ struct Scale {
     int cs_mod = 1;
 };
 
-// C = op(A)·B (single problem, optional stride batch); split-K chosen automatically.
+struct GemmSpec {
+    int m, n, k;
+    const cplx* A;
+    long long lda;
+    const cplx* B;
+    long long ldb;
+    cplx* C;
+    long long ldc;
+    Scale sc{};
+    int batch = 1;
+    long long sA = 0, sB = 0, sC = 0;
+};
+
+// Grouped complex GEMMs sharing op(A); split-K chosen so the whole group fills the GPU.
+void gemm_many(rrsvd_b200_ctx* c, GemmOp opA, const std::vector<GemmSpec>& specs);
 void gemm(rrsvd_b200_ctx* c, GemmOp opA, int m, int n, int k, const cplx* A, long long lda,
           const cplx* B, long long ldb, cplx* C, long long ldc, const Scale& sc = {}, int batch = 1,
           long long sA = 0, long long sB = 0, long long sC = 0);
 
-// Q (m x l, ld l) = orthonormal basis of Y (m x l, ld l) by shifted CholeskyQR3.
-// Q may alias Y.  ndead (nullable, device int) = dependent columns in the last pass.
+// Q (m x l, ld l) = orthonormal basis of Y (m x l, ld l): shifted CholeskyQR3 (Fukaya et al.)
+// with dependent-column zeroing.  Q may alias Y.
+struct OrthSpec {
+    const cplx* Y;
+    int m, l;
+    cplx* Q;
+    int* ndead = nullptr;
+};
+void orth_many(rrsvd_b200_ctx* c, const std::vector<OrthSpec>& specs);
 void orth(rrsvd_b200_ctx* c, const cplx* Y, int m, int l, cplx* Q, int* ndead = nullptr);
 
 // Gaussian sketch into `out` (n x l).
@@ -30,13 +56,31 @@ void make_omega(rrsvd_b200_ctx* c, int n, int l, uint64_t seed, int mode, cplx* 
 
 // RRSVD core (randomized.cpp:88-107 without the weight): A (m x n) -> U (m x l), sigma (l,
 // non-increasing), V (n x l).  omega: n x l device sketch.
+struct RrsvdSpec {
+    const cplx* A;
+    int m, n, l, q;
+    const cplx* omega;
+    cplx* U;
+    double* sigma;
+    cplx* V;
+};
+void rrsvd_core_many(rrsvd_b200_ctx* c, const std::vector<RrsvdSpec>& specs);
 void rrsvd_core(rrsvd_b200_ctx* c, const cplx* A, int m, int n, int l, int q, const cplx* omega,
                 cplx* U, double* sigma, cplx* V);
 
-// Full SVD by one-sided Jacobi (linalg.cpp:67-88): U (m x r), sigma (r), V (n x r), r = min(m,n).
+// Full SVD by QR-preconditioned one-sided Jacobi (linalg.cpp:67-88):
+// U (m x r), sigma (r), V (n x r), r = min(m,n).
+struct SvdSpec {
+    const cplx* A;
+    int m, n;
+    cplx* U;
+    double* sigma;
+    cplx* V;
+};
+void svd_jacobi_many(rrsvd_b200_ctx* c, const std::vector<SvdSpec>& specs);
 void svd_jacobi(rrsvd_b200_ctx* c, const cplx* A, int m, int n, cplx* U, double* sigma, cplx* V);
 
-// Device scalars of one decimation, read back by the host at the end of an update.
+// Device scalars of one decimation, read back by the host at the end of an update/sweep.
 struct DecimScalars {
     int kept;
     int nonfinite;
@@ -56,18 +100,46 @@ struct DecimPlan {  // host-side decisions of decimate (tebd.cpp:144-186)
 DecimPlan plan_decimation(int d1, int d2, int cl, int cr, size_t chi_max, int kind, size_t target_rank,
                           size_t oversampling, size_t det_crossover);
 
-// The whole decimation of an unfolded M on the device: norm, factorization (RRSVD or Jacobi),
+// One decimation of an unfolded M (tebd.cpp:141-237): norm, factorization (RRSVD or Jacobi),
 // truncation, λ renormalisation, Γ reshape.  Writes gamma_l (m x kept), lambda (kept),
 // gamma_r (kept x n) packed with the device-side kept; scalars into *sc (device).
-void decimate_device(rrsvd_b200_ctx* c, const DecimPlan& pl, const cplx* M, int d1, int cr,
-                     const double* ll, const double* lr, size_t chi_max, double trunc_tol, int q,
-                     uint64_t call_seed, int omega_mode, const cplx* omega, int renormalize,
-                     cplx* gamma_l, double* lambda, cplx* gamma_r, DecimScalars* sc);
+struct DecimJob {
+    DecimPlan pl;
+    const cplx* M;
+    int d1, cr;
+    const double* ll;
+    const double* lr;
+    size_t chi_max;
+    double trunc_tol;
+    int q;
+    uint64_t seed;
+    int omega_mode;
+    const cplx* omega;  // nullable: generate from seed
+    int renormalize;
+    cplx* gamma_l;
+    double* lambda;
+    cplx* gamma_r;
+    DecimScalars* sc;
+};
+void decimate_many(rrsvd_b200_ctx* c, const std::vector<DecimJob>& jobs);
 
 // Θ = λΓλΓλ in the unfolded layout (tebd.cpp:76-124) and the gate (tebd.cpp:126-139).
-void build_theta_device(rrsvd_b200_ctx* c, const cplx* G1, const cplx* G2, const double* ll,
-                        const double* lm, const double* lr, int cl, int d1, int cm, int d2, int cr, cplx* M);
-void apply_gate_device(rrsvd_b200_ctx* c, const cplx* G, int d1, int d2, int cl, int cr,
-                       const cplx* Min, cplx* Mout);
+struct ThetaJob {
+    const cplx* G1;
+    const cplx* G2;
+    const double* ll;
+    const double* lm;
+    const double* lr;
+    int cl, d1, cm, d2, cr;
+    cplx* M;
+};
+void build_theta_many(rrsvd_b200_ctx* c, const std::vector<ThetaJob>& jobs);
+struct GateJob {
+    const cplx* G;
+    int d1, d2, cl, cr;
+    const cplx* Min;
+    cplx* Mout;
+};
+void apply_gate_many(rrsvd_b200_ctx* c, const std::vector<GateJob>& jobs);
 
 }  // namespace rb
