@@ -4,7 +4,7 @@
 
 namespace rb {
 
-constexpr int kMaxSmall = 32;  // problems per launch of the small-matrix kernels
+constexpr int kMaxSmall = 64;  // problems per launch of the small-matrix kernels
 
 // ---- Cholesky + triangular inverse (the "R^-1" of one CholeskyQR pass) -------------------
 // G (l x l, Hermitian, row-major) -> T = R^-1 (l x l upper, zeros below), G (+ s I) = R^H R.
