@@ -171,7 +171,12 @@ def run_ours(args, rank, world, local_rank):
     import ctypes as C
     fl, ms, calls = C.c_double(), C.c_double(), C.c_uint64()
     ctx.check(lib.rrsvd_b200_gemm_stats(ctx.h, C.byref(fl), C.byref(ms), C.byref(calls)))
+    sfl, sms = (C.c_double * 8)(), (C.c_double * 8)()
+    ctx.check(lib.rrsvd_b200_gemm_stage_stats(ctx.h, sfl, sms))
     ctx.check(lib.rrsvd_b200_set_gemm_timing(ctx.h, 0))
+    stage_names = ["theta", "gate", "rrsvd_A_products", "qr_gram", "qr_apply", "svd_assembly", "det_precond"]
+    stages = {nm: {"tflops": round(sfl[i] / (sms[i] * 1e-3) / 1e12, 2), "ms_per_step": round(sms[i] / args.steps, 2)}
+              for i, nm in enumerate(stage_names) if sms[i] > 0}
     dev_update_us = sum(u["t_theta_us"] + u["t_gate_us"] + u["t_svd_us"] for u in diag.updates)
     if dist:
         t = torch.tensor([elapsed], device="cuda")
@@ -224,7 +229,7 @@ def run_ours(args, rank, world, local_rank):
                                         " MEASURED_PEAKS.json has no FP64 entry",
                          "frac_of_40tf_nominal": round(achieved / 40.0, 4),
                          "gemm_time_share": round(ms.value / (1e3 * elapsed), 4),
-                         "gemm_launches": int(calls.value), "traffic": None},
+                         "gemm_launches": int(calls.value), "stages": stages, "traffic": None},
             "e2e": {"value": round(e2e, 6), "unit": "steps/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": int(d2h)},
             "gpu_launches": int(gpu_launches),

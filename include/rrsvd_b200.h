@@ -212,6 +212,9 @@ int rrsvd_b200_schmidt_entropy(rrsvd_b200_mps* mps, size_t bond, double* out);
  * device milliseconds and launch count. */
 int rrsvd_b200_set_gemm_timing(rrsvd_b200_ctx* ctx, int on);
 int rrsvd_b200_gemm_stats(rrsvd_b200_ctx* ctx, double* flops, double* ms, uint64_t* calls);
+/* The same split by stage (8 slots): 0 theta, 1 gate, 2 RRSVD A-products, 3 QR Gram,
+ * 4 QR apply, 5 small-SVD assembly, 6 deterministic-SVD preconditioning. */
+int rrsvd_b200_gemm_stage_stats(rrsvd_b200_ctx* ctx, double* flops8, double* ms8);
 /* Measured device peak: what = 0 FP64 DMMA (mma.sync f64), 1 FP64 DFMA; TFLOP/s. */
 int rrsvd_b200_probe_peak(rrsvd_b200_ctx* ctx, int what, double* tflops);
 

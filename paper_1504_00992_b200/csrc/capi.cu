@@ -380,6 +380,7 @@ int rrsvd_b200_set_gemm_timing(rrsvd_b200_ctx* c, int on) {
             c->gemm_ms = 0.0;
             c->gemm_flops = 0.0;
             c->gemm_calls = 0;
+            for (int i = 0; i < 8; ++i) c->tag_ms[i] = c->tag_flops[i] = 0.0;
         }
     });
 }
@@ -390,6 +391,16 @@ int rrsvd_b200_gemm_stats(rrsvd_b200_ctx* c, double* flops, double* ms, uint64_t
         if (flops) *flops = c->gemm_flops;
         if (ms) *ms = c->gemm_ms;
         if (calls) *calls = c->gemm_calls;
+    });
+}
+
+int rrsvd_b200_gemm_stage_stats(rrsvd_b200_ctx* c, double* flops8, double* ms8) {
+    return api(c, [&] {
+        flush_gemm_timing(c);
+        for (int i = 0; i < 8; ++i) {
+            if (flops8) flops8[i] = c->tag_flops[i];
+            if (ms8) ms8[i] = c->tag_ms[i];
+        }
     });
 }
 

@@ -101,6 +101,8 @@ void flush_gemm_timing(rrsvd_b200_ctx* c) {
         check_cuda(c, cudaEventElapsedTime(&ms, p.a, p.b), "event elapsed");
         c->gemm_ms += ms;
         c->gemm_flops += p.flops;
+        c->tag_ms[p.tag & 7] += ms;
+        c->tag_flops[p.tag & 7] += p.flops;
         c->gemm_calls++;
         c->event_pool.push_back(p.a);
         c->event_pool.push_back(p.b);

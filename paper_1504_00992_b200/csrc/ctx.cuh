@@ -25,7 +25,10 @@ struct rrsvd_b200_ctx {
     struct PendingGemm {
         cudaEvent_t a, b;
         double flops;
+        int tag;
     };
+    int gemm_tag = 0;              // category of the next zgemm launches (debug statistics)
+    double tag_ms[8] = {}, tag_flops[8] = {};
     bool gemm_timing = false;
     std::vector<PendingGemm> pending;
     std::vector<cudaEvent_t> event_pool;

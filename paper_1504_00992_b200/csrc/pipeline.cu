@@ -28,7 +28,9 @@ void gemm_many(rrsvd_b200_ctx* c, GemmOp opA, const std::vector<GemmSpec>& specs
     for (const GemmSpec& s : specs)
         if (s.m > 0 && s.n > 0) total += gemm_tiles(s);
     if (total == 0) return;
-    const long long target = 2 * kNumSMs;  // two CTAs per SM
+    // Split K when the group has too few tiles: aim for >= 4 waves of 2 CTAs/SM so the tail
+    // wave is a small fraction of the launch.
+    const long long target = 8 * kNumSMs;
     for (size_t base = 0; base < specs.size(); base += kMaxGroup) {
         GemmGroup g;
         g.count = 0;
@@ -44,6 +46,7 @@ void gemm_many(rrsvd_b200_ctx* c, GemmOp opA, const std::vector<GemmSpec>& specs
             P.B = s.B; P.ldb = s.ldb; P.strideB = s.sB;
             P.C = s.C; P.ldc = s.ldc; P.strideC = s.sC;
             P.rs = s.sc.rs; P.rs_div = s.sc.rs_div; P.ks = s.sc.ks; P.cs = s.sc.cs; P.cs_mod = s.sc.cs_mod;
+            P.structure = s.structure;
             int split = 1;
             if (total < target && s.k > 128) {
                 split = (int)std::min<long long>((target + total - 1) / total, (s.k + 63) / 64);
@@ -67,7 +70,7 @@ void gemm_many(rrsvd_b200_ctx* c, GemmOp opA, const std::vector<GemmSpec>& specs
         c->launches += any_split ? 2 : 1;
         if (c->gemm_timing) {
             check_cuda(c, cudaEventRecord(eb, c->stream), "event record");
-            c->pending.push_back({ea, eb, flops});
+            c->pending.push_back({ea, eb, flops, c->gemm_tag});
         }
     }
 }
@@ -102,8 +105,11 @@ void orth_many(rrsvd_b200_ctx* c, const std::vector<OrthSpec>& specs) {
         std::vector<GemmSpec> gram, apply;
         for (size_t i = 0; i < specs.size(); ++i) {
             const OrthSpec& s = specs[i];
-            gram.push_back({s.l, s.l, s.m, cur[i], s.l, cur[i], s.l, bufs[i].G, s.l});
+            GemmSpec gsp{s.l, s.l, s.m, cur[i], s.l, cur[i], s.l, bufs[i].G, s.l};
+            gsp.structure = kUpperC;  // chol_inv reads only the upper triangle of G
+            gram.push_back(gsp);
         }
+        c->gemm_tag = 3;
         gemm_many(c, kOpC, gram);
         for (size_t base = 0; base < specs.size(); base += kMaxSmall) {
             CholBatch cb{};
@@ -124,9 +130,12 @@ void orth_many(rrsvd_b200_ctx* c, const std::vector<OrthSpec>& specs) {
         for (size_t i = 0; i < specs.size(); ++i) {
             const OrthSpec& s = specs[i];
             cplx* dst = pass == 2 ? s.Q : (pass == 0 ? bufs[i].a : bufs[i].b);
-            apply.push_back({s.m, s.l, s.l, cur[i], s.l, bufs[i].T, s.l, dst, s.l});
+            GemmSpec asp{s.m, s.l, s.l, cur[i], s.l, bufs[i].T, s.l, dst, s.l};
+            asp.structure = kTriB;  // T = R^-1 is upper triangular
+            apply.push_back(asp);
             cur[i] = dst;
         }
+        c->gemm_tag = 4;
         gemm_many(c, kOpN, apply);
     }
 }
@@ -234,6 +243,7 @@ void rrsvd_core_many(rrsvd_b200_ctx* c, const std::vector<RrsvdSpec>& specs) {
         gs.push_back({s.m, s.l, s.n, s.A, s.n, s.omega, s.l, b[i].Y, s.l});
         os.push_back({b[i].Y, s.m, s.l, b[i].Q});
     }
+    c->gemm_tag = 2;
     gemm_many(c, kOpN, gs);
     orth_many(c, os);
     for (int j = 0; j < max_q; ++j) {
@@ -244,6 +254,7 @@ void rrsvd_core_many(rrsvd_b200_ctx* c, const std::vector<RrsvdSpec>& specs) {
             gs.push_back({s.n, s.l, s.m, s.A, s.n, b[i].Q, s.l, b[i].Z, s.l});
             os.push_back({b[i].Z, s.n, s.l, b[i].Qb});
         }
+        c->gemm_tag = 2;
         gemm_many(c, kOpC, gs);
         orth_many(c, os);
         gs.clear(); os.clear();
@@ -253,6 +264,7 @@ void rrsvd_core_many(rrsvd_b200_ctx* c, const std::vector<RrsvdSpec>& specs) {
             gs.push_back({s.m, s.l, s.n, s.A, s.n, b[i].Qb, s.l, b[i].Y, s.l});
             os.push_back({b[i].Y, s.m, s.l, b[i].Q});
         }
+        c->gemm_tag = 2;
         gemm_many(c, kOpN, gs);
         orth_many(c, os);
     }
@@ -263,6 +275,7 @@ void rrsvd_core_many(rrsvd_b200_ctx* c, const std::vector<RrsvdSpec>& specs) {
         gs.push_back({s.n, s.l, s.m, s.A, s.n, b[i].Q, s.l, b[i].Z, s.l});
         os.push_back({b[i].Z, s.n, s.l, b[i].Qb});
     }
+    c->gemm_tag = 2;
     gemm_many(c, kOpC, gs);
     orth_many(c, os);
     gs.clear();
@@ -270,6 +283,7 @@ void rrsvd_core_many(rrsvd_b200_ctx* c, const std::vector<RrsvdSpec>& specs) {
         const RrsvdSpec& s = specs[i];
         gs.push_back({s.l, s.l, s.n, b[i].Qb, s.l, b[i].Z, s.l, b[i].X, s.l});
     }
+    c->gemm_tag = 5;
     gemm_many(c, kOpC, gs);
     // B = X^H Qb^H.  One-sided Jacobi on X^H (the R^H of a QR converges in a few sweeps,
     // Drmac-Veselic): X^H K = Z Sigma  =>  B = Z Sigma (Qb K)^H, so U_B = Z, V = Qb K.
@@ -285,6 +299,7 @@ void rrsvd_core_many(rrsvd_b200_ctx* c, const std::vector<RrsvdSpec>& specs) {
         gs.push_back({s.m, s.l, s.l, b[i].Q, s.l, b[i].Xn, s.l, s.U, s.l});   // U = Q U_B
         gs.push_back({s.n, s.l, s.l, b[i].Qb, s.l, b[i].Js, s.l, s.V, s.l});  // V = Qb K
     }
+    c->gemm_tag = 5;
     gemm_many(c, kOpN, gs);
 }
 
@@ -332,6 +347,7 @@ void svd_jacobi_many(rrsvd_b200_ctx* c, const std::vector<SvdSpec>& specs) {
     for (const Pre& p : pres) os.push_back({p.X, p.r, p.cc, p.Qr});
     orth_many(c, os);
     for (const Pre& p : pres) gs.push_back({p.cc, p.cc, p.r, p.Qr, p.cc, p.X, p.cc, p.R, p.cc});
+    c->gemm_tag = 6;
     gemm_many(c, kOpC, gs);
     for (const Pre& p : pres)
         pre.push_back({p.R, p.cc, p.cc, 1, p.cc, p.s->sigma, p.tall ? p.s->V : p.s->U, p.K});
@@ -340,6 +356,7 @@ void svd_jacobi_many(rrsvd_b200_ctx* c, const std::vector<SvdSpec>& specs) {
     small_svd_many(c, all);
     gs.clear();
     for (const Pre& p : pres) gs.push_back({p.r, p.cc, p.cc, p.Qr, p.cc, p.K, p.cc, p.tall ? p.s->U : p.s->V, p.cc});
+    c->gemm_tag = 6;
     gemm_many(c, kOpN, gs);
 }
 
@@ -377,6 +394,7 @@ void build_theta_many(rrsvd_b200_ctx* c, const std::vector<ThetaJob>& jobs) {
         sc.rs = j.ll; sc.rs_div = j.d1; sc.ks = j.lm; sc.cs = j.lr; sc.cs_mod = j.cr;
         gs.push_back({m, n, j.cm, j.G1, j.cm, j.G2, n, j.M, n, sc});
     }
+    c->gemm_tag = 0;
     gemm_many(c, kOpN, gs);
 }
 
@@ -392,6 +410,7 @@ void apply_gate_many(rrsvd_b200_ctx* c, const std::vector<GateJob>& jobs) {
                           (long long)dd * j.cr});
         }
     }
+    c->gemm_tag = 1;
     gemm_many(c, kOpN, gs);
 }
 

@@ -32,6 +32,7 @@ struct GemmSpec {
     Scale sc{};
     int batch = 1;
     long long sA = 0, sB = 0, sC = 0;
+    int structure = kGeneral;  // kTriB / kUpperC hints (zgemm.cuh)
 };
 
 // Grouped complex GEMMs sharing op(A); split-K chosen so the whole group fills the GPU.

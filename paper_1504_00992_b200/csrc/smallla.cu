@@ -49,6 +49,7 @@ __global__ void __launch_bounds__(CHOL_THREADS) chol_inv_kernel(const __grid_con
     __syncthreads();
 
     // ---- right-looking Cholesky, G = R^H R, R upper, row j of R overwrites row j of G.
+    // Trailing update: warp w owns rows i ≡ w (mod nw), lanes sweep the row (coalesced).
     for (int j = 0; j < l; ++j) {
         const double d = P[poff(j, l)].x;
         const bool isdead = !(d > b.dep_tol[p] * g0[j]) || !(d > 0.0) || !(g0[j] > 0.0);
@@ -63,37 +64,52 @@ __global__ void __launch_bounds__(CHOL_THREADS) chol_inv_kernel(const __grid_con
         if (!isdead) {
             for (int i = j + 1 + warp; i < l; i += nw) {
                 const cplx ri = cconj(row[i]);
-                const int oi = poff(i, l);
+                cplx* Pi = P + poff(i, l) - i;  // Pi[k] = P[i][k]
+#pragma unroll 4
                 for (int k = i + lane; k < l; k += 32) {
-                    cplx v = P[oi + k - i];
-                    const cplx t = cmul(ri, row[k]);
-                    v.x -= t.x;
-                    v.y -= t.y;
-                    P[oi + k - i] = v;
+                    const cplx rk = row[k];
+                    cplx v = Pi[k];
+                    v.x -= ri.x * rk.x - ri.y * rk.y;
+                    v.y -= ri.x * rk.y + ri.y * rk.x;
+                    Pi[k] = v;
                 }
             }
         }
         __syncthreads();
     }
 
-    // ---- in-place triangular inverse, column by column (T[0:j, j] = -t_jj * T_11 * R[0:j, j])
-    for (int j = 0; j < l; ++j) {
-        if (dead[j]) {
-            for (int i = tid; i <= j; i += CHOL_THREADS) P[poff(i, l) + j - i] = mk(0.0, 0.0);
-            __syncthreads();
-            continue;
-        }
-        const double tjj = 1.0 / P[poff(j, l)].x;
-        for (int i = warp; i < j; i += nw) {
-            const int oi = poff(i, l);
-            cplx x = mk(0.0, 0.0);
-            for (int q = i + lane; q < j; q += 32) cfma(x, P[oi + q - i], P[poff(q, l) + j - q]);
-            x = warp_sum(x);
-            if (lane == 0) row[i] = x;
-        }
+    // ---- in-place triangular inverse T = R^-1, bottom-up by rows:
+    //   T[i][i] = 1/R[i][i],  T[i][k] = -T[i][i] * sum_{q=i+1..k} R[i][q] T[q][k]   (k > i)
+    // Row i of R is staged in `row`; rows > i already hold T.  Four threads per column k split
+    // the q-sum (two shuffle levels); consecutive columns read consecutive packed addresses.
+    // A dependent (dead) row gets T[i][:] = 0, which zeroes column i of T as well.
+    const int c4 = tid >> 2, s4 = tid & 3;
+    for (int i = l - 1; i >= 0; --i) {
+        const int oi = poff(i, l);
+        const bool dd = dead[i] != 0;
+        const double tii = dd ? 0.0 : 1.0 / P[oi].x;
+        for (int k = i + 1 + tid; k < l; k += CHOL_THREADS) row[k] = P[oi + k - i];
         __syncthreads();
-        for (int i = tid; i < j; i += CHOL_THREADS) P[poff(i, l) + j - i] = cscale(row[i], -tjj);
-        if (tid == 0) P[poff(j, l)] = mk(tjj, 0.0);
+        for (int k0 = i + 1; k0 < l; k0 += CHOL_THREADS / 4) {
+            const int k = k0 + c4;
+            cplx s = mk(0.0, 0.0), s2 = mk(0.0, 0.0);
+            if (k < l && !dd) {
+                int q = i + 1 + s4;
+                for (; q + 4 <= k; q += 8) {  // two independent accumulators
+                    cfma(s, row[q], P[poff(q, l) + k - q]);
+                    cfma(s2, row[q + 4], P[poff(q + 4, l) + k - q - 4]);
+                }
+                if (q <= k) cfma(s, row[q], P[poff(q, l) + k - q]);
+            }
+            s.x += s2.x;
+            s.y += s2.y;
+            s.x += __shfl_xor_sync(0xffffffffu, s.x, 1);
+            s.y += __shfl_xor_sync(0xffffffffu, s.y, 1);
+            s.x += __shfl_xor_sync(0xffffffffu, s.x, 2);
+            s.y += __shfl_xor_sync(0xffffffffu, s.y, 2);
+            if (k < l && s4 == 0) P[oi + k - i] = cscale(s, -tii);
+        }
+        if (tid == 0) P[oi] = mk(tii, 0.0);
         __syncthreads();
     }
 

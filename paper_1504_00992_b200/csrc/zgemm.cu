@@ -1,4 +1,6 @@
 // zgemm.cu — see zgemm.cuh for the contract.
+#include <algorithm>
+
 #include "zgemm.cuh"
 
 namespace rb {
@@ -23,11 +25,15 @@ struct Cfg {
     static constexpr int A_STAGE = (BM * LDA_N > BK * LDA_C) ? BM * LDA_N : BK * LDA_C;
     static constexpr int B_STAGE = BK * LDB;
     static constexpr int SMEM_BYTES = STAGES * (A_STAGE + B_STAGE) * (int)sizeof(cplx);
-    static_assert((BM * BK) % NTHREADS == 0 && (BK * BN) % NTHREADS == 0, "tile loads");
+    static_assert((BM * BK) % NTHREADS == 0, "A tile loads");
+    static constexpr int MIN_BLOCKS = NTHREADS <= 128 ? 2 : 1;
     static_assert(LDB % 8 == 2 && LDA_N % 8 == 4 && LDA_C % 8 == 2, "bank-conflict-free strides");
 };
 using Cfg64 = Cfg<64, 64, 32, 32>;
 using Cfg56 = Cfg<64, 56, 16, 56>;
+// Cfg80: 80x104 CTA tile (10 warps of 8x104) — exact for the d=20 gate blocks (400 x χ=100:
+// 5 x 1 tiles, 4% padding instead of 25% with 64x56).
+using Cfg80 = Cfg<80, 104, 8, 104>;
 
 __device__ __forceinline__ int find_problem(const GemmGroup& g, int tile) {
     int lo = 0, hi = g.count - 1;
@@ -39,7 +45,7 @@ __device__ __forceinline__ int find_problem(const GemmGroup& g, int tile) {
 }
 
 template <class CF, int OPA>
-__global__ void __launch_bounds__(CF::NTHREADS, 2)
+__global__ void __launch_bounds__(CF::NTHREADS, CF::MIN_BLOCKS)
 zgemm_dmma_kernel(const __grid_constant__ GemmGroup g) {
     constexpr int BM = CF::BM, BN = CF::BN, BK = CF::BK, STAGES = CF::STAGES;
     constexpr int WM = CF::WM, WN = CF::WN, WARPS_N = CF::WARPS_N, NTHREADS = CF::NTHREADS;
@@ -58,11 +64,14 @@ zgemm_dmma_kernel(const __grid_constant__ GemmGroup g) {
     const int bz = t % P.batch;   t /= P.batch;
     const int sk = t;  // split index
 
-    const int M = P.m, N = P.n, K = P.k;
-    const int kchunk = (((K + P.split - 1) / P.split) + BK - 1) / BK * BK;
+    const int M = P.m, N = P.n;
+    const int m0 = tm * BM, n0 = tn * BN;
+    if (P.structure == kUpperC && m0 >= n0 + BN) return;  // tile strictly below the diagonal
+    // kTriB: B upper triangular → columns [n0, n0+BN) only see k < n0 + BN
+    const int K = (P.structure == kTriB) ? min(P.k, n0 + BN) : P.k;
+    const int kchunk = (((P.k + P.split - 1) / P.split) + BK - 1) / BK * BK;
     const int kbeg = sk * kchunk;
     const int kend = min(K, kbeg + kchunk);
-    const int m0 = tm * BM, n0 = tn * BN;
 
     const cplx* __restrict__ A = P.A + (long long)bz * P.strideA;
     const cplx* __restrict__ B = P.B + (long long)bz * P.strideB;
@@ -97,8 +106,9 @@ zgemm_dmma_kernel(const __grid_constant__ GemmGroup g) {
             }
         }
 #pragma unroll
-        for (int i = 0; i < (BK * BN) / NTHREADS; ++i) {
+        for (int i = 0; i < (BK * BN + NTHREADS - 1) / NTHREADS; ++i) {
             const int idx = i * NTHREADS + tid;
+            if ((BK * BN) % NTHREADS != 0 && idx >= BK * BN) break;
             const int r = idx / BN, c = idx % BN;
             const int gk = k0 + r, gn = n0 + c;
             const bool ok = gk < kend && gn < N;
@@ -260,18 +270,21 @@ cudaError_t launch_cfg(GemmGroup& g, GemmOp opA, cudaStream_t s) {
 }
 
 cudaError_t zgemm_grouped(GemmGroup& g, GemmOp opA, cudaStream_t s) {
-    // Pick the CTA tile that wastes the least DMMA work on N padding for this group.
-    double pad64 = 0.0, pad56 = 0.0;
+    // Pick the CTA tile that wastes the least padded DMMA work (M and N quantisation) for this
+    // group; ties favour the larger warp tile of Cfg64.
+    double pad64 = 0.0, pad56 = 0.0, pad80 = 0.0;
     for (int i = 0; i < g.count; ++i) {
         GemmProblem& P = g.p[i];
         if (P.batch < 1) P.batch = 1;
         if (P.split < 1) P.split = 1;
         if (P.rs_div < 1) P.rs_div = 1;
         if (P.cs_mod < 1) P.cs_mod = 1;
-        const double w = (double)P.m * P.k * P.batch;
-        pad64 += w * ((P.n + 63) / 64 * 64);
-        pad56 += w * ((P.n + 55) / 56 * 56);
+        const double w = (double)P.k * P.batch;
+        pad64 += w * ((P.m + 63) / 64 * 64) * ((P.n + 63) / 64 * 64);
+        pad56 += w * ((P.m + 63) / 64 * 64) * ((P.n + 55) / 56 * 56);
+        pad80 += w * ((P.m + 79) / 80 * 80) * ((P.n + 103) / 104 * 104);
     }
+    if (pad80 < 0.92 * std::min(pad56, pad64)) return launch_cfg<Cfg80>(g, opA, s);
     if (pad56 < 0.95 * pad64) return launch_cfg<Cfg56>(g, opA, s);
     return launch_cfg<Cfg64>(g, opA, s);
 }

@@ -16,6 +16,7 @@
 namespace rb {
 
 enum GemmOp : int { kOpN = 0, kOpC = 1 };
+enum GemmStructure : int { kGeneral = 0, kTriB = 1, kUpperC = 2 };
 
 // One (possibly strided-batched) product  C[b] = diag(rs) · op(A[b]) · diag(ks) · B[b] · diag(cs)
 // with all three scalings optional; row scale index = row / rs_div, column scale index
@@ -35,6 +36,10 @@ struct GemmProblem {
     int rs_div, cs_mod;
     int split;         // split-K factor (1 = none)
     cplx* partial;     // split-K workspace: split * batch * m * n (only if split > 1)
+    // Structure hints: kTriB — B is upper triangular (k > col terms vanish: a column tile
+    // stops its K loop at its last column); kUpperC — only the upper-triangular part of C is
+    // needed (tiles entirely below the diagonal are skipped and left unwritten).
+    int structure;
     // filled by the launcher
     int tiles_m, tiles_n, tile_begin;
 };
