@@ -152,8 +152,8 @@ def run_ours(args, rank, world, local_rank):
     # ---- device-resident timed region
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     lib = P.lib()
+    import ctypes as C
     launches0 = ctx.launches
-    ctx.check(lib.rrsvd_b200_set_gemm_timing(ctx.h, 1))
     if dist:
         dist.barrier()
     ctx.synchronize()
@@ -168,16 +168,28 @@ def run_ours(args, rank, world, local_rank):
     elapsed = ev0.elapsed_time(ev1) / 1e3  # device time (CUDA events on the launching stream)
     wall = t1 - t0
     gpu_launches = ctx.launches - launches0
-    import ctypes as C
+    dev_update_us = sum(u["t_theta_us"] + u["t_gate_us"] + u["t_svd_us"] for u in diag.updates)
+
+    # ---- roofline pass: the same step with the two-lane overlap off, every zgemm launch
+    # event-timed on its stream (with overlap on, concurrent launches inflate each other's
+    # durations, so per-launch kernel efficiency is read from this serial pass).
+    ctx.check(lib.rrsvd_b200_set_overlap(ctx.h, 0))
+    ctx.check(lib.rrsvd_b200_set_gemm_timing(ctx.h, 1))
+    er0, er1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    er0.record(stream)
+    one_step()
+    er1.record(stream)
+    er1.synchronize()
+    serial_step_s = er0.elapsed_time(er1) / 1e3
     fl, ms, calls = C.c_double(), C.c_double(), C.c_uint64()
     ctx.check(lib.rrsvd_b200_gemm_stats(ctx.h, C.byref(fl), C.byref(ms), C.byref(calls)))
     sfl, sms = (C.c_double * 8)(), (C.c_double * 8)()
     ctx.check(lib.rrsvd_b200_gemm_stage_stats(ctx.h, sfl, sms))
     ctx.check(lib.rrsvd_b200_set_gemm_timing(ctx.h, 0))
+    ctx.check(lib.rrsvd_b200_set_overlap(ctx.h, 1))
     stage_names = ["theta", "gate", "rrsvd_A_products", "qr_gram", "qr_apply", "svd_assembly", "det_precond"]
-    stages = {nm: {"tflops": round(sfl[i] / (sms[i] * 1e-3) / 1e12, 2), "ms_per_step": round(sms[i] / args.steps, 2)}
+    stages = {nm: {"tflops": round(sfl[i] / (sms[i] * 1e-3) / 1e12, 2), "ms_per_step": round(sms[i], 2)}
               for i, nm in enumerate(stage_names) if sms[i] > 0}
-    dev_update_us = sum(u["t_theta_us"] + u["t_gate_us"] + u["t_svd_us"] for u in diag.updates)
     if dist:
         t = torch.tensor([elapsed], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -222,14 +234,18 @@ def run_ours(args, rank, world, local_rank):
                        "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
                        "l2": "inputs larger than L2 (MPS %.0f MB)" % (h2d / 1e6)},
             "decimations_per_s": round(world * ups * args.steps / elapsed, 3),
-            "roofline": {"bound": "tensor", "kernel": "zgemm_dmma (all zgemm-stage launches)",
+            "roofline": {"bound": "tensor",
+                         "kernel": "zgemm_dmma_kernel: every zgemm launch of one step (serial roofline pass,"
+                                   " CUDA events per launch on its stream)",
                          "achieved": round(achieved, 3), "peak": round(peak_dmma, 3), "unit": "TFLOP/s",
                          "frac": round(achieved / peak_dmma, 4) if peak_dmma else None,
                          "peak_source": "measured live: DMMA probe (mma.sync m8n8k4 f64) on this GPU;"
                                         " MEASURED_PEAKS.json has no FP64 entry",
                          "frac_of_40tf_nominal": round(achieved / 40.0, 4),
-                         "gemm_time_share": round(ms.value / (1e3 * elapsed), 4),
-                         "gemm_launches": int(calls.value), "stages": stages, "traffic": None},
+                         "gemm_time_share_serial": round(ms.value / (1e3 * serial_step_s), 4),
+                         "serial_step_ms": round(1e3 * serial_step_s, 3),
+                         "step_level_tflops": round(fl.value / (elapsed / args.steps) / 1e12, 3),
+                         "gemm_launches": int(calls.value), "stages": stages, **traffic_entry()},
             "e2e": {"value": round(e2e, 6), "unit": "steps/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": int(d2h)},
             "gpu_launches": int(gpu_launches),
@@ -243,6 +259,17 @@ def run_ours(args, rank, world, local_rank):
     if dist:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def traffic_entry():
+    """DRAM traffic of the dominant kernel from the committed ncu --set full capture (per
+    launch), with the launch's algorithmic bytes for comparison; null if absent."""
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    if not os.path.exists(path):
+        return {"traffic": None}
+    with open(path) as f:
+        t = json.load(f)
+    return {"traffic": t.get("dram_bytes_per_launch"), "traffic_note": t.get("note")}
 
 
 # ----------------------------------------------------------------------------- CPU reference

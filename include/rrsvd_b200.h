@@ -206,6 +206,10 @@ int rrsvd_b200_evolve(rrsvd_b200_mps* mps, size_t n_sweeps, const rrsvd_b200_swe
 int rrsvd_b200_expectation_local(rrsvd_b200_mps* mps, size_t site, const double* op, double* out2);
 int rrsvd_b200_schmidt_entropy(rrsvd_b200_mps* mps, size_t bond, double* out);
 
+/* evolve splits each sweep's bonds over two auxiliary streams so one half's latency-bound
+ * kernels overlap the other half's GEMMs (default on).  Off = one stream, serial stages. */
+int rrsvd_b200_set_overlap(rrsvd_b200_ctx* ctx, int on);
+
 /* ---- diagnostics ------------------------------------------------------------------------ */
 /* Event-time every zgemm launch (with its split-K reduction) on this context; on = 1 also
  * resets the counters.  Stats are cumulative algorithmic flops (8 m n k per complex GEMM),

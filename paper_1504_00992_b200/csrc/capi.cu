@@ -101,6 +101,8 @@ void rrsvd_b200_ctx_destroy(rrsvd_b200_ctx* c) {
     release_staged(c);
     cudaStreamSynchronize(c->stream);
     if (c->pinned) cudaFreeHost(c->pinned);
+    release_lanes(c);
+    for (cudaEvent_t e : c->event_pool) cudaEventDestroy(e);
     if (c->own_stream) cudaStreamDestroy(c->stream);
     delete c;
 }
@@ -371,6 +373,10 @@ int rrsvd_b200_decimate_unfolded(rrsvd_b200_ctx* c, const double* M, size_t d1, 
 }
 
 // ------------------------------------------------------------------------------------------ misc
+
+int rrsvd_b200_set_overlap(rrsvd_b200_ctx* c, int on) {
+    return api(c, [&] { c->use_lanes = on != 0; });
+}
 
 int rrsvd_b200_set_gemm_timing(rrsvd_b200_ctx* c, int on) {
     return api(c, [&] {

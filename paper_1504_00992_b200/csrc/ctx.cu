@@ -83,6 +83,36 @@ void release_staged(rrsvd_b200_ctx* c) {
     c->staged.clear();
 }
 
+void lanes_fork(rrsvd_b200_ctx* c) {
+    if (c->lane[0] == nullptr) {
+        for (int i = 0; i < 2; ++i) {
+            check_cuda(c, cudaStreamCreateWithFlags(&c->lane[i], cudaStreamNonBlocking), "lane stream");
+            check_cuda(c, cudaEventCreateWithFlags(&c->ev_join[i], cudaEventDisableTiming), "lane event");
+        }
+        check_cuda(c, cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming), "lane event");
+    }
+    check_cuda(c, cudaEventRecord(c->ev_fork, c->stream), "fork record");
+    for (int i = 0; i < 2; ++i) check_cuda(c, cudaStreamWaitEvent(c->lane[i], c->ev_fork, 0), "fork wait");
+}
+
+void lanes_join(rrsvd_b200_ctx* c) {
+    for (int i = 0; i < 2; ++i) {
+        check_cuda(c, cudaEventRecord(c->ev_join[i], c->lane[i]), "join record");
+        check_cuda(c, cudaStreamWaitEvent(c->stream, c->ev_join[i], 0), "join wait");
+    }
+}
+
+void release_lanes(rrsvd_b200_ctx* c) {
+    for (int i = 0; i < 2; ++i) {
+        if (c->lane[i]) cudaStreamDestroy(c->lane[i]);
+        if (c->ev_join[i]) cudaEventDestroy(c->ev_join[i]);
+        c->lane[i] = nullptr;
+        c->ev_join[i] = nullptr;
+    }
+    if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+    c->ev_fork = nullptr;
+}
+
 cudaEvent_t pooled_event(rrsvd_b200_ctx* c) {
     if (!c->event_pool.empty()) {
         cudaEvent_t e = c->event_pool.back();

@@ -32,6 +32,12 @@ struct rrsvd_b200_ctx {
     bool gemm_timing = false;
     std::vector<PendingGemm> pending;
     std::vector<cudaEvent_t> event_pool;
+
+    // Two auxiliary streams ("lanes") so independent halves of a sweep overlap: one lane's
+    // latency-bound small kernels (Cholesky, Jacobi) run beside the other lane's GEMMs.
+    cudaStream_t lane[2] = {nullptr, nullptr};
+    cudaEvent_t ev_fork = nullptr, ev_join[2] = {nullptr, nullptr};
+    bool use_lanes = true;
     double gemm_ms = 0.0, gemm_flops = 0.0;
     uint64_t gemm_calls = 0;
 };
@@ -77,6 +83,12 @@ struct OutBuf {
 void* stage_out(rrsvd_b200_ctx* c, void* p, size_t bytes, std::vector<OutBuf>& outs);
 void finish_out(rrsvd_b200_ctx* c, std::vector<OutBuf>& outs);  // D2H copies + sync
 void release_staged(rrsvd_b200_ctx* c);
+
+// Lanes: fork(c) makes both lanes wait for the work already queued on c->stream; join(c)
+// makes c->stream wait for both lanes.  release_lanes at context destruction.
+void lanes_fork(rrsvd_b200_ctx* c);
+void lanes_join(rrsvd_b200_ctx* c);
+void release_lanes(rrsvd_b200_ctx* c);
 
 // zgemm timing: events around each GEMM launch (incl. its split-K reduction) while enabled.
 cudaEvent_t pooled_event(rrsvd_b200_ctx* c);

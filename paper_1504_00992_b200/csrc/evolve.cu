@@ -60,9 +60,24 @@ void ensure_lambda(rrsvd_b200_mps* s, int bond, size_t elems) {
     s->lcap[bond] = elems;
 }
 
-struct HostScalars {
-    DecimScalars s;
-};
+// Growth without freeing: the old buffer may still be read by work being enqueued; the caller
+// frees `old` after the streams that read it have joined.
+void grow_gamma(rrsvd_b200_mps* s, int site, size_t elems, std::vector<void*>& old) {
+    if (s->gcap[site] >= elems) return;
+    if (s->g[site]) old.push_back(s->g[site]);
+    s->g[site] = nullptr;
+    check_cuda(s->c, cudaMallocAsync(reinterpret_cast<void**>(&s->g[site]), elems * sizeof(cplx), s->c->stream),
+               "alloc gamma");
+    s->gcap[site] = elems;
+}
+void grow_lambda(rrsvd_b200_mps* s, int bond, size_t elems, std::vector<void*>& old) {
+    if (s->lcap[bond] >= elems) return;
+    if (s->lam[bond]) old.push_back(s->lam[bond]);
+    s->lam[bond] = nullptr;
+    check_cuda(s->c, cudaMallocAsync(reinterpret_cast<void**>(&s->lam[bond]), elems * sizeof(double), s->c->stream),
+               "alloc lambda");
+    s->lcap[bond] = elems;
+}
 
 }  // namespace
 
@@ -242,40 +257,57 @@ int rrsvd_b200_evolve(rrsvd_b200_mps* s, size_t n_sweeps, const rrsvd_b200_sweep
                 }
                 auto* sc_host = static_cast<DecimScalars*>(pinned_scratch(c, nbnd * sizeof(DecimScalars)));
                 std::vector<DecimPlan> plans(nbnd);
-                std::vector<ThetaJob> tj;
-                std::vector<GateJob> gj;
-                std::vector<DecimJob> dj;
-                std::vector<cplx*> M2(nbnd);
+                std::vector<uint64_t> seeds(nbnd);
+                // Inputs of Θ are the CURRENT buffers; outputs that need more room get NEW
+                // buffers, and the old ones are freed only after both lanes have joined.
+                std::vector<cplx*> gin1(nbnd), gin2(nbnd);
+                std::vector<double*> lin(nbnd);
+                std::vector<void*> old_bufs;
                 for (size_t i = 0; i < nbnd; ++i) {
                     const int b = bonds[i];
-                    const int d1 = s->d[b], d2 = s->d[b + 1];
-                    const int cl = s->dl[b], cm = s->dr[b], cr = s->dr[b + 1];
-                    plans[i] = plan_decimation(d1, d2, cl, cr, s->chi_max, be->kind, be->target_rank,
-                                               be->oversampling, be->det_crossover);
+                    plans[i] = plan_decimation(s->d[b], s->d[b + 1], s->dl[b], s->dr[b + 1], s->chi_max, be->kind,
+                                               be->target_rank, be->oversampling, be->det_crossover);
                     if (plans[i].randomized && be->accuracy_check)
                         throw_contract(c, "evolve: accuracy_check (fixed-precision RRSVD) is not implemented on the device yet");
-                    cplx* M1 = ws_get<cplx>(c, (size_t)plans[i].m * plans[i].n);
-                    M2[i] = ws_get<cplx>(c, (size_t)plans[i].m * plans[i].n);
-                    tj.push_back({s->g[b], s->g[b + 1], b > 0 ? s->lam[b - 1] : nullptr, s->lam[b],
-                                  b + 2 < n ? s->lam[b + 1] : nullptr, cl, d1, cm, d2, cr, M1});
-                    gj.push_back({staged[gates[sw * nb + b]], d1, d2, cl, cr, M1, M2[i]});
+                    seeds[i] = be->seed++;  // ascending bond order, as the reference (tebd.cpp:162)
+                    gin1[i] = s->g[b];
+                    gin2[i] = s->g[b + 1];
+                    lin[i] = s->lam[b];
+                    grow_gamma(s, b, (size_t)plans[i].m * plans[i].kmax, old_bufs);
+                    grow_gamma(s, b + 1, (size_t)plans[i].kmax * plans[i].n, old_bufs);
+                    grow_lambda(s, b, (size_t)plans[i].kmax, old_bufs);
                 }
                 check_cuda(c, cudaEventRecord(ev[0], c->stream), "event");
-                build_theta_many(c, tj);
-                check_cuda(c, cudaEventRecord(ev[1], c->stream), "event");
-                apply_gate_many(c, gj);
-                check_cuda(c, cudaEventRecord(ev[2], c->stream), "event");
-                for (size_t i = 0; i < nbnd; ++i) {  // after Θ is enqueued: outputs may reallocate
-                    const int b = bonds[i];
-                    const DecimPlan& pl = plans[i];
-                    ensure_gamma(s, b, (size_t)pl.m * pl.kmax);
-                    ensure_gamma(s, b + 1, (size_t)pl.kmax * pl.n);
-                    ensure_lambda(s, b, (size_t)pl.kmax);
-                    dj.push_back({pl, M2[i], s->d[b], s->dr[b + 1], b > 0 ? s->lam[b - 1] : nullptr,
-                                  b + 2 < n ? s->lam[b + 1] : nullptr, s->chi_max, s->tol, (int)be->power_iterations,
-                                  be->seed++, omode, nullptr, renorm, s->g[b], s->lam[b], s->g[b + 1], sc_dev + i});
+                const cudaStream_t main_stream = c->stream;
+                const bool two_lanes = nbnd >= 2 && c->use_lanes;
+                if (two_lanes) lanes_fork(c);
+                for (int lane = 0; lane < (two_lanes ? 2 : 1); ++lane) {
+                    if (two_lanes) c->stream = c->lane[lane];
+                    std::vector<ThetaJob> tj;
+                    std::vector<GateJob> gj;
+                    std::vector<DecimJob> dj;
+                    for (size_t i = lane; i < nbnd; i += (two_lanes ? 2 : 1)) {
+                        const int b = bonds[i];
+                        const int d1 = s->d[b], d2 = s->d[b + 1];
+                        const int cl = s->dl[b], cm = s->dr[b], cr = s->dr[b + 1];
+                        cplx* M1 = ws_get<cplx>(c, (size_t)plans[i].m * plans[i].n);
+                        cplx* M2 = ws_get<cplx>(c, (size_t)plans[i].m * plans[i].n);
+                        const double* ll = b > 0 ? s->lam[b - 1] : nullptr;
+                        const double* lr = b + 2 < n ? s->lam[b + 1] : nullptr;
+                        tj.push_back({gin1[i], gin2[i], ll, lin[i], lr, cl, d1, cm, d2, cr, M1});
+                        gj.push_back({staged[gates[sw * nb + b]], d1, d2, cl, cr, M1, M2});
+                        dj.push_back({plans[i], M2, d1, cr, ll, lr, s->chi_max, s->tol, (int)be->power_iterations,
+                                      seeds[i], omode, nullptr, renorm, s->g[b], s->lam[b], s->g[b + 1], sc_dev + i});
+                    }
+                    build_theta_many(c, tj);
+                    if (lane == 0) check_cuda(c, cudaEventRecord(ev[1], c->stream), "event");
+                    apply_gate_many(c, gj);
+                    if (lane == 0) check_cuda(c, cudaEventRecord(ev[2], c->stream), "event");
+                    decimate_many(c, dj);
                 }
-                decimate_many(c, dj);
+                c->stream = main_stream;
+                if (two_lanes) lanes_join(c);
+                for (void* p : old_bufs) cudaFreeAsync(p, c->stream);
                 check_cuda(c, cudaEventRecord(ev[3], c->stream), "event");
                 check_cuda(c, cudaMemcpyAsync(sc_host, sc_dev, nbnd * sizeof(DecimScalars), cudaMemcpyDeviceToHost,
                                               c->stream), "D2H");
