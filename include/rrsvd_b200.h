@@ -190,6 +190,12 @@ void rrsvd_b200_mps_destroy(rrsvd_b200_mps* mps);
  * `site` (dim_right values).  dim_left must equal the right dimension of site-1. */
 int rrsvd_b200_mps_set_site(rrsvd_b200_mps* mps, size_t site, size_t dim_left, size_t dim_right,
                             const double* gamma, const double* lambda_right);
+/* Chain-block support for the multi-GPU partition: the weights of the bonds
+ * OUTSIDE this block — left of site 0 and right of the last site — i.e. the neighbouring
+ * blocks' λ.  NULL = open chain end (unit weights, tebd.cpp:82-87).  With edge weights set,
+ * the end sites may carry bond dimensions > 1. */
+int rrsvd_b200_mps_set_edge_lambdas(rrsvd_b200_mps* mps, const double* left, size_t n_left,
+                                    const double* right, size_t n_right);
 /* dims3 <- (left, phys, right); gamma / lambda_right copied out when non-NULL. */
 int rrsvd_b200_mps_get_site(rrsvd_b200_mps* mps, size_t site, size_t* dims3, double* gamma,
                             double* lambda_right);

@@ -20,6 +20,12 @@ struct rrsvd_b200_mps {
     std::vector<size_t> gcap;   // capacity in elements
     std::vector<double*> lam;   // λ per bond (device)
     std::vector<size_t> lcap;
+    // chain-block edges: λ of the bonds outside the block (null = open chain end)
+    double* edge[2] = {nullptr, nullptr};
+    size_t edge_n[2] = {0, 0};
+    size_t edge_cap[2] = {0, 0};
+    const double* ll_of(int b) const { return b > 0 ? lam[b - 1] : edge[0]; }
+    const double* lr_of(int b) const { return b + 2 < n ? lam[b + 1] : edge[1]; }
 };
 
 namespace {
@@ -134,6 +140,8 @@ void rrsvd_b200_mps_destroy(rrsvd_b200_mps* s) {
             if (p) cudaFreeAsync(p, s->c->stream);
         for (double* p : s->lam)
             if (p) cudaFreeAsync(p, s->c->stream);
+        for (double* p : s->edge)
+            if (p) cudaFreeAsync(p, s->c->stream);
         cudaStreamSynchronize(s->c->stream);
     }
     delete s;
@@ -144,8 +152,10 @@ int rrsvd_b200_mps_set_site(rrsvd_b200_mps* s, size_t site, size_t dim_left, siz
     return mps_api(s, [&](rrsvd_b200_ctx* c) {
         if (site >= (size_t)s->n) throw_contract(c, "mps_set_site: bad site");
         if (dim_left < 1 || dim_right < 1) throw_contract(c, "mps_set_site: bond dimensions must be >= 1");
-        if (site == 0 && dim_left != 1) throw_contract(c, "mps_set_site: open left end needs dim_left = 1");
-        if (site + 1 == (size_t)s->n && dim_right != 1) throw_contract(c, "mps_set_site: open right end needs dim_right = 1");
+        if (site == 0 && dim_left != 1 && s->edge[0] == nullptr)
+            throw_contract(c, "mps_set_site: open left end needs dim_left = 1 (or edge lambdas)");
+        if (site + 1 == (size_t)s->n && dim_right != 1 && s->edge[1] == nullptr)
+            throw_contract(c, "mps_set_site: open right end needs dim_right = 1 (or edge lambdas)");
         const size_t elems = dim_left * s->d[site] * dim_right;
         ensure_gamma(s, (int)site, elems);
         check_cuda(c, cudaMemcpyAsync(s->g[site], gamma, elems * sizeof(cplx), cudaMemcpyDefault, c->stream), "set gamma");
@@ -156,6 +166,32 @@ int rrsvd_b200_mps_set_site(rrsvd_b200_mps* s, size_t site, size_t dim_left, siz
         }
         s->dl[site] = (int)dim_left;
         s->dr[site] = (int)dim_right;
+        check_cuda(c, cudaStreamSynchronize(c->stream), "sync");
+    });
+}
+
+int rrsvd_b200_mps_set_edge_lambdas(rrsvd_b200_mps* s, const double* left, size_t n_left, const double* right,
+                                    size_t n_right) {
+    return mps_api(s, [&](rrsvd_b200_ctx* c) {
+        const double* src[2] = {left, right};
+        const size_t cnt[2] = {n_left, n_right};
+        for (int e = 0; e < 2; ++e) {
+            if (src[e] == nullptr) {
+                if (s->edge[e]) cudaFreeAsync(s->edge[e], c->stream);
+                s->edge[e] = nullptr;
+                s->edge_n[e] = s->edge_cap[e] = 0;
+                continue;
+            }
+            if (s->edge_cap[e] < cnt[e]) {
+                if (s->edge[e]) cudaFreeAsync(s->edge[e], c->stream);
+                check_cuda(c, cudaMallocAsync(reinterpret_cast<void**>(&s->edge[e]), std::max<size_t>(cnt[e], 1) * sizeof(double),
+                                              c->stream), "alloc edge");
+                s->edge_cap[e] = cnt[e];
+            }
+            s->edge_n[e] = cnt[e];
+            check_cuda(c, cudaMemcpyAsync(s->edge[e], src[e], cnt[e] * sizeof(double), cudaMemcpyDefault, c->stream),
+                       "set edge");
+        }
         check_cuda(c, cudaStreamSynchronize(c->stream), "sync");
     });
 }
@@ -292,8 +328,8 @@ int rrsvd_b200_evolve(rrsvd_b200_mps* s, size_t n_sweeps, const rrsvd_b200_sweep
                         const int cl = s->dl[b], cm = s->dr[b], cr = s->dr[b + 1];
                         cplx* M1 = ws_get<cplx>(c, (size_t)plans[i].m * plans[i].n);
                         cplx* M2 = ws_get<cplx>(c, (size_t)plans[i].m * plans[i].n);
-                        const double* ll = b > 0 ? s->lam[b - 1] : nullptr;
-                        const double* lr = b + 2 < n ? s->lam[b + 1] : nullptr;
+                        const double* ll = s->ll_of(b);
+                        const double* lr = s->lr_of(b);
                         tj.push_back({gin1[i], gin2[i], ll, lin[i], lr, cl, d1, cm, d2, cr, M1});
                         gj.push_back({staged[gates[sw * nb + b]], d1, d2, cl, cr, M1, M2});
                         dj.push_back({plans[i], M2, d1, cr, ll, lr, s->chi_max, s->tol, (int)be->power_iterations,
@@ -349,8 +385,8 @@ int rrsvd_b200_expectation_local(rrsvd_b200_mps* s, size_t site, const double* o
         if (op == nullptr || out2 == nullptr) throw_contract(c, "expectation_local: null argument");
         const int d = s->d[site];
         const auto* dop = static_cast<const cplx*>(stage_in(c, op, (size_t)d * d * sizeof(cplx)));
-        const double* ll = site > 0 ? s->lam[site - 1] : nullptr;
-        const double* lr = site + 1 < (size_t)s->n ? s->lam[site] : nullptr;
+        const double* ll = site > 0 ? s->lam[site - 1] : s->edge[0];
+        const double* lr = site + 1 < (size_t)s->n ? s->lam[site] : s->edge[1];
         double* res = ws_get<double>(c, 2 * kNumSMs * 2 + 2);
         check_cuda(c, expectation_local_dev(s->g[site], s->dl[site], d, s->dr[site], ll, lr, dop, res, c->stream),
                    "expectation_local");
