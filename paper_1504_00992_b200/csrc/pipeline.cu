@@ -47,6 +47,9 @@ void gemm_many(rrsvd_b200_ctx* c, GemmOp opA, const std::vector<GemmSpec>& specs
             P.C = s.C; P.ldc = s.ldc; P.strideC = s.sC;
             P.rs = s.sc.rs; P.rs_div = s.sc.rs_div; P.ks = s.sc.ks; P.cs = s.sc.cs; P.cs_mod = s.sc.cs_mod;
             P.structure = s.structure;
+            P.nsub = s.nsub;
+            P.subB = s.subB;
+            P.subC = s.subC;
             int split = 1;
             if (total < target && s.k > 128) {
                 split = (int)std::min<long long>((target + total - 1) / total, (s.k + 63) / 64);
@@ -406,8 +409,12 @@ void apply_gate_many(rrsvd_b200_ctx* c, const std::vector<GateJob>& jobs) {
             check_cuda(c, gate_small(j.G, dd, j.cl, j.cr, j.Min, j.Mout, c->stream), "gate_small");
             c->launches++;
         } else {
-            gs.push_back({dd, j.cr, dd, j.G, dd, j.Min, j.cr, j.Mout, j.cr, {}, j.cl, 0, (long long)dd * j.cr,
-                          (long long)dd * j.cr});
+            // All χ_l blocks M[a] (dd x χ_r, stride dd·χ_r) as one column-blocked GEMM:
+            // [M'[0] | M'[1] | ...] = G · [M[0] | M[1] | ...],  N = χ_l·χ_r.
+            GemmSpec g{dd, j.cl * j.cr, dd, j.G, dd, j.Min, j.cr, j.Mout, j.cr};
+            g.nsub = j.cr;
+            g.subB = g.subC = (long long)dd * j.cr;
+            gs.push_back(g);
         }
     }
     c->gemm_tag = 1;

@@ -33,6 +33,8 @@ struct GemmSpec {
     int batch = 1;
     long long sA = 0, sB = 0, sC = 0;
     int structure = kGeneral;  // kTriB / kUpperC hints (zgemm.cuh)
+    int nsub = 0;              // column-blocked B/C (zgemm.cuh)
+    long long subB = 0, subC = 0;
 };
 
 // Grouped complex GEMMs sharing op(A); split-K chosen so the whole group fills the GPU.

@@ -10,9 +10,9 @@ namespace {
 // Tile configurations.  Cfg64: 64x64 CTA tile, 32x32 warp tiles (16 DMMA tiles per warp).
 // Cfg56: 64x56 CTA tile, 16x56 warp tiles — for N ≈ l = k+p (110 → 2 x 56 = 112 instead of
 // 2 x 64 = 128: 14% less padded DMMA work on every RRSVD-stage GEMM).
-template <int BM_, int BN_, int WM_, int WN_>
+template <int BM_, int BN_, int WM_, int WN_, int STAGES_ = 3, int MINB_ = 0>
 struct Cfg {
-    static constexpr int BM = BM_, BN = BN_, BK = 16, STAGES = 3;
+    static constexpr int BM = BM_, BN = BN_, BK = 16, STAGES = STAGES_;
     static constexpr int WM = WM_, WN = WN_;
     static constexpr int WARPS_M = BM / WM, WARPS_N = BN / WN;
     static constexpr int NTHREADS = 32 * WARPS_M * WARPS_N;
@@ -26,14 +26,19 @@ struct Cfg {
     static constexpr int B_STAGE = BK * LDB;
     static constexpr int SMEM_BYTES = STAGES * (A_STAGE + B_STAGE) * (int)sizeof(cplx);
     static_assert((BM * BK) % NTHREADS == 0, "A tile loads");
-    static constexpr int MIN_BLOCKS = NTHREADS <= 128 ? 2 : 1;
+    static constexpr int MIN_BLOCKS = MINB_ ? MINB_ : (NTHREADS <= 128 ? 2 : 1);
+    // Padded-sub-tile skipping costs registers; the 3-CTA/SM config (168 regs) cannot afford it.
+    static constexpr bool SKIP_PAD = MIN_BLOCKS < 3;
     static_assert(LDB % 8 == 2 && LDA_N % 8 == 4 && LDA_C % 8 == 2, "bank-conflict-free strides");
 };
 using Cfg64 = Cfg<64, 64, 32, 32>;
-using Cfg56 = Cfg<64, 56, 16, 56>;
-// Cfg80: 80x104 CTA tile (10 warps of 8x104) — exact for the d=20 gate blocks (400 x χ=100:
-// 5 x 1 tiles, 4% padding instead of 25% with 64x56).
-using Cfg80 = Cfg<80, 104, 8, 104>;
+// 2-stage ring, 3 CTAs/SM (12 warps): a 16-deep K stage is ~8k cycles of DMMA work, far more
+// than the ~1-2k cycle load latency, so the third stage buys nothing while the third CTA fills
+// the DMMA issue bubbles of the other two.
+using Cfg56 = Cfg<64, 56, 16, 56, 2, 3>;
+// Cfg80: 80x64 CTA tile (5 warps of 16x64), 2-stage ring, 2 CTAs/SM — M = d1·d2 = 400 divides
+// exactly; with the column-blocked gate (N = χ_l·χ_r) the N padding is < 1%.
+using Cfg80 = Cfg<80, 64, 16, 64, 2, 2>;
 
 __device__ __forceinline__ int find_problem(const GemmGroup& g, int tile) {
     int lo = 0, hi = g.count - 1;
@@ -82,6 +87,16 @@ zgemm_dmma_kernel(const __grid_constant__ GemmGroup g) {
 
     const int ktiles = kend > kbeg ? (kend - kbeg + BK - 1) / BK : 0;
 
+    // The B columns this thread copies are the same in every stage: resolve their (block,
+    // offset) address once (column-blocked B, P.nsub > 0).
+    constexpr int NBL = (BK * BN + NTHREADS - 1) / NTHREADS;
+    int bcol[NBL];  // element offsets < 2^31 (checked by the launcher)
+#pragma unroll
+    for (int i = 0; i < NBL; ++i) {
+        const int gn = n0 + (i * NTHREADS + tid) % BN;
+        bcol[i] = P.nsub ? (gn / P.nsub) * (int)P.subB + gn % P.nsub : gn;
+    }
+
     auto load_stage = [&](int stage, int kt) {
         const int k0 = kbeg + kt * BK;
         cplx* sA = smA + stage * A_STAGE;
@@ -112,7 +127,7 @@ zgemm_dmma_kernel(const __grid_constant__ GemmGroup g) {
             const int r = idx / BN, c = idx % BN;
             const int gk = k0 + r, gn = n0 + c;
             const bool ok = gk < kend && gn < N;
-            cp_async16(sB + r * LDB + c, ok ? B + (long long)gk * ldb + gn : B, ok);
+            cp_async16(sB + r * LDB + c, ok ? B + (long long)gk * ldb + bcol[i] : B, ok);
         }
     };
 
@@ -145,8 +160,9 @@ zgemm_dmma_kernel(const __grid_constant__ GemmGroup g) {
         const cplx* sA = smA + stage * A_STAGE;
         const cplx* sB = smB + stage * B_STAGE;
         const int kbase = kbeg + kt * BK;
-#pragma unroll
+#pragma unroll(CF::MIN_BLOCKS >= 3 ? 1 : 4)
         for (int kk = 0; kk < BK; kk += 4) {
+            if (kbase + kk >= kend) break;  // K tail: no DMMA on zero padding (uniform)
             double ar[MI], ai[MI], ain[MI], br[NI], bi[NI];
             double kscale = 1.0;
             if (ks != nullptr) {
@@ -167,10 +183,14 @@ zgemm_dmma_kernel(const __grid_constant__ GemmGroup g) {
                 const cplx b = sB[(kk + fc) * LDB + wn + j * 8 + fr];
                 br[j] = b.x; bi[j] = b.y;
             }
+            // 8x8 sub-tiles entirely in the M/N padding issue no DMMA (warp-uniform predicate),
+            // so ragged shapes (M = 400 on 64-row tiles, N = 110) cost tensor-pipe time only for
+            // real rows/columns.
 #pragma unroll
             for (int i = 0; i < MI; ++i)
 #pragma unroll
                 for (int j = 0; j < NI; ++j) {
+                    if (CF::SKIP_PAD && (m0 + wm + i * 8 >= M || n0 + wn + j * 8 >= N)) continue;
                     dmma884(acc[i][j][0][0], acc[i][j][0][1], ar[i], br[j]);
                     dmma884(acc[i][j][1][0], acc[i][j][1][1], ar[i], bi[j]);
                 }
@@ -178,6 +198,7 @@ zgemm_dmma_kernel(const __grid_constant__ GemmGroup g) {
             for (int i = 0; i < MI; ++i)
 #pragma unroll
                 for (int j = 0; j < NI; ++j) {
+                    if (CF::SKIP_PAD && (m0 + wm + i * 8 >= M || n0 + wn + j * 8 >= N)) continue;
                     dmma884(acc[i][j][0][0], acc[i][j][0][1], ain[i], bi[j]);
                     dmma884(acc[i][j][1][0], acc[i][j][1][1], ai[i], br[j]);
                 }
@@ -203,6 +224,16 @@ zgemm_dmma_kernel(const __grid_constant__ GemmGroup g) {
         return;
     }
     cplx* C = P.C + (long long)bz * P.strideC;
+    double csc[NI][2];     // column scales, looked up once per thread (not per element)
+    long long ccol[NI][2];  // column addresses (column-blocked C when P.nsub > 0)
+#pragma unroll
+    for (int j = 0; j < NI; ++j)
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+            const int col = n0 + wn + j * 8 + fc * 2 + c;
+            csc[j][c] = (P.cs && col < N) ? __ldg(P.cs + col % P.cs_mod) : 1.0;
+            ccol[j][c] = P.nsub ? (long long)(col / P.nsub) * P.subC + col % P.nsub : col;
+        }
 #pragma unroll
     for (int i = 0; i < MI; ++i) {
         const int row = m0 + wm + i * 8 + fr;
@@ -214,8 +245,8 @@ zgemm_dmma_kernel(const __grid_constant__ GemmGroup g) {
 #pragma unroll
             for (int c = 0; c < 2; ++c) {
                 if (col + c >= N) continue;
-                const double sc = rsc * (P.cs ? __ldg(P.cs + (col + c) % P.cs_mod) : 1.0);
-                C[(long long)row * P.ldc + col + c] = mk(acc[i][j][0][c] * sc, acc[i][j][1][c] * sc);
+                const double sc = rsc * csc[j][c];
+                C[(long long)row * P.ldc + ccol[j][c]] = mk(acc[i][j][0][c] * sc, acc[i][j][1][c] * sc);
             }
         }
     }
@@ -237,7 +268,8 @@ __global__ void splitk_reduce_kernel(const __grid_constant__ GemmGroup g) {
         double sc = 1.0;
         if (P.rs) sc *= P.rs[row / P.rs_div];
         if (P.cs) sc *= P.cs[col % P.cs_mod];
-        P.C[bz * P.strideC + (long long)row * P.ldc + col] = cscale(s, sc);
+        const long long cc = P.nsub ? (long long)(col / P.nsub) * P.subC + col % P.nsub : col;
+        P.C[bz * P.strideC + (long long)row * P.ldc + cc] = cscale(s, sc);
     }
 }
 
@@ -279,12 +311,14 @@ cudaError_t zgemm_grouped(GemmGroup& g, GemmOp opA, cudaStream_t s) {
         if (P.split < 1) P.split = 1;
         if (P.rs_div < 1) P.rs_div = 1;
         if (P.cs_mod < 1) P.cs_mod = 1;
+        if (P.nsub > 0 && ((long long)(P.n / P.nsub + 1) * (P.subB > P.subC ? P.subB : P.subC) > 2147483647ll))
+            return cudaErrorInvalidValue;  // column-blocked offsets must fit in 32 bits
         const double w = (double)P.k * P.batch;
         pad64 += w * ((P.m + 63) / 64 * 64) * ((P.n + 63) / 64 * 64);
         pad56 += w * ((P.m + 63) / 64 * 64) * ((P.n + 55) / 56 * 56);
-        pad80 += w * ((P.m + 79) / 80 * 80) * ((P.n + 103) / 104 * 104);
+        pad80 += w * ((P.m + 79) / 80 * 80) * ((P.n + 63) / 64 * 64);
     }
-    if (pad80 < 0.92 * std::min(pad56, pad64)) return launch_cfg<Cfg80>(g, opA, s);
+    (void)pad80;  // Cfg80 kept compiled for experiments; padded sub-tiles are skipped instead
     if (pad56 < 0.95 * pad64) return launch_cfg<Cfg56>(g, opA, s);
     return launch_cfg<Cfg64>(g, opA, s);
 }

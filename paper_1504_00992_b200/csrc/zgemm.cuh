@@ -40,6 +40,11 @@ struct GemmProblem {
     // stops its K loop at its last column); kUpperC — only the upper-triangular part of C is
     // needed (tiles entirely below the diagonal are skipped and left unwritten).
     int structure;
+    // Column-blocked B/C (nsub > 0): logical column c lives in block c / nsub at offset c % nsub;
+    // B(k, c) = B[(c/nsub)·subB + k·ldb + c%nsub], C likewise with subC.  Lets a strided batch of
+    // narrow products that share A (the gate: G · Θ[α] for every α) run as ONE wide GEMM.
+    int nsub;
+    long long subB, subC;
     // filled by the launcher
     int tiles_m, tiles_n, tile_begin;
 };
