@@ -390,12 +390,23 @@ DecimPlan plan_decimation(int d1, int d2, int cl, int cr, size_t chi_max, int ki
 }
 
 void build_theta_many(rrsvd_b200_ctx* c, const std::vector<ThetaJob>& jobs) {
+    // λ_m is folded into Γ2's rows by a bandwidth-bound pre-pass (Γ2 is cm x d2·cr, 3 MB at
+    // config 3), so the DMMA GEMM carries only epilogue scalings (λ_l rows, λ_r columns).
     std::vector<GemmSpec> gs;
-    for (const ThetaJob& j : jobs) {
-        const int m = j.cl * j.d1, n = j.d2 * j.cr;
-        Scale sc;
-        sc.rs = j.ll; sc.rs_div = j.d1; sc.ks = j.lm; sc.cs = j.lr; sc.cs_mod = j.cr;
-        gs.push_back({m, n, j.cm, j.G1, j.cm, j.G2, n, j.M, n, sc});
+    for (size_t base = 0; base < jobs.size(); base += kMaxEpi) {
+        ScaleRowsBatch sb{};
+        for (size_t i = base; i < std::min(jobs.size(), base + kMaxEpi); ++i) {
+            const ThetaJob& j = jobs[i];
+            const int n = j.d2 * j.cr;
+            cplx* g2s = ws_get<cplx>(c, (size_t)j.cm * n);
+            const int k = sb.count++;
+            sb.in[k] = j.G2; sb.s[k] = j.lm; sb.rows[k] = j.cm; sb.cols[k] = n; sb.out[k] = g2s;
+            Scale sc;
+            sc.rs = j.ll; sc.rs_div = j.d1; sc.cs = j.lr; sc.cs_mod = j.cr;
+            gs.push_back({j.cl * j.d1, n, j.cm, j.G1, j.cm, g2s, n, j.M, n, sc});
+        }
+        check_cuda(c, scale_rows_many(sb, c->stream), "scale_rows");
+        c->launches++;
     }
     c->gemm_tag = 0;
     gemm_many(c, kOpN, gs);
@@ -429,21 +440,43 @@ void decimate_many(rrsvd_b200_ctx* c, const std::vector<DecimJob>& jobs) {
     std::vector<Out> outs(jobs.size());
     std::vector<RrsvdSpec> rs;
     std::vector<SvdSpec> ds;
+    // ‖Θ‖² + finite check for every bond: one launch pair per 64 bonds (tebd.cpp:156-160)
+    for (size_t base = 0; base < jobs.size(); base += kMaxSmall) {
+        SumsqBatch sb{};
+        for (size_t i = base; i < std::min(jobs.size(), base + kMaxSmall); ++i) {
+            const int k = sb.count++;
+            sb.a[k] = jobs[i].M;
+            sb.n[k] = (long long)jobs[i].pl.m * jobs[i].pl.n;
+            sb.out_sq[k] = &jobs[i].sc->total_sq;
+            sb.out_bad[k] = &jobs[i].sc->nonfinite;
+        }
+        double* part = ws_get<double>(c, (size_t)sb.count * 2 * kNumSMs);
+        int* bad = ws_get<int>(c, (size_t)sb.count * 2 * kNumSMs);
+        check_cuda(c, sumsq_many(sb, part, bad, c->stream), "sumsq_many");
+        c->launches += 2;
+    }
+    PhiloxBatch pb{};
+    auto flush_philox = [&] {
+        check_cuda(c, omega_philox_many(pb, c->stream), "philox_many");
+        if (pb.count) c->launches++;
+        pb.count = 0;
+    };
     for (size_t i = 0; i < jobs.size(); ++i) {
         const DecimJob& j = jobs[i];
         const DecimPlan& pl = j.pl;
-        double* part = ws_get<double>(c, 2 * kNumSMs);
-        int* bad = ws_get<int>(c, 2 * kNumSMs);
-        check_cuda(c, sumsq(j.M, (long long)pl.m * pl.n, part, bad, &j.sc->total_sq, &j.sc->nonfinite, c->stream),
-                   "sumsq");
-        c->launches += 2;
         outs[i] = {ws_get<cplx>(c, (size_t)pl.m * pl.ns), ws_get<cplx>(c, (size_t)pl.n * pl.ns),
                    ws_get<double>(c, pl.ns)};
         if (pl.randomized) {
             const cplx* om = j.omega;
             if (om == nullptr) {
                 cplx* o = ws_get<cplx>(c, (size_t)pl.n * pl.l);
-                make_omega(c, pl.n, pl.l, j.seed, j.omega_mode, o);
+                if (j.omega_mode == 1) {  // RRSVD_B200_OMEGA_PHILOX: batched over bonds
+                    const int k = pb.count++;
+                    pb.seed[k] = j.seed; pb.n[k] = (long long)pl.n * pl.l; pb.out[k] = o;
+                    if (pb.count == kMaxEpi) flush_philox();
+                } else {
+                    make_omega(c, pl.n, pl.l, j.seed, j.omega_mode, o);
+                }
                 om = o;
             }
             rs.push_back({j.M, pl.m, pl.n, pl.l, j.q, om, outs[i].U, outs[i].sig, outs[i].V});
@@ -451,21 +484,33 @@ void decimate_many(rrsvd_b200_ctx* c, const std::vector<DecimJob>& jobs) {
             ds.push_back({j.M, pl.m, pl.n, outs[i].U, outs[i].sig, outs[i].V});
         }
     }
+    flush_philox();
     rrsvd_core_many(c, rs);
     svd_jacobi_many(c, ds);
-    for (size_t i = 0; i < jobs.size(); ++i) {
-        const DecimJob& j = jobs[i];
-        const DecimPlan& pl = j.pl;
-        TruncArgs ta{};
-        ta.sigma = outs[i].sig; ta.ns = pl.ns; ta.total_sq = &j.sc->total_sq; ta.trunc_tol = j.trunc_tol;
-        ta.cap = (long long)j.chi_max; ta.renormalize = j.renormalize; ta.kept = &j.sc->kept;
-        ta.lambda = j.lambda; ta.discarded = &j.sc->discarded;
-        check_cuda(c, truncate(ta, c->stream), "truncate");
-        GammaArgs ga{};
-        ga.U = outs[i].U; ga.ldu = pl.ns; ga.V = outs[i].V; ga.ldv = pl.ns; ga.ll = j.ll; ga.lr = j.lr;
-        ga.m = pl.m; ga.n = pl.n; ga.d1 = j.d1; ga.cr = j.cr; ga.kept = &j.sc->kept;
-        ga.gamma_l = j.gamma_l; ga.gamma_r = j.gamma_r; ga.pinv = &j.sc->pinv;
-        check_cuda(c, gamma_reshape(ga, pl.kmax, c->stream), "gamma_reshape");
+    // truncation (tebd.cpp:188-209) and Γ reshape (tebd.cpp:211-235), one launch set per 64 bonds
+    for (size_t base = 0; base < jobs.size(); base += kMaxEpi) {
+        TruncBatch tb{};
+        GammaBatch gb{};
+        gb.max_kept = gb.max_m = gb.max_n = 0;
+        for (size_t i = base; i < std::min(jobs.size(), base + kMaxEpi); ++i) {
+            const DecimJob& j = jobs[i];
+            const DecimPlan& pl = j.pl;
+            TruncArgs& ta = tb.a[tb.count++];
+            ta = TruncArgs{};
+            ta.sigma = outs[i].sig; ta.ns = pl.ns; ta.total_sq = &j.sc->total_sq; ta.trunc_tol = j.trunc_tol;
+            ta.cap = (long long)j.chi_max; ta.renormalize = j.renormalize; ta.kept = &j.sc->kept;
+            ta.lambda = j.lambda; ta.discarded = &j.sc->discarded;
+            GammaArgs& ga = gb.a[gb.count++];
+            ga = GammaArgs{};
+            ga.U = outs[i].U; ga.ldu = pl.ns; ga.V = outs[i].V; ga.ldv = pl.ns; ga.ll = j.ll; ga.lr = j.lr;
+            ga.m = pl.m; ga.n = pl.n; ga.d1 = j.d1; ga.cr = j.cr; ga.kept = &j.sc->kept;
+            ga.gamma_l = j.gamma_l; ga.gamma_r = j.gamma_r; ga.pinv = &j.sc->pinv;
+            gb.max_kept = std::max(gb.max_kept, pl.kmax);
+            gb.max_m = std::max(gb.max_m, pl.m);
+            gb.max_n = std::max(gb.max_n, pl.n);
+        }
+        check_cuda(c, truncate_many(tb, c->stream), "truncate_many");
+        check_cuda(c, gamma_reshape_many(gb, c->stream), "gamma_reshape_many");
         c->launches += 4;
     }
 }

@@ -316,6 +316,45 @@ __global__ void __launch_bounds__(RED_THREADS) sumsq_partial(const cplx* __restr
     }
 }
 
+__global__ void __launch_bounds__(RED_THREADS) sumsq_partial_many(const __grid_constant__ SumsqBatch b,
+                                                                  double* partial, int* bad) {
+    const int p = blockIdx.y;
+    const cplx* __restrict__ a = b.a[p];
+    const long long n = b.n[p];
+    double s = 0.0;
+    int nb = 0;
+    for (long long i = blockIdx.x * (long long)RED_THREADS + threadIdx.x; i < n;
+         i += (long long)gridDim.x * RED_THREADS) {
+        const cplx v = a[i];
+        nb += !(isfinite(v.x) && isfinite(v.y));
+        s += cabs2(v);
+    }
+    __shared__ double ss[RED_THREADS / 32];
+    __shared__ int sb[RED_THREADS / 32];
+    s = warp_sum(s);
+    for (int o = 16; o > 0; o >>= 1) nb += __shfl_xor_sync(0xffffffffu, nb, o);
+    if ((threadIdx.x & 31) == 0) { ss[threadIdx.x >> 5] = s; sb[threadIdx.x >> 5] = nb; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        int tb = 0;
+        for (int w = 0; w < RED_THREADS / 32; ++w) { t += ss[w]; tb += sb[w]; }
+        partial[p * gridDim.x + blockIdx.x] = t;
+        bad[p * gridDim.x + blockIdx.x] = tb;
+    }
+}
+
+__global__ void sumsq_final_many(const __grid_constant__ SumsqBatch b, const double* partial, const int* bad,
+                                 int nblocks) {
+    if (threadIdx.x != 0) return;
+    const int p = blockIdx.x;
+    double t = 0.0;
+    int tb = 0;
+    for (int i = 0; i < nblocks; ++i) { t += partial[p * nblocks + i]; tb += bad[p * nblocks + i]; }
+    *b.out_sq[p] = t;
+    if (b.out_bad[p]) *b.out_bad[p] = tb;
+}
+
 __global__ void sumsq_final(const double* partial, const int* bad, double* out, int* nonfinite) {
     if (threadIdx.x == 0) {
         double t = 0.0;
@@ -383,6 +422,14 @@ cudaError_t jacobi_finish(const JacobiFinBatch& b, int max_c, cudaStream_t s) {
     if (b.count == 0) return cudaSuccess;
     const size_t smem = (size_t)max_c * (sizeof(double) + sizeof(int));
     jacobi_finish_kernel<<<b.count, 256, smem, s>>>(b);
+    return cudaGetLastError();
+}
+
+cudaError_t sumsq_many(const SumsqBatch& b, double* partial, int* partial_bad, cudaStream_t s) {
+    if (b.count == 0) return cudaSuccess;
+    // fixed per-problem block count: deterministic order, independent of the batch size
+    sumsq_partial_many<<<dim3(RED_BLOCKS, b.count), RED_THREADS, 0, s>>>(b, partial, partial_bad);
+    sumsq_final_many<<<b.count, 32, 0, s>>>(b, partial, partial_bad, RED_BLOCKS);
     return cudaGetLastError();
 }
 

@@ -71,5 +71,14 @@ cudaError_t jacobi_finish(const JacobiFinBatch& b, int max_c, cudaStream_t s);
 // partial: >= 2*148 doubles + 2*148 ints of scratch. out_sq / out_nonfinite: device scalars.
 cudaError_t sumsq(const cplx* a, long long n, double* partial, int* partial_bad, double* out_sq,
                   int* out_nonfinite, cudaStream_t s);
+// The same for many arrays in one launch pair; partial/bad: count * 296 scratch entries.
+struct SumsqBatch {
+    int count;
+    const cplx* a[kMaxSmall];
+    long long n[kMaxSmall];
+    double* out_sq[kMaxSmall];
+    int* out_bad[kMaxSmall];
+};
+cudaError_t sumsq_many(const SumsqBatch& b, double* partial, int* partial_bad, cudaStream_t s);
 
 }  // namespace rb

@@ -221,6 +221,116 @@ __global__ void pinv_flag_kernel(const double* ll, int cl, const double* lr, int
 
 __global__ void fill_int_kernel(int* p, int v) { *p = v; }
 
+// ---- batched epilogue kernels (blockIdx.y / z = problem) ------------------------------------
+__global__ void truncate_many_kernel(const __grid_constant__ TruncBatch b) {
+    if (threadIdx.x == 0) {
+        // same code path as truncate_kernel (tebd.cpp:188-209)
+        const TruncArgs& a = b.a[blockIdx.x];
+        const double total = *a.total_sq;
+        const double sigma1 = a.ns > 0 ? a.sigma[0] : 0.0;
+        int kept = 0;
+        for (int i = 0; i < a.ns; ++i) {
+            const double s = a.sigma[i];
+            if (s <= sigma1 * 1e-15) break;
+            if (a.trunc_tol > 0.0 && s * s / total < a.trunc_tol) break;
+            ++kept;
+        }
+        if (kept < 1) kept = 1;
+        if (a.cap > 0 && kept > a.cap) kept = (int)a.cap;
+        double kept_sq = 0.0;
+        for (int i = 0; i < kept; ++i) kept_sq += a.sigma[i] * a.sigma[i];
+        double w = 1.0 - kept_sq / total;
+        w = w < 0.0 ? 0.0 : (w > 1.0 ? 1.0 : w);
+        *a.discarded = w;
+        *a.kept = kept;
+        if (a.lambda) {
+            const double scale = a.renormalize ? 1.0 / sqrt(kept_sq) : 1.0;
+            for (int i = 0; i < kept; ++i) a.lambda[i] = a.renormalize ? a.sigma[i] * scale : a.sigma[i];
+        }
+    }
+}
+
+__global__ void gamma_left_many_kernel(const __grid_constant__ GammaBatch b) {
+    const GammaArgs& a = b.a[blockIdx.y];
+    const int kept = *a.kept;
+    const long long total = (long long)a.m * kept;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+         e += (long long)gridDim.x * blockDim.x) {
+        const int row = (int)(e / kept), g = (int)(e % kept);
+        double inv = 1.0;
+        if (a.ll) {
+            const double lv = a.ll[row / a.d1];
+            inv = lv < 1e-14 ? 0.0 : 1.0 / lv;
+        }
+        a.gamma_l[e] = cscale(a.U[(long long)row * a.ldu + g], inv);
+    }
+}
+
+__global__ void gamma_right_many_kernel(const __grid_constant__ GammaBatch b) {
+    __shared__ cplx tile[32][33];
+    const GammaArgs& a = b.a[blockIdx.z];
+    const int kept = *a.kept;
+    const int g0 = blockIdx.y * 32, c0 = blockIdx.x * 32;
+    if (g0 >= kept || c0 >= a.n) return;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    for (int yy = ty; yy < 32; yy += 8) {
+        const int c = c0 + yy, g = g0 + tx;
+        tile[yy][tx] = (c < a.n && g < kept) ? a.V[(long long)c * a.ldv + g] : mk(0.0, 0.0);
+    }
+    __syncthreads();
+    for (int yy = ty; yy < 32; yy += 8) {
+        const int g = g0 + yy, c = c0 + tx;
+        if (g < kept && c < a.n) {
+            double inv = 1.0;
+            if (a.lr) {
+                const double lv = a.lr[c % a.cr];
+                inv = lv < 1e-14 ? 0.0 : 1.0 / lv;
+            }
+            a.gamma_r[(long long)g * a.n + c] = cscale(cconj(tile[tx][yy]), inv);
+        }
+    }
+}
+
+__global__ void pinv_many_kernel(const __grid_constant__ GammaBatch b) {
+    const GammaArgs& a = b.a[blockIdx.x];
+    const int cl = a.ll ? a.m / a.d1 : 0, cr = a.lr ? a.cr : 0;
+    int f = 0;
+    for (int i = threadIdx.x; i < cl; i += blockDim.x) f |= a.ll[i] < 1e-14;
+    for (int i = threadIdx.x; i < cr; i += blockDim.x) f |= a.lr[i] < 1e-14;
+    f = __syncthreads_or(f);
+    if (threadIdx.x == 0) *a.pinv = f;
+}
+
+__global__ void philox_many_kernel(const __grid_constant__ PhiloxBatch b) {
+    const int p = blockIdx.y;
+    const uint64_t seed = b.seed[p];
+    cplx* out = b.out[p];
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < b.n[p];
+         e += (long long)gridDim.x * blockDim.x) {
+        uint32_t c[4] = {(uint32_t)e, (uint32_t)(e >> 32), 0x243F6A88u, 0x85A308D3u};
+        uint32_t k[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
+#pragma unroll
+        for (int r = 0; r < 10; ++r) {
+            philox_round(c, k);
+            k[0] += 0x9E3779B9u;
+            k[1] += 0xBB67AE85u;
+        }
+        out[e] = box_muller(((unsigned long long)c[1] << 32) | c[0], ((unsigned long long)c[3] << 32) | c[2]);
+    }
+}
+
+__global__ void scale_rows_many_kernel(const __grid_constant__ ScaleRowsBatch b) {
+    const int p = blockIdx.y;
+    const long long total = (long long)b.rows[p] * b.cols[p];
+    const cplx* in = b.in[p];
+    cplx* out = b.out[p];
+    const double* s = b.s[p];
+    const int cols = b.cols[p];
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+         e += (long long)gridDim.x * blockDim.x)
+        out[e] = cscale(in[e], s[e / cols]);
+}
+
 __global__ void conj_transpose_kernel(const cplx* __restrict__ A, int rows, int cols, cplx* __restrict__ out) {
     __shared__ cplx tile[32][33];
     const int r0 = blockIdx.y * 32, c0 = blockIdx.x * 32;
@@ -383,6 +493,32 @@ cudaError_t gamma_reshape(const GammaArgs& a, int max_kept, cudaStream_t s) {
     dim3 grid((a.n + 31) / 32, (max_kept + 31) / 32);
     gamma_right_kernel<<<grid, 256, 0, s>>>(a);
     pinv_flag_kernel<<<1, 256, 0, s>>>(a.ll, a.ll ? a.m / a.d1 : 0, a.lr, a.lr ? a.cr : 0, a.pinv);
+    return cudaGetLastError();
+}
+
+cudaError_t truncate_many(const TruncBatch& b, cudaStream_t s) {
+    if (b.count == 0) return cudaSuccess;
+    truncate_many_kernel<<<b.count, 32, 0, s>>>(b);
+    return cudaGetLastError();
+}
+
+cudaError_t gamma_reshape_many(const GammaBatch& b, cudaStream_t s) {
+    if (b.count == 0) return cudaSuccess;
+    gamma_left_many_kernel<<<dim3(std::max(1, 4 * kNumSMs / b.count), b.count), 256, 0, s>>>(b);
+    gamma_right_many_kernel<<<dim3((b.max_n + 31) / 32, (b.max_kept + 31) / 32, b.count), 256, 0, s>>>(b);
+    pinv_many_kernel<<<b.count, 256, 0, s>>>(b);
+    return cudaGetLastError();
+}
+
+cudaError_t omega_philox_many(const PhiloxBatch& b, cudaStream_t s) {
+    if (b.count == 0) return cudaSuccess;
+    philox_many_kernel<<<dim3(std::max(1, 4 * kNumSMs / b.count), b.count), 256, 0, s>>>(b);
+    return cudaGetLastError();
+}
+
+cudaError_t scale_rows_many(const ScaleRowsBatch& b, cudaStream_t s) {
+    if (b.count == 0) return cudaSuccess;
+    scale_rows_many_kernel<<<dim3(std::max(1, 4 * kNumSMs / b.count), b.count), 256, 0, s>>>(b);
     return cudaGetLastError();
 }
 

@@ -59,6 +59,36 @@ struct GammaArgs {
 };
 cudaError_t gamma_reshape(const GammaArgs& a, int max_kept, cudaStream_t s);
 
+// ---- batched forms: one launch for all bonds of a sweep ----------------------------------------
+constexpr int kMaxEpi = 64;
+struct TruncBatch {
+    int count;
+    TruncArgs a[kMaxEpi];
+};
+cudaError_t truncate_many(const TruncBatch& b, cudaStream_t s);
+struct GammaBatch {
+    int count;
+    int max_kept, max_m, max_n;
+    GammaArgs a[kMaxEpi];
+};
+cudaError_t gamma_reshape_many(const GammaBatch& b, cudaStream_t s);
+struct PhiloxBatch {
+    int count;
+    uint64_t seed[kMaxEpi];
+    long long n[kMaxEpi];
+    cplx* out[kMaxEpi];
+};
+cudaError_t omega_philox_many(const PhiloxBatch& b, cudaStream_t s);
+// Θ pre-scaling for the Θ GEMM: out[r][c] = in[r][c] * s[r]  (rows x cols, row-major)
+struct ScaleRowsBatch {
+    int count;
+    const cplx* in[kMaxEpi];
+    const double* s[kMaxEpi];
+    int rows[kMaxEpi], cols[kMaxEpi];
+    cplx* out[kMaxEpi];
+};
+cudaError_t scale_rows_many(const ScaleRowsBatch& b, cudaStream_t s);
+
 cudaError_t fill_int(int* p, int v, cudaStream_t s);
 
 // out (cols x rows) = A^H for A (rows x cols), both row-major.
