@@ -208,6 +208,21 @@ int rrsvd_b200_evolve(rrsvd_b200_mps* mps, size_t n_sweeps, const rrsvd_b200_swe
                       const double* const* gates, size_t n_steps, rrsvd_b200_backend* backend,
                       const rrsvd_b200_evolve_options* options, rrsvd_b200_evolve_diag* diag,
                       rrsvd_b200_update_record* records, size_t max_records);
+/* A two-site gate made resident on the device once: the copy plus its exact block structure
+ * (connected components of the nonzero pattern; excitation-number-conserving gates are
+ * block-diagonal up to a permutation and are then applied block-sparsely — same result as the
+ * dense product).  The gate passed to the reference is a TwoSiteGate (tebd.hpp:35-39). */
+typedef struct rrsvd_b200_gate rrsvd_b200_gate;
+int rrsvd_b200_gate_create(rrsvd_b200_ctx* ctx, const double* G, size_t dd, rrsvd_b200_gate** out);
+void rrsvd_b200_gate_destroy(rrsvd_b200_gate* gate);
+/* 1 if the gate is applied block-sparsely (nblocks out), 0 if dense. */
+int rrsvd_b200_gate_blocks(const rrsvd_b200_gate* gate, size_t* nblocks);
+/* evolve with prepared gates: gates[s*(n_sites-1)+b] (NULL = no term). */
+int rrsvd_b200_evolve_prepared(rrsvd_b200_mps* mps, size_t n_sweeps, const rrsvd_b200_sweep* sweeps,
+                               const rrsvd_b200_gate* const* gates, size_t n_steps,
+                               rrsvd_b200_backend* backend, const rrsvd_b200_evolve_options* options,
+                               rrsvd_b200_evolve_diag* diag, rrsvd_b200_update_record* records,
+                               size_t max_records);
 /* <psi| O_site |psi> (mps.cpp:50-70) -> out2 = (re, im); S = -sum λ² ln λ² (mps.cpp:40-48). */
 int rrsvd_b200_expectation_local(rrsvd_b200_mps* mps, size_t site, const double* op, double* out2);
 int rrsvd_b200_schmidt_entropy(rrsvd_b200_mps* mps, size_t bond, double* out);

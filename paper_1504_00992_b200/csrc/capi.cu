@@ -293,7 +293,10 @@ int rrsvd_b200_apply_gate_unfolded(rrsvd_b200_ctx* c, const double* G, size_t d1
         const auto* dG = static_cast<const cplx*>(stage_in(c, G, dd * dd * sizeof(cplx)));
         const auto* dI = static_cast<const cplx*>(stage_in(c, M_in, tot * sizeof(cplx)));
         auto* dO = static_cast<cplx*>(stage_out(c, M_out, tot * sizeof(cplx), outs));
-        apply_gate_many(c, {GateJob{dG, (int)d1, (int)d2, (int)cl, (int)cr, dI, dO}});
+        GateBlocksOwned gbo;
+        const bool blocked = dd > 16 && make_gate_blocks(c, dG, (int)dd, gbo);
+        apply_gate_many(c, {GateJob{dG, (int)d1, (int)d2, (int)cl, (int)cr, dI, dO, blocked ? &gbo.dev : nullptr}});
+        free_gate_blocks(c, gbo);
         finish_out(c, outs);
     });
 }
@@ -413,6 +416,12 @@ int rrsvd_b200_gemm_stage_stats(rrsvd_b200_ctx* c, double* flops8, double* ms8) 
 int rrsvd_b200_probe_peak(rrsvd_b200_ctx* c, int what, double* tflops) {
     return api(c, [&] {
         if (tflops == nullptr) throw_contract(c, "probe_peak: null output");
+        if (what >= 100) {  // 100 + warps*10 + chains: DMMA at a given residency (diagnostics)
+            const int code = what - 100;
+            check_cuda(c, probe_dmma_occupancy(code / 10, code % 10, tflops, c->stream), "probe_dmma_occupancy");
+            c->launches += 2;
+            return;
+        }
         check_cuda(c, probe_peak(what, tflops, c->stream), "probe_peak");
         c->launches += 2;
     });

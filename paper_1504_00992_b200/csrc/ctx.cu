@@ -83,27 +83,27 @@ void release_staged(rrsvd_b200_ctx* c) {
     c->staged.clear();
 }
 
-void lanes_fork(rrsvd_b200_ctx* c) {
-    if (c->lane[0] == nullptr) {
-        for (int i = 0; i < 2; ++i) {
+void lanes_fork(rrsvd_b200_ctx* c, int n) {
+    if (c->ev_fork == nullptr)
+        check_cuda(c, cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming), "lane event");
+    for (int i = 0; i < n; ++i)
+        if (c->lane[i] == nullptr) {
             check_cuda(c, cudaStreamCreateWithFlags(&c->lane[i], cudaStreamNonBlocking), "lane stream");
             check_cuda(c, cudaEventCreateWithFlags(&c->ev_join[i], cudaEventDisableTiming), "lane event");
         }
-        check_cuda(c, cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming), "lane event");
-    }
     check_cuda(c, cudaEventRecord(c->ev_fork, c->stream), "fork record");
-    for (int i = 0; i < 2; ++i) check_cuda(c, cudaStreamWaitEvent(c->lane[i], c->ev_fork, 0), "fork wait");
+    for (int i = 0; i < n; ++i) check_cuda(c, cudaStreamWaitEvent(c->lane[i], c->ev_fork, 0), "fork wait");
 }
 
-void lanes_join(rrsvd_b200_ctx* c) {
-    for (int i = 0; i < 2; ++i) {
+void lanes_join(rrsvd_b200_ctx* c, int n) {
+    for (int i = 0; i < n; ++i) {
         check_cuda(c, cudaEventRecord(c->ev_join[i], c->lane[i]), "join record");
         check_cuda(c, cudaStreamWaitEvent(c->stream, c->ev_join[i], 0), "join wait");
     }
 }
 
 void release_lanes(rrsvd_b200_ctx* c) {
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < rrsvd_b200_ctx::kMaxLanes; ++i) {
         if (c->lane[i]) cudaStreamDestroy(c->lane[i]);
         if (c->ev_join[i]) cudaEventDestroy(c->ev_join[i]);
         c->lane[i] = nullptr;

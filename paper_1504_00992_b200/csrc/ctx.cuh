@@ -35,9 +35,11 @@ struct rrsvd_b200_ctx {
 
     // Two auxiliary streams ("lanes") so independent halves of a sweep overlap: one lane's
     // latency-bound small kernels (Cholesky, Jacobi) run beside the other lane's GEMMs.
-    cudaStream_t lane[2] = {nullptr, nullptr};
-    cudaEvent_t ev_fork = nullptr, ev_join[2] = {nullptr, nullptr};
+    static constexpr int kMaxLanes = 8;
+    cudaStream_t lane[kMaxLanes] = {};
+    cudaEvent_t ev_fork = nullptr, ev_join[kMaxLanes] = {};
     bool use_lanes = true;
+    int n_lanes = 2;  // RRSVD_B200_LANES overrides
     double gemm_ms = 0.0, gemm_flops = 0.0;
     uint64_t gemm_calls = 0;
 };
@@ -86,8 +88,8 @@ void release_staged(rrsvd_b200_ctx* c);
 
 // Lanes: fork(c) makes both lanes wait for the work already queued on c->stream; join(c)
 // makes c->stream wait for both lanes.  release_lanes at context destruction.
-void lanes_fork(rrsvd_b200_ctx* c);
-void lanes_join(rrsvd_b200_ctx* c);
+void lanes_fork(rrsvd_b200_ctx* c, int n);
+void lanes_join(rrsvd_b200_ctx* c, int n);
 void release_lanes(rrsvd_b200_ctx* c);
 
 // zgemm timing: events around each GEMM launch (incl. its split-K reduction) while enabled.

@@ -213,40 +213,63 @@ int rrsvd_b200_mps_get_site(rrsvd_b200_mps* s, size_t site, size_t* dims3, doubl
     });
 }
 
-int rrsvd_b200_evolve(rrsvd_b200_mps* s, size_t n_sweeps, const rrsvd_b200_sweep* sweeps, const double* const* gates,
-                      size_t n_steps, rrsvd_b200_backend* be, const rrsvd_b200_evolve_options* opt,
-                      rrsvd_b200_evolve_diag* diag, rrsvd_b200_update_record* records, size_t max_records) {
-    return mps_api(s, [&](rrsvd_b200_ctx* c) {
+}  // extern "C"
+
+// A gate resident on the device with its exact block structure (made once, reused by every
+// sweep and every evolve call).
+struct rrsvd_b200_gate {
+    rrsvd_b200_ctx* c = nullptr;
+    int dd = 0;
+    cplx* dev = nullptr;
+    bool blocked = false;
+    GateBlocksOwned blk;
+};
+
+namespace {
+
+rrsvd_b200_gate* prepare_gate(rrsvd_b200_ctx* c, const double* G, size_t dd) {
+    auto* g = new rrsvd_b200_gate();
+    g->c = c;
+    g->dd = (int)dd;
+    try {
+        check_cuda(c, cudaMallocAsync(reinterpret_cast<void**>(&g->dev), dd * dd * sizeof(cplx), c->stream), "alloc gate");
+        check_cuda(c, cudaMemcpyAsync(g->dev, G, dd * dd * sizeof(cplx), cudaMemcpyDefault, c->stream), "stage gate");
+        // excitation-number-conserving gates are block-diagonal up to a permutation
+        g->blocked = dd > 16 && make_gate_blocks(c, g->dev, (int)dd, g->blk);
+    } catch (...) {
+        if (g->dev) cudaFreeAsync(g->dev, c->stream);
+        delete g;
+        throw;
+    }
+    return g;
+}
+
+void release_gate(rrsvd_b200_gate* g) {
+    if (g == nullptr) return;
+    if (g->c) {
+        free_gate_blocks(g->c, g->blk);
+        if (g->dev) cudaFreeAsync(g->dev, g->c->stream);
+    }
+    delete g;
+}
+
+void evolve_core(rrsvd_b200_mps* s, rrsvd_b200_ctx* c, size_t n_sweeps, const rrsvd_b200_sweep* sweeps,
+                 const rrsvd_b200_gate* const* gates, size_t n_steps, rrsvd_b200_backend* be,
+                 const rrsvd_b200_evolve_options* opt, rrsvd_b200_evolve_diag* diag,
+                 rrsvd_b200_update_record* records, size_t max_records) {
+    {
         if (be == nullptr || diag == nullptr || (n_sweeps && (sweeps == nullptr || gates == nullptr)))
             throw_contract(c, "evolve: null argument");
         const int n = s->n, nb = n - 1;
         const double abort_thr = opt ? opt->abort_discarded_threshold : 1.0;
         const int renorm = opt ? opt->renormalize : 1;
         const int omode = opt ? opt->omega_mode : RRSVD_B200_OMEGA_REFERENCE;
-        // Stage each distinct gate once (the reference builds one per (bond, coefficient),
-        // tebd.cpp:276-285).
-        std::map<const double*, const cplx*> staged;
-        std::vector<void*> gate_bufs;
         for (size_t sw = 0; sw < n_sweeps; ++sw)
             for (int b = 0; b < nb; ++b) {
-                const double* gp = gates[sw * nb + b];
-                if (gp == nullptr || staged.count(gp)) continue;
-                const size_t dd = (size_t)s->d[b] * s->d[b + 1];
-                if (is_device_ptr(gp)) {
-                    staged[gp] = reinterpret_cast<const cplx*>(gp);
-                } else {
-                    void* buf = nullptr;
-                    check_cuda(c, cudaMallocAsync(&buf, dd * dd * sizeof(cplx), c->stream), "alloc gate");
-                    check_cuda(c, cudaMemcpyAsync(buf, gp, dd * dd * sizeof(cplx), cudaMemcpyHostToDevice, c->stream), "H2D gate");
-                    gate_bufs.push_back(buf);
-                    staged[gp] = static_cast<const cplx*>(buf);
-                }
+                const rrsvd_b200_gate* g = gates[sw * nb + b];
+                if (g != nullptr && g->dd != s->d[b] * s->d[b + 1])
+                    throw_contract(c, "evolve: term dimension mismatch");
             }
-        struct GateGuard {
-            rrsvd_b200_ctx* c;
-            std::vector<void*>& v;
-            ~GateGuard() { for (void* p : v) cudaFreeAsync(p, c->stream); }
-        } guard{c, gate_bufs};
 
         DecimScalars* sc_dev = nullptr;
         size_t sc_cap = 0;
@@ -315,14 +338,19 @@ int rrsvd_b200_evolve(rrsvd_b200_mps* s, size_t n_sweeps, const rrsvd_b200_sweep
                 }
                 check_cuda(c, cudaEventRecord(ev[0], c->stream), "event");
                 const cudaStream_t main_stream = c->stream;
-                const bool two_lanes = nbnd >= 2 && c->use_lanes;
-                if (two_lanes) lanes_fork(c);
-                for (int lane = 0; lane < (two_lanes ? 2 : 1); ++lane) {
-                    if (two_lanes) c->stream = c->lane[lane];
+                static const int env_lanes = [] {
+                    const char* e = std::getenv("RRSVD_B200_LANES");
+                    return e ? std::atoi(e) : 0;
+                }();
+                const int want = env_lanes > 0 ? env_lanes : c->n_lanes;
+                const int nl = c->use_lanes ? std::max(1, std::min<int>({want, (int)nbnd, rrsvd_b200_ctx::kMaxLanes})) : 1;
+                if (nl > 1) lanes_fork(c, nl);
+                for (int lane = 0; lane < nl; ++lane) {
+                    if (nl > 1) c->stream = c->lane[lane];
                     std::vector<ThetaJob> tj;
                     std::vector<GateJob> gj;
                     std::vector<DecimJob> dj;
-                    for (size_t i = lane; i < nbnd; i += (two_lanes ? 2 : 1)) {
+                    for (size_t i = lane; i < nbnd; i += nl) {
                         const int b = bonds[i];
                         const int d1 = s->d[b], d2 = s->d[b + 1];
                         const int cl = s->dl[b], cm = s->dr[b], cr = s->dr[b + 1];
@@ -331,7 +359,8 @@ int rrsvd_b200_evolve(rrsvd_b200_mps* s, size_t n_sweeps, const rrsvd_b200_sweep
                         const double* ll = s->ll_of(b);
                         const double* lr = s->lr_of(b);
                         tj.push_back({gin1[i], gin2[i], ll, lin[i], lr, cl, d1, cm, d2, cr, M1});
-                        gj.push_back({staged[gates[sw * nb + b]], d1, d2, cl, cr, M1, M2});
+                        const rrsvd_b200_gate* G = gates[sw * nb + b];
+                        gj.push_back({G->dev, d1, d2, cl, cr, M1, M2, G->blocked ? &G->blk.dev : nullptr});
                         dj.push_back({plans[i], M2, d1, cr, ll, lr, s->chi_max, s->tol, (int)be->power_iterations,
                                       seeds[i], omode, nullptr, renorm, s->g[b], s->lam[b], s->g[b + 1], sc_dev + i});
                     }
@@ -342,7 +371,7 @@ int rrsvd_b200_evolve(rrsvd_b200_mps* s, size_t n_sweeps, const rrsvd_b200_sweep
                     decimate_many(c, dj);
                 }
                 c->stream = main_stream;
-                if (two_lanes) lanes_join(c);
+                if (nl > 1) lanes_join(c, nl);
                 for (void* p : old_bufs) cudaFreeAsync(p, c->stream);
                 check_cuda(c, cudaEventRecord(ev[3], c->stream), "event");
                 check_cuda(c, cudaMemcpyAsync(sc_host, sc_dev, nbnd * sizeof(DecimScalars), cudaMemcpyDeviceToHost,
@@ -376,6 +405,72 @@ int rrsvd_b200_evolve(rrsvd_b200_mps* s, size_t n_sweeps, const rrsvd_b200_sweep
                 }
             }
         }
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+int rrsvd_b200_gate_create(rrsvd_b200_ctx* c, const double* G, size_t dd, rrsvd_b200_gate** out) {
+    if (c == nullptr || out == nullptr) return kContract;
+    *out = nullptr;
+    int code = kOk;
+    try {
+        cudaSetDevice(c->device);
+        if (G == nullptr || dd == 0) throw_contract(c, "gate_create: empty gate");
+        *out = prepare_gate(c, G, dd);
+    } catch (const Fail& e) {
+        code = e.code;
+    }
+    return code;
+}
+
+void rrsvd_b200_gate_destroy(rrsvd_b200_gate* g) {
+    if (g && g->c) cudaSetDevice(g->c->device);
+    release_gate(g);
+}
+
+int rrsvd_b200_gate_blocks(const rrsvd_b200_gate* g, size_t* nblocks) {
+    if (g == nullptr) return 0;
+    if (nblocks) *nblocks = g->blocked ? (size_t)g->blk.dev.nblocks : 1;
+    return g->blocked ? 1 : 0;
+}
+
+int rrsvd_b200_evolve_prepared(rrsvd_b200_mps* s, size_t n_sweeps, const rrsvd_b200_sweep* sweeps,
+                               const rrsvd_b200_gate* const* gates, size_t n_steps, rrsvd_b200_backend* be,
+                               const rrsvd_b200_evolve_options* opt, rrsvd_b200_evolve_diag* diag,
+                               rrsvd_b200_update_record* records, size_t max_records) {
+    return mps_api(s, [&](rrsvd_b200_ctx* c) {
+        evolve_core(s, c, n_sweeps, sweeps, gates, n_steps, be, opt, diag, records, max_records);
+    });
+}
+
+// Raw gate matrices: each distinct gate (the reference builds one per (bond, coefficient),
+// tebd.cpp:276-285) is prepared for this call only.  Repeated calls should prepare gates once
+// with rrsvd_b200_gate_create and use rrsvd_b200_evolve_prepared.
+int rrsvd_b200_evolve(rrsvd_b200_mps* s, size_t n_sweeps, const rrsvd_b200_sweep* sweeps, const double* const* gates,
+                      size_t n_steps, rrsvd_b200_backend* be, const rrsvd_b200_evolve_options* opt,
+                      rrsvd_b200_evolve_diag* diag, rrsvd_b200_update_record* records, size_t max_records) {
+    return mps_api(s, [&](rrsvd_b200_ctx* c) {
+        if (n_sweeps && (sweeps == nullptr || gates == nullptr)) throw_contract(c, "evolve: null argument");
+        const int nb = s->n - 1;
+        std::map<const double*, rrsvd_b200_gate*> made;
+        struct Guard {
+            std::map<const double*, rrsvd_b200_gate*>& m;
+            ~Guard() { for (auto& kv : m) release_gate(kv.second); }
+        } guard{made};
+        std::vector<const rrsvd_b200_gate*> table(n_sweeps * nb, nullptr);
+        for (size_t sw = 0; sw < n_sweeps; ++sw)
+            for (int b = 0; b < nb; ++b) {
+                const double* gp = gates[sw * nb + b];
+                if (gp == nullptr) continue;
+                auto it = made.find(gp);
+                if (it == made.end())
+                    it = made.emplace(gp, prepare_gate(c, gp, (size_t)s->d[b] * s->d[b + 1])).first;
+                table[sw * nb + b] = it->second;
+            }
+        evolve_core(s, c, n_sweeps, sweeps, table.data(), n_steps, be, opt, diag, records, max_records);
     });
 }
 

@@ -412,11 +412,86 @@ void build_theta_many(rrsvd_b200_ctx* c, const std::vector<ThetaJob>& jobs) {
     gemm_many(c, kOpN, gs);
 }
 
+bool make_gate_blocks(rrsvd_b200_ctx* c, const cplx* G, int dd, GateBlocksOwned& out) {
+    std::vector<cplx> h((size_t)dd * dd);
+    check_cuda(c, cudaMemcpyAsync(h.data(), G, h.size() * sizeof(cplx), cudaMemcpyDefault, c->stream), "gate D2H");
+    check_cuda(c, cudaStreamSynchronize(c->stream), "sync");
+    std::vector<int> parent(dd);
+    for (int i = 0; i < dd; ++i) parent[i] = i;
+    auto find = [&](int x) {
+        while (parent[x] != x) x = parent[x] = parent[parent[x]];
+        return x;
+    };
+    for (int r = 0; r < dd; ++r)
+        for (int k = 0; k < dd; ++k) {
+            const cplx v = h[(size_t)r * dd + k];
+            if (v.x != 0.0 || v.y != 0.0) {
+                const int a = find(r), b = find(k);
+                if (a != b) parent[a] = b;
+            }
+        }
+    std::vector<std::vector<int>> groups;
+    std::vector<int> gid(dd, -1);
+    for (int i = 0; i < dd; ++i) {
+        const int root = find(i);
+        if (gid[root] < 0) {
+            gid[root] = (int)groups.size();
+            groups.emplace_back();
+        }
+        groups[gid[root]].push_back(i);
+    }
+    if (groups.size() < 2) return false;
+    for (const auto& g : groups)
+        if ((int)g.size() > kMaxGateBlock) return false;
+    std::vector<int> offs{0}, idx, goff;
+    std::vector<cplx> gblk;
+    for (const auto& g : groups) {
+        goff.push_back((int)gblk.size());
+        for (int r : g) {
+            idx.push_back(r);
+            for (int k : g) gblk.push_back(h[(size_t)r * dd + k]);
+        }
+        offs.push_back((int)idx.size());
+    }
+    auto upload = [&](const void* src, size_t bytes) {
+        void* d = nullptr;
+        check_cuda(c, cudaMallocAsync(&d, std::max<size_t>(bytes, 16), c->stream), "alloc gate blocks");
+        check_cuda(c, cudaMemcpyAsync(d, src, bytes, cudaMemcpyHostToDevice, c->stream), "upload gate blocks");
+        out.bufs.push_back(d);
+        return d;
+    };
+    out.dev.nblocks = (int)groups.size();
+    out.dev.dd = dd;
+    out.dev.offs = static_cast<const int*>(upload(offs.data(), offs.size() * sizeof(int)));
+    out.dev.idx = static_cast<const int*>(upload(idx.data(), idx.size() * sizeof(int)));
+    out.dev.goff = static_cast<const int*>(upload(goff.data(), goff.size() * sizeof(int)));
+    out.dev.gblk = static_cast<const cplx*>(upload(gblk.data(), gblk.size() * sizeof(cplx)));
+    check_cuda(c, cudaStreamSynchronize(c->stream), "sync");  // host vectors die at return
+    return true;
+}
+
+void free_gate_blocks(rrsvd_b200_ctx* c, GateBlocksOwned& g) {
+    for (void* p : g.bufs) cudaFreeAsync(p, c->stream);
+    g.bufs.clear();
+}
+
 void apply_gate_many(rrsvd_b200_ctx* c, const std::vector<GateJob>& jobs) {
     std::vector<GemmSpec> gs;
+    GateBlockBatch gbb{};
+    long long max_cols = 0;
+    auto flush_blocks = [&] {
+        check_cuda(c, gate_blocks_many(gbb, max_cols, c->stream), "gate_blocks");
+        if (gbb.count) c->launches++;
+        gbb.count = 0;
+        max_cols = 0;
+    };
     for (const GateJob& j : jobs) {
         const int dd = j.d1 * j.d2;
-        if (dd <= 16) {
+        if (j.blocks != nullptr) {
+            gbb.j[gbb.count++] = GateBlockJob{*j.blocks, j.Min, j.Mout, j.cl, j.cr};
+            max_cols = std::max(max_cols, (long long)j.cl * j.cr);
+            if (gbb.count == kMaxEpi) flush_blocks();
+        } else if (dd <= 16) {
             check_cuda(c, gate_small(j.G, dd, j.cl, j.cr, j.Min, j.Mout, c->stream), "gate_small");
             c->launches++;
         } else {
@@ -428,6 +503,7 @@ void apply_gate_many(rrsvd_b200_ctx* c, const std::vector<GateJob>& jobs) {
             gs.push_back(g);
         }
     }
+    flush_blocks();
     c->gemm_tag = 1;
     gemm_many(c, kOpN, gs);
 }

@@ -142,7 +142,18 @@ struct GateJob {
     int d1, d2, cl, cr;
     const cplx* Min;
     cplx* Mout;
+    const GateBlocks* blocks = nullptr;  // exact block structure of G (block kernel) or dense
 };
 void apply_gate_many(rrsvd_b200_ctx* c, const std::vector<GateJob>& jobs);
+
+// Exact block structure of a gate (connected components of its nonzero pattern, host-side, once
+// per gate).  Device arrays are allocated on c->stream and must be freed with free_gate_blocks.
+// Returns false (nothing allocated) when G is dense or a block exceeds kMaxGateBlock.
+struct GateBlocksOwned {
+    GateBlocks dev{};
+    std::vector<void*> bufs;
+};
+bool make_gate_blocks(rrsvd_b200_ctx* c, const cplx* G, int dd, GateBlocksOwned& out);
+void free_gate_blocks(rrsvd_b200_ctx* c, GateBlocksOwned& g);
 
 }  // namespace rb

@@ -124,6 +124,39 @@ __global__ void gate_small_kernel(const cplx* __restrict__ G, int dd, int cl, in
     }
 }
 
+// ============================================================================ block gate
+// grid (column chunks of 256, job); each thread owns one column (a, b) of the job's Θ and runs
+// through all blocks; the block G_B is staged in shared memory, the |S_B| inputs in registers.
+__global__ void __launch_bounds__(256) gate_blocks_kernel(const __grid_constant__ GateBlockBatch bt) {
+    __shared__ cplx sg[kMaxGateBlock * kMaxGateBlock];
+    const GateBlockJob& J = bt.j[blockIdx.y];
+    const GateBlocks& B = J.gb;
+    const long long cols = (long long)J.cl * J.cr;
+    const long long c = blockIdx.x * 256LL + threadIdx.x;
+    const bool active = c < cols;
+    const long long a = active ? c / J.cr : 0, bcol = active ? c % J.cr : 0;
+    const long long base = a * B.dd * J.cr + bcol;
+    for (int k = 0; k < B.nblocks; ++k) {
+        const int off = B.offs[k], sz = B.offs[k + 1] - off;
+        const cplx* g = B.gblk + B.goff[k];
+        __syncthreads();
+        for (int t = threadIdx.x; t < sz * sz; t += 256) sg[t] = g[t];
+        __syncthreads();
+        if (!active) continue;
+        cplx v[kMaxGateBlock];
+#pragma unroll
+        for (int t = 0; t < kMaxGateBlock; ++t)
+            if (t < sz) v[t] = J.Min[base + (long long)B.idx[off + t] * J.cr];
+        for (int r = 0; r < sz; ++r) {
+            cplx acc = mk(0.0, 0.0);
+#pragma unroll
+            for (int t = 0; t < kMaxGateBlock; ++t)
+                if (t < sz) cfma(acc, sg[r * sz + t], v[t]);
+            J.Mout[base + (long long)B.idx[off + r] * J.cr] = acc;
+        }
+    }
+}
+
 // ============================================================================ layout
 __global__ void theta_unfold_kernel(const cplx* __restrict__ src, int d1, int d2, int cl, int cr,
                                     cplx* __restrict__ dst, int to_unfolded) {
@@ -433,6 +466,22 @@ __global__ void __launch_bounds__(256) probe_dmma_kernel(double* sink, double se
     if (s == 12345.678) sink[threadIdx.x] = s;
 }
 
+template <int CHAINS>
+__global__ void probe_dmma_occ_kernel(double* sink, double seed, int iters) {
+    double acc[CHAINS][2];
+#pragma unroll
+    for (int i = 0; i < CHAINS; ++i) acc[i][0] = acc[i][1] = 0.0;
+    double a = seed + threadIdx.x * 1e-9, b = seed * 0.5;
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int i = 0; i < CHAINS; ++i) dmma884(acc[i][0], acc[i][1], a, b);
+    }
+    double s = 0.0;
+#pragma unroll
+    for (int i = 0; i < CHAINS; ++i) s += acc[i][0] + acc[i][1];
+    if (s == 12345.678) sink[threadIdx.x] = s;
+}
+
 __global__ void __launch_bounds__(256) probe_dfma_kernel(double* sink, double seed) {
     double acc[8];
 #pragma unroll
@@ -496,6 +545,12 @@ cudaError_t gamma_reshape(const GammaArgs& a, int max_kept, cudaStream_t s) {
     return cudaGetLastError();
 }
 
+cudaError_t gate_blocks_many(const GateBlockBatch& b, long long max_cols, cudaStream_t s) {
+    if (b.count == 0) return cudaSuccess;
+    gate_blocks_kernel<<<dim3((unsigned)((max_cols + 255) / 256), b.count), 256, 0, s>>>(b);
+    return cudaGetLastError();
+}
+
 cudaError_t truncate_many(const TruncBatch& b, cudaStream_t s) {
     if (b.count == 0) return cudaSuccess;
     truncate_many_kernel<<<b.count, 32, 0, s>>>(b);
@@ -550,6 +605,39 @@ cudaError_t expectation_local_dev(const cplx* G, int dl, int d, int dr, const do
 cudaError_t schmidt_entropy_dev(const double* lam, int n, double* out, cudaStream_t s) {
     entropy_kernel<<<1, 32, 0, s>>>(lam, n, out);
     return cudaGetLastError();
+}
+
+// DMMA throughput at a given residency: `warps` warps per SM (one CTA per SM), `chains`
+// independent accumulators per warp.  Diagnostics for the zgemm occupancy/ILP trade-off.
+cudaError_t probe_dmma_occupancy(int warps, int chains, double* tflops, cudaStream_t s) {
+    double* sink = nullptr;
+    cudaError_t e = cudaMallocAsync(&sink, 1024 * sizeof(double), s);
+    if (e != cudaSuccess) return e;
+    cudaEvent_t t0, t1;
+    cudaEventCreate(&t0);
+    cudaEventCreate(&t1);
+    const int iters = 8192;
+    auto launch = [&] {
+        switch (chains) {
+            case 1: probe_dmma_occ_kernel<1><<<kNumSMs, 32 * warps, 0, s>>>(sink, 1.0, iters); break;
+            case 2: probe_dmma_occ_kernel<2><<<kNumSMs, 32 * warps, 0, s>>>(sink, 1.0, iters); break;
+            case 4: probe_dmma_occ_kernel<4><<<kNumSMs, 32 * warps, 0, s>>>(sink, 1.0, iters); break;
+            default: probe_dmma_occ_kernel<8><<<kNumSMs, 32 * warps, 0, s>>>(sink, 1.0, iters); break;
+        }
+    };
+    launch();
+    cudaEventRecord(t0, s);
+    launch();
+    cudaEventRecord(t1, s);
+    e = cudaEventSynchronize(t1);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, t0, t1);
+    const int ch = (chains == 1 || chains == 2 || chains == 4) ? chains : 8;
+    *tflops = (double)kNumSMs * warps * iters * ch * 512.0 / (ms * 1e-3) / 1e12;
+    cudaEventDestroy(t0);
+    cudaEventDestroy(t1);
+    cudaFreeAsync(sink, s);
+    return e == cudaSuccess ? cudaGetLastError() : e;
 }
 
 cudaError_t probe_peak(int what, double* tflops, cudaStream_t s) {

@@ -4,6 +4,8 @@
 
 namespace rb {
 
+constexpr int kMaxEpi = 64;  // problems per launch of the batched epilogue kernels
+
 // ---- Gaussian sketch Omega (n x l, row-major) --------------------------------------------
 // Reference stream (randomized.cpp:17-45,79-86): std::mt19937_64(seed); entry e consumes draws
 // 2e (u1 = ((x>>11)+1)·2^-53) and 2e+1 (u2 = (x>>11)·2^-53); re = r cos(2πu2), im = r sin(2πu2),
@@ -19,6 +21,31 @@ cudaError_t omega_philox(uint64_t seed, long long n_entries, cplx* out, cudaStre
 // M_out[a][x][b] = sum_y G[x][y] M_in[a][y][b],  x, y < dd = d1*d2 <= 64.
 cudaError_t gate_small(const cplx* G, int dd, int cl, int cr, const cplx* Min, cplx* Mout,
                        cudaStream_t s);
+
+// ---- two-site gate with exact block structure --------------------------------------------
+// A gate G (dd x dd) that is block-diagonal up to a permutation of the two-site states (e.g.
+// excitation-number-conserving bosonic gates) is applied block by block: for each block B with
+// state set S_B, M_out[a][S_B][b] = G_B · M_in[a][S_B][b].  One pass over Θ (bandwidth-bound)
+// instead of the dense dd x dd GEMM.  Exact zeros only — the result equals the dense product.
+constexpr int kMaxGateBlock = 32;
+struct GateBlocks {
+    int nblocks, dd;
+    const int* offs;   // nblocks + 1 offsets into idx
+    const int* idx;    // the dd states grouped by block (row indices into G)
+    const int* goff;   // nblocks offsets into gblk
+    const cplx* gblk;  // dense blocks G_B (|S_B| x |S_B|, row-major, local indices)
+};
+struct GateBlockJob {
+    GateBlocks gb;
+    const cplx* Min;
+    cplx* Mout;
+    int cl, cr;
+};
+struct GateBlockBatch {
+    int count;
+    GateBlockJob j[kMaxEpi];
+};
+cudaError_t gate_blocks_many(const GateBlockBatch& b, long long max_cols, cudaStream_t s);
 
 // ---- layout conversion (i, j, a, b) <-> (a*d1+i, j*cr+b) ----------------------------------
 cudaError_t theta_to_unfolded(const cplx* theta, int d1, int d2, int cl, int cr, cplx* M, cudaStream_t s);
@@ -60,7 +87,6 @@ struct GammaArgs {
 cudaError_t gamma_reshape(const GammaArgs& a, int max_kept, cudaStream_t s);
 
 // ---- batched forms: one launch for all bonds of a sweep ----------------------------------------
-constexpr int kMaxEpi = 64;
 struct TruncBatch {
     int count;
     TruncArgs a[kMaxEpi];
@@ -108,5 +134,6 @@ cudaError_t schmidt_entropy_dev(const double* lam, int n, double* out, cudaStrea
 
 // Peak probes (diagnostics): TFLOP/s of DMMA f64 and of DFMA.
 cudaError_t probe_peak(int what, double* tflops, cudaStream_t s);
+cudaError_t probe_dmma_occupancy(int warps, int chains, double* tflops, cudaStream_t s);
 
 }  // namespace rb

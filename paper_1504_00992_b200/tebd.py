@@ -122,27 +122,59 @@ def build_gates(site_dims, terms: dict, dt: float, plan=None):
     return plan, gates
 
 
+class PreparedGates(dict):
+    """{(sweep, bond): rrsvd_b200_gate handle} — gates resident on the device with their block
+    structure analysed once (rrsvd_b200_gate_create); reused across evolve calls."""
+
+    def __init__(self, gates: dict, ctx):
+        super().__init__()
+        self.ctx = ctx
+        self._owned = []
+        made = {}
+        for key, g in gates.items():
+            if id(g) not in made:
+                arr = np.ascontiguousarray(g, np.complex128) if isinstance(g, np.ndarray) else g
+                h = C.c_void_p()
+                ctx.check(L.lib().rrsvd_b200_gate_create(ctx.h, ptr(arr), sz(arr.shape[0]), C.byref(h)))
+                made[id(g)] = h
+                self._owned.append(h)
+            self[key] = made[id(g)]
+
+    def n_blocks(self, key) -> int:
+        n = C.c_size_t()
+        L.lib().rrsvd_b200_gate_blocks(self[key], C.byref(n))
+        return int(n.value)
+
+    def __del__(self):
+        for h in getattr(self, "_owned", []):
+            L.lib().rrsvd_b200_gate_destroy(h)
+        self._owned = []
+
+
 def evolve(mps: DeviceMps, terms: dict, dt: float, n_steps: int, backend: DecimationBackend,
            abort_discarded_threshold: float = 1.0, renormalize: bool = True, record_updates: bool = True,
            gates=None, plan=None) -> EvolveDiagnostics:
-    """rrsvd::tebd::evolve (tebd.cpp:260-326) on the device; advances backend.seed."""
+    """rrsvd::tebd::evolve (tebd.cpp:260-326) on the device; advances backend.seed.
+    `gates` may be raw matrices (prepared for this call) or a PreparedGates table."""
     if gates is None:
         plan, gates = build_gates(mps.site_dims, terms, dt, plan)
     nb = mps.n_sites - 1
     sweeps = (Sweep * len(plan))(*[Sweep(p, c) for p, c in plan])
     keep = []
     arr = (C.c_void_p * (len(plan) * nb))()
+    prepared = isinstance(gates, PreparedGates) or (len(gates) > 0 and all(
+        isinstance(v, C.c_void_p) for v in gates.values()))
     for (s, b), g in gates.items():
         keep.append(g)
-        arr[s * nb + b] = ptr(g).value
+        arr[s * nb + b] = g.value if prepared else ptr(g).value
     be = backend.to_c()
     opt = EvolveOptions(abort_discarded_threshold, int(renormalize), backend.omega_mode)
     diag = EvolveDiag()
     nrec = n_steps * sum(len(range(p, nb, 2)) for p, _ in plan) if record_updates else 0
     recs = (UpdateRecord * max(nrec, 1))()
-    mps.ctx.check(L.lib().rrsvd_b200_evolve(mps.h, sz(len(plan)), sweeps, arr, sz(n_steps), C.byref(be),
-                                            C.byref(opt), C.byref(diag), recs if record_updates else None,
-                                            sz(nrec)))
+    fn = L.lib().rrsvd_b200_evolve_prepared if prepared else L.lib().rrsvd_b200_evolve
+    mps.ctx.check(fn(mps.h, sz(len(plan)), sweeps, arr, sz(n_steps), C.byref(be), C.byref(opt), C.byref(diag),
+                     recs if record_updates else None, sz(nrec)))
     backend.seed = be.seed
     ups = [{"step": r.step, "bond": r.bond, "chi": r.chi, "discarded_weight": r.discarded_weight,
             "t_theta_us": r.t_theta_us, "t_gate_us": r.t_gate_us, "t_svd_us": r.t_svd_us,

@@ -296,3 +296,20 @@ def test_decimate_truncation_tolerance(ctx, ref):
     want = ref.decimate(theta, ll, lr, 0, 1e-6, ref.Backend(), renormalize=False)
     assert got.chi == want.chi
     assert np.max(np.abs(np.asarray(got.lam) - want.lam)) < 1e-12
+
+
+@pytest.mark.parametrize("d", [5, 20])
+def test_apply_block_structured_gate(ctx, ref, d):
+    """An excitation-number-conserving boson-boson gate (TEDOPA hopping + number terms) is
+    block-diagonal up to a permutation; the device applies it block-sparsely.  Must equal the
+    reference's dense zgemm (tebd.cpp:126-139)."""
+    from paper_1504_00992_b200 import models as Mdl
+    t0, om, hop = Mdl.ohmic_chain(4, 2001)
+    _, terms = Mdl.build_chain_terms(t0, om, hop, d, 0.5 * Mdl.SZ, Mdl.SZ)
+    gate = Mdl.bond_gate(terms[2], 0.07)
+    assert len(Mdl.sparsity_blocks(gate)) == 2 * d - 1
+    rng = np.random.default_rng(d)
+    theta = cplx_randn(rng, d, d, 6, 7)
+    got = P.apply_gate_to_theta(theta, gate, ctx=ctx)
+    want = ref.apply_gate(theta, gate)
+    assert np.max(np.abs(got - want)) < 1e-13
