@@ -361,7 +361,7 @@ def run_ours(args, rank, world, local_rank):
             "wall_ms_per_step": round(1e3 * wall / args.steps, 3),
         }
         if not args.no_cpu_baseline and world == 1:
-            line["cpu_baseline"] = cpu_baseline(args, wl, gammas, lambdas, gates, plan, samples=2)
+            line["cpu_baseline"] = cpu_baseline(args, wl, gammas, lambdas, gates_host, plan, samples=2)
         print(json.dumps(line), flush=True)
     if dist:
         dist.barrier()

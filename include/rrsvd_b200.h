@@ -118,6 +118,14 @@ int rrsvd_b200_fixed_rank(rrsvd_b200_ctx* ctx, const double* A, size_t m, size_t
                           size_t p, size_t q, uint64_t seed, int omega_mode, const double* omega,
                           double* U, double* S, double* V, double* discarded);
 
+/* `count` independent rrsvd_fixed_rank calls on same-shaped matrices, batched through every
+ * stage of the pipeline (one launch per stage for all of them).  A[i] (m x n), seeds[i]; U[i],
+ * S[i], V[i] as in rrsvd_b200_fixed_rank (U/V entries may be NULL); discarded[count]. */
+int rrsvd_b200_fixed_rank_batch(rrsvd_b200_ctx* ctx, size_t count, const double* const* A, size_t m,
+                                size_t n, size_t k, size_t p, size_t q, const uint64_t* seeds,
+                                int omega_mode, double* const* U, double* const* S,
+                                double* const* V, double* discarded);
+
 /* ---- L3: the TEBD two-site trio in the unfolded layout (tebd.hpp:98-110) ---------------
  * Unfolded two-site matrix M: (cl*d1) x (d2*cr), row a*d1+i, column j*cr+b (tebd.cpp:150-155).
  * Gamma tensors are Tensor3 (left, phys, right) row-major (mps.hpp:20-25). */

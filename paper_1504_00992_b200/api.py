@@ -171,6 +171,26 @@ def rrsvd_fixed_rank(a, k: int, p: int, q: int, seed: int, omega=None,
     return SvdResult(u, s, v, w.value, k)
 
 
+def rrsvd_fixed_rank_batch(As, k: int, p: int, q: int, seeds, mode: int = OMEGA_PHILOX,
+                           vectors: bool = False, ctx=None):
+    """Many same-shaped rrsvd_fixed_rank calls batched through every pipeline stage.
+    Returns (list of sigma arrays, discarded weights)."""
+    c = _ctx(ctx)
+    As = [_prep(a) for a in As]
+    cnt = len(As)
+    m, n = _shape(As[0])
+    S = [_empty(As[0], (k,), np.float64) for _ in range(cnt)]
+    U = [_empty(As[0], (m, k), np.complex128) for _ in range(cnt)] if vectors else None
+    V = [_empty(As[0], (n, k), np.complex128) for _ in range(cnt)] if vectors else None
+    P = C.c_void_p * cnt
+    w = (C.c_double * cnt)()
+    seeds_arr = (C.c_uint64 * cnt)(*[int(s) for s in seeds])
+    c.check(L.lib().rrsvd_b200_fixed_rank_batch(
+        c.h, sz(cnt), P(*[ptr(a) for a in As]), sz(m), sz(n), sz(k), sz(p), sz(q), seeds_arr, C.c_int(mode),
+        P(*[ptr(u) for u in U]) if U else None, P(*[ptr(s) for s in S]), P(*[ptr(v) for v in V]) if V else None, w))
+    return (S, list(w)) if not vectors else (U, S, V, list(w))
+
+
 # ------------------------------------------------------------------------ tebd.hpp
 
 @dataclass

@@ -261,6 +261,71 @@ int rrsvd_b200_fixed_rank(rrsvd_b200_ctx* c, const double* A, size_t m, size_t n
     });
 }
 
+int rrsvd_b200_fixed_rank_batch(rrsvd_b200_ctx* c, size_t count, const double* const* A, size_t m, size_t n,
+                                size_t k, size_t p, size_t q, const uint64_t* seeds, int omega_mode,
+                                double* const* U, double* const* S, double* const* V, double* discarded) {
+    return api(c, [&] {
+        if (count == 0) return;
+        if (A == nullptr || S == nullptr || seeds == nullptr) throw_contract(c, "fixed_rank_batch: null argument");
+        if (k < 2 || p < 2) throw_contract(c, "rrsvd_fixed_rank: requires k >= 2 and p >= 2");
+        if (k + p > std::min(m, n)) throw_contract(c, "rrsvd_fixed_rank: k + p exceeds min(m, n)");
+        const size_t l = k + p;
+        std::vector<RrsvdSpec> specs;
+        std::vector<cplx*> dU(count), dV(count);
+        std::vector<double*> dS(count);
+        std::vector<const cplx*> dA(count);
+        PhiloxBatch pb{};
+        for (size_t i = 0; i < count; ++i) {
+            dA[i] = static_cast<const cplx*>(stage_in(c, A[i], m * n * sizeof(cplx)));
+            cplx* om = ws_get<cplx>(c, n * l);
+            if (omega_mode == RRSVD_B200_OMEGA_PHILOX) {
+                const int t = pb.count++;
+                pb.seed[t] = seeds[i]; pb.n[t] = (long long)(n * l); pb.out[t] = om;
+                if (pb.count == kMaxEpi) {
+                    check_cuda(c, omega_philox_many(pb, c->stream), "philox_many");
+                    c->launches++;
+                    pb.count = 0;
+                }
+            } else {
+                make_omega(c, (int)n, (int)l, seeds[i], omega_mode, om);
+            }
+            dU[i] = ws_get<cplx>(c, m * l);
+            dV[i] = ws_get<cplx>(c, n * l);
+            dS[i] = ws_get<double>(c, l);
+            specs.push_back({dA[i], (int)m, (int)n, (int)l, (int)q, om, dU[i], dS[i], dV[i]});
+        }
+        if (pb.count) {
+            check_cuda(c, omega_philox_many(pb, c->stream), "philox_many");
+            c->launches++;
+        }
+        rrsvd_core_many(c, specs);
+        auto* sc = ws_get<Scalars>(c, count);
+        for (size_t base = 0; base < count; base += kMaxSmall) {
+            SumsqBatch sb{};
+            for (size_t i = base; i < std::min(count, base + kMaxSmall); ++i) {
+                const int t = sb.count++;
+                sb.a[t] = dA[i]; sb.n[t] = (long long)(m * n); sb.out_sq[t] = &sc[i].total_sq; sb.out_bad[t] = &sc[i].nonfinite;
+            }
+            double* part = ws_get<double>(c, (size_t)sb.count * 2 * kNumSMs);
+            int* bad = ws_get<int>(c, (size_t)sb.count * 2 * kNumSMs);
+            check_cuda(c, sumsq_many(sb, part, bad, c->stream), "sumsq_many");
+            c->launches += 2;
+        }
+        for (size_t i = 0; i < count; ++i) {
+            check_cuda(c, discarded_weight(dS[i], (int)k, &sc[i].total_sq, &sc[i].discarded, c->stream), "weight");
+            c->launches++;
+            if (U && U[i]) copy_out2d(c, U[i], k * sizeof(cplx), dU[i], l * sizeof(cplx), k * sizeof(cplx), m);
+            if (V && V[i]) copy_out2d(c, V[i], k * sizeof(cplx), dV[i], l * sizeof(cplx), k * sizeof(cplx), n);
+            copy_out(c, S[i], dS[i], k * sizeof(double));
+        }
+        std::vector<Scalars> h(count);
+        check_cuda(c, cudaMemcpyAsync(h.data(), sc, count * sizeof(Scalars), cudaMemcpyDeviceToHost, c->stream), "D2H");
+        check_cuda(c, cudaStreamSynchronize(c->stream), "sync");
+        if (discarded)
+            for (size_t i = 0; i < count; ++i) discarded[i] = h[i].discarded;
+    });
+}
+
 // ------------------------------------------------------------------------------------------ L3
 
 int rrsvd_b200_build_theta_unfolded(rrsvd_b200_ctx* c, const double* G1, const double* G2,

@@ -87,7 +87,7 @@ void gemm(rrsvd_b200_ctx* c, GemmOp opA, int m, int n, int k, const cplx* A, lon
 
 // ================================================================================== orth
 
-void orth_many(rrsvd_b200_ctx* c, const std::vector<OrthSpec>& specs) {
+void orth_many(rrsvd_b200_ctx* c, const std::vector<OrthSpec>& specs, int passes) {
     if (specs.empty()) return;
     struct Buf {
         cplx *G, *T, *a, *b;
@@ -104,7 +104,8 @@ void orth_many(rrsvd_b200_ctx* c, const std::vector<OrthSpec>& specs) {
     }
     std::vector<const cplx*> cur(specs.size());
     for (size_t i = 0; i < specs.size(); ++i) cur[i] = specs[i].Y;
-    for (int pass = 0; pass < 3; ++pass) {
+    const int last = passes - 1;
+    for (int pass = 0; pass < passes; ++pass) {
         std::vector<GemmSpec> gram, apply;
         for (size_t i = 0; i < specs.size(); ++i) {
             const OrthSpec& s = specs[i];
@@ -124,7 +125,7 @@ void orth_many(rrsvd_b200_ctx* c, const std::vector<OrthSpec>& specs) {
                 cb.T[k] = bufs[i].T;
                 cb.shift_scale[k] = pass == 0 ? 10.0 * (specs[i].m + specs[i].l) : 0.0;
                 cb.dep_tol[k] = pass == 0 ? 0.0 : kDepTol;
-                cb.ndead[k] = pass == 2 ? specs[i].ndead : nullptr;
+                cb.ndead[k] = pass == last ? specs[i].ndead : nullptr;
                 max_l = std::max(max_l, specs[i].l);
             }
             check_cuda(c, chol_inv(cb, max_l, c->stream), "chol_inv");
@@ -132,7 +133,7 @@ void orth_many(rrsvd_b200_ctx* c, const std::vector<OrthSpec>& specs) {
         }
         for (size_t i = 0; i < specs.size(); ++i) {
             const OrthSpec& s = specs[i];
-            cplx* dst = pass == 2 ? s.Q : (pass == 0 ? bufs[i].a : bufs[i].b);
+            cplx* dst = pass == last ? s.Q : (pass == 0 ? bufs[i].a : bufs[i].b);
             GemmSpec asp{s.m, s.l, s.l, cur[i], s.l, bufs[i].T, s.l, dst, s.l};
             asp.structure = kTriB;  // T = R^-1 is upper triangular
             apply.push_back(asp);
@@ -229,9 +230,10 @@ void rrsvd_core_many(rrsvd_b200_ctx* c, const std::vector<RrsvdSpec>& specs) {
         cplx *Y, *Q, *Z, *Qb, *X, *Xn, *Js;
     };
     std::vector<Buf> b(specs.size());
-    int max_q = 0;
+    int max_q = 0, min_q = 1 << 30;
     for (size_t i = 0; i < specs.size(); ++i) {
         const RrsvdSpec& s = specs[i];
+        min_q = std::min(min_q, s.q);
         b[i] = {ws_get<cplx>(c, (size_t)s.m * s.l), ws_get<cplx>(c, (size_t)s.m * s.l),
                 ws_get<cplx>(c, (size_t)s.n * s.l), ws_get<cplx>(c, (size_t)s.n * s.l),
                 ws_get<cplx>(c, (size_t)s.l * s.l), ws_get<cplx>(c, (size_t)s.l * s.l),
@@ -248,7 +250,11 @@ void rrsvd_core_many(rrsvd_b200_ctx* c, const std::vector<RrsvdSpec>& specs) {
     }
     c->gemm_tag = 2;
     gemm_many(c, kOpN, gs);
-    orth_many(c, os);
+    // Only the last Q (the basis B = Q^H A is built on) must be orthonormal; the intermediate
+    // bases of the power iteration carry just their span, so one shifted pass suffices there.
+    // With q = 0 this Q is the last one; a batch with mixed q keeps three passes throughout.
+    const int inter = min_q == max_q ? 1 : 3;
+    orth_many(c, os, max_q > 0 ? inter : 3);
     for (int j = 0; j < max_q; ++j) {
         gs.clear(); os.clear();
         for (size_t i = 0; i < specs.size(); ++i) {  // Z = A^H Q, QR
@@ -259,7 +265,7 @@ void rrsvd_core_many(rrsvd_b200_ctx* c, const std::vector<RrsvdSpec>& specs) {
         }
         c->gemm_tag = 2;
         gemm_many(c, kOpC, gs);
-        orth_many(c, os);
+        orth_many(c, os, inter);
         gs.clear(); os.clear();
         for (size_t i = 0; i < specs.size(); ++i) {  // Y = A Q~, QR
             const RrsvdSpec& s = specs[i];
@@ -269,7 +275,7 @@ void rrsvd_core_many(rrsvd_b200_ctx* c, const std::vector<RrsvdSpec>& specs) {
         }
         c->gemm_tag = 2;
         gemm_many(c, kOpN, gs);
-        orth_many(c, os);
+        orth_many(c, os, j + 1 < max_q ? inter : 3);
     }
     // B = Q^H A held as B^H = A^H Q = Qb X  (assemble_from_basis, randomized.cpp:57-66)
     gs.clear(); os.clear();

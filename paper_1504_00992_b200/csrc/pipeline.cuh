@@ -51,7 +51,10 @@ struct OrthSpec {
     cplx* Q;
     int* ndead = nullptr;
 };
-void orth_many(rrsvd_b200_ctx* c, const std::vector<OrthSpec>& specs);
+// passes = 3: shifted CholeskyQR3, an orthonormal basis (the reference's QR, linalg.cpp:37-58).
+// passes = 1: one shifted pass, a well-conditioned basis of the same span: enough for the
+// intermediate power-iteration bases of the range finder, whose only use is their span.
+void orth_many(rrsvd_b200_ctx* c, const std::vector<OrthSpec>& specs, int passes = 3);
 void orth(rrsvd_b200_ctx* c, const cplx* Y, int m, int l, cplx* Q, int* ndead = nullptr);
 
 // Gaussian sketch into `out` (n x l).

@@ -128,6 +128,25 @@ def test_fixed_rank_config1(ctx, ref, omega_fed):
     assert np.linalg.norm(rec - rec_r) / np.linalg.norm(rec_r) < 1e-10
 
 
+def test_fixed_rank_batch_matches_single_calls(ctx, ref):
+    """rrsvd_b200_fixed_rank_batch: each member equals the reference call with its own seed
+    (reference Ω stream), and the per-call C-ABI entry point, on the same inputs."""
+    rng = np.random.default_rng(21)
+    k, p, q = 24, 6, 2
+    mats = [c1_matrix(ref, 160)[0], cplx_randn(rng, 160, 160), c1_matrix(ref, 160)[0] * 3.0]
+    seeds = [5, 6, 7]
+    U, S, V, W = P.rrsvd_fixed_rank_batch(mats, k, p, q, seeds, mode=P.OMEGA_REFERENCE,
+                                          vectors=True, ctx=ctx)
+    for a, s, u, v, w, seed in zip(mats, S, U, V, W, seeds):
+        u_r, s_r, v_r, w_r = ref.fixed_rank(a, k, p, q, seed)
+        assert np.max(np.abs(s - s_r)) <= 1e-10 * s_r[0]
+        assert abs(w - w_r) <= 1e-10 * max(1.0, w_r)
+        one = P.rrsvd_fixed_rank(a, k, p, q, seed, ctx=ctx)
+        assert np.max(np.abs(s - one.sigma)) <= 1e-12 * s_r[0]
+        rec, rec_r = (u * s) @ v.conj().T, (u_r * s_r) @ v_r.conj().T
+        assert np.linalg.norm(rec - rec_r) / np.linalg.norm(rec_r) < 1e-9
+
+
 def test_sketched_svd_lowrank_exact(ctx):
     """test_randomized.cpp:91-101: exact low-rank input — σ recovered to 1e-10."""
     rng = np.random.default_rng(11)
