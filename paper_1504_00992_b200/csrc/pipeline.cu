@@ -87,24 +87,61 @@ void gemm(rrsvd_b200_ctx* c, GemmOp opA, int m, int n, int k, const cplx* A, lon
 
 // ================================================================================== orth
 
+// Widths beyond the single-CTA Cholesky (l > kMaxCholL) use one level of 2x2 blocking,
+//   G = [G11 G12; . G22]:  T11 = chol_inv(G11),  R12 = T11^H G12,  S = G22 - R12^H R12,
+//   T22 = chol_inv(S),  T12 = -T11 R12 T22,
+// with the shift taken from the trace of the whole G and the dependence test against G's own
+// diagonal, so it is the same factorization as the unblocked kernel (up to rounding order).
+constexpr int chol_split(int l) { return ((l + 1) / 2 + 7) / 8 * 8; }
+static_assert(chol_split(kMaxOrthL) <= kMaxCholL && kMaxOrthL - chol_split(kMaxOrthL) <= kMaxCholL,
+              "blocked halves must fit chol_inv");
+
 void orth_many(rrsvd_b200_ctx* c, const std::vector<OrthSpec>& specs, int passes) {
     if (specs.empty()) return;
     struct Buf {
         cplx *G, *T, *a, *b;
+        int l1, l2;
+        cplx *R12, *Sub, *Tn, *W;  // blocked path only
     };
     std::vector<Buf> bufs(specs.size());
+    std::vector<size_t> big;
     for (size_t i = 0; i < specs.size(); ++i) {
         const OrthSpec& s = specs[i];
-        if (s.l > kMaxCholL)
+        if (s.l > kMaxOrthL)
             throw_contract(c, "orth: sketch width l = " + std::to_string(s.l) + " exceeds the supported " +
-                                  std::to_string(kMaxCholL));
+                                  std::to_string(kMaxOrthL));
         if (s.m < s.l) throw_contract(c, "qr: requires rows >= cols");
-        bufs[i] = {ws_get<cplx>(c, (size_t)s.l * s.l), ws_get<cplx>(c, (size_t)s.l * s.l),
-                   ws_get<cplx>(c, (size_t)s.m * s.l), ws_get<cplx>(c, (size_t)s.m * s.l)};
+        Buf& b = bufs[i];
+        b = {ws_get<cplx>(c, (size_t)s.l * s.l), ws_get<cplx>(c, (size_t)s.l * s.l),
+             ws_get<cplx>(c, (size_t)s.m * s.l), ws_get<cplx>(c, (size_t)s.m * s.l), s.l, 0,
+             nullptr, nullptr, nullptr, nullptr};
+        if (s.l > kMaxCholL) {
+            b.l1 = chol_split(s.l);
+            b.l2 = s.l - b.l1;
+            b.R12 = ws_get<cplx>(c, (size_t)b.l1 * b.l2);
+            b.Sub = ws_get<cplx>(c, (size_t)b.l2 * b.l2);
+            b.Tn = ws_get<cplx>(c, (size_t)b.l2 * s.l);  // written with the same ld as T
+            b.W = ws_get<cplx>(c, (size_t)b.l1 * b.l2);
+            // T21 stays zero for every pass
+            check_cuda(c, cudaMemset2DAsync(b.T + (size_t)b.l1 * s.l, s.l * sizeof(cplx), 0, b.l1 * sizeof(cplx),
+                                            b.l2, c->stream), "memset");
+            big.push_back(i);
+        }
     }
     std::vector<const cplx*> cur(specs.size());
     for (size_t i = 0; i < specs.size(); ++i) cur[i] = specs[i].Y;
+    // Schedule: up to two shifted passes, then plain ones.
+    // The second shifted pass bounds cond(Q) even for rank-deficient Y (whose first-pass basis
+    // keeps roundoff-level directions at ~1e-10), so the plain passes never meet a numerically
+    // indefinite Gram matrix and no live direction is ever dropped — only exactly vanishing
+    // pivots mark a dependent (zero) column, as Householder QR keeps tiny directions too.
     const int last = passes - 1;
+    const int shifted = std::min(passes, 2);
+    auto chol_launch = [&](CholBatch& cb, int max_l) {
+        check_cuda(c, chol_inv(cb, max_l, c->stream), "chol_inv");
+        c->launches++;
+        cb = CholBatch{};
+    };
     for (int pass = 0; pass < passes; ++pass) {
         std::vector<GemmSpec> gram, apply;
         for (size_t i = 0; i < specs.size(); ++i) {
@@ -115,21 +152,78 @@ void orth_many(rrsvd_b200_ctx* c, const std::vector<OrthSpec>& specs, int passes
         }
         c->gemm_tag = 3;
         gemm_many(c, kOpC, gram);
-        for (size_t base = 0; base < specs.size(); base += kMaxSmall) {
-            CholBatch cb{};
-            int max_l = 0;
-            for (size_t i = base; i < std::min(specs.size(), base + kMaxSmall); ++i) {
-                const int k = cb.count++;
-                cb.l[k] = specs[i].l;
-                cb.G[k] = bufs[i].G;
-                cb.T[k] = bufs[i].T;
-                cb.shift_scale[k] = pass == 0 ? 10.0 * (specs[i].m + specs[i].l) : 0.0;
-                cb.dep_tol[k] = pass == 0 ? 0.0 : kDepTol;
-                cb.ndead[k] = pass == last ? specs[i].ndead : nullptr;
-                max_l = std::max(max_l, specs[i].l);
+        // leading diagonal block (or the whole G when l <= kMaxCholL)
+        CholBatch cb{};
+        int max_l = 0;
+        for (size_t i = 0; i < specs.size(); ++i) {
+            const OrthSpec& s = specs[i];
+            const Buf& b = bufs[i];
+            const int k = cb.count++;
+            cb.l[k] = b.l1;
+            cb.G[k] = b.G;
+            cb.ldg[k] = s.l;
+            cb.trace_src[k] = b.G; cb.trace_n[k] = s.l; cb.trace_ld[k] = s.l;
+            cb.T[k] = b.T;
+            cb.ldt[k] = s.l;
+            cb.shift_scale[k] = pass < shifted ? 10.0 * (s.m + s.l) : 0.0;
+            cb.dep_tol[k] = 0.0;
+            cb.ndead[k] = pass == last ? s.ndead : nullptr;
+            max_l = std::max(max_l, b.l1);
+            if (cb.count == kMaxSmall) { chol_launch(cb, max_l); max_l = 0; }
+        }
+        if (cb.count) chol_launch(cb, max_l);
+        if (!big.empty()) {
+            std::vector<GemmSpec> g1, g2;
+            for (size_t i : big) {  // R12 = T11^H G12
+                const Buf& b = bufs[i];
+                const int l = specs[i].l;
+                g1.push_back({b.l1, b.l2, b.l1, b.T, l, b.G + b.l1, l, b.R12, b.l2});
             }
-            check_cuda(c, chol_inv(cb, max_l, c->stream), "chol_inv");
-            c->launches++;
+            c->gemm_tag = 3;
+            gemm_many(c, kOpC, g1);
+            for (size_t i : big) {  // Sub = R12^H R12 (upper triangle)
+                const Buf& b = bufs[i];
+                GemmSpec gs{b.l2, b.l2, b.l1, b.R12, b.l2, b.R12, b.l2, b.Sub, b.l2};
+                gs.structure = kUpperC;
+                g2.push_back(gs);
+            }
+            gemm_many(c, kOpC, g2);
+            max_l = 0;
+            for (size_t i : big) {  // trailing block: T22 = chol_inv(G22 - Sub), also -T22
+                const OrthSpec& s = specs[i];
+                const Buf& b = bufs[i];
+                const int k = cb.count++;
+                const size_t off = (size_t)b.l1 * s.l + b.l1;
+                cb.l[k] = b.l2;
+                cb.G[k] = b.G + off;
+                cb.ldg[k] = s.l;
+                cb.Gsub[k] = b.Sub;
+                cb.trace_src[k] = b.G; cb.trace_n[k] = s.l; cb.trace_ld[k] = s.l;
+                cb.T[k] = b.T + off;
+                cb.ldt[k] = s.l;
+                cb.Tneg[k] = b.Tn;
+                cb.shift_scale[k] = pass < shifted ? 10.0 * (s.m + s.l) : 0.0;
+                cb.dep_tol[k] = 0.0;
+                cb.ndead[k] = pass == last ? s.ndead : nullptr;
+                cb.ndead_acc[k] = 1;
+                max_l = std::max(max_l, b.l2);
+                if (cb.count == kMaxSmall) { chol_launch(cb, max_l); max_l = 0; }
+            }
+            if (cb.count) chol_launch(cb, max_l);
+            g1.clear(); g2.clear();
+            for (size_t i : big) {  // W = T11 R12
+                const Buf& b = bufs[i];
+                g1.push_back({b.l1, b.l2, b.l1, b.T, specs[i].l, b.R12, b.l2, b.W, b.l2});
+            }
+            c->gemm_tag = 4;
+            gemm_many(c, kOpN, g1);
+            for (size_t i : big) {  // T12 = W (-T22)
+                const Buf& b = bufs[i];
+                GemmSpec gs{b.l1, b.l2, b.l2, b.W, b.l2, b.Tn, specs[i].l, b.T + b.l1, specs[i].l};
+                gs.structure = kTriB;
+                g2.push_back(gs);
+            }
+            gemm_many(c, kOpN, g2);
         }
         for (size_t i = 0; i < specs.size(); ++i) {
             const OrthSpec& s = specs[i];
@@ -251,10 +345,13 @@ void rrsvd_core_many(rrsvd_b200_ctx* c, const std::vector<RrsvdSpec>& specs) {
     c->gemm_tag = 2;
     gemm_many(c, kOpN, gs);
     // Only the last Q (the basis B = Q^H A is built on) must be orthonormal; the intermediate
-    // bases of the power iteration carry just their span, so one shifted pass suffices there.
-    // With q = 0 this Q is the last one; a batch with mixed q keeps three passes throughout.
-    const int inter = min_q == max_q ? 1 : 3;
-    orth_many(c, os, max_q > 0 ? inter : 3);
+    // bases of the power iteration carry just their span, so they stop after the two shifted
+    // passes (cond <= ~1e5 even for rank-deficient input; one shifted pass is NOT enough: it
+    // leaves directions below ~1e-7·σ1 attenuated by σ/sqrt(shift), and the next product with
+    // A pushes them under roundoff).  With q = 0 this Q is the last one; a batch with mixed q
+    // keeps full passes throughout.
+    const int inter = min_q == max_q ? kSpanPasses : kFullPasses;
+    orth_many(c, os, max_q > 0 ? inter : kFullPasses);
     for (int j = 0; j < max_q; ++j) {
         gs.clear(); os.clear();
         for (size_t i = 0; i < specs.size(); ++i) {  // Z = A^H Q, QR
@@ -275,7 +372,7 @@ void rrsvd_core_many(rrsvd_b200_ctx* c, const std::vector<RrsvdSpec>& specs) {
         }
         c->gemm_tag = 2;
         gemm_many(c, kOpN, gs);
-        orth_many(c, os, j + 1 < max_q ? inter : 3);
+        orth_many(c, os, j + 1 < max_q ? inter : kFullPasses);
     }
     // B = Q^H A held as B^H = A^H Q = Qb X  (assemble_from_basis, randomized.cpp:57-66)
     gs.clear(); os.clear();
@@ -333,7 +430,7 @@ void svd_jacobi_many(rrsvd_b200_ctx* c, const std::vector<SvdSpec>& specs) {
     for (const SvdSpec& s : specs) {
         const bool tall = s.m >= s.n;
         const int r = tall ? s.m : s.n, cc = tall ? s.n : s.m;
-        if (cc > kMaxCholL) {
+        if (cc > kMaxOrthL || !jacobi_fits(cc, cc)) {
             // Unpreconditioned one-sided Jacobi (converges, in more sweeps).
             // tall: X = A, X J = U S -> U = Xn, V = J.   wide: X = A^H -> V = Xn, U = J.
             direct.push_back({s.A, r, cc, tall ? 0 : 1, s.n, s.sigma, tall ? s.U : s.V, tall ? s.V : s.U});

@@ -51,10 +51,13 @@ struct OrthSpec {
     cplx* Q;
     int* ndead = nullptr;
 };
-// passes = 3: shifted CholeskyQR3, an orthonormal basis (the reference's QR, linalg.cpp:37-58).
-// passes = 1: one shifted pass, a well-conditioned basis of the same span: enough for the
-// intermediate power-iteration bases of the range finder, whose only use is their span.
-void orth_many(rrsvd_b200_ctx* c, const std::vector<OrthSpec>& specs, int passes = 3);
+// passes = kFullPasses: two shifted CholeskyQR passes then two plain ones — an orthonormal
+// basis of the full span (the reference's Householder QR, linalg.cpp:49-65, keeps every live
+// direction too).  passes = kSpanPasses: the two shifted passes only — a well-conditioned basis
+// of the same span (cond <= ~1e5), enough for the intermediate power-iteration bases.
+constexpr int kFullPasses = 4;
+constexpr int kSpanPasses = 2;
+void orth_many(rrsvd_b200_ctx* c, const std::vector<OrthSpec>& specs, int passes = kFullPasses);
 void orth(rrsvd_b200_ctx* c, const cplx* Y, int m, int l, cplx* Q, int* ndead = nullptr);
 
 // Gaussian sketch into `out` (n x l).

@@ -31,21 +31,33 @@ __global__ void __launch_bounds__(CHOL_THREADS) chol_inv_kernel(const __grid_con
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = CHOL_THREADS / 32;
     const cplx* G = b.G[p];
+    const long long ldg = b.ldg[p] > 0 ? b.ldg[p] : l;
+    const cplx* Gs = b.Gsub[p];
 
-    for (int i = warp; i < l; i += nw)
-        for (int k = i + lane; k < l; k += 32) P[poff(i, l) + k - i] = G[(long long)i * l + k];
-    __syncthreads();
-    if (tid == 0) {
+    if (warp == 0) {  // shift from the trace of the whole Gram matrix (also for a trailing block)
+        const cplx* ts = b.trace_src[p] ? b.trace_src[p] : G;
+        const int tn = b.trace_src[p] ? b.trace_n[p] : l;
+        const long long tld = (b.trace_src[p] ? (long long)b.trace_ld[p] : ldg) + 1;
         double tr = 0.0;
-        for (int i = 0; i < l; ++i) tr += P[poff(i, l)].x;
-        s_shift = b.shift_scale[p] * kU * tr;
+        for (int i = lane; i < tn; i += 32) tr += ts[i * tld].x;
+        tr = warp_sum(tr);
+        if (lane == 0) s_shift = b.shift_scale[p] * kU * tr;
     }
     __syncthreads();
-    for (int i = tid; i < l; i += CHOL_THREADS) {
-        P[poff(i, l)].x += s_shift;
-        P[poff(i, l)].y = 0.0;
-        g0[i] = P[poff(i, l)].x;
-    }
+    for (int i = warp; i < l; i += nw)
+        for (int k = i + lane; k < l; k += 32) {
+            cplx v = G[(long long)i * ldg + k];
+            if (k == i) {
+                v = mk(v.x + s_shift, 0.0);
+                g0[i] = v.x;  // dependence is judged against the pivot's original diagonal
+            }
+            if (Gs != nullptr) {
+                const cplx w = Gs[(long long)i * l + k];
+                v.x -= w.x;
+                v.y -= (k == i) ? 0.0 : w.y;
+            }
+            P[poff(i, l) + k - i] = v;
+        }
     __syncthreads();
 
     // ---- right-looking Cholesky, G = R^H R, R upper, row j of R overwrites row j of G.
@@ -114,13 +126,19 @@ __global__ void __launch_bounds__(CHOL_THREADS) chol_inv_kernel(const __grid_con
     }
 
     cplx* T = b.T[p];
+    cplx* Tn = b.Tneg[p];
+    const long long ldt = b.ldt[p] > 0 ? b.ldt[p] : l;
     for (int i = warp; i < l; i += nw)
-        for (int k = lane; k < l; k += 32)
-            T[(long long)i * l + k] = (k >= i) ? P[poff(i, l) + k - i] : mk(0.0, 0.0);
+        for (int k = lane; k < l; k += 32) {
+            const cplx v = (k >= i) ? P[poff(i, l) + k - i] : mk(0.0, 0.0);
+            T[(long long)i * ldt + k] = v;
+            if (Tn != nullptr) Tn[(long long)i * ldt + k] = mk(-v.x, -v.y);
+        }
     if (b.ndead[p] != nullptr && tid == 0) {
         int n = 0;
         for (int j = 0; j < l; ++j) n += dead[j];
-        *b.ndead[p] = n;
+        if (b.ndead_acc[p]) *b.ndead[p] += n;
+        else *b.ndead[p] = n;
     }
 }
 
@@ -385,18 +403,22 @@ cudaError_t jacobi_init(const JacobiInitBatch& b, cudaStream_t s) {
 
 // Chooses the cluster size (8 portable, else 16 non-portable) so that a CTA's block pair fits
 // in shared memory; returns cudaErrorInvalidValue if even 16 CTAs cannot hold it.
+namespace {
+constexpr size_t kJacBudget = 200 * 1024;
+size_t jacobi_need(int r, int c, int csz) {
+    const int bs = (c + 2 * csz - 1) / (2 * csz);
+    return (size_t)2 * bs * (r + c) * sizeof(cplx);
+}
+}  // namespace
+
+bool jacobi_fits(int r, int c) { return jacobi_need(r, c, 16) <= kJacBudget; }
+
 cudaError_t jacobi_svd(const JacobiBatch& b, int max_r, int max_c, cudaStream_t s) {
     if (b.count == 0) return cudaSuccess;
-    const int ld = max_r + max_c;
     int cs = 8;
-    auto need = [&](int csz) {
-        const int bs = (max_c + 2 * csz - 1) / (2 * csz);
-        return (size_t)2 * bs * ld * sizeof(cplx);
-    };
-    const size_t kBudget = 200 * 1024;
-    if (need(8) > kBudget) cs = 16;
-    if (need(cs) > kBudget) return cudaErrorInvalidValue;
-    const size_t smem = need(cs);
+    if (jacobi_need(max_r, max_c, 8) > kJacBudget) cs = 16;
+    if (jacobi_need(max_r, max_c, cs) > kJacBudget) return cudaErrorInvalidValue;
+    const size_t smem = jacobi_need(max_r, max_c, cs);
     cudaError_t e = cudaFuncSetAttribute(jacobi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     if (cs > 8) {

@@ -11,22 +11,32 @@ constexpr int kMaxSmall = 64;  // problems per launch of the small-matrix kernel
 // Columns whose Cholesky pivot falls to <= dep_tol * (original diagonal) (or to <= 0) are
 // numerically dependent: their T column is zeroed, so the orthonormalised basis gets a zero
 // column (the reference's Householder QR returns an arbitrary orthonormal completion there,
-// linalg.hpp:35-37; either way no NaN and an unchanged span).  The shifted first pass uses
-// dep_tol = 0 (its pivots are >= the shift, so only exactly-zero columns die — anything else
-// would discard genuine small-σ directions); the refinement passes use kDepTol.
-constexpr double kDepTol = 1e-14;
+// linalg.hpp:35-37; either way no NaN and an unchanged span).  The orthonormalisation
+// schedule (pipeline.cu orth_many) keeps the Gram matrices of its plain passes well
+// conditioned, so it runs with dep_tol = 0: only non-positive pivots (exactly vanishing
+// columns) die, and no genuine small-σ direction is discarded.
 constexpr int kMaxCholL = 168;  // packed upper triangle must fit in 227 KB of shared memory
+constexpr int kMaxOrthL = 2 * kMaxCholL - 8;  // one level of 2x2 blocking (pipeline.cu orth_many)
 
 struct CholBatch {
     int count;
     int l[kMaxSmall];
     const cplx* G[kMaxSmall];
+    int ldg[kMaxSmall];               // 0: l
+    const cplx* Gsub[kMaxSmall];      // nullable: factor G - Gsub instead (Gsub l x l, ld l)
+    const cplx* trace_src[kMaxSmall]; // nullable: the shift's trace is taken over this matrix's
+    int trace_n[kMaxSmall];           //   first trace_n diagonal entries (ld trace_ld) instead of G
+    int trace_ld[kMaxSmall];
     cplx* T[kMaxSmall];
-    double shift_scale[kMaxSmall];  // 0: no shift; else s = shift_scale * u * trace(G)
-    double dep_tol[kMaxSmall];      // relative pivot floor for "dependent"
-    int* ndead[kMaxSmall];          // nullable: number of dependent columns found
+    int ldt[kMaxSmall];               // 0: l
+    cplx* Tneg[kMaxSmall];            // nullable: also write -T (ld ldt)
+    double shift_scale[kMaxSmall];    // 0: no shift; else s = shift_scale * u * trace
+    double dep_tol[kMaxSmall];        // relative pivot floor for "dependent"
+    int* ndead[kMaxSmall];            // nullable: number of dependent columns found
+    int ndead_acc[kMaxSmall];         // 1: add to *ndead instead of storing
 };
 cudaError_t chol_inv(const CholBatch& b, int max_l, cudaStream_t s);
+bool jacobi_fits(int r, int c);  // an r x c problem fits jacobi_svd's on-chip capacity
 
 // ---- One-sided (Hestenes) Jacobi SVD ------------------------------------------------------
 // Works on W (column-major, ld = r + c): rows [0, r) hold X (r x c), rows [r, r + c) hold the

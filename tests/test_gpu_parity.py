@@ -45,9 +45,11 @@ def test_philox_sketch_statistics(ctx):
 
 # ------------------------------------------------------------------ QR / SVD (linalg.cpp)
 
-@pytest.mark.parametrize("m,n", [(40, 40), (300, 74), (2000, 110), (1000, 168)])
+@pytest.mark.parametrize("m,n", [(40, 40), (300, 74), (2000, 110), (1000, 168), (1000, 169), (2000, 200),
+                                 (300, 256), (700, 328)])
 def test_qr_orthonormal_and_reconstructs(ctx, m, n):
-    """test_linalg.cpp:114-121: orthonormality and reconstruction < 1e-12."""
+    """test_linalg.cpp:114-121: orthonormality and reconstruction < 1e-12.  Widths above 168
+    go through the 2x2-blocked Cholesky (one level, up to 328)."""
     rng = np.random.default_rng(m + n)
     a = cplx_randn(rng, m, n)
     q, r = P.qr(a, ctx=ctx)
@@ -69,10 +71,11 @@ def test_qr_zero_and_dependent_columns_no_nan(ctx):
     assert np.linalg.norm(ql.conj().T @ ql - np.eye(ql.shape[1])) < 1e-12
 
 
-def test_qr_ill_conditioned(ctx):
+@pytest.mark.parametrize("l", [90, 200])
+def test_qr_ill_conditioned(ctx, l):
     """TEBD spectra decay fast: cond(Y) up to 1e16 must not break the orthonormalisation."""
     rng = np.random.default_rng(5)
-    m, l = 1500, 90
+    m = 1500
     uq, _ = np.linalg.qr(cplx_randn(rng, m, l))
     vq, _ = np.linalg.qr(cplx_randn(rng, l, l))
     for dec in (1e-8, 1e-14, 1e-20):
@@ -84,7 +87,7 @@ def test_qr_ill_conditioned(ctx):
         assert np.linalg.norm(y - q @ (q.conj().T @ y), 2) < 1e-11
 
 
-@pytest.mark.parametrize("m,n", [(30, 30), (96, 64), (64, 96), (256, 256), (600, 120)])
+@pytest.mark.parametrize("m,n", [(30, 30), (96, 64), (64, 96), (256, 256), (600, 120), (400, 240), (200, 288)])
 def test_svd_full_matches_reference(ctx, ref, m, n):
     """svd_full (linalg.cpp:67-88) — test_linalg.cpp:184-194 reconstruction 1e-10."""
     rng = np.random.default_rng(m * n)
@@ -96,7 +99,7 @@ def test_svd_full_matches_reference(ctx, ref, m, n):
     u, s, v = P.svd_full(a, ctx=ctx)
     _, s_ref, _ = ref.svd_full(a)
     assert np.all(np.diff(s) <= 0)
-    # 1e-12·σ1: 100x inside the 1e-10 parity bar (c > 168 uses unpreconditioned Jacobi)
+    # 1e-12·σ1: 100x inside the 1e-10 parity bar
     assert np.max(np.abs(s - s_ref)) <= 1e-12 * s_ref[0]
     assert np.linalg.norm((u * s) @ v.conj().T - a) / np.linalg.norm(a) < 1e-12
     assert np.linalg.norm(u.conj().T @ u - np.eye(r)) < 1e-11
@@ -123,6 +126,21 @@ def test_fixed_rank_config1(ctx, ref, omega_fed):
     assert np.max(np.abs(res.sigma - s_r) / s_r) < 1e-10
     assert abs(res.discarded_weight - w_r) < 1e-12
     # gauge-invariant: rank-k reconstruction
+    rec = (res.u * res.sigma) @ res.v.conj().T
+    rec_r = (u_r * s_r) @ v_r.conj().T
+    assert np.linalg.norm(rec - rec_r) / np.linalg.norm(rec_r) < 1e-10
+
+
+@pytest.mark.parametrize("n", [900, 1600])
+def test_fixed_rank_paper_k100_p100(ctx, ref, n):
+    """The paper's own benchmark setting: k = p = 100 (l = 200), q = 2,
+    exponentially decaying spectrum (as bench_rrsvd.cpp:11-12); σ within 1e-10 relative."""
+    sigma = 0.95 ** np.arange(n)
+    a = ref.structured_matrix(sigma, n, n, n + 1)
+    res = P.rrsvd_fixed_rank(a, 100, 100, 2, 5, ctx=ctx)
+    u_r, s_r, v_r, w_r = ref.fixed_rank(a, 100, 100, 2, 5)
+    assert np.max(np.abs(res.sigma - s_r) / s_r) < 1e-10
+    assert abs(res.discarded_weight - w_r) < 1e-12
     rec = (res.u * res.sigma) @ res.v.conj().T
     rec_r = (u_r * s_r) @ v_r.conj().T
     assert np.linalg.norm(rec - rec_r) / np.linalg.norm(rec_r) < 1e-10
@@ -242,6 +260,13 @@ DEC_CASES = [
     (40, 4, 40, 4, 40, 40, True, 0, 40, 10),
     (20, 20, 25, 20, 30, 20, True, 256, 20, 10),
     (8, 3, 12, 3, 10, 0, False, 256, 0, 0),
+    # C2 shape (d=2, chi=128, n=256): reference defaults take the deterministic path; forced
+    # RRSVD with p = k gives the full-width sketch l = 256 (blocked CholeskyQR).  λ decay 0.85
+    # keeps the spectrum above the 1e-15 floor, so χ is set by chi_max (see the tail test below)
+    (128, 2, 128, 2, 128, 128, True, 256, 128, 128, 0.85),
+    (128, 2, 128, 2, 128, 128, True, 0, 128, 128, 0.85),
+    # C3 shape with p = 100 (l = 200)
+    (100, 20, 100, 20, 100, 100, True, 256, 100, 100, 0.85),
 ]
 
 
@@ -250,9 +275,9 @@ def test_decimate_matches_reference(ctx, ref, case):
     """decimate (tebd.cpp:141-237) vs the reference on the same Θ and seed (reference Ω
     stream regenerated on the device): λ within 1e-10, w within 1e-10, same χ and path,
     gauge-invariant Θ reconstruction within 1e-9."""
-    cl, d1, cm, d2, cr, chi, rnd, cross, k, p = case
+    cl, d1, cm, d2, cr, chi, rnd, cross, k, p = case[:10]
     rng = np.random.default_rng(cl * 7 + cr)
-    g1, g2, ll, lm, lr = random_fragment(rng, cl, d1, cm, d2, cr, decay=0.6)
+    g1, g2, ll, lm, lr = random_fragment(rng, cl, d1, cm, d2, cr, decay=case[10] if len(case) > 10 else 0.6)
     gate, _ = np.linalg.qr(cplx_randn(rng, d1 * d2, d1 * d2))
     theta = ref.apply_gate(ref.build_theta(g1, g2, ll, lm, lr), gate)
     be = P.DecimationBackend(randomized=rnd, target_rank=k, oversampling=p, power_iterations=2,
@@ -269,6 +294,29 @@ def test_decimate_matches_reference(ctx, ref, case):
     rec_g = theta_from(got, ll, lr)
     rec_r = theta_from(want, ll, lr)
     assert np.linalg.norm(rec_g - rec_r) / np.linalg.norm(rec_r) < 1e-9
+
+
+def test_decimate_deep_tail_deterministic(ctx, ref):
+    """C2-shaped Θ whose spectrum falls through the 1e-15·σ1 floor (tebd.cpp:191) inside χ_max:
+    every σ the reference resolves above 1e-13·σ1 agrees to 1e-10·σ1, the kept counts differ only
+    by values within a few ulps of the floor (σ at 1e-15·σ1 carries ~u·σ1 absolute error in any
+    SVD, the reference's included), and the discarded weights agree to 1e-12."""
+    rng = np.random.default_rng(128 * 7 + 128)
+    g1, g2, ll, lm, lr = random_fragment(rng, 128, 2, 128, 2, 128, decay=0.6)
+    gate, _ = np.linalg.qr(cplx_randn(rng, 4, 4))
+    theta = ref.apply_gate(ref.build_theta(g1, g2, ll, lm, lr), gate)
+    be = P.DecimationBackend(randomized=True, target_rank=128, oversampling=128, det_crossover=256, seed=3)
+    rbe = ref.Backend(randomized=True, target_rank=128, oversampling=128, det_crossover=256, seed=3)
+    got = P.decimate(theta, ll, lr, 128, 0.0, be, ctx=ctx)
+    want = ref.decimate(theta, ll, lr, 128, 0.0, rbe)
+    assert not got.randomized_path and not want.randomized_path
+    _, s_ref, _ = ref.svd_full(unfold(theta))
+    lo, hi = sorted((got.chi, want.chi))
+    assert np.all(np.abs(s_ref[lo:hi] / s_ref[0] - 1e-15) < 1e-16), (got.chi, want.chi)
+    n = min(got.chi, want.chi)
+    big = want.lam[:n] > 1e-13 * want.lam[0]
+    assert np.max(np.abs(np.asarray(got.lam)[:n][big] - want.lam[:n][big])) < 1e-10
+    assert abs(got.discarded - want.discarded) < 1e-12
 
 
 def test_decimate_bell_pair(ctx):
