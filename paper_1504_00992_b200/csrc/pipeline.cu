@@ -50,6 +50,7 @@ void gemm_many(rrsvd_b200_ctx* c, GemmOp opA, const std::vector<GemmSpec>& specs
             P.nsub = s.nsub;
             P.subB = s.subB;
             P.subC = s.subC;
+            P.D = s.D; P.ldd = s.ldd; P.alpha = s.alpha;
             int split = 1;
             if (total < target && s.k > 128) {
                 split = (int)std::min<long long>((target + total - 1) / total, (s.k + 63) / 64);
@@ -87,45 +88,53 @@ void gemm(rrsvd_b200_ctx* c, GemmOp opA, int m, int n, int k, const cplx* A, lon
 
 // ================================================================================== orth
 
-// Widths beyond the single-CTA Cholesky (l > kMaxCholL) use one level of 2x2 blocking,
-//   G = [G11 G12; . G22]:  T11 = chol_inv(G11),  R12 = T11^H G12,  S = G22 - R12^H R12,
-//   T22 = chol_inv(S),  T12 = -T11 R12 T22,
-// with the shift taken from the trace of the whole G and the dependence test against G's own
-// diagonal, so it is the same factorization as the unblocked kernel (up to rounding order).
-constexpr int chol_split(int l) { return ((l + 1) / 2 + 7) / 8 * 8; }
-static_assert(chol_split(kMaxOrthL) <= kMaxCholL && kMaxOrthL - chol_split(kMaxOrthL) <= kMaxCholL,
-              "blocked halves must fit chol_inv");
+// Widths beyond the single-CTA Cholesky (l > kMaxCholL) are blocked: nbk diagonal blocks of
+// width <= kMaxCholL, right-looking over the Gram matrix (updated in place),
+//   T_JJ = chol_inv(G_JJ),  R_J,>J = T_JJ^H G_J,>J,  G_>J,>J -= R_J,>J^H R_J,>J,
+// then the inverse's off-diagonal blocks bottom-up,  T_I,>I = -T_II (R_I,>I T_>I,>I).
+// The shift is taken once from the trace of the whole (unmodified) G by block 0, so this is
+// the same factorization as the unblocked kernel up to rounding order.
+struct CholBlocking {
+    int nbk = 1, bsz = 0;
+    int begin(int J) const { return J * bsz; }
+    int width(int J, int l) const { return std::min(bsz, l - J * bsz); }
+};
+CholBlocking chol_blocking(int l) {
+    CholBlocking cbk;
+    cbk.nbk = (l + kMaxCholL - 1) / kMaxCholL;
+    cbk.bsz = ((l + cbk.nbk - 1) / cbk.nbk + 7) / 8 * 8;
+    cbk.nbk = (l + cbk.bsz - 1) / cbk.bsz;
+    return cbk;
+}
 
 void orth_many(rrsvd_b200_ctx* c, const std::vector<OrthSpec>& specs, int passes) {
     if (specs.empty()) return;
     struct Buf {
         cplx *G, *T, *a, *b;
-        int l1, l2;
-        cplx *R12, *Sub, *Tn, *W;  // blocked path only
+        CholBlocking blk;
+        cplx *R, *W;      // blocked path only
+        double* shift;
     };
     std::vector<Buf> bufs(specs.size());
-    std::vector<size_t> big;
+    int max_nbk = 1;
     for (size_t i = 0; i < specs.size(); ++i) {
         const OrthSpec& s = specs[i];
-        if (s.l > kMaxOrthL)
-            throw_contract(c, "orth: sketch width l = " + std::to_string(s.l) + " exceeds the supported " +
-                                  std::to_string(kMaxOrthL));
         if (s.m < s.l) throw_contract(c, "qr: requires rows >= cols");
         Buf& b = bufs[i];
-        b = {ws_get<cplx>(c, (size_t)s.l * s.l), ws_get<cplx>(c, (size_t)s.l * s.l),
-             ws_get<cplx>(c, (size_t)s.m * s.l), ws_get<cplx>(c, (size_t)s.m * s.l), s.l, 0,
-             nullptr, nullptr, nullptr, nullptr};
-        if (s.l > kMaxCholL) {
-            b.l1 = chol_split(s.l);
-            b.l2 = s.l - b.l1;
-            b.R12 = ws_get<cplx>(c, (size_t)b.l1 * b.l2);
-            b.Sub = ws_get<cplx>(c, (size_t)b.l2 * b.l2);
-            b.Tn = ws_get<cplx>(c, (size_t)b.l2 * s.l);  // written with the same ld as T
-            b.W = ws_get<cplx>(c, (size_t)b.l1 * b.l2);
-            // T21 stays zero for every pass
-            check_cuda(c, cudaMemset2DAsync(b.T + (size_t)b.l1 * s.l, s.l * sizeof(cplx), 0, b.l1 * sizeof(cplx),
-                                            b.l2, c->stream), "memset");
-            big.push_back(i);
+        b.G = ws_get<cplx>(c, (size_t)s.l * s.l);
+        b.T = ws_get<cplx>(c, (size_t)s.l * s.l);
+        b.a = ws_get<cplx>(c, (size_t)s.m * s.l);
+        b.b = ws_get<cplx>(c, (size_t)s.m * s.l);
+        b.blk = chol_blocking(s.l);
+        b.R = b.W = nullptr;
+        b.shift = nullptr;
+        if (b.blk.nbk > 1) {
+            b.R = ws_get<cplx>(c, (size_t)s.l * s.l);
+            b.W = ws_get<cplx>(c, (size_t)b.blk.bsz * s.l);
+            b.shift = ws_get<double>(c, 1);
+            // the strictly lower blocks of T stay zero for every pass
+            check_cuda(c, cudaMemsetAsync(b.T, 0, (size_t)s.l * s.l * sizeof(cplx), c->stream), "memset");
+            max_nbk = std::max(max_nbk, b.blk.nbk);
         }
     }
     std::vector<const cplx*> cur(specs.size());
@@ -142,6 +151,7 @@ void orth_many(rrsvd_b200_ctx* c, const std::vector<OrthSpec>& specs, int passes
         c->launches++;
         cb = CholBatch{};
     };
+    auto off = [](int l, int r0, int c0) { return (size_t)r0 * l + c0; };
     for (int pass = 0; pass < passes; ++pass) {
         std::vector<GemmSpec> gram, apply;
         for (size_t i = 0; i < specs.size(); ++i) {
@@ -152,78 +162,78 @@ void orth_many(rrsvd_b200_ctx* c, const std::vector<OrthSpec>& specs, int passes
         }
         c->gemm_tag = 3;
         gemm_many(c, kOpC, gram);
-        // leading diagonal block (or the whole G when l <= kMaxCholL)
-        CholBatch cb{};
-        int max_l = 0;
-        for (size_t i = 0; i < specs.size(); ++i) {
-            const OrthSpec& s = specs[i];
-            const Buf& b = bufs[i];
-            const int k = cb.count++;
-            cb.l[k] = b.l1;
-            cb.G[k] = b.G;
-            cb.ldg[k] = s.l;
-            cb.trace_src[k] = b.G; cb.trace_n[k] = s.l; cb.trace_ld[k] = s.l;
-            cb.T[k] = b.T;
-            cb.ldt[k] = s.l;
-            cb.shift_scale[k] = pass < shifted ? 10.0 * (s.m + s.l) : 0.0;
-            cb.dep_tol[k] = 0.0;
-            cb.ndead[k] = pass == last ? s.ndead : nullptr;
-            max_l = std::max(max_l, b.l1);
-            if (cb.count == kMaxSmall) { chol_launch(cb, max_l); max_l = 0; }
-        }
-        if (cb.count) chol_launch(cb, max_l);
-        if (!big.empty()) {
-            std::vector<GemmSpec> g1, g2;
-            for (size_t i : big) {  // R12 = T11^H G12
-                const Buf& b = bufs[i];
-                const int l = specs[i].l;
-                g1.push_back({b.l1, b.l2, b.l1, b.T, l, b.G + b.l1, l, b.R12, b.l2});
-            }
-            c->gemm_tag = 3;
-            gemm_many(c, kOpC, g1);
-            for (size_t i : big) {  // Sub = R12^H R12 (upper triangle)
-                const Buf& b = bufs[i];
-                GemmSpec gs{b.l2, b.l2, b.l1, b.R12, b.l2, b.R12, b.l2, b.Sub, b.l2};
-                gs.structure = kUpperC;
-                g2.push_back(gs);
-            }
-            gemm_many(c, kOpC, g2);
-            max_l = 0;
-            for (size_t i : big) {  // trailing block: T22 = chol_inv(G22 - Sub), also -T22
+        for (int J = 0; J < max_nbk; ++J) {
+            CholBatch cb{};
+            int max_l = 0;
+            for (size_t i = 0; i < specs.size(); ++i) {
                 const OrthSpec& s = specs[i];
                 const Buf& b = bufs[i];
+                if (J >= b.blk.nbk) continue;
+                const int j0 = b.blk.begin(J), w = b.blk.width(J, s.l);
                 const int k = cb.count++;
-                const size_t off = (size_t)b.l1 * s.l + b.l1;
-                cb.l[k] = b.l2;
-                cb.G[k] = b.G + off;
+                cb.l[k] = w;
+                cb.G[k] = b.G + off(s.l, j0, j0);
                 cb.ldg[k] = s.l;
-                cb.Gsub[k] = b.Sub;
                 cb.trace_src[k] = b.G; cb.trace_n[k] = s.l; cb.trace_ld[k] = s.l;
-                cb.T[k] = b.T + off;
+                if (b.blk.nbk > 1) {
+                    if (J == 0) cb.shift_save[k] = b.shift;
+                    else cb.shift_use[k] = b.shift;
+                }
+                cb.T[k] = b.T + off(s.l, j0, j0);
                 cb.ldt[k] = s.l;
-                cb.Tneg[k] = b.Tn;
                 cb.shift_scale[k] = pass < shifted ? 10.0 * (s.m + s.l) : 0.0;
                 cb.dep_tol[k] = 0.0;
                 cb.ndead[k] = pass == last ? s.ndead : nullptr;
-                cb.ndead_acc[k] = 1;
-                max_l = std::max(max_l, b.l2);
+                cb.ndead_acc[k] = J > 0 ? 1 : 0;
+                max_l = std::max(max_l, w);
                 if (cb.count == kMaxSmall) { chol_launch(cb, max_l); max_l = 0; }
             }
             if (cb.count) chol_launch(cb, max_l);
-            g1.clear(); g2.clear();
-            for (size_t i : big) {  // W = T11 R12
+            std::vector<GemmSpec> g1, g2;
+            for (size_t i = 0; i < specs.size(); ++i) {
+                const OrthSpec& s = specs[i];
                 const Buf& b = bufs[i];
-                g1.push_back({b.l1, b.l2, b.l1, b.T, specs[i].l, b.R12, b.l2, b.W, b.l2});
+                if (J + 1 >= b.blk.nbk) continue;
+                const int j0 = b.blk.begin(J), w = b.blk.width(J, s.l), r0 = j0 + w, rest = s.l - r0;
+                // R_J,>J = T_JJ^H G_J,>J
+                g1.push_back({w, rest, w, b.T + off(s.l, j0, j0), s.l, b.G + off(s.l, j0, r0), s.l,
+                              b.R + off(s.l, j0, r0), s.l});
+                // G_>J,>J -= R_J,>J^H R_J,>J  (upper part, in place)
+                GemmSpec up{rest, rest, w, b.R + off(s.l, j0, r0), s.l, b.R + off(s.l, j0, r0), s.l,
+                            b.G + off(s.l, r0, r0), s.l};
+                up.structure = kUpperC;
+                up.D = b.G + off(s.l, r0, r0);
+                up.ldd = s.l;
+                up.alpha = -1.0;
+                g2.push_back(up);
             }
-            c->gemm_tag = 4;
-            gemm_many(c, kOpN, g1);
-            for (size_t i : big) {  // T12 = W (-T22)
+            if (!g1.empty()) {
+                c->gemm_tag = 3;
+                gemm_many(c, kOpC, g1);
+                gemm_many(c, kOpC, g2);
+            }
+        }
+        for (int I = max_nbk - 2; I >= 0; --I) {
+            std::vector<GemmSpec> g1, g2;
+            for (size_t i = 0; i < specs.size(); ++i) {
+                const OrthSpec& s = specs[i];
                 const Buf& b = bufs[i];
-                GemmSpec gs{b.l1, b.l2, b.l2, b.W, b.l2, b.Tn, specs[i].l, b.T + b.l1, specs[i].l};
-                gs.structure = kTriB;
-                g2.push_back(gs);
+                if (I + 1 >= b.blk.nbk) continue;
+                const int i0 = b.blk.begin(I), w = b.blk.width(I, s.l), r0 = i0 + w, rest = s.l - r0;
+                // W = R_I,>I T_>I,>I  (T upper triangular)
+                GemmSpec ws{w, rest, rest, b.R + off(s.l, i0, r0), s.l, b.T + off(s.l, r0, r0), s.l, b.W, rest};
+                ws.structure = kTriB;
+                g1.push_back(ws);
+                // T_I,>I = -T_II W
+                GemmSpec ts{w, rest, w, b.T + off(s.l, i0, i0), s.l, b.W, rest, b.T + off(s.l, i0, r0), s.l};
+                ts.alpha = -1.0;
+                g2.push_back(ts);
             }
-            gemm_many(c, kOpN, g2);
+            if (!g1.empty()) {
+                c->gemm_tag = 4;
+                gemm_many(c, kOpN, g1);
+                gemm_many(c, kOpN, g2);
+            }
         }
         for (size_t i = 0; i < specs.size(); ++i) {
             const OrthSpec& s = specs[i];
@@ -274,17 +284,34 @@ struct SmallSvdSpec {
 void small_svd_many(rrsvd_b200_ctx* c, const std::vector<SmallSvdSpec>& specs) {
     std::vector<cplx*> W(specs.size());
     std::vector<int*> dsweeps(specs.size(), nullptr);
+    std::vector<size_t> onchip, global;
     for (size_t i = 0; i < specs.size(); ++i) {
         W[i] = ws_get<cplx>(c, (size_t)(specs[i].r + specs[i].cc) * specs[i].cc);
         if (debug_enabled()) dsweeps[i] = ws_get<int>(c, 1);
+        (jacobi_fits(specs[i].r, specs[i].cc) ? onchip : global).push_back(i);
     }
-    for (size_t base = 0; base < specs.size(); base += kMaxSmall) {
-        const size_t end = std::min(specs.size(), base + kMaxSmall);
+    // problems beyond the cluster's shared memory: one cooperative grid each, W in L2/HBM
+    for (size_t i : global) {
+        const SmallSvdSpec& s = specs[i];
+        JacobiInitBatch ib{};
+        JacobiFinBatch fb{};
+        ib.count = fb.count = 1;
+        ib.r[0] = s.r; ib.c[0] = s.cc; ib.A[0] = s.X; ib.lda[0] = s.lda; ib.adj[0] = s.adj; ib.W[0] = W[i];
+        fb.r[0] = s.r; fb.c[0] = s.cc; fb.W[0] = W[i]; fb.sigma[0] = s.sigma; fb.Xn[0] = s.Xn; fb.Js[0] = s.Js;
+        check_cuda(c, jacobi_init(ib, c->stream), "jacobi_init");
+        check_cuda(c, jacobi_svd_global(W[i], s.r, s.cc, ws_get<int>(c, 2), dsweeps[i], c->stream),
+                   "jacobi_svd_global");
+        check_cuda(c, jacobi_finish(fb, s.cc, c->stream), "jacobi_finish");
+        c->launches += 3;
+    }
+    for (size_t base = 0; base < onchip.size(); base += kMaxSmall) {
+        const size_t end = std::min(onchip.size(), base + kMaxSmall);
         JacobiInitBatch ib{};
         JacobiBatch jb{};
         JacobiFinBatch fb{};
         int max_r = 0, max_c = 0;
-        for (size_t i = base; i < end; ++i) {
+        for (size_t ii = base; ii < end; ++ii) {
+            const size_t i = onchip[ii];
             const SmallSvdSpec& s = specs[i];
             const int k = ib.count++;
             ib.r[k] = s.r; ib.c[k] = s.cc; ib.A[k] = s.X; ib.lda[k] = s.lda; ib.adj[k] = s.adj; ib.W[k] = W[i];
@@ -296,11 +323,7 @@ void small_svd_many(rrsvd_b200_ctx* c, const std::vector<SmallSvdSpec>& specs) {
             max_c = std::max(max_c, s.cc);
         }
         check_cuda(c, jacobi_init(ib, c->stream), "jacobi_init");
-        const cudaError_t e = jacobi_svd(jb, max_r, max_c, c->stream);
-        if (e == cudaErrorInvalidValue)
-            throw_contract(c, "jacobi: matrix " + std::to_string(max_r) + "x" + std::to_string(max_c) +
-                                  " exceeds the on-chip Jacobi capacity");
-        check_cuda(c, e, "jacobi_svd");
+        check_cuda(c, jacobi_svd(jb, max_r, max_c, c->stream), "jacobi_svd");
         check_cuda(c, jacobi_finish(fb, max_c, c->stream), "jacobi_finish");
         c->launches += 3;
     }
@@ -418,7 +441,7 @@ void rrsvd_core(rrsvd_b200_ctx* c, const cplx* A, int m, int n, int l, int q, co
 
 void svd_jacobi_many(rrsvd_b200_ctx* c, const std::vector<SvdSpec>& specs) {
     if (specs.empty()) return;
-    std::vector<SmallSvdSpec> direct, pre;
+    std::vector<SmallSvdSpec> pre;
     struct Pre {
         const cplx* X;
         int r, cc;
@@ -430,12 +453,6 @@ void svd_jacobi_many(rrsvd_b200_ctx* c, const std::vector<SvdSpec>& specs) {
     for (const SvdSpec& s : specs) {
         const bool tall = s.m >= s.n;
         const int r = tall ? s.m : s.n, cc = tall ? s.n : s.m;
-        if (cc > kMaxOrthL || !jacobi_fits(cc, cc)) {
-            // Unpreconditioned one-sided Jacobi (converges, in more sweeps).
-            // tall: X = A, X J = U S -> U = Xn, V = J.   wide: X = A^H -> V = Xn, U = J.
-            direct.push_back({s.A, r, cc, tall ? 0 : 1, s.n, s.sigma, tall ? s.U : s.V, tall ? s.V : s.U});
-            continue;
-        }
         const cplx* X = s.A;
         if (!tall) {
             cplx* Xt = ws_get<cplx>(c, (size_t)r * cc);
@@ -457,9 +474,7 @@ void svd_jacobi_many(rrsvd_b200_ctx* c, const std::vector<SvdSpec>& specs) {
     gemm_many(c, kOpC, gs);
     for (const Pre& p : pres)
         pre.push_back({p.R, p.cc, p.cc, 1, p.cc, p.s->sigma, p.tall ? p.s->V : p.s->U, p.K});
-    std::vector<SmallSvdSpec> all = direct;
-    all.insert(all.end(), pre.begin(), pre.end());
-    small_svd_many(c, all);
+    small_svd_many(c, pre);
     gs.clear();
     for (const Pre& p : pres) gs.push_back({p.r, p.cc, p.cc, p.Qr, p.cc, p.K, p.cc, p.tall ? p.s->U : p.s->V, p.cc});
     c->gemm_tag = 6;

@@ -35,6 +35,9 @@ struct GemmSpec {
     int structure = kGeneral;  // kTriB / kUpperC hints (zgemm.cuh)
     int nsub = 0;              // column-blocked B/C (zgemm.cuh)
     long long subB = 0, subC = 0;
+    const cplx* D = nullptr;   // optional addend: C = D + alpha * product (zgemm.cuh)
+    long long ldd = 0;
+    double alpha = 1.0;
 };
 
 // Grouped complex GEMMs sharing op(A); split-K chosen so the whole group fills the GPU.

@@ -1,5 +1,6 @@
 // smallla.cu — batched small dense kernels: Cholesky + inverse, cluster Jacobi SVD,
 // deterministic reductions.  See smallla.cuh.
+#include <algorithm>
 #include <cooperative_groups.h>
 
 #include "smallla.cuh"
@@ -14,7 +15,19 @@ constexpr double kU = 1.1102230246251565e-16;  // unit roundoff 2^-53
 constexpr double kEps = 2.220446049250313e-16;  // 2^-52
 
 // ============================================================================ Cholesky + inverse
-constexpr int CHOL_THREADS = 512;
+constexpr int CHOL_THREADS = 256;
+constexpr int NB = 8;       // Cholesky panel / inverse block rows
+constexpr int RG = 4;       // trailing-update rows per warp tile
+constexpr int SPLIT = 4;    // threads per column in the inverse's q-sums
+constexpr int kChunks = (kMaxCholL + CHOL_THREADS / SPLIT - 1) / (CHOL_THREADS / SPLIT);
+
+// acc -= conj(a) * b
+__device__ __forceinline__ void cfnmac(cplx& acc, cplx a, cplx b) {
+    acc.x = fma(-a.x, b.x, acc.x);
+    acc.x = fma(-a.y, b.y, acc.x);
+    acc.y = fma(-a.x, b.y, acc.y);
+    acc.y = fma(a.y, b.x, acc.y);
+}
 
 __device__ __forceinline__ int poff(int i, int l) { return i * l - (i * (i - 1)) / 2; }
 
@@ -24,8 +37,7 @@ __global__ void __launch_bounds__(CHOL_THREADS) chol_inv_kernel(const __grid_con
     const int l = b.l[p];
     const int npk = l * (l + 1) / 2;
     cplx* P = reinterpret_cast<cplx*>(sm);
-    cplx* row = P + npk;
-    double* g0 = reinterpret_cast<double*>(row + l);
+    double* g0 = reinterpret_cast<double*>(P + npk);
     int* dead = reinterpret_cast<int*>(g0 + l);
     __shared__ double s_shift;
 
@@ -35,13 +47,20 @@ __global__ void __launch_bounds__(CHOL_THREADS) chol_inv_kernel(const __grid_con
     const cplx* Gs = b.Gsub[p];
 
     if (warp == 0) {  // shift from the trace of the whole Gram matrix (also for a trailing block)
-        const cplx* ts = b.trace_src[p] ? b.trace_src[p] : G;
-        const int tn = b.trace_src[p] ? b.trace_n[p] : l;
-        const long long tld = (b.trace_src[p] ? (long long)b.trace_ld[p] : ldg) + 1;
-        double tr = 0.0;
-        for (int i = lane; i < tn; i += 32) tr += ts[i * tld].x;
-        tr = warp_sum(tr);
-        if (lane == 0) s_shift = b.shift_scale[p] * kU * tr;
+        if (b.shift_use[p] != nullptr) {
+            if (lane == 0) s_shift = *b.shift_use[p];
+        } else {
+            const cplx* ts = b.trace_src[p] ? b.trace_src[p] : G;
+            const int tn = b.trace_src[p] ? b.trace_n[p] : l;
+            const long long tld = (b.trace_src[p] ? (long long)b.trace_ld[p] : ldg) + 1;
+            double tr = 0.0;
+            for (int i = lane; i < tn; i += 32) tr += ts[i * tld].x;
+            tr = warp_sum(tr);
+            if (lane == 0) {
+                s_shift = b.shift_scale[p] * kU * tr;
+                if (b.shift_save[p] != nullptr) *b.shift_save[p] = s_shift;
+            }
+        }
     }
     __syncthreads();
     for (int i = warp; i < l; i += nw)
@@ -60,68 +79,149 @@ __global__ void __launch_bounds__(CHOL_THREADS) chol_inv_kernel(const __grid_con
         }
     __syncthreads();
 
-    // ---- right-looking Cholesky, G = R^H R, R upper, row j of R overwrites row j of G.
-    // Trailing update: warp w owns rows i ≡ w (mod nw), lanes sweep the row (coalesced).
-    for (int j = 0; j < l; ++j) {
-        const double d = P[poff(j, l)].x;
-        const bool isdead = !(d > b.dep_tol[p] * g0[j]) || !(d > 0.0) || !(g0[j] > 0.0);
-        const double rjj = isdead ? 0.0 : sqrt(d);
-        const double inv = isdead ? 0.0 : 1.0 / rjj;
-        const int oj = poff(j, l);
-        for (int k = j + tid; k < l; k += CHOL_THREADS)
-            row[k] = (k == j) ? mk(rjj, 0.0) : cscale(P[oj + k - j], inv);
-        if (tid == 0) dead[j] = isdead ? 1 : 0;
+    // ---- blocked right-looking Cholesky, G = R^H R, R upper; row j of R overwrites row j of G.
+    // Panels of NB rows.  Every thread factors the panel's NB x NB diagonal block redundantly in
+    // registers (broadcast reads — no barrier per pivot), then forward-solves one column of the
+    // panel's off-diagonal rows: R[J][k] = R_JJ^-H G[J][k].  The rank-NB trailing update
+    // G[i][k] -= sum_t conj(R[t][i]) R[t][k] is register-tiled: a warp takes RG consecutive rows
+    // (their NB coefficients in registers), its lanes sweep the columns.  Two barriers per panel.
+    const double dtol = b.dep_tol[p];
+    for (int j0 = 0; j0 < l; j0 += NB) {
+        const int nb = min(NB, l - j0);
+        cplx D[NB][NB];
+        double inv[NB];
+        unsigned deadmask = 0;
+#pragma unroll
+        for (int t = 0; t < NB; ++t)
+#pragma unroll
+            for (int u = t; u < NB; ++u) D[t][u] = (u < nb) ? P[poff(j0 + t, l) + u - t] : mk(0.0, 0.0);
+#pragma unroll
+        for (int t = 0; t < NB; ++t) {
+            inv[t] = 0.0;
+            if (t < nb) {
+                const double d = D[t][t].x, g = g0[j0 + t];
+                const bool isdead = !(d > dtol * g) || !(d > 0.0) || !(g > 0.0);
+                const double r = isdead ? 0.0 : sqrt(d);
+                inv[t] = isdead ? 0.0 : 1.0 / r;
+                deadmask |= isdead ? (1u << t) : 0u;
+                D[t][t] = mk(r, 0.0);
+#pragma unroll
+                for (int u = t + 1; u < NB; ++u) D[t][u] = cscale(D[t][u], inv[t]);
+#pragma unroll
+                for (int v = t + 1; v < NB; ++v)
+#pragma unroll
+                    for (int u = v; u < NB; ++u) cfnmac(D[v][u], D[t][v], D[t][u]);
+            }
+        }
+        for (int k = j0 + nb + tid; k < l; k += CHOL_THREADS) {
+            cplx X[NB];
+#pragma unroll
+            for (int t = 0; t < NB; ++t) X[t] = (t < nb) ? P[poff(j0 + t, l) + k - j0 - t] : mk(0.0, 0.0);
+#pragma unroll
+            for (int t = 0; t < NB; ++t) {
+#pragma unroll
+                for (int v = 0; v < t; ++v) cfnmac(X[t], D[v][t], X[v]);
+                X[t] = cscale(X[t], inv[t]);
+            }
+#pragma unroll
+            for (int t = 0; t < NB; ++t)
+                if (t < nb) P[poff(j0 + t, l) + k - j0 - t] = X[t];
+        }
+        if (tid == 0) {
+#pragma unroll
+            for (int t = 0; t < NB; ++t)
+#pragma unroll
+                for (int u = t; u < NB; ++u)
+                    if (u < nb) P[poff(j0 + t, l) + u - t] = D[t][u];
+#pragma unroll
+            for (int t = 0; t < NB; ++t)
+                if (t < nb) dead[j0 + t] = (deadmask >> t) & 1u;
+        }
         __syncthreads();
-        for (int k = j + tid; k < l; k += CHOL_THREADS) P[oj + k - j] = row[k];
-        if (!isdead) {
-            for (int i = j + 1 + warp; i < l; i += nw) {
-                const cplx ri = cconj(row[i]);
-                cplx* Pi = P + poff(i, l) - i;  // Pi[k] = P[i][k]
-#pragma unroll 4
-                for (int k = i + lane; k < l; k += 32) {
-                    const cplx rk = row[k];
-                    cplx v = Pi[k];
-                    v.x -= ri.x * rk.x - ri.y * rk.y;
-                    v.y -= ri.x * rk.y + ri.y * rk.x;
-                    Pi[k] = v;
+        for (int r0 = j0 + nb + RG * warp; r0 < l; r0 += RG * nw) {
+            cplx a[RG][NB];
+#pragma unroll
+            for (int ri = 0; ri < RG; ++ri)
+#pragma unroll
+                for (int t = 0; t < NB; ++t)
+                    a[ri][t] = (t < nb && r0 + ri < l) ? P[poff(j0 + t, l) + r0 + ri - j0 - t] : mk(0.0, 0.0);
+            for (int k = r0 + lane; k < l; k += 32) {
+                cplx bb[NB];
+#pragma unroll
+                for (int t = 0; t < NB; ++t) bb[t] = (t < nb) ? P[poff(j0 + t, l) + k - j0 - t] : mk(0.0, 0.0);
+#pragma unroll
+                for (int ri = 0; ri < RG; ++ri) {
+                    const int i = r0 + ri;
+                    if (i <= k) {
+                        cplx* pv = P + poff(i, l) + k - i;
+                        cplx v = *pv;
+#pragma unroll
+                        for (int t = 0; t < NB; ++t) cfnmac(v, a[ri][t], bb[t]);
+                        *pv = v;
+                    }
                 }
             }
         }
         __syncthreads();
     }
 
-    // ---- in-place triangular inverse T = R^-1, bottom-up by rows:
-    //   T[i][i] = 1/R[i][i],  T[i][k] = -T[i][i] * sum_{q=i+1..k} R[i][q] T[q][k]   (k > i)
-    // Row i of R is staged in `row`; rows > i already hold T.  Four threads per column k split
-    // the q-sum (two shuffle levels); consecutive columns read consecutive packed addresses.
+    // ---- in-place triangular inverse T = R^-1, bottom-up by blocks of NB rows:
+    //   T[i][i] = 1/R[i][i],  T[i][k] = -T[i][i] * sum_{q=i+1..k} R[i][q] T[q][k]   (k > i).
+    // For block rows [i0, i0+nb) and one column k, the q-sum splits into q >= i0+nb (rows that
+    // already hold T: NB dot products sharing T[q][k], split over SPLIT threads) and q inside
+    // the block (an NB x NB triangular recurrence, done redundantly by the SPLIT threads).
+    // Results wait in registers for a barrier: every column reads the block's R rows.
     // A dependent (dead) row gets T[i][:] = 0, which zeroes column i of T as well.
-    const int c4 = tid >> 2, s4 = tid & 3;
-    for (int i = l - 1; i >= 0; --i) {
-        const int oi = poff(i, l);
-        const bool dd = dead[i] != 0;
-        const double tii = dd ? 0.0 : 1.0 / P[oi].x;
-        for (int k = i + 1 + tid; k < l; k += CHOL_THREADS) row[k] = P[oi + k - i];
-        __syncthreads();
-        for (int k0 = i + 1; k0 < l; k0 += CHOL_THREADS / 4) {
-            const int k = k0 + c4;
-            cplx s = mk(0.0, 0.0), s2 = mk(0.0, 0.0);
-            if (k < l && !dd) {
-                int q = i + 1 + s4;
-                for (; q + 4 <= k; q += 8) {  // two independent accumulators
-                    cfma(s, row[q], P[poff(q, l) + k - q]);
-                    cfma(s2, row[q + 4], P[poff(q + 4, l) + k - q - 4]);
+    const int grp = tid / SPLIT, sub = tid % SPLIT;
+    constexpr int kGroups = CHOL_THREADS / SPLIT;
+    for (int i0 = (l - 1) / NB * NB; i0 >= 0; i0 -= NB) {
+        const int nb = min(NB, l - i0);
+        double tii[NB];
+#pragma unroll
+        for (int t = 0; t < NB; ++t)
+            tii[t] = (t < nb && !dead[i0 + t]) ? 1.0 / P[poff(i0 + t, l)].x : 0.0;
+        cplx res[kChunks][NB];
+#pragma unroll
+        for (int ch = 0; ch < kChunks; ++ch) {
+            const int k = i0 + grp + ch * kGroups;
+            cplx S[NB];
+#pragma unroll
+            for (int t = 0; t < NB; ++t) S[t] = mk(0.0, 0.0);
+            if (k < l) {
+                for (int q = i0 + nb + sub; q <= k; q += SPLIT) {
+                    const cplx tq = P[poff(q, l) + k - q];
+#pragma unroll
+                    for (int t = 0; t < NB; ++t)
+                        if (t < nb) cfma(S[t], P[poff(i0 + t, l) + q - i0 - t], tq);
                 }
-                if (q <= k) cfma(s, row[q], P[poff(q, l) + k - q]);
             }
-            s.x += s2.x;
-            s.y += s2.y;
-            s.x += __shfl_xor_sync(0xffffffffu, s.x, 1);
-            s.y += __shfl_xor_sync(0xffffffffu, s.y, 1);
-            s.x += __shfl_xor_sync(0xffffffffu, s.x, 2);
-            s.y += __shfl_xor_sync(0xffffffffu, s.y, 2);
-            if (k < l && s4 == 0) P[oi + k - i] = cscale(s, -tii);
+#pragma unroll
+            for (int t = 0; t < NB; ++t) {
+#pragma unroll
+                for (int o = 1; o < SPLIT; o <<= 1) {
+                    S[t].x += __shfl_xor_sync(0xffffffffu, S[t].x, o);
+                    S[t].y += __shfl_xor_sync(0xffffffffu, S[t].y, o);
+                }
+            }
+#pragma unroll
+            for (int t = NB - 1; t >= 0; --t) {
+                cplx acc = S[t];
+#pragma unroll
+                for (int u = t + 1; u < NB; ++u)
+                    if (u < nb && i0 + u <= k) cfma(acc, P[poff(i0 + t, l) + u - t], res[ch][u]);
+                res[ch][t] = (i0 + t == k) ? mk(tii[t], 0.0) : cscale(acc, -tii[t]);
+            }
         }
-        if (tid == 0) P[oi] = mk(tii, 0.0);
+        __syncthreads();
+        if (sub == 0) {
+#pragma unroll
+            for (int ch = 0; ch < kChunks; ++ch) {
+                const int k = i0 + grp + ch * kGroups;
+#pragma unroll
+                for (int t = 0; t < NB; ++t)
+                    if (t < nb && i0 + t <= k && k < l) P[poff(i0 + t, l) + k - i0 - t] = res[ch][t];
+            }
+        }
         __syncthreads();
     }
 
@@ -246,6 +346,62 @@ __global__ void __launch_bounds__(JAC_THREADS) jacobi_kernel(const __grid_consta
     }
     cluster.sync();  // peers may still read our counters
     if (rank == 0 && tid == 0 && b.sweeps[p] != nullptr) *b.sweeps[p] = sweep + 1;
+}
+
+__global__ void __launch_bounds__(JAC_THREADS) jacobi_global_kernel(cplx* __restrict__ W, int r, int c,
+                                                                   int* counters, int* sweeps_out) {
+    cg::grid_group grid = cg::this_grid();
+    const int n = c + (c & 1);  // odd c: one dummy player sits out each step
+    const int ld = r + c;
+    const int lane = threadIdx.x & 31;
+    const int nwarps = gridDim.x * (JAC_THREADS / 32);
+    const int gw = blockIdx.x * (JAC_THREADS / 32) + (threadIdx.x >> 5);
+    const double tol = sqrt((double)max(r, 1)) * kEps;
+    int sweep = 0;
+    for (; sweep < kMaxSweeps; ++sweep) {
+        int myrot = 0;
+        for (int t = 0; t < n - 1; ++t) {
+            for (int k = gw; k < n / 2; k += nwarps) {
+                const int gp = circle(k, t, n), gq = circle(n - 1 - k, t, n);
+                if (gp >= c || gq >= c) continue;
+                cplx* xp = W + (long long)gp * ld;
+                cplx* xq = W + (long long)gq * ld;
+                double a = 0.0, bb = 0.0;
+                cplx g = mk(0.0, 0.0);
+                for (int rr = lane; rr < r; rr += 32) {
+                    const cplx u = xp[rr], v = xq[rr];
+                    a += cabs2(u);
+                    bb += cabs2(v);
+                    cfmac(g, u, v);
+                }
+                a = warp_sum(a);
+                bb = warp_sum(bb);
+                g = warp_sum(g);
+                const double ag = hypot(g.x, g.y);
+                if (!(a > 0.0) || !(bb > 0.0) || !(ag > tol * sqrt(a) * sqrt(bb))) continue;
+                ++myrot;
+                const cplx e = mk(g.x / ag, -g.y / ag);
+                const double zeta = (bb - a) / (2.0 * ag);
+                const double tt = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + hypot(1.0, zeta));
+                const double cc = 1.0 / sqrt(1.0 + tt * tt);
+                const double ss = cc * tt;
+                for (int rr = lane; rr < ld; rr += 32) {
+                    const cplx u = xp[rr];
+                    const cplx ev = cmul(e, xq[rr]);
+                    xp[rr] = mk(cc * u.x - ss * ev.x, cc * u.y - ss * ev.y);
+                    xq[rr] = mk(ss * u.x + cc * ev.x, ss * u.y + cc * ev.y);
+                }
+            }
+            grid.sync();
+        }
+        if (lane == 0 && myrot) atomicAdd(&counters[sweep & 1], myrot);
+        grid.sync();
+        const int total = *((volatile int*)&counters[sweep & 1]);
+        // every block read the other slot at the previous check: recycle it for the next sweep
+        if (blockIdx.x == 0 && threadIdx.x == 0) counters[(sweep + 1) & 1] = 0;
+        if (total == 0) break;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0 && sweeps_out != nullptr) *sweeps_out = sweep + 1;
 }
 
 __global__ void jacobi_init_kernel(const __grid_constant__ JacobiInitBatch b) {
@@ -387,11 +543,29 @@ __global__ void sumsq_final(const double* partial, const int* bad, double* out, 
 
 cudaError_t chol_inv(const CholBatch& b, int max_l, cudaStream_t s) {
     if (b.count == 0) return cudaSuccess;
-    const size_t smem = (size_t)max_l * (max_l + 1) / 2 * sizeof(cplx) + max_l * sizeof(cplx) +
-                        max_l * sizeof(double) + max_l * sizeof(int);
+    const size_t smem = (size_t)max_l * (max_l + 1) / 2 * sizeof(cplx) + max_l * sizeof(double) +
+                        max_l * sizeof(int);
     cudaError_t e = cudaFuncSetAttribute(chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     chol_inv_kernel<<<b.count, CHOL_THREADS, smem, s>>>(b);
+    return cudaGetLastError();
+}
+
+cudaError_t jacobi_svd_global(cplx* W, int r, int c, int* counters, int* sweeps, cudaStream_t s) {
+    cudaError_t e = cudaMemsetAsync(counters, 0, 2 * sizeof(int), s);
+    if (e != cudaSuccess) return e;
+    int per_sm = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, jacobi_global_kernel, JAC_THREADS, 0);
+    if (e != cudaSuccess) return e;
+    int dev = 0, nsm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    const int pairs = (c + 1) / 2;
+    const int want = (pairs + JAC_THREADS / 32 - 1) / (JAC_THREADS / 32);
+    const int grid = std::max(1, std::min(want, per_sm * nsm));
+    void* args[] = {&W, &r, &c, &counters, &sweeps};
+    e = cudaLaunchCooperativeKernel((const void*)jacobi_global_kernel, dim3(grid), dim3(JAC_THREADS), args, 0, s);
+    if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }
 

@@ -16,7 +16,6 @@ constexpr int kMaxSmall = 64;  // problems per launch of the small-matrix kernel
 // conditioned, so it runs with dep_tol = 0: only non-positive pivots (exactly vanishing
 // columns) die, and no genuine small-σ direction is discarded.
 constexpr int kMaxCholL = 168;  // packed upper triangle must fit in 227 KB of shared memory
-constexpr int kMaxOrthL = 2 * kMaxCholL - 8;  // one level of 2x2 blocking (pipeline.cu orth_many)
 
 struct CholBatch {
     int count;
@@ -34,6 +33,8 @@ struct CholBatch {
     double dep_tol[kMaxSmall];        // relative pivot floor for "dependent"
     int* ndead[kMaxSmall];            // nullable: number of dependent columns found
     int ndead_acc[kMaxSmall];         // 1: add to *ndead instead of storing
+    double* shift_save[kMaxSmall];    // nullable: store the shift used (for later blocks)
+    const double* shift_use[kMaxSmall];  // nullable: use this stored shift instead
 };
 cudaError_t chol_inv(const CholBatch& b, int max_l, cudaStream_t s);
 bool jacobi_fits(int r, int c);  // an r x c problem fits jacobi_svd's on-chip capacity
@@ -50,6 +51,12 @@ struct JacobiBatch {
     int* sweeps[kMaxSmall];  // nullable: sweeps used
 };
 cudaError_t jacobi_svd(const JacobiBatch& b, int max_r, int max_c, cudaStream_t s);
+
+// The same one-sided Jacobi for ONE problem too large for the on-chip cluster: W stays in
+// global memory (L2-resident when it fits), a persistent cooperative grid runs the round-robin
+// steps (one warp per column pair, a grid barrier between steps).  `counters` = 2 device ints
+// (zeroed here); `sweeps` (nullable) receives the sweep count.
+cudaError_t jacobi_svd_global(cplx* W, int r, int c, int* counters, int* sweeps, cudaStream_t s);
 
 // Load W from a row-major matrix: X = A (r x c) if !adj, or X = A^H when adj (A is c x r);
 // J = I.

@@ -234,11 +234,12 @@ zgemm_dmma_kernel(const __grid_constant__ GemmGroup g) {
             csc[j][c] = (P.cs && col < N) ? __ldg(P.cs + col % P.cs_mod) : 1.0;
             ccol[j][c] = P.nsub ? (long long)(col / P.nsub) * P.subC + col % P.nsub : col;
         }
+    const cplx* Dd = P.D ? P.D + (long long)bz * P.strideC : nullptr;
 #pragma unroll
     for (int i = 0; i < MI; ++i) {
         const int row = m0 + wm + i * 8 + fr;
         if (row >= M) continue;
-        const double rsc = P.rs ? __ldg(P.rs + row / P.rs_div) : 1.0;
+        const double rsc = (P.rs ? __ldg(P.rs + row / P.rs_div) : 1.0) * P.alpha;
 #pragma unroll
         for (int j = 0; j < NI; ++j) {
             const int col = n0 + wn + j * 8 + fc * 2;
@@ -246,7 +247,9 @@ zgemm_dmma_kernel(const __grid_constant__ GemmGroup g) {
             for (int c = 0; c < 2; ++c) {
                 if (col + c >= N) continue;
                 const double sc = rsc * csc[j][c];
-                C[(long long)row * P.ldc + ccol[j][c]] = mk(acc[i][j][0][c] * sc, acc[i][j][1][c] * sc);
+                cplx v = mk(acc[i][j][0][c] * sc, acc[i][j][1][c] * sc);
+                if (Dd) v = cadd(v, Dd[(long long)row * P.ldd + col + c]);
+                C[(long long)row * P.ldc + ccol[j][c]] = v;
             }
         }
     }
@@ -265,11 +268,13 @@ __global__ void splitk_reduce_kernel(const __grid_constant__ GemmGroup g) {
         const int row = (int)(rem / P.n), col = (int)(rem % P.n);
         cplx s = mk(0.0, 0.0);
         for (int k = 0; k < P.split; ++k) s = cadd(s, P.partial[(long long)k * total + e]);
-        double sc = 1.0;
+        double sc = P.alpha;
         if (P.rs) sc *= P.rs[row / P.rs_div];
         if (P.cs) sc *= P.cs[col % P.cs_mod];
         const long long cc = P.nsub ? (long long)(col / P.nsub) * P.subC + col % P.nsub : col;
-        P.C[bz * P.strideC + (long long)row * P.ldc + cc] = cscale(s, sc);
+        cplx v = cscale(s, sc);
+        if (P.D) v = cadd(v, P.D[bz * P.strideC + (long long)row * P.ldd + col]);
+        P.C[bz * P.strideC + (long long)row * P.ldc + cc] = v;
     }
 }
 

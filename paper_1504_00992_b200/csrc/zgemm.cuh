@@ -45,6 +45,11 @@ struct GemmProblem {
     // narrow products that share A (the gate: G · Θ[α] for every α) run as ONE wide GEMM.
     int nsub;
     long long subB, subC;
+    // Optional addend: C = D + alpha * (scaled product), D with its own ld (may alias C: each
+    // element is read and written by the same thread).  Not combined with nsub.
+    const cplx* D;
+    long long ldd;
+    double alpha;
     // filled by the launcher
     int tiles_m, tiles_n, tile_begin;
 };

@@ -46,10 +46,10 @@ def test_philox_sketch_statistics(ctx):
 # ------------------------------------------------------------------ QR / SVD (linalg.cpp)
 
 @pytest.mark.parametrize("m,n", [(40, 40), (300, 74), (2000, 110), (1000, 168), (1000, 169), (2000, 200),
-                                 (300, 256), (700, 328)])
+                                 (300, 256), (700, 328), (1200, 500), (2000, 1000)])
 def test_qr_orthonormal_and_reconstructs(ctx, m, n):
     """test_linalg.cpp:114-121: orthonormality and reconstruction < 1e-12.  Widths above 168
-    go through the 2x2-blocked Cholesky (one level, up to 328)."""
+    go through the block-right-looking Cholesky (diagonal blocks <= 168, DMMA updates)."""
     rng = np.random.default_rng(m + n)
     a = cplx_randn(rng, m, n)
     q, r = P.qr(a, ctx=ctx)
@@ -87,9 +87,11 @@ def test_qr_ill_conditioned(ctx, l):
         assert np.linalg.norm(y - q @ (q.conj().T @ y), 2) < 1e-11
 
 
-@pytest.mark.parametrize("m,n", [(30, 30), (96, 64), (64, 96), (256, 256), (600, 120), (400, 240), (200, 288)])
+@pytest.mark.parametrize("m,n", [(30, 30), (96, 64), (64, 96), (256, 256), (600, 120), (400, 240), (200, 288),
+                                 (400, 400), (1000, 700), (500, 900)])
 def test_svd_full_matches_reference(ctx, ref, m, n):
-    """svd_full (linalg.cpp:67-88) — test_linalg.cpp:184-194 reconstruction 1e-10."""
+    """svd_full (linalg.cpp:67-88) — test_linalg.cpp:184-194 reconstruction 1e-10.  Minor
+    dimensions above ~290 run the grid-wide (cooperative) Jacobi on the QR's R^H."""
     rng = np.random.default_rng(m * n)
     r = min(m, n)
     s_true = np.logspace(0, -12, r)
@@ -267,6 +269,8 @@ DEC_CASES = [
     (128, 2, 128, 2, 128, 128, True, 0, 128, 128, 0.85),
     # C3 shape with p = 100 (l = 200)
     (100, 20, 100, 20, 100, 100, True, 256, 100, 100, 0.85),
+    # C3 shape, deterministic (svd_full of the 2000 x 2000 unfolding)
+    (100, 20, 100, 20, 100, 100, False, 256, 0, 0, 0.85),
 ]
 
 
