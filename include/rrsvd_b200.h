@@ -56,7 +56,7 @@ typedef struct rrsvd_b200_backend {
     uint64_t target_rank;      /* 0 -> chi_max */
     uint64_t oversampling;     /* 0 -> target rank */
     uint64_t power_iterations; /* q */
-    int accuracy_check;        /* fixed-precision mode (not yet supported: returns 1) */
+    int accuracy_check;        /* fixed-precision mode with bond growth (tebd.cpp:173-179) */
     double epsilon;
     uint64_t probe_count;
     uint64_t det_crossover; /* minor <= crossover -> deterministic SVD */
@@ -126,6 +126,18 @@ int rrsvd_b200_fixed_rank_batch(rrsvd_b200_ctx* ctx, size_t count, const double*
                                 int omega_mode, double* const* U, double* const* S,
                                 double* const* V, double* discarded);
 
+/* rrsvd_fixed_precision (randomized.hpp:64-66, randomized.cpp:124-176) with
+ * AccuracyCheckParams{epsilon, probe_count, growth_block = 0}: range finder at initial_l, then
+ * probe rounds (seeds seed + 0x9e3779b97f4a7c15 * draw) that certify
+ * max_j ||(I - Q Q^H) A omega_j|| <= epsilon or double the basis (up to min(m, n)).  Writes all
+ * l produced columns: U (m x l), S (l), V (n x l) — size them for l = min(m, n) — and *l_out,
+ * *certified (tolerance_certified), *discarded (w over all l values).  omega_mode selects the
+ * reference mt19937_64 stream or Philox for every draw. */
+int rrsvd_b200_fixed_precision(rrsvd_b200_ctx* ctx, const double* A, size_t m, size_t n,
+                               size_t initial_l, size_t q, size_t probe_count, double epsilon,
+                               uint64_t seed, int omega_mode, double* U, double* S, double* V,
+                               size_t* l_out, int* certified, double* discarded);
+
 /* ---- L3: the TEBD two-site trio in the unfolded layout (tebd.hpp:98-110) ---------------
  * Unfolded two-site matrix M: (cl*d1) x (d2*cr), row a*d1+i, column j*cr+b (tebd.cpp:150-155).
  * Gamma tensors are Tensor3 (left, phys, right) row-major (mps.hpp:20-25). */
@@ -141,7 +153,9 @@ int rrsvd_b200_apply_gate_unfolded(rrsvd_b200_ctx* ctx, const double* G, size_t 
                                    size_t cl, size_t cr, const double* M_in, double* M_out);
 /* decimate (tebd.cpp:141-237) of the unfolded M.  call_seed is the value the reference takes
  * from backend.seed++ (tebd.cpp:162).  Outputs are sized for chi <= min(chi_max or minor, l):
- * gamma_l cl x d1 x chi, lambda chi, gamma_r chi x d2 x cr (packed with the returned chi). */
+ * gamma_l cl x d1 x chi, lambda chi, gamma_r chi x d2 x cr (packed with the returned chi).
+ * With backend->accuracy_check the fixed-precision path may grow the bond past chi_max
+ * (tebd.cpp:177-179): size the outputs for chi <= min(d1*cl, d2*cr) then. */
 int rrsvd_b200_decimate_unfolded(rrsvd_b200_ctx* ctx, const double* M, size_t d1, size_t d2,
                                  size_t cl, size_t cr, const double* ll, const double* lr,
                                  size_t chi_max, double trunc_tol,

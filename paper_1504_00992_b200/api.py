@@ -171,6 +171,29 @@ def rrsvd_fixed_rank(a, k: int, p: int, q: int, seed: int, omega=None,
     return SvdResult(u, s, v, w.value, k)
 
 
+def rrsvd_fixed_precision(a, epsilon: float, probe_count: int, initial_l: int, q: int, seed: int,
+                          mode: int = OMEGA_REFERENCE, vectors: bool = True, ctx=None) -> SvdResult:
+    """randomized.cpp:124-176 (AccuracyCheckParams{epsilon, probe_count, growth_block=0}):
+    range finder at initial_l, then probe rounds that certify max_j ||(I-QQ^H) A w_j|| <= eps
+    or double the basis.  Returns all l columns; tolerance_certified as the reference."""
+    c = _ctx(ctx)
+    a = _prep(a)
+    m, n = _shape(a)
+    mn = min(m, n)
+    u = _empty(a, (m * mn,), np.complex128) if vectors else None
+    s = _empty(a, (mn,), np.float64)
+    v = _empty(a, (n * mn,), np.complex128) if vectors else None
+    lo, cert, w = C.c_size_t(), C.c_int(), C.c_double()
+    c.check(L.lib().rrsvd_b200_fixed_precision(c.h, ptr(a), sz(m), sz(n), sz(initial_l), sz(q),
+                                               sz(probe_count), C.c_double(epsilon), C.c_uint64(seed),
+                                               C.c_int(mode), ptr(u), ptr(s), ptr(v), C.byref(lo),
+                                               C.byref(cert), C.byref(w)))
+    l = lo.value
+    uu = u[:m * l].reshape(m, l) if vectors else None
+    vv = v[:n * l].reshape(n, l) if vectors else None
+    return SvdResult(uu, s[:l], vv, w.value, l, bool(cert.value))
+
+
 def rrsvd_fixed_rank_batch(As, k: int, p: int, q: int, seeds, mode: int = OMEGA_PHILOX,
                            vectors: bool = False, ctx=None):
     """Many same-shaped rrsvd_fixed_rank calls batched through every pipeline stage.
@@ -294,7 +317,8 @@ def decimate_unfolded(m, d1: int, d2: int, ll, lr, chi_max: int, trunc_tol: floa
     cl, cr = rows // d1, cols // d2
     minor = min(rows, cols)
     ll_, lr_, omega = _prep(ll, np.float64), _prep(lr, np.float64), _prep(omega)
-    kmax = minor if chi_max == 0 else min(minor, chi_max)
+    # the accuracy check may grow the bond past chi_max (tebd.cpp:177-179)
+    kmax = minor if (chi_max == 0 or backend.accuracy_check) else min(minor, chi_max)
     gl = _empty(m, (cl * d1 * kmax,), np.complex128)
     lam = _empty(m, (kmax,), np.float64)
     gr = _empty(m, (kmax * d2 * cr,), np.complex128)

@@ -261,6 +261,39 @@ int rrsvd_b200_fixed_rank(rrsvd_b200_ctx* c, const double* A, size_t m, size_t n
     });
 }
 
+int rrsvd_b200_fixed_precision(rrsvd_b200_ctx* c, const double* A, size_t m, size_t n, size_t initial_l,
+                               size_t q, size_t probe_count, double epsilon, uint64_t seed, int omega_mode,
+                               double* U, double* S, double* V, size_t* out_l, int* certified,
+                               double* discarded) {
+    return api(c, [&] {
+        if (S == nullptr || out_l == nullptr) throw_contract(c, "fixed_precision: null argument");
+        if (probe_count < 1) throw_contract(c, "rrsvd_fixed_precision: probe_count >= 1 required");
+        if (initial_l < 1 || initial_l + probe_count > n)
+            throw_contract(c, "rrsvd_fixed_precision: requires initial_l + probe_count <= n");
+        const auto* dA = static_cast<const cplx*>(stage_in(c, A, m * n * sizeof(cplx)));
+        std::vector<FixedPrecSpec> fp{FixedPrecSpec{dA, (int)m, (int)n, (int)initial_l, (int)q, (int)probe_count,
+                                                    epsilon, seed, omega_mode}};
+        rrsvd_fixed_precision_many(c, fp);
+        const size_t l = (size_t)fp[0].l;
+        auto* sc = ws_get<Scalars>(c, 1);
+        SumsqBatch sb{};
+        sb.count = 1;
+        sb.a[0] = dA; sb.n[0] = (long long)(m * n); sb.out_sq[0] = &sc->total_sq; sb.out_bad[0] = &sc->nonfinite;
+        check_cuda(c, sumsq_many(sb, ws_get<double>(c, 2 * kNumSMs), ws_get<int>(c, 2 * kNumSMs), c->stream),
+                   "sumsq");
+        check_cuda(c, discarded_weight(fp[0].sigma, (int)l, &sc->total_sq, &sc->discarded, c->stream), "weight");
+        c->launches += 3;
+        if (U) copy_out(c, U, fp[0].U, m * l * sizeof(cplx));
+        if (V) copy_out(c, V, fp[0].V, n * l * sizeof(cplx));
+        copy_out(c, S, fp[0].sigma, l * sizeof(double));
+        Scalars h;
+        read_scalars(c, sc, &h);
+        *out_l = l;
+        if (certified) *certified = fp[0].certified ? 1 : 0;
+        if (discarded) *discarded = h.discarded;
+    });
+}
+
 int rrsvd_b200_fixed_rank_batch(rrsvd_b200_ctx* c, size_t count, const double* const* A, size_t m, size_t n,
                                 size_t k, size_t p, size_t q, const uint64_t* seeds, int omega_mode,
                                 double* const* U, double* const* S, double* const* V, double* discarded) {
@@ -404,10 +437,9 @@ int rrsvd_b200_decimate_unfolded(rrsvd_b200_ctx* c, const double* M, size_t d1, 
         const size_t m = d1 * cl, n = d2 * cr;
         if (m == 0 || n == 0) throw_contract(c, "decimate: theta is identically zero");
         const DecimPlan pl = plan_decimation((int)d1, (int)d2, (int)cl, (int)cr, chi_max, be->kind,
-                                             be->target_rank, be->oversampling, be->det_crossover);
+                                             be->target_rank, be->oversampling, be->det_crossover,
+                                             be->accuracy_check, be->probe_count);
         const bool randomized = pl.randomized;
-        if (randomized && be->accuracy_check)
-            throw_contract(c, "decimate: accuracy_check (fixed-precision RRSVD) is not implemented on the device yet");
         const size_t kmax = (size_t)pl.kmax;
         const auto* dM = static_cast<const cplx*>(stage_in(c, M, m * n * sizeof(cplx)));
         const auto* dll = static_cast<const double*>(stage_in(c, ll, cl * sizeof(double)));
@@ -420,9 +452,12 @@ int rrsvd_b200_decimate_unfolded(rrsvd_b200_ctx* c, const double* M, size_t d1, 
         cplx* gl = dev_gl ? reinterpret_cast<cplx*>(gamma_l) : ws_get<cplx>(c, m * kmax);
         double* lam = dev_lam ? lambda : ws_get<double>(c, kmax);
         cplx* gr = dev_gr ? reinterpret_cast<cplx*>(gamma_r) : ws_get<cplx>(c, kmax * n);
-        decimate_many(c, {DecimJob{pl, dM, (int)d1, (int)cr, dll, dlr, chi_max, trunc_tol,
-                                   (int)be->power_iterations, call_seed, omega_mode, dO, renormalize, gl, lam, gr,
-                                   reinterpret_cast<DecimScalars*>(sc)}});
+        int certified = 1;
+        DecimJob job{pl, dM, (int)d1, (int)cr, dll, dlr, chi_max, trunc_tol, (int)be->power_iterations,
+                     call_seed, omega_mode, dO, renormalize, gl, lam, gr, reinterpret_cast<DecimScalars*>(sc)};
+        job.eps = be->epsilon;
+        job.certified = &certified;
+        decimate_many(c, {job});
         Scalars h;
         read_scalars(c, sc, &h);
         if (h.nonfinite) throw_contract(c, "decimate: theta has non-finite entries");
@@ -435,7 +470,7 @@ int rrsvd_b200_decimate_unfolded(rrsvd_b200_ctx* c, const double* M, size_t d1, 
         info->discarded = h.discarded;
         info->chi = kept;
         info->randomized_path = randomized ? 1 : 0;
-        info->tolerance_certified = 1;
+        info->tolerance_certified = certified;
         info->pseudo_inverse_applied = h.pinv ? 1 : 0;
     });
 }

@@ -324,10 +324,11 @@ void evolve_core(rrsvd_b200_mps* s, rrsvd_b200_ctx* c, size_t n_sweeps, const rr
                 std::vector<void*> old_bufs;
                 for (size_t i = 0; i < nbnd; ++i) {
                     const int b = bonds[i];
+                    // with the accuracy check a bond may grow past chi_max (tebd.cpp:177-179):
+                    // its plan's kmax is then the minor dimension
                     plans[i] = plan_decimation(s->d[b], s->d[b + 1], s->dl[b], s->dr[b + 1], s->chi_max, be->kind,
-                                               be->target_rank, be->oversampling, be->det_crossover);
-                    if (plans[i].randomized && be->accuracy_check)
-                        throw_contract(c, "evolve: accuracy_check (fixed-precision RRSVD) is not implemented on the device yet");
+                                               be->target_rank, be->oversampling, be->det_crossover,
+                                               be->accuracy_check, be->probe_count);
                     seeds[i] = be->seed++;  // ascending bond order, as the reference (tebd.cpp:162)
                     gin1[i] = s->g[b];
                     gin2[i] = s->g[b + 1];
@@ -361,8 +362,10 @@ void evolve_core(rrsvd_b200_mps* s, rrsvd_b200_ctx* c, size_t n_sweeps, const rr
                         tj.push_back({gin1[i], gin2[i], ll, lin[i], lr, cl, d1, cm, d2, cr, M1});
                         const rrsvd_b200_gate* G = gates[sw * nb + b];
                         gj.push_back({G->dev, d1, d2, cl, cr, M1, M2, G->blocked ? &G->blk.dev : nullptr});
-                        dj.push_back({plans[i], M2, d1, cr, ll, lr, s->chi_max, s->tol, (int)be->power_iterations,
-                                      seeds[i], omode, nullptr, renorm, s->g[b], s->lam[b], s->g[b + 1], sc_dev + i});
+                        DecimJob job{plans[i], M2, d1, cr, ll, lr, s->chi_max, s->tol, (int)be->power_iterations,
+                                     seeds[i], omode, nullptr, renorm, s->g[b], s->lam[b], s->g[b + 1], sc_dev + i};
+                        job.eps = be->epsilon;
+                        dj.push_back(job);
                     }
                     build_theta_many(c, tj);
                     if (lane == 0) check_cuda(c, cudaEventRecord(ev[1], c->stream), "event");

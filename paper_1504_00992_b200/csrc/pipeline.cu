@@ -341,29 +341,27 @@ void small_svd_many(rrsvd_b200_ctx* c, const std::vector<SmallSvdSpec>& specs) {
 
 // ================================================================================== RRSVD
 
-void rrsvd_core_many(rrsvd_b200_ctx* c, const std::vector<RrsvdSpec>& specs) {
+void range_finder_many(rrsvd_b200_ctx* c, const std::vector<RangeSpec>& specs) {
     if (specs.empty()) return;
     struct Buf {
-        cplx *Y, *Q, *Z, *Qb, *X, *Xn, *Js;
+        cplx *Y, *Z, *Qt;
     };
     std::vector<Buf> b(specs.size());
     int max_q = 0, min_q = 1 << 30;
     for (size_t i = 0; i < specs.size(); ++i) {
-        const RrsvdSpec& s = specs[i];
+        const RangeSpec& s = specs[i];
         min_q = std::min(min_q, s.q);
-        b[i] = {ws_get<cplx>(c, (size_t)s.m * s.l), ws_get<cplx>(c, (size_t)s.m * s.l),
-                ws_get<cplx>(c, (size_t)s.n * s.l), ws_get<cplx>(c, (size_t)s.n * s.l),
-                ws_get<cplx>(c, (size_t)s.l * s.l), ws_get<cplx>(c, (size_t)s.l * s.l),
-                ws_get<cplx>(c, (size_t)s.l * s.l)};
         max_q = std::max(max_q, s.q);
+        b[i] = {ws_get<cplx>(c, (size_t)s.m * s.l), ws_get<cplx>(c, (size_t)s.n * s.l),
+                ws_get<cplx>(c, (size_t)s.n * s.l)};
     }
     std::vector<GemmSpec> gs;
     std::vector<OrthSpec> os;
-    // range finder, Algorithm 1 (randomized.cpp:88-99): Y = A Omega, QR
+    // Algorithm 1 (randomized.cpp:88-99): Y = A Omega, QR
     for (size_t i = 0; i < specs.size(); ++i) {
-        const RrsvdSpec& s = specs[i];
+        const RangeSpec& s = specs[i];
         gs.push_back({s.m, s.l, s.n, s.A, s.n, s.omega, s.l, b[i].Y, s.l});
-        os.push_back({b[i].Y, s.m, s.l, b[i].Q});
+        os.push_back({b[i].Y, s.m, s.l, s.Q});
     }
     c->gemm_tag = 2;
     gemm_many(c, kOpN, gs);
@@ -378,30 +376,45 @@ void rrsvd_core_many(rrsvd_b200_ctx* c, const std::vector<RrsvdSpec>& specs) {
     for (int j = 0; j < max_q; ++j) {
         gs.clear(); os.clear();
         for (size_t i = 0; i < specs.size(); ++i) {  // Z = A^H Q, QR
-            const RrsvdSpec& s = specs[i];
+            const RangeSpec& s = specs[i];
             if (j >= s.q) continue;
-            gs.push_back({s.n, s.l, s.m, s.A, s.n, b[i].Q, s.l, b[i].Z, s.l});
-            os.push_back({b[i].Z, s.n, s.l, b[i].Qb});
+            gs.push_back({s.n, s.l, s.m, s.A, s.n, s.Q, s.l, b[i].Z, s.l});
+            os.push_back({b[i].Z, s.n, s.l, b[i].Qt});
         }
         c->gemm_tag = 2;
         gemm_many(c, kOpC, gs);
         orth_many(c, os, inter);
         gs.clear(); os.clear();
         for (size_t i = 0; i < specs.size(); ++i) {  // Y = A Q~, QR
-            const RrsvdSpec& s = specs[i];
+            const RangeSpec& s = specs[i];
             if (j >= s.q) continue;
-            gs.push_back({s.m, s.l, s.n, s.A, s.n, b[i].Qb, s.l, b[i].Y, s.l});
-            os.push_back({b[i].Y, s.m, s.l, b[i].Q});
+            gs.push_back({s.m, s.l, s.n, s.A, s.n, b[i].Qt, s.l, b[i].Y, s.l});
+            os.push_back({b[i].Y, s.m, s.l, s.Q});
         }
         c->gemm_tag = 2;
         gemm_many(c, kOpN, gs);
         orth_many(c, os, j + 1 < max_q ? inter : kFullPasses);
     }
-    // B = Q^H A held as B^H = A^H Q = Qb X  (assemble_from_basis, randomized.cpp:57-66)
-    gs.clear(); os.clear();
+}
+
+void assemble_many(rrsvd_b200_ctx* c, const std::vector<AssembleSpec>& specs) {
+    if (specs.empty()) return;
+    struct Buf {
+        cplx *Z, *Qb, *X, *Xn, *Js;
+    };
+    std::vector<Buf> b(specs.size());
     for (size_t i = 0; i < specs.size(); ++i) {
-        const RrsvdSpec& s = specs[i];
-        gs.push_back({s.n, s.l, s.m, s.A, s.n, b[i].Q, s.l, b[i].Z, s.l});
+        const AssembleSpec& s = specs[i];
+        b[i] = {ws_get<cplx>(c, (size_t)s.n * s.l), ws_get<cplx>(c, (size_t)s.n * s.l),
+                ws_get<cplx>(c, (size_t)s.l * s.l), ws_get<cplx>(c, (size_t)s.l * s.l),
+                ws_get<cplx>(c, (size_t)s.l * s.l)};
+    }
+    // B = Q^H A held as B^H = A^H Q = Qb X  (assemble_from_basis, randomized.cpp:57-66)
+    std::vector<GemmSpec> gs;
+    std::vector<OrthSpec> os;
+    for (size_t i = 0; i < specs.size(); ++i) {
+        const AssembleSpec& s = specs[i];
+        gs.push_back({s.n, s.l, s.m, s.A, s.n, s.Q, s.l, b[i].Z, s.l});
         os.push_back({b[i].Z, s.n, s.l, b[i].Qb});
     }
     c->gemm_tag = 2;
@@ -409,7 +422,7 @@ void rrsvd_core_many(rrsvd_b200_ctx* c, const std::vector<RrsvdSpec>& specs) {
     orth_many(c, os);
     gs.clear();
     for (size_t i = 0; i < specs.size(); ++i) {  // X = Qb^H B^H  (l x l, ~upper triangular)
-        const RrsvdSpec& s = specs[i];
+        const AssembleSpec& s = specs[i];
         gs.push_back({s.l, s.l, s.n, b[i].Qb, s.l, b[i].Z, s.l, b[i].X, s.l});
     }
     c->gemm_tag = 5;
@@ -418,18 +431,162 @@ void rrsvd_core_many(rrsvd_b200_ctx* c, const std::vector<RrsvdSpec>& specs) {
     // Drmac-Veselic): X^H K = Z Sigma  =>  B = Z Sigma (Qb K)^H, so U_B = Z, V = Qb K.
     std::vector<SmallSvdSpec> ss;
     for (size_t i = 0; i < specs.size(); ++i) {
-        const RrsvdSpec& s = specs[i];
+        const AssembleSpec& s = specs[i];
         ss.push_back({b[i].X, s.l, s.l, 1, s.l, s.sigma, b[i].Xn, b[i].Js});
     }
     small_svd_many(c, ss);
     gs.clear();
     for (size_t i = 0; i < specs.size(); ++i) {
-        const RrsvdSpec& s = specs[i];
-        gs.push_back({s.m, s.l, s.l, b[i].Q, s.l, b[i].Xn, s.l, s.U, s.l});   // U = Q U_B
+        const AssembleSpec& s = specs[i];
+        gs.push_back({s.m, s.l, s.l, s.Q, s.l, b[i].Xn, s.l, s.U, s.l});   // U = Q U_B
         gs.push_back({s.n, s.l, s.l, b[i].Qb, s.l, b[i].Js, s.l, s.V, s.l});  // V = Qb K
     }
     c->gemm_tag = 5;
     gemm_many(c, kOpN, gs);
+}
+
+void rrsvd_core_many(rrsvd_b200_ctx* c, const std::vector<RrsvdSpec>& specs) {
+    if (specs.empty()) return;
+    std::vector<RangeSpec> rf;
+    std::vector<AssembleSpec> as;
+    for (const RrsvdSpec& s : specs) {
+        cplx* Q = ws_get<cplx>(c, (size_t)s.m * s.l);
+        rf.push_back({s.A, s.m, s.n, s.l, s.q, s.omega, Q});
+        as.push_back({s.A, s.m, s.n, s.l, Q, s.U, s.sigma, s.V});
+    }
+    range_finder_many(c, rf);
+    assemble_many(c, as);
+}
+
+// Fixed-precision RRSVD (randomized.cpp:124-176), all problems in lock-step rounds.  Each round
+// draws `probes` fresh Gaussian columns per active problem (seed + 0x9e3779b97f4a7c15·draw), forms
+// D = (I - Q Q^H) A Omega_p, and either certifies max_j ||D_j|| <= eps or grows the basis by l
+// columns (the probe images first, then A times fresh sketch columns) and re-orthonormalises
+// [Q, block].  The per-round decision needs the norms on the host: one small D2H per round.
+void rrsvd_fixed_precision_many(rrsvd_b200_ctx* c, std::vector<FixedPrecSpec>& specs) {
+    if (specs.empty()) return;
+    constexpr uint64_t kGolden = 0x9e3779b97f4a7c15ull;
+    const size_t np = specs.size();
+    std::vector<cplx*> Q(np);
+    std::vector<uint64_t> draw(np, 1);
+    std::vector<char> active(np, 1);
+    {
+        std::vector<RangeSpec> rf;
+        for (size_t i = 0; i < np; ++i) {
+            FixedPrecSpec& s = specs[i];
+            const int r = s.probes, minor = std::min(s.m, s.n);
+            if (r < 1) throw_contract(c, "rrsvd_fixed_precision: probe_count >= 1 required");
+            if (s.l0 < 1 || s.l0 + r > s.n)
+                throw_contract(c, "rrsvd_fixed_precision: requires initial_l + probe_count <= n");
+            (void)minor;
+            s.l = s.l0;
+            s.certified = false;
+            Q[i] = ws_get<cplx>(c, (size_t)s.m * s.l);
+            const cplx* om = s.omega0;
+            if (om == nullptr) {
+                cplx* o = ws_get<cplx>(c, (size_t)s.n * s.l);
+                make_omega(c, s.n, s.l, s.seed, s.omega_mode, o);
+                om = o;
+            }
+            rf.push_back({s.A, s.m, s.n, s.l, s.q, om, Q[i]});
+        }
+        range_finder_many(c, rf);
+    }
+    double* dmax = ws_get<double>(c, np);
+    auto* hmax = static_cast<double*>(pinned_scratch(c, np * sizeof(double)));
+    while (true) {
+        std::vector<size_t> act;
+        for (size_t i = 0; i < np; ++i)
+            if (active[i]) act.push_back(i);
+        if (act.empty()) break;
+        std::vector<cplx*> Bp(np, nullptr), QhB(np, nullptr), Dm(np, nullptr);
+        std::vector<GemmSpec> g1, g2, g3;
+        for (size_t i : act) {
+            FixedPrecSpec& s = specs[i];
+            const int r = s.probes;
+            cplx* om = ws_get<cplx>(c, (size_t)s.n * r);
+            make_omega(c, s.n, r, s.seed + kGolden * draw[i], s.omega_mode, om);
+            ++draw[i];
+            Bp[i] = ws_get<cplx>(c, (size_t)s.m * r);
+            QhB[i] = ws_get<cplx>(c, (size_t)s.l * r);
+            Dm[i] = ws_get<cplx>(c, (size_t)s.m * r);
+            g1.push_back({s.m, r, s.n, s.A, s.n, om, r, Bp[i], r});           // B = A Omega_p
+            g2.push_back({s.l, r, s.m, Q[i], s.l, Bp[i], r, QhB[i], r});      // Q^H B
+            GemmSpec d{s.m, r, s.l, Q[i], s.l, QhB[i], r, Dm[i], r};         // D = B - Q (Q^H B)
+            d.D = Bp[i];
+            d.ldd = r;
+            d.alpha = -1.0;
+            g3.push_back(d);
+        }
+        c->gemm_tag = 7;
+        gemm_many(c, kOpN, g1);
+        gemm_many(c, kOpC, g2);
+        gemm_many(c, kOpN, g3);
+        ColNormBatch cn{};
+        std::vector<size_t> slot(np, 0);
+        for (size_t t = 0; t < act.size(); ++t) {
+            const size_t i = act[t];
+            const int k = cn.count++;
+            cn.D[k] = Dm[i]; cn.m[k] = specs[i].m; cn.r[k] = specs[i].probes; cn.out[k] = dmax + t;
+            if (cn.count == kMaxSmall) {
+                check_cuda(c, colnorm_max_many(cn, c->stream), "colnorm_max");
+                c->launches++;
+                cn = ColNormBatch{};
+            }
+        }
+        if (cn.count) {
+            check_cuda(c, colnorm_max_many(cn, c->stream), "colnorm_max");
+            c->launches++;
+        }
+        check_cuda(c, cudaMemcpyAsync(hmax, dmax, act.size() * sizeof(double), cudaMemcpyDeviceToHost, c->stream),
+                   "D2H");
+        check_cuda(c, cudaStreamSynchronize(c->stream), "sync");
+        std::vector<OrthSpec> os;
+        std::vector<GemmSpec> gx;
+        std::vector<int> grown(np, 0);
+        for (size_t t = 0; t < act.size(); ++t) {
+            const size_t i = act[t];
+            FixedPrecSpec& s = specs[i];
+            const int r = s.probes, minor = std::min(s.m, s.n);
+            if (hmax[t] <= s.eps) {
+                s.certified = true;
+                active[i] = 0;
+                continue;
+            }
+            if (s.l + r > minor) { active[i] = 0; continue; }
+            const int grow = std::min(s.l, minor - s.l);  // growth_block 0: double the basis
+            if (grow == 0) { active[i] = 0; continue; }
+            const int ln = s.l + grow, from_probe = std::min(r, grow);
+            cplx* Qn = ws_get<cplx>(c, (size_t)s.m * ln);
+            check_cuda(c, cudaMemcpy2DAsync(Qn, ln * sizeof(cplx), Q[i], s.l * sizeof(cplx), s.l * sizeof(cplx),
+                                            s.m, cudaMemcpyDeviceToDevice, c->stream), "copy");
+            check_cuda(c, cudaMemcpy2DAsync(Qn + s.l, ln * sizeof(cplx), Bp[i], r * sizeof(cplx),
+                                            from_probe * sizeof(cplx), s.m, cudaMemcpyDeviceToDevice, c->stream),
+                       "copy");
+            if (grow > from_probe) {
+                const int ne = grow - from_probe;
+                cplx* om = ws_get<cplx>(c, (size_t)s.n * ne);
+                make_omega(c, s.n, ne, s.seed + kGolden * draw[i], s.omega_mode, om);
+                ++draw[i];
+                gx.push_back({s.m, ne, s.n, s.A, s.n, om, ne, Qn + s.l + from_probe, ln});
+            }
+            os.push_back({Qn, s.m, ln, Qn});
+            Q[i] = Qn;
+            s.l = ln;
+        }
+        c->gemm_tag = 7;
+        gemm_many(c, kOpN, gx);
+        orth_many(c, os);
+    }
+    std::vector<AssembleSpec> as;
+    for (size_t i = 0; i < np; ++i) {
+        FixedPrecSpec& s = specs[i];
+        s.U = ws_get<cplx>(c, (size_t)s.m * s.l);
+        s.V = ws_get<cplx>(c, (size_t)s.n * s.l);
+        s.sigma = ws_get<double>(c, s.l);
+        as.push_back({s.A, s.m, s.n, s.l, Q[i], s.U, s.sigma, s.V});
+    }
+    assemble_many(c, as);
 }
 
 void rrsvd_core(rrsvd_b200_ctx* c, const cplx* A, int m, int n, int l, int q, const cplx* omega,
@@ -488,7 +645,7 @@ void svd_jacobi(rrsvd_b200_ctx* c, const cplx* A, int m, int n, cplx* U, double*
 // ================================================================================== TEBD trio
 
 DecimPlan plan_decimation(int d1, int d2, int cl, int cr, size_t chi_max, int kind, size_t target_rank,
-                          size_t oversampling, size_t det_crossover) {
+                          size_t oversampling, size_t det_crossover, int accuracy_check, size_t probe_count) {
     DecimPlan p{};
     p.m = d1 * cl;
     p.n = d2 * cr;
@@ -501,9 +658,15 @@ DecimPlan plan_decimation(int d1, int d2, int cl, int cr, size_t chi_max, int ki
         const size_t pp = oversampling != 0 ? oversampling : k;            // tebd.cpp:171
         p.l = (int)std::min<size_t>(k + pp, (size_t)p.minor);              // tebd.cpp:172
         p.ns = p.l;
+        // tebd.cpp:173: the accuracy check runs when the probes fit beside the sketch
+        p.fixed_precision = accuracy_check && (size_t)p.l + probe_count <= (size_t)p.n &&
+                            (size_t)p.l + probe_count <= (size_t)p.minor;
+        p.probes = (int)probe_count;
+        if (p.fixed_precision) p.ns = p.minor;  // the basis may grow up to the minor dimension
     }
     p.kmax = p.ns;
-    if (chi_max != 0) p.kmax = (int)std::min<size_t>((size_t)p.kmax, chi_max);
+    // the accuracy check owns the retained rank: no chi_max cap (tebd.cpp:177-179)
+    if (chi_max != 0 && !p.fixed_precision) p.kmax = (int)std::min<size_t>((size_t)p.kmax, chi_max);
     return p;
 }
 
@@ -632,8 +795,28 @@ void decimate_many(rrsvd_b200_ctx* c, const std::vector<DecimJob>& jobs) {
         double* sig;
     };
     std::vector<Out> outs(jobs.size());
+    std::vector<int> ns(jobs.size());
     std::vector<RrsvdSpec> rs;
     std::vector<SvdSpec> ds;
+    // fixed-precision bonds first: their data-dependent width is settled on the host
+    std::vector<FixedPrecSpec> fp;
+    std::vector<size_t> fp_job;
+    for (size_t i = 0; i < jobs.size(); ++i) {
+        const DecimJob& j = jobs[i];
+        ns[i] = j.pl.ns;
+        if (!j.pl.fixed_precision) continue;
+        FixedPrecSpec f{j.M, j.pl.m, j.pl.n, j.pl.l, j.q, j.pl.probes, j.eps, j.seed, j.omega_mode};
+        f.omega0 = j.omega;
+        fp.push_back(f);
+        fp_job.push_back(i);
+    }
+    rrsvd_fixed_precision_many(c, fp);
+    for (size_t t = 0; t < fp.size(); ++t) {
+        const size_t i = fp_job[t];
+        outs[i] = {fp[t].U, fp[t].V, fp[t].sigma};
+        ns[i] = fp[t].l;
+        if (jobs[i].certified) *jobs[i].certified = fp[t].certified ? 1 : 0;
+    }
     // ‖Θ‖² + finite check for every bond: one launch pair per 64 bonds (tebd.cpp:156-160)
     for (size_t base = 0; base < jobs.size(); base += kMaxSmall) {
         SumsqBatch sb{};
@@ -658,6 +841,7 @@ void decimate_many(rrsvd_b200_ctx* c, const std::vector<DecimJob>& jobs) {
     for (size_t i = 0; i < jobs.size(); ++i) {
         const DecimJob& j = jobs[i];
         const DecimPlan& pl = j.pl;
+        if (pl.fixed_precision) continue;
         outs[i] = {ws_get<cplx>(c, (size_t)pl.m * pl.ns), ws_get<cplx>(c, (size_t)pl.n * pl.ns),
                    ws_get<double>(c, pl.ns)};
         if (pl.randomized) {
@@ -691,15 +875,16 @@ void decimate_many(rrsvd_b200_ctx* c, const std::vector<DecimJob>& jobs) {
             const DecimPlan& pl = j.pl;
             TruncArgs& ta = tb.a[tb.count++];
             ta = TruncArgs{};
-            ta.sigma = outs[i].sig; ta.ns = pl.ns; ta.total_sq = &j.sc->total_sq; ta.trunc_tol = j.trunc_tol;
-            ta.cap = (long long)j.chi_max; ta.renormalize = j.renormalize; ta.kept = &j.sc->kept;
+            ta.sigma = outs[i].sig; ta.ns = ns[i]; ta.total_sq = &j.sc->total_sq; ta.trunc_tol = j.trunc_tol;
+            ta.cap = pl.fixed_precision ? 0 : (long long)j.chi_max;
+            ta.renormalize = j.renormalize; ta.kept = &j.sc->kept;
             ta.lambda = j.lambda; ta.discarded = &j.sc->discarded;
             GammaArgs& ga = gb.a[gb.count++];
             ga = GammaArgs{};
-            ga.U = outs[i].U; ga.ldu = pl.ns; ga.V = outs[i].V; ga.ldv = pl.ns; ga.ll = j.ll; ga.lr = j.lr;
+            ga.U = outs[i].U; ga.ldu = ns[i]; ga.V = outs[i].V; ga.ldv = ns[i]; ga.ll = j.ll; ga.lr = j.lr;
             ga.m = pl.m; ga.n = pl.n; ga.d1 = j.d1; ga.cr = j.cr; ga.kept = &j.sc->kept;
             ga.gamma_l = j.gamma_l; ga.gamma_r = j.gamma_r; ga.pinv = &j.sc->pinv;
-            gb.max_kept = std::max(gb.max_kept, pl.kmax);
+            gb.max_kept = std::max(gb.max_kept, pl.fixed_precision ? ns[i] : pl.kmax);
             gb.max_m = std::max(gb.max_m, pl.m);
             gb.max_n = std::max(gb.max_n, pl.n);
         }

@@ -77,6 +77,44 @@ struct RrsvdSpec {
     cplx* V;
 };
 void rrsvd_core_many(rrsvd_b200_ctx* c, const std::vector<RrsvdSpec>& specs);
+
+// The two halves of rrsvd_core: the range finder (randomized.cpp:88-99) producing an
+// orthonormal Q (m x l), and assemble_from_basis (randomized.cpp:57-66): U (m x l), sigma, V.
+struct RangeSpec {
+    const cplx* A;
+    int m, n, l, q;
+    const cplx* omega;
+    cplx* Q;
+};
+void range_finder_many(rrsvd_b200_ctx* c, const std::vector<RangeSpec>& specs);
+struct AssembleSpec {
+    const cplx* A;
+    int m, n, l;
+    const cplx* Q;
+    cplx* U;
+    double* sigma;
+    cplx* V;
+};
+void assemble_many(rrsvd_b200_ctx* c, const std::vector<AssembleSpec>& specs);
+
+// Fixed-precision RRSVD with the probabilistic accuracy check and basis growth
+// (randomized.cpp:124-176, growth_block 0).  Inputs: A, m, n, l0 (initial width), q, probes, eps,
+// seed, omega_mode.  Outputs (host-visible after the call): l (final width), certified, and
+// workspace device buffers U (m x l), sigma (l), V (n x l).  Synchronises once per round.
+struct FixedPrecSpec {
+    const cplx* A;
+    int m, n, l0, q, probes;
+    double eps;
+    uint64_t seed;
+    int omega_mode;
+    const cplx* omega0 = nullptr;  // nullable: the initial n x l0 sketch, fed instead of drawn
+    int l = 0;
+    bool certified = false;
+    cplx* U = nullptr;
+    double* sigma = nullptr;
+    cplx* V = nullptr;
+};
+void rrsvd_fixed_precision_many(rrsvd_b200_ctx* c, std::vector<FixedPrecSpec>& specs);
 void rrsvd_core(rrsvd_b200_ctx* c, const cplx* A, int m, int n, int l, int q, const cplx* omega,
                 cplx* U, double* sigma, cplx* V);
 
@@ -105,12 +143,15 @@ struct DecimScalars {
 struct DecimPlan {  // host-side decisions of decimate (tebd.cpp:144-186)
     int m, n, minor;
     bool randomized;
-    int l;      // sketch width (randomized) ; ns = l or minor
-    int ns;
-    int kmax;   // upper bound on the kept rank
+    bool fixed_precision;  // accuracy check with bond growth (tebd.cpp:173-179)
+    int probes;
+    int l;      // (initial) sketch width (randomized) ; ns = l or minor
+    int ns;     // singular values produced (an upper bound when fixed_precision)
+    int kmax;   // upper bound on the kept rank (no chi_max cap when fixed_precision)
 };
 DecimPlan plan_decimation(int d1, int d2, int cl, int cr, size_t chi_max, int kind, size_t target_rank,
-                          size_t oversampling, size_t det_crossover);
+                          size_t oversampling, size_t det_crossover, int accuracy_check = 0,
+                          size_t probe_count = 0);
 
 // One decimation of an unfolded M (tebd.cpp:141-237): norm, factorization (RRSVD or Jacobi),
 // truncation, λ renormalisation, Γ reshape.  Writes gamma_l (m x kept), lambda (kept),
@@ -132,6 +173,8 @@ struct DecimJob {
     double* lambda;
     cplx* gamma_r;
     DecimScalars* sc;
+    double eps = 0.0;          // accuracy-check tolerance (fixed_precision plans)
+    int* certified = nullptr;  // host, nullable: tolerance_certified (fixed_precision plans)
 };
 void decimate_many(rrsvd_b200_ctx* c, const std::vector<DecimJob>& jobs);
 

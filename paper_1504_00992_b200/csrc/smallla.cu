@@ -404,6 +404,28 @@ __global__ void __launch_bounds__(JAC_THREADS) jacobi_global_kernel(cplx* __rest
     if (blockIdx.x == 0 && threadIdx.x == 0 && sweeps_out != nullptr) *sweeps_out = sweep + 1;
 }
 
+__global__ void __launch_bounds__(256) colnorm_max_kernel(const __grid_constant__ ColNormBatch b) {
+    const int p = blockIdx.x;
+    const int m = b.m[p], r = b.r[p];
+    const cplx* D = b.D[p];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    __shared__ double wmax[8];
+    double mx = 0.0;
+    for (int j = warp; j < r; j += 8) {
+        double a = 0.0;
+        for (int i = lane; i < m; i += 32) a += cabs2(D[(long long)i * r + j]);
+        a = warp_sum(a);
+        mx = fmax(mx, sqrt(a));
+    }
+    if (lane == 0) wmax[warp] = mx;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double v = 0.0;
+        for (int w = 0; w < 8; ++w) v = fmax(v, wmax[w]);
+        *b.out[p] = v;
+    }
+}
+
 __global__ void jacobi_init_kernel(const __grid_constant__ JacobiInitBatch b) {
     const int p = blockIdx.y;
     const int r = b.r[p], c = b.c[p], ld = r + c;
@@ -566,6 +588,12 @@ cudaError_t jacobi_svd_global(cplx* W, int r, int c, int* counters, int* sweeps,
     void* args[] = {&W, &r, &c, &counters, &sweeps};
     e = cudaLaunchCooperativeKernel((const void*)jacobi_global_kernel, dim3(grid), dim3(JAC_THREADS), args, 0, s);
     if (e != cudaSuccess) return e;
+    return cudaGetLastError();
+}
+
+cudaError_t colnorm_max_many(const ColNormBatch& b, cudaStream_t s) {
+    if (b.count == 0) return cudaSuccess;
+    colnorm_max_kernel<<<b.count, 256, 0, s>>>(b);
     return cudaGetLastError();
 }
 

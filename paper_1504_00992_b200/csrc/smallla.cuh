@@ -39,6 +39,16 @@ struct CholBatch {
 cudaError_t chol_inv(const CholBatch& b, int max_l, cudaStream_t s);
 bool jacobi_fits(int r, int c);  // an r x c problem fits jacobi_svd's on-chip capacity
 
+// ---- max_j ||D[:, j]|| of row-major m x r matrices (the accuracy check's probe residuals,
+// randomized.cpp:47-53,149-150); one CTA per matrix, fixed reduction order.
+struct ColNormBatch {
+    int count;
+    const cplx* D[kMaxSmall];
+    int m[kMaxSmall], r[kMaxSmall];
+    double* out[kMaxSmall];
+};
+cudaError_t colnorm_max_many(const ColNormBatch& b, cudaStream_t s);
+
 // ---- One-sided (Hestenes) Jacobi SVD ------------------------------------------------------
 // Works on W (column-major, ld = r + c): rows [0, r) hold X (r x c), rows [r, r + c) hold the
 // accumulated rotations J (initialised to I).  On exit X·J_total has orthogonal columns.

@@ -167,6 +167,54 @@ def test_fixed_rank_batch_matches_single_calls(ctx, ref):
         assert np.linalg.norm(rec - rec_r) / np.linalg.norm(rec_r) < 1e-9
 
 
+@pytest.mark.parametrize("case", ["certified_at_once", "grows", "uncertifiable"])
+def test_fixed_precision_matches_reference(ctx, ref, case):
+    """rrsvd_fixed_precision (randomized.cpp:124-176): same final width l, same certification,
+    σ within 1e-10·σ1, w within 1e-12, gauge-invariant reconstruction within 1e-9."""
+    n = 400
+    if case == "certified_at_once":
+        a = ref.structured_matrix(0.7 ** np.arange(n), n, 3, 4)
+        eps, l0 = 1e-3, 40
+    elif case == "grows":
+        a = ref.structured_matrix(0.97 ** np.arange(n), n, 5, 6)
+        eps, l0 = 1e-3, 20
+    else:  # wide 300 x 400: l 148 -> 296, then 296 + 10 > minor stops the growth uncertified
+        a = cplx_randn(np.random.default_rng(8), 300, n)
+        eps, l0 = 1e-9, 148
+    res = P.rrsvd_fixed_precision(a, eps, 10, l0, 2, 17, ctx=ctx)
+    u_r, s_r, v_r, w_r, cert_r = ref.fixed_precision(a, eps, 10, l0, 2, 17)
+    assert res.achieved_rank == len(s_r)
+    assert res.tolerance_certified == cert_r
+    if case == "grows":
+        assert len(s_r) > l0 and cert_r
+    if case == "uncertifiable":
+        assert not cert_r
+    assert np.max(np.abs(res.sigma - s_r)) <= 1e-10 * s_r[0]
+    assert abs(res.discarded_weight - w_r) < 1e-12
+    k = int(np.sum(s_r > 1e-12 * s_r[0]))
+    rec = (res.u[:, :k] * res.sigma[:k]) @ res.v[:, :k].conj().T
+    rec_r = (u_r[:, :k] * s_r[:k]) @ v_r[:, :k].conj().T
+    assert np.linalg.norm(rec - rec_r) / np.linalg.norm(rec_r) < 1e-9
+
+
+def test_decimate_accuracy_check_grows_past_chi_max(ctx, ref):
+    """decimate with the accuracy check (tebd.cpp:173-179): the bond grows past chi_max."""
+    rng = np.random.default_rng(44)
+    g1, g2, ll, lm, lr = random_fragment(rng, 40, 4, 40, 4, 40, decay=0.9)
+    gate, _ = np.linalg.qr(cplx_randn(rng, 16, 16))
+    theta = ref.apply_gate(ref.build_theta(g1, g2, ll, lm, lr), gate)
+    kw = dict(randomized=True, target_rank=10, oversampling=10, power_iterations=2, det_crossover=0,
+              accuracy_check=True, epsilon=1e-4, probe_count=10, seed=3)
+    got = P.decimate(theta, ll, lr, 20, 0.0, P.DecimationBackend(**kw), ctx=ctx)
+    want = ref.decimate(theta, ll, lr, 20, 0.0, ref.Backend(**kw))
+    assert want.chi > 20 and got.chi == want.chi
+    assert got.tolerance_certified == want.tolerance_certified
+    assert np.max(np.abs(np.asarray(got.lam) - want.lam)) < 1e-10
+    assert abs(got.discarded - want.discarded) < 1e-10
+    rec_g, rec_r = theta_from(got, ll, lr), theta_from(want, ll, lr)
+    assert np.linalg.norm(rec_g - rec_r) / np.linalg.norm(rec_r) < 1e-9
+
+
 def test_sketched_svd_lowrank_exact(ctx):
     """test_randomized.cpp:91-101: exact low-rank input — σ recovered to 1e-10."""
     rng = np.random.default_rng(11)

@@ -62,6 +62,21 @@ def test_ising_randomized_reference_stream(ref):
     observables_match(rm, dm, [Mdl.SZ] * n)
 
 
+def test_ising_fixed_precision_bond_growth(ref):
+    """Accuracy check on (tebd.cpp:173-179): k=p=4 sketches that fail the probe test grow past
+    chi_max; χ profile, kept fraction and observables follow the reference (reference Ω stream,
+    probes seeded seed + φ·draw as randomized.cpp:136-140)."""
+    n, dt, steps, chi = 8, 0.05, 10, 6
+    terms = Mdl.ising_terms(n, 1.0, 0.7)
+    kw = dict(randomized=True, target_rank=4, oversampling=4, power_iterations=2, det_crossover=0,
+              accuracy_check=True, epsilon=1e-6, probe_count=2, seed=9)
+    rm, dm, rd, dd = run_both(ref, [2] * n, terms, dt, steps, chi, kw)
+    assert rd["max_bond_dim"] > chi  # the check actually grew bonds past the cap
+    assert dd.max_bond_dim == rd["max_bond_dim"]
+    assert abs(dd.kept_fraction - rd["kept_fraction"]) < 1e-8
+    observables_match(rm, dm, [Mdl.SZ] * n)
+
+
 def test_tedopa_small_chain(ref):
     """A short spin-boson TEDOPA chain (config-3 model at small d, χ): system ⟨σz⟩ and boson
     occupations ⟨n⟩ within 1e-8; randomized path on the wide bonds."""
