@@ -93,6 +93,14 @@ int rrsvd_b200_zgemm(rrsvd_b200_ctx* ctx, int op_a, int op_b, size_t m, size_t n
  * (linalg.cpp:49-65).  Like the reference, rank-deficient A yields no NaN; dependent columns
  * of Q come back as zero columns instead of an arbitrary orthonormal completion. */
 int rrsvd_b200_qr(rrsvd_b200_ctx* ctx, const double* A, size_t m, size_t n, double* Q, double* R);
+/* One shifted-CholeskyQR factor step on an already-formed (e.g. all-reduced) Gram matrix:
+ * T = R^-1 (l x l, upper) with G + s I = R^H R, s = shift_scale * 2^-53 * trace(G) (0: none;
+ * the CholeskyQR passes use 10 * (rows + l)).  Only the upper triangle of G is read.
+ * Non-positive pivots mark dependent columns: their T columns are zero, *ndead counts them.
+ * The building block of the row-sharded QR (linalg.cpp:49-65 over a distributed Y). */
+int rrsvd_b200_chol_inv(rrsvd_b200_ctx* ctx, const double* G, size_t l, double shift_scale,
+                        double* T, int* ndead);
+
 /* Full economy SVD A = U diag(S) V^H (U m x r, S r, V n x r, r = min(m,n)), S non-increasing;
  * replaces rrsvd::svd_full (linalg.cpp:67-88).  One-sided Jacobi on the device. */
 int rrsvd_b200_svd(rrsvd_b200_ctx* ctx, const double* A, size_t m, size_t n, double* U,

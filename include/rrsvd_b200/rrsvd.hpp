@@ -113,10 +113,15 @@ struct SvdResult {
     bool tolerance_certified = true;
 };
 
-// randomized.hpp:17-28
+// randomized.hpp:17-35
 struct RrsvdParams {
     std::size_t target_rank, oversampling, power_iterations;
     std::uint64_t seed;
+};
+struct AccuracyCheckParams {
+    double tolerance;
+    std::size_t probe_count;
+    std::size_t growth_block = 0;  // the device path implements the reference default (doubling)
 };
 
 // ---- linalg.hpp:29-56 (device) ----------------------------------------------------------
@@ -192,6 +197,30 @@ inline SvdResult rrsvd_fixed_rank(const DenseMatrix& a, const RrsvdParams& p) {
                                       b200::D(out.u.data()), out.sigma.data(), b200::D(out.v.data()),
                                       &out.discarded_weight), a.rows(), a.cols());
     out.achieved_rank = k;
+    return out;
+}
+
+inline SvdResult rrsvd_fixed_precision(const DenseMatrix& a, const AccuracyCheckParams& check,
+                                       std::size_t initial_l, std::size_t q, std::uint64_t seed) {
+    if (check.growth_block != 0)
+        throw contract_violation("rrsvd_fixed_precision: the device path grows by doubling (growth_block 0)");
+    const std::size_t mn = std::min(a.rows(), a.cols());
+    std::vector<cplx> u(a.rows() * mn), v(a.cols() * mn);
+    std::vector<double> s(mn);
+    std::size_t l = 0;
+    int cert = 0;
+    SvdResult out;
+    b200::check(rrsvd_b200_fixed_precision(b200::context(), b200::D(a.data()), a.rows(), a.cols(), initial_l, q,
+                                           check.probe_count, check.tolerance, seed, RRSVD_B200_OMEGA_REFERENCE,
+                                           b200::D(u.data()), s.data(), b200::D(v.data()), &l, &cert,
+                                           &out.discarded_weight), a.rows(), a.cols());
+    out.u = DenseMatrix(a.rows(), l);
+    out.v = DenseMatrix(a.cols(), l);
+    std::copy_n(u.begin(), a.rows() * l, out.u.data());
+    std::copy_n(v.begin(), a.cols() * l, out.v.data());
+    out.sigma.assign(s.begin(), s.begin() + static_cast<std::ptrdiff_t>(l));
+    out.achieved_rank = l;
+    out.tolerance_certified = cert != 0;
     return out;
 }
 

@@ -181,6 +181,26 @@ int rrsvd_b200_qr(rrsvd_b200_ctx* c, const double* A, size_t m, size_t n, double
     });
 }
 
+int rrsvd_b200_chol_inv(rrsvd_b200_ctx* c, const double* G, size_t l, double shift_scale, double* T,
+                        int* ndead) {
+    return api(c, [&] {
+        if (l == 0) return;
+        if (G == nullptr || T == nullptr) throw_contract(c, "chol_inv: null argument");
+        std::vector<OutBuf> outs;
+        // the factorization works in place: always on a workspace copy of G
+        auto* dG = ws_get<cplx>(c, l * l);
+        check_cuda(c, cudaMemcpyAsync(dG, G, l * l * sizeof(cplx), cudaMemcpyDefault, c->stream), "copy G");
+        auto* dT = static_cast<cplx*>(stage_out(c, T, l * l * sizeof(cplx), outs));
+        int* dn = ws_get<int>(c, 1);
+        chol_inv_many(c, {CholSpec{dG, (int)l, shift_scale, dT, dn}});
+        finish_out(c, outs);
+        int h = 0;
+        check_cuda(c, cudaMemcpyAsync(&h, dn, sizeof(int), cudaMemcpyDeviceToHost, c->stream), "D2H");
+        check_cuda(c, cudaStreamSynchronize(c->stream), "sync");
+        if (ndead) *ndead = h;
+    });
+}
+
 int rrsvd_b200_svd(rrsvd_b200_ctx* c, const double* A, size_t m, size_t n, double* U, double* S,
                    double* V) {
     return api(c, [&] {

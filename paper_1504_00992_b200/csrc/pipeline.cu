@@ -107,24 +107,18 @@ CholBlocking chol_blocking(int l) {
     return cbk;
 }
 
-void orth_many(rrsvd_b200_ctx* c, const std::vector<OrthSpec>& specs, int passes) {
+void chol_inv_many(rrsvd_b200_ctx* c, const std::vector<CholSpec>& specs) {
     if (specs.empty()) return;
     struct Buf {
-        cplx *G, *T, *a, *b;
         CholBlocking blk;
-        cplx *R, *W;      // blocked path only
+        cplx *R, *W;  // blocked path only
         double* shift;
     };
     std::vector<Buf> bufs(specs.size());
     int max_nbk = 1;
     for (size_t i = 0; i < specs.size(); ++i) {
-        const OrthSpec& s = specs[i];
-        if (s.m < s.l) throw_contract(c, "qr: requires rows >= cols");
+        const CholSpec& s = specs[i];
         Buf& b = bufs[i];
-        b.G = ws_get<cplx>(c, (size_t)s.l * s.l);
-        b.T = ws_get<cplx>(c, (size_t)s.l * s.l);
-        b.a = ws_get<cplx>(c, (size_t)s.m * s.l);
-        b.b = ws_get<cplx>(c, (size_t)s.m * s.l);
         b.blk = chol_blocking(s.l);
         b.R = b.W = nullptr;
         b.shift = nullptr;
@@ -132,10 +126,103 @@ void orth_many(rrsvd_b200_ctx* c, const std::vector<OrthSpec>& specs, int passes
             b.R = ws_get<cplx>(c, (size_t)s.l * s.l);
             b.W = ws_get<cplx>(c, (size_t)b.blk.bsz * s.l);
             b.shift = ws_get<double>(c, 1);
-            // the strictly lower blocks of T stay zero for every pass
-            check_cuda(c, cudaMemsetAsync(b.T, 0, (size_t)s.l * s.l * sizeof(cplx), c->stream), "memset");
+            // the strictly lower blocks of T are never written
+            check_cuda(c, cudaMemsetAsync(s.T, 0, (size_t)s.l * s.l * sizeof(cplx), c->stream), "memset");
             max_nbk = std::max(max_nbk, b.blk.nbk);
         }
+    }
+    auto chol_launch = [&](CholBatch& cb, int max_l) {
+        check_cuda(c, chol_inv(cb, max_l, c->stream), "chol_inv");
+        c->launches++;
+        cb = CholBatch{};
+    };
+    auto off = [](int l, int r0, int c0) { return (size_t)r0 * l + c0; };
+    for (int J = 0; J < max_nbk; ++J) {
+        CholBatch cb{};
+        int max_l = 0;
+        for (size_t i = 0; i < specs.size(); ++i) {
+            const CholSpec& s = specs[i];
+            const Buf& b = bufs[i];
+            if (J >= b.blk.nbk) continue;
+            const int j0 = b.blk.begin(J), w = b.blk.width(J, s.l);
+            const int k = cb.count++;
+            cb.l[k] = w;
+            cb.G[k] = s.G + off(s.l, j0, j0);
+            cb.ldg[k] = s.l;
+            cb.trace_src[k] = s.G; cb.trace_n[k] = s.l; cb.trace_ld[k] = s.l;
+            if (b.blk.nbk > 1) {
+                if (J == 0) cb.shift_save[k] = b.shift;
+                else cb.shift_use[k] = b.shift;
+            }
+            cb.T[k] = s.T + off(s.l, j0, j0);
+            cb.ldt[k] = s.l;
+            cb.shift_scale[k] = s.shift_scale;
+            cb.dep_tol[k] = 0.0;
+            cb.ndead[k] = s.ndead;
+            cb.ndead_acc[k] = J > 0 ? 1 : 0;
+            max_l = std::max(max_l, w);
+            if (cb.count == kMaxSmall) { chol_launch(cb, max_l); max_l = 0; }
+        }
+        if (cb.count) chol_launch(cb, max_l);
+        std::vector<GemmSpec> g1, g2;
+        for (size_t i = 0; i < specs.size(); ++i) {
+            const CholSpec& s = specs[i];
+            const Buf& b = bufs[i];
+            if (J + 1 >= b.blk.nbk) continue;
+            const int j0 = b.blk.begin(J), w = b.blk.width(J, s.l), r0 = j0 + w, rest = s.l - r0;
+            // R_J,>J = T_JJ^H G_J,>J
+            g1.push_back({w, rest, w, s.T + off(s.l, j0, j0), s.l, s.G + off(s.l, j0, r0), s.l,
+                          b.R + off(s.l, j0, r0), s.l});
+            // G_>J,>J -= R_J,>J^H R_J,>J  (upper part, in place)
+            GemmSpec up{rest, rest, w, b.R + off(s.l, j0, r0), s.l, b.R + off(s.l, j0, r0), s.l,
+                        s.G + off(s.l, r0, r0), s.l};
+            up.structure = kUpperC;
+            up.D = s.G + off(s.l, r0, r0);
+            up.ldd = s.l;
+            up.alpha = -1.0;
+            g2.push_back(up);
+        }
+        if (!g1.empty()) {
+            c->gemm_tag = 3;
+            gemm_many(c, kOpC, g1);
+            gemm_many(c, kOpC, g2);
+        }
+    }
+    for (int I = max_nbk - 2; I >= 0; --I) {
+        std::vector<GemmSpec> g1, g2;
+        for (size_t i = 0; i < specs.size(); ++i) {
+            const CholSpec& s = specs[i];
+            const Buf& b = bufs[i];
+            if (I + 1 >= b.blk.nbk) continue;
+            const int i0 = b.blk.begin(I), w = b.blk.width(I, s.l), r0 = i0 + w, rest = s.l - r0;
+            // W = R_I,>I T_>I,>I  (T upper triangular)
+            GemmSpec ws{w, rest, rest, b.R + off(s.l, i0, r0), s.l, s.T + off(s.l, r0, r0), s.l, b.W, rest};
+            ws.structure = kTriB;
+            g1.push_back(ws);
+            // T_I,>I = -T_II W
+            GemmSpec ts{w, rest, w, s.T + off(s.l, i0, i0), s.l, b.W, rest, s.T + off(s.l, i0, r0), s.l};
+            ts.alpha = -1.0;
+            g2.push_back(ts);
+        }
+        if (!g1.empty()) {
+            c->gemm_tag = 4;
+            gemm_many(c, kOpN, g1);
+            gemm_many(c, kOpN, g2);
+        }
+    }
+}
+
+void orth_many(rrsvd_b200_ctx* c, const std::vector<OrthSpec>& specs, int passes) {
+    if (specs.empty()) return;
+    struct Buf {
+        cplx *G, *T, *a, *b;
+    };
+    std::vector<Buf> bufs(specs.size());
+    for (size_t i = 0; i < specs.size(); ++i) {
+        const OrthSpec& s = specs[i];
+        if (s.m < s.l) throw_contract(c, "qr: requires rows >= cols");
+        bufs[i] = {ws_get<cplx>(c, (size_t)s.l * s.l), ws_get<cplx>(c, (size_t)s.l * s.l),
+                   ws_get<cplx>(c, (size_t)s.m * s.l), ws_get<cplx>(c, (size_t)s.m * s.l)};
     }
     std::vector<const cplx*> cur(specs.size());
     for (size_t i = 0; i < specs.size(); ++i) cur[i] = specs[i].Y;
@@ -146,95 +233,20 @@ void orth_many(rrsvd_b200_ctx* c, const std::vector<OrthSpec>& specs, int passes
     // pivots mark a dependent (zero) column, as Householder QR keeps tiny directions too.
     const int last = passes - 1;
     const int shifted = std::min(passes, 2);
-    auto chol_launch = [&](CholBatch& cb, int max_l) {
-        check_cuda(c, chol_inv(cb, max_l, c->stream), "chol_inv");
-        c->launches++;
-        cb = CholBatch{};
-    };
-    auto off = [](int l, int r0, int c0) { return (size_t)r0 * l + c0; };
     for (int pass = 0; pass < passes; ++pass) {
         std::vector<GemmSpec> gram, apply;
+        std::vector<CholSpec> chol;
         for (size_t i = 0; i < specs.size(); ++i) {
             const OrthSpec& s = specs[i];
             GemmSpec gsp{s.l, s.l, s.m, cur[i], s.l, cur[i], s.l, bufs[i].G, s.l};
             gsp.structure = kUpperC;  // chol_inv reads only the upper triangle of G
             gram.push_back(gsp);
+            chol.push_back({bufs[i].G, s.l, pass < shifted ? 10.0 * (s.m + s.l) : 0.0, bufs[i].T,
+                            pass == last ? s.ndead : nullptr});
         }
         c->gemm_tag = 3;
         gemm_many(c, kOpC, gram);
-        for (int J = 0; J < max_nbk; ++J) {
-            CholBatch cb{};
-            int max_l = 0;
-            for (size_t i = 0; i < specs.size(); ++i) {
-                const OrthSpec& s = specs[i];
-                const Buf& b = bufs[i];
-                if (J >= b.blk.nbk) continue;
-                const int j0 = b.blk.begin(J), w = b.blk.width(J, s.l);
-                const int k = cb.count++;
-                cb.l[k] = w;
-                cb.G[k] = b.G + off(s.l, j0, j0);
-                cb.ldg[k] = s.l;
-                cb.trace_src[k] = b.G; cb.trace_n[k] = s.l; cb.trace_ld[k] = s.l;
-                if (b.blk.nbk > 1) {
-                    if (J == 0) cb.shift_save[k] = b.shift;
-                    else cb.shift_use[k] = b.shift;
-                }
-                cb.T[k] = b.T + off(s.l, j0, j0);
-                cb.ldt[k] = s.l;
-                cb.shift_scale[k] = pass < shifted ? 10.0 * (s.m + s.l) : 0.0;
-                cb.dep_tol[k] = 0.0;
-                cb.ndead[k] = pass == last ? s.ndead : nullptr;
-                cb.ndead_acc[k] = J > 0 ? 1 : 0;
-                max_l = std::max(max_l, w);
-                if (cb.count == kMaxSmall) { chol_launch(cb, max_l); max_l = 0; }
-            }
-            if (cb.count) chol_launch(cb, max_l);
-            std::vector<GemmSpec> g1, g2;
-            for (size_t i = 0; i < specs.size(); ++i) {
-                const OrthSpec& s = specs[i];
-                const Buf& b = bufs[i];
-                if (J + 1 >= b.blk.nbk) continue;
-                const int j0 = b.blk.begin(J), w = b.blk.width(J, s.l), r0 = j0 + w, rest = s.l - r0;
-                // R_J,>J = T_JJ^H G_J,>J
-                g1.push_back({w, rest, w, b.T + off(s.l, j0, j0), s.l, b.G + off(s.l, j0, r0), s.l,
-                              b.R + off(s.l, j0, r0), s.l});
-                // G_>J,>J -= R_J,>J^H R_J,>J  (upper part, in place)
-                GemmSpec up{rest, rest, w, b.R + off(s.l, j0, r0), s.l, b.R + off(s.l, j0, r0), s.l,
-                            b.G + off(s.l, r0, r0), s.l};
-                up.structure = kUpperC;
-                up.D = b.G + off(s.l, r0, r0);
-                up.ldd = s.l;
-                up.alpha = -1.0;
-                g2.push_back(up);
-            }
-            if (!g1.empty()) {
-                c->gemm_tag = 3;
-                gemm_many(c, kOpC, g1);
-                gemm_many(c, kOpC, g2);
-            }
-        }
-        for (int I = max_nbk - 2; I >= 0; --I) {
-            std::vector<GemmSpec> g1, g2;
-            for (size_t i = 0; i < specs.size(); ++i) {
-                const OrthSpec& s = specs[i];
-                const Buf& b = bufs[i];
-                if (I + 1 >= b.blk.nbk) continue;
-                const int i0 = b.blk.begin(I), w = b.blk.width(I, s.l), r0 = i0 + w, rest = s.l - r0;
-                // W = R_I,>I T_>I,>I  (T upper triangular)
-                GemmSpec ws{w, rest, rest, b.R + off(s.l, i0, r0), s.l, b.T + off(s.l, r0, r0), s.l, b.W, rest};
-                ws.structure = kTriB;
-                g1.push_back(ws);
-                // T_I,>I = -T_II W
-                GemmSpec ts{w, rest, w, b.T + off(s.l, i0, i0), s.l, b.W, rest, b.T + off(s.l, i0, r0), s.l};
-                ts.alpha = -1.0;
-                g2.push_back(ts);
-            }
-            if (!g1.empty()) {
-                c->gemm_tag = 4;
-                gemm_many(c, kOpN, g1);
-                gemm_many(c, kOpN, g2);
-            }
-        }
+        chol_inv_many(c, chol);
         for (size_t i = 0; i < specs.size(); ++i) {
             const OrthSpec& s = specs[i];
             cplx* dst = pass == last ? s.Q : (pass == 0 ? bufs[i].a : bufs[i].b);

@@ -63,6 +63,18 @@ constexpr int kSpanPasses = 2;
 void orth_many(rrsvd_b200_ctx* c, const std::vector<OrthSpec>& specs, int passes = kFullPasses);
 void orth(rrsvd_b200_ctx* c, const cplx* Y, int m, int l, cplx* Q, int* ndead = nullptr);
 
+// T = R^-1 (l x l, upper) for G (+ s I) = R^H R, s = shift_scale * u * trace(G) (0: none), any
+// l: one chol_inv block up to kMaxCholL, else block-right-looking with DMMA updates.  G (upper
+// triangle read) is overwritten.  Non-positive pivots mark dependent columns (zero T columns).
+struct CholSpec {
+    cplx* G;
+    int l;
+    double shift_scale;
+    cplx* T;
+    int* ndead;
+};
+void chol_inv_many(rrsvd_b200_ctx* c, const std::vector<CholSpec>& specs);
+
 // Gaussian sketch into `out` (n x l).
 void make_omega(rrsvd_b200_ctx* c, int n, int l, uint64_t seed, int mode, cplx* out);
 

@@ -73,6 +73,15 @@ int main() {
         const SvdResult rr = rrsvd_fixed_rank(a, {6, 4, 1, 9});
         for (std::size_t i = 0; i < 6; ++i) CHECK(std::abs(rr.sigma[i] - full.sigma[i]) < 1e-10 * full.sigma[0]);
     }
+    {  // test_randomized.cpp fixed-precision shape: exact rank 6 is certified at l = 8
+        const DenseMatrix l = gaussian_test_matrix(120, 6, 4), r = gaussian_test_matrix(80, 6, 5);
+        const DenseMatrix a = gemm(l, false, adjoint(r), false);
+        const SvdResult fp = rrsvd_fixed_precision(a, {1e-8, 4}, 8, 1, 11);
+        CHECK(fp.tolerance_certified);
+        CHECK(fp.achieved_rank == 8);
+        const SvdResult full = svd_full(a);
+        for (std::size_t i = 0; i < 6; ++i) CHECK(std::abs(fp.sigma[i] - full.sigma[i]) < 1e-10 * full.sigma[0]);
+    }
     {  // bond_gate is unitary (test_tebd.cpp:143-155 shape)
         DenseMatrix h(4, 4);
         h(0, 1) = cplx(0.3, 0.2); h(1, 0) = cplx(0.3, -0.2); h(2, 2) = 1.5; h(3, 0) = 0.7; h(0, 3) = 0.7;
