@@ -368,6 +368,136 @@ def run_ours(args, rank, world, local_rank):
         dist.destroy_process_group()
 
 
+# ----------------------------------------------------------------------------- row-sharded RRSVD
+
+SHARDED = {  # C5 top of the sweep and the C4 interpretation (i)
+    "c5": dict(name="c5_rrsvd_n16000_k100_p10_q2", n=16000, k=100, p=10, q=2,
+               desc="single RRSVD of a 16000^2 matrix, exponential spectrum 0.95^i, k=100 p=10 q=2"),
+    "c4": dict(name="c4i_rrsvd_n80000_k200_p10_q2", n=80000, k=200, p=10, q=2,
+               desc="config-4 interpretation (i): single RRSVD of an 80000^2 matrix (102 GB), "
+                    "exponential spectrum 0.95^i, k=200 p=10 q=2, row-sharded"),
+}
+SPECTRUM_RANK = 800  # 0.95^799 ~ 1.6e-18: the truncated tail is below double resolution
+
+
+def run_sharded(args, rank, world, local_rank):
+    """Row-sharded RRSVD (SURVEY §8(e) level 2): the matrix's rows are split over the ranks (and,
+    past the GEMM's 32-bit offsets, over several in-process shards per rank); Gram matrices and
+    A^H products are all-reduced (NCCL).  Strong scaling: the matrix is fixed as N grows."""
+    import torch
+    import paper_1504_00992_b200 as P
+    from paper_1504_00992_b200.sharded import DeviceOps, LocalSum, ShardedRrsvd, TorchSum
+
+    torch.cuda.set_device(local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
+    ctx = P.Context(local_rank, stream=stream.cuda_stream)
+    peak_dmma = P.probe_peak(0, ctx=ctx)
+    wl = SHARDED[args.workload]
+    n, k, p, q = wl["n"], wl["k"], wl["p"], wl["q"]
+    l = k + p
+    rows = [(n * r) // world for r in range(world + 1)]
+    r0, r1 = rows[rank], rows[rank + 1]
+    per = max(1, -(-((r1 - r0) * n) // 900_000_000))  # in-process shards: < 2^31 doubles each
+    cuts = [r0 + ((r1 - r0) * i) // per for i in range(per + 1)]
+    comm = TorchSum(f"cuda:{local_rank}") if world > 1 else LocalSum()
+    ops = DeviceOps(ctx)
+    drv = ShardedRrsvd(comm, ops)
+    # synthetic A = U diag(0.95^i) V^H, U (n x r) orthonormal across all shards, V replicated
+    rk = SPECTRUM_RANK
+    sig = torch.tensor(0.95 ** np.arange(rk), dtype=torch.float64, device="cuda")
+    ys = [P.gaussian_test_matrix(cuts[i + 1] - cuts[i], rk, 1000 + cuts[i], P.OMEGA_PHILOX, ctx=ctx,
+                                 device="cuda") for i in range(per)]
+    us = drv._orth_sharded(ys, n, 4)
+    v, _ = P.qr(P.gaussian_test_matrix(n, rk, 2, P.OMEGA_PHILOX, ctx=ctx, device="cuda"), ctx=ctx)
+    vh = v.conj().T.contiguous()
+    del ys, v
+    shards = [P.gemm(u * sig, False, vh, ctx=ctx) for u in us]
+    del us, vh
+    torch.cuda.synchronize()
+
+    def one():
+        return drv.fixed_rank(shards, n, k, p, q, 11, mode=P.OMEGA_PHILOX)
+
+    for _ in range(args.warmup):
+        one()
+    launches0 = ctx.launches
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            res = one()
+        ev1.record(stream)
+        ev1.synchronize()
+    elapsed = ev0.elapsed_time(ev1) / 1e3
+    gpu_launches = ctx.launches - launches0
+    if dist:
+        t = torch.tensor([elapsed], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        elapsed = float(t.item())
+    per_dec = elapsed / args.steps
+    w_rr = 8.0 * (2 * q + 2) * n * n * l
+    sig_out = res[1].cpu().numpy()
+    check = float(np.max(np.abs(sig_out[:20] - 0.95 ** np.arange(20)) / 0.95 ** np.arange(20)))
+    line = None
+    if rank == 0:
+        line = {
+            "metric": "RRSVD decimations/s (row-sharded single matrix; FP64 tensor-core roofline)",
+            "value": round(1.0 / per_dec, 5), "unit": "decimations/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * per_dec, 3),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "c128 (fp64)",
+            "data": f"synthetic: U diag(0.95^i, i<{rk}) V^H with Philox-Gaussian orthonormalised U, V",
+            "config": {"workload": wl["name"], "desc": wl["desc"], "n": n, "k": k, "p": p, "q": q,
+                       "shards_per_rank": per, "sketch": "Philox in-kernel",
+                       "parallelism": f"row-sharded x{world}" if world > 1 else f"one GPU, {per} row shards",
+                       "l2": "inputs larger than L2 (A %.1f GB)" % (16.0 * n * n / 1e9)},
+            "roofline": {"bound": "tensor", "kernel": "whole decimation: W_rr = 8(2q+2) m n l over the step time",
+                         "achieved": round(w_rr / per_dec / 1e12, 3), "peak": round(peak_dmma * world, 3),
+                         "unit": "TFLOP/s", "frac": round(w_rr / per_dec / 1e12 / (peak_dmma * world), 4),
+                         "peak_source": "measured live: DMMA probe (mma.sync m8n8k4 f64) x n_gpus",
+                         "traffic": None},
+            "sigma_check_top20_rel_err": check,
+            "e2e": None, "e2e_note": "input is the resident matrix (%.0f GB); host staging not timed" % (16.0 * n * n / 1e9),
+            "gpu_launches": int(gpu_launches), "clocks": clk.summary(),
+        }
+        if not args.no_cpu_baseline and world == 1 and args.workload == "c5":
+            line["cpu_baseline"] = sharded_cpu_baseline(wl)
+        elif args.workload == "c4":
+            line["cpu_baseline"] = None
+            line["cpu_baseline_note"] = "not run: the 102 GB input exceeds a host-core run's budget"
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def sharded_cpu_baseline(wl):
+    """The reference rrsvd_fixed_rank on the host cores, one call on a 4000^2 sample of the same
+    synthetic family, extrapolated by its GEMM work (n^2) to the configured n."""
+    from oracle import ref
+    if not ref.available():
+        return None
+    cores = os.cpu_count() or 1
+    ref.set_threads(cores)
+    ns = 4000
+    rng = np.random.default_rng(0)
+    u, _ = np.linalg.qr(rng.standard_normal((ns, 400)) + 1j * rng.standard_normal((ns, 400)))
+    v, _ = np.linalg.qr(rng.standard_normal((ns, 400)) + 1j * rng.standard_normal((ns, 400)))
+    a = (u * 0.95 ** np.arange(400)) @ v.conj().T
+    t0 = time.perf_counter()
+    ref.fixed_rank(a, wl["k"], wl["p"], wl["q"], 11, vectors=True)
+    dt = (time.perf_counter() - t0) * (wl["n"] / ns) ** 2
+    return {"value": round(1.0 / dt, 6), "unit": "decimations/s", "cores": cores, "kind": "reference",
+            "sample": f"one rrsvd_fixed_rank at n={ns} on the host, x(n/{ns})^2 to n={wl['n']}"}
+
+
 def traffic_entry():
     """DRAM traffic of the dominant kernel from the committed ncu --set full capture (per
     launch), with the launch's algorithmic bytes for comparison; null if absent."""
@@ -457,7 +587,8 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="c3", choices=["c3", "c2"])
+    ap.add_argument("--workload", default="c3", choices=["c3", "c2", "c5", "c4"],
+                    help="c3 (headline TEBD), c2; c5/c4: row-sharded single-matrix RRSVD")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--force-partition", action="store_true",
                     help="use the chain-block partition driver even on one GPU (smoke test of the N>1 path)")
@@ -467,7 +598,23 @@ def main():
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     local_rank = int(os.environ.get("LOCAL_RANK", 0))
-    if args.impl == "reference":
+    if args.workload in SHARDED and args.impl == "reference":
+        if rank == 0:
+            wl = SHARDED[args.workload]
+            cb = sharded_cpu_baseline(wl) if args.workload == "c5" else None
+            if cb is None:
+                print(json.dumps({"impl": "reference", "unavailable": "c4: 102 GB input exceeds a host run"
+                                  if args.workload == "c4" else "oracle/_ref not built"}))
+            else:
+                print(json.dumps({"impl": "reference", "metric": "RRSVD decimations/s (row-sharded single matrix;"
+                                  " FP64 tensor-core roofline)", "value": cb["value"], "unit": "decimations/s",
+                                  "n_gpus": world, "steps": 1, "warmup": 0, "higher_is_better": True,
+                                  "config": {"workload": wl["name"]}, "cpu_baseline": cb,
+                                  "e2e": {"value": cb["value"], "unit": "decimations/s", "h2d_bytes_per_step": 0,
+                                          "d2h_bytes_per_step": 0}}), flush=True)
+    elif args.workload in SHARDED:
+        run_sharded(args, rank, world, local_rank)
+    elif args.impl == "reference":
         run_reference(args, rank, world)
     elif world > 1 or args.force_partition:
         run_partitioned(args, rank, world, local_rank)
