@@ -755,6 +755,7 @@ bool make_gate_blocks(rrsvd_b200_ctx* c, const cplx* G, int dd, GateBlocksOwned&
     };
     out.dev.nblocks = (int)groups.size();
     out.dev.dd = dd;
+    out.dev.total = (int)gblk.size();
     out.dev.offs = static_cast<const int*>(upload(offs.data(), offs.size() * sizeof(int)));
     out.dev.idx = static_cast<const int*>(upload(idx.data(), idx.size() * sizeof(int)));
     out.dev.goff = static_cast<const int*>(upload(goff.data(), goff.size() * sizeof(int)));

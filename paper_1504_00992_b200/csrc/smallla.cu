@@ -243,14 +243,71 @@ __global__ void __launch_bounds__(CHOL_THREADS) chol_inv_kernel(const __grid_con
 }
 
 // ============================================================================ Jacobi SVD
-constexpr int JAC_THREADS = 256;
+constexpr int JAC_THREADS = 256;      // grid-wide kernel: one warp per column pair
+constexpr int JAC_CL_THREADS = 512;   // cluster kernel: up to 16 column pairs per round
+constexpr int kMaxPairsPerRound = JAC_CL_THREADS / 32;
 constexpr int kMaxSweeps = 60;
 
 __device__ __forceinline__ int circle(int i, int t, int n) {  // round-robin slot -> player
     return i == 0 ? 0 : ((i - 1 + t) % (n - 1)) + 1;
 }
 
-__global__ void __launch_bounds__(JAC_THREADS) jacobi_kernel(const __grid_constant__ JacobiBatch b) {
+// One Hestenes rotation of columns xp, xq (r data rows, ld rows in all: the trailing c rows
+// accumulate the right vectors), executed by one warp.  Returns whether it rotated.
+//   a = |xp|^2, b = |xq|^2, g = xp^H xq;  rotate iff |g| > tol sqrt(a b)
+//   e = conj(g)/|g|, zeta = (b - a)/(2|g|), t = sign(zeta)/(|zeta| + sqrt(1 + zeta^2)),
+//   c = 1/sqrt(1 + t^2), s = c t:   xp' = c xp - s e xq,  xq' = s xp + c e xq.
+// The parameters use rsqrt/rcp (a few ulps): the rotation only has to be unitary to working
+// precision, the convergence test is exact.
+__device__ __forceinline__ bool hestenes_rotate(cplx* __restrict__ xp, cplx* __restrict__ xq, int r, int ld,
+                                                int lane, double tol) {
+    double a0 = 0.0, b0 = 0.0, a1 = 0.0, b1 = 0.0;
+    cplx g0 = mk(0.0, 0.0), g1 = mk(0.0, 0.0);
+    int rr = lane;
+    for (; rr + 32 < r; rr += 64) {  // two independent accumulator sets
+        const cplx u = xp[rr], v = xq[rr], u1 = xp[rr + 32], v1 = xq[rr + 32];
+        a0 += cabs2(u); b0 += cabs2(v); cfmac(g0, u, v);
+        a1 += cabs2(u1); b1 += cabs2(v1); cfmac(g1, u1, v1);
+    }
+    if (rr < r) {
+        const cplx u = xp[rr], v = xq[rr];
+        a0 += cabs2(u); b0 += cabs2(v); cfmac(g0, u, v);
+    }
+    double a = a0 + a1, bb = b0 + b1;
+    cplx g = mk(g0.x + g1.x, g0.y + g1.y);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        a += __shfl_xor_sync(0xffffffffu, a, o);
+        bb += __shfl_xor_sync(0xffffffffu, bb, o);
+        g.x += __shfl_xor_sync(0xffffffffu, g.x, o);
+        g.y += __shfl_xor_sync(0xffffffffu, g.y, o);
+    }
+    const double g2 = g.x * g.x + g.y * g.y;
+    if (!(a > 0.0) || !(bb > 0.0) || !(g2 > tol * tol * a * bb)) return false;
+    const double rg = rsqrt(g2);  // 1/|g|
+    const cplx e = mk(g.x * rg, -g.y * rg);
+    const double zeta = 0.5 * (bb - a) * rg;
+    const double az = fabs(zeta);
+    const double h = az > 1e150 ? az : sqrt(fma(zeta, zeta, 1.0));
+    const double tt = (zeta >= 0.0 ? 1.0 : -1.0) / (az + h);
+    const double cc = rsqrt(fma(tt, tt, 1.0));
+    const double ss = cc * tt;
+#pragma unroll 4
+    for (int k = lane; k < ld; k += 32) {
+        const cplx u = xp[k];
+        const cplx ev = cmul(e, xq[k]);
+        xp[k] = mk(cc * u.x - ss * ev.x, cc * u.y - ss * ev.y);
+        xq[k] = mk(ss * u.x + cc * ev.x, ss * u.y + cc * ev.y);
+    }
+    return true;
+}
+
+// Block one-sided Jacobi on a thread-block cluster.  The c columns form 2*cs blocks of bs; CTA k
+// holds two blocks per step (a round-robin tournament over blocks, nblk - 1 steps per sweep, data
+// through L2).  Per step a CTA rotates the bs^2 CROSS pairs of its two blocks in bs rounds of bs
+// disjoint pairs (one warp each); the pairs inside a block are rotated once per sweep, in step 0
+// (where every block is resident exactly once).  Every column pair is visited once per sweep.
+__global__ void __launch_bounds__(JAC_CL_THREADS) jacobi_kernel(const __grid_constant__ JacobiBatch b) {
     extern __shared__ __align__(16) unsigned char sm[];
     cg::cluster_group cluster = cg::this_cluster();
     const int cs = (int)cluster.num_blocks();
@@ -259,77 +316,63 @@ __global__ void __launch_bounds__(JAC_THREADS) jacobi_kernel(const __grid_consta
     const int r = b.r[p], c = b.c[p], ld = r + c;
     const int nblk = 2 * cs;
     const int bs = (c + nblk - 1) / nblk;
-    cplx* col = reinterpret_cast<cplx*>(sm);  // [2bs][ld]
+    cplx* col = reinterpret_cast<cplx*>(sm);  // [2bs][ld]: block A columns, then block B
     __shared__ int cnt[2];
     __shared__ int s_rot;
     cplx* W = b.W[p];
 
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = JAC_THREADS / 32;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const double tol = sqrt((double)max(r, 1)) * kEps;
     if (tid == 0) { cnt[0] = cnt[1] = 0; }
     cluster.sync();
 
     int sweep = 0;
     for (; sweep < kMaxSweeps; ++sweep) {
+        int myrot = 0;
         for (int t = 0; t < nblk - 1; ++t) {
             const int blkA = circle(rank, t, nblk), blkB = circle(nblk - 1 - rank, t, nblk);
-            // load the 2*bs columns (column-major, contiguous) through L2
+            auto gcol = [&](int lc) { return lc < bs ? blkA * bs + lc : blkB * bs + (lc - bs); };
             for (int lc = 0; lc < 2 * bs; ++lc) {
-                const int g = (lc < bs) ? blkA * bs + lc : blkB * bs + (lc - bs);
+                const int g = gcol(lc);
                 if (g >= c) continue;
                 const cplx* src = W + (long long)g * ld;
-                for (int rr = tid; rr < ld; rr += JAC_THREADS) cp_async16(col + lc * ld + rr, src + rr, true);
+                for (int rr = tid; rr < ld; rr += JAC_CL_THREADS) cp_async16(col + lc * ld + rr, src + rr, true);
             }
             cp_async_commit();
             cp_async_wait<0>();
             if (tid == 0) s_rot = 0;
             __syncthreads();
-            int myrot = 0;
-            const int n2 = 2 * bs;
-            for (int ti = 0; ti < n2 - 1; ++ti) {
-                for (int k = warp; k < bs; k += nw) {
-                    const int lp = circle(k, ti, n2), lq = circle(n2 - 1 - k, ti, n2);
-                    const int gp = (lp < bs) ? blkA * bs + lp : blkB * bs + (lp - bs);
-                    const int gq = (lq < bs) ? blkA * bs + lq : blkB * bs + (lq - bs);
-                    if (gp >= c || gq >= c) continue;
-                    cplx* xp = col + lp * ld;
-                    cplx* xq = col + lq * ld;
-                    double a = 0.0, bb = 0.0;
-                    cplx g = mk(0.0, 0.0);
-                    for (int rr = lane; rr < r; rr += 32) {
-                        const cplx u = xp[rr], v = xq[rr];
-                        a += cabs2(u);
-                        bb += cabs2(v);
-                        cfmac(g, u, v);
+            if (t == 0) {  // pairs inside each block, round-robin over its bs columns
+                const int bp = bs + (bs & 1);
+                for (int ir = 0; ir < bp - 1; ++ir) {
+                    const int half = bp / 2;
+                    if (warp < 2 * half) {
+                        const int blk = warp / half, k = warp % half;
+                        const int lp = circle(k, ir, bp), lq = circle(bp - 1 - k, ir, bp);
+                        if (lp < bs && lq < bs && gcol(blk * bs + lp) < c && gcol(blk * bs + lq) < c)
+                            myrot += hestenes_rotate(col + (blk * bs + lp) * ld, col + (blk * bs + lq) * ld, r, ld,
+                                                     lane, tol);
                     }
-                    a = warp_sum(a);
-                    bb = warp_sum(bb);
-                    g = warp_sum(g);
-                    const double ag = hypot(g.x, g.y);
-                    if (!(a > 0.0) || !(bb > 0.0) || !(ag > tol * sqrt(a) * sqrt(bb))) continue;
-                    ++myrot;
-                    const cplx e = mk(g.x / ag, -g.y / ag);  // conj(g)/|g|
-                    const double zeta = (bb - a) / (2.0 * ag);
-                    const double tt = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + hypot(1.0, zeta));
-                    const double cc = 1.0 / sqrt(1.0 + tt * tt);
-                    const double ss = cc * tt;
-                    for (int rr = lane; rr < ld; rr += 32) {
-                        const cplx u = xp[rr];
-                        const cplx ev = cmul(e, xq[rr]);
-                        xp[rr] = mk(cc * u.x - ss * ev.x, cc * u.y - ss * ev.y);
-                        xq[rr] = mk(ss * u.x + cc * ev.x, ss * u.y + cc * ev.y);
-                    }
+                    __syncthreads();
+                }
+            }
+            for (int j = 0; j < bs; ++j) {  // cross pairs (A[i], B[(i + j) mod bs])
+                if (warp < bs) {
+                    const int lp = warp, lq = bs + (warp + j) % bs;
+                    if (gcol(lp) < c && gcol(lq) < c)
+                        myrot += hestenes_rotate(col + lp * ld, col + lq * ld, r, ld, lane, tol);
                 }
                 __syncthreads();
             }
             if (lane == 0 && myrot) atomicAdd(&s_rot, myrot);
+            myrot = 0;
             __syncthreads();
             if (tid == 0) cnt[sweep & 1] += s_rot;
             for (int lc = 0; lc < 2 * bs; ++lc) {
-                const int g = (lc < bs) ? blkA * bs + lc : blkB * bs + (lc - bs);
+                const int g = gcol(lc);
                 if (g >= c) continue;
                 cplx* dst = W + (long long)g * ld;
-                for (int rr = tid; rr < ld; rr += JAC_THREADS) dst[rr] = col[lc * ld + rr];
+                for (int rr = tid; rr < ld; rr += JAC_CL_THREADS) dst[rr] = col[lc * ld + rr];
             }
             __threadfence();
             cluster.sync();
@@ -364,33 +407,7 @@ __global__ void __launch_bounds__(JAC_THREADS) jacobi_global_kernel(cplx* __rest
             for (int k = gw; k < n / 2; k += nwarps) {
                 const int gp = circle(k, t, n), gq = circle(n - 1 - k, t, n);
                 if (gp >= c || gq >= c) continue;
-                cplx* xp = W + (long long)gp * ld;
-                cplx* xq = W + (long long)gq * ld;
-                double a = 0.0, bb = 0.0;
-                cplx g = mk(0.0, 0.0);
-                for (int rr = lane; rr < r; rr += 32) {
-                    const cplx u = xp[rr], v = xq[rr];
-                    a += cabs2(u);
-                    bb += cabs2(v);
-                    cfmac(g, u, v);
-                }
-                a = warp_sum(a);
-                bb = warp_sum(bb);
-                g = warp_sum(g);
-                const double ag = hypot(g.x, g.y);
-                if (!(a > 0.0) || !(bb > 0.0) || !(ag > tol * sqrt(a) * sqrt(bb))) continue;
-                ++myrot;
-                const cplx e = mk(g.x / ag, -g.y / ag);
-                const double zeta = (bb - a) / (2.0 * ag);
-                const double tt = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + hypot(1.0, zeta));
-                const double cc = 1.0 / sqrt(1.0 + tt * tt);
-                const double ss = cc * tt;
-                for (int rr = lane; rr < ld; rr += 32) {
-                    const cplx u = xp[rr];
-                    const cplx ev = cmul(e, xq[rr]);
-                    xp[rr] = mk(cc * u.x - ss * ev.x, cc * u.y - ss * ev.y);
-                    xq[rr] = mk(ss * u.x + cc * ev.x, ss * u.y + cc * ev.y);
-                }
+                myrot += hestenes_rotate(W + (long long)gp * ld, W + (long long)gq * ld, r, ld, lane, tol);
             }
             grid.sync();
         }
@@ -611,15 +628,23 @@ size_t jacobi_need(int r, int c, int csz) {
     const int bs = (c + 2 * csz - 1) / (2 * csz);
     return (size_t)2 * bs * (r + c) * sizeof(cplx);
 }
+// smallest cluster whose two blocks fit the shared-memory budget with at most one pair per
+// warp per round; 0 if none (16 CTAs is the non-portable maximum)
+int jacobi_cluster(int r, int c) {
+    for (int csz = 1; csz <= 16; csz *= 2) {
+        const int bs = (c + 2 * csz - 1) / (2 * csz);
+        if (bs <= kMaxPairsPerRound && jacobi_need(r, c, csz) <= kJacBudget) return csz;
+    }
+    return 0;
+}
 }  // namespace
 
-bool jacobi_fits(int r, int c) { return jacobi_need(r, c, 16) <= kJacBudget; }
+bool jacobi_fits(int r, int c) { return jacobi_cluster(r, c) > 0; }
 
 cudaError_t jacobi_svd(const JacobiBatch& b, int max_r, int max_c, cudaStream_t s) {
     if (b.count == 0) return cudaSuccess;
-    int cs = 8;
-    if (jacobi_need(max_r, max_c, 8) > kJacBudget) cs = 16;
-    if (jacobi_need(max_r, max_c, cs) > kJacBudget) return cudaErrorInvalidValue;
+    const int cs = jacobi_cluster(max_r, max_c);
+    if (cs == 0) return cudaErrorInvalidValue;
     const size_t smem = jacobi_need(max_r, max_c, cs);
     cudaError_t e = cudaFuncSetAttribute(jacobi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
@@ -629,7 +654,7 @@ cudaError_t jacobi_svd(const JacobiBatch& b, int max_r, int max_c, cudaStream_t 
     }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(cs * b.count);
-    cfg.blockDim = dim3(JAC_THREADS);
+    cfg.blockDim = dim3(JAC_CL_THREADS);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
     cudaLaunchAttribute attr[1];

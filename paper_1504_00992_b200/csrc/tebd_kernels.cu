@@ -1,3 +1,4 @@
+#include <algorithm>
 // tebd_kernels.cu — sketch generation, gate for small d, layout conversion, truncation,
 // Gamma reshape, peak probes.  See tebd_kernels.cuh.
 #include "tebd_kernels.cuh"
@@ -153,6 +154,68 @@ __global__ void __launch_bounds__(256) gate_blocks_kernel(const __grid_constant_
             for (int t = 0; t < kMaxGateBlock; ++t)
                 if (t < sz) cfma(acc, sg[r * sz + t], v[t]);
             J.Mout[base + (long long)B.idx[off + r] * J.cr] = acc;
+        }
+    }
+}
+
+// Staged variant: every block of the gate (sum |S_B|^2 entries) and the state index list sit in
+// shared memory for the whole CTA, and each block runs an exact-size unrolled body (the generic
+// kernel above pays 32-wide predicated loops and two barriers per block).  One thread per
+// Θ column (a, β): it gathers the |S_B| entries of its column that the block mixes, applies G_B
+// from shared memory (broadcast reads) and scatters the results — coalesced across the warp.
+template <int SZ>
+__device__ __forceinline__ void gate_block_apply(const cplx* __restrict__ g, const int* __restrict__ idx,
+                                                 const cplx* __restrict__ Min, cplx* __restrict__ Mout,
+                                                 long long base, long long stride) {
+    cplx v[SZ];
+#pragma unroll
+    for (int t = 0; t < SZ; ++t) v[t] = Min[base + (long long)idx[t] * stride];
+#pragma unroll 1
+    for (int r = 0; r < SZ; ++r) {
+        cplx acc = mk(0.0, 0.0), acc2 = mk(0.0, 0.0);
+#pragma unroll
+        for (int t = 0; t < SZ; t += 2) {
+            cfma(acc, g[r * SZ + t], v[t]);
+            if (t + 1 < SZ) cfma(acc2, g[r * SZ + t + 1], v[t + 1]);
+        }
+        Mout[base + (long long)idx[r] * stride] = mk(acc.x + acc2.x, acc.y + acc2.y);
+    }
+}
+
+__global__ void __launch_bounds__(256, 2) gate_blocks_staged_kernel(const __grid_constant__ GateBlockBatch bt) {
+    extern __shared__ __align__(16) unsigned char sm[];
+    const GateBlockJob& J = bt.j[blockIdx.y];
+    const GateBlocks& B = J.gb;
+    cplx* sg = reinterpret_cast<cplx*>(sm);
+    int* sidx = reinterpret_cast<int*>(sg + B.total);
+    int* soff = sidx + B.dd;  // nblocks + 1 offsets, then nblocks gate offsets
+    int* sgoff = soff + B.nblocks + 1;
+    for (int t = threadIdx.x; t < B.total; t += 256) sg[t] = B.gblk[t];
+    for (int t = threadIdx.x; t < B.dd; t += 256) sidx[t] = B.idx[t];
+    for (int t = threadIdx.x; t <= B.nblocks; t += 256) soff[t] = B.offs[t];
+    for (int t = threadIdx.x; t < B.nblocks; t += 256) sgoff[t] = B.goff[t];
+    __syncthreads();
+    const long long cols = (long long)J.cl * J.cr;
+    const long long c = blockIdx.x * 256LL + threadIdx.x;
+    if (c >= cols) return;
+    const long long a = c / J.cr, bcol = c % J.cr;
+    const long long base = a * B.dd * J.cr + bcol;
+    const long long stride = J.cr;
+    for (int k = 0; k < B.nblocks; ++k) {
+        const int off = soff[k], sz = soff[k + 1] - off;
+        const cplx* g = sg + sgoff[k];
+        const int* ix = sidx + off;
+        switch (sz) {
+#define RB_GATE_CASE(N) \
+    case N: gate_block_apply<N>(g, ix, J.Min, J.Mout, base, stride); break;
+            RB_GATE_CASE(1) RB_GATE_CASE(2) RB_GATE_CASE(3) RB_GATE_CASE(4) RB_GATE_CASE(5) RB_GATE_CASE(6)
+            RB_GATE_CASE(7) RB_GATE_CASE(8) RB_GATE_CASE(9) RB_GATE_CASE(10) RB_GATE_CASE(11) RB_GATE_CASE(12)
+            RB_GATE_CASE(13) RB_GATE_CASE(14) RB_GATE_CASE(15) RB_GATE_CASE(16) RB_GATE_CASE(17) RB_GATE_CASE(18)
+            RB_GATE_CASE(19) RB_GATE_CASE(20) RB_GATE_CASE(21) RB_GATE_CASE(22) RB_GATE_CASE(23) RB_GATE_CASE(24)
+            RB_GATE_CASE(25) RB_GATE_CASE(26) RB_GATE_CASE(27) RB_GATE_CASE(28) RB_GATE_CASE(29) RB_GATE_CASE(30)
+            RB_GATE_CASE(31) RB_GATE_CASE(32)
+#undef RB_GATE_CASE
+            default: break;
         }
     }
 }
@@ -547,7 +610,20 @@ cudaError_t gamma_reshape(const GammaArgs& a, int max_kept, cudaStream_t s) {
 
 cudaError_t gate_blocks_many(const GateBlockBatch& b, long long max_cols, cudaStream_t s) {
     if (b.count == 0) return cudaSuccess;
-    gate_blocks_kernel<<<dim3((unsigned)((max_cols + 255) / 256), b.count), 256, 0, s>>>(b);
+    size_t smem = 0;
+    for (int i = 0; i < b.count; ++i) {
+        const GateBlocks& g = b.j[i].gb;
+        smem = std::max(smem, (size_t)g.total * sizeof(cplx) + (size_t)(g.dd + 2 * g.nblocks + 1) * sizeof(int));
+    }
+    const dim3 grid((unsigned)((max_cols + 255) / 256), b.count);
+    if (smem <= 160 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(gate_blocks_staged_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem);
+        if (e != cudaSuccess) return e;
+        gate_blocks_staged_kernel<<<grid, 256, smem, s>>>(b);
+    } else {
+        gate_blocks_kernel<<<grid, 256, 0, s>>>(b);
+    }
     return cudaGetLastError();
 }
 

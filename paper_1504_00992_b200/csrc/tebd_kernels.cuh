@@ -34,6 +34,7 @@ struct GateBlocks {
     const int* idx;    // the dd states grouped by block (row indices into G)
     const int* goff;   // nblocks offsets into gblk
     const cplx* gblk;  // dense blocks G_B (|S_B| x |S_B|, row-major, local indices)
+    int total;         // sum over blocks of |S_B|^2 (entries of gblk)
 };
 struct GateBlockJob {
     GateBlocks gb;
