@@ -1,0 +1,60 @@
+// blockjac.cuh — block one-sided Jacobi SVD for problems beyond the on-chip cluster kernel
+// (deterministic decimation of large minor dimensions, C2's batched 256^2, wide fixed-precision
+// bases).  The same Hestenes iteration as jacobi_kernel, reorganised around GEMMs:
+//
+//   columns of X (r x c, padded to cp = nbp*b) form nbp blocks of b; a circle-method tournament
+//   pairs the blocks, pair k occupying the adjacent slots 2k, 2k+1.  One step, for all pairs
+//   (bj_step_kernel, one CTA per pair):
+//     G_k = [X_i X_j]^H [X_i X_j]          row chunks staged in shared memory, fixed order
+//     W_k = one sweep of two-sided Jacobi  the Hestenes rotations applied to the Gram (same
+//           on G_k                         formulas, same scaled stopping test), accumulating
+//                                          the 2b x 2b unitary W_k
+//     [X_i X_j] W_k, [V_i V_j] W_k         written to the blocks' positions of the next step
+//                                          in the other buffer
+//   The Gram is recomputed from the columns every step (rounding never accumulates in it); a
+//   sweep visits every block pair once; the iteration stops after a sweep whose pair solves all
+//   found their Gram already diagonal to tol = sqrt(r)·eps in the scaled sense.
+#pragma once
+#include "common.cuh"
+
+namespace rb {
+
+constexpr int kBjMaxProblems = 64;
+constexpr int kBjMaxSlots = 512;  // padded blocks per problem (c <= 512*b)
+
+struct BjInit {
+    int count, r, c, cp, b, nbp;
+    const cplx* A[kBjMaxProblems];  // the matrix to decompose: element (i, j) = adj ? conj(A[j*lda+i]) : A[i*lda+j]
+    int lda[kBjMaxProblems], adj[kBjMaxProblems];
+    cplx* X[kBjMaxProblems];  // r x cp row-major, slots in step-0 placement
+    cplx* V[kBjMaxProblems];  // cp x cp row-major (rows: original column index; columns: slots)
+    int place[kBjMaxSlots];   // block id at each slot's block position (step-0 placement)
+};
+cudaError_t bj_init(const BjInit& a, cudaStream_t s);
+
+// One tournament step for every block pair of every problem, fused (one CTA per pair): the
+// pair's Gram from row chunks staged in shared memory, one sweep of the pair solve, then
+// [X_i X_j] W and [V_i V_j] W written straight to the blocks' positions of the next step.
+struct BjStep {
+    int count, r, cp, b, npairs;
+    const cplx* Xs[kBjMaxProblems];
+    cplx* Xd[kBjMaxProblems];
+    const cplx* Vs[kBjMaxProblems];
+    cplx* Vd[kBjMaxProblems];
+    int* rot[kBjMaxProblems];  // per-problem rotation counters (added to)
+    int dst[kBjMaxSlots];      // block position now -> block position at the next step
+};
+cudaError_t bj_step(const BjStep& a, cudaStream_t s);
+
+struct BjFinish {
+    int count, r, c, cp, b;
+    const cplx* X[kBjMaxProblems];
+    const cplx* V[kBjMaxProblems];
+    double* sigma[kBjMaxProblems];  // c, non-increasing
+    cplx* Xn[kBjMaxProblems];       // nullable: r x c row-major, X columns / sigma (sorted)
+    cplx* Js[kBjMaxProblems];       // nullable: c x c row-major, V columns (sorted)
+    int place[kBjMaxSlots];         // block id at each block position (final placement)
+};
+cudaError_t bj_finish(const BjFinish& a, cudaStream_t s);
+
+}  // namespace rb

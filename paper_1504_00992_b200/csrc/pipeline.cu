@@ -293,6 +293,98 @@ struct SmallSvdSpec {
     cplx* Js;
 };
 
+// Block one-sided Jacobi (blockjac.cuh) for same-shaped problems: the tournament schedule is
+// host-side bookkeeping; one fused launch per step for all pairs of all problems; one
+// 4-byte-per-problem D2H per sweep for the convergence test.
+int block_jacobi_min_c() {  // above this the block method is used (RRSVD_B200_BJ_MIN_C overrides)
+    // measured: the cluster kernel wins while it fits (256^2: 10.6 vs 13.6 ms; C2 4.6 vs 3.3
+    // steps/s); the block method takes the widths the cluster cannot hold
+    static const int v = [] {
+        const char* e = std::getenv("RRSVD_B200_BJ_MIN_C");
+        return e ? std::atoi(e) : 300;
+    }();
+    return v;
+}
+constexpr int kBjBlock = 16;
+
+void block_jacobi_group(rrsvd_b200_ctx* c, const std::vector<const SmallSvdSpec*>& grp) {
+    const int np = (int)grp.size();
+    const int r = grp[0]->r, cc = grp[0]->cc, b = kBjBlock;
+    const int nb = (cc + b - 1) / b, nbp = nb + (nb & 1), cp = nbp * b, npairs = nbp / 2;
+    if (nbp > kBjMaxSlots) throw_contract(c, "jacobi: too many columns for the block Jacobi");
+    // placement(t): block id at block position pos (pair k: positions 2k, 2k+1)
+    auto placement = [&](int t, std::vector<int>& pl) {
+        pl.assign(nbp, 0);
+        for (int k = 0; k < npairs; ++k) {
+            auto circ = [&](int i) { return i == 0 ? 0 : ((i - 1 + t) % (nbp - 1)) + 1; };
+            pl[2 * k] = circ(k);
+            pl[2 * k + 1] = circ(nbp - 1 - k);
+        }
+    };
+    std::vector<cplx*> X1(np), X2(np), V1(np), V2(np);
+    int* rot = ws_get<int>(c, np);
+    for (int p = 0; p < np; ++p) {
+        X1[p] = ws_get<cplx>(c, (size_t)r * cp);
+        X2[p] = ws_get<cplx>(c, (size_t)r * cp);
+        V1[p] = ws_get<cplx>(c, (size_t)cp * cp);
+        V2[p] = ws_get<cplx>(c, (size_t)cp * cp);
+    }
+    std::vector<int> pl0, plt, pln;
+    placement(0, pl0);
+    {
+        BjInit in{};
+        in.count = np; in.r = r; in.c = cc; in.cp = cp; in.b = b; in.nbp = nbp;
+        for (int p = 0; p < np; ++p) {
+            in.A[p] = grp[p]->X; in.lda[p] = grp[p]->lda; in.adj[p] = grp[p]->adj; in.X[p] = X1[p]; in.V[p] = V1[p];
+        }
+        std::copy(pl0.begin(), pl0.end(), in.place);
+        check_cuda(c, bj_init(in, c->stream), "bj_init");
+        c->launches++;
+    }
+    // per-step destination tables (the schedule repeats every sweep)
+    std::vector<std::vector<int>> dst(nbp - 1, std::vector<int>(nbp));
+    for (int t = 0; t < nbp - 1; ++t) {
+        placement(t, plt);
+        placement((t + 1) % (nbp - 1), pln);
+        std::vector<int> where(nbp);
+        for (int pos = 0; pos < nbp; ++pos) where[pln[pos]] = pos;
+        for (int pos = 0; pos < nbp; ++pos) dst[t][pos] = where[plt[pos]];
+    }
+    auto* hrot = static_cast<int*>(pinned_scratch(c, np * sizeof(int)));
+    int sweep = 0;
+    for (; sweep < 60; ++sweep) {
+        check_cuda(c, cudaMemsetAsync(rot, 0, np * sizeof(int), c->stream), "memset");
+        for (int t = 0; t < nbp - 1; ++t) {
+            BjStep st{};
+            st.count = np; st.r = r; st.cp = cp; st.b = b; st.npairs = npairs;
+            for (int p = 0; p < np; ++p) {
+                st.Xs[p] = X1[p]; st.Xd[p] = X2[p]; st.Vs[p] = V1[p]; st.Vd[p] = V2[p]; st.rot[p] = rot + p;
+            }
+            std::copy(dst[t].begin(), dst[t].end(), st.dst);
+            check_cuda(c, bj_step(st, c->stream), "bj_step");
+            c->launches++;
+            std::swap(X1, X2);
+            std::swap(V1, V2);
+        }
+        check_cuda(c, cudaMemcpyAsync(hrot, rot, np * sizeof(int), cudaMemcpyDeviceToHost, c->stream), "D2H");
+        check_cuda(c, cudaStreamSynchronize(c->stream), "sync");
+        bool any = false;
+        for (int p = 0; p < np; ++p) any = any || hrot[p] != 0;
+        if (!any) break;
+    }
+    if (debug_enabled())
+        std::fprintf(stderr, "[rrsvd_b200] block jacobi %dx%d x%d: %d sweeps\n", r, cc, np, sweep + 1);
+    BjFinish fin{};
+    fin.count = np; fin.r = r; fin.c = cc; fin.cp = cp; fin.b = b;
+    for (int p = 0; p < np; ++p) {
+        fin.X[p] = X1[p]; fin.V[p] = V1[p];
+        fin.sigma[p] = grp[p]->sigma; fin.Xn[p] = grp[p]->Xn; fin.Js[p] = grp[p]->Js;
+    }
+    std::copy(pl0.begin(), pl0.end(), fin.place);
+    check_cuda(c, bj_finish(fin, c->stream), "bj_finish");
+    c->launches++;
+}
+
 void small_svd_many(rrsvd_b200_ctx* c, const std::vector<SmallSvdSpec>& specs) {
     std::vector<cplx*> W(specs.size());
     std::vector<int*> dsweeps(specs.size(), nullptr);
@@ -300,21 +392,21 @@ void small_svd_many(rrsvd_b200_ctx* c, const std::vector<SmallSvdSpec>& specs) {
     for (size_t i = 0; i < specs.size(); ++i) {
         W[i] = ws_get<cplx>(c, (size_t)(specs[i].r + specs[i].cc) * specs[i].cc);
         if (debug_enabled()) dsweeps[i] = ws_get<int>(c, 1);
-        (jacobi_fits(specs[i].r, specs[i].cc) ? onchip : global).push_back(i);
+        (specs[i].cc <= block_jacobi_min_c() && jacobi_fits(specs[i].r, specs[i].cc) ? onchip : global).push_back(i);
     }
-    // problems beyond the cluster's shared memory: one cooperative grid each, W in L2/HBM
-    for (size_t i : global) {
-        const SmallSvdSpec& s = specs[i];
-        JacobiInitBatch ib{};
-        JacobiFinBatch fb{};
-        ib.count = fb.count = 1;
-        ib.r[0] = s.r; ib.c[0] = s.cc; ib.A[0] = s.X; ib.lda[0] = s.lda; ib.adj[0] = s.adj; ib.W[0] = W[i];
-        fb.r[0] = s.r; fb.c[0] = s.cc; fb.W[0] = W[i]; fb.sigma[0] = s.sigma; fb.Xn[0] = s.Xn; fb.Js[0] = s.Js;
-        check_cuda(c, jacobi_init(ib, c->stream), "jacobi_init");
-        check_cuda(c, jacobi_svd_global(W[i], s.r, s.cc, ws_get<int>(c, 2), dsweeps[i], c->stream),
-                   "jacobi_svd_global");
-        check_cuda(c, jacobi_finish(fb, s.cc, c->stream), "jacobi_finish");
-        c->launches += 3;
+    // wide problems: block Jacobi over DMMA GEMMs, grouped by shape
+    while (!global.empty()) {
+        std::vector<const SmallSvdSpec*> grp;
+        std::vector<size_t> rest;
+        for (size_t i : global) {
+            const SmallSvdSpec& s = specs[i];
+            if (grp.empty() || (s.r == grp[0]->r && s.cc == grp[0]->cc && (int)grp.size() < kBjMaxProblems))
+                grp.push_back(&s);
+            else
+                rest.push_back(i);
+        }
+        block_jacobi_group(c, grp);
+        global.swap(rest);
     }
     for (size_t base = 0; base < onchip.size(); base += kMaxSmall) {
         const size_t end = std::min(onchip.size(), base + kMaxSmall);

@@ -6,6 +6,7 @@
 #pragma once
 #include <vector>
 
+#include "blockjac.cuh"
 #include "ctx.cuh"
 #include "smallla.cuh"
 #include "tebd_kernels.cuh"

@@ -243,7 +243,6 @@ __global__ void __launch_bounds__(CHOL_THREADS) chol_inv_kernel(const __grid_con
 }
 
 // ============================================================================ Jacobi SVD
-constexpr int JAC_THREADS = 256;      // grid-wide kernel: one warp per column pair
 constexpr int JAC_CL_THREADS = 512;   // cluster kernel: up to 16 column pairs per round
 constexpr int kMaxPairsPerRound = JAC_CL_THREADS / 32;
 constexpr int kMaxSweeps = 60;
@@ -389,36 +388,6 @@ __global__ void __launch_bounds__(JAC_CL_THREADS) jacobi_kernel(const __grid_con
     }
     cluster.sync();  // peers may still read our counters
     if (rank == 0 && tid == 0 && b.sweeps[p] != nullptr) *b.sweeps[p] = sweep + 1;
-}
-
-__global__ void __launch_bounds__(JAC_THREADS) jacobi_global_kernel(cplx* __restrict__ W, int r, int c,
-                                                                   int* counters, int* sweeps_out) {
-    cg::grid_group grid = cg::this_grid();
-    const int n = c + (c & 1);  // odd c: one dummy player sits out each step
-    const int ld = r + c;
-    const int lane = threadIdx.x & 31;
-    const int nwarps = gridDim.x * (JAC_THREADS / 32);
-    const int gw = blockIdx.x * (JAC_THREADS / 32) + (threadIdx.x >> 5);
-    const double tol = sqrt((double)max(r, 1)) * kEps;
-    int sweep = 0;
-    for (; sweep < kMaxSweeps; ++sweep) {
-        int myrot = 0;
-        for (int t = 0; t < n - 1; ++t) {
-            for (int k = gw; k < n / 2; k += nwarps) {
-                const int gp = circle(k, t, n), gq = circle(n - 1 - k, t, n);
-                if (gp >= c || gq >= c) continue;
-                myrot += hestenes_rotate(W + (long long)gp * ld, W + (long long)gq * ld, r, ld, lane, tol);
-            }
-            grid.sync();
-        }
-        if (lane == 0 && myrot) atomicAdd(&counters[sweep & 1], myrot);
-        grid.sync();
-        const int total = *((volatile int*)&counters[sweep & 1]);
-        // every block read the other slot at the previous check: recycle it for the next sweep
-        if (blockIdx.x == 0 && threadIdx.x == 0) counters[(sweep + 1) & 1] = 0;
-        if (total == 0) break;
-    }
-    if (blockIdx.x == 0 && threadIdx.x == 0 && sweeps_out != nullptr) *sweeps_out = sweep + 1;
 }
 
 __global__ void __launch_bounds__(256) colnorm_max_kernel(const __grid_constant__ ColNormBatch b) {
@@ -587,24 +556,6 @@ cudaError_t chol_inv(const CholBatch& b, int max_l, cudaStream_t s) {
     cudaError_t e = cudaFuncSetAttribute(chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     chol_inv_kernel<<<b.count, CHOL_THREADS, smem, s>>>(b);
-    return cudaGetLastError();
-}
-
-cudaError_t jacobi_svd_global(cplx* W, int r, int c, int* counters, int* sweeps, cudaStream_t s) {
-    cudaError_t e = cudaMemsetAsync(counters, 0, 2 * sizeof(int), s);
-    if (e != cudaSuccess) return e;
-    int per_sm = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, jacobi_global_kernel, JAC_THREADS, 0);
-    if (e != cudaSuccess) return e;
-    int dev = 0, nsm = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    const int pairs = (c + 1) / 2;
-    const int want = (pairs + JAC_THREADS / 32 - 1) / (JAC_THREADS / 32);
-    const int grid = std::max(1, std::min(want, per_sm * nsm));
-    void* args[] = {&W, &r, &c, &counters, &sweeps};
-    e = cudaLaunchCooperativeKernel((const void*)jacobi_global_kernel, dim3(grid), dim3(JAC_THREADS), args, 0, s);
-    if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }
 

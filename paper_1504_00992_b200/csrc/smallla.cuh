@@ -62,11 +62,7 @@ struct JacobiBatch {
 };
 cudaError_t jacobi_svd(const JacobiBatch& b, int max_r, int max_c, cudaStream_t s);
 
-// The same one-sided Jacobi for ONE problem too large for the on-chip cluster: W stays in
-// global memory (L2-resident when it fits), a persistent cooperative grid runs the round-robin
-// steps (one warp per column pair, a grid barrier between steps).  `counters` = 2 device ints
-// (zeroed here); `sweeps` (nullable) receives the sweep count.
-cudaError_t jacobi_svd_global(cplx* W, int r, int c, int* counters, int* sweeps, cudaStream_t s);
+
 
 // Load W from a row-major matrix: X = A (r x c) if !adj, or X = A^H when adj (A is c x r);
 // J = I.
