@@ -137,6 +137,12 @@ def run_partitioned(args, rank, world, local_rank):
     from paper_1504_00992_b200.parallel import BlockSpec, ChainPartition, DeviceBlock, TorchComm
 
     torch.cuda.set_device(local_rank)
+    if "RANK" not in os.environ:  # --force-partition without torchrun: a one-rank group on 127.0.0.1
+        import socket
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        os.environ.update(RANK="0", WORLD_SIZE="1", LOCAL_RANK="0", MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
@@ -205,6 +211,33 @@ def run_partitioned(args, rank, world, local_rank):
     ups_rank = sum(1 for p, _ in plan for j in spec.local_bonds if j % 2 == p)
     ups = torch.tensor([ups_rank], device="cuda", dtype=torch.float64)
     dist.all_reduce(ups)
+
+    # ---- end-to-end: every step each rank uploads its block from pinned host memory through the
+    # C ABI, steps, and downloads its owned sites back; max over ranks of the wall time
+    import ctypes as C
+    pin_g = [torch.from_numpy(site_gamma(gs)).pin_memory() for gs in local]
+    pin_l = [torch.from_numpy(lam(gs)).pin_memory() if i + 1 < len(local) else None for i, gs in enumerate(local)]
+    own = b - a
+    e2e_steps = max(1, min(args.steps, 2))
+    dist.barrier()
+    torch.cuda.synchronize()
+    te0 = time.perf_counter()
+    h2d = d2h = 0
+    for st in range(e2e_steps):
+        blk.set_edges(lam(a - 1) if a > 0 else None, lam(local[-1]) if local[-1] + 1 < n else None)
+        for i in range(len(local)):
+            blk.set_gamma(i, pin_g[i], pin_l[i])
+        h2d = sum(t.numel() * 16 for t in pin_g) + sum(t.numel() * 8 for t in pin_l if t is not None)
+        part.evolve(gates, plan, dt, 1, be, 7, step0=st)
+        d2h = 0
+        for i in range(own):
+            buf = torch.empty(blk.mps.dims(i), dtype=torch.complex128).pin_memory()
+            ctx.check(P.lib().rrsvd_b200_mps_get_site(blk.mps.h, i, None, C.c_void_p(buf.data_ptr()), None))
+            d2h += buf.numel() * 16
+    torch.cuda.synchronize()
+    te = torch.tensor([time.perf_counter() - te0], device="cuda")
+    dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e = world * e2e_steps / float(te.item())
     if rank == 0:
         print(json.dumps({
             "metric": METRIC, "value": round(world * args.steps / elapsed, 6), "unit": "steps/s",
@@ -221,7 +254,9 @@ def run_partitioned(args, rank, world, local_rank):
             "decimations_per_s": round(float(ups.item()) * args.steps / elapsed, 3),
             "roofline": {"bound": "tensor", "peak": round(peak_dmma, 3), "unit": "TFLOP/s", "achieved": None,
                          "frac": None, "note": "per-launch roofline is reported by the N=1 run"},
-            "e2e": None, "gpu_launches": int(gpu_launches), "clocks": clk.summary(),
+            "e2e": {"value": round(e2e, 6), "unit": "steps/s", "h2d_bytes_per_step": int(h2d),
+                    "d2h_bytes_per_step": int(d2h), "note": "rank 0's bytes; every rank stages its own block"},
+            "gpu_launches": int(gpu_launches), "clocks": clk.summary(),
         }), flush=True)
     dist.barrier()
     dist.destroy_process_group()
