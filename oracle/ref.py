@@ -426,3 +426,45 @@ class RefMps:
         out = np.empty(total, np.complex128)
         _check(lib().ref_dense_coefficients(C.c_void_p(self.h), _p(out)))
         return out
+
+
+# ---- file formats and the experiment drivers -----------------------
+
+def _s(text: str) -> bytes:
+    return text.encode()
+
+
+def write_rrsm(path: str, a):
+    a = _c(a)
+    _check(lib().ref_write_rrsm(_s(path), _p(a), U64(a.shape[0]), U64(a.shape[1])))
+
+
+def read_rrsm(path: str) -> np.ndarray:
+    r, c = U64(), U64()
+    _check(lib().ref_read_rrsm_dims(_s(path), C.byref(r), C.byref(c)))
+    out = np.empty((r.value, c.value), np.complex128)
+    _check(lib().ref_read_rrsm(_s(path), _p(out)))
+    return out
+
+
+def write_value_lines(path: str, values):
+    v = _d(values)
+    _check(lib().ref_write_value_lines(_s(path), _p(v), U64(v.size)))
+
+
+def write_coefficients(path: str, t0: float, omegas, hoppings):
+    om, hop = _d(omegas), _d(hoppings if len(hoppings) else [0.0])
+    _check(lib().ref_write_coefficients(_s(path), C.c_double(t0), _p(om), U64(om.size), _p(hop)))
+
+
+def run_tebd(out: str, model: str = "ising", coeffs: str = "", sites: int = 6, chi: int = 32, dt: float = 1e-3,
+             steps: int = 100, backend: str = "det", epsilon: float = 0.0, q: int = 2, oversampling: int = 0,
+             crossover: int = 256, coupling: float = 1.0, field: float = 1.0, trunc_tolerance: float = 0.0,
+             abort_threshold: float = 1.0, boson_dim: int = 4, sys_epsilon: float = 1.0, sys_delta: float = 1.0,
+             seed: int = 1, observables_out: str = "", state_out: str = "") -> int:
+    """experiments.cpp run_tebd (the reference's `tebd-run`); returns its exit code."""
+    D = C.c_double
+    return int(lib().ref_run_tebd(_s(model), _s(coeffs), U64(sites), U64(chi), D(dt), U64(steps), _s(backend),
+                                  D(epsilon), U64(q), U64(oversampling), U64(crossover), D(coupling), D(field),
+                                  D(trunc_tolerance), D(abort_threshold), U64(boson_dim), D(sys_epsilon),
+                                  D(sys_delta), U64(seed), _s(out), _s(observables_out), _s(state_out)))

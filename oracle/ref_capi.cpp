@@ -24,7 +24,9 @@
 #include "rrsvd/matgen.hpp"
 #include "rrsvd/mps.hpp"
 #include "rrsvd/randomized.hpp"
+#include "rrsvd/matrix_io.hpp"
 #include "rrsvd/tebd.hpp"
+#include "experiments.hpp"
 
 using rrsvd::cplx;
 using rrsvd::DenseMatrix;
@@ -458,6 +460,64 @@ int ref_dense_coefficients(void* h, double* out) {
         const auto c = tebd::dense_coefficients(*static_cast<tebd::MpsState*>(h));
         std::memcpy(out, c.data(), c.size() * sizeof(cplx));
     });
+}
+
+}  // extern "C"
+
+// ---- file formats and the experiment drivers -------------------
+extern "C" {
+
+int ref_write_rrsm(const char* path, const double* a, std::uint64_t rows, std::uint64_t cols) {
+    return guarded([&] { rrsvd::write_rrsm(path, load(a, rows, cols)); });
+}
+
+int ref_read_rrsm_dims(const char* path, std::uint64_t* rows, std::uint64_t* cols) {
+    return guarded([&] {
+        const rrsvd::DenseMatrix m = rrsvd::read_rrsm(path);
+        *rows = m.rows();
+        *cols = m.cols();
+    });
+}
+
+int ref_read_rrsm(const char* path, double* out) {
+    return guarded([&] { store(rrsvd::read_rrsm(path), out); });
+}
+
+int ref_write_value_lines(const char* path, const double* v, std::uint64_t n) {
+    return guarded([&] { rrsvd::write_value_lines(path, std::vector<double>(v, v + n)); });
+}
+
+int ref_write_coefficients(const char* path, double t0, const double* omegas, std::uint64_t n,
+                           const double* hoppings) {
+    return guarded([&] {
+        rrsvd::chainmap::ChainCoefficients c;
+        c.t0 = t0;
+        c.omegas.assign(omegas, omegas + n);
+        if (n > 1) c.hoppings.assign(hoppings, hoppings + n - 1);
+        rrsvd::chainmap::write_coefficients_file(path, c);
+    });
+}
+
+// experiments.cpp run_tebd with every TebdRunConfig field; returns the driver's exit code
+// (or -1 when it threw).
+int ref_run_tebd(const char* model, const char* coeffs, std::uint64_t sites, std::uint64_t chi, double dt,
+                 std::uint64_t steps, const char* backend, double epsilon, std::uint64_t q,
+                 std::uint64_t oversampling, std::uint64_t crossover, double coupling, double field,
+                 double trunc_tol, double abort_thr, std::uint64_t boson_dim, double sys_eps,
+                 double sys_delta, std::uint64_t seed, const char* out, const char* obs_out,
+                 const char* state_out) {
+    int rc = -1;
+    guarded([&] {
+        rrsvd::bench::TebdRunConfig c;
+        c.model = model; c.coeffs_file = coeffs; c.sites = sites; c.chi = chi; c.dt = dt; c.steps = steps;
+        c.backend = backend; c.epsilon = epsilon; c.q = q; c.oversampling = oversampling;
+        c.det_crossover = crossover; c.coupling = coupling; c.field = field; c.trunc_tolerance = trunc_tol;
+        c.abort_threshold = abort_thr; c.boson_dim = boson_dim; c.sys_epsilon = sys_eps;
+        c.sys_delta = sys_delta; c.seed = seed; c.out = out; c.observables_out = obs_out;
+        c.state_out = state_out;
+        rc = rrsvd::bench::run_tebd(c);
+    });
+    return rc;
 }
 
 }  // extern "C"
