@@ -322,6 +322,35 @@ void evolve_core(rrsvd_b200_mps* s, rrsvd_b200_ctx* c, size_t n_sweeps, const rr
                 std::vector<cplx*> gin1(nbnd), gin2(nbnd);
                 std::vector<double*> lin(nbnd);
                 std::vector<void*> old_bufs;
+                // An abort (tebd.cpp:317-321) leaves the bonds after the offending one untouched;
+                // the batch updates them all, so with an abort threshold in force the sweep's
+                // inputs are snapshotted and those bonds restored if it fires.
+                struct Snap {
+                    cplx *g1, *g2;
+                    double* lam;
+                    int chi;
+                    size_t n1, n2;
+                };
+                std::vector<Snap> snaps;
+                if (abort_thr < 1.0) {
+                    for (size_t i = 0; i < nbnd; ++i) {
+                        const int b = bonds[i];
+                        Snap sn;
+                        sn.chi = s->dr[b];
+                        sn.n1 = (size_t)s->dl[b] * s->d[b] * s->dr[b];
+                        sn.n2 = (size_t)s->dl[b + 1] * s->d[b + 1] * s->dr[b + 1];
+                        sn.g1 = ws_get<cplx>(c, sn.n1);
+                        sn.g2 = ws_get<cplx>(c, sn.n2);
+                        sn.lam = ws_get<double>(c, (size_t)sn.chi);
+                        check_cuda(c, cudaMemcpyAsync(sn.g1, s->g[b], sn.n1 * sizeof(cplx), cudaMemcpyDeviceToDevice,
+                                                      c->stream), "snapshot");
+                        check_cuda(c, cudaMemcpyAsync(sn.g2, s->g[b + 1], sn.n2 * sizeof(cplx),
+                                                      cudaMemcpyDeviceToDevice, c->stream), "snapshot");
+                        check_cuda(c, cudaMemcpyAsync(sn.lam, s->lam[b], (size_t)sn.chi * sizeof(double),
+                                                      cudaMemcpyDeviceToDevice, c->stream), "snapshot");
+                        snaps.push_back(sn);
+                    }
+                }
                 for (size_t i = 0; i < nbnd; ++i) {
                     const int b = bonds[i];
                     // with the accuracy check a bond may grow past chi_max (tebd.cpp:177-179):
@@ -381,7 +410,6 @@ void evolve_core(rrsvd_b200_mps* s, rrsvd_b200_ctx* c, size_t n_sweeps, const rr
                                               c->stream), "D2H");
                 check_cuda(c, cudaStreamSynchronize(c->stream), "sync");
                 if (c->gemm_timing) flush_gemm_timing(c);
-                ws_reset(c);
                 float t01 = 0, t12 = 0, t23 = 0;
                 cudaEventElapsedTime(&t01, ev[0], ev[1]);
                 cudaEventElapsedTime(&t12, ev[1], ev[2]);
@@ -403,9 +431,24 @@ void evolve_core(rrsvd_b200_mps* s, rrsvd_b200_ctx* c, size_t n_sweeps, const rr
                     if (1.0 - diag->kept_fraction > abort_thr) {  // tebd.cpp:317-321
                         diag->aborted = 1;
                         diag->abort_step = step;
+                        for (size_t j = i + 1; j < nbnd; ++j) {  // un-apply the later bonds of the batch
+                            const int bj = bonds[j];
+                            const Snap& sn = snaps[j];
+                            check_cuda(c, cudaMemcpyAsync(s->g[bj], sn.g1, sn.n1 * sizeof(cplx),
+                                                          cudaMemcpyDeviceToDevice, c->stream), "restore");
+                            check_cuda(c, cudaMemcpyAsync(s->g[bj + 1], sn.g2, sn.n2 * sizeof(cplx),
+                                                          cudaMemcpyDeviceToDevice, c->stream), "restore");
+                            check_cuda(c, cudaMemcpyAsync(s->lam[bj], sn.lam, (size_t)sn.chi * sizeof(double),
+                                                          cudaMemcpyDeviceToDevice, c->stream), "restore");
+                            s->dr[bj] = sn.chi;
+                            s->dl[bj + 1] = sn.chi;
+                        }
+                        check_cuda(c, cudaStreamSynchronize(c->stream), "sync");
+                        ws_reset(c);
                         return;
                     }
                 }
+                ws_reset(c);
             }
         }
     }
