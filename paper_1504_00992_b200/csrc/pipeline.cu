@@ -51,6 +51,7 @@ void gemm_many(rrsvd_b200_ctx* c, GemmOp opA, const std::vector<GemmSpec>& specs
             P.subB = s.subB;
             P.subC = s.subC;
             P.D = s.D; P.ldd = s.ldd; P.alpha = s.alpha;
+            P.pred = s.pred; P.pred_want = s.pred_want;
             int split = 1;
             if (total < target && s.k > 128) {
                 split = (int)std::min<long long>((target + total - 1) / total, (s.k + 63) / 64);
@@ -61,7 +62,9 @@ void gemm_many(rrsvd_b200_ctx* c, GemmOp opA, const std::vector<GemmSpec>& specs
                 P.partial = ws_get<cplx>(c, (size_t)split * s.batch * s.m * s.n);
                 any_split = true;
             }
-            flops += 8.0 * s.m * s.n * (double)s.k * s.batch;
+            // a predicated problem may not run: its flops are left out of the roofline (its
+            // launch time still counts — conservative)
+            if (s.pred == nullptr) flops += 8.0 * s.m * s.n * (double)s.k * s.batch;
         }
         if (g.count == 0) continue;
         cudaEvent_t ea = nullptr, eb = nullptr;
@@ -212,8 +215,105 @@ void chol_inv_many(rrsvd_b200_ctx* c, const std::vector<CholSpec>& specs) {
     }
 }
 
+// Adaptive schedule (every l <= kMaxCholL): the first, shifted pass also reports whether some
+// pivot fell within kIllRatio of the shift (cond(Y) beyond what one shifted pass resolves,
+// rank deficiency included).  Only then do the robust schedule's extra passes run — predicated
+// on that device flag, so the host never waits:
+//   full (kFullPasses):  shifted Y->a | [ill] shifted a->b, plain b->a | plain a->Q
+//   span (kSpanPasses):  shifted Y->a | [ill] shifted a->b              | Q = ill ? b : a
+// A well-conditioned basis thus costs 2 (full) or 1 (span) passes instead of 4 or 2, with the
+// same guarantees: after a shifted pass with every pivot >= 1e4 s, cond(Q) - 1 <= 5e-5.
+void orth_many_adaptive(rrsvd_b200_ctx* c, const std::vector<OrthSpec>& specs, bool full) {
+    const size_t np = specs.size();
+    struct Buf {
+        cplx *G, *T, *a, *b;
+        const cplx* y;
+    };
+    std::vector<Buf> bufs(np);
+    int* ill = ws_get<int>(c, np);
+    for (size_t i = 0; i < np; ++i) {
+        const OrthSpec& s = specs[i];
+        if (s.m < s.l) throw_contract(c, "qr: requires rows >= cols");
+        bufs[i] = {ws_get<cplx>(c, (size_t)s.l * s.l), ws_get<cplx>(c, (size_t)s.l * s.l),
+                   ws_get<cplx>(c, (size_t)s.m * s.l), ws_get<cplx>(c, (size_t)s.m * s.l), s.Y};
+    }
+    // one pass for every problem: Gram, chol_inv, apply  (pred: run only if *pred == want)
+    auto pass = [&](bool shifted, std::vector<const cplx*> src, std::vector<cplx*> dst, bool first,
+                     const int* pred_base, int want, bool last) {
+        std::vector<GemmSpec> gram, apply;
+        for (size_t base = 0; base < np; base += kMaxSmall) {
+            CholBatch cb{};
+            int max_l = 0;
+            for (size_t i = base; i < std::min(np, base + kMaxSmall); ++i) {
+                const OrthSpec& s = specs[i];
+                const int k = cb.count++;
+                cb.l[k] = s.l;
+                cb.G[k] = bufs[i].G;
+                cb.T[k] = bufs[i].T;
+                cb.shift_scale[k] = shifted ? 10.0 * (s.m + s.l) : 0.0;
+                cb.dep_tol[k] = 0.0;
+                cb.ndead[k] = last ? s.ndead : nullptr;
+                cb.ill_out[k] = first ? ill + i : nullptr;
+                cb.pred[k] = pred_base ? pred_base + i : nullptr;
+                max_l = std::max(max_l, s.l);
+            }
+            (void)want;
+            if (base == 0) {
+                for (size_t i = 0; i < np; ++i) {
+                    const OrthSpec& s = specs[i];
+                    GemmSpec gs{s.l, s.l, s.m, src[i], s.l, src[i], s.l, bufs[i].G, s.l};
+                    gs.structure = kUpperC;
+                    if (pred_base) { gs.pred = pred_base + i; gs.pred_want = want; }
+                    gram.push_back(gs);
+                }
+                c->gemm_tag = 3;
+                gemm_many(c, kOpC, gram);
+            }
+            check_cuda(c, chol_inv(cb, max_l, c->stream), "chol_inv");
+            c->launches++;
+        }
+        for (size_t i = 0; i < np; ++i) {
+            const OrthSpec& s = specs[i];
+            GemmSpec as{s.m, s.l, s.l, src[i], s.l, bufs[i].T, s.l, dst[i], s.l};
+            as.structure = kTriB;
+            if (pred_base) { as.pred = pred_base + i; as.pred_want = want; }
+            apply.push_back(as);
+        }
+        c->gemm_tag = 4;
+        gemm_many(c, kOpN, apply);
+    };
+    std::vector<const cplx*> Y(np), A(np), B(np);
+    std::vector<cplx*> Aw(np), Bw(np), Q(np);
+    for (size_t i = 0; i < np; ++i) {
+        Y[i] = specs[i].Y; A[i] = Aw[i] = bufs[i].a; B[i] = Bw[i] = bufs[i].b; Q[i] = specs[i].Q;
+    }
+    pass(true, Y, Aw, true, nullptr, 1, false);          // shifted Y -> a, flags
+    pass(true, A, Bw, false, ill, 1, false);             // [ill] shifted a -> b
+    if (full) {
+        pass(false, B, Aw, false, ill, 1, false);        // [ill] plain b -> a
+        pass(false, A, Q, false, nullptr, 1, true);      // plain a -> Q
+    } else {
+        for (size_t base = 0; base < np; base += kMaxSmall) {  // Q = ill ? b : a
+            SelectBatch sb{};
+            for (size_t i = base; i < std::min(np, base + kMaxSmall); ++i) {
+                const int k = sb.count++;
+                sb.flag[k] = ill + i; sb.A[k] = bufs[i].a; sb.B[k] = bufs[i].b; sb.Q[k] = specs[i].Q;
+                sb.n[k] = (long long)specs[i].m * specs[i].l;
+            }
+            check_cuda(c, select_many(sb, c->stream), "select");
+            c->launches++;
+        }
+    }
+}
+
 void orth_many(rrsvd_b200_ctx* c, const std::vector<OrthSpec>& specs, int passes) {
     if (specs.empty()) return;
+    bool adaptive = passes == kFullPasses || passes == kSpanPasses;
+    for (const OrthSpec& s : specs) adaptive = adaptive && s.l <= kMaxCholL;
+    if (adaptive) {
+        orth_many_adaptive(c, specs, passes == kFullPasses);
+        return;
+    }
     struct Buf {
         cplx *G, *T, *a, *b;
     };

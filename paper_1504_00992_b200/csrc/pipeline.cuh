@@ -39,6 +39,8 @@ struct GemmSpec {
     const cplx* D = nullptr;   // optional addend: C = D + alpha * product (zgemm.cuh)
     long long ldd = 0;
     double alpha = 1.0;
+    const int* pred = nullptr;  // optional device predicate (zgemm.cuh)
+    int pred_want = 1;
 };
 
 // Grouped complex GEMMs sharing op(A); split-K chosen so the whole group fills the GPU.

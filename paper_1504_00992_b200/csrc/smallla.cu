@@ -42,10 +42,13 @@ __global__ void __launch_bounds__(CHOL_THREADS) chol_inv_kernel(const __grid_con
     __shared__ double s_shift;
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = CHOL_THREADS / 32;
+    if (b.pred[p] != nullptr && *b.pred[p] == 0) return;
     const cplx* G = b.G[p];
     const long long ldg = b.ldg[p] > 0 ? b.ldg[p] : l;
     const cplx* Gs = b.Gsub[p];
+    __shared__ int s_ill;
 
+    if (tid == 0) s_ill = 0;
     if (warp == 0) {  // shift from the trace of the whole Gram matrix (also for a trailing block)
         if (b.shift_use[p] != nullptr) {
             if (lane == 0) s_shift = *b.shift_use[p];
@@ -86,32 +89,53 @@ __global__ void __launch_bounds__(CHOL_THREADS) chol_inv_kernel(const __grid_con
     // G[i][k] -= sum_t conj(R[t][i]) R[t][k] is register-tiled: a warp takes RG consecutive rows
     // (their NB coefficients in registers), its lanes sweep the columns.  Two barriers per panel.
     const double dtol = b.dep_tol[p];
+    __shared__ cplx sD[NB * NB];
+    __shared__ double sinv[NB];
     for (int j0 = 0; j0 < l; j0 += NB) {
         const int nb = min(NB, l - j0);
         cplx D[NB][NB];
         double inv[NB];
-        unsigned deadmask = 0;
+        if (warp == 0) {  // the diagonal block, factored by one warp (lanes redundantly)
+            unsigned deadmask = 0;
 #pragma unroll
-        for (int t = 0; t < NB; ++t)
+            for (int t = 0; t < NB; ++t)
 #pragma unroll
-            for (int u = t; u < NB; ++u) D[t][u] = (u < nb) ? P[poff(j0 + t, l) + u - t] : mk(0.0, 0.0);
+                for (int u = t; u < NB; ++u) D[t][u] = (u < nb) ? P[poff(j0 + t, l) + u - t] : mk(0.0, 0.0);
+#pragma unroll
+            for (int t = 0; t < NB; ++t) {
+                inv[t] = 0.0;
+                if (t < nb) {
+                    const double d = D[t][t].x, g = g0[j0 + t];
+                    const bool isdead = !(d > dtol * g) || !(d > 0.0) || !(g > 0.0);
+                    if (lane == 0 && (isdead || !(d >= kIllRatio * s_shift))) s_ill = 1;
+                    const double r = isdead ? 0.0 : sqrt(d);
+                    inv[t] = isdead ? 0.0 : 1.0 / r;
+                    deadmask |= isdead ? (1u << t) : 0u;
+                    D[t][t] = mk(r, 0.0);
+#pragma unroll
+                    for (int u = t + 1; u < NB; ++u) D[t][u] = cscale(D[t][u], inv[t]);
+#pragma unroll
+                    for (int v = t + 1; v < NB; ++v)
+#pragma unroll
+                        for (int u = v; u < NB; ++u) cfnmac(D[v][u], D[t][v], D[t][u]);
+                }
+            }
+            if (lane == 0) {
+#pragma unroll
+                for (int t = 0; t < NB; ++t) {
+                    sinv[t] = inv[t];
+#pragma unroll
+                    for (int u = t; u < NB; ++u) sD[t * NB + u] = D[t][u];
+                    if (t < nb) dead[j0 + t] = (deadmask >> t) & 1u;
+                }
+            }
+        }
+        __syncthreads();
 #pragma unroll
         for (int t = 0; t < NB; ++t) {
-            inv[t] = 0.0;
-            if (t < nb) {
-                const double d = D[t][t].x, g = g0[j0 + t];
-                const bool isdead = !(d > dtol * g) || !(d > 0.0) || !(g > 0.0);
-                const double r = isdead ? 0.0 : sqrt(d);
-                inv[t] = isdead ? 0.0 : 1.0 / r;
-                deadmask |= isdead ? (1u << t) : 0u;
-                D[t][t] = mk(r, 0.0);
+            inv[t] = sinv[t];
 #pragma unroll
-                for (int u = t + 1; u < NB; ++u) D[t][u] = cscale(D[t][u], inv[t]);
-#pragma unroll
-                for (int v = t + 1; v < NB; ++v)
-#pragma unroll
-                    for (int u = v; u < NB; ++u) cfnmac(D[v][u], D[t][v], D[t][u]);
-            }
+            for (int u = t; u < NB; ++u) D[t][u] = sD[t * NB + u];
         }
         for (int k = j0 + nb + tid; k < l; k += CHOL_THREADS) {
             cplx X[NB];
@@ -133,9 +157,6 @@ __global__ void __launch_bounds__(CHOL_THREADS) chol_inv_kernel(const __grid_con
 #pragma unroll
                 for (int u = t; u < NB; ++u)
                     if (u < nb) P[poff(j0 + t, l) + u - t] = D[t][u];
-#pragma unroll
-            for (int t = 0; t < NB; ++t)
-                if (t < nb) dead[j0 + t] = (deadmask >> t) & 1u;
         }
         __syncthreads();
         for (int r0 = j0 + nb + RG * warp; r0 < l; r0 += RG * nw) {
@@ -184,6 +205,11 @@ __global__ void __launch_bounds__(CHOL_THREADS) chol_inv_kernel(const __grid_con
 #pragma unroll
         for (int ch = 0; ch < kChunks; ++ch) {
             const int k = i0 + grp + ch * kGroups;
+            if (i0 + ch * kGroups >= l) {  // block-uniform: this chunk has no column at all
+#pragma unroll
+                for (int t = 0; t < NB; ++t) res[ch][t] = mk(0.0, 0.0);
+                continue;
+            }
             cplx S[NB];
 #pragma unroll
             for (int t = 0; t < NB; ++t) S[t] = mk(0.0, 0.0);
@@ -234,6 +260,7 @@ __global__ void __launch_bounds__(CHOL_THREADS) chol_inv_kernel(const __grid_con
             T[(long long)i * ldt + k] = v;
             if (Tn != nullptr) Tn[(long long)i * ldt + k] = mk(-v.x, -v.y);
         }
+    if (b.ill_out[p] != nullptr && tid == 0) *b.ill_out[p] = s_ill;
     if (b.ndead[p] != nullptr && tid == 0) {
         int n = 0;
         for (int j = 0; j < l; ++j) n += dead[j];
@@ -388,6 +415,14 @@ __global__ void __launch_bounds__(JAC_CL_THREADS) jacobi_kernel(const __grid_con
     }
     cluster.sync();  // peers may still read our counters
     if (rank == 0 && tid == 0 && b.sweeps[p] != nullptr) *b.sweeps[p] = sweep + 1;
+}
+
+__global__ void __launch_bounds__(256) select_kernel(const __grid_constant__ SelectBatch b) {
+    const int p = blockIdx.y;
+    const cplx* src = *b.flag[p] ? b.B[p] : b.A[p];
+    cplx* dst = b.Q[p];
+    for (long long e = blockIdx.x * 256LL + threadIdx.x; e < b.n[p]; e += (long long)gridDim.x * 256)
+        dst[e] = src[e];
 }
 
 __global__ void __launch_bounds__(256) colnorm_max_kernel(const __grid_constant__ ColNormBatch b) {
@@ -556,6 +591,12 @@ cudaError_t chol_inv(const CholBatch& b, int max_l, cudaStream_t s) {
     cudaError_t e = cudaFuncSetAttribute(chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     chol_inv_kernel<<<b.count, CHOL_THREADS, smem, s>>>(b);
+    return cudaGetLastError();
+}
+
+cudaError_t select_many(const SelectBatch& b, cudaStream_t s) {
+    if (b.count == 0) return cudaSuccess;
+    select_kernel<<<dim3(64, b.count), 256, 0, s>>>(b);
     return cudaGetLastError();
 }
 

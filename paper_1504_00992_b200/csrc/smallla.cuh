@@ -35,7 +35,23 @@ struct CholBatch {
     int ndead_acc[kMaxSmall];         // 1: add to *ndead instead of storing
     double* shift_save[kMaxSmall];    // nullable: store the shift used (for later blocks)
     const double* shift_use[kMaxSmall];  // nullable: use this stored shift instead
+    int* ill_out[kMaxSmall];          // nullable: 1 if some pivot is < kIllRatio x the shift (or
+                                      //   dependent), i.e. cond(Y) is beyond one shifted pass
+    const int* pred[kMaxSmall];       // nullable: run only if *pred != 0 (else exit at once)
 };
+constexpr double kIllRatio = 1e4;
+
+// Q[i] = (*flag[i] != 0) ? B[i] : A[i] (n[i] elements each) — the data-dependent end of the
+// adaptive orthonormalisation schedule (pipeline.cu orth_many).
+struct SelectBatch {
+    int count;
+    const int* flag[kMaxSmall];
+    const cplx* A[kMaxSmall];
+    const cplx* B[kMaxSmall];
+    cplx* Q[kMaxSmall];
+    long long n[kMaxSmall];
+};
+cudaError_t select_many(const SelectBatch& b, cudaStream_t s);
 cudaError_t chol_inv(const CholBatch& b, int max_l, cudaStream_t s);
 bool jacobi_fits(int r, int c);  // an r x c problem fits jacobi_svd's on-chip capacity
 

@@ -63,6 +63,7 @@ zgemm_dmma_kernel(const __grid_constant__ GemmGroup g) {
 
     const int pid = find_problem(g, blockIdx.x);
     const GemmProblem& P = g.p[pid];
+    if (P.pred != nullptr && *P.pred != P.pred_want) return;
     int t = blockIdx.x - P.tile_begin;
     const int tn = t % P.tiles_n; t /= P.tiles_n;
     const int tm = t % P.tiles_m; t /= P.tiles_m;
@@ -260,6 +261,7 @@ __global__ void splitk_reduce_kernel(const __grid_constant__ GemmGroup g) {
     const int pid = blockIdx.y;
     const GemmProblem& P = g.p[pid];
     if (P.split <= 1) return;
+    if (P.pred != nullptr && *P.pred != P.pred_want) return;
     const long long per = (long long)P.m * P.n;
     const long long total = per * P.batch;
     for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;

@@ -50,6 +50,10 @@ struct GemmProblem {
     const cplx* D;
     long long ldd;
     double alpha;
+    // Optional device predicate: the problem runs only if *pred == pred_want (otherwise its CTAs
+    // exit at once and C is left untouched) — data-dependent schedules without a host sync.
+    const int* pred;
+    int pred_want;
     // filled by the launcher
     int tiles_m, tiles_n, tile_begin;
 };
