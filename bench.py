@@ -580,7 +580,8 @@ def cpu_baseline(args, wl, gammas, lambdas, gates, plan, samples=2):
     sec = ref_update_sample(ref, wl, gammas, lambdas, gates, plan, bonds, 7)
     ups = updates_per_step(wl["site_dims"], wl["terms"])
     return {"value": round(1.0 / (sec * ups), 8), "unit": "steps/s", "cores": cores, "kind": "reference",
-            "sample": f"{samples} interior bond updates (build_theta+apply_gate+decimate, RRSVD) of the "
+            "sample": f"{samples} interior bond updates (build_theta+apply_gate+decimate, "
+                      f"{'RRSVD' if wl['backend'].get('randomized') else 'deterministic SVD'}) of the "
                       f"same state, {sec:.3f} s/update, extrapolated x{ups} updates/step",
             "blas": ref.blas_info()["core"]}
 
