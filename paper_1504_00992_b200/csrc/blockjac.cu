@@ -51,8 +51,8 @@ __global__ void __launch_bounds__(kBjThreads) bj_step_kernel(const __grid_consta
     cg::cluster_group cluster = cg::this_cluster();
     const int S = (int)cluster.num_blocks(), crank = (int)cluster.block_rank();
     extern __shared__ __align__(16) unsigned char sm[];
-    auto ch = reinterpret_cast<cplx(*)[n2]>(sm);                        // [kBjRows][n2]
-    auto sG = reinterpret_cast<cplx(*)[ld]>(sm + sizeof(cplx) * kBjRows * n2);  // [n2][ld]
+    auto ch = reinterpret_cast<cplx(*)[ld]>(sm);                        // [kBjRows][ld]
+    auto sG = reinterpret_cast<cplx(*)[ld]>(sm + sizeof(cplx) * kBjRows * ld);  // [n2][ld]
     auto sW = sG + n2;                                                    // [n2][ld]
     __shared__ double pc[half], ps[half];
     __shared__ cplx pe[half];
@@ -65,55 +65,61 @@ __global__ void __launch_bounds__(kBjThreads) bj_step_kernel(const __grid_consta
     const long long col0 = (long long)k0 * n2;  // the pair's first column (slots 2k0, 2k0+1)
     const cplx* X = a.Xs[pr];
 
-    // ---- Gram: thread (pi, qi) of a 16 x 16 grid owns the 2 x 2 block rows 2pi.., columns
-    // 2qi..; only blocks on or above the diagonal work (136 of 256 threads)
-    const int pi = tid >> 4, qi = tid & 15;
-    const bool gw = qi >= pi;
-    cplx g00 = mk(0.0, 0.0), g01 = g00, g10 = g00, g11 = g00;
+    // ---- Gram of this CTA's row slice on the FP64 tensor core: the 32 x 32 result is 4 x 4 tiles
+    // of 8 x 8; warp w accumulates tiles (pt = w/2, qt = 2(w%2) + {0,1}).  Fragments are one
+    // LDS.128 (re, im) per lane; conj(X)^T X in 4M form: Re += xr xr' + xi xi', Im += xr xi' - xi xr'.
+    const int lane = tid & 31, warp = tid >> 5;
+    const int pt = warp >> 1, qa = 2 * (warp & 1);
+    double gre[2][2] = {{0.0, 0.0}, {0.0, 0.0}}, gim[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
     for (int r0 = xr0; r0 < xr1; r0 += kBjRows) {
-        const int nr = min(kBjRows, xr1 - r0);
+        const int nr = min(kBjRows, xr1 - r0), nr4 = (nr + 3) & ~3;
         __syncthreads();
-        for (int e = tid; e < nr * n2; e += kBjThreads)
-            ch[e / n2][e % n2] = X[(long long)(r0 + e / n2) * cp + col0 + e % n2];
+        for (int e = tid; e < nr4 * n2; e += kBjThreads) {
+            const int i = e / n2, j = e % n2;
+            ch[i][j] = i < nr ? X[(long long)(r0 + i) * cp + col0 + j] : mk(0.0, 0.0);
+        }
         __syncthreads();
-        if (gw) {
-#pragma unroll 4
-            for (int i = 0; i < nr; ++i) {
-                const cplx x0 = ch[i][2 * pi], x1 = ch[i][2 * pi + 1];
-                const cplx y0 = ch[i][2 * qi], y1 = ch[i][2 * qi + 1];
-                cfmac(g00, x0, y0); cfmac(g01, x0, y1);
-                cfmac(g10, x1, y0); cfmac(g11, x1, y1);
+        for (int k0 = 0; k0 < nr4; k0 += 4) {
+            const cplx xa = ch[k0 + (lane & 3)][pt * 8 + (lane >> 2)];
+#pragma unroll
+            for (int qq = 0; qq < 2; ++qq) {
+                const cplx xb = ch[k0 + (lane & 3)][(qa + qq) * 8 + (lane >> 2)];
+                dmma884(gre[qq][0], gre[qq][1], xa.x, xb.x);
+                dmma884(gre[qq][0], gre[qq][1], xa.y, xb.y);
+                dmma884(gim[qq][0], gim[qq][1], xa.x, xb.y);
+                dmma884(gim[qq][0], gim[qq][1], -xa.y, xb.x);
             }
         }
     }
-    if (gw) {  // the slice's partial Gram (upper blocks) into this CTA's sG
-        sG[2 * pi][2 * qi] = g00; sG[2 * pi][2 * qi + 1] = g01;
-        sG[2 * pi + 1][2 * qi] = g10; sG[2 * pi + 1][2 * qi + 1] = g11;
-    }
+#pragma unroll
+    for (int qq = 0; qq < 2; ++qq)
+#pragma unroll
+        for (int c = 0; c < 2; ++c)
+            sG[pt * 8 + (lane >> 2)][(qa + qq) * 8 + 2 * (lane & 3) + c] = mk(gre[qq][c], gim[qq][c]);
     cluster.sync();
     if (crank == 0) {  // (uniform per CTA; barriers below are reached by every thread)
-        // sum the slices in rank order, then mirror to the lower triangle
-        cplx gg[2][2] = {{mk(0.0, 0.0), mk(0.0, 0.0)}, {mk(0.0, 0.0), mk(0.0, 0.0)}};
-        if (gw) {
+        // sum the slices in rank order, then keep the upper triangle and mirror it
+        cplx sum[n2 * n2 / kBjThreads];
+#pragma unroll
+        for (int u = 0; u < n2 * n2 / kBjThreads; ++u) {
+            const int e = tid + u * kBjThreads;
+            sum[u] = mk(0.0, 0.0);
             for (int q = 0; q < S; ++q) {
                 const cplx(*pg)[ld] = cluster.map_shared_rank(sG, q);
-#pragma unroll
-                for (int u = 0; u < 2; ++u)
-#pragma unroll
-                    for (int v = 0; v < 2; ++v) gg[u][v] = cadd(gg[u][v], pg[2 * pi + u][2 * qi + v]);
+                sum[u] = cadd(sum[u], pg[e / n2][e % n2]);
             }
         }
         __syncthreads();  // every read of the partials precedes the writes below
-        if (gw) {
 #pragma unroll
-            for (int u = 0; u < 2; ++u)
-#pragma unroll
-                for (int v = 0; v < 2; ++v) {
-                    const int p = 2 * pi + u, q = 2 * qi + v;
-                    if (q < p) continue;
-                    sG[p][q] = p == q ? mk(gg[u][v].x, 0.0) : gg[u][v];
-                    if (p != q) sG[q][p] = cconj(gg[u][v]);
-                }
+        for (int u = 0; u < n2 * n2 / kBjThreads; ++u) {
+            const int e = tid + u * kBjThreads;
+            sG[e / n2][e % n2] = sum[u];
+        }
+        __syncthreads();
+        for (int e = tid; e < n2 * n2; e += kBjThreads) {
+            const int p = e / n2, q = e % n2;
+            if (p > q) sG[p][q] = cconj(sG[q][p]);
+            else if (p == q) sG[p][q].y = 0.0;
         }
         for (int e = tid; e < n2 * n2; e += kBjThreads) sW[e / n2][e % n2] = mk(e / n2 == e % n2 ? 1.0 : 0.0, 0.0);
         if (tid == 0) s_rot = 0;
@@ -187,39 +193,41 @@ __global__ void __launch_bounds__(kBjThreads) bj_step_kernel(const __grid_consta
         cplx* D = m == 0 ? a.Xd[pr] : a.Vd[pr];
         const int rbeg = m == 0 ? xr0 : vr0, rend = m == 0 ? xr1 : vr1;
         for (int r0 = rbeg; r0 < rend; r0 += kBjRows) {
-            const int nr = min(kBjRows, rend - r0);
+            const int nr = min(kBjRows, rend - r0), nr8 = (nr + 7) & ~7;
             __syncthreads();
-            for (int e = tid; e < nr * n2; e += kBjThreads)
-                ch[e / n2][e % n2] = S[(long long)(r0 + e / n2) * cp + col0 + e % n2];
+            for (int e = tid; e < nr8 * n2; e += kBjThreads) {
+                const int i = e / n2, j = e % n2;
+                ch[i][j] = i < nr ? S[(long long)(r0 + i) * cp + col0 + j] : mk(0.0, 0.0);
+            }
             __syncthreads();
-            // thread: rows tr, tr + 32 of the chunk, columns c0 .. c0 + 3
-            const int tr = tid >> 3, c0 = (tid & 7) * 4;
-            cplx o[2][4];
+            // warp w: rows 8w .. 8w+7 of the chunk times all of W (4 column tiles), on DMMA
+            const int rt = warp;
+            if (rt * 8 < nr) {
+                double are[4][2], aim[4][2];
 #pragma unroll
-            for (int u = 0; u < 2; ++u)
+                for (int ct = 0; ct < 4; ++ct) are[ct][0] = are[ct][1] = aim[ct][0] = aim[ct][1] = 0.0;
 #pragma unroll
-                for (int v = 0; v < 4; ++v) o[u][v] = mk(0.0, 0.0);
-            const bool r1ok = tr + 32 < nr;
-            if (tr < nr) {
-#pragma unroll 4
-                for (int t = 0; t < n2; ++t) {
-                    const cplx x0 = ch[tr][t], x1 = r1ok ? ch[tr + 32][t] : mk(0.0, 0.0);
+                for (int kk = 0; kk < n2 / 4; ++kk) {
+                    const cplx xa = ch[rt * 8 + (lane >> 2)][kk * 4 + (lane & 3)];
 #pragma unroll
-                    for (int v = 0; v < 4; ++v) {
-                        const cplx w = sW[t][c0 + v];
-                        cfma(o[0][v], x0, w);
-                        cfma(o[1][v], x1, w);
+                    for (int ct = 0; ct < 4; ++ct) {
+                        const cplx wb = sW[kk * 4 + (lane & 3)][ct * 8 + (lane >> 2)];
+                        dmma884(are[ct][0], are[ct][1], xa.x, wb.x);
+                        dmma884(are[ct][0], are[ct][1], -xa.y, wb.y);
+                        dmma884(aim[ct][0], aim[ct][1], xa.x, wb.y);
+                        dmma884(aim[ct][0], aim[ct][1], xa.y, wb.x);
                     }
                 }
+                const int i = rt * 8 + (lane >> 2);
+                if (i < nr) {
+                    const long long row = (long long)(r0 + i) * cp;
 #pragma unroll
-                for (int u = 0; u < 2; ++u) {
-                    if (u == 1 && !r1ok) break;
-                    const long long row = (long long)(r0 + tr + 32 * u) * cp;
+                    for (int ct = 0; ct < 4; ++ct)
 #pragma unroll
-                    for (int v = 0; v < 4; ++v) {
-                        const int j = c0 + v;
-                        D[row + (j < b ? dA + j : dB + j - b)] = o[u][v];
-                    }
+                        for (int c = 0; c < 2; ++c) {
+                            const int j = ct * 8 + 2 * (lane & 3) + c;
+                            D[row + (j < b ? dA + j : dB + j - b)] = mk(are[ct][c], aim[ct][c]);
+                        }
                 }
             }
         }
@@ -286,7 +294,7 @@ cudaError_t bj_init(const BjInit& a, cudaStream_t s) {
 cudaError_t bj_step(const BjStep& a, cudaStream_t s) {
     if (a.count == 0) return cudaSuccess;
     if (2 * a.b != kBjN2) return cudaErrorInvalidValue;
-    constexpr size_t smem = sizeof(cplx) * (kBjRows * kBjN2 + 2 * kBjN2 * (kBjN2 + 1));
+    constexpr size_t smem = sizeof(cplx) * (kBjRows * (kBjN2 + 1) + 2 * kBjN2 * (kBjN2 + 1));
     cudaError_t e = cudaFuncSetAttribute(bj_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     // row slices per pair: enough CTAs to cover the GPU ~2x, at most 8 (portable cluster)
