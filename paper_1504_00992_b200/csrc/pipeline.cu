@@ -397,11 +397,12 @@ struct SmallSvdSpec {
 // host-side bookkeeping; one fused launch per step for all pairs of all problems; one
 // 4-byte-per-problem D2H per sweep for the convergence test.
 int block_jacobi_min_c() {  // above this the block method is used (RRSVD_B200_BJ_MIN_C overrides)
-    // measured: the cluster kernel wins while it fits (256^2: 10.6 vs 13.6 ms; C2 4.6 vs 3.3
-    // steps/s); the block method takes the widths the cluster cannot hold
+    // measured: the cluster kernel wins for l = 74 (C1: 2.6 vs 3.0 ms) and the batched 110^2 of
+    // C3 (162 vs 186 ms per step); the DMMA block method wins for C2's batched 256^2 (5.25 vs
+    // 4.60 steps/s) and everything wider
     static const int v = [] {
         const char* e = std::getenv("RRSVD_B200_BJ_MIN_C");
-        return e ? std::atoi(e) : 300;
+        return e ? std::atoi(e) : 160;
     }();
     return v;
 }
