@@ -127,6 +127,9 @@ __global__ void __launch_bounds__(kBjThreads) bj_step_kernel(const __grid_consta
 
     // ---- one sweep of the pair solve
     const double tol = sqrt((double)max(r, 1)) * kEpsBj;
+    __shared__ int s_first;  // rotations of the first inner sweep: the outer convergence signal
+    for (int isw = 0; isw < a.inner_sweeps; ++isw) {
+    const int rot_before = s_rot;
     for (int rd = 0; rd < n2 - 1; ++rd) {
         if (tid < half) {
             const int p = circle_bj(tid, rd, n2), q = circle_bj(n2 - 1 - tid, rd, n2);
@@ -177,7 +180,13 @@ __global__ void __launch_bounds__(kBjThreads) bj_step_kernel(const __grid_consta
         }
         __syncthreads();
     }
-        if (tid == 0 && s_rot) atomicAdd(a.rot[pr], s_rot);
+    if (isw == 0 && tid == 0) s_first = s_rot;
+    const bool more = s_rot != rot_before;
+    __syncthreads();  // (all threads read s_rot before the next sweep changes it)
+    if (!more) break;
+    }
+
+        if (tid == 0 && s_first) atomicAdd(a.rot[pr], s_first);
     }
     cluster.sync();  // W is ready in CTA 0
     if (crank != 0) {

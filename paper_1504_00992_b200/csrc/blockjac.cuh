@@ -37,6 +37,7 @@ cudaError_t bj_init(const BjInit& a, cudaStream_t s);
 // [X_i X_j] W and [V_i V_j] W written straight to the blocks' positions of the next step.
 struct BjStep {
     int count, r, cp, b, npairs;
+    int inner_sweeps;  // sweeps of the pair solve per step (stops early once a sweep rotates nothing)
     const cplx* Xs[kBjMaxProblems];
     cplx* Xd[kBjMaxProblems];
     const cplx* Vs[kBjMaxProblems];

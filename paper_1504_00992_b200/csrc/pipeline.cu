@@ -407,6 +407,13 @@ int block_jacobi_min_c() {  // above this the block method is used (RRSVD_B200_B
     return v;
 }
 constexpr int kBjBlock = 16;
+int bj_inner_sweeps() {  // RRSVD_B200_BJ_INNER overrides
+    static const int v = [] {
+        const char* e = std::getenv("RRSVD_B200_BJ_INNER");
+        return e ? std::max(1, std::atoi(e)) : 1;
+    }();
+    return v;
+}
 
 void block_jacobi_group(rrsvd_b200_ctx* c, const std::vector<const SmallSvdSpec*>& grp) {
     const int np = (int)grp.size();
@@ -458,6 +465,7 @@ void block_jacobi_group(rrsvd_b200_ctx* c, const std::vector<const SmallSvdSpec*
         for (int t = 0; t < nbp - 1; ++t) {
             BjStep st{};
             st.count = np; st.r = r; st.cp = cp; st.b = b; st.npairs = npairs;
+            st.inner_sweeps = bj_inner_sweeps();
             for (int p = 0; p < np; ++p) {
                 st.Xs[p] = X1[p]; st.Xd[p] = X2[p]; st.Vs[p] = V1[p]; st.Vd[p] = V2[p]; st.rot[p] = rot + p;
             }
