@@ -43,6 +43,13 @@ def workload(name: str):
                     backend=dict(randomized=True, target_rank=0, oversampling=10, power_iterations=2,
                                  det_crossover=256, seed=7),
                     desc="TEDOPA spin-boson, spin + 100 bosons (d=20), chi=100, n=2000, RRSVD p=10 q=2")
+    if name == "c3p100":  # config 3 with the paper's oversampling p = k (l = 200)
+        site_dims, terms = M.tedopa_system(n_chain=100, boson_dim=20)
+        return dict(name="tedopa_spin_boson_101sites_d20_chi100_p100", site_dims=site_dims,
+                    terms={b: t for b, t in enumerate(terms)}, chi=100, dt=0.01,
+                    backend=dict(randomized=True, target_rank=0, oversampling=100, power_iterations=2,
+                                 det_crossover=256, seed=7),
+                    desc="TEDOPA spin-boson, spin + 100 bosons (d=20), chi=100, n=2000, RRSVD p=100 q=2")
     if name == "c3det":  # config 3's "vs full SVD" arm: deterministic decimation (tebd.cpp:185)
         site_dims, terms = M.tedopa_system(n_chain=100, boson_dim=20)
         return dict(name="tedopa_spin_boson_101sites_d20_chi100_fullsvd", site_dims=site_dims,
@@ -629,7 +636,7 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="c3", choices=["c3", "c3det", "c2", "c5", "c4"],
+    ap.add_argument("--workload", default="c3", choices=["c3", "c3p100", "c3det", "c2", "c5", "c4"],
                     help="c3 (headline TEBD), c2; c5/c4: row-sharded single-matrix RRSVD")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--force-partition", action="store_true",

@@ -163,6 +163,8 @@ void chol_inv_many(rrsvd_b200_ctx* c, const std::vector<CholSpec>& specs) {
             cb.dep_tol[k] = 0.0;
             cb.ndead[k] = s.ndead;
             cb.ndead_acc[k] = J > 0 ? 1 : 0;
+            cb.ill_out[k] = s.ill_out;
+            cb.pred[k] = s.pred;
             max_l = std::max(max_l, w);
             if (cb.count == kMaxSmall) { chol_launch(cb, max_l); max_l = 0; }
         }
@@ -183,6 +185,7 @@ void chol_inv_many(rrsvd_b200_ctx* c, const std::vector<CholSpec>& specs) {
             up.D = s.G + off(s.l, r0, r0);
             up.ldd = s.l;
             up.alpha = -1.0;
+            if (s.pred) { g1.back().pred = s.pred; up.pred = s.pred; }
             g2.push_back(up);
         }
         if (!g1.empty()) {
@@ -205,6 +208,7 @@ void chol_inv_many(rrsvd_b200_ctx* c, const std::vector<CholSpec>& specs) {
             // T_I,>I = -T_II W
             GemmSpec ts{w, rest, w, s.T + off(s.l, i0, i0), s.l, b.W, rest, s.T + off(s.l, i0, r0), s.l};
             ts.alpha = -1.0;
+            if (s.pred) { g1.back().pred = s.pred; ts.pred = s.pred; }
             g2.push_back(ts);
         }
         if (!g1.empty()) {
@@ -215,7 +219,7 @@ void chol_inv_many(rrsvd_b200_ctx* c, const std::vector<CholSpec>& specs) {
     }
 }
 
-// Adaptive schedule (every l <= kMaxCholL): the first, shifted pass also reports whether some
+// Adaptive schedule (any width): the first, shifted pass also reports whether some
 // pivot fell within kIllRatio of the shift (cond(Y) beyond what one shifted pass resolves,
 // rank deficiency included).  Only then do the robust schedule's extra passes run — predicated
 // on that device flag, so the host never waits:
@@ -237,48 +241,29 @@ void orth_many_adaptive(rrsvd_b200_ctx* c, const std::vector<OrthSpec>& specs, b
         bufs[i] = {ws_get<cplx>(c, (size_t)s.l * s.l), ws_get<cplx>(c, (size_t)s.l * s.l),
                    ws_get<cplx>(c, (size_t)s.m * s.l), ws_get<cplx>(c, (size_t)s.m * s.l), s.Y};
     }
-    // one pass for every problem: Gram, chol_inv, apply  (pred: run only if *pred == want)
+    // one pass for every problem: Gram, chol_inv (any width), apply  (pred: run only if *pred != 0)
     auto pass = [&](bool shifted, std::vector<const cplx*> src, std::vector<cplx*> dst, bool first,
-                     const int* pred_base, int want, bool last) {
+                     const int* pred_base, bool last) {
         std::vector<GemmSpec> gram, apply;
-        for (size_t base = 0; base < np; base += kMaxSmall) {
-            CholBatch cb{};
-            int max_l = 0;
-            for (size_t i = base; i < std::min(np, base + kMaxSmall); ++i) {
-                const OrthSpec& s = specs[i];
-                const int k = cb.count++;
-                cb.l[k] = s.l;
-                cb.G[k] = bufs[i].G;
-                cb.T[k] = bufs[i].T;
-                cb.shift_scale[k] = shifted ? 10.0 * (s.m + s.l) : 0.0;
-                cb.dep_tol[k] = 0.0;
-                cb.ndead[k] = last ? s.ndead : nullptr;
-                cb.ill_out[k] = first ? ill + i : nullptr;
-                cb.pred[k] = pred_base ? pred_base + i : nullptr;
-                max_l = std::max(max_l, s.l);
-            }
-            (void)want;
-            if (base == 0) {
-                for (size_t i = 0; i < np; ++i) {
-                    const OrthSpec& s = specs[i];
-                    GemmSpec gs{s.l, s.l, s.m, src[i], s.l, src[i], s.l, bufs[i].G, s.l};
-                    gs.structure = kUpperC;
-                    if (pred_base) { gs.pred = pred_base + i; gs.pred_want = want; }
-                    gram.push_back(gs);
-                }
-                c->gemm_tag = 3;
-                gemm_many(c, kOpC, gram);
-            }
-            check_cuda(c, chol_inv(cb, max_l, c->stream), "chol_inv");
-            c->launches++;
-        }
+        std::vector<CholSpec> chol;
         for (size_t i = 0; i < np; ++i) {
             const OrthSpec& s = specs[i];
+            GemmSpec gs{s.l, s.l, s.m, src[i], s.l, src[i], s.l, bufs[i].G, s.l};
+            gs.structure = kUpperC;
+            if (pred_base) gs.pred = pred_base + i;
+            gram.push_back(gs);
+            CholSpec cs{bufs[i].G, s.l, shifted ? 10.0 * (s.m + s.l) : 0.0, bufs[i].T, last ? s.ndead : nullptr};
+            cs.ill_out = first ? ill + i : nullptr;
+            cs.pred = pred_base ? pred_base + i : nullptr;
+            chol.push_back(cs);
             GemmSpec as{s.m, s.l, s.l, src[i], s.l, bufs[i].T, s.l, dst[i], s.l};
             as.structure = kTriB;
-            if (pred_base) { as.pred = pred_base + i; as.pred_want = want; }
+            if (pred_base) as.pred = pred_base + i;
             apply.push_back(as);
         }
+        c->gemm_tag = 3;
+        gemm_many(c, kOpC, gram);
+        chol_inv_many(c, chol);
         c->gemm_tag = 4;
         gemm_many(c, kOpN, apply);
     };
@@ -287,11 +272,12 @@ void orth_many_adaptive(rrsvd_b200_ctx* c, const std::vector<OrthSpec>& specs, b
     for (size_t i = 0; i < np; ++i) {
         Y[i] = specs[i].Y; A[i] = Aw[i] = bufs[i].a; B[i] = Bw[i] = bufs[i].b; Q[i] = specs[i].Q;
     }
-    pass(true, Y, Aw, true, nullptr, 1, false);          // shifted Y -> a, flags
-    pass(true, A, Bw, false, ill, 1, false);             // [ill] shifted a -> b
+    check_cuda(c, cudaMemsetAsync(ill, 0, np * sizeof(int), c->stream), "memset");
+    pass(true, Y, Aw, true, nullptr, false);             // shifted Y -> a, flags
+    pass(true, A, Bw, false, ill, false);                // [ill] shifted a -> b
     if (full) {
-        pass(false, B, Aw, false, ill, 1, false);        // [ill] plain b -> a
-        pass(false, A, Q, false, nullptr, 1, true);      // plain a -> Q
+        pass(false, B, Aw, false, ill, false);           // [ill] plain b -> a
+        pass(false, A, Q, false, nullptr, true);         // plain a -> Q
     } else {
         for (size_t base = 0; base < np; base += kMaxSmall) {  // Q = ill ? b : a
             SelectBatch sb{};
@@ -308,56 +294,8 @@ void orth_many_adaptive(rrsvd_b200_ctx* c, const std::vector<OrthSpec>& specs, b
 
 void orth_many(rrsvd_b200_ctx* c, const std::vector<OrthSpec>& specs, int passes) {
     if (specs.empty()) return;
-    bool adaptive = passes == kFullPasses || passes == kSpanPasses;
-    for (const OrthSpec& s : specs) adaptive = adaptive && s.l <= kMaxCholL;
-    if (adaptive) {
-        orth_many_adaptive(c, specs, passes == kFullPasses);
-        return;
-    }
-    struct Buf {
-        cplx *G, *T, *a, *b;
-    };
-    std::vector<Buf> bufs(specs.size());
-    for (size_t i = 0; i < specs.size(); ++i) {
-        const OrthSpec& s = specs[i];
-        if (s.m < s.l) throw_contract(c, "qr: requires rows >= cols");
-        bufs[i] = {ws_get<cplx>(c, (size_t)s.l * s.l), ws_get<cplx>(c, (size_t)s.l * s.l),
-                   ws_get<cplx>(c, (size_t)s.m * s.l), ws_get<cplx>(c, (size_t)s.m * s.l)};
-    }
-    std::vector<const cplx*> cur(specs.size());
-    for (size_t i = 0; i < specs.size(); ++i) cur[i] = specs[i].Y;
-    // Schedule: up to two shifted passes, then plain ones.
-    // The second shifted pass bounds cond(Q) even for rank-deficient Y (whose first-pass basis
-    // keeps roundoff-level directions at ~1e-10), so the plain passes never meet a numerically
-    // indefinite Gram matrix and no live direction is ever dropped — only exactly vanishing
-    // pivots mark a dependent (zero) column, as Householder QR keeps tiny directions too.
-    const int last = passes - 1;
-    const int shifted = std::min(passes, 2);
-    for (int pass = 0; pass < passes; ++pass) {
-        std::vector<GemmSpec> gram, apply;
-        std::vector<CholSpec> chol;
-        for (size_t i = 0; i < specs.size(); ++i) {
-            const OrthSpec& s = specs[i];
-            GemmSpec gsp{s.l, s.l, s.m, cur[i], s.l, cur[i], s.l, bufs[i].G, s.l};
-            gsp.structure = kUpperC;  // chol_inv reads only the upper triangle of G
-            gram.push_back(gsp);
-            chol.push_back({bufs[i].G, s.l, pass < shifted ? 10.0 * (s.m + s.l) : 0.0, bufs[i].T,
-                            pass == last ? s.ndead : nullptr});
-        }
-        c->gemm_tag = 3;
-        gemm_many(c, kOpC, gram);
-        chol_inv_many(c, chol);
-        for (size_t i = 0; i < specs.size(); ++i) {
-            const OrthSpec& s = specs[i];
-            cplx* dst = pass == last ? s.Q : (pass == 0 ? bufs[i].a : bufs[i].b);
-            GemmSpec asp{s.m, s.l, s.l, cur[i], s.l, bufs[i].T, s.l, dst, s.l};
-            asp.structure = kTriB;  // T = R^-1 is upper triangular
-            apply.push_back(asp);
-            cur[i] = dst;
-        }
-        c->gemm_tag = 4;
-        gemm_many(c, kOpN, apply);
-    }
+    if (passes != kFullPasses && passes != kSpanPasses) throw_contract(c, "orth: unknown pass schedule");
+    orth_many_adaptive(c, specs, passes == kFullPasses);
 }
 
 void orth(rrsvd_b200_ctx* c, const cplx* Y, int m, int l, cplx* Q, int* ndead) {

@@ -75,6 +75,8 @@ struct CholSpec {
     double shift_scale;
     cplx* T;
     int* ndead;
+    int* ill_out = nullptr;     // nullable: set to 1 if a pivot falls within kIllRatio of the shift
+    const int* pred = nullptr;  // nullable: the whole factorization runs only if *pred != 0
 };
 void chol_inv_many(rrsvd_b200_ctx* c, const std::vector<CholSpec>& specs);
 

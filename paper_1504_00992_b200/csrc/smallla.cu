@@ -260,7 +260,7 @@ __global__ void __launch_bounds__(CHOL_THREADS) chol_inv_kernel(const __grid_con
             T[(long long)i * ldt + k] = v;
             if (Tn != nullptr) Tn[(long long)i * ldt + k] = mk(-v.x, -v.y);
         }
-    if (b.ill_out[p] != nullptr && tid == 0) *b.ill_out[p] = s_ill;
+    if (b.ill_out[p] != nullptr && tid == 0 && s_ill) *b.ill_out[p] = 1;  // (zeroed by the caller)
     if (b.ndead[p] != nullptr && tid == 0) {
         int n = 0;
         for (int j = 0; j < l; ++j) n += dead[j];

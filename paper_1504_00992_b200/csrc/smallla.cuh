@@ -35,8 +35,9 @@ struct CholBatch {
     int ndead_acc[kMaxSmall];         // 1: add to *ndead instead of storing
     double* shift_save[kMaxSmall];    // nullable: store the shift used (for later blocks)
     const double* shift_use[kMaxSmall];  // nullable: use this stored shift instead
-    int* ill_out[kMaxSmall];          // nullable: 1 if some pivot is < kIllRatio x the shift (or
-                                      //   dependent), i.e. cond(Y) is beyond one shifted pass
+    int* ill_out[kMaxSmall];          // nullable: set to 1 if some pivot is < kIllRatio x the shift
+                                      //   (or dependent): cond(Y) beyond one shifted pass; the
+                                      //   caller zeroes it (diagonal blocks of one matrix OR in)
     const int* pred[kMaxSmall];       // nullable: run only if *pred != 0 (else exit at once)
 };
 constexpr double kIllRatio = 1e4;
