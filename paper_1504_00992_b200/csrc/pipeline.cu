@@ -397,27 +397,36 @@ void block_jacobi_group(rrsvd_b200_ctx* c, const std::vector<const SmallSvdSpec*
         for (int pos = 0; pos < nbp; ++pos) dst[t][pos] = where[plt[pos]];
     }
     auto* hrot = static_cast<int*>(pinned_scratch(c, np * sizeof(int)));
+    // problems drop out of the launches once a sweep of theirs rotates nothing (the batch would
+    // otherwise run every problem for the slowest one's sweeps); each keeps its own buffers
+    std::vector<int> active(np);
+    for (int p = 0; p < np; ++p) active[p] = p;
     int sweep = 0;
     for (; sweep < 60; ++sweep) {
         check_cuda(c, cudaMemsetAsync(rot, 0, np * sizeof(int), c->stream), "memset");
         for (int t = 0; t < nbp - 1; ++t) {
             BjStep st{};
-            st.count = np; st.r = r; st.cp = cp; st.b = b; st.npairs = npairs;
+            st.count = (int)active.size(); st.r = r; st.cp = cp; st.b = b; st.npairs = npairs;
             st.inner_sweeps = bj_inner_sweeps();
-            for (int p = 0; p < np; ++p) {
-                st.Xs[p] = X1[p]; st.Xd[p] = X2[p]; st.Vs[p] = V1[p]; st.Vd[p] = V2[p]; st.rot[p] = rot + p;
+            for (size_t q = 0; q < active.size(); ++q) {
+                const int p = active[q];
+                st.Xs[q] = X1[p]; st.Xd[q] = X2[p]; st.Vs[q] = V1[p]; st.Vd[q] = V2[p]; st.rot[q] = rot + p;
             }
             std::copy(dst[t].begin(), dst[t].end(), st.dst);
             check_cuda(c, bj_step(st, c->stream), "bj_step");
             c->launches++;
-            std::swap(X1, X2);
-            std::swap(V1, V2);
+            for (int p : active) {
+                std::swap(X1[p], X2[p]);
+                std::swap(V1[p], V2[p]);
+            }
         }
         check_cuda(c, cudaMemcpyAsync(hrot, rot, np * sizeof(int), cudaMemcpyDeviceToHost, c->stream), "D2H");
         check_cuda(c, cudaStreamSynchronize(c->stream), "sync");
-        bool any = false;
-        for (int p = 0; p < np; ++p) any = any || hrot[p] != 0;
-        if (!any) break;
+        std::vector<int> still;
+        for (int p : active)
+            if (hrot[p] != 0) still.push_back(p);
+        if (still.empty()) break;
+        active.swap(still);
     }
     if (debug_enabled())
         std::fprintf(stderr, "[rrsvd_b200] block jacobi %dx%d x%d: %d sweeps\n", r, cc, np, sweep + 1);
