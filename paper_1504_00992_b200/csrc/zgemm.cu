@@ -36,9 +36,6 @@ using Cfg64 = Cfg<64, 64, 32, 32>;
 // than the ~1-2k cycle load latency, so the third stage buys nothing while the third CTA fills
 // the DMMA issue bubbles of the other two.
 using Cfg56 = Cfg<64, 56, 16, 56, 2, 3>;
-// Cfg80: 80x64 CTA tile (5 warps of 16x64), 2-stage ring, 2 CTAs/SM — M = d1·d2 = 400 divides
-// exactly; with the column-blocked gate (N = χ_l·χ_r) the N padding is < 1%.
-using Cfg80 = Cfg<80, 64, 16, 64, 2, 2>;
 
 __device__ __forceinline__ int find_problem(const GemmGroup& g, int tile) {
     int lo = 0, hi = g.count - 1;
@@ -311,7 +308,7 @@ cudaError_t launch_cfg(GemmGroup& g, GemmOp opA, cudaStream_t s) {
 cudaError_t zgemm_grouped(GemmGroup& g, GemmOp opA, cudaStream_t s) {
     // Pick the CTA tile that wastes the least padded DMMA work (M and N quantisation) for this
     // group; ties favour the larger warp tile of Cfg64.
-    double pad64 = 0.0, pad56 = 0.0, pad80 = 0.0;
+    double pad64 = 0.0, pad56 = 0.0;
     for (int i = 0; i < g.count; ++i) {
         GemmProblem& P = g.p[i];
         if (P.batch < 1) P.batch = 1;
@@ -323,9 +320,7 @@ cudaError_t zgemm_grouped(GemmGroup& g, GemmOp opA, cudaStream_t s) {
         const double w = (double)P.k * P.batch;
         pad64 += w * ((P.m + 63) / 64 * 64) * ((P.n + 63) / 64 * 64);
         pad56 += w * ((P.m + 63) / 64 * 64) * ((P.n + 55) / 56 * 56);
-        pad80 += w * ((P.m + 79) / 80 * 80) * ((P.n + 63) / 64 * 64);
     }
-    (void)pad80;  // Cfg80 kept compiled for experiments; padded sub-tiles are skipped instead
     if (pad56 < 0.95 * pad64) return launch_cfg<Cfg56>(g, opA, s);
     return launch_cfg<Cfg64>(g, opA, s);
 }
