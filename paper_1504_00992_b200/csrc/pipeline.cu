@@ -765,6 +765,7 @@ void svd_jacobi_many(rrsvd_b200_ctx* c, const std::vector<SvdSpec>& specs) {
         bool tall;
         cplx *Qr, *R, *K;
         const SvdSpec* s;
+        int* perm;
     };
     std::vector<Pre> pres;
     for (const SvdSpec& s : specs) {
@@ -778,10 +779,29 @@ void svd_jacobi_many(rrsvd_b200_ctx* c, const std::vector<SvdSpec>& specs) {
             X = Xt;
         }
         pres.push_back({X, r, cc, tall, ws_get<cplx>(c, (size_t)r * cc), ws_get<cplx>(c, (size_t)cc * cc),
-                        ws_get<cplx>(c, (size_t)cc * cc), &s});
+                        ws_get<cplx>(c, (size_t)cc * cc), &s, nullptr});
     }
-    // QR-preconditioned Jacobi: X (r x cc) = A or A^H, X = Qr R, R^H K = Z S
-    //   =>  X = (Qr K) S Z^H : left vectors Qr K, right vectors Z.
+    // Static column pivoting: X's columns sorted by decreasing norm (Xp = X Pi) before the QR
+    // gives R a decreasing diagonal, and the one-sided Jacobi on R^H then converges in fewer
+    // sweeps (graded columns are the TEBD norm: column norms scale with lambda_r).
+    std::vector<cplx*> Vp(pres.size());
+    for (size_t base = 0; base < pres.size(); base += kMaxSmall) {
+        ColPermBatch cp{};
+        int max_c = 0;
+        for (size_t i = base; i < std::min(pres.size(), base + kMaxSmall); ++i) {
+            Pre& p = pres[i];
+            const int k = cp.count++;
+            cplx* Xp = ws_get<cplx>(c, (size_t)p.r * p.cc);
+            cp.X[k] = p.X; cp.Xp[k] = Xp; cp.r[k] = p.r; cp.c[k] = p.cc;
+            cp.perm[k] = p.perm = ws_get<int>(c, p.cc);
+            p.X = Xp;
+            max_c = std::max(max_c, p.cc);
+        }
+        check_cuda(c, colperm_sort_gather(cp, max_c, c->stream), "colperm");
+        c->launches += 2;
+    }
+    // QR-preconditioned Jacobi: X (r x cc) = A or A^H (columns permuted), X = Qr R, R^H K = Z S
+    //   =>  X = (Qr K) S Z^H : left vectors Qr K, right vectors Z (rows un-permuted at the end).
     std::vector<OrthSpec> os;
     std::vector<GemmSpec> gs;
     for (const Pre& p : pres) os.push_back({p.X, p.r, p.cc, p.Qr});
@@ -789,9 +809,22 @@ void svd_jacobi_many(rrsvd_b200_ctx* c, const std::vector<SvdSpec>& specs) {
     for (const Pre& p : pres) gs.push_back({p.cc, p.cc, p.r, p.Qr, p.cc, p.X, p.cc, p.R, p.cc});
     c->gemm_tag = 6;
     gemm_many(c, kOpC, gs);
-    for (const Pre& p : pres)
-        pre.push_back({p.R, p.cc, p.cc, 1, p.cc, p.s->sigma, p.tall ? p.s->V : p.s->U, p.K});
+    for (size_t i = 0; i < pres.size(); ++i) {
+        const Pre& p = pres[i];
+        Vp[i] = ws_get<cplx>(c, (size_t)p.cc * p.cc);
+        pre.push_back({p.R, p.cc, p.cc, 1, p.cc, p.s->sigma, Vp[i], p.K});
+    }
     small_svd_many(c, pre);
+    for (size_t base = 0; base < pres.size(); base += kMaxSmall) {
+        ColPermBatch cp{};
+        for (size_t i = base; i < std::min(pres.size(), base + kMaxSmall); ++i) {
+            const Pre& p = pres[i];
+            const int k = cp.count++;
+            cp.c[k] = p.cc; cp.perm[k] = p.perm; cp.Vp[k] = Vp[i]; cp.V[k] = p.tall ? p.s->V : p.s->U;
+        }
+        check_cuda(c, colperm_scatter_rows(cp, c->stream), "colperm scatter");
+        c->launches++;
+    }
     gs.clear();
     for (const Pre& p : pres) gs.push_back({p.r, p.cc, p.cc, p.Qr, p.cc, p.K, p.cc, p.tall ? p.s->U : p.s->V, p.cc});
     c->gemm_tag = 6;

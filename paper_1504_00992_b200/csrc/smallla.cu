@@ -417,6 +417,44 @@ __global__ void __launch_bounds__(JAC_CL_THREADS) jacobi_kernel(const __grid_con
     if (rank == 0 && tid == 0 && b.sweeps[p] != nullptr) *b.sweeps[p] = sweep + 1;
 }
 
+__global__ void __launch_bounds__(256) colperm_rank_kernel(const __grid_constant__ ColPermBatch b) {
+    extern __shared__ __align__(16) unsigned char sm[];
+    const int p = blockIdx.x, r = b.r[p], c = b.c[p];
+    double* nrm = reinterpret_cast<double*>(sm);
+    const cplx* X = b.X[p];
+    for (int j = threadIdx.x; j < c; j += 256) {
+        double a = 0.0;
+        for (int i = 0; i < r; ++i) a += cabs2(X[(long long)i * c + j]);
+        nrm[j] = a;
+    }
+    __syncthreads();
+    for (int j = threadIdx.x; j < c; j += 256) {
+        const double v = nrm[j];
+        int rk = 0;
+        for (int t = 0; t < c; ++t) rk += (nrm[t] > v) || (nrm[t] == v && t < j);
+        b.perm[p][rk] = j;
+    }
+}
+
+__global__ void __launch_bounds__(256) colperm_gather_kernel(const __grid_constant__ ColPermBatch b) {
+    const int p = blockIdx.y, c = b.c[p];
+    const long long n = (long long)b.r[p] * c;
+    for (long long e = blockIdx.x * 256LL + threadIdx.x; e < n; e += (long long)gridDim.x * 256) {
+        const long long i = e / c;
+        const int k = (int)(e % c);
+        b.Xp[p][e] = b.X[p][i * c + b.perm[p][k]];
+    }
+}
+
+__global__ void __launch_bounds__(256) colperm_scatter_kernel(const __grid_constant__ ColPermBatch b) {
+    const int p = blockIdx.y, c = b.c[p];
+    const long long n = (long long)c * c;
+    for (long long e = blockIdx.x * 256LL + threadIdx.x; e < n; e += (long long)gridDim.x * 256) {
+        const int k = (int)(e / c), j = (int)(e % c);
+        b.V[p][(long long)b.perm[p][k] * c + j] = b.Vp[p][e];
+    }
+}
+
 __global__ void __launch_bounds__(256) select_kernel(const __grid_constant__ SelectBatch b) {
     const int p = blockIdx.y;
     const cplx* src = *b.flag[p] ? b.B[p] : b.A[p];
@@ -591,6 +629,22 @@ cudaError_t chol_inv(const CholBatch& b, int max_l, cudaStream_t s) {
     cudaError_t e = cudaFuncSetAttribute(chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     chol_inv_kernel<<<b.count, CHOL_THREADS, smem, s>>>(b);
+    return cudaGetLastError();
+}
+
+cudaError_t colperm_sort_gather(const ColPermBatch& b, int max_c, cudaStream_t s) {
+    if (b.count == 0) return cudaSuccess;
+    const size_t smem = (size_t)max_c * sizeof(double);
+    cudaError_t e = cudaFuncSetAttribute(colperm_rank_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    colperm_rank_kernel<<<b.count, 256, smem, s>>>(b);
+    colperm_gather_kernel<<<dim3(2 * kNumSMs, b.count), 256, 0, s>>>(b);
+    return cudaGetLastError();
+}
+
+cudaError_t colperm_scatter_rows(const ColPermBatch& b, cudaStream_t s) {
+    if (b.count == 0) return cudaSuccess;
+    colperm_scatter_kernel<<<dim3(kNumSMs, b.count), 256, 0, s>>>(b);
     return cudaGetLastError();
 }
 

@@ -56,6 +56,21 @@ cudaError_t select_many(const SelectBatch& b, cudaStream_t s);
 cudaError_t chol_inv(const CholBatch& b, int max_l, cudaStream_t s);
 bool jacobi_fits(int r, int c);  // an r x c problem fits jacobi_svd's on-chip capacity
 
+// ---- static column pivoting for the QR-preconditioned Jacobi: order the columns of each
+// row-major r x c matrix X by decreasing norm (ties by index), Xp[:, k] = X[:, perm[k]]; after
+// the SVD of Xp the right vectors' rows go back: V[perm[k], :] = Vp[k, :].
+struct ColPermBatch {
+    int count;
+    const cplx* X[kMaxSmall];
+    cplx* Xp[kMaxSmall];
+    int r[kMaxSmall], c[kMaxSmall];
+    int* perm[kMaxSmall];
+    const cplx* Vp[kMaxSmall];  // for the row scatter
+    cplx* V[kMaxSmall];
+};
+cudaError_t colperm_sort_gather(const ColPermBatch& b, int max_c, cudaStream_t s);
+cudaError_t colperm_scatter_rows(const ColPermBatch& b, cudaStream_t s);
+
 // ---- max_j ||D[:, j]|| of row-major m x r matrices (the accuracy check's probe residuals,
 // randomized.cpp:47-53,149-150); one CTA per matrix, fixed reduction order.
 struct ColNormBatch {
