@@ -11,7 +11,10 @@ namespace rb {
 namespace {
 
 bool debug_enabled() {
-    static const bool d = std::getenv("RRSVD_B200_DEBUG") != nullptr;
+    static const bool d = [] {
+        const char* e = std::getenv("RRSVD_B200_DEBUG");
+        return e != nullptr && e[0] != '\0' && e[0] != '0';
+    }();
     return d;
 }
 
@@ -488,7 +491,7 @@ void small_svd_many(rrsvd_b200_ctx* c, const std::vector<SmallSvdSpec>& specs) {
         c->launches += 3;
     }
     if (debug_enabled()) {
-        for (size_t i = 0; i < specs.size(); ++i) {
+        for (size_t i : onchip) {  // (the block path prints its own sweep counts)
             int h = -1;
             cudaMemcpyAsync(&h, dsweeps[i], sizeof(int), cudaMemcpyDeviceToHost, c->stream);
             cudaStreamSynchronize(c->stream);
