@@ -306,10 +306,11 @@ cudaError_t bj_step(const BjStep& a, cudaStream_t s) {
     constexpr size_t smem = sizeof(cplx) * (kBjRows * (kBjN2 + 1) + 2 * kBjN2 * (kBjN2 + 1));
     cudaError_t e = cudaFuncSetAttribute(bj_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    // row slices per pair: enough CTAs to cover the GPU ~2x, at most 8 (portable cluster)
+    // row slices per pair: as many as keep every CTA resident in one wave (3 per SM at this
+    // shared-memory size), at most 8 (portable cluster), at least one 64-row chunk per slice
     const long long pairs = (long long)a.npairs * a.count;
     int S = 1;
-    while (S < 8 && pairs * S * 2 <= 2LL * 148 && (a.r / (2 * S)) >= kBjRows) S *= 2;
+    while (S < 8 && pairs * (2 * S) <= 3LL * 148 && (a.r / (2 * S)) >= kBjRows) S *= 2;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(a.npairs * S, a.count);
     cfg.blockDim = dim3(kBjThreads);
