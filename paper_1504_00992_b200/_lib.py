@@ -13,7 +13,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "librrsvd_b200.so")
+# (RRSVD_B200_LIB: an alternative in-tree build, for A/B timing of kernel variants)
+LIB_PATH = os.environ.get("RRSVD_B200_LIB") or os.path.join(_HERE, "lib", "librrsvd_b200.so")
 HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "rrsvd_b200.h")
 
 OK, CONTRACT_VIOLATION, NUMERIC_FAILURE, CUDA_ERROR = 0, 1, 2, 3

@@ -48,16 +48,17 @@ constexpr int kBjN2 = 32;    // 2b (b = 16)
 // back over DSMEM and rotate their own slices of X and V.
 __global__ void __launch_bounds__(kBjThreads) bj_step_kernel(const __grid_constant__ BjStep a) {
     constexpr int n2 = kBjN2, ld = n2 + 1, half = n2 / 2;
+    __shared__ double pc[half], ps[half];
+    __shared__ cplx pe[half];
+    static_assert(kBjThreads == (n2 / 2) * (n2 / 2), "one thread per 2x2 block of the pair Gram");
     cg::cluster_group cluster = cg::this_cluster();
     const int S = (int)cluster.num_blocks(), crank = (int)cluster.block_rank();
     extern __shared__ __align__(16) unsigned char sm[];
     auto ch = reinterpret_cast<cplx(*)[ld]>(sm);                        // [kBjRows][ld]
     auto sG = reinterpret_cast<cplx(*)[ld]>(sm + sizeof(cplx) * kBjRows * ld);  // [n2][ld]
     auto sW = sG + n2;                                                    // [n2][ld]
-    __shared__ double pc[half], ps[half];
-    __shared__ cplx pe[half];
-    __shared__ int pp[half], pq[half];
     __shared__ int s_rot;
+    __shared__ unsigned long long s_off2, s_off2_first;
     const int pr = blockIdx.y, k0 = blockIdx.x / S, tid = threadIdx.x;
     const int r = a.r, cp = a.cp, b = a.b;
     const int xr0 = (int)((long long)r * crank / S), xr1 = (int)((long long)r * (crank + 1) / S);
@@ -66,10 +67,16 @@ __global__ void __launch_bounds__(kBjThreads) bj_step_kernel(const __grid_consta
     const cplx* X = a.Xs[pr];
 
     // ---- Gram of this CTA's row slice on the FP64 tensor core: the 32 x 32 result is 4 x 4 tiles
-    // of 8 x 8; warp w accumulates tiles (pt = w/2, qt = 2(w%2) + {0,1}).  Fragments are one
-    // LDS.128 (re, im) per lane; conj(X)^T X in 4M form: Re += xr xr' + xi xi', Im += xr xi' - xi xr'.
+    // of 8 x 8, of which the 10 upper-triangular ones are formed (the solve mirrors them); warps
+    // 0..4 accumulate two tiles each.  Fragments are one LDS.128 (re, im) per lane; conj(X)^T X in
+    // 4M form: Re += xr xr' + xi xi', Im += xr xi' - xi xr'.
     const int lane = tid & 31, warp = tid >> 5;
-    const int pt = warp >> 1, qa = 2 * (warp & 1);
+    // upper tiles t = 0..9 as 4-bit (p | q << 2) fields: (0,0) (0,1) (0,2) (0,3) (1,1) (1,2) (1,3) (2,2) (2,3) (3,3)
+    constexpr unsigned long long kTiles = 0xfead95c840ull;
+    const bool gwarp = warp < 5;
+    const int ta = gwarp ? 2 * warp : 0;
+    const int fa = (int)(kTiles >> (4 * ta)) & 15, fb = (int)(kTiles >> (4 * ta + 4)) & 15;
+    const int pa = fa & 3, qa_ = fa >> 2, pb = fb & 3, qb = fb >> 2;
     double gre[2][2] = {{0.0, 0.0}, {0.0, 0.0}}, gim[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
     for (int r0 = xr0; r0 < xr1; r0 += kBjRows) {
         const int nr = min(kBjRows, xr1 - r0), nr4 = (nr + 3) & ~3;
@@ -79,23 +86,30 @@ __global__ void __launch_bounds__(kBjThreads) bj_step_kernel(const __grid_consta
             ch[i][j] = i < nr ? X[(long long)(r0 + i) * cp + col0 + j] : mk(0.0, 0.0);
         }
         __syncthreads();
-        for (int k0 = 0; k0 < nr4; k0 += 4) {
-            const cplx xa = ch[k0 + (lane & 3)][pt * 8 + (lane >> 2)];
-#pragma unroll
-            for (int qq = 0; qq < 2; ++qq) {
-                const cplx xb = ch[k0 + (lane & 3)][(qa + qq) * 8 + (lane >> 2)];
-                dmma884(gre[qq][0], gre[qq][1], xa.x, xb.x);
-                dmma884(gre[qq][0], gre[qq][1], xa.y, xb.y);
-                dmma884(gim[qq][0], gim[qq][1], xa.x, xb.y);
-                dmma884(gim[qq][0], gim[qq][1], -xa.y, xb.x);
+        if (gwarp) {
+            for (int k0 = 0; k0 < nr4; k0 += 4) {
+                const cplx* row = ch[k0 + (lane & 3)];
+                const int cl = lane >> 2;
+                const cplx x0 = row[pa * 8 + cl], y0 = row[qa_ * 8 + cl];
+                const cplx x1 = row[pb * 8 + cl], y1 = row[qb * 8 + cl];
+                dmma884(gre[0][0], gre[0][1], x0.x, y0.x);
+                dmma884(gre[1][0], gre[1][1], x1.x, y1.x);
+                dmma884(gim[0][0], gim[0][1], x0.x, y0.y);
+                dmma884(gim[1][0], gim[1][1], x1.x, y1.y);
+                dmma884(gre[0][0], gre[0][1], x0.y, y0.y);
+                dmma884(gre[1][0], gre[1][1], x1.y, y1.y);
+                dmma884(gim[0][0], gim[0][1], -x0.y, y0.x);
+                dmma884(gim[1][0], gim[1][1], -x1.y, y1.x);
             }
         }
     }
+    if (gwarp) {
 #pragma unroll
-    for (int qq = 0; qq < 2; ++qq)
-#pragma unroll
-        for (int c = 0; c < 2; ++c)
-            sG[pt * 8 + (lane >> 2)][(qa + qq) * 8 + 2 * (lane & 3) + c] = mk(gre[qq][c], gim[qq][c]);
+        for (int c = 0; c < 2; ++c) {
+            sG[pa * 8 + (lane >> 2)][qa_ * 8 + 2 * (lane & 3) + c] = mk(gre[0][c], gim[0][c]);
+            sG[pb * 8 + (lane >> 2)][qb * 8 + 2 * (lane & 3) + c] = mk(gre[1][c], gim[1][c]);
+        }
+    }
     cluster.sync();
     if (crank == 0) {  // (uniform per CTA; barriers below are reached by every thread)
         // sum the slices in rank order, then keep the upper triangle and mirror it
@@ -104,6 +118,7 @@ __global__ void __launch_bounds__(kBjThreads) bj_step_kernel(const __grid_consta
         for (int u = 0; u < n2 * n2 / kBjThreads; ++u) {
             const int e = tid + u * kBjThreads;
             sum[u] = mk(0.0, 0.0);
+            if ((e >> 3) % (n2 / 8) < (e / n2) >> 3) continue;  // strictly-lower 8x8 tile: not formed
             for (int q = 0; q < S; ++q) {
                 const cplx(*pg)[ld] = cluster.map_shared_rank(sG, q);
                 sum[u] = cadd(sum[u], pg[e / n2][e % n2]);
@@ -122,19 +137,29 @@ __global__ void __launch_bounds__(kBjThreads) bj_step_kernel(const __grid_consta
             else if (p == q) sG[p][q].y = 0.0;
         }
         for (int e = tid; e < n2 * n2; e += kBjThreads) sW[e / n2][e % n2] = mk(e / n2 == e % n2 ? 1.0 : 0.0, 0.0);
-        if (tid == 0) s_rot = 0;
+        if (tid == 0) { s_rot = 0; s_off2 = 0ull; }
         __syncthreads();
 
-    // ---- one sweep of the pair solve
+    // ---- one sweep of the pair solve.  Round rd rotates the n2/2 disjoint pairs of the circle
+    // method; thread (ka, kb) owns the 2 x 2 block of G at pair ka's rows x pair kb's columns and
+    // forms it as J_ka^H (G J_kb) (the column rotation first, then the row rotation — the same
+    // operations, in the same order, as rotating all columns and then all rows), reading G from
+    // one buffer and writing the other: a round is two barriers (parameters, update) instead of
+    // three.  The thread also rotates rows 2ka, 2ka+1 of W in pair kb's columns.
     const double tol = sqrt((double)max(r, 1)) * kEpsBj;
     __shared__ int s_first;  // rotations of the first inner sweep: the outer convergence signal
+    cplx(*Gi)[ld] = sG;
+    cplx(*Go)[ld] = ch;  // (the chunk buffer is idle during the solve)
+    const int ka = tid >> 4, kb = tid & 15;
     for (int isw = 0; isw < a.inner_sweeps; ++isw) {
     const int rot_before = s_rot;
     for (int rd = 0; rd < n2 - 1; ++rd) {
-        if (tid < half) {
-            const int p = circle_bj(tid, rd, n2), q = circle_bj(n2 - 1 - tid, rd, n2);
-            const double ga = sG[p][p].x, gb = sG[q][q].x;
-            const cplx g = sG[p][q];
+        const int p = circle_bj(ka, rd, n2), q = circle_bj(n2 - 1 - ka, rd, n2);
+        const int p2 = circle_bj(kb, rd, n2), q2 = circle_bj(n2 - 1 - kb, rd, n2);
+        if (tid < half) {  // parameters of pair tid (= ka at threads (ka, ka))
+            const int pp = circle_bj(tid, rd, n2), qq = circle_bj(n2 - 1 - tid, rd, n2);
+            const double ga = Gi[pp][pp].x, gb = Gi[qq][qq].x;
+            const cplx g = Gi[pp][qq];
             const double g2 = g.x * g.x + g.y * g.y;
             double c = 1.0, s = 0.0;
             cplx e = mk(1.0, 0.0);
@@ -148,45 +173,54 @@ __global__ void __launch_bounds__(kBjThreads) bj_step_kernel(const __grid_consta
                 c = rsqrt(fma(tt, tt, 1.0));
                 s = c * tt;
                 atomicAdd(&s_rot, 1);
+                atomicMax(&s_off2, (unsigned long long)__double_as_longlong(g2 / (ga * gb)));
             }
-            pc[tid] = c; ps[tid] = s; pe[tid] = e; pp[tid] = p; pq[tid] = q;
+            pc[tid] = c; ps[tid] = s; pe[tid] = e;
         }
         __syncthreads();
-        for (int idx = tid; idx < half * n2; idx += kBjThreads) {  // columns: G J, W J
-            const int k = idx / n2, i = idx % n2;
-            const double s = ps[k];
-            if (s == 0.0) continue;
-            const double c = pc[k];
-            const cplx e = pe[k];
-            const int p = pp[k], q = pq[k];
-            const cplx u = sG[i][p], ev = cmul(e, sG[i][q]);
-            sG[i][p] = mk(c * u.x - s * ev.x, c * u.y - s * ev.y);
-            sG[i][q] = mk(s * u.x + c * ev.x, s * u.y + c * ev.y);
-            const cplx w = sW[i][p], wv = cmul(e, sW[i][q]);
-            sW[i][p] = mk(c * w.x - s * wv.x, c * w.y - s * wv.y);
-            sW[i][q] = mk(s * w.x + c * wv.x, s * w.y + c * wv.y);
+        const double ca = pc[ka], sa = ps[ka], cb = pc[kb], sb = ps[kb];
+        const cplx ea = pe[ka], eb = pe[kb];
+        cplx g_pp = Gi[p][p2], g_pq = Gi[p][q2], g_qp = Gi[q][p2], g_qq = Gi[q][q2];
+        if (sb != 0.0) {  // columns p2, q2: G J
+            const cplx v0 = cmul(eb, g_pq), v1 = cmul(eb, g_qq);
+            const cplx u0 = g_pp, u1 = g_qp;
+            g_pp = mk(cb * u0.x - sb * v0.x, cb * u0.y - sb * v0.y);
+            g_pq = mk(sb * u0.x + cb * v0.x, sb * u0.y + cb * v0.y);
+            g_qp = mk(cb * u1.x - sb * v1.x, cb * u1.y - sb * v1.y);
+            g_qq = mk(sb * u1.x + cb * v1.x, sb * u1.y + cb * v1.y);
+        }
+        if (sa != 0.0) {  // rows p, q: J^H (G J)
+            const cplx ec = cconj(ea);
+            const cplx v0 = cmul(ec, g_qp), v1 = cmul(ec, g_qq);
+            const cplx u0 = g_pp, u1 = g_pq;
+            g_pp = mk(ca * u0.x - sa * v0.x, ca * u0.y - sa * v0.y);
+            g_qp = mk(sa * u0.x + ca * v0.x, sa * u0.y + ca * v0.y);
+            g_pq = mk(ca * u1.x - sa * v1.x, ca * u1.y - sa * v1.y);
+            g_qq = mk(sa * u1.x + ca * v1.x, sa * u1.y + ca * v1.y);
+        }
+        Go[p][p2] = g_pp; Go[p][q2] = g_pq; Go[q][p2] = g_qp; Go[q][q2] = g_qq;
+        if (sb != 0.0) {  // W J on rows 2ka, 2ka+1
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int i = 2 * ka + h;
+                const cplx w = sW[i][p2], wv = cmul(eb, sW[i][q2]);
+                sW[i][p2] = mk(cb * w.x - sb * wv.x, cb * w.y - sb * wv.y);
+                sW[i][q2] = mk(sb * w.x + cb * wv.x, sb * w.y + cb * wv.y);
+            }
         }
         __syncthreads();
-        for (int idx = tid; idx < half * n2; idx += kBjThreads) {  // rows: J^H G
-            const int k = idx / n2, j = idx % n2;
-            const double s = ps[k];
-            if (s == 0.0) continue;
-            const double c = pc[k];
-            const cplx ec = cconj(pe[k]);
-            const int p = pp[k], q = pq[k];
-            const cplx u = sG[p][j], ev = cmul(ec, sG[q][j]);
-            sG[p][j] = mk(c * u.x - s * ev.x, c * u.y - s * ev.y);
-            sG[q][j] = mk(s * u.x + c * ev.x, s * u.y + c * ev.y);
-        }
-        __syncthreads();
+        cplx(*t)[ld] = Gi; Gi = Go; Go = t;
     }
-    if (isw == 0 && tid == 0) s_first = s_rot;
+    if (isw == 0 && tid == 0) { s_first = s_rot; s_off2_first = s_off2; }
     const bool more = s_rot != rot_before;
     __syncthreads();  // (all threads read s_rot before the next sweep changes it)
     if (!more) break;
     }
 
-        if (tid == 0 && s_first) atomicAdd(a.rot[pr], s_first);
+        if (tid == 0 && s_first) {
+            atomicAdd(&a.stat[pr]->rot, s_first);
+            atomicMax(&a.stat[pr]->off2, s_off2_first);
+        }
     }
     cluster.sync();  // W is ready in CTA 0
     if (crank != 0) {

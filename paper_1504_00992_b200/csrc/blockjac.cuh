@@ -35,6 +35,13 @@ cudaError_t bj_init(const BjInit& a, cudaStream_t s);
 // One tournament step for every block pair of every problem, fused (one CTA per pair): the
 // pair's Gram from row chunks staged in shared memory, one sweep of the pair solve, then
 // [X_i X_j] W and [V_i V_j] W written straight to the blocks' positions of the next step.
+// per-problem sweep statistics (zeroed by the host before each sweep)
+struct BjStat {
+    int rot;                  // rotations applied
+    int pad;
+    unsigned long long off2;  // max over rotated pairs of |g_pq|^2 / (g_pp g_qq), as ordered bits
+};
+
 struct BjStep {
     int count, r, cp, b, npairs;
     int inner_sweeps;  // sweeps of the pair solve per step (stops early once a sweep rotates nothing)
@@ -42,7 +49,7 @@ struct BjStep {
     cplx* Xd[kBjMaxProblems];
     const cplx* Vs[kBjMaxProblems];
     cplx* Vd[kBjMaxProblems];
-    int* rot[kBjMaxProblems];  // per-problem rotation counters (added to)
+    BjStat* stat[kBjMaxProblems];  // per-problem sweep statistics (added to / maxed into)
     int dst[kBjMaxSlots];      // block position now -> block position at the next step
 };
 cudaError_t bj_step(const BjStep& a, cudaStream_t s);

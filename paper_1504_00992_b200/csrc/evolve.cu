@@ -373,7 +373,11 @@ void evolve_core(rrsvd_b200_mps* s, rrsvd_b200_ctx* c, size_t n_sweeps, const rr
                     return e ? std::atoi(e) : 0;
                 }();
                 const int want = env_lanes > 0 ? env_lanes : c->n_lanes;
-                const int nl = c->use_lanes ? std::max(1, std::min<int>({want, (int)nbnd, rrsvd_b200_ctx::kMaxLanes})) : 1;
+                bool syncs = false;  // lanes are submitted in turn: a host-synchronising batch serialises them
+                for (size_t i = 0; i < nbnd; ++i) syncs = syncs || decimation_syncs_host(plans[i]);
+                const int nl = c->use_lanes && !syncs
+                                   ? std::max(1, std::min<int>({want, (int)nbnd, rrsvd_b200_ctx::kMaxLanes}))
+                                   : 1;
                 if (nl > 1) lanes_fork(c, nl);
                 for (int lane = 0; lane < nl; ++lane) {
                     if (nl > 1) c->stream = c->lane[lane];

@@ -1,4 +1,5 @@
 // pipeline.cu — batched orchestration of the decimation pipeline.  See pipeline.cuh.
+#include <cstring>
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
@@ -371,7 +372,7 @@ void block_jacobi_group(rrsvd_b200_ctx* c, const std::vector<const SmallSvdSpec*
         }
     };
     std::vector<cplx*> X1(np), X2(np), V1(np), V2(np);
-    int* rot = ws_get<int>(c, np);
+    BjStat* stat = ws_get<BjStat>(c, np);
     for (int p = 0; p < np; ++p) {
         X1[p] = ws_get<cplx>(c, (size_t)r * cp);
         X2[p] = ws_get<cplx>(c, (size_t)r * cp);
@@ -399,21 +400,24 @@ void block_jacobi_group(rrsvd_b200_ctx* c, const std::vector<const SmallSvdSpec*
         for (int pos = 0; pos < nbp; ++pos) where[pln[pos]] = pos;
         for (int pos = 0; pos < nbp; ++pos) dst[t][pos] = where[plt[pos]];
     }
-    auto* hrot = static_cast<int*>(pinned_scratch(c, np * sizeof(int)));
+    auto* hstat = static_cast<BjStat*>(pinned_scratch(c, np * sizeof(BjStat)));
     // problems drop out of the launches once a sweep of theirs rotates nothing (the batch would
     // otherwise run every problem for the slowest one's sweeps); each keeps its own buffers
     std::vector<int> active(np);
     for (int p = 0; p < np; ++p) active[p] = p;
+    // the kernel's rotation threshold tol = sqrt(r) eps; noise level sqrt(c) tol (squared)
+    const double tol_r = std::sqrt((double)std::max(r, 1)) * 2.220446049250313e-16;
+    const double noise2 = (double)cc * tol_r * tol_r;
     int sweep = 0;
     for (; sweep < 60; ++sweep) {
-        check_cuda(c, cudaMemsetAsync(rot, 0, np * sizeof(int), c->stream), "memset");
+        check_cuda(c, cudaMemsetAsync(stat, 0, np * sizeof(BjStat), c->stream), "memset");
         for (int t = 0; t < nbp - 1; ++t) {
             BjStep st{};
             st.count = (int)active.size(); st.r = r; st.cp = cp; st.b = b; st.npairs = npairs;
             st.inner_sweeps = bj_inner_sweeps();
             for (size_t q = 0; q < active.size(); ++q) {
                 const int p = active[q];
-                st.Xs[q] = X1[p]; st.Xd[q] = X2[p]; st.Vs[q] = V1[p]; st.Vd[q] = V2[p]; st.rot[q] = rot + p;
+                st.Xs[q] = X1[p]; st.Xd[q] = X2[p]; st.Vs[q] = V1[p]; st.Vd[q] = V2[p]; st.stat[q] = stat + p;
             }
             std::copy(dst[t].begin(), dst[t].end(), st.dst);
             check_cuda(c, bj_step(st, c->stream), "bj_step");
@@ -423,11 +427,22 @@ void block_jacobi_group(rrsvd_b200_ctx* c, const std::vector<const SmallSvdSpec*
                 std::swap(V1[p], V2[p]);
             }
         }
-        check_cuda(c, cudaMemcpyAsync(hrot, rot, np * sizeof(int), cudaMemcpyDeviceToHost, c->stream), "D2H");
+        check_cuda(c, cudaMemcpyAsync(hstat, stat, np * sizeof(BjStat), cudaMemcpyDeviceToHost, c->stream), "D2H");
         check_cuda(c, cudaStreamSynchronize(c->stream), "sync");
         std::vector<int> still;
-        for (int p : active)
-            if (hrot[p] != 0) still.push_back(p);
+        double worst = 0.0;
+        for (int p : active) {
+            double o2;
+            std::memcpy(&o2, &hstat[p].off2, sizeof o2);
+            worst = std::max(worst, o2);
+            // converged: no rotation, or only noise-level ones (every rotated pair had
+            // |g_pq| <= sqrt(c) tol sqrt(g_pp g_qq), LAPACK zgesvj's test): the next sweep would
+            // rotate rounding noise again without changing the result
+            if (hstat[p].rot != 0 && o2 > noise2) still.push_back(p);
+        }
+        if (debug_enabled())
+            std::fprintf(stderr, "[rrsvd_b200] block jacobi sweep %d: %zu active, %zu rotating, max |g|/sqrt(gg) %.3g\n",
+                         sweep, active.size(), still.size(), std::sqrt(worst));
         if (still.empty()) break;
         active.swap(still);
     }
@@ -839,6 +854,12 @@ void svd_jacobi(rrsvd_b200_ctx* c, const cplx* A, int m, int n, cplx* U, double*
 }
 
 // ================================================================================== TEBD trio
+
+bool decimation_syncs_host(const DecimPlan& pl) {
+    if (pl.fixed_precision) return true;
+    const int cc = pl.randomized ? pl.l : pl.minor;  // the small SVD's column count
+    return cc > block_jacobi_min_c() || !jacobi_fits(cc, cc);
+}
 
 DecimPlan plan_decimation(int d1, int d2, int cl, int cr, size_t chi_max, int kind, size_t target_rank,
                           size_t oversampling, size_t det_crossover, int accuracy_check, size_t probe_count) {

@@ -170,6 +170,11 @@ DecimPlan plan_decimation(int d1, int d2, int cl, int cr, size_t chi_max, int ki
                           size_t oversampling, size_t det_crossover, int accuracy_check = 0,
                           size_t probe_count = 0);
 
+// True when decimate_many synchronises the host for this plan (the block Jacobi's per-sweep
+// convergence read, the accuracy check's per-round certification): such batches gain nothing
+// from lanes, which are submitted one after the other from the host.
+bool decimation_syncs_host(const DecimPlan& pl);
+
 // One decimation of an unfolded M (tebd.cpp:141-237): norm, factorization (RRSVD or Jacobi),
 // truncation, λ renormalisation, Γ reshape.  Writes gamma_l (m x kept), lambda (kept),
 // gamma_r (kept x n) packed with the device-side kept; scalars into *sc (device).

@@ -58,7 +58,7 @@ class DeviceMps:
         self.chi_max = chi_max
 
     def __del__(self):
-        if getattr(self, "h", None):
+        if getattr(self, "h", None) and L is not None:  # (module globals are gone at interpreter exit)
             L.lib().rrsvd_b200_mps_destroy(self.h)
             self.h = None
 
@@ -146,7 +146,7 @@ class PreparedGates(dict):
         return int(n.value)
 
     def __del__(self):
-        for h in getattr(self, "_owned", []):
+        for h in getattr(self, "_owned", []) if L is not None else []:
             L.lib().rrsvd_b200_gate_destroy(h)
         self._owned = []
 
