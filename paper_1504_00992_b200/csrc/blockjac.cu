@@ -37,7 +37,15 @@ __global__ void __launch_bounds__(kBjThreads) bj_init_kernel(const __grid_consta
     }
 }
 
-constexpr int kBjRows = 64;  // row chunk staged per pass
+constexpr int kBjRows = 32;  // rows per staged chunk (two chunk buffers, cp.async double-buffered)
+
+__device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc, bool valid) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(sdst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(gsrc), "r"(valid ? 16 : 0));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 constexpr int kBjN2 = 32;    // 2b (b = 16)
 
 // One block pair, one CTA: Gram, one sweep of two-sided Jacobi (round-robin rounds of n2/2
@@ -54,9 +62,10 @@ __global__ void __launch_bounds__(kBjThreads) bj_step_kernel(const __grid_consta
     cg::cluster_group cluster = cg::this_cluster();
     const int S = (int)cluster.num_blocks(), crank = (int)cluster.block_rank();
     extern __shared__ __align__(16) unsigned char sm[];
-    auto ch = reinterpret_cast<cplx(*)[ld]>(sm);                        // [kBjRows][ld]
-    auto sG = reinterpret_cast<cplx(*)[ld]>(sm + sizeof(cplx) * kBjRows * ld);  // [n2][ld]
-    auto sW = sG + n2;                                                    // [n2][ld]
+    typedef cplx Chunk[kBjRows][ld];
+    Chunk* buf = reinterpret_cast<Chunk*>(sm);                                    // [2] chunks
+    auto sG = reinterpret_cast<cplx(*)[ld]>(sm + 2 * sizeof(Chunk));              // [n2][ld]
+    auto sW = sG + n2;                                                            // [n2][ld]
     __shared__ int s_rot;
     __shared__ unsigned long long s_off2, s_off2_first;
     const int pr = blockIdx.y, k0 = blockIdx.x / S, tid = threadIdx.x;
@@ -65,11 +74,23 @@ __global__ void __launch_bounds__(kBjThreads) bj_step_kernel(const __grid_consta
     const int vr0 = (int)((long long)cp * crank / S), vr1 = (int)((long long)cp * (crank + 1) / S);
     const long long col0 = (long long)k0 * n2;  // the pair's first column (slots 2k0, 2k0+1)
     const cplx* X = a.Xs[pr];
+    const cplx* V = a.Vs[pr];
+    // stage rows [r0, r0 + kBjRows) of the pair's columns of M (zero-filled from rend on)
+    auto stage = [&](const cplx* M, int r0, int rend, Chunk& dst) {
+#pragma unroll
+        for (int u = 0; u < kBjRows * n2 / kBjThreads; ++u) {
+            const int e = tid + u * kBjThreads, i = e / n2, j = e % n2;
+            const bool ok = r0 + i < rend;
+            cp_async16(&dst[i][j], ok ? M + (long long)(r0 + i) * cp + col0 + j : M, ok);
+        }
+        cp_async_commit();
+    };
 
     // ---- Gram of this CTA's row slice on the FP64 tensor core: the 32 x 32 result is 4 x 4 tiles
     // of 8 x 8, of which the 10 upper-triangular ones are formed (the solve mirrors them); warps
     // 0..4 accumulate two tiles each.  Fragments are one LDS.128 (re, im) per lane; conj(X)^T X in
-    // 4M form: Re += xr xr' + xi xi', Im += xr xi' - xi xr'.
+    // 4M form: Re += xr xr' + xi xi', Im += xr xi' - xi xr'.  Chunks stream through two buffers
+    // (cp.async: chunk t+1 lands while chunk t is multiplied).
     const int lane = tid & 31, warp = tid >> 5;
     // upper tiles t = 0..9 as 4-bit (p | q << 2) fields: (0,0) (0,1) (0,2) (0,3) (1,1) (1,2) (1,3) (2,2) (2,3) (3,3)
     constexpr unsigned long long kTiles = 0xfead95c840ull;
@@ -78,17 +99,21 @@ __global__ void __launch_bounds__(kBjThreads) bj_step_kernel(const __grid_consta
     const int fa = (int)(kTiles >> (4 * ta)) & 15, fb = (int)(kTiles >> (4 * ta + 4)) & 15;
     const int pa = fa & 3, qa_ = fa >> 2, pb = fb & 3, qb = fb >> 2;
     double gre[2][2] = {{0.0, 0.0}, {0.0, 0.0}}, gim[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
-    for (int r0 = xr0; r0 < xr1; r0 += kBjRows) {
-        const int nr = min(kBjRows, xr1 - r0), nr4 = (nr + 3) & ~3;
-        __syncthreads();
-        for (int e = tid; e < nr4 * n2; e += kBjThreads) {
-            const int i = e / n2, j = e % n2;
-            ch[i][j] = i < nr ? X[(long long)(r0 + i) * cp + col0 + j] : mk(0.0, 0.0);
+    const int ngc = (xr1 - xr0 + kBjRows - 1) / kBjRows;
+    if (ngc > 0) stage(X, xr0, xr1, buf[0]);
+    for (int t = 0; t < ngc; ++t) {
+        if (t + 1 < ngc) {
+            stage(X, xr0 + (t + 1) * kBjRows, xr1, buf[(t + 1) & 1]);
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
         }
         __syncthreads();
         if (gwarp) {
-            for (int k0 = 0; k0 < nr4; k0 += 4) {
-                const cplx* row = ch[k0 + (lane & 3)];
+            const Chunk& ch = buf[t & 1];
+#pragma unroll 2
+            for (int kq = 0; kq < kBjRows; kq += 4) {
+                const cplx* row = ch[kq + (lane & 3)];
                 const int cl = lane >> 2;
                 const cplx x0 = row[pa * 8 + cl], y0 = row[qa_ * 8 + cl];
                 const cplx x1 = row[pb * 8 + cl], y1 = row[qb * 8 + cl];
@@ -102,7 +127,16 @@ __global__ void __launch_bounds__(kBjThreads) bj_step_kernel(const __grid_consta
                 dmma884(gim[1][0], gim[1][1], -x1.y, y1.x);
             }
         }
+        __syncthreads();  // (the buffer is refilled two chunks later)
     }
+    // the first chunk of the rotation apply streams in during the solve (buffer 1: the solve
+    // uses buffer 0 as its second G)
+    const int nxc = (xr1 - xr0 + kBjRows - 1) / kBjRows, nvc = (vr1 - vr0 + kBjRows - 1) / kBjRows;
+    auto stage_apply = [&](int t, Chunk& dst) {
+        if (t < nxc) stage(X, xr0 + t * kBjRows, xr1, dst);
+        else stage(V, vr0 + (t - nxc) * kBjRows, vr1, dst);
+    };
+    if (nxc + nvc > 0) stage_apply(0, buf[1]);
     if (gwarp) {
 #pragma unroll
         for (int c = 0; c < 2; ++c) {
@@ -149,7 +183,7 @@ __global__ void __launch_bounds__(kBjThreads) bj_step_kernel(const __grid_consta
     const double tol = sqrt((double)max(r, 1)) * kEpsBj;
     __shared__ int s_first;  // rotations of the first inner sweep: the outer convergence signal
     cplx(*Gi)[ld] = sG;
-    cplx(*Go)[ld] = ch;  // (the chunk buffer is idle during the solve)
+    cplx(*Go)[ld] = buf[0];  // (chunk buffer 0 is idle during the solve)
     const int ka = tid >> 4, kb = tid & 15;
     for (int isw = 0; isw < a.inner_sweeps; ++isw) {
     const int rot_before = s_rot;
@@ -229,51 +263,54 @@ __global__ void __launch_bounds__(kBjThreads) bj_step_kernel(const __grid_consta
     }
     cluster.sync();  // CTA 0's W may now be left (and the kernel may end) — peers have copied it
 
-    // ---- [X_i X_j] W and [V_i V_j] W into the next step's block positions
+    // ---- [X_i X_j] W and [V_i V_j] W into the next step's block positions: the X chunks, then the
+    // V chunks, double-buffered (chunk t in buffer (t + 1) & 1).  Warp w: row tile w & 3 of the
+    // chunk times column tiles 2 (w >> 2) + {0, 1} of W, on DMMA.
     const long long dA = (long long)a.dst[2 * k0] * b, dB = (long long)a.dst[2 * k0 + 1] * b;
-    for (int m = 0; m < 2; ++m) {
-        const cplx* S = m == 0 ? X : a.Vs[pr];
-        cplx* D = m == 0 ? a.Xd[pr] : a.Vd[pr];
-        const int rbeg = m == 0 ? xr0 : vr0, rend = m == 0 ? xr1 : vr1;
-        for (int r0 = rbeg; r0 < rend; r0 += kBjRows) {
-            const int nr = min(kBjRows, rend - r0), nr8 = (nr + 7) & ~7;
-            __syncthreads();
-            for (int e = tid; e < nr8 * n2; e += kBjThreads) {
-                const int i = e / n2, j = e % n2;
-                ch[i][j] = i < nr ? S[(long long)(r0 + i) * cp + col0 + j] : mk(0.0, 0.0);
+    const int nac = nxc + nvc;
+    const int rt = warp & 3, ct0 = 2 * (warp >> 2);
+    for (int t = 0; t < nac; ++t) {
+        if (t + 1 < nac) {
+            stage_apply(t + 1, buf[t & 1]);
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
+        __syncthreads();
+        const Chunk& ch = buf[(t + 1) & 1];
+        const bool isx = t < nxc;
+        cplx* D = isx ? a.Xd[pr] : a.Vd[pr];
+        const int r0 = isx ? xr0 + t * kBjRows : vr0 + (t - nxc) * kBjRows;
+        const int nr = min(kBjRows, (isx ? xr1 : vr1) - r0);
+        if (rt * 8 < nr) {
+            double are[2][2] = {{0.0, 0.0}, {0.0, 0.0}}, aim[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+#pragma unroll
+            for (int kk = 0; kk < n2 / 4; ++kk) {
+                const cplx xa = ch[rt * 8 + (lane >> 2)][kk * 4 + (lane & 3)];
+                const cplx w0 = sW[kk * 4 + (lane & 3)][ct0 * 8 + (lane >> 2)];
+                const cplx w1 = sW[kk * 4 + (lane & 3)][(ct0 + 1) * 8 + (lane >> 2)];
+                dmma884(are[0][0], are[0][1], xa.x, w0.x);
+                dmma884(are[1][0], are[1][1], xa.x, w1.x);
+                dmma884(aim[0][0], aim[0][1], xa.x, w0.y);
+                dmma884(aim[1][0], aim[1][1], xa.x, w1.y);
+                dmma884(are[0][0], are[0][1], -xa.y, w0.y);
+                dmma884(are[1][0], are[1][1], -xa.y, w1.y);
+                dmma884(aim[0][0], aim[0][1], xa.y, w0.x);
+                dmma884(aim[1][0], aim[1][1], xa.y, w1.x);
             }
-            __syncthreads();
-            // warp w: rows 8w .. 8w+7 of the chunk times all of W (4 column tiles), on DMMA
-            const int rt = warp;
-            if (rt * 8 < nr) {
-                double are[4][2], aim[4][2];
+            const int i = rt * 8 + (lane >> 2);
+            if (i < nr) {
+                const long long row = (long long)(r0 + i) * cp;
 #pragma unroll
-                for (int ct = 0; ct < 4; ++ct) are[ct][0] = are[ct][1] = aim[ct][0] = aim[ct][1] = 0.0;
+                for (int q = 0; q < 2; ++q)
 #pragma unroll
-                for (int kk = 0; kk < n2 / 4; ++kk) {
-                    const cplx xa = ch[rt * 8 + (lane >> 2)][kk * 4 + (lane & 3)];
-#pragma unroll
-                    for (int ct = 0; ct < 4; ++ct) {
-                        const cplx wb = sW[kk * 4 + (lane & 3)][ct * 8 + (lane >> 2)];
-                        dmma884(are[ct][0], are[ct][1], xa.x, wb.x);
-                        dmma884(are[ct][0], are[ct][1], -xa.y, wb.y);
-                        dmma884(aim[ct][0], aim[ct][1], xa.x, wb.y);
-                        dmma884(aim[ct][0], aim[ct][1], xa.y, wb.x);
+                    for (int c = 0; c < 2; ++c) {
+                        const int j = (ct0 + q) * 8 + 2 * (lane & 3) + c;
+                        D[row + (j < b ? dA + j : dB + j - b)] = mk(are[q][c], aim[q][c]);
                     }
-                }
-                const int i = rt * 8 + (lane >> 2);
-                if (i < nr) {
-                    const long long row = (long long)(r0 + i) * cp;
-#pragma unroll
-                    for (int ct = 0; ct < 4; ++ct)
-#pragma unroll
-                        for (int c = 0; c < 2; ++c) {
-                            const int j = ct * 8 + 2 * (lane & 3) + c;
-                            D[row + (j < b ? dA + j : dB + j - b)] = mk(are[ct][c], aim[ct][c]);
-                        }
-                }
             }
         }
+        __syncthreads();  // (the buffer is refilled by the next iteration's prefetch)
     }
 }
 
@@ -337,14 +374,14 @@ cudaError_t bj_init(const BjInit& a, cudaStream_t s) {
 cudaError_t bj_step(const BjStep& a, cudaStream_t s) {
     if (a.count == 0) return cudaSuccess;
     if (2 * a.b != kBjN2) return cudaErrorInvalidValue;
-    constexpr size_t smem = sizeof(cplx) * (kBjRows * (kBjN2 + 1) + 2 * kBjN2 * (kBjN2 + 1));
+    constexpr size_t smem = sizeof(cplx) * (2 * kBjRows * (kBjN2 + 1) + 2 * kBjN2 * (kBjN2 + 1));
     cudaError_t e = cudaFuncSetAttribute(bj_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     // row slices per pair: as many as keep every CTA resident in one wave (3 per SM at this
     // shared-memory size), at most 8 (portable cluster), at least one 64-row chunk per slice
     const long long pairs = (long long)a.npairs * a.count;
     int S = 1;
-    while (S < 8 && pairs * (2 * S) <= 3LL * 148 && (a.r / (2 * S)) >= kBjRows) S *= 2;
+    while (S < 8 && pairs * (2 * S) <= 3LL * 148 && (a.r / (2 * S)) >= 64) S *= 2;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(a.npairs * S, a.count);
     cfg.blockDim = dim3(kBjThreads);

@@ -16,10 +16,15 @@ constexpr double kEps = 2.220446049250313e-16;  // 2^-52
 
 // ============================================================================ Cholesky + inverse
 constexpr int CHOL_THREADS = 256;
-constexpr int NB = 8;       // Cholesky panel / inverse block rows
-constexpr int RG = 4;       // trailing-update rows per warp tile
-constexpr int SPLIT = 4;    // threads per column in the inverse's q-sums
-constexpr int kChunks = (kMaxCholL + CHOL_THREADS / SPLIT - 1) / (CHOL_THREADS / SPLIT);
+constexpr int NB = 8;  // panel width = the DMMA tile edge
+
+// G (L x L, L = l rounded up to 8) lives unpacked in shared memory with ld = L + 2: ld = 2 (mod 8)
+// makes the 8 x 4 / 4 x 8 complex fragment loads of mma.m8n8k4 conflict-free.
+__host__ __device__ constexpr int chol_ld(int L) { return L + 2; }
+size_t chol_smem_bytes(int max_l) {
+    const int L = (max_l + 7) & ~7;
+    return (size_t)(L + NB) * chol_ld(L) * sizeof(cplx) + (size_t)L * (2 * sizeof(double) + sizeof(int));
+}
 
 // acc -= conj(a) * b
 __device__ __forceinline__ void cfnmac(cplx& acc, cplx a, cplx b) {
@@ -29,24 +34,41 @@ __device__ __forceinline__ void cfnmac(cplx& acc, cplx a, cplx b) {
     acc.y = fma(a.y, b.x, acc.y);
 }
 
-__device__ __forceinline__ int poff(int i, int l) { return i * l - (i * (i - 1)) / 2; }
-
-__global__ void __launch_bounds__(CHOL_THREADS) chol_inv_kernel(const __grid_constant__ CholBatch b) {
+// One CTA per problem.  Shifted Cholesky G + sI = R^H R (R upper) and T = R^-1, in place.
+//  * panels of NB = 8 rows: warp 0 factors the 8 x 8 diagonal block (lanes redundantly, no
+//    barrier per pivot); one thread per column forward-solves the panel's off-diagonal rows;
+//    the rank-8 trailing update G_>J,>J -= R_J,>J^H R_J,>J runs on the FP64 tensor core as
+//    8 x 8 tiles of the upper triangle (mma.m8n8k4, 4M complex form).
+//  * the inverse bottom-up by block rows: S = R_I,>I T_>I,k as DMMA tiles (T_qk = 0 for q > k
+//    bounds each tile's K), then per column the 8-step in-block recurrence
+//    T_ik = -T_ii (S_ik + sum_{u in block, u > i} R_iu T_uk), T_ii = 1 / R_ii.
+// The strictly lower triangle of the buffer stays zero throughout (T is read as a full tile).
+// A dependent (dead) pivot gets R_ii = 0 and T_i: = 0.  ill_out: some pivot within kIllRatio of
+// the shift (or dead).
+__global__ void __launch_bounds__(CHOL_THREADS, 1) chol_inv_kernel(const __grid_constant__ CholBatch b) {
     extern __shared__ __align__(16) unsigned char sm[];
     const int p = blockIdx.x;
+    if (b.pred[p] != nullptr && *b.pred[p] == 0) return;
     const int l = b.l[p];
-    const int npk = l * (l + 1) / 2;
-    cplx* P = reinterpret_cast<cplx*>(sm);
-    double* g0 = reinterpret_cast<double*>(P + npk);
-    int* dead = reinterpret_cast<int*>(g0 + l);
+    const int L = (l + 7) & ~7, ld = chol_ld(L);
+    cplx* P = reinterpret_cast<cplx*>(sm);        // [L][ld]: G -> R (upper) -> T
+    cplx* sS = P + (size_t)L * ld;                // [NB][ld]: the inverse's block-row sums
+    double* g0 = reinterpret_cast<double*>(sS + (size_t)NB * ld);
+    double* rinv = g0 + L;                        // 1 / R_ii (0 for a dead pivot)
+    int* dead = reinterpret_cast<int*>(rinv + L);
+    // upper-triangle tiles (ti <= tk) of the L/8 x L/8 tile grid ordered by ti DESCENDING: the
+    // trailing tiles of panel J (ti, tk > J) are then a prefix of the table
+    constexpr int kMaxTiles = (kMaxCholL / NB) * (kMaxCholL / NB + 1) / 2;
+    __shared__ unsigned short s_tile[kMaxTiles];
     __shared__ double s_shift;
+    __shared__ int s_ill;
+    __shared__ cplx sD[NB * NB];
+    __shared__ double sinv[NB];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = CHOL_THREADS / 32;
-    if (b.pred[p] != nullptr && *b.pred[p] == 0) return;
     const cplx* G = b.G[p];
     const long long ldg = b.ldg[p] > 0 ? b.ldg[p] : l;
     const cplx* Gs = b.Gsub[p];
-    __shared__ int s_ill;
 
     if (tid == 0) s_ill = 0;
     if (warp == 0) {  // shift from the trace of the whole Gram matrix (also for a trailing block)
@@ -66,31 +88,50 @@ __global__ void __launch_bounds__(CHOL_THREADS) chol_inv_kernel(const __grid_con
         }
     }
     __syncthreads();
-    for (int i = warp; i < l; i += nw)
-        for (int k = i + lane; k < l; k += 32) {
-            cplx v = G[(long long)i * ldg + k];
-            if (k == i) {
-                v = mk(v.x + s_shift, 0.0);
-                g0[i] = v.x;  // dependence is judged against the pivot's original diagonal
-            }
-            if (Gs != nullptr) {
-                const cplx w = Gs[(long long)i * l + k];
-                v.x -= w.x;
-                v.y -= (k == i) ? 0.0 : w.y;
-            }
-            P[poff(i, l) + k - i] = v;
+    {
+        const int n8 = L / NB;
+        for (int tt = tid; tt < n8 * (n8 + 1) / 2; tt += CHOL_THREADS) {
+            int ti = n8 - 1, rem = tt;  // rows of the grid from the bottom: row ti has n8 - ti tiles
+            while (rem >= n8 - ti) { rem -= n8 - ti; --ti; }
+            s_tile[tt] = (unsigned short)(ti << 8 | (ti + rem));
         }
+    }
+    // fill: the upper triangle of G (+ shift on the diagonal, - Gsub), zeros elsewhere; a warp per
+    // pair of rows, eight independent loads in flight per lane
+    for (int i2 = 2 * warp; i2 < L; i2 += 2 * nw) {
+        cplx v[2][4];
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int i = i2 + h, k = lane + 32 * u;
+                v[h][u] = (i < l && k < l && k >= i) ? G[(long long)i * ldg + k] : mk(0.0, 0.0);
+            }
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int i = i2 + h, k = lane + 32 * u;
+                if (i >= L || k >= L) continue;
+                cplx x = v[h][u];
+                if (i < l && k < l && k >= i) {
+                    if (k == i) {
+                        x = mk(x.x + s_shift, 0.0);
+                        g0[i] = x.x;  // dependence is judged against the pivot's original diagonal
+                    }
+                    if (Gs != nullptr) {
+                        const cplx w = Gs[(long long)i * l + k];
+                        x.x -= w.x;
+                        x.y -= (k == i) ? 0.0 : w.y;
+                    }
+                }
+                P[(size_t)i * ld + k] = x;
+            }
+    }
     __syncthreads();
 
-    // ---- blocked right-looking Cholesky, G = R^H R, R upper; row j of R overwrites row j of G.
-    // Panels of NB rows.  Every thread factors the panel's NB x NB diagonal block redundantly in
-    // registers (broadcast reads — no barrier per pivot), then forward-solves one column of the
-    // panel's off-diagonal rows: R[J][k] = R_JJ^-H G[J][k].  The rank-NB trailing update
-    // G[i][k] -= sum_t conj(R[t][i]) R[t][k] is register-tiled: a warp takes RG consecutive rows
-    // (their NB coefficients in registers), its lanes sweep the columns.  Two barriers per panel.
+    // ---- right-looking Cholesky by panels of NB rows
     const double dtol = b.dep_tol[p];
-    __shared__ cplx sD[NB * NB];
-    __shared__ double sinv[NB];
     for (int j0 = 0; j0 < l; j0 += NB) {
         const int nb = min(NB, l - j0);
         cplx D[NB][NB];
@@ -100,7 +141,7 @@ __global__ void __launch_bounds__(CHOL_THREADS) chol_inv_kernel(const __grid_con
 #pragma unroll
             for (int t = 0; t < NB; ++t)
 #pragma unroll
-                for (int u = t; u < NB; ++u) D[t][u] = (u < nb) ? P[poff(j0 + t, l) + u - t] : mk(0.0, 0.0);
+                for (int u = t; u < NB; ++u) D[t][u] = (u < nb) ? P[(size_t)(j0 + t) * ld + j0 + u] : mk(0.0, 0.0);
 #pragma unroll
             for (int t = 0; t < NB; ++t) {
                 inv[t] = 0.0;
@@ -126,21 +167,25 @@ __global__ void __launch_bounds__(CHOL_THREADS) chol_inv_kernel(const __grid_con
                     sinv[t] = inv[t];
 #pragma unroll
                     for (int u = t; u < NB; ++u) sD[t * NB + u] = D[t][u];
-                    if (t < nb) dead[j0 + t] = (deadmask >> t) & 1u;
+                    if (t < nb) {
+                        dead[j0 + t] = (deadmask >> t) & 1u;
+                        rinv[j0 + t] = inv[t];
+                    }
                 }
             }
         }
         __syncthreads();
-#pragma unroll
-        for (int t = 0; t < NB; ++t) {
-            inv[t] = sinv[t];
-#pragma unroll
-            for (int u = t; u < NB; ++u) D[t][u] = sD[t * NB + u];
-        }
+        // panel: R[J][k] = R_JJ^-H G[J][k], one column per thread
         for (int k = j0 + nb + tid; k < l; k += CHOL_THREADS) {
+#pragma unroll
+            for (int t = 0; t < NB; ++t) {
+                inv[t] = sinv[t];
+#pragma unroll
+                for (int u = t; u < NB; ++u) D[t][u] = sD[t * NB + u];
+            }
             cplx X[NB];
 #pragma unroll
-            for (int t = 0; t < NB; ++t) X[t] = (t < nb) ? P[poff(j0 + t, l) + k - j0 - t] : mk(0.0, 0.0);
+            for (int t = 0; t < NB; ++t) X[t] = (t < nb) ? P[(size_t)(j0 + t) * ld + k] : mk(0.0, 0.0);
 #pragma unroll
             for (int t = 0; t < NB; ++t) {
 #pragma unroll
@@ -149,104 +194,88 @@ __global__ void __launch_bounds__(CHOL_THREADS) chol_inv_kernel(const __grid_con
             }
 #pragma unroll
             for (int t = 0; t < NB; ++t)
-                if (t < nb) P[poff(j0 + t, l) + k - j0 - t] = X[t];
+                if (t < nb) P[(size_t)(j0 + t) * ld + k] = X[t];
         }
         if (tid == 0) {
 #pragma unroll
             for (int t = 0; t < NB; ++t)
 #pragma unroll
                 for (int u = t; u < NB; ++u)
-                    if (u < nb) P[poff(j0 + t, l) + u - t] = D[t][u];
+                    if (u < nb) P[(size_t)(j0 + t) * ld + j0 + u] = sD[t * NB + u];
         }
         __syncthreads();
-        for (int r0 = j0 + nb + RG * warp; r0 < l; r0 += RG * nw) {
-            cplx a[RG][NB];
+        if (nb == NB) {  // trailing update on DMMA (a partial panel is the last: nothing trails it)
+            const int t0 = j0 / NB + 1, nt = L / NB - t0;
+            const int ntiles = nt * (nt + 1) / 2;
+            for (int tt = warp; tt < ntiles; tt += nw) {
+                const int code = s_tile[tt];
+                const int r0 = (code >> 8) * NB, c0 = (code & 255) * NB;
+                cplx* Cp = P + (size_t)(r0 + (lane >> 2)) * ld + c0 + 2 * (lane & 3);
+                double cre[2] = {Cp[0].x, Cp[1].x}, cim[2] = {Cp[0].y, Cp[1].y};
+                double dre[2] = {0.0, 0.0}, dim[2] = {0.0, 0.0};
 #pragma unroll
-            for (int ri = 0; ri < RG; ++ri)
-#pragma unroll
-                for (int t = 0; t < NB; ++t)
-                    a[ri][t] = (t < nb && r0 + ri < l) ? P[poff(j0 + t, l) + r0 + ri - j0 - t] : mk(0.0, 0.0);
-            for (int k = r0 + lane; k < l; k += 32) {
-                cplx bb[NB];
-#pragma unroll
-                for (int t = 0; t < NB; ++t) bb[t] = (t < nb) ? P[poff(j0 + t, l) + k - j0 - t] : mk(0.0, 0.0);
-#pragma unroll
-                for (int ri = 0; ri < RG; ++ri) {
-                    const int i = r0 + ri;
-                    if (i <= k) {
-                        cplx* pv = P + poff(i, l) + k - i;
-                        cplx v = *pv;
-#pragma unroll
-                        for (int t = 0; t < NB; ++t) cfnmac(v, a[ri][t], bb[t]);
-                        *pv = v;
-                    }
+                for (int ks = 0; ks < 2; ++ks) {
+                    const cplx* Rrow = P + (size_t)(j0 + 4 * ks + (lane & 3)) * ld;
+                    const cplx a = Rrow[r0 + (lane >> 2)], bb = Rrow[c0 + (lane >> 2)];
+                    // C -= conj(A)^T B:  Re -= ar br + ai bi,  Im -= ar bi - ai br
+                    dmma884(cre[0], cre[1], -a.x, bb.x);
+                    dmma884(dre[0], dre[1], -a.y, bb.y);
+                    dmma884(cim[0], cim[1], -a.x, bb.y);
+                    dmma884(dim[0], dim[1], a.y, bb.x);
                 }
+                const int row = r0 + (lane >> 2);
+#pragma unroll
+                for (int c = 0; c < 2; ++c)
+                    if (c0 + 2 * (lane & 3) + c >= row) Cp[c] = mk(cre[c] + dre[c], cim[c] + dim[c]);
             }
         }
         __syncthreads();
     }
 
-    // ---- in-place triangular inverse T = R^-1, bottom-up by blocks of NB rows:
-    //   T[i][i] = 1/R[i][i],  T[i][k] = -T[i][i] * sum_{q=i+1..k} R[i][q] T[q][k]   (k > i).
-    // For block rows [i0, i0+nb) and one column k, the q-sum splits into q >= i0+nb (rows that
-    // already hold T: NB dot products sharing T[q][k], split over SPLIT threads) and q inside
-    // the block (an NB x NB triangular recurrence, done redundantly by the SPLIT threads).
-    // Results wait in registers for a barrier: every column reads the block's R rows.
-    // A dependent (dead) row gets T[i][:] = 0, which zeroes column i of T as well.
-    const int grp = tid / SPLIT, sub = tid % SPLIT;
-    constexpr int kGroups = CHOL_THREADS / SPLIT;
+    // ---- in-place inverse, bottom-up by block rows
     for (int i0 = (l - 1) / NB * NB; i0 >= 0; i0 -= NB) {
         const int nb = min(NB, l - i0);
+        const int kt0 = i0 / NB + 1, nkt = L / NB - kt0;
+        for (int tt = warp; tt < nkt; tt += nw) {  // S[:, tile] = R[I][q > I] T[q][tile]
+            const int c0 = (kt0 + tt) * NB;
+            double sre[2] = {0.0, 0.0}, sim[2] = {0.0, 0.0}, ure[2] = {0.0, 0.0}, uim[2] = {0.0, 0.0};
+            const cplx* Arow = P + (size_t)(i0 + (lane >> 2)) * ld + (lane & 3);
+            const cplx* Bcol = P + (size_t)(lane & 3) * ld + c0 + (lane >> 2);
+            for (int q0 = i0 + NB; q0 < c0 + NB; q0 += 4) {
+                const cplx a = Arow[q0], bb = Bcol[(size_t)q0 * ld];
+                dmma884(sre[0], sre[1], a.x, bb.x);
+                dmma884(ure[0], ure[1], -a.y, bb.y);
+                dmma884(sim[0], sim[1], a.x, bb.y);
+                dmma884(uim[0], uim[1], a.y, bb.x);
+            }
+            cplx* Sp = sS + (size_t)(lane >> 2) * ld + c0 + 2 * (lane & 3);
+            Sp[0] = mk(sre[0] + ure[0], sim[0] + uim[0]);
+            Sp[1] = mk(sre[1] + ure[1], sim[1] + uim[1]);
+        }
+        __syncthreads();
         double tii[NB];
 #pragma unroll
         for (int t = 0; t < NB; ++t)
-            tii[t] = (t < nb && !dead[i0 + t]) ? 1.0 / P[poff(i0 + t, l)].x : 0.0;
-        cplx res[kChunks][NB];
-#pragma unroll
-        for (int ch = 0; ch < kChunks; ++ch) {
-            const int k = i0 + grp + ch * kGroups;
-            if (i0 + ch * kGroups >= l) {  // block-uniform: this chunk has no column at all
-#pragma unroll
-                for (int t = 0; t < NB; ++t) res[ch][t] = mk(0.0, 0.0);
-                continue;
-            }
-            cplx S[NB];
-#pragma unroll
-            for (int t = 0; t < NB; ++t) S[t] = mk(0.0, 0.0);
-            if (k < l) {
-                for (int q = i0 + nb + sub; q <= k; q += SPLIT) {
-                    const cplx tq = P[poff(q, l) + k - q];
-#pragma unroll
-                    for (int t = 0; t < NB; ++t)
-                        if (t < nb) cfma(S[t], P[poff(i0 + t, l) + q - i0 - t], tq);
-                }
-            }
-#pragma unroll
-            for (int t = 0; t < NB; ++t) {
-#pragma unroll
-                for (int o = 1; o < SPLIT; o <<= 1) {
-                    S[t].x += __shfl_xor_sync(0xffffffffu, S[t].x, o);
-                    S[t].y += __shfl_xor_sync(0xffffffffu, S[t].y, o);
-                }
-            }
+            tii[t] = t < nb ? rinv[i0 + t] : 0.0;  // (= 1 / R_ii as the factorization formed it; 0 if dead)
+        const int k = i0 + tid;
+        cplx res[NB];
+        if (k < l) {
 #pragma unroll
             for (int t = NB - 1; t >= 0; --t) {
-                cplx acc = S[t];
+                res[t] = mk(0.0, 0.0);
+                if (t >= nb || i0 + t > k) continue;
+                cplx acc = k >= i0 + NB ? sS[(size_t)t * ld + k] : mk(0.0, 0.0);
 #pragma unroll
                 for (int u = t + 1; u < NB; ++u)
-                    if (u < nb && i0 + u <= k) cfma(acc, P[poff(i0 + t, l) + u - t], res[ch][u]);
-                res[ch][t] = (i0 + t == k) ? mk(tii[t], 0.0) : cscale(acc, -tii[t]);
+                    if (u < nb && i0 + u <= k) cfma(acc, P[(size_t)(i0 + t) * ld + i0 + u], res[u]);
+                res[t] = (i0 + t == k) ? mk(tii[t], 0.0) : cscale(acc, -tii[t]);
             }
         }
-        __syncthreads();
-        if (sub == 0) {
+        __syncthreads();  // every read of the block's R rows precedes the writes
+        if (k < l) {
 #pragma unroll
-            for (int ch = 0; ch < kChunks; ++ch) {
-                const int k = i0 + grp + ch * kGroups;
-#pragma unroll
-                for (int t = 0; t < NB; ++t)
-                    if (t < nb && i0 + t <= k && k < l) P[poff(i0 + t, l) + k - i0 - t] = res[ch][t];
-            }
+            for (int t = 0; t < NB; ++t)
+                if (t < nb && i0 + t <= k) P[(size_t)(i0 + t) * ld + k] = res[t];
         }
         __syncthreads();
     }
@@ -254,12 +283,16 @@ __global__ void __launch_bounds__(CHOL_THREADS) chol_inv_kernel(const __grid_con
     cplx* T = b.T[p];
     cplx* Tn = b.Tneg[p];
     const long long ldt = b.ldt[p] > 0 ? b.ldt[p] : l;
-    for (int i = warp; i < l; i += nw)
+    for (int i = warp; i < l; i += nw) {  // (the lower triangle of the buffer is zero)
+        const cplx* src = P + (size_t)i * ld;
+        cplx* dt = T + (long long)i * ldt;
+        cplx* dn = Tn != nullptr ? Tn + (long long)i * ldt : nullptr;
         for (int k = lane; k < l; k += 32) {
-            const cplx v = (k >= i) ? P[poff(i, l) + k - i] : mk(0.0, 0.0);
-            T[(long long)i * ldt + k] = v;
-            if (Tn != nullptr) Tn[(long long)i * ldt + k] = mk(-v.x, -v.y);
+            const cplx v = src[k];
+            dt[k] = v;
+            if (dn != nullptr) dn[k] = mk(-v.x, -v.y);
         }
+    }
     if (b.ill_out[p] != nullptr && tid == 0 && s_ill) *b.ill_out[p] = 1;  // (zeroed by the caller)
     if (b.ndead[p] != nullptr && tid == 0) {
         int n = 0;
@@ -624,8 +657,8 @@ __global__ void sumsq_final(const double* partial, const int* bad, double* out, 
 
 cudaError_t chol_inv(const CholBatch& b, int max_l, cudaStream_t s) {
     if (b.count == 0) return cudaSuccess;
-    const size_t smem = (size_t)max_l * (max_l + 1) / 2 * sizeof(cplx) + max_l * sizeof(double) +
-                        max_l * sizeof(int);
+    if (max_l > kMaxCholL) return cudaErrorInvalidValue;
+    const size_t smem = chol_smem_bytes(max_l);
     cudaError_t e = cudaFuncSetAttribute(chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     chol_inv_kernel<<<b.count, CHOL_THREADS, smem, s>>>(b);

@@ -15,7 +15,7 @@ constexpr int kMaxSmall = 64;  // problems per launch of the small-matrix kernel
 // schedule (pipeline.cu orth_many) keeps the Gram matrices of its plain passes well
 // conditioned, so it runs with dep_tol = 0: only non-positive pivots (exactly vanishing
 // columns) die, and no genuine small-σ direction is discarded.
-constexpr int kMaxCholL = 168;  // packed upper triangle must fit in 227 KB of shared memory
+constexpr int kMaxCholL = 112;  // the unpacked L x (L + 2) Gram (+ an 8-row scratch) fits 227 KB of shared memory
 
 struct CholBatch {
     int count;

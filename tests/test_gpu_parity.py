@@ -45,11 +45,12 @@ def test_philox_sketch_statistics(ctx):
 
 # ------------------------------------------------------------------ QR / SVD (linalg.cpp)
 
-@pytest.mark.parametrize("m,n", [(40, 40), (300, 74), (2000, 110), (1000, 168), (1000, 169), (2000, 200),
-                                 (300, 256), (700, 328), (1200, 500), (2000, 1000)])
+@pytest.mark.parametrize("m,n", [(40, 40), (300, 74), (2000, 110), (500, 111), (1000, 112), (1000, 113),
+                                 (1000, 168), (1000, 169), (2000, 200), (300, 256), (700, 328), (1200, 500),
+                                 (2000, 1000)])
 def test_qr_orthonormal_and_reconstructs(ctx, m, n):
-    """test_linalg.cpp:114-121: orthonormality and reconstruction < 1e-12.  Widths above 168
-    go through the block-right-looking Cholesky (diagonal blocks <= 168, DMMA updates)."""
+    """test_linalg.cpp:114-121: orthonormality and reconstruction < 1e-12.  Widths above 112
+    go through the block-right-looking Cholesky (diagonal blocks <= 112, DMMA updates)."""
     rng = np.random.default_rng(m + n)
     a = cplx_randn(rng, m, n)
     q, r = P.qr(a, ctx=ctx)
