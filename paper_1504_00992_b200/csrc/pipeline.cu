@@ -468,19 +468,21 @@ void small_svd_many(rrsvd_b200_ctx* c, const std::vector<SmallSvdSpec>& specs) {
         if (debug_enabled()) dsweeps[i] = ws_get<int>(c, 1);
         (specs[i].cc <= block_jacobi_min_c() && jacobi_fits(specs[i].r, specs[i].cc) ? onchip : global).push_back(i);
     }
-    // wide problems: block Jacobi over DMMA GEMMs, grouped by shape
-    while (!global.empty()) {
-        std::vector<const SmallSvdSpec*> grp;
-        std::vector<size_t> rest;
-        for (size_t i : global) {
-            const SmallSvdSpec& s = specs[i];
-            if (grp.empty() || (s.r == grp[0]->r && s.cc == grp[0]->cc && (int)grp.size() < kBjMaxProblems))
-                grp.push_back(&s);
-            else
-                rest.push_back(i);
+    // The on-chip batch (one launch of a few clusters) runs on a side stream beside the block
+    // Jacobi groups (many short launches with a host read per sweep), which leave SMs free.
+    const cudaStream_t main_stream = c->stream;
+    constexpr int kSide = rrsvd_b200_ctx::kMaxLanes - 1;
+    const bool fork = !global.empty() && !onchip.empty() && c->stream != c->lane[kSide];
+    if (fork) {
+        if (c->lane[kSide] == nullptr) {
+            check_cuda(c, cudaStreamCreateWithFlags(&c->lane[kSide], cudaStreamNonBlocking), "side stream");
+            check_cuda(c, cudaEventCreateWithFlags(&c->ev_join[kSide], cudaEventDisableTiming), "side event");
         }
-        block_jacobi_group(c, grp);
-        global.swap(rest);
+        if (c->ev_fork == nullptr)
+            check_cuda(c, cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming), "fork event");
+        check_cuda(c, cudaEventRecord(c->ev_fork, main_stream), "fork record");
+        check_cuda(c, cudaStreamWaitEvent(c->lane[kSide], c->ev_fork, 0), "fork wait");
+        c->stream = c->lane[kSide];
     }
     for (size_t base = 0; base < onchip.size(); base += kMaxSmall) {
         const size_t end = std::min(onchip.size(), base + kMaxSmall);
@@ -504,6 +506,25 @@ void small_svd_many(rrsvd_b200_ctx* c, const std::vector<SmallSvdSpec>& specs) {
         check_cuda(c, jacobi_svd(jb, max_r, max_c, c->stream), "jacobi_svd");
         check_cuda(c, jacobi_finish(fb, max_c, c->stream), "jacobi_finish");
         c->launches += 3;
+    }
+    c->stream = main_stream;
+    // wide problems: block Jacobi over DMMA GEMMs, grouped by shape
+    while (!global.empty()) {
+        std::vector<const SmallSvdSpec*> grp;
+        std::vector<size_t> rest;
+        for (size_t i : global) {
+            const SmallSvdSpec& s = specs[i];
+            if (grp.empty() || (s.r == grp[0]->r && s.cc == grp[0]->cc && (int)grp.size() < kBjMaxProblems))
+                grp.push_back(&s);
+            else
+                rest.push_back(i);
+        }
+        block_jacobi_group(c, grp);
+        global.swap(rest);
+    }
+    if (fork) {
+        check_cuda(c, cudaEventRecord(c->ev_join[kSide], c->lane[kSide]), "join record");
+        check_cuda(c, cudaStreamWaitEvent(main_stream, c->ev_join[kSide], 0), "join wait");
     }
     if (debug_enabled()) {
         for (size_t i : onchip) {  // (the block path prints its own sweep counts)
