@@ -1,5 +1,6 @@
 // blockjac.cu — kernels of the block one-sided Jacobi SVD (see blockjac.cuh).
 #include <algorithm>
+#include <cstdlib>
 #include <cooperative_groups.h>
 
 #include "blockjac.cuh"
@@ -54,7 +55,18 @@ constexpr int kBjN2 = 32;    // 2b (b = 16)
 // The pair's rows are split over the S CTAs of a thread-block cluster: each CTA forms the Gram
 // of its row slice, CTA 0 sums the slices over DSMEM (fixed order) and solves, the peers read W
 // back over DSMEM and rotate their own slices of X and V.
-__global__ void __launch_bounds__(kBjThreads) bj_step_kernel(const __grid_constant__ BjStep a) {
+// One block pair of one step (the body shared by the per-step cluster kernel and the persistent
+// sweep kernel; a launch without cluster dimensions is an implicit cluster of one CTA).
+struct BjPair {
+    const cplx* Xs;
+    const cplx* Vs;
+    cplx* Xd;
+    cplx* Vd;
+    const int* dst;  // this step's slot -> next-step slot table
+    BjStat* stat;
+    int r, cp, b, inner_sweeps;
+};
+__device__ __forceinline__ void bj_pair(const BjPair& a, const int k0) {
     constexpr int n2 = kBjN2, ld = n2 + 1, half = n2 / 2;
     __shared__ double pc[half], ps[half];
     __shared__ cplx pe[half];
@@ -68,13 +80,13 @@ __global__ void __launch_bounds__(kBjThreads) bj_step_kernel(const __grid_consta
     auto sW = sG + n2;                                                            // [n2][ld]
     __shared__ int s_rot;
     __shared__ unsigned long long s_off2, s_off2_first;
-    const int pr = blockIdx.y, k0 = blockIdx.x / S, tid = threadIdx.x;
+    const int tid = threadIdx.x;
     const int r = a.r, cp = a.cp, b = a.b;
     const int xr0 = (int)((long long)r * crank / S), xr1 = (int)((long long)r * (crank + 1) / S);
     const int vr0 = (int)((long long)cp * crank / S), vr1 = (int)((long long)cp * (crank + 1) / S);
     const long long col0 = (long long)k0 * n2;  // the pair's first column (slots 2k0, 2k0+1)
-    const cplx* X = a.Xs[pr];
-    const cplx* V = a.Vs[pr];
+    const cplx* X = a.Xs;
+    const cplx* V = a.Vs;
     // stage rows [r0, r0 + kBjRows) of the pair's columns of M (zero-filled from rend on)
     auto stage = [&](const cplx* M, int r0, int rend, Chunk& dst) {
 #pragma unroll
@@ -252,8 +264,8 @@ __global__ void __launch_bounds__(kBjThreads) bj_step_kernel(const __grid_consta
     }
 
         if (tid == 0 && s_first) {
-            atomicAdd(&a.stat[pr]->rot, s_first);
-            atomicMax(&a.stat[pr]->off2, s_off2_first);
+            atomicAdd(&a.stat->rot, s_first);
+            atomicMax(&a.stat->off2, s_off2_first);
         }
     }
     cluster.sync();  // W is ready in CTA 0
@@ -279,7 +291,7 @@ __global__ void __launch_bounds__(kBjThreads) bj_step_kernel(const __grid_consta
         __syncthreads();
         const Chunk& ch = buf[(t + 1) & 1];
         const bool isx = t < nxc;
-        cplx* D = isx ? a.Xd[pr] : a.Vd[pr];
+        cplx* D = isx ? a.Xd : a.Vd;
         const int r0 = isx ? xr0 + t * kBjRows : vr0 + (t - nxc) * kBjRows;
         const int nr = min(kBjRows, (isx ? xr1 : vr1) - r0);
         if (rt * 8 < nr) {
@@ -311,6 +323,64 @@ __global__ void __launch_bounds__(kBjThreads) bj_step_kernel(const __grid_consta
             }
         }
         __syncthreads();  // (the buffer is refilled by the next iteration's prefetch)
+    }
+}
+
+
+__global__ void __launch_bounds__(kBjThreads) bj_step_kernel(const __grid_constant__ BjStep a) {
+    const int S = (int)cg::this_cluster().num_blocks();
+    const int pr = blockIdx.y;
+    const BjPair q{a.Xs[pr], a.Vs[pr], a.Xd[pr], a.Vd[pr], a.dst, a.stat[pr], a.r, a.cp, a.b, a.inner_sweeps};
+    bj_pair(q, blockIdx.x / S);
+}
+
+__device__ __forceinline__ int ld_acquire(const int* p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release(int* p, int v) {
+    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// A whole sweep in one launch.  Work items (step t, problem q, pair k) are claimed from a counter
+// in step-major order; an item of step t > 0 waits for the (at most four) items of step t-1 it
+// depends on: the two that produced its blocks, and the two that read its destination slots of
+// the ping-pong buffer it writes.  Every waited-on item was claimed earlier by a running CTA, so
+// the scheme cannot deadlock whatever the residency; steps overlap instead of meeting at a
+// grid-wide barrier per launch.
+__global__ void __launch_bounds__(kBjThreads, 3) bj_sweep_kernel(const __grid_constant__ BjSweep a) {
+    __shared__ int s_item;
+    const int per_step = a.count * a.npairs, total = per_step * a.nsteps;
+    for (;;) {
+        __syncthreads();  // (s_item is rewritten below)
+        if (threadIdx.x == 0) s_item = atomicAdd(a.counter, 1);
+        __syncthreads();
+        const int item = s_item;
+        if (item >= total) return;
+        const int t = item / per_step, rem = item % per_step, qi = rem / a.npairs, k = rem % a.npairs;
+        const int nbp = 2 * a.npairs;
+        int* done = a.done + (size_t)qi * a.nsteps * a.npairs;
+        if (t > 0 && threadIdx.x < 4) {
+            const int* dstt = a.dst + (size_t)t * nbp;
+            const int* prod = a.prod + (size_t)t * nbp;
+            const int dep = threadIdx.x < 2 ? prod[2 * k + threadIdx.x] : dstt[2 * k + threadIdx.x - 2] >> 1;
+            const int* f = done + (size_t)(t - 1) * a.npairs + dep;
+            long long spins = 0;
+            while (ld_acquire(f) < a.epoch) {
+                __nanosleep(64);
+                if (++spins > (1ll << 26)) __trap();  // (a broken dependency: fail, never hang)
+            }
+        }
+        __syncthreads();
+        const BjPair q{a.X[t & 1][qi], a.V[t & 1][qi], a.X[(t + 1) & 1][qi], a.V[(t + 1) & 1][qi],
+                       a.dst + (size_t)t * nbp, a.stat[qi], a.r, a.cp, a.b, a.inner_sweeps};
+        bj_pair(q, k);
+        __syncthreads();  // every write of the item precedes the release
+        if (threadIdx.x == 0) {
+            __threadfence();
+            st_release(done + (size_t)t * a.npairs + k, a.epoch);
+        }
     }
 }
 
@@ -378,10 +448,8 @@ cudaError_t bj_step(const BjStep& a, cudaStream_t s) {
     cudaError_t e = cudaFuncSetAttribute(bj_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     // row slices per pair: as many as keep every CTA resident in one wave (3 per SM at this
-    // shared-memory size), at most 8 (portable cluster), at least one 64-row chunk per slice
-    const long long pairs = (long long)a.npairs * a.count;
-    int S = 1;
-    while (S < 8 && pairs * (2 * S) <= 3LL * 148 && (a.r / (2 * S)) >= 64) S *= 2;
+    // shared-memory size), at most 8 (portable cluster), at least 64 rows per slice
+    const int S = bj_slices(a.npairs * a.count, a.r);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(a.npairs * S, a.count);
     cfg.blockDim = dim3(kBjThreads);
@@ -396,6 +464,34 @@ cudaError_t bj_step(const BjStep& a, cudaStream_t s) {
     cfg.numAttrs = 1;
     e = cudaLaunchKernelEx(&cfg, bj_step_kernel, a);
     if (e != cudaSuccess) return e;
+    return cudaGetLastError();
+}
+
+int bj_slices(int pairs, int r) {
+    int S = 1;
+    while (S < 8 && (long long)pairs * (2 * S) <= 3LL * 148 && (r / (2 * S)) >= 64) S *= 2;
+    static const int env_s = [] {  // (RRSVD_B200_BJ_S: force the row-slice count, for tuning)
+        const char* e = std::getenv("RRSVD_B200_BJ_S");
+        return e ? std::atoi(e) : 0;
+    }();
+    if (env_s == 1 || env_s == 2 || env_s == 4 || env_s == 8) S = std::min(env_s, std::max(1, r / 32));
+    return S;
+}
+
+cudaError_t bj_sweep(const BjSweep& a, cudaStream_t s) {
+    if (a.count == 0) return cudaSuccess;
+    if (2 * a.b != kBjN2) return cudaErrorInvalidValue;
+    constexpr size_t smem = sizeof(cplx) * (2 * kBjRows * (kBjN2 + 1) + 2 * kBjN2 * (kBjN2 + 1));
+    cudaError_t e = cudaFuncSetAttribute(bj_sweep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    int per_sm = 0, dev = 0, nsm = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bj_sweep_kernel, kBjThreads, smem);
+    if (e != cudaSuccess) return e;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    const long long total = (long long)a.count * a.npairs * a.nsteps;
+    const int grid = (int)std::min<long long>(total, (long long)std::max(1, per_sm) * nsm);
+    bj_sweep_kernel<<<grid, kBjThreads, smem, s>>>(a);
     return cudaGetLastError();
 }
 

@@ -54,6 +54,24 @@ struct BjStep {
 };
 cudaError_t bj_step(const BjStep& a, cudaStream_t s);
 
+// Row slices (cluster size) bj_step uses for this many block pairs of r rows; 1 = the
+// persistent sweep kernel applies.
+int bj_slices(int pairs, int r);
+
+// One whole sweep (all nsteps tournament steps) in one launch of single-CTA pairs.
+struct BjSweep {
+    int count, r, cp, b, npairs, nsteps, inner_sweeps;
+    int epoch;                      // > every value already in done[] (the sweep number + 1)
+    cplx* X[2][kBjMaxProblems];     // step t reads X[t & 1], writes X[(t + 1) & 1]
+    cplx* V[2][kBjMaxProblems];
+    BjStat* stat[kBjMaxProblems];
+    const int* dst;                 // device [nsteps][2 npairs]: slot at step t -> slot at step t+1
+    const int* prod;                // device [nsteps][2 npairs]: pair of step t-1 that wrote slot (row t)
+    int* done;                      // device [count][nsteps][npairs]: epoch of the item's completion
+    int* counter;                   // device work counter, zero at launch
+};
+cudaError_t bj_sweep(const BjSweep& a, cudaStream_t s);
+
 struct BjFinish {
     int count, r, c, cp, b;
     const cplx* X[kBjMaxProblems];

@@ -338,6 +338,14 @@ struct SmallSvdSpec {
 // Block one-sided Jacobi (blockjac.cuh) for same-shaped problems: the tournament schedule is
 // host-side bookkeeping; one fused launch per step for all pairs of all problems; one
 // 4-byte-per-problem D2H per sweep for the convergence test.
+bool bj_per_step() {  // RRSVD_B200_BJ_PER_STEP=1: one launch per tournament step (A/B timing)
+    static const bool v = [] {
+        const char* e = std::getenv("RRSVD_B200_BJ_PER_STEP");
+        return e != nullptr && std::atoi(e) != 0;
+    }();
+    return v;
+}
+
 int block_jacobi_min_c() {  // above this the block method is used (RRSVD_B200_BJ_MIN_C overrides)
     // measured: the cluster kernel wins for l = 74 (C1: 2.6 vs 3.0 ms) and the batched 110^2 of
     // C3 (162 vs 186 ms per step); the DMMA block method wins for C2's batched 256^2 (5.25 vs
@@ -401,6 +409,27 @@ void block_jacobi_group(rrsvd_b200_ctx* c, const std::vector<const SmallSvdSpec*
         for (int pos = 0; pos < nbp; ++pos) dst[t][pos] = where[plt[pos]];
     }
     auto* hstat = static_cast<BjStat*>(pinned_scratch(c, np * sizeof(BjStat)));
+    // single-CTA pairs: one persistent launch per sweep (bj_sweep), with device copies of the
+    // whole schedule and per-item completion flags
+    const int nsteps = nbp - 1;
+    const bool persistent = bj_slices(npairs * np, r) == 1 && !bj_per_step();
+    int *d_dst = nullptr, *d_prod = nullptr, *d_done = nullptr, *d_counter = nullptr;
+    if (persistent) {
+        std::vector<int> hd((size_t)nsteps * nbp), hp((size_t)nsteps * nbp, 0);
+        for (int t = 0; t < nsteps; ++t)
+            for (int pos = 0; pos < nbp; ++pos) {
+                hd[(size_t)t * nbp + pos] = dst[t][pos];
+                if (t + 1 < nsteps) hp[(size_t)(t + 1) * nbp + dst[t][pos]] = pos >> 1;
+            }
+        d_dst = ws_get<int>(c, hd.size());
+        d_prod = ws_get<int>(c, hp.size());
+        d_done = ws_get<int>(c, (size_t)np * nsteps * npairs);
+        d_counter = ws_get<int>(c, 1);
+        check_cuda(c, cudaMemcpyAsync(d_dst, hd.data(), hd.size() * sizeof(int), cudaMemcpyHostToDevice, c->stream), "H2D");
+        check_cuda(c, cudaMemcpyAsync(d_prod, hp.data(), hp.size() * sizeof(int), cudaMemcpyHostToDevice, c->stream), "H2D");
+        check_cuda(c, cudaMemsetAsync(d_done, 0, (size_t)np * nsteps * npairs * sizeof(int), c->stream), "memset");
+        check_cuda(c, cudaStreamSynchronize(c->stream), "sync");  // (the host vectors go out of scope)
+    }
     // problems drop out of the launches once a sweep of theirs rotates nothing (the batch would
     // otherwise run every problem for the slowest one's sweeps); each keeps its own buffers
     std::vector<int> active(np);
@@ -411,7 +440,27 @@ void block_jacobi_group(rrsvd_b200_ctx* c, const std::vector<const SmallSvdSpec*
     int sweep = 0;
     for (; sweep < 60; ++sweep) {
         check_cuda(c, cudaMemsetAsync(stat, 0, np * sizeof(BjStat), c->stream), "memset");
-        for (int t = 0; t < nbp - 1; ++t) {
+        if (persistent) {
+            BjSweep sw{};
+            sw.count = (int)active.size(); sw.r = r; sw.cp = cp; sw.b = b; sw.npairs = npairs; sw.nsteps = nsteps;
+            sw.inner_sweeps = bj_inner_sweeps();
+            sw.epoch = sweep + 1;
+            for (size_t q = 0; q < active.size(); ++q) {
+                const int p = active[q];
+                sw.X[0][q] = X1[p]; sw.X[1][q] = X2[p]; sw.V[0][q] = V1[p]; sw.V[1][q] = V2[p];
+                sw.stat[q] = stat + p;
+            }
+            sw.dst = d_dst; sw.prod = d_prod; sw.done = d_done; sw.counter = d_counter;
+            check_cuda(c, cudaMemsetAsync(d_counter, 0, sizeof(int), c->stream), "memset");
+            check_cuda(c, bj_sweep(sw, c->stream), "bj_sweep");
+            c->launches++;
+            if (nsteps & 1)
+                for (int p : active) {
+                    std::swap(X1[p], X2[p]);
+                    std::swap(V1[p], V2[p]);
+                }
+        }
+        for (int t = 0; t < (persistent ? 0 : nbp - 1); ++t) {
             BjStep st{};
             st.count = (int)active.size(); st.r = r; st.cp = cp; st.b = b; st.npairs = npairs;
             st.inner_sweeps = bj_inner_sweeps();
