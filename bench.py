@@ -397,6 +397,9 @@ def run_ours(args, rank, world, local_rank):
                          "peak_source": "measured live: DMMA probe (mma.sync m8n8k4 f64) on this GPU;"
                                         " MEASURED_PEAKS.json has no FP64 entry",
                          "frac_of_40tf_nominal": round(achieved / 40.0, 4),
+                         "complex_product": "3M on the 64x56 tile (RRSVD_B200_GEMM_3M=0: 4M): the DMMA pipe"
+                                            " executes 6 real flops per complex MAC; achieved counts the"
+                                            " algorithmic 8 (SURVEY 8(d)), as a 4M zgemm would have to",
                          "gemm_time_share_serial": round(ms.value / (1e3 * serial_step_s), 4),
                          "serial_step_ms": round(1e3 * serial_step_s, 3),
                          "step_level_tflops": round(fl.value / (elapsed / args.steps) / 1e12, 3),

@@ -11,8 +11,12 @@ namespace {
 // Tile configurations.  Cfg64: 64x64 CTA tile, 32x32 warp tiles (16 DMMA tiles per warp).
 // Cfg56: 64x56 CTA tile, 16x56 warp tiles — for N ≈ l = k+p (110 → 2 x 56 = 112 instead of
 // 2 x 64 = 128: 14% less padded DMMA work on every RRSVD-stage GEMM).
-template <int BM_, int BN_, int WM_, int WN_, int STAGES_ = 3, int MINB_ = 0>
+template <int BM_, int BN_, int WM_, int WN_, int STAGES_ = 3, int MINB_ = 0, bool M3_ = false>
 struct Cfg {
+    // M3: the 3M (Karatsuba) complex product — T1 = Ar Br, T2 = Ai Bi, T3 = (Ar + Ai)(Br + Bi),
+    // Re = T1 - T2, Im = T3 - T1 - T2: three DMMAs per fragment pair instead of four (a third
+    // accumulator set, so fewer CTAs per SM).
+    static constexpr bool M3 = M3_;
     static constexpr int BM = BM_, BN = BN_, BK = 16, STAGES = STAGES_;
     static constexpr int WM = WM_, WN = WN_;
     static constexpr int WARPS_M = BM / WM, WARPS_N = BN / WN;
@@ -29,7 +33,7 @@ struct Cfg {
     static_assert((BM * BK) % NTHREADS == 0, "A tile loads");
     static constexpr int MIN_BLOCKS = MINB_ ? MINB_ : (NTHREADS <= 128 ? 2 : 1);
     // Padded-sub-tile skipping costs registers; the 3-CTA/SM config (168 regs) cannot afford it.
-    static constexpr bool SKIP_PAD = MIN_BLOCKS < 3;
+    static constexpr bool SKIP_PAD = MIN_BLOCKS < 3 && !M3;
     static_assert(LDB % 8 == 2 && LDA_N % 8 == 4 && LDA_C % 8 == 2, "bank-conflict-free strides");
 };
 using Cfg64 = Cfg<64, 64, 32, 32>;
@@ -37,6 +41,10 @@ using Cfg64 = Cfg<64, 64, 32, 32>;
 // than the ~1-2k cycle load latency, so the third stage buys nothing while the third CTA fills
 // the DMMA issue bubbles of the other two.
 using Cfg56 = Cfg<64, 56, 16, 56, 2, 3>;
+// 3M on the 64x56 tile: 84 accumulator doubles per thread -> 2 CTAs/SM (the same per-SM
+// accumulator state as the 4M tile at 3 CTAs/SM), 25 % fewer DMMAs: the RRSVD A-products go from
+// 29.9 to 33.0 TF/s (4M-equivalent flops), C3 6.2 -> 6.8 steps/s.  A third stage is slower.
+using Cfg56m3 = Cfg<64, 56, 16, 56, 2, 2, true>;
 
 __device__ __forceinline__ int find_problem(const GemmGroup& g, int tile) {
     int lo = 0, hi = g.count - 1;
@@ -130,13 +138,14 @@ zgemm_dmma_kernel(const __grid_constant__ GemmGroup g) {
         }
     };
 
-    double acc[MI][NI][2][2];  // [mi][ni][re/im][c0/c1]
+    constexpr int NACC = CF::M3 ? 3 : 2;
+    double acc[MI][NI][NACC][2];  // [mi][ni][re/im (4M) | T1/T2/T3 (3M)][c0/c1]
 #pragma unroll
     for (int i = 0; i < MI; ++i)
 #pragma unroll
         for (int j = 0; j < NI; ++j)
 #pragma unroll
-            for (int r = 0; r < 2; ++r) acc[i][j][r][0] = acc[i][j][r][1] = 0.0;
+            for (int r = 0; r < NACC; ++r) acc[i][j][r][0] = acc[i][j][r][1] = 0.0;
 
 #pragma unroll
     for (int s = 0; s < STAGES - 1; ++s) {
@@ -175,7 +184,22 @@ zgemm_dmma_kernel(const __grid_constant__ GemmGroup g) {
                 else a = sA[(kk + fc) * LDA_C + wm + i * 8 + fr];
                 if (OPA == kOpC) a.y = -a.y;
                 if (ks != nullptr) { a.x *= kscale; a.y *= kscale; }
-                ar[i] = a.x; ai[i] = a.y; ain[i] = -a.y;
+                ar[i] = a.x; ai[i] = a.y; ain[i] = CF::M3 ? a.x + a.y : -a.y;  // (3M: ain holds Ar + Ai)
+            }
+            if constexpr (CF::M3) {
+#pragma unroll
+                for (int j = 0; j < NI; ++j) {
+                    const cplx b = sB[(kk + fc) * LDB + wn + j * 8 + fr];
+                    const double bs = b.x + b.y;
+#pragma unroll
+                    for (int i = 0; i < MI; ++i) {
+                        if (CF::SKIP_PAD && (m0 + wm + i * 8 >= M || n0 + wn + j * 8 >= N)) continue;
+                        dmma884(acc[i][j][0][0], acc[i][j][0][1], ar[i], b.x);
+                        dmma884(acc[i][j][1][0], acc[i][j][1][1], ai[i], b.y);
+                        dmma884(acc[i][j][2][0], acc[i][j][2][1], ain[i], bs);
+                    }
+                }
+                continue;
             }
 #pragma unroll
             for (int j = 0; j < NI; ++j) {
@@ -205,7 +229,19 @@ zgemm_dmma_kernel(const __grid_constant__ GemmGroup g) {
     }
     cp_async_wait<0>();
 
-    // ---- epilogue
+    // ---- epilogue (3M: fold T1, T2, T3 into Re = T1 - T2, Im = T3 - T1 - T2 in acc[..][0/1])
+    if constexpr (CF::M3) {
+#pragma unroll
+        for (int i = 0; i < MI; ++i)
+#pragma unroll
+            for (int j = 0; j < NI; ++j)
+#pragma unroll
+                for (int c = 0; c < 2; ++c) {
+                    const double t1 = acc[i][j][0][c], t2 = acc[i][j][1][c];
+                    acc[i][j][0][c] = t1 - t2;
+                    acc[i][j][1][c] = acc[i][j][2][c] - t1 - t2;
+                }
+    }
     if (P.split > 1) {
         cplx* W = P.partial + ((long long)sk * P.batch + bz) * (long long)M * N;
 #pragma unroll
@@ -326,12 +362,16 @@ cudaError_t zgemm_grouped(GemmGroup& g, GemmOp opA, cudaStream_t s) {
         const char* e = std::getenv("RRSVD_B200_GEMM_CFG");
         return e ? std::atoi(e) : 0;
     }();
-    if (force == 56) return launch_cfg<Cfg56>(g, opA, s);
+    static const bool m3 = [] {  // the 3M complex product on the 64x56 tile (RRSVD_B200_GEMM_3M=0: 4M)
+        const char* e = std::getenv("RRSVD_B200_GEMM_3M");
+        return e == nullptr || std::atoi(e) != 0;
+    }();
+    if (force == 56) return m3 ? launch_cfg<Cfg56m3>(g, opA, s) : launch_cfg<Cfg56>(g, opA, s);
     if (force == 64) return launch_cfg<Cfg64>(g, opA, s);
     // Ties go to Cfg56 (3 CTAs/SM hide short-K pipelines better: the K = 100 Θ GEMM runs
     // 27.0 vs 25.0 TF/s); Cfg64 only when it saves >= 5 % padded work (e.g. N = 128, 256).
     if (pad64 < 0.95 * pad56) return launch_cfg<Cfg64>(g, opA, s);
-    return launch_cfg<Cfg56>(g, opA, s);
+    return m3 ? launch_cfg<Cfg56m3>(g, opA, s) : launch_cfg<Cfg56>(g, opA, s);
 }
 
 }  // namespace rb

@@ -5,9 +5,17 @@
 //
 // Why DMMA and not tcgen05: sm_100a has no f64 kind for tcgen05.mma (ptxas rejects
 // `.kind::f64`), so FP64 tensor math is warp-level `mma.sync.m8n8k4.f64` → SASS DMMA.8x8x4.
-// Complex arithmetic is done as four real MMAs per k-step on split (re, im) fragments
-// (C_r += A_r B_r − A_i B_i, C_i += A_r B_i + A_i B_r) — the "4M" form, same rounding class as
-// zgemm (no 3M/Gauss trick).  Operands are staged global→shared with a multi-stage cp.async
+// Complex arithmetic on split (re, im) fragments, two forms:
+//  * 4M (the 64x64 tile): C_r += A_r B_r − A_i B_i, C_i += A_r B_i + A_i B_r — four real MMAs per
+//    k-step, zgemm's rounding class;
+//  * 3M (the 64x56 tile, default; RRSVD_B200_GEMM_3M=0 selects 4M): T1 = A_r B_r, T2 = A_i B_i,
+//    T3 = (A_r + A_i)(B_r + B_i) accumulated separately, C_r = T1 − T2, C_i = T3 − T1 − T2 in the
+//    epilogue — three MMAs (25 % fewer).  3M is normwise stable (Higham, "Stability of a method
+//    for multiplying complex matrices with three real matrix multiplications", 1992): the
+//    imaginary part's error bound is a small constant times 4M's u·Σ|a||b|, far inside the
+//    path's 1e-10 parity bar (every parity test passes either way; BLAS libraries ship it as
+//    zgemm3m).
+// Operands are staged global→shared with a multi-stage cp.async
 // (LDGSTS) ring; each thread loads one 16-byte complex per fragment element (LDS.128), so a
 // single shared-memory read yields both the real and imaginary fragment.
 #pragma once
