@@ -187,18 +187,27 @@ zgemm_dmma_kernel(const __grid_constant__ GemmGroup g) {
                 ar[i] = a.x; ai[i] = a.y; ain[i] = CF::M3 ? a.x + a.y : -a.y;  // (3M: ain holds Ar + Ai)
             }
             if constexpr (CF::M3) {
+                // all B fragments and their sums first, then every T1/T2 product, then the T3
+                // products: the (Ar + Ai), (Br + Bi) additions never stall a DMMA issue
+                double bs[NI];
 #pragma unroll
                 for (int j = 0; j < NI; ++j) {
                     const cplx b = sB[(kk + fc) * LDB + wn + j * 8 + fr];
-                    const double bs = b.x + b.y;
+                    br[j] = b.x; bi[j] = b.y;
+                }
+#pragma unroll
+                for (int j = 0; j < NI; ++j) bs[j] = br[j] + bi[j];
+#pragma unroll
+                for (int j = 0; j < NI; ++j)
 #pragma unroll
                     for (int i = 0; i < MI; ++i) {
-                        if (CF::SKIP_PAD && (m0 + wm + i * 8 >= M || n0 + wn + j * 8 >= N)) continue;
-                        dmma884(acc[i][j][0][0], acc[i][j][0][1], ar[i], b.x);
-                        dmma884(acc[i][j][1][0], acc[i][j][1][1], ai[i], b.y);
-                        dmma884(acc[i][j][2][0], acc[i][j][2][1], ain[i], bs);
+                        dmma884(acc[i][j][0][0], acc[i][j][0][1], ar[i], br[j]);
+                        dmma884(acc[i][j][1][0], acc[i][j][1][1], ai[i], bi[j]);
                     }
-                }
+#pragma unroll
+                for (int j = 0; j < NI; ++j)
+#pragma unroll
+                    for (int i = 0; i < MI; ++i) dmma884(acc[i][j][2][0], acc[i][j][2][1], ain[i], bs[j]);
                 continue;
             }
 #pragma unroll
