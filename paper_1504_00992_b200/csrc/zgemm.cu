@@ -55,7 +55,7 @@ __device__ __forceinline__ int find_problem(const GemmGroup& g, int tile) {
     return lo;
 }
 
-template <class CF, int OPA>
+template <class CF, int OPA, bool KS>  // KS: some problem of the group has a k-scale (P.ks)
 __global__ void __launch_bounds__(CF::NTHREADS, CF::MIN_BLOCKS)
 zgemm_dmma_kernel(const __grid_constant__ GemmGroup g) {
     constexpr int BM = CF::BM, BN = CF::BN, BK = CF::BK, STAGES = CF::STAGES;
@@ -154,7 +154,7 @@ zgemm_dmma_kernel(const __grid_constant__ GemmGroup g) {
     }
 
     const int fr = lane >> 2, fc = lane & 3;
-    const double* ks = P.ks;
+    const double* ks = KS ? P.ks : nullptr;  // (without KS no multiply by 1.0 is compiled in)
 
     for (int kt = 0; kt < ktiles; ++kt) {
         cp_async_wait<STAGES - 2>();
@@ -339,14 +339,23 @@ cudaError_t launch_cfg(GemmGroup& g, GemmOp opA, cudaStream_t s) {
     }
     g.total_tiles = total;
     if (total == 0) return cudaSuccess;
+    bool any_ks = false;
+    for (int i = 0; i < g.count; ++i) any_ks |= g.p[i].ks != nullptr;
     static bool configured = false;
     if (!configured) {
-        cudaFuncSetAttribute(zgemm_dmma_kernel<CF, kOpN>, cudaFuncAttributeMaxDynamicSharedMemorySize, CF::SMEM_BYTES);
-        cudaFuncSetAttribute(zgemm_dmma_kernel<CF, kOpC>, cudaFuncAttributeMaxDynamicSharedMemorySize, CF::SMEM_BYTES);
+        cudaFuncSetAttribute(zgemm_dmma_kernel<CF, kOpN, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, CF::SMEM_BYTES);
+        cudaFuncSetAttribute(zgemm_dmma_kernel<CF, kOpC, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, CF::SMEM_BYTES);
+        cudaFuncSetAttribute(zgemm_dmma_kernel<CF, kOpN, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, CF::SMEM_BYTES);
+        cudaFuncSetAttribute(zgemm_dmma_kernel<CF, kOpC, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, CF::SMEM_BYTES);
         configured = true;
     }
-    if (opA == kOpN) zgemm_dmma_kernel<CF, kOpN><<<total, CF::NTHREADS, CF::SMEM_BYTES, s>>>(g);
-    else zgemm_dmma_kernel<CF, kOpC><<<total, CF::NTHREADS, CF::SMEM_BYTES, s>>>(g);
+    if (opA == kOpN) {
+        if (any_ks) zgemm_dmma_kernel<CF, kOpN, true><<<total, CF::NTHREADS, CF::SMEM_BYTES, s>>>(g);
+        else zgemm_dmma_kernel<CF, kOpN, false><<<total, CF::NTHREADS, CF::SMEM_BYTES, s>>>(g);
+    } else {
+        if (any_ks) zgemm_dmma_kernel<CF, kOpC, true><<<total, CF::NTHREADS, CF::SMEM_BYTES, s>>>(g);
+        else zgemm_dmma_kernel<CF, kOpC, false><<<total, CF::NTHREADS, CF::SMEM_BYTES, s>>>(g);
+    }
     if (any_split) splitk_reduce_kernel<<<dim3(2 * kNumSMs, g.count), 256, 0, s>>>(g);
     return cudaGetLastError();
 }
