@@ -45,6 +45,8 @@ using Cfg56 = Cfg<64, 56, 16, 56, 2, 3>;
 // accumulator state as the 4M tile at 3 CTAs/SM), 25 % fewer DMMAs: the RRSVD A-products go from
 // 29.9 to 33.0 TF/s (4M-equivalent flops), C3 6.2 -> 6.8 steps/s.  A third stage is slower.
 using Cfg56m3 = Cfg<64, 56, 16, 56, 2, 2, true>;
+// 3M on the 64x64 tile: eight 16x32 warp tiles, one CTA/SM (the same 8 warps/SM as the 4M tile)
+using Cfg64m3 = Cfg<64, 64, 16, 32, 2, 1, true>;
 
 __device__ __forceinline__ int find_problem(const GemmGroup& g, int tile) {
     int lo = 0, hi = g.count - 1;
@@ -385,10 +387,14 @@ cudaError_t zgemm_grouped(GemmGroup& g, GemmOp opA, cudaStream_t s) {
         return e == nullptr || std::atoi(e) != 0;
     }();
     if (force == 56) return m3 ? launch_cfg<Cfg56m3>(g, opA, s) : launch_cfg<Cfg56>(g, opA, s);
-    if (force == 64) return launch_cfg<Cfg64>(g, opA, s);
+    if (force == 64) return m3 ? launch_cfg<Cfg64m3>(g, opA, s) : launch_cfg<Cfg64>(g, opA, s);
     // Ties go to Cfg56 (3 CTAs/SM hide short-K pipelines better: the K = 100 Θ GEMM runs
     // 27.0 vs 25.0 TF/s); Cfg64 only when it saves >= 5 % padded work (e.g. N = 128, 256).
-    if (pad64 < 0.95 * pad56) return launch_cfg<Cfg64>(g, opA, s);
+    static const bool m3_64 = [] {  // RRSVD_B200_GEMM_3M64=1: 3M on the 64x64 tile too (experiment)
+        const char* e = std::getenv("RRSVD_B200_GEMM_3M64");
+        return e != nullptr && std::atoi(e) != 0;
+    }();
+    if (pad64 < 0.95 * pad56) return m3 && m3_64 ? launch_cfg<Cfg64m3>(g, opA, s) : launch_cfg<Cfg64>(g, opA, s);
     return m3 ? launch_cfg<Cfg56m3>(g, opA, s) : launch_cfg<Cfg56>(g, opA, s);
 }
 
