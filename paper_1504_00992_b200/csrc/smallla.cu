@@ -319,7 +319,7 @@ __device__ __forceinline__ int circle(int i, int t, int n) {  // round-robin slo
 // The parameters use rsqrt/rcp (a few ulps): the rotation only has to be unitary to working
 // precision, the convergence test is exact.
 __device__ __forceinline__ bool hestenes_rotate(cplx* __restrict__ xp, cplx* __restrict__ xq, int r, int ld,
-                                                int lane, double tol) {
+                                                int lane, double tol, double& off2) {
     double a0 = 0.0, b0 = 0.0, a1 = 0.0, b1 = 0.0;
     cplx g0 = mk(0.0, 0.0), g1 = mk(0.0, 0.0);
     int rr = lane;
@@ -343,6 +343,7 @@ __device__ __forceinline__ bool hestenes_rotate(cplx* __restrict__ xp, cplx* __r
     }
     const double g2 = g.x * g.x + g.y * g.y;
     if (!(a > 0.0) || !(bb > 0.0) || !(g2 > tol * tol * a * bb)) return false;
+    off2 = fmax(off2, g2 / (a * bb));
     const double rg = rsqrt(g2);  // 1/|g|
     const cplx e = mk(g.x * rg, -g.y * rg);
     const double zeta = 0.5 * (bb - a) * rg;
@@ -377,17 +378,23 @@ __global__ void __launch_bounds__(JAC_CL_THREADS) jacobi_kernel(const __grid_con
     const int bs = (c + nblk - 1) / nblk;
     cplx* col = reinterpret_cast<cplx*>(sm);  // [2bs][ld]: block A columns, then block B
     __shared__ int cnt[2];
+    __shared__ unsigned long long offm[2];  // max rotated |g|^2/(a b) of the sweep (ordered bits)
     __shared__ int s_rot;
     cplx* W = b.W[p];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const double tol = sqrt((double)max(r, 1)) * kEps;
-    if (tid == 0) { cnt[0] = cnt[1] = 0; }
+    if (tid == 0) { cnt[0] = cnt[1] = 0; offm[0] = offm[1] = 0ull; }
     cluster.sync();
+    // noise level (LAPACK zgesvj's test, as the block Jacobi): a sweep whose every rotated pair
+    // had |g| <= sqrt(c) tol sqrt(a b) leaves only rounding noise, and another sweep would only
+    // rotate noise again
+    const double noise2 = (double)c * tol * tol;
 
     int sweep = 0;
     for (; sweep < kMaxSweeps; ++sweep) {
         int myrot = 0;
+        double myoff2 = 0.0;
         for (int t = 0; t < nblk - 1; ++t) {
             const int blkA = circle(rank, t, nblk), blkB = circle(nblk - 1 - rank, t, nblk);
             auto gcol = [&](int lc) { return lc < bs ? blkA * bs + lc : blkB * bs + (lc - bs); };
@@ -410,7 +417,7 @@ __global__ void __launch_bounds__(JAC_CL_THREADS) jacobi_kernel(const __grid_con
                         const int lp = circle(k, ir, bp), lq = circle(bp - 1 - k, ir, bp);
                         if (lp < bs && lq < bs && gcol(blk * bs + lp) < c && gcol(blk * bs + lq) < c)
                             myrot += hestenes_rotate(col + (blk * bs + lp) * ld, col + (blk * bs + lq) * ld, r, ld,
-                                                     lane, tol);
+                                                     lane, tol, myoff2);
                     }
                     __syncthreads();
                 }
@@ -419,12 +426,16 @@ __global__ void __launch_bounds__(JAC_CL_THREADS) jacobi_kernel(const __grid_con
                 if (warp < bs) {
                     const int lp = warp, lq = bs + (warp + j) % bs;
                     if (gcol(lp) < c && gcol(lq) < c)
-                        myrot += hestenes_rotate(col + lp * ld, col + lq * ld, r, ld, lane, tol);
+                        myrot += hestenes_rotate(col + lp * ld, col + lq * ld, r, ld, lane, tol, myoff2);
                 }
                 __syncthreads();
             }
-            if (lane == 0 && myrot) atomicAdd(&s_rot, myrot);
+            if (lane == 0 && myrot) {
+                atomicAdd(&s_rot, myrot);
+                atomicMax(&offm[sweep & 1], (unsigned long long)__double_as_longlong(myoff2));
+            }
             myrot = 0;
+            myoff2 = 0.0;
             __syncthreads();
             if (tid == 0) cnt[sweep & 1] += s_rot;
             for (int lc = 0; lc < 2 * bs; ++lc) {
@@ -436,15 +447,18 @@ __global__ void __launch_bounds__(JAC_CL_THREADS) jacobi_kernel(const __grid_con
             __threadfence();
             cluster.sync();
             // every peer is past its end-of-previous-sweep read of our counters: recycle the slot
-            if (t == 0 && tid == 0) cnt[(sweep + 1) & 1] = 0;
+            if (t == 0 && tid == 0) { cnt[(sweep + 1) & 1] = 0; offm[(sweep + 1) & 1] = 0ull; }
         }
         // convergence: sum of all CTAs' rotation counts of this sweep (read through DSMEM)
         int total = 0;
+        double worst2 = 0.0;
         for (int q = 0; q < cs; ++q) {
             const int* peer = cluster.map_shared_rank(cnt, q);
+            const unsigned long long* poff = cluster.map_shared_rank(offm, q);
             total += peer[sweep & 1];
+            worst2 = fmax(worst2, __longlong_as_double((long long)poff[sweep & 1]));
         }
-        if (total == 0) break;
+        if (total == 0 || worst2 <= noise2) break;
     }
     cluster.sync();  // peers may still read our counters
     if (rank == 0 && tid == 0 && b.sweeps[p] != nullptr) *b.sweeps[p] = sweep + 1;
