@@ -636,7 +636,8 @@ def run_reference(args, rank, world):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=None,
+                    help="timed steps (default 10; 1 for c3det, whose steps take ~40 s)")
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="c3", choices=["c3", "c3p100", "c3det", "c2", "c5", "c4"],
@@ -645,6 +646,8 @@ def main():
     ap.add_argument("--force-partition", action="store_true",
                     help="use the chain-block partition driver even on one GPU (smoke test of the N>1 path)")
     args = ap.parse_args()
+    if args.steps is None:
+        args.steps = 1 if args.workload == "c3det" else 10
     if args.warmup < 3:
         args.warmup = 3
     rank = int(os.environ.get("RANK", 0))
