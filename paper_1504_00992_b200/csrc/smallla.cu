@@ -464,18 +464,38 @@ __global__ void __launch_bounds__(JAC_CL_THREADS) jacobi_kernel(const __grid_con
     if (rank == 0 && tid == 0 && b.sweeps[p] != nullptr) *b.sweeps[p] = sweep + 1;
 }
 
-__global__ void __launch_bounds__(256) colperm_rank_kernel(const __grid_constant__ ColPermBatch b) {
+constexpr int kColPermThreads = 512;
+__global__ void __launch_bounds__(kColPermThreads) colperm_rank_kernel(const __grid_constant__ ColPermBatch b) {
     extern __shared__ __align__(16) unsigned char sm[];
     const int p = blockIdx.x, r = b.r[p], c = b.c[p];
     double* nrm = reinterpret_cast<double*>(sm);
+    __shared__ double part[kColPermThreads];
     const cplx* X = b.X[p];
-    for (int j = threadIdx.x; j < c; j += 256) {
-        double a = 0.0;
-        for (int i = 0; i < r; ++i) a += cabs2(X[(long long)i * c + j]);
-        nrm[j] = a;
+    // column norms: cpp consecutive columns per pass (coalesced rows), tpc threads per column over
+    // interleaved rows, two accumulators each; partials summed in a fixed order (deterministic)
+    const int cpp = min(c, kColPermThreads), tpc = kColPermThreads / cpp;
+    const int jl = threadIdx.x % cpp, q = threadIdx.x / cpp;
+    for (int j0 = 0; j0 < c; j0 += cpp) {
+        const int j = j0 + jl;
+        double a0 = 0.0, a1 = 0.0;
+        if (q < tpc && j < c) {
+            int i = q;
+            for (; i + tpc < r; i += 2 * tpc) {
+                a0 += cabs2(X[(long long)i * c + j]);
+                a1 += cabs2(X[(long long)(i + tpc) * c + j]);
+            }
+            if (i < r) a0 += cabs2(X[(long long)i * c + j]);
+        }
+        part[threadIdx.x] = a0 + a1;
+        __syncthreads();
+        if (q == 0 && j < c) {
+            double a = 0.0;
+            for (int t = 0; t < tpc; ++t) a += part[t * cpp + jl];
+            nrm[j] = a;
+        }
+        __syncthreads();
     }
-    __syncthreads();
-    for (int j = threadIdx.x; j < c; j += 256) {
+    for (int j = threadIdx.x; j < c; j += kColPermThreads) {
         const double v = nrm[j];
         int rk = 0;
         for (int t = 0; t < c; ++t) rk += (nrm[t] > v) || (nrm[t] == v && t < j);
@@ -684,7 +704,7 @@ cudaError_t colperm_sort_gather(const ColPermBatch& b, int max_c, cudaStream_t s
     const size_t smem = (size_t)max_c * sizeof(double);
     cudaError_t e = cudaFuncSetAttribute(colperm_rank_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    colperm_rank_kernel<<<b.count, 256, smem, s>>>(b);
+    colperm_rank_kernel<<<b.count, kColPermThreads, smem, s>>>(b);
     colperm_gather_kernel<<<dim3(2 * kNumSMs, b.count), 256, 0, s>>>(b);
     return cudaGetLastError();
 }
