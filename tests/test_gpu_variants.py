@@ -1,0 +1,87 @@
+"""The kernel variants behind the environment switches, each in its own process
+(the switches are read once per process): every variant must meet the same parity bar as the
+default, so an A/B switch can never hide a wrong result.
+
+  * zgemm: 3M (default on the 64x56 tile) vs 4M, and 3M on the 64x64 tile — vs numpy, the
+    reference's cblas_zgemm contract (linalg.cpp:20-40);
+  * block Jacobi: the persistent sweep kernel (forced with RRSVD_B200_BJ_S=1) vs one launch per
+    tournament step — singular values vs LAPACK (the reference's svd_full, linalg.cpp:67-88).
+"""
+import json
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+GEMM_SCRIPT = r"""
+import json, sys
+import numpy as np
+sys.path.insert(0, %(root)r)
+import paper_1504_00992_b200 as P
+rng = np.random.default_rng(5)
+out = {}
+for (m, k, n, adj) in [(2000, 2000, 110, False), (2000, 1500, 110, True), (400, 300, 256, False), (333, 100, 2000, False)]:
+    a = rng.standard_normal((k, m) if adj else (m, k)) + 1j * rng.standard_normal((k, m) if adj else (m, k))
+    b = rng.standard_normal((k, n)) + 1j * rng.standard_normal((k, n))
+    c = P.gemm(a, adj, b)
+    want = (a.conj().T if adj else a) @ b
+    bound = np.abs(a.conj().T if adj else a) @ np.abs(b)
+    out["%%d_%%d_%%d_%%d" %% (m, k, n, adj)] = float(np.max(np.abs(c - want) / bound))
+print(json.dumps(out))
+"""
+
+SVD_SCRIPT = r"""
+import json, sys
+import numpy as np
+sys.path.insert(0, %(root)r)
+import paper_1504_00992_b200 as P
+rng = np.random.default_rng(11)
+out = {}
+for (m, n) in [(600, 500), (256, 256), (300, 420)]:
+    s_true = 0.8 ** np.arange(min(m, n))
+    u, _ = np.linalg.qr(rng.standard_normal((m, min(m, n))) + 1j * rng.standard_normal((m, min(m, n))))
+    v, _ = np.linalg.qr(rng.standard_normal((n, min(m, n))) + 1j * rng.standard_normal((n, min(m, n))))
+    a = (u * s_true) @ v.conj().T
+    U, s, V = P.svd_full(a)
+    sref = np.linalg.svd(a, compute_uv=False)
+    recon = np.linalg.norm((U * s) @ V.conj().T - a) / np.linalg.norm(a)
+    orth = np.linalg.norm(U.conj().T @ U - np.eye(U.shape[1]))
+    out["%%dx%%d" %% (m, n)] = [float(np.max(np.abs(s - sref)) / sref[0]), float(recon), float(orth)]
+print(json.dumps(out))
+"""
+
+
+def run_variant(script, env_extra):
+    env = dict(os.environ)
+    env.update(env_extra)
+    r = subprocess.run([sys.executable, "-c", script % {"root": ROOT}], env=env, capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    return json.loads(r.stdout.strip().splitlines()[-1])
+
+
+@pytest.mark.parametrize("env", [{"RRSVD_B200_GEMM_3M": "1"}, {"RRSVD_B200_GEMM_3M": "0"},
+                                 {"RRSVD_B200_GEMM_3M": "1", "RRSVD_B200_GEMM_3M64": "1"},
+                                 {"RRSVD_B200_GEMM_CFG": "56"}, {"RRSVD_B200_GEMM_CFG": "64"}])
+def test_zgemm_variants_componentwise(env):
+    """Every tile / complex-product form: |C - AB| <= 1e-13 |A||B| elementwise (FP64 GEMM error
+    bound class; 3M's imaginary-part bound is a small constant times 4M's)."""
+    res = run_variant(GEMM_SCRIPT, env)
+    for shape, err in res.items():
+        assert err <= 1e-13, (env, shape, err)
+
+
+@pytest.mark.parametrize("env", [{}, {"RRSVD_B200_BJ_S": "1"}, {"RRSVD_B200_BJ_S": "1", "RRSVD_B200_BJ_PER_STEP": "1"},
+                                 {"RRSVD_B200_BJ_MIN_C": "64"}])
+def test_block_jacobi_variants(env):
+    """Persistent sweep kernel, per-step kernel and the block path for narrow problems:
+    σ within 1e-13·σ1 of LAPACK, reconstruction and orthonormality at 1e-12."""
+    res = run_variant(SVD_SCRIPT, env)
+    for shape, (ds, recon, orth) in res.items():
+        assert ds <= 1e-13 and recon <= 1e-12 and orth <= 1e-12, (env, shape, ds, recon, orth)
