@@ -361,18 +361,19 @@ def run_ours(args, rank, world, local_rank):
         dist.barrier()
     te0 = time.perf_counter()
     d2h = 0
+    out_l = [torch.empty(l.shape, dtype=torch.float64).pin_memory() for l in lambdas]
     for _ in range(e2e_steps):
-        for s in range(len(site_dims)):
-            mps.set_site(s, pin_g[s], pin_l[s] if s < len(pin_l) else None)
+        mps.upload(pin_g, pin_l)  # rrsvd_b200_state_upload: every Γ and λ, one sync
         one_step()
-        d2h = 0
+        dims = mps.all_dims()
         for s in range(len(site_dims)):
-            dims = mps.dims(s)
-            buf = out_g[s] if tuple(out_g[s].shape) == dims else torch.empty(dims, dtype=torch.complex128).pin_memory()
-            ctx.check(lib.rrsvd_b200_mps_get_site(mps.h, s, None, C.c_void_p(buf.data_ptr()), None))
-            d2h += buf.numel() * 16
+            if tuple(out_g[s].shape) != dims[s]:
+                out_g[s] = torch.empty(dims[s], dtype=torch.complex128).pin_memory()
         for b in range(len(site_dims) - 1):
-            d2h += mps.dims(b)[2] * 8
+            if out_l[b].shape[0] != dims[b][2]:
+                out_l[b] = torch.empty(dims[b][2], dtype=torch.float64).pin_memory()
+        mps.download(out_g, out_l)  # rrsvd_b200_state_download: every Γ and λ, one sync
+        d2h = sum(g.numel() * 16 for g in out_g) + sum(l.numel() * 8 for l in out_l)
     te1 = time.perf_counter()
     e2e = world * e2e_steps / (te1 - te0)
 

@@ -229,6 +229,16 @@ int rrsvd_b200_mps_set_edge_lambdas(rrsvd_b200_mps* mps, const double* left, siz
 /* dims3 <- (left, phys, right); gamma / lambda_right copied out when non-NULL. */
 int rrsvd_b200_mps_get_site(rrsvd_b200_mps* mps, size_t site, size_t* dims3, double* gamma,
                             double* lambda_right);
+/* The whole state in one call (SURVEY §8(b) "rrsvd_b200_state_{upload,download}"; the
+ * MpsState constructor / field reads of mps.hpp:31-41): every site's Γ (dims[3*i+0] x d_i x
+ * dims[3*i+2]; dims[3*i+1] is ignored on upload) and every bond's λ (lambdas[i], i < n-1; a NULL
+ * entry skips that λ).  All copies are queued on the context's stream and synchronised once —
+ * host buffers (pinned for full PCIe rate) may be reused when the call returns.  Download fills
+ * dims (when non-NULL) and requires gammas[i] to hold the current size (query with dims first
+ * by passing gammas = NULL). */
+int rrsvd_b200_state_upload(rrsvd_b200_mps* mps, const size_t* dims, const double* const* gammas,
+                            const double* const* lambdas);
+int rrsvd_b200_state_download(rrsvd_b200_mps* mps, size_t* dims, double* const* gammas, double* const* lambdas);
 /* evolve (tebd.cpp:260-326): n_steps x sweeps x (bonds of the sweep's parity, ascending):
  * build_theta -> gate -> decimate on the device, state resident in HBM.  gates[s*(n_sites-1)+b]
  * is the (d_b d_{b+1})^2 gate exp(-i c_s dt h_b) for sweep s (NULL = no term on that bond); the

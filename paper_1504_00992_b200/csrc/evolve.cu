@@ -213,6 +213,58 @@ int rrsvd_b200_mps_get_site(rrsvd_b200_mps* s, size_t site, size_t* dims3, doubl
     });
 }
 
+int rrsvd_b200_state_upload(rrsvd_b200_mps* s, const size_t* dims, const double* const* gammas,
+                            const double* const* lambdas) {
+    return mps_api(s, [&](rrsvd_b200_ctx* c) {
+        if (dims == nullptr || gammas == nullptr) throw_contract(c, "state_upload: dims and gammas are required");
+        for (int site = 0; site < s->n; ++site) {
+            const size_t dl = dims[3 * site], dr = dims[3 * site + 2];
+            if (dl < 1 || dr < 1) throw_contract(c, "state_upload: bond dimensions must be >= 1");
+            if (site > 0 && dl != dims[3 * (site - 1) + 2]) throw_contract(c, "state_upload: bond dimensions disagree");
+            if (site == 0 && dl != 1 && s->edge[0] == nullptr)
+                throw_contract(c, "state_upload: open left end needs dim_left = 1 (or edge lambdas)");
+            if (site + 1 == s->n && dr != 1 && s->edge[1] == nullptr)
+                throw_contract(c, "state_upload: open right end needs dim_right = 1 (or edge lambdas)");
+            if (gammas[site] == nullptr) throw_contract(c, "state_upload: missing gamma");
+        }
+        for (int site = 0; site < s->n; ++site) {
+            const size_t dl = dims[3 * site], dr = dims[3 * site + 2];
+            const size_t elems = dl * s->d[site] * dr;
+            ensure_gamma(s, site, elems);
+            check_cuda(c, cudaMemcpyAsync(s->g[site], gammas[site], elems * sizeof(cplx), cudaMemcpyDefault, c->stream),
+                       "upload gamma");
+            if (lambdas != nullptr && lambdas[site] != nullptr && site + 1 < s->n) {
+                ensure_lambda(s, site, dr);
+                check_cuda(c, cudaMemcpyAsync(s->lam[site], lambdas[site], dr * sizeof(double), cudaMemcpyDefault, c->stream),
+                           "upload lambda");
+            }
+            s->dl[site] = (int)dl;
+            s->dr[site] = (int)dr;
+        }
+        check_cuda(c, cudaStreamSynchronize(c->stream), "sync");
+    });
+}
+
+int rrsvd_b200_state_download(rrsvd_b200_mps* s, size_t* dims, double* const* gammas, double* const* lambdas) {
+    return mps_api(s, [&](rrsvd_b200_ctx* c) {
+        for (int site = 0; site < s->n; ++site) {
+            if (dims) {
+                dims[3 * site] = s->dl[site];
+                dims[3 * site + 1] = s->d[site];
+                dims[3 * site + 2] = s->dr[site];
+            }
+            const size_t elems = (size_t)s->dl[site] * s->d[site] * s->dr[site];
+            if (gammas != nullptr && gammas[site] != nullptr)
+                check_cuda(c, cudaMemcpyAsync(gammas[site], s->g[site], elems * sizeof(cplx), cudaMemcpyDefault, c->stream),
+                           "download gamma");
+            if (lambdas != nullptr && lambdas[site] != nullptr && site + 1 < s->n)
+                check_cuda(c, cudaMemcpyAsync(lambdas[site], s->lam[site], s->dr[site] * sizeof(double), cudaMemcpyDefault,
+                                              c->stream), "download lambda");
+        }
+        check_cuda(c, cudaStreamSynchronize(c->stream), "sync");
+    });
+}
+
 }  // extern "C"
 
 // A gate resident on the device with its exact block structure (made once, reused by every

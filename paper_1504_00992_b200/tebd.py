@@ -73,8 +73,46 @@ class DeviceMps:
         self.ctx.check(L.lib().rrsvd_b200_mps_set_site(self.h, sz(site), sz(dl), sz(dr), ptr(g), ptr(l_)))
 
     def load(self, gammas, lambdas):
-        for s, g in enumerate(gammas):
-            self.set_site(s, g, lambdas[s] if s < len(lambdas) else None)
+        self.upload(gammas, lambdas)
+
+    def upload(self, gammas, lambdas=None):
+        """The whole state in one call (rrsvd_b200_state_upload: all copies queued, one sync).
+        gammas: numpy arrays or (pinned) torch tensors (dim_left, d, dim_right); lambdas: per
+        bond (len n-1) or None."""
+        n = self.n_sites
+        dims = (C.c_size_t * (3 * n))()
+        gp = (C.c_void_p * n)()
+        lp = (C.c_void_p * n)()
+        keep = []
+        for s_, g in enumerate(gammas):
+            g = np.ascontiguousarray(g, np.complex128) if isinstance(g, np.ndarray) else g
+            keep.append(g)
+            dl, _, dr = g.shape
+            dims[3 * s_], dims[3 * s_ + 1], dims[3 * s_ + 2] = dl, 0, dr
+            gp[s_] = ptr(g).value
+            if lambdas is not None and s_ < len(lambdas) and lambdas[s_] is not None:
+                lam = lambdas[s_]
+                lam = np.ascontiguousarray(lam, np.float64) if isinstance(lam, np.ndarray) else lam
+                keep.append(lam)
+                lp[s_] = ptr(lam).value
+        self.ctx.check(L.lib().rrsvd_b200_state_upload(self.h, dims, gp, lp))
+
+    def download(self, gammas, lambdas=None):
+        """Fill pre-shaped buffers (rrsvd_b200_state_download: one sync) — gammas[i] must have
+        the current dims(i) shape; lambdas[i] (optional) the bond's dimension."""
+        n = self.n_sites
+        gp = (C.c_void_p * n)(*[ptr(g).value for g in gammas])
+        lp = None
+        if lambdas is not None:
+            lp = (C.c_void_p * n)(*([ptr(x).value if x is not None else None for x in lambdas]
+                                    + [None] * (n - len(lambdas))))
+        self.ctx.check(L.lib().rrsvd_b200_state_download(self.h, None, gp, lp))
+
+    def all_dims(self):
+        n = self.n_sites
+        dims = (C.c_size_t * (3 * n))()
+        self.ctx.check(L.lib().rrsvd_b200_state_download(self.h, dims, None, None))
+        return [tuple(int(dims[3 * i + j]) for j in range(3)) for i in range(n)]
 
     def dims(self, site: int):
         d3 = (C.c_size_t * 3)()
