@@ -531,10 +531,17 @@ inline EvolveDiagnostics evolve(MpsState& state, const std::vector<HamiltonianTe
         rrsvd_b200_mps* m;
         ~Guard() { rrsvd_b200_mps_destroy(m); }
     } guard{dm};
-    for (std::size_t s = 0; s < n; ++s)
-        b200::check(rrsvd_b200_mps_set_site(dm, s, state.gammas[s].dim_left, state.gammas[s].dim_right,
-                                            b200::D(state.gammas[s].values.data()),
-                                            s + 1 < n ? state.lambdas[s].data() : nullptr));
+    {  // the whole state in one call (one stream sync)
+        std::vector<std::size_t> dims(3 * n);
+        std::vector<const double*> gp(n), lp(n, nullptr);
+        for (std::size_t s = 0; s < n; ++s) {
+            dims[3 * s] = state.gammas[s].dim_left;
+            dims[3 * s + 2] = state.gammas[s].dim_right;
+            gp[s] = b200::D(state.gammas[s].values.data());
+            if (s + 1 < n) lp[s] = state.lambdas[s].data();
+        }
+        b200::check(rrsvd_b200_state_upload(dm, dims.data(), gp.data(), lp.data()));
+    }
     std::vector<rrsvd_b200_sweep> sw;
     for (const auto& x : plan.sweeps) sw.push_back({x.bond_parity, x.coefficient});
     rrsvd_b200_backend be = detail::to_c(backend);
@@ -548,13 +555,19 @@ inline EvolveDiagnostics evolve(MpsState& state, const std::vector<HamiltonianTe
     b200::check(rrsvd_b200_evolve(dm, sw.size(), sw.data(), gptr.data(), n_steps, &be, &opt, &diag,
                                   rec.empty() ? nullptr : rec.data(), rec.size()));
     backend.seed = be.seed;
-    for (std::size_t s = 0; s < n; ++s) {
-        std::size_t d3[3];
-        b200::check(rrsvd_b200_mps_get_site(dm, s, d3, nullptr, nullptr));
-        state.gammas[s] = Tensor3(d3[0], d3[1], d3[2]);
-        if (s + 1 < n) state.lambdas[s].assign(d3[2], 0.0);
-        b200::check(rrsvd_b200_mps_get_site(dm, s, d3, b200::D(state.gammas[s].values.data()),
-                                            s + 1 < n ? state.lambdas[s].data() : nullptr));
+    {  // dims first, then every Γ and λ in one call
+        std::vector<std::size_t> dims(3 * n);
+        b200::check(rrsvd_b200_state_download(dm, dims.data(), nullptr, nullptr));
+        std::vector<double*> gp(n), lp(n, nullptr);
+        for (std::size_t s = 0; s < n; ++s) {
+            state.gammas[s] = Tensor3(dims[3 * s], dims[3 * s + 1], dims[3 * s + 2]);
+            gp[s] = reinterpret_cast<double*>(state.gammas[s].values.data());
+            if (s + 1 < n) {
+                state.lambdas[s].assign(dims[3 * s + 2], 0.0);
+                lp[s] = state.lambdas[s].data();
+            }
+        }
+        b200::check(rrsvd_b200_state_download(dm, nullptr, gp.data(), lp.data()));
     }
     EvolveDiagnostics out;
     out.kept_fraction = diag.kept_fraction;
