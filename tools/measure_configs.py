@@ -117,6 +117,27 @@ for n in ns:
     del Ad, G1, G2h
     torch.cuda.empty_cache()
 
+# ---------------------------------------------------------------- config 5, deterministic arm
+# (BASELINE configs[4]: "vs reference CPU RRSVD and deterministic SVD"): full SVD of a graded
+# full-rank n x n matrix (column scales 0.99^i), device vs the reference's svd_full (zgesdd)
+if not args.quick:
+    for n in [1000, 4000]:
+        G1 = torch.randn(n, n, dtype=torch.complex128, device="cuda") * torch.tensor(0.99 ** np.arange(n), device="cuda")
+        Ad = P.gemm(G1, False, torch.randn(n, n, dtype=torch.complex128, device="cuda"), ctx=ctx)
+        t = dev_time(lambda: P.svd_full(Ad, ctx=ctx), 2 if n <= 1000 else 1)
+        line = {"config": f"c5_full_svd_{n}x{n}", "device_s_per_svd": round(t, 4)}
+        if have_ref:
+            Ah = Ad.cpu().numpy()
+            tr = cpu_time(lambda: ref.svd_full(Ah), 1)
+            _, s_r, _ = ref.svd_full(Ah)
+            _, s_d, _ = P.svd_full(Ad, ctx=ctx)
+            line.update({"reference_s_per_svd": round(tr, 3), "speedup_vs_reference": round(tr / t, 2),
+                         "reference_cores": os.cpu_count(),
+                         "sigma_max_abs_err_over_s1": float(np.max(np.abs(s_d.cpu().numpy() - s_r)) / s_r[0])})
+        print(json.dumps(line), flush=True)
+        del Ad, G1
+        torch.cuda.empty_cache()
+
 # ---------------------------------------------------------------- config 3, full-SVD arm (A13)
 if not args.quick:
     n = 2000
