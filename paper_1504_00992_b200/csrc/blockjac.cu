@@ -65,7 +65,22 @@ struct BjPair {
     const int* dst;  // this step's slot -> next-step slot table
     BjStat* stat;
     int r, cp, b, inner_sweeps;
+    int cross_only;  // rotate only (block i, block j) column pairs: 16 rounds instead of 31
 };
+// Pair k of round rd: the circle method over all 2b columns (31 rounds), or — cross_only, every
+// step of a sweep but the first — column k of block i against column b + (k + rd) mod b of block
+// j (16 rounds).  Each block's own column pairs are rotated at the first step of every sweep,
+// where every block is in exactly one block pair, so a sweep still visits every column pair.
+__device__ __forceinline__ void bj_round_pair(int k, int rd, bool cross, int& p, int& q) {
+    constexpr int n2 = kBjN2, half = n2 / 2;
+    if (cross) {
+        p = k;
+        q = half + (k + rd) % half;
+    } else {
+        p = circle_bj(k, rd, n2);
+        q = circle_bj(n2 - 1 - k, rd, n2);
+    }
+}
 __device__ __forceinline__ void bj_pair(const BjPair& a, const int k0) {
     constexpr int n2 = kBjN2, ld = n2 + 1, half = n2 / 2;
     __shared__ double pc[half], ps[half];
@@ -199,11 +214,15 @@ __device__ __forceinline__ void bj_pair(const BjPair& a, const int k0) {
     const int ka = tid >> 4, kb = tid & 15;
     for (int isw = 0; isw < a.inner_sweeps; ++isw) {
     const int rot_before = s_rot;
-    for (int rd = 0; rd < n2 - 1; ++rd) {
-        const int p = circle_bj(ka, rd, n2), q = circle_bj(n2 - 1 - ka, rd, n2);
-        const int p2 = circle_bj(kb, rd, n2), q2 = circle_bj(n2 - 1 - kb, rd, n2);
+    const bool cross = a.cross_only != 0;
+    const int nrounds = cross ? half : n2 - 1;
+    for (int rd = 0; rd < nrounds; ++rd) {
+        int p, q, p2, q2;
+        bj_round_pair(ka, rd, cross, p, q);
+        bj_round_pair(kb, rd, cross, p2, q2);
         if (tid < half) {  // parameters of pair tid (= ka at threads (ka, ka))
-            const int pp = circle_bj(tid, rd, n2), qq = circle_bj(n2 - 1 - tid, rd, n2);
+            int pp, qq;
+            bj_round_pair(tid, rd, cross, pp, qq);
             const double ga = Gi[pp][pp].x, gb = Gi[qq][qq].x;
             const cplx g = Gi[pp][qq];
             const double g2 = g.x * g.x + g.y * g.y;
@@ -330,7 +349,8 @@ __device__ __forceinline__ void bj_pair(const BjPair& a, const int k0) {
 __global__ void __launch_bounds__(kBjThreads) bj_step_kernel(const __grid_constant__ BjStep a) {
     const int S = (int)cg::this_cluster().num_blocks();
     const int pr = blockIdx.y;
-    const BjPair q{a.Xs[pr], a.Vs[pr], a.Xd[pr], a.Vd[pr], a.dst, a.stat[pr], a.r, a.cp, a.b, a.inner_sweeps};
+    const BjPair q{a.Xs[pr], a.Vs[pr], a.Xd[pr], a.Vd[pr], a.dst, a.stat[pr], a.r, a.cp, a.b, a.inner_sweeps,
+                   a.cross_only};
     bj_pair(q, blockIdx.x / S);
 }
 
@@ -374,7 +394,8 @@ __global__ void __launch_bounds__(kBjThreads, 3) bj_sweep_kernel(const __grid_co
         }
         __syncthreads();
         const BjPair q{a.X[t & 1][qi], a.V[t & 1][qi], a.X[(t + 1) & 1][qi], a.V[(t + 1) & 1][qi],
-                       a.dst + (size_t)t * nbp, a.stat[qi], a.r, a.cp, a.b, a.inner_sweeps};
+                       a.dst + (size_t)t * nbp, a.stat[qi], a.r, a.cp, a.b, a.inner_sweeps,
+                       a.cross_steps && t > 0};
         bj_pair(q, k);
         __syncthreads();  // every write of the item precedes the release
         if (threadIdx.x == 0) {

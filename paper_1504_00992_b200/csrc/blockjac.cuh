@@ -45,6 +45,7 @@ struct BjStat {
 struct BjStep {
     int count, r, cp, b, npairs;
     int inner_sweeps;  // sweeps of the pair solve per step (stops early once a sweep rotates nothing)
+    int cross_only;    // rotate only the cross (block i, block j) column pairs (steps after the first)
     const cplx* Xs[kBjMaxProblems];
     cplx* Xd[kBjMaxProblems];
     const cplx* Vs[kBjMaxProblems];
@@ -61,6 +62,7 @@ int bj_slices(int pairs, int r);
 // One whole sweep (all nsteps tournament steps) in one launch of single-CTA pairs.
 struct BjSweep {
     int count, r, cp, b, npairs, nsteps, inner_sweeps;
+    int cross_steps;                // steps t > 0 rotate only the cross column pairs
     int epoch;                      // > every value already in done[] (the sweep number + 1)
     cplx* X[2][kBjMaxProblems];     // step t reads X[t & 1], writes X[(t + 1) & 1]
     cplx* V[2][kBjMaxProblems];

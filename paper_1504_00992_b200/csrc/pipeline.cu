@@ -338,6 +338,14 @@ struct SmallSvdSpec {
 // Block one-sided Jacobi (blockjac.cuh) for same-shaped problems: the tournament schedule is
 // host-side bookkeeping; one fused launch per step for all pairs of all problems; one
 // 4-byte-per-problem D2H per sweep for the convergence test.
+bool bj_cross_steps() {  // RRSVD_B200_BJ_CROSS=0: the full 31-round pair solve at every step
+    static const bool v = [] {
+        const char* e = std::getenv("RRSVD_B200_BJ_CROSS");
+        return e == nullptr || std::atoi(e) != 0;
+    }();
+    return v;
+}
+
 bool bj_per_step() {  // RRSVD_B200_BJ_PER_STEP=1: one launch per tournament step (A/B timing)
     static const bool v = [] {
         const char* e = std::getenv("RRSVD_B200_BJ_PER_STEP");
@@ -444,6 +452,7 @@ void block_jacobi_group(rrsvd_b200_ctx* c, const std::vector<const SmallSvdSpec*
             BjSweep sw{};
             sw.count = (int)active.size(); sw.r = r; sw.cp = cp; sw.b = b; sw.npairs = npairs; sw.nsteps = nsteps;
             sw.inner_sweeps = bj_inner_sweeps();
+            sw.cross_steps = bj_cross_steps();
             sw.epoch = sweep + 1;
             for (size_t q = 0; q < active.size(); ++q) {
                 const int p = active[q];
@@ -464,6 +473,7 @@ void block_jacobi_group(rrsvd_b200_ctx* c, const std::vector<const SmallSvdSpec*
             BjStep st{};
             st.count = (int)active.size(); st.r = r; st.cp = cp; st.b = b; st.npairs = npairs;
             st.inner_sweeps = bj_inner_sweeps();
+            st.cross_only = bj_cross_steps() && t > 0;
             for (size_t q = 0; q < active.size(); ++q) {
                 const int p = active[q];
                 st.Xs[q] = X1[p]; st.Xd[q] = X2[p]; st.Vs[q] = V1[p]; st.Vd[q] = V2[p]; st.stat[q] = stat + p;

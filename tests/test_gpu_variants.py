@@ -78,7 +78,7 @@ def test_zgemm_variants_componentwise(env):
 
 
 @pytest.mark.parametrize("env", [{}, {"RRSVD_B200_BJ_S": "1"}, {"RRSVD_B200_BJ_S": "1", "RRSVD_B200_BJ_PER_STEP": "1"},
-                                 {"RRSVD_B200_BJ_MIN_C": "64"}])
+                                 {"RRSVD_B200_BJ_MIN_C": "64"}, {"RRSVD_B200_BJ_CROSS": "0"}])
 def test_block_jacobi_variants(env):
     """Persistent sweep kernel, per-step kernel and the block path for narrow problems:
     σ within 1e-13·σ1 of LAPACK, reconstruction and orthonormality at 1e-12."""
