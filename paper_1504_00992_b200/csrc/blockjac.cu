@@ -94,6 +94,7 @@ __device__ __forceinline__ void bj_pair(const BjPair& a, const int k0) {
     auto sG = reinterpret_cast<cplx(*)[ld]>(sm + 2 * sizeof(Chunk));              // [n2][ld]
     auto sW = sG + n2;                                                            // [n2][ld]
     __shared__ int s_rot;
+    __shared__ int s_ident;  // the pair's solve rotated nothing: W = I exactly (set by CTA 0)
     __shared__ unsigned long long s_off2, s_off2_first;
     const int tid = threadIdx.x;
     const int r = a.r, cp = a.cp, b = a.b;
@@ -282,6 +283,7 @@ __device__ __forceinline__ void bj_pair(const BjPair& a, const int k0) {
     if (!more) break;
     }
 
+        if (tid == 0) s_ident = s_first == 0;
         if (tid == 0 && s_first) {
             atomicAdd(&a.stat->rot, s_first);
             atomicMax(&a.stat->off2, s_off2_first);
@@ -291,6 +293,7 @@ __device__ __forceinline__ void bj_pair(const BjPair& a, const int k0) {
     if (crank != 0) {
         const cplx(*pw)[ld] = cluster.map_shared_rank(sW, 0);
         for (int e = tid; e < n2 * n2; e += kBjThreads) sW[e / n2][e % n2] = pw[e / n2][e % n2];
+        if (tid == 0) s_ident = *cluster.map_shared_rank(&s_ident, 0);
     }
     cluster.sync();  // CTA 0's W may now be left (and the kernel may end) — peers have copied it
 
@@ -313,7 +316,12 @@ __device__ __forceinline__ void bj_pair(const BjPair& a, const int k0) {
         cplx* D = isx ? a.Xd : a.Vd;
         const int r0 = isx ? xr0 + t * kBjRows : vr0 + (t - nxc) * kBjRows;
         const int nr = min(kBjRows, (isx ? xr1 : vr1) - r0);
-        if (rt * 8 < nr) {
+        if (s_ident) {  // W = I: the blocks only move to their next slots
+            for (int e = tid; e < nr * n2; e += kBjThreads) {
+                const int i = e / n2, j = e % n2;
+                D[(long long)(r0 + i) * cp + (j < b ? dA + j : dB + j - b)] = ch[i][j];
+            }
+        } else if (rt * 8 < nr) {
             double are[2][2] = {{0.0, 0.0}, {0.0, 0.0}}, aim[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
 #pragma unroll
             for (int kk = 0; kk < n2 / 4; ++kk) {
