@@ -413,49 +413,77 @@ __global__ void __launch_bounds__(kBjThreads, 3) bj_sweep_kernel(const __grid_co
     }
 }
 
-__global__ void __launch_bounds__(kBjThreads) bj_finish_kernel(const __grid_constant__ BjFinish a) {
+// Finish, part 1 (one CTA per problem): column norms of X (σ per slot; row-parallel, partial sums
+// in a fixed order), each genuine slot's rank in the non-increasing order (ties by original
+// column), σ written sorted.
+constexpr int kBjFinThreads = 512;
+__global__ void __launch_bounds__(kBjFinThreads) bj_rank_kernel(const __grid_constant__ BjFinish a) {
     extern __shared__ __align__(16) unsigned char sm[];
     const int pr = blockIdx.x;
     double* sig = reinterpret_cast<double*>(sm);     // per slot (genuine columns)
     int* orig = reinterpret_cast<int*>(sig + a.cp);  // per slot: original column or -1
-    int* rank = orig + a.cp;
+    __shared__ double part[kBjFinThreads];
     const cplx* X = a.X[pr];
-    for (int s = threadIdx.x; s < a.cp; s += kBjThreads) {
+    const int cp = a.cp;
+    for (int s = threadIdx.x; s < cp; s += kBjFinThreads) {
         const int o = a.place[s / a.b] * a.b + s % a.b;
         orig[s] = o < a.c ? o : -1;
-        double acc = 0.0;
-        if (o < a.c)
-            for (int i = 0; i < a.r; ++i) acc += cabs2(X[(long long)i * a.cp + s]);
-        sig[s] = sqrt(acc);
     }
-    __syncthreads();
-    for (int s = threadIdx.x; s < a.cp; s += kBjThreads) {
-        if (orig[s] < 0) { rank[s] = -1; continue; }
-        const double v = sig[s];
-        int rk = 0;
-        for (int t = 0; t < a.cp; ++t)
-            if (orig[t] >= 0) rk += (sig[t] > v) || (sig[t] == v && orig[t] < orig[s]);
-        rank[s] = rk;
-    }
-    __syncthreads();
-    for (int s = threadIdx.x; s < a.cp; s += kBjThreads)
-        if (rank[s] >= 0) a.sigma[pr][rank[s]] = sig[s];
-    if (a.Xn[pr]) {
-        cplx* Xn = a.Xn[pr];
-        for (long long e = threadIdx.x; e < (long long)a.r * a.cp; e += kBjThreads) {
-            const int i = (int)(e / a.cp), s = (int)(e % a.cp);
-            if (rank[s] < 0) continue;
-            const double inv = sig[s] > 0.0 ? 1.0 / sig[s] : 0.0;
-            Xn[(long long)i * a.c + rank[s]] = cscale(X[e], inv);
+    const int cpp = min(cp, kBjFinThreads), tpc = kBjFinThreads / cpp;
+    const int jl = threadIdx.x % cpp, q = threadIdx.x / cpp;
+    for (int j0 = 0; j0 < cp; j0 += cpp) {
+        const int s = j0 + jl;
+        double a0 = 0.0, a1 = 0.0;
+        if (q < tpc && s < cp) {
+            int i = q;
+            for (; i + tpc < a.r; i += 2 * tpc) {
+                a0 += cabs2(X[(long long)i * cp + s]);
+                a1 += cabs2(X[(long long)(i + tpc) * cp + s]);
+            }
+            if (i < a.r) a0 += cabs2(X[(long long)i * cp + s]);
         }
+        part[threadIdx.x] = a0 + a1;
+        __syncthreads();
+        if (q == 0 && s < cp) {
+            double acc = 0.0;
+            for (int t = 0; t < tpc; ++t) acc += part[t * cpp + jl];
+            sig[s] = sqrt(acc);
+        }
+        __syncthreads();
     }
-    if (a.Js[pr]) {
-        cplx* Js = a.Js[pr];
-        const cplx* V = a.V[pr];
-        for (long long e = threadIdx.x; e < (long long)a.c * a.cp; e += kBjThreads) {
-            const int i = (int)(e / a.cp), s = (int)(e % a.cp);
-            if (rank[s] < 0) continue;
-            Js[(long long)i * a.c + rank[s]] = V[e];
+    for (int s = threadIdx.x; s < cp; s += kBjFinThreads) {
+        int rk = -1;
+        if (orig[s] >= 0) {
+            const double v = sig[s];
+            rk = 0;
+            for (int t = 0; t < cp; ++t)
+                if (orig[t] >= 0) rk += (sig[t] > v) || (sig[t] == v && orig[t] < orig[s]);
+            a.sigma[pr][rk] = v;
+        }
+        a.rank_ws[(size_t)pr * cp + s] = rk;
+        a.sig_ws[(size_t)pr * cp + s] = sig[s];
+    }
+}
+
+// Finish, part 2 (a 2-D grid of CTAs per problem): Xn = X columns / σ and Js = V columns, each
+// slot written to its sorted position.
+__global__ void __launch_bounds__(256) bj_scatter_kernel(const __grid_constant__ BjFinish a) {
+    const int pr = blockIdx.y;
+    const int cp = a.cp;
+    const int* rank = a.rank_ws + (size_t)pr * cp;
+    const double* sig = a.sig_ws + (size_t)pr * cp;
+    const long long nx = a.Xn[pr] ? (long long)a.r * cp : 0, nv = a.Js[pr] ? (long long)a.c * cp : 0;
+    for (long long e = blockIdx.x * 256LL + threadIdx.x; e < nx + nv; e += (long long)gridDim.x * 256) {
+        const bool isx = e < nx;
+        const long long f = isx ? e : e - nx;
+        const int i = (int)(f / cp), s = (int)(f % cp);
+        const int rk = rank[s];
+        if (rk < 0) continue;
+        if (isx) {
+            const double inv = sig[s] > 0.0 ? 1.0 / sig[s] : 0.0;
+            a.Xn[pr][(long long)i * a.c + rk] = cscale(a.X[pr][f], inv);
+        } else {
+            a.Js[pr][(long long)i * a.c + rk] = a.V[pr][f];
         }
     }
 }
@@ -526,10 +554,13 @@ cudaError_t bj_sweep(const BjSweep& a, cudaStream_t s) {
 
 cudaError_t bj_finish(const BjFinish& a, cudaStream_t s) {
     if (a.count == 0) return cudaSuccess;
-    const size_t smem = (size_t)a.cp * (sizeof(double) + 2 * sizeof(int));
-    cudaError_t e = cudaFuncSetAttribute(bj_finish_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const size_t smem = (size_t)a.cp * (sizeof(double) + sizeof(int));
+    cudaError_t e = cudaFuncSetAttribute(bj_rank_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    bj_finish_kernel<<<a.count, kBjThreads, smem, s>>>(a);
+    bj_rank_kernel<<<a.count, kBjFinThreads, smem, s>>>(a);
+    const long long per = (long long)(a.r + a.c) * a.cp;
+    const int gx = (int)std::max<long long>(1, std::min<long long>((per + 255) / 256, std::max(1, 4 * 148 / a.count)));
+    bj_scatter_kernel<<<dim3(gx, a.count), 256, 0, s>>>(a);
     return cudaGetLastError();
 }
 

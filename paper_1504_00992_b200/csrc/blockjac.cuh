@@ -82,6 +82,8 @@ struct BjFinish {
     cplx* Xn[kBjMaxProblems];       // nullable: r x c row-major, X columns / sigma (sorted)
     cplx* Js[kBjMaxProblems];       // nullable: c x c row-major, V columns (sorted)
     int place[kBjMaxSlots];         // block id at each block position (final placement)
+    double* sig_ws;                 // device scratch: count x cp column norms
+    int* rank_ws;                   // device scratch: count x cp output rank per slot (-1 = padding)
 };
 cudaError_t bj_finish(const BjFinish& a, cudaStream_t s);
 

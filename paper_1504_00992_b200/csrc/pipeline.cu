@@ -514,8 +514,10 @@ void block_jacobi_group(rrsvd_b200_ctx* c, const std::vector<const SmallSvdSpec*
         fin.sigma[p] = grp[p]->sigma; fin.Xn[p] = grp[p]->Xn; fin.Js[p] = grp[p]->Js;
     }
     std::copy(pl0.begin(), pl0.end(), fin.place);
+    fin.sig_ws = ws_get<double>(c, (size_t)np * cp);
+    fin.rank_ws = ws_get<int>(c, (size_t)np * cp);
     check_cuda(c, bj_finish(fin, c->stream), "bj_finish");
-    c->launches++;
+    c->launches += 2;
 }
 
 void small_svd_many(rrsvd_b200_ctx* c, const std::vector<SmallSvdSpec>& specs) {
