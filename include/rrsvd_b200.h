@@ -135,15 +135,16 @@ int rrsvd_b200_fixed_rank_batch(rrsvd_b200_ctx* ctx, size_t count, const double*
                                 double* const* V, double* discarded);
 
 /* rrsvd_fixed_precision (randomized.hpp:64-66, randomized.cpp:124-176) with
- * AccuracyCheckParams{epsilon, probe_count, growth_block = 0}: range finder at initial_l, then
- * probe rounds (seeds seed + 0x9e3779b97f4a7c15 * draw) that certify
- * max_j ||(I - Q Q^H) A omega_j|| <= epsilon or double the basis (up to min(m, n)).  Writes all
+ * AccuracyCheckParams{epsilon, probe_count, growth_block} (randomized.hpp:30-35): range finder at
+ * initial_l, then probe rounds (seeds seed + 0x9e3779b97f4a7c15 * draw) that certify
+ * max_j ||(I - Q Q^H) A omega_j|| <= epsilon or grow the basis by growth_block columns
+ * (0 doubles it; never past min(m, n)).  Writes all
  * l produced columns: U (m x l), S (l), V (n x l) — size them for l = min(m, n) — and *l_out,
  * *certified (tolerance_certified), *discarded (w over all l values).  omega_mode selects the
  * reference mt19937_64 stream or Philox for every draw. */
 int rrsvd_b200_fixed_precision(rrsvd_b200_ctx* ctx, const double* A, size_t m, size_t n,
-                               size_t initial_l, size_t q, size_t probe_count, double epsilon,
-                               uint64_t seed, int omega_mode, double* U, double* S, double* V,
+                               size_t initial_l, size_t q, size_t probe_count, size_t growth_block,
+                               double epsilon, uint64_t seed, int omega_mode, double* U, double* S, double* V,
                                size_t* l_out, int* certified, double* discarded);
 
 /* ---- L3: the TEBD two-site trio in the unfolded layout (tebd.hpp:98-110) ---------------

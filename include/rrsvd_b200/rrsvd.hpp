@@ -121,7 +121,7 @@ struct RrsvdParams {
 struct AccuracyCheckParams {
     double tolerance;
     std::size_t probe_count;
-    std::size_t growth_block = 0;  // the device path implements the reference default (doubling)
+    std::size_t growth_block = 0;  // columns appended per failed round; 0 doubles the basis
 };
 
 // ---- linalg.hpp:29-56 (device) ----------------------------------------------------------
@@ -202,8 +202,6 @@ inline SvdResult rrsvd_fixed_rank(const DenseMatrix& a, const RrsvdParams& p) {
 
 inline SvdResult rrsvd_fixed_precision(const DenseMatrix& a, const AccuracyCheckParams& check,
                                        std::size_t initial_l, std::size_t q, std::uint64_t seed) {
-    if (check.growth_block != 0)
-        throw contract_violation("rrsvd_fixed_precision: the device path grows by doubling (growth_block 0)");
     const std::size_t mn = std::min(a.rows(), a.cols());
     std::vector<cplx> u(a.rows() * mn), v(a.cols() * mn);
     std::vector<double> s(mn);
@@ -211,7 +209,7 @@ inline SvdResult rrsvd_fixed_precision(const DenseMatrix& a, const AccuracyCheck
     int cert = 0;
     SvdResult out;
     b200::check(rrsvd_b200_fixed_precision(b200::context(), b200::D(a.data()), a.rows(), a.cols(), initial_l, q,
-                                           check.probe_count, check.tolerance, seed, RRSVD_B200_OMEGA_REFERENCE,
+                                           check.probe_count, check.growth_block, check.tolerance, seed, RRSVD_B200_OMEGA_REFERENCE,
                                            b200::D(u.data()), s.data(), b200::D(v.data()), &l, &cert,
                                            &out.discarded_weight), a.rows(), a.cols());
     out.u = DenseMatrix(a.rows(), l);

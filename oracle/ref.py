@@ -177,7 +177,7 @@ def fixed_rank(a, k: int, p: int, q: int, seed: int, vectors: bool = True):
     return u, s, v, w.value
 
 
-def fixed_precision(a, eps: float, probes: int, initial_l: int, q: int, seed: int):
+def fixed_precision(a, eps: float, probes: int, initial_l: int, q: int, seed: int, growth_block: int = 0):
     """rrsvd_fixed_precision (randomized.cpp:124-176) -> (u, s, v, w, certified)."""
     a = _c(a)
     m, n = a.shape
@@ -187,7 +187,7 @@ def fixed_precision(a, eps: float, probes: int, initial_l: int, q: int, seed: in
     v = np.empty(n * mn, np.complex128)
     lo, cert, w = U64(), C.c_int(), C.c_double()
     _check(lib().ref_fixed_precision(_p(a), U64(m), U64(n), U64(initial_l), U64(q), U64(probes),
-                                     C.c_double(eps), U64(seed), _p(u), _p(s), _p(v), C.byref(lo),
+                                     U64(growth_block), C.c_double(eps), U64(seed), _p(u), _p(s), _p(v), C.byref(lo),
                                      C.byref(cert), C.byref(w)))
     l = lo.value
     return u[:m * l].reshape(m, l), s[:l], v[:n * l].reshape(n, l), w.value, bool(cert.value)

@@ -192,14 +192,14 @@ int ref_fixed_rank(const double* a, std::uint64_t m, std::uint64_t n, std::uint6
     });
 }
 
-// rrsvd_fixed_precision (randomized.cpp:124-176), growth_block 0.  u/v sized for min(m, n)
+// rrsvd_fixed_precision (randomized.cpp:124-176) with AccuracyCheckParams{eps, probes, growth}.  u/v sized for min(m, n)
 // columns (the worst case); *l_out = columns produced.
 int ref_fixed_precision(const double* a, std::uint64_t m, std::uint64_t n, std::uint64_t initial_l,
-                        std::uint64_t q, std::uint64_t probes, double eps, std::uint64_t seed, double* u,
+                        std::uint64_t q, std::uint64_t probes, std::uint64_t growth, double eps, std::uint64_t seed, double* u,
                         double* s, double* v, std::uint64_t* l_out, int* certified, double* discarded) {
     return guarded([&] {
         const rrsvd::SvdResult r = rrsvd::rrsvd_fixed_precision(
-            load(a, m, n), rrsvd::AccuracyCheckParams{eps, probes, 0}, initial_l, q, seed);
+            load(a, m, n), rrsvd::AccuracyCheckParams{eps, probes, growth}, initial_l, q, seed);
         if (u) store(r.u, u);
         std::memcpy(s, r.sigma.data(), r.sigma.size() * sizeof(double));
         if (v) store(r.v, v);

@@ -185,10 +185,11 @@ def rrsvd_fixed_rank(a, k: int, p: int, q: int, seed: int, omega=None,
 
 
 def rrsvd_fixed_precision(a, epsilon: float, probe_count: int, initial_l: int, q: int, seed: int,
-                          mode: int = OMEGA_REFERENCE, vectors: bool = True, ctx=None) -> SvdResult:
-    """randomized.cpp:124-176 (AccuracyCheckParams{epsilon, probe_count, growth_block=0}):
+                          mode: int = OMEGA_REFERENCE, vectors: bool = True, ctx=None,
+                          growth_block: int = 0) -> SvdResult:
+    """randomized.cpp:124-176 (AccuracyCheckParams{epsilon, probe_count, growth_block}):
     range finder at initial_l, then probe rounds that certify max_j ||(I-QQ^H) A w_j|| <= eps
-    or double the basis.  Returns all l columns; tolerance_certified as the reference."""
+    or grow the basis by growth_block columns (0 doubles it).  Returns all l columns; tolerance_certified as the reference."""
     c = _ctx(ctx)
     a = _prep(a)
     m, n = _shape(a)
@@ -198,7 +199,7 @@ def rrsvd_fixed_precision(a, epsilon: float, probe_count: int, initial_l: int, q
     v = _empty(a, (n * mn,), np.complex128) if vectors else None
     lo, cert, w = C.c_size_t(), C.c_int(), C.c_double()
     c.check(L.lib().rrsvd_b200_fixed_precision(c.h, ptr(a), sz(m), sz(n), sz(initial_l), sz(q),
-                                               sz(probe_count), C.c_double(epsilon), C.c_uint64(seed),
+                                               sz(probe_count), sz(growth_block), C.c_double(epsilon), C.c_uint64(seed),
                                                C.c_int(mode), ptr(u), ptr(s), ptr(v), C.byref(lo),
                                                C.byref(cert), C.byref(w)))
     l = lo.value

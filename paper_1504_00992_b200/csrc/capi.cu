@@ -282,8 +282,8 @@ int rrsvd_b200_fixed_rank(rrsvd_b200_ctx* c, const double* A, size_t m, size_t n
 }
 
 int rrsvd_b200_fixed_precision(rrsvd_b200_ctx* c, const double* A, size_t m, size_t n, size_t initial_l,
-                               size_t q, size_t probe_count, double epsilon, uint64_t seed, int omega_mode,
-                               double* U, double* S, double* V, size_t* out_l, int* certified,
+                               size_t q, size_t probe_count, size_t growth_block, double epsilon, uint64_t seed,
+                               int omega_mode, double* U, double* S, double* V, size_t* out_l, int* certified,
                                double* discarded) {
     return api(c, [&] {
         if (S == nullptr || out_l == nullptr) throw_contract(c, "fixed_precision: null argument");
@@ -293,6 +293,7 @@ int rrsvd_b200_fixed_precision(rrsvd_b200_ctx* c, const double* A, size_t m, siz
         const auto* dA = static_cast<const cplx*>(stage_in(c, A, m * n * sizeof(cplx)));
         std::vector<FixedPrecSpec> fp{FixedPrecSpec{dA, (int)m, (int)n, (int)initial_l, (int)q, (int)probe_count,
                                                     epsilon, seed, omega_mode}};
+        fp[0].growth_block = (int)std::min(growth_block, std::min(m, n));
         rrsvd_fixed_precision_many(c, fp);
         const size_t l = (size_t)fp[0].l;
         auto* sc = ws_get<Scalars>(c, 1);

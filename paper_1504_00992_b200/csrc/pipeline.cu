@@ -720,8 +720,8 @@ void rrsvd_core_many(rrsvd_b200_ctx* c, const std::vector<RrsvdSpec>& specs) {
 
 // Fixed-precision RRSVD (randomized.cpp:124-176), all problems in lock-step rounds.  Each round
 // draws `probes` fresh Gaussian columns per active problem (seed + 0x9e3779b97f4a7c15·draw), forms
-// D = (I - Q Q^H) A Omega_p, and either certifies max_j ||D_j|| <= eps or grows the basis by l
-// columns (the probe images first, then A times fresh sketch columns) and re-orthonormalises
+// D = (I - Q Q^H) A Omega_p, and either certifies max_j ||D_j|| <= eps or grows the basis by
+// growth_block (0: l) columns (the probe images first, then A times fresh sketch columns) and re-orthonormalises
 // [Q, block].  The per-round decision needs the norms on the host: one small D2H per round.
 void rrsvd_fixed_precision_many(rrsvd_b200_ctx* c, std::vector<FixedPrecSpec>& specs) {
     if (specs.empty()) return;
@@ -814,7 +814,8 @@ void rrsvd_fixed_precision_many(rrsvd_b200_ctx* c, std::vector<FixedPrecSpec>& s
                 continue;
             }
             if (s.l + r > minor) { active[i] = 0; continue; }
-            const int grow = std::min(s.l, minor - s.l);  // growth_block 0: double the basis
+            // randomized.cpp:156-157: growth_block columns, or double the basis when it is 0
+            const int grow = std::min(s.growth_block == 0 ? s.l : s.growth_block, minor - s.l);
             if (grow == 0) { active[i] = 0; continue; }
             const int ln = s.l + grow, from_probe = std::min(r, grow);
             cplx* Qn = ws_get<cplx>(c, (size_t)s.m * ln);

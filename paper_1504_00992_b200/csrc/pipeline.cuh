@@ -115,8 +115,8 @@ struct AssembleSpec {
 void assemble_many(rrsvd_b200_ctx* c, const std::vector<AssembleSpec>& specs);
 
 // Fixed-precision RRSVD with the probabilistic accuracy check and basis growth
-// (randomized.cpp:124-176, growth_block 0).  Inputs: A, m, n, l0 (initial width), q, probes, eps,
-// seed, omega_mode.  Outputs (host-visible after the call): l (final width), certified, and
+// (randomized.cpp:124-176).  Inputs: A, m, n, l0 (initial width), q, probes, eps, seed, omega_mode,
+// growth_block (columns appended per failed round; 0 doubles the basis, randomized.cpp:156).  Outputs (host-visible after the call): l (final width), certified, and
 // workspace device buffers U (m x l), sigma (l), V (n x l).  Synchronises once per round.
 struct FixedPrecSpec {
     const cplx* A;
@@ -125,6 +125,7 @@ struct FixedPrecSpec {
     uint64_t seed;
     int omega_mode;
     const cplx* omega0 = nullptr;  // nullable: the initial n x l0 sketch, fed instead of drawn
+    int growth_block = 0;          // AccuracyCheckParams::growth_block (randomized.hpp:34)
     int l = 0;
     bool certified = false;
     cplx* U = nullptr;

@@ -79,6 +79,9 @@ int main() {
         const SvdResult fp = rrsvd_fixed_precision(a, {1e-8, 4}, 8, 1, 11);
         CHECK(fp.tolerance_certified);
         CHECK(fp.achieved_rank == 8);
+        const SvdResult fg = rrsvd_fixed_precision(a, {1e-8, 4, 3}, 2, 1, 11);  // growth_block 3: 2 -> 5 -> 8
+        CHECK(fg.tolerance_certified);
+        CHECK(fg.achieved_rank == 8);
         const SvdResult full = svd_full(a);
         for (std::size_t i = 0; i < 6; ++i) CHECK(std::abs(fp.sigma[i] - full.sigma[i]) < 1e-10 * full.sigma[0]);
     }

@@ -168,6 +168,37 @@ def test_fixed_rank_batch_matches_single_calls(ctx, ref):
         assert np.linalg.norm(rec - rec_r) / np.linalg.norm(rec_r) < 1e-9
 
 
+@pytest.mark.parametrize("growth", [7, 50])
+def test_fixed_precision_growth_block_matches_reference(ctx, ref, growth):
+    """AccuracyCheckParams::growth_block != 0 (randomized.cpp:156-167): growth-block columns per
+    failed round (the probe images, then fresh sketch columns when growth > probe_count)."""
+    n = 400
+    a = ref.structured_matrix(0.97 ** np.arange(n), n, 5, 6)
+    res = P.rrsvd_fixed_precision(a, 1e-3, 10, 20, 2, 17, growth_block=growth, ctx=ctx)
+    u_r, s_r, v_r, w_r, cert_r = ref.fixed_precision(a, 1e-3, 10, 20, 2, 17, growth_block=growth)
+    assert cert_r and len(s_r) > 20 and (len(s_r) - 20) % growth == 0
+    assert res.achieved_rank == len(s_r) and res.tolerance_certified == cert_r
+    assert np.max(np.abs(res.sigma - s_r)) <= 1e-10 * s_r[0]
+    assert abs(res.discarded_weight - w_r) < 1e-12
+
+
+def test_fixed_precision_acceptance_criterion3(ctx, ref):
+    """acceptance.cpp:143-152: spectrum 1/j (n=750), m=1500, AccuracyCheckParams{1e-2·‖A‖_F, 10,
+    50}, initial l=500, q=2, seed 35 — certified, same width and σ as the reference, and the
+    retained rank for relative tolerance 1e-2 within 650 ± 5 %."""
+    n, m = 750, 1500
+    a = ref.structured_matrix(1.0 / np.arange(1, n + 1), m, 33, 34)
+    a_norm = float(np.linalg.norm(a))
+    res = P.rrsvd_fixed_precision(a, 1e-2 * a_norm, 10, 500, 2, 35, growth_block=50, ctx=ctx)
+    u_r, s_r, v_r, w_r, cert_r = ref.fixed_precision(a, 1e-2 * a_norm, 10, 500, 2, 35, growth_block=50)
+    assert res.tolerance_certified and cert_r and res.achieved_rank == len(s_r)
+    assert np.max(np.abs(res.sigma - s_r)) <= 1e-10 * s_r[0]
+    # retained_rank_for_tolerance (acceptance.cpp:145): smallest k whose Frobenius tail <= tol·‖A‖
+    tail = np.sqrt(np.maximum(a_norm ** 2 - np.cumsum(res.sigma ** 2), 0.0))
+    k = int(np.argmax(tail <= 1e-2 * a_norm)) + 1
+    assert 618 <= k <= 682
+
+
 @pytest.mark.parametrize("case", ["certified_at_once", "grows", "uncertifiable"])
 def test_fixed_precision_matches_reference(ctx, ref, case):
     """rrsvd_fixed_precision (randomized.cpp:124-176): same final width l, same certification,
