@@ -721,8 +721,8 @@ void rrsvd_core_many(rrsvd_b200_ctx* c, const std::vector<RrsvdSpec>& specs) {
 // Fixed-precision RRSVD (randomized.cpp:124-176), all problems in lock-step rounds.  Each round
 // draws `probes` fresh Gaussian columns per active problem (seed + 0x9e3779b97f4a7c15·draw), forms
 // D = (I - Q Q^H) A Omega_p, and either certifies max_j ||D_j|| <= eps or grows the basis by
-// growth_block (0: l) columns (the probe images first, then A times fresh sketch columns) and re-orthonormalises
-// [Q, block].  The per-round decision needs the norms on the host: one small D2H per round.
+// growth_block (0: l) columns (the probe images first, then A times fresh sketch columns),
+// orthonormalised against Q.  The per-round decision needs the norms on the host: one small D2H per round.
 void rrsvd_fixed_precision_many(rrsvd_b200_ctx* c, std::vector<FixedPrecSpec>& specs) {
     if (specs.empty()) return;
     constexpr uint64_t kGolden = 0x9e3779b97f4a7c15ull;
@@ -801,9 +801,16 @@ void rrsvd_fixed_precision_many(rrsvd_b200_ctx* c, std::vector<FixedPrecSpec>& s
         check_cuda(c, cudaMemcpyAsync(hmax, dmax, act.size() * sizeof(double), cudaMemcpyDeviceToHost, c->stream),
                    "D2H");
         check_cuda(c, cudaStreamSynchronize(c->stream), "sync");
-        std::vector<OrthSpec> os;
+        // Growth (randomized.cpp:155-168): the new block X (the probe images, then A times fresh
+        // sketch columns) is orthonormalised against the kept basis by block classical
+        // Gram-Schmidt with reorthogonalisation — twice {X <- X - Q (Q^H X); X <- orth(X)} — and
+        // Q_new = [Q, X] spans what the reference's Householder QR of [Q, X] spans.  A Cholesky
+        // QR of the whole [Q, X], or one projection before orth(X), lets X's dependent columns
+        // (a basis grown past the rank) turn into normalised noise that leaks along Q, and the
+        // probe then fails to certify a basis that does span the range.
+        struct Grow { size_t i; int l, g; cplx *Qn, *Xa, *Xb, *Pq, *Xq; };
+        std::vector<Grow> gw;
         std::vector<GemmSpec> gx;
-        std::vector<int> grown(np, 0);
         for (size_t t = 0; t < act.size(); ++t) {
             const size_t i = act[t];
             FixedPrecSpec& s = specs[i];
@@ -817,11 +824,11 @@ void rrsvd_fixed_precision_many(rrsvd_b200_ctx* c, std::vector<FixedPrecSpec>& s
             // randomized.cpp:156-157: growth_block columns, or double the basis when it is 0
             const int grow = std::min(s.growth_block == 0 ? s.l : s.growth_block, minor - s.l);
             if (grow == 0) { active[i] = 0; continue; }
-            const int ln = s.l + grow, from_probe = std::min(r, grow);
-            cplx* Qn = ws_get<cplx>(c, (size_t)s.m * ln);
-            check_cuda(c, cudaMemcpy2DAsync(Qn, ln * sizeof(cplx), Q[i], s.l * sizeof(cplx), s.l * sizeof(cplx),
-                                            s.m, cudaMemcpyDeviceToDevice, c->stream), "copy");
-            check_cuda(c, cudaMemcpy2DAsync(Qn + s.l, ln * sizeof(cplx), Bp[i], r * sizeof(cplx),
+            const int from_probe = std::min(r, grow);
+            Grow w{i, s.l, grow, ws_get<cplx>(c, (size_t)s.m * (s.l + grow)), ws_get<cplx>(c, (size_t)s.m * grow),
+                   ws_get<cplx>(c, (size_t)s.m * grow), ws_get<cplx>(c, (size_t)s.l * grow),
+                   ws_get<cplx>(c, (size_t)s.m * grow)};
+            check_cuda(c, cudaMemcpy2DAsync(w.Xa, grow * sizeof(cplx), Bp[i], r * sizeof(cplx),
                                             from_probe * sizeof(cplx), s.m, cudaMemcpyDeviceToDevice, c->stream),
                        "copy");
             if (grow > from_probe) {
@@ -829,15 +836,41 @@ void rrsvd_fixed_precision_many(rrsvd_b200_ctx* c, std::vector<FixedPrecSpec>& s
                 cplx* om = ws_get<cplx>(c, (size_t)s.n * ne);
                 make_omega(c, s.n, ne, s.seed + kGolden * draw[i], s.omega_mode, om);
                 ++draw[i];
-                gx.push_back({s.m, ne, s.n, s.A, s.n, om, ne, Qn + s.l + from_probe, ln});
+                gx.push_back({s.m, ne, s.n, s.A, s.n, om, ne, w.Xa + from_probe, grow});
             }
-            os.push_back({Qn, s.m, ln, Qn});
-            Q[i] = Qn;
-            s.l = ln;
+            gw.push_back(w);
         }
         c->gemm_tag = 7;
         gemm_many(c, kOpN, gx);
-        orth_many(c, os);
+        for (int pass = 0; pass < 2; ++pass) {  // X -> Xb = X - Q (Q^H X) -> orth: Xa -> Xq, then Xq -> Xa
+            std::vector<GemmSpec> gp, gs;
+            std::vector<OrthSpec> os;
+            for (const Grow& w : gw) {
+                const FixedPrecSpec& s = specs[w.i];
+                const cplx* X = pass == 0 ? w.Xa : w.Xq;
+                gp.push_back({w.l, w.g, s.m, Q[w.i], w.l, X, w.g, w.Pq, w.g});       // P = Q^H X
+                GemmSpec d{s.m, w.g, w.l, Q[w.i], w.l, w.Pq, w.g, w.Xb, w.g};      // Xb = X - Q P
+                d.D = X;
+                d.ldd = w.g;
+                d.alpha = -1.0;
+                gs.push_back(d);
+                os.push_back({w.Xb, s.m, w.g, pass == 0 ? w.Xq : w.Xa});
+            }
+            c->gemm_tag = 7;
+            gemm_many(c, kOpC, gp);
+            gemm_many(c, kOpN, gs);
+            orth_many(c, os);
+        }
+        for (const Grow& w : gw) {
+            FixedPrecSpec& s = specs[w.i];
+            const int ln = w.l + w.g;
+            check_cuda(c, cudaMemcpy2DAsync(w.Qn, ln * sizeof(cplx), Q[w.i], w.l * sizeof(cplx), w.l * sizeof(cplx),
+                                            s.m, cudaMemcpyDeviceToDevice, c->stream), "copy");
+            check_cuda(c, cudaMemcpy2DAsync(w.Qn + w.l, ln * sizeof(cplx), w.Xa, w.g * sizeof(cplx),
+                                            w.g * sizeof(cplx), s.m, cudaMemcpyDeviceToDevice, c->stream), "copy");
+            Q[w.i] = w.Qn;
+            s.l = ln;
+        }
     }
     std::vector<AssembleSpec> as;
     for (size_t i = 0; i < np; ++i) {

@@ -182,6 +182,22 @@ def test_fixed_precision_growth_block_matches_reference(ctx, ref, growth):
     assert abs(res.discarded_weight - w_r) < 1e-12
 
 
+def test_fixed_precision_rank_deficient_growth(ctx, ref):
+    """Basis growth past the rank (a rank-6 120x80 A, test_randomized.cpp's fixed-precision shape):
+    for every growth_block / initial width / q the device stops at the reference's width — the
+    grown block is orthonormalised against the kept basis, so dependent probe images cannot spoil
+    the certificate."""
+    lf, rf = ref.gaussian_test_matrix(120, 6, 4), ref.gaussian_test_matrix(80, 6, 5)
+    a = lf @ rf.conj().T
+    for g in (0, 1, 2, 3, 4, 5):
+        for l0 in (1, 2, 3, 5, 8):
+            for q in (0, 1):
+                _, s_r, _, _, cert_r = ref.fixed_precision(a, 1e-8, 4, l0, q, 11, growth_block=g)
+                res = P.rrsvd_fixed_precision(a, 1e-8, 4, l0, q, 11, growth_block=g, ctx=ctx)
+                assert (res.achieved_rank, res.tolerance_certified) == (len(s_r), cert_r), (g, l0, q)
+                assert np.max(np.abs(res.sigma[:6] - s_r[:6])) <= 1e-10 * s_r[0]
+
+
 def test_fixed_precision_acceptance_criterion3(ctx, ref):
     """acceptance.cpp:143-152: spectrum 1/j (n=750), m=1500, AccuracyCheckParams{1e-2·‖A‖_F, 10,
     50}, initial l=500, q=2, seed 35 — certified, same width and σ as the reference, and the
