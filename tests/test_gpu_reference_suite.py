@@ -182,6 +182,49 @@ def test_fixed_precision_terminates_immediately_on_low_rank(ctx):
     assert np.allclose(res.sigma[:3], [2.0, 1.0, 0.5], atol=1e-10)
 
 
+def _retained_rank_for_tolerance(sigma, a_norm, rel_tol):
+    """randomized.cpp:228-238 (test helper)."""
+    budget, resid = (rel_tol * a_norm) ** 2, a_norm ** 2
+    if resid <= budget:
+        return 0
+    for k, s in enumerate(np.asarray(sigma)):
+        resid -= s * s
+        if resid <= budget:
+            return k + 1
+    return len(sigma)
+
+
+def test_fixed_precision_identifies_retention_rank_for_tolerance(ctx, ref):
+    """test_randomized.cpp:170-185: spectrum 1/j (n=150), m=200, AccuracyCheckParams{5e-2·‖A‖,
+    5, growth_block 10}, initial l=20, q=2, seed 83 — certified, retained rank within the
+    reference's band around the spectrum-tail oracle."""
+    spec = 1.0 / np.arange(1, 151)
+    a = ref.structured_matrix(spec, 200, 81, 82)
+    a_norm, tol = float(np.linalg.norm(a)), 5e-2
+    tail = np.sqrt(np.maximum(np.sum(spec ** 2) - np.concatenate([[0.0], np.cumsum(spec ** 2)]), 0.0))
+    oracle = int(np.argmax(tail <= tol * a_norm))
+    res = P.rrsvd_fixed_precision(a, tol * a_norm, 5, 20, 2, 83, growth_block=10, ctx=ctx)
+    assert res.tolerance_certified
+    certified = _retained_rank_for_tolerance(res.sigma, a_norm, tol)
+    assert oracle * 95 // 100 <= certified <= oracle * 105 // 100 + 2
+    _, s_r, _, _, cert_r = ref.fixed_precision(a, tol * a_norm, 5, 20, 2, 83, growth_block=10)
+    assert (res.achieved_rank, res.tolerance_certified) == (len(s_r), cert_r)
+
+
+def test_fixed_precision_flags_exhaustion_instead_of_throwing(ctx):
+    """test_randomized.cpp:187-193: identity(24), tolerance 1e-30, 3 probes, initial l=4, q=0."""
+    res = P.rrsvd_fixed_precision(np.eye(24, dtype=complex), 1e-30, 3, 4, 0, 3, ctx=ctx)
+    assert not res.tolerance_certified
+
+
+def test_range_finder_on_identity_with_full_l(ctx):
+    """test_randomized.cpp:59-65: the full-width sketch of identity(8) spans everything —
+    ‖A − U Σ Vᴴ‖_F ≤ 1e-12 through the sketched SVD (l = 8, q = 0, seed 8)."""
+    a = np.eye(8, dtype=complex)
+    r = P.rrsvd_sketched_svd(a, 8, 0, 8, ctx=ctx)
+    assert np.linalg.norm(a - (r.u * r.sigma) @ r.v.conj().T) <= 1e-12
+
+
 def test_identical_seeds_give_bit_identical_factorizations(ctx):
     """test_randomized.cpp:324-332 — the device path is deterministic too (fixed reduction orders,
     no atomics on data)."""
