@@ -7,10 +7,13 @@ oscillators (d=20), χ=100 (n = d·χ = 2000 at interior bonds), RRSVD decimatio
 synthetic MPS (Gaussian Γ, λ ∝ 0.9^i) held in HBM; the gates are the real
 TEDOPA bond gates.  Inputs are larger than L2 (MPS ≈ 320 MB > 126 MB) so no L2 flush is needed.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload c3|c2|c1]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--workload c3|c3p100|c3det|c2|c5|c4]
 
-Under torchrun (N > 1) every rank evolves its own chain (weak scaling, replicas) and rank 0 prints
-the max-over-ranks timing.  `--impl reference` times the reference C++ core (oracle/_ref, built
+Under torchrun (N > 1) the chain is partitioned into contiguous site blocks, one per rank (weak
+scaling: 100 oscillator sites per rank, boundary Γ/λ exchanged by NCCL send/recv), and rank 0
+prints the max-over-ranks timing.  Only the JSON line goes to stdout (library and NCCL chatter is
+redirected to stderr).  `--impl reference` times the reference C++ core (oracle/_ref, built
 from /root/reference) on the host cores on a bounded sample of the same workload.
 """
 from __future__ import annotations
@@ -28,6 +31,17 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+
+_JSON_FD = None  # the process's original stdout: the JSON line only (see main)
+
+
+def emit(obj) -> None:
+    line = json.dumps(obj) + "\n"
+    if _JSON_FD is None:
+        sys.stdout.write(line)
+        sys.stdout.flush()
+    else:
+        os.write(_JSON_FD, line.encode())
 
 METRIC = "TEBD steps/s at n=d·χ (RRSVD decimation; FP64 tensor-core roofline of the zgemm stages)"
 
@@ -246,7 +260,7 @@ def run_partitioned(args, rank, world, local_rank):
     dist.all_reduce(te, op=dist.ReduceOp.MAX)
     e2e = world * e2e_steps / float(te.item())
     if rank == 0:
-        print(json.dumps({
+        emit({
             "metric": METRIC, "value": round(world * args.steps / elapsed, 6), "unit": "steps/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(1e3 * elapsed / args.steps, 3), "higher_is_better": True, "scaling": "weak",
@@ -264,7 +278,7 @@ def run_partitioned(args, rank, world, local_rank):
             "e2e": {"value": round(e2e, 6), "unit": "steps/s", "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h), "note": "rank 0's bytes; every rank stages its own block"},
             "gpu_launches": int(gpu_launches), "clocks": clk.summary(),
-        }), flush=True)
+        })
     dist.barrier()
     dist.destroy_process_group()
 
@@ -414,7 +428,7 @@ def run_ours(args, rank, world, local_rank):
         }
         if not args.no_cpu_baseline and world == 1:
             line["cpu_baseline"] = cpu_baseline(args, wl, gammas, lambdas, gates_host, plan, samples=2)
-        print(json.dumps(line), flush=True)
+        emit(line)
     if dist:
         dist.barrier()
         dist.destroy_process_group()
@@ -524,7 +538,7 @@ def run_sharded(args, rank, world, local_rank):
         elif args.workload == "c4":
             line["cpu_baseline"] = None
             line["cpu_baseline_note"] = "not run: the 102 GB input exceeds a host-core run's budget"
-        print(json.dumps(line), flush=True)
+        emit(line)
     if dist:
         dist.barrier()
         dist.destroy_process_group()
@@ -604,7 +618,7 @@ def run_reference(args, rank, world):
     from paper_1504_00992_b200 import models as M
     from paper_1504_00992_b200.tebd import build_gates
     if not ref.available():
-        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/librrsvd_ref.so not built"}))
+        emit({"impl": "reference", "unavailable": "oracle/_ref/librrsvd_ref.so not built"})
         return
     cores = os.cpu_count() or 1
     ref.set_threads(cores)
@@ -620,7 +634,7 @@ def run_reference(args, rank, world):
         secs.append(ref_update_sample(ref, wl, gammas, lambdas, gates, plan, [nb // 2 - 1 + (k % 2)], 7 + k))
     per_update = sum(secs) / len(secs)
     v = 1.0 / (per_update * ups)
-    print(json.dumps({
+    emit({
         "impl": "reference", "metric": METRIC, "value": round(v, 8), "unit": "steps/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * per_update * ups, 1),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128 (fp64)",
@@ -631,7 +645,7 @@ def run_reference(args, rank, world):
                                    f"timed on the host, extrapolated x{ups} updates/step",
                          "blas": ref.blas_info()["core"]},
         "e2e": {"value": round(v, 8), "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-    }), flush=True)
+    })
 
 
 def main():
@@ -647,6 +661,10 @@ def main():
     ap.add_argument("--force-partition", action="store_true",
                     help="use the chain-block partition driver even on one GPU (smoke test of the N>1 path)")
     args = ap.parse_args()
+    global _JSON_FD
+    sys.stdout.flush()
+    _JSON_FD = os.dup(1)
+    os.dup2(2, 1)  # NCCL's version banner and any library prints go to stderr
     if args.steps is None:
         args.steps = 1 if args.workload == "c3det" else 10
     if args.warmup < 3:
@@ -659,15 +677,15 @@ def main():
             wl = SHARDED[args.workload]
             cb = sharded_cpu_baseline(wl) if args.workload == "c5" else None
             if cb is None:
-                print(json.dumps({"impl": "reference", "unavailable": "c4: 102 GB input exceeds a host run"
-                                  if args.workload == "c4" else "oracle/_ref not built"}))
+                emit({"impl": "reference", "unavailable": "c4: 102 GB input exceeds a host run"
+                                  if args.workload == "c4" else "oracle/_ref not built"})
             else:
-                print(json.dumps({"impl": "reference", "metric": "RRSVD decimations/s (row-sharded single matrix;"
+                emit({"impl": "reference", "metric": "RRSVD decimations/s (row-sharded single matrix;"
                                   " FP64 tensor-core roofline)", "value": cb["value"], "unit": "decimations/s",
                                   "n_gpus": world, "steps": 1, "warmup": 0, "higher_is_better": True,
                                   "config": {"workload": wl["name"]}, "cpu_baseline": cb,
                                   "e2e": {"value": cb["value"], "unit": "decimations/s", "h2d_bytes_per_step": 0,
-                                          "d2h_bytes_per_step": 0}}), flush=True)
+                                          "d2h_bytes_per_step": 0}})
     elif args.workload in SHARDED:
         run_sharded(args, rank, world, local_rank)
     elif args.impl == "reference":
