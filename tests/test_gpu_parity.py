@@ -134,6 +134,47 @@ def test_fixed_rank_config1(ctx, ref, omega_fed):
     assert np.linalg.norm(rec - rec_r) / np.linalg.norm(rec_r) < 1e-10
 
 
+@pytest.mark.parametrize("case", ["config1", "config5_n1000"])
+def test_philox_rrsvd_within_reference_seed_envelope(ctx, ref, case):
+    """GPU-own RNG (Philox sketch) — the statistical tolerance of the north star, stated here: over
+    8 device seeds and 20 reference seeds (mt19937_64 stream) on the same matrix, per σ index and
+    for w: the means agree, |mean_dev − mean_ref| ≤ 5·s_ref·√(1/8 + 1/20) (Welch-style, widened
+    by a rounding floor of 1e-13·σ1 for σ and 1e-14 for w), and the spreads agree: s_dev/s_ref
+    ∈ [1/6, 6] per index (and for w) wherever the reference spread is above the floor, with a
+    geometric mean over the indices in [1/2, 2] (the trailing σ errors are one-sided and
+    heavy-tailed, so 8-vs-20-sample spreads scatter by ~4x; a per-sample band would test the
+    tail shape, not the sketch).  The seeds are fixed, so the outcome is deterministic."""
+    if case == "config1":
+        a, _ = c1_matrix(ref)
+        k, p, q = 64, 10, 2
+    else:
+        n = 1000
+        a = ref.structured_matrix(ref.spectrum_exponential(n, 0.95), n, n, n + 1)
+        k, p, q = 100, 10, 2
+    ref_s, ref_w = [], []
+    for t in range(20):
+        _, s_r, _, w_r = ref.fixed_rank(a, k, p, q, 1000 + t)
+        ref_s.append(s_r)
+        ref_w.append(w_r)
+    ref_s, ref_w = np.array(ref_s), np.array(ref_w)
+    dev = [P.rrsvd_fixed_rank(a, k, p, q, 5000 + t, mode=P.OMEGA_PHILOX, vectors=False, ctx=ctx)
+           for t in range(8)]
+    dev_s = np.array([np.asarray(r.sigma) for r in dev])
+    dev_w = np.array([r.discarded_weight for r in dev])
+    floor_s, floor_w = 1e-13 * ref_s[0, 0], 1e-14
+    mu, sd = ref_s.mean(0), ref_s.std(0, ddof=1)
+    dmu, dsd = dev_s.mean(0), dev_s.std(0, ddof=1)
+    assert np.all(np.abs(dmu - mu) <= 5 * sd * np.sqrt(1 / 8 + 1 / 20) + floor_s), np.max(
+        np.abs(dmu - mu) / (sd + floor_s))
+    live = sd > 10 * floor_s
+    ratio = dsd[live] / sd[live]
+    assert live.sum() > 0 and np.all((ratio >= 1 / 6) & (ratio <= 6.0)), (ratio.min(), ratio.max())
+    assert 0.5 <= np.exp(np.mean(np.log(ratio))) <= 2.0, np.exp(np.mean(np.log(ratio)))
+    mw, sw = ref_w.mean(), ref_w.std(ddof=1)
+    assert abs(dev_w.mean() - mw) <= 5 * sw * np.sqrt(1 / 8 + 1 / 20) + floor_w
+    assert 1 / 6 <= dev_w.std(ddof=1) / sw <= 6.0, dev_w.std(ddof=1) / sw
+
+
 @pytest.mark.parametrize("n", [900, 1600])
 def test_fixed_rank_paper_k100_p100(ctx, ref, n):
     """The paper's own benchmark setting: k = p = 100 (l = 200), q = 2,

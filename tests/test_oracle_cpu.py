@@ -35,6 +35,26 @@ def test_port_fixed_rank_and_sketch():
     assert abs(w2 - float(GOLD["sk_w"])) < 1e-14
 
 
+def test_port_fixed_precision_matches_reference(ref):
+    """port.rrsvd_fixed_precision (randomized.cpp:124-176) against the compiled reference: the same
+    final width and certificate for growth_block 0 / 1 / 3 / 5 / 7 / 50 — including a basis grown
+    past the rank of a rank-6 matrix — and σ, w to rounding."""
+    lf, rf = ref.gaussian_test_matrix(120, 6, 4), ref.gaussian_test_matrix(80, 6, 5)
+    low = lf @ rf.conj().T
+    for g in (0, 1, 3, 5):
+        for l0 in (1, 2, 5, 8):
+            _, s_r, _, _, c_r = ref.fixed_precision(low, 1e-8, 4, l0, 1, 11, growth_block=g)
+            _, s_p, _, _, c_p = port.rrsvd_fixed_precision(low, 1e-8, 4, l0, 1, 11, growth_block=g)
+            assert (len(s_p), c_p) == (len(s_r), c_r), (g, l0)
+            assert np.max(np.abs(s_p[:6] - s_r[:6])) <= 1e-12 * s_r[0]
+    a = ref.structured_matrix(0.97 ** np.arange(400), 400, 5, 6)
+    for g in (0, 7, 50):
+        _, s_r, _, w_r, c_r = ref.fixed_precision(a, 1e-3, 10, 20, 2, 17, growth_block=g)
+        _, s_p, _, w_p, c_p = port.rrsvd_fixed_precision(a, 1e-3, 10, 20, 2, 17, growth_block=g)
+        assert (len(s_p), c_p) == (len(s_r), c_r)
+        assert np.max(np.abs(s_p - s_r)) <= 1e-12 * s_r[0] and abs(w_p - w_r) <= 1e-13
+
+
 def test_port_theta_gate_decimate():
     lam = GOLD["tb_lam"]
     th = port.build_theta(GOLD["tb_g1"], GOLD["tb_g2"], lam, lam, lam)
