@@ -89,13 +89,17 @@ def test_criterion6_magnetisation_trace_and_trotter_order():
         assert abs(np.log2(e0 / e1) - 2.0) <= 0.2
 
 
-def test_criterion7_backend_equivalence():
+@pytest.mark.parametrize("omega_mode", [P.OMEGA_REFERENCE, P.OMEGA_PHILOX])
+def test_criterion7_backend_equivalence(omega_mode):
     """acceptance.cpp:320-363: deterministic vs randomized (accuracy check on, ε = 1e-3) quench —
-    observables and Schmidt values within 1e-6 at every sample."""
+    observables and Schmidt values within 1e-6 at every sample; with the reference's Ω stream and
+    with the GPU's own Philox sketch (the criterion is the reference's statistical tolerance for
+    any Gaussian sketch)."""
     n, chi = 6, 32
     a_m, a_l = run_quench(n, 1e-3, 1000, 50, P.DecimationBackend(), chi)
     rnd = P.DecimationBackend(randomized=True, target_rank=chi, oversampling=chi, power_iterations=2,
-                              accuracy_check=True, epsilon=1e-3, det_crossover=0, seed=99)
+                              accuracy_check=True, epsilon=1e-3, det_crossover=0, seed=99,
+                              omega_mode=omega_mode)
     b_m, b_l = run_quench(n, 1e-3, 1000, 50, rnd, chi)
     assert np.max(np.abs(a_m - b_m)) <= 1e-6
     worst = 0.0
