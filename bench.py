@@ -212,6 +212,7 @@ def run_partitioned(args, rank, world, local_rank):
     part = ChainPartition(blk, TorchComm("cuda"), list(range(n - 1)))
     be = P.DecimationBackend(omega_mode=P.OMEGA_PHILOX, randomized=True, target_rank=0, oversampling=10,
                              power_iterations=2, det_crossover=256, seed=7)
+    dist.barrier()  # a collective on the whole group before the first batched P2P exchange (NCCL)
     for w in range(args.warmup):
         part.evolve(gates, plan, dt, 1, be, 7, step0=w)
         load_state()
