@@ -157,6 +157,13 @@ def run_partitioned(args, rank, world, local_rank):
     from paper_1504_00992_b200 import models as M
     from paper_1504_00992_b200.parallel import BlockSpec, ChainPartition, DeviceBlock, TorchComm
 
+    # RRSVD_B200_BENCH_GLOO=1: gloo with host-staged exchanges and every rank on GPU
+    # local_rank % device_count — a protocol check of this N > 1 driver on a one-GPU box (ranks
+    # never wait on each other's kernels); never a measurement.
+    gloo = os.environ.get("RRSVD_B200_BENCH_GLOO", "0") not in ("", "0")
+    if gloo:
+        local_rank %= torch.cuda.device_count()
+    red = "cpu" if gloo else "cuda"  # where the reductions' tensors live
     torch.cuda.set_device(local_rank)
     if "RANK" not in os.environ:  # --force-partition without torchrun: a one-rank group on 127.0.0.1
         import socket
@@ -164,7 +171,10 @@ def run_partitioned(args, rank, world, local_rank):
             sk.bind(("127.0.0.1", 0))
             port = sk.getsockname()[1]
         os.environ.update(RANK="0", WORLD_SIZE="1", LOCAL_RANK="0", MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
-    dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
+    if gloo:
+        dist.init_process_group("gloo")
+    else:
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
     ctx = P.Context(local_rank, stream=stream.cuda_stream)
@@ -209,7 +219,7 @@ def run_partitioned(args, rank, world, local_rank):
             blk.set_gamma(i, site_gamma(gs), lam(gs) if i + 1 < len(local) else None)
 
     load_state()
-    part = ChainPartition(blk, TorchComm("cuda"), list(range(n - 1)))
+    part = ChainPartition(blk, TorchComm(red), list(range(n - 1)))
     be = P.DecimationBackend(omega_mode=P.OMEGA_PHILOX, randomized=True, target_rank=0, oversampling=10,
                              power_iterations=2, det_crossover=256, seed=7)
     dist.barrier()  # a collective on the whole group before the first batched P2P exchange (NCCL)
@@ -227,11 +237,11 @@ def run_partitioned(args, rank, world, local_rank):
         ev1.synchronize()
     elapsed = ev0.elapsed_time(ev1) / 1e3
     gpu_launches = ctx.launches - launches0
-    t = torch.tensor([elapsed], device="cuda")
+    t = torch.tensor([elapsed], device=red)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     elapsed = float(t.item())
     ups_rank = sum(1 for p, _ in plan for j in spec.local_bonds if j % 2 == p)
-    ups = torch.tensor([ups_rank], device="cuda", dtype=torch.float64)
+    ups = torch.tensor([ups_rank], device=red, dtype=torch.float64)
     dist.all_reduce(ups)
 
     # ---- end-to-end: every step each rank uploads its block from pinned host memory through the
@@ -257,7 +267,7 @@ def run_partitioned(args, rank, world, local_rank):
             ctx.check(P.lib().rrsvd_b200_mps_get_site(blk.mps.h, i, None, C.c_void_p(buf.data_ptr()), None))
             d2h += buf.numel() * 16
     torch.cuda.synchronize()
-    te = torch.tensor([time.perf_counter() - te0], device="cuda")
+    te = torch.tensor([time.perf_counter() - te0], device=red)
     dist.all_reduce(te, op=dist.ReduceOp.MAX)
     e2e = world * e2e_steps / float(te.item())
     if rank == 0:
@@ -271,7 +281,9 @@ def run_partitioned(args, rank, world, local_rank):
                        "desc": "weak scaling: one config-3-sized block (100 bosons, n=2000 bonds) per GPU; "
                                "value = blocks x steps / s (each block is a config-3 chain)",
                        "sites": n, "chi": chi, "updates_per_step": int(ups.item()),
-                       "parallelism": f"chain-block partition x{world}, NCCL P2P boundary exchange",
+                       "parallelism": f"chain-block partition x{world}, " + (
+                           "gloo host-staged exchange on shared GPUs (protocol check, not a measurement)"
+                           if gloo else "NCCL P2P boundary exchange"),
                        "l2": "inputs larger than L2"},
             "decimations_per_s": round(float(ups.item()) * args.steps / elapsed, 3),
             "roofline": {"bound": "tensor", "peak": round(peak_dmma, 3), "unit": "TFLOP/s", "achieved": None,
