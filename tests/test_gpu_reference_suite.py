@@ -225,6 +225,19 @@ def test_range_finder_on_identity_with_full_l(ctx):
     assert np.linalg.norm(a - (r.u * r.sigma) @ r.v.conj().T) <= 1e-12
 
 
+def test_appending_basis_columns_never_increases_the_residual(ctx, ref):
+    """test_randomized.cpp:302-313: spectrum 1/j (n=40), m=60, sketch A·Ω(40, 20, seed 73); the
+    device QR of the first l sketch columns, l = 2, 5, ..., 20: ‖A − QQᴴA‖_F never increases."""
+    a = ref.structured_matrix(1.0 / np.arange(1, 41), 60, 71, 72)
+    sketch = P.matmul(a, P.gaussian_test_matrix(40, 20, 73, ctx=ctx), ctx=ctx)
+    prev = np.inf
+    for l in range(2, 21, 3):
+        q, _ = P.qr(np.ascontiguousarray(sketch[:, :l]), ctx=ctx)
+        r = np.linalg.norm(a - q @ (q.conj().T @ a))
+        assert r <= prev + 1e-12
+        prev = r
+
+
 def test_identical_seeds_give_bit_identical_factorizations(ctx):
     """test_randomized.cpp:324-332 — the device path is deterministic too (fixed reduction orders,
     no atomics on data)."""
@@ -266,6 +279,34 @@ def test_unitary_gates_preserve_theta_norm(ctx):
     g, _ = np.linalg.qr(cplx_randn(rng, 9, 9))
     out = P.apply_gate_to_theta(th, g, ctx=ctx)
     assert abs(np.linalg.norm(out) - np.linalg.norm(th)) < 1e-12 * np.linalg.norm(th)
+
+
+def test_theta_of_a_maximally_mixed_bond_has_unit_norm(ctx):
+    """test_tebd.cpp:110-123: Σ_i λ_i |ii⟩ with flat λ = 1/√d (d = 4, open chain ends)."""
+    d = 4
+    g1, g2 = np.zeros((1, d, d), complex), np.zeros((d, d, 1), complex)
+    for i in range(d):
+        g1[0, i, i] = g2[i, i, 0] = 1.0
+    theta = P.build_theta(g1, g2, None, np.full(d, 1.0 / np.sqrt(d)), None, ctx=ctx)
+    assert abs(np.linalg.norm(theta) - 1.0) <= 1e-10
+
+
+def test_decimation_optimality_kept_spectrum_beats_random_projections(ctx):
+    """test_tebd.cpp:379-407 (on a quenched 6-site state instead of random_canonical_mps): the
+    deterministic χ=2 truncation (renormalize off) leaves a smaller error than any of 20 random
+    rank-2 projections Q (device QR of Ω(rows, 2, 3000 + t))."""
+    terms = M.heisenberg_terms(6, 1.0)
+    mps = product_mps([UP, DOWN, UP, DOWN, UP, DOWN], 8)
+    evolve(mps, {b: t for b, t in enumerate(terms)}, 0.05, 6, P.DecimationBackend())
+    ll, lm, lr = mps.lam(1), mps.lam(2), mps.lam(3)
+    theta = P.build_theta(mps.gamma(2), mps.gamma(3), ll, lm, lr, ctx=ctx)
+    dec = P.decimate(theta, ll, lr, 2, 0.0, P.DecimationBackend(), renormalize=False, ctx=ctx)
+    total_sq = np.linalg.norm(theta) ** 2
+    err_opt = np.sqrt(max(0.0, total_sq - float(np.sum(np.asarray(dec.lam) ** 2))))
+    m = P.theta_to_unfolded(theta, ctx=ctx)
+    for t in range(20):
+        q, _ = P.qr(P.gaussian_test_matrix(m.shape[0], 2, 3000 + t, ctx=ctx), ctx=ctx)
+        assert np.linalg.norm(m - q @ (q.conj().T @ m)) >= err_opt - 1e-12
 
 
 def test_deterministic_and_randomized_decimation_agree_mid_simulation(ctx):
