@@ -85,13 +85,14 @@ uint64_t rrsvd_b200_launch_count(const rrsvd_b200_ctx* ctx);
 
 /* ---- L1: dense linear algebra (linalg.hpp:29-56) ---------------------------------------- */
 /* C (m x n) = op_a(A) (m x k) * op_b(B) (k x n); replaces rrsvd::gemm (linalg.cpp:20-35).
- * Only op_b = N is supported.  lda/ldb/ldc are row strides in complex elements. */
+ * lda/ldb/ldc are row strides in complex elements (of A, B as stored: B is n x k for op_b = C). */
 int rrsvd_b200_zgemm(rrsvd_b200_ctx* ctx, int op_a, int op_b, size_t m, size_t n, size_t k,
                      const double* A, size_t lda, const double* B, size_t ldb, double* C,
                      size_t ldc);
-/* Thin orthonormal basis Q (m x n, m >= n) of A plus R = Q^H A (n x n); replaces rrsvd::qr
- * (linalg.cpp:49-65).  Like the reference, rank-deficient A yields no NaN; dependent columns
- * of Q come back as zero columns instead of an arbitrary orthonormal completion. */
+/* Thin orthonormal basis Q (m x n, m >= n) of A plus R = Q^H A (n x n), A = Q R; replaces
+ * rrsvd::qr (linalg.cpp:49-65).  Like the reference's Householder QR, Q is orthonormal for ANY
+ * A (linalg.hpp:35-37): columns of a rank-deficient A that CholeskyQR finds dependent get an
+ * orthonormal completion (orthogonal to the live columns), and R has (near-)zero rows there. */
 int rrsvd_b200_qr(rrsvd_b200_ctx* ctx, const double* A, size_t m, size_t n, double* Q, double* R);
 /* One shifted-CholeskyQR factor step on an already-formed (e.g. all-reduced) Gram matrix:
  * T = R^-1 (l x l, upper) with G + s I = R^H R, s = shift_scale * 2^-53 * trace(G) (0: none;

@@ -60,17 +60,16 @@ def _shape(x):
 def gemm(a, adj_a: bool, b, adj_b: bool = False, ctx=None):
     """rrsvd::gemm (linalg.cpp:20-35): op(a) @ op(b), op ∈ {N, ᴴ}."""
     c = _ctx(ctx)
-    if adj_b:
-        raise ContractViolation("gemm: adj_b is not supported by the device kernel")
     a, b = _prep(a), _prep(b)
     ar, ac = _shape(a)
     br, bc = _shape(b)
     m, k = (ac, ar) if adj_a else (ar, ac)
-    if k != br:
+    kb, n = (bc, br) if adj_b else (br, bc)
+    if k != kb:
         raise ContractViolation("gemm: inner dimension mismatch")
-    out = _empty(a, (m, bc), np.complex128)
-    c.check(L.lib().rrsvd_b200_zgemm(c.h, int(adj_a), 0, sz(m), sz(bc), sz(k), ptr(a), sz(ac), ptr(b),
-                                     sz(bc), ptr(out), sz(bc)))
+    out = _empty(a, (m, n), np.complex128)
+    c.check(L.lib().rrsvd_b200_zgemm(c.h, int(adj_a), int(adj_b), sz(m), sz(n), sz(k), ptr(a), sz(ac), ptr(b),
+                                     sz(bc), ptr(out), sz(n)))
     return out
 
 

@@ -25,6 +25,7 @@ int api(rrsvd_b200_ctx* c, F&& f) {
         c->err = e.what();
         code = kCuda;
     }
+    if (code != kOk) recover_after_failure(c);
     ws_reset(c);
     return code;
 }
@@ -56,6 +57,43 @@ void copy_out(rrsvd_b200_ctx* c, void* dst, const void* src, size_t bytes) {
     check_cuda(c, cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, c->stream), "copy out");
 }
 
+// Householder QR returns an orthonormal Q even for rank-deficient input (linalg.hpp:35-37,
+// tested at test_linalg.cpp:152-159); CholeskyQR leaves the dependent columns of Q at exactly
+// zero.  Fill them with an orthonormal basis of a random subspace orthogonal to the live
+// columns: E (m x nd, Philox) <- E - Q (Q^H E) twice, then E <- orth(E), scattered into the
+// dead column slots.  R = Q^H A afterwards has (numerically) zero rows there, and Q R = A still
+// holds because A lies in the span of the live columns.
+void complete_basis(rrsvd_b200_ctx* c, cplx* Q, int m, int n) {
+    // column norms^2 = diag(Q^H Q)
+    cplx* G = ws_get<cplx>(c, (size_t)n * n);
+    gemm(c, kOpC, n, n, m, Q, n, Q, n, G, n);
+    std::vector<cplx> diag(n);
+    check_cuda(c, cudaMemcpy2DAsync(diag.data(), sizeof(cplx), G, (size_t)(n + 1) * sizeof(cplx), sizeof(cplx), n,
+                                    cudaMemcpyDeviceToHost, c->stream), "D2H diag");
+    check_cuda(c, cudaStreamSynchronize(c->stream), "sync");
+    std::vector<int> dead;
+    for (int j = 0; j < n; ++j)
+        if (!(diag[j].x > 0.5)) dead.push_back(j);
+    const int nd = (int)dead.size();
+    if (nd == 0) return;
+    cplx* E = ws_get<cplx>(c, (size_t)m * nd);
+    cplx* P = ws_get<cplx>(c, (size_t)n * nd);
+    cplx* F = ws_get<cplx>(c, (size_t)m * nd);
+    make_omega(c, m, nd, 0x51a7e5eedull, RRSVD_B200_OMEGA_PHILOX, E);
+    for (int pass = 0; pass < 2; ++pass) {
+        gemm(c, kOpC, n, nd, m, Q, n, E, nd, P, nd);  // P = Q^H E
+        GemmSpec up{m, nd, n, Q, n, P, nd, E, nd};    // E = E - Q P
+        up.D = E;
+        up.ldd = nd;
+        up.alpha = -1.0;
+        gemm_many(c, kOpN, {up});
+    }
+    orth(c, E, m, nd, F);
+    for (int t = 0; t < nd; ++t)
+        check_cuda(c, cudaMemcpy2DAsync(Q + dead[t], (size_t)n * sizeof(cplx), F + t, (size_t)nd * sizeof(cplx),
+                                        sizeof(cplx), m, cudaMemcpyDeviceToDevice, c->stream), "scatter");
+}
+
 }  // namespace
 
 extern "C" {
@@ -84,6 +122,7 @@ int rrsvd_b200_ctx_create(int device, void* stream, rrsvd_b200_ctx** out) {
         }
         c->own_stream = true;
     }
+    c->home = c->stream;
     // keep workspace allocations cached in the stream-ordered pool
     cudaMemPool_t pool;
     if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
@@ -114,7 +153,7 @@ int rrsvd_b200_set_stream(rrsvd_b200_ctx* c, void* stream) {
         check_cuda(c, cudaStreamSynchronize(c->stream), "sync");
         if (c->own_stream) cudaStreamDestroy(c->stream);
         c->own_stream = false;
-        c->stream = static_cast<cudaStream_t>(stream);
+        c->stream = c->home = static_cast<cudaStream_t>(stream);
     });
 }
 
@@ -129,13 +168,30 @@ uint64_t rrsvd_b200_launch_count(const rrsvd_b200_ctx* c) { return c ? c->launch
 int rrsvd_b200_zgemm(rrsvd_b200_ctx* c, int op_a, int op_b, size_t m, size_t n, size_t k,
                      const double* A, size_t lda, const double* B, size_t ldb, double* C, size_t ldc) {
     return api(c, [&] {
-        if (op_b != RRSVD_B200_OP_N) throw_contract(c, "zgemm: only op_b = N is supported");
         if (op_a != RRSVD_B200_OP_N && op_a != RRSVD_B200_OP_C) throw_contract(c, "zgemm: bad op_a");
+        if (op_b != RRSVD_B200_OP_N && op_b != RRSVD_B200_OP_C) throw_contract(c, "zgemm: bad op_b");
         if (m == 0 || n == 0) return;
         const size_t a_rows = op_a == RRSVD_B200_OP_N ? m : k;
         std::vector<OutBuf> outs;
         const auto* dA = static_cast<const cplx*>(stage_in(c, A, a_rows * lda * sizeof(cplx)));
-        const auto* dB = static_cast<const cplx*>(stage_in(c, B, k * ldb * sizeof(cplx)));
+        const cplx* dB;
+        if (op_b == RRSVD_B200_OP_N) {
+            dB = static_cast<const cplx*>(stage_in(c, B, k * ldb * sizeof(cplx)));
+        } else if (k > 0) {
+            // op_b = C (B is n x k): one conjugate-transpose pass into a k x n workspace, then
+            // the N kernel — adj_b is a boundary convenience (linalg.cpp:20-35), never on the
+            // decimation path.
+            auto* packed = ws_get<cplx>(c, n * k);
+            check_cuda(c, cudaMemcpy2DAsync(packed, k * sizeof(cplx), B, ldb * sizeof(cplx), k * sizeof(cplx), n,
+                                            cudaMemcpyDefault, c->stream), "stage B");
+            auto* bt = ws_get<cplx>(c, k * n);
+            check_cuda(c, conj_transpose(packed, (int)n, (int)k, bt, c->stream), "conj_transpose");
+            c->launches++;
+            dB = bt;
+            ldb = n;
+        } else {
+            dB = nullptr;
+        }
         auto* dC = static_cast<cplx*>(stage_out(c, C, m * ldc * sizeof(cplx), outs));
         if (k == 0) {
             check_cuda(c, cudaMemsetAsync(dC, 0, m * ldc * sizeof(cplx), c->stream), "memset");
@@ -172,7 +228,12 @@ int rrsvd_b200_qr(rrsvd_b200_ctx* c, const double* A, size_t m, size_t n, double
         const auto* dA = static_cast<const cplx*>(stage_in(c, A, m * n * sizeof(cplx)));
         auto* dQ = static_cast<cplx*>(stage_out(c, Q, m * n * sizeof(cplx), outs));
         if (dQ == nullptr) dQ = ws_get<cplx>(c, m * n);
-        orth(c, dA, (int)m, (int)n, dQ);
+        int* dn = ws_get<int>(c, 1);
+        orth(c, dA, (int)m, (int)n, dQ, dn);
+        int ndead = 0;
+        check_cuda(c, cudaMemcpyAsync(&ndead, dn, sizeof(int), cudaMemcpyDeviceToHost, c->stream), "D2H");
+        check_cuda(c, cudaStreamSynchronize(c->stream), "sync");
+        if (ndead > 0) complete_basis(c, dQ, (int)m, (int)n);
         if (R != nullptr) {
             auto* dR = static_cast<cplx*>(stage_out(c, R, n * n * sizeof(cplx), outs));
             gemm(c, kOpC, (int)n, (int)n, (int)m, dQ, (long long)n, dA, (long long)n, dR, (long long)n);

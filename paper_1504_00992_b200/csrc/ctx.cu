@@ -127,6 +127,19 @@ void release_lanes(rrsvd_b200_ctx* c) {
     c->ev_fork = nullptr;
 }
 
+void recover_after_failure(rrsvd_b200_ctx* c) {
+    if (c->home != nullptr) c->stream = c->home;
+    for (cudaStream_t l : c->lane)
+        if (l) cudaStreamSynchronize(l);
+    cudaStreamSynchronize(c->stream);
+    for (auto& p : c->pending) {  // timing events of launches that may never have run
+        c->event_pool.push_back(p.a);
+        c->event_pool.push_back(p.b);
+    }
+    c->pending.clear();
+    cudaGetLastError();
+}
+
 cudaEvent_t pooled_event(rrsvd_b200_ctx* c) {
     if (!c->event_pool.empty()) {
         cudaEvent_t e = c->event_pool.back();

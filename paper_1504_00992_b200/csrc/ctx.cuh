@@ -10,7 +10,8 @@
 
 struct rrsvd_b200_ctx {
     int device = 0;
-    cudaStream_t stream = nullptr;
+    cudaStream_t stream = nullptr;  // current stream (a lane or the side stream inside a call)
+    cudaStream_t home = nullptr;    // the caller's stream (ctx_create / set_stream)
     bool own_stream = false;
     std::string err;
     uint64_t launches = 0;
@@ -91,6 +92,19 @@ void release_staged(rrsvd_b200_ctx* c);
 void lanes_fork(rrsvd_b200_ctx* c, int n);
 void lanes_join(rrsvd_b200_ctx* c, int n);
 void release_lanes(rrsvd_b200_ctx* c);
+// After a failed public call: put c->stream back on the caller's stream and drain every lane
+// and the side stream, so no work the failed call forked still uses the workspace that the
+// boundary releases next (and later calls order against the caller's stream again).
+void recover_after_failure(rrsvd_b200_ctx* c);
+// Scoped stream switch: restores c->stream on every exit path (normal or exception).
+struct StreamSwitch {
+    rrsvd_b200_ctx* c;
+    cudaStream_t saved;
+    explicit StreamSwitch(rrsvd_b200_ctx* cc) : c(cc), saved(cc->stream) {}
+    ~StreamSwitch() { c->stream = saved; }
+    StreamSwitch(const StreamSwitch&) = delete;
+    StreamSwitch& operator=(const StreamSwitch&) = delete;
+};
 
 // zgemm timing: events around each GEMM launch (incl. its split-K reduction) while enabled.
 cudaEvent_t pooled_event(rrsvd_b200_ctx* c);

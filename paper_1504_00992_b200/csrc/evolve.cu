@@ -44,6 +44,7 @@ int mps_api(rrsvd_b200_mps* s, F&& f) {
         c->err = e.what();
         code = kCuda;
     }
+    if (code != kOk) recover_after_failure(c);
     ws_reset(c);
     return code;
 }
@@ -68,17 +69,26 @@ void ensure_lambda(rrsvd_b200_mps* s, int bond, size_t elems) {
 
 // Growth without freeing: the old buffer may still be read by work being enqueued; the caller
 // frees `old` after the streams that read it have joined.
-void grow_gamma(rrsvd_b200_mps* s, int site, size_t elems, std::vector<void*>& old) {
+// A replaced buffer, kept until the sweep's results are validated: freed after a good update,
+// swapped back (and the new buffer freed) when the bond's Θ was rejected.
+struct Regrown {
+    int kind;  // 0 gamma, 1 lambda
+    int idx;
+    void* old;
+    size_t old_cap;
+};
+
+void grow_gamma(rrsvd_b200_mps* s, int site, size_t elems, std::vector<Regrown>& old) {
     if (s->gcap[site] >= elems) return;
-    if (s->g[site]) old.push_back(s->g[site]);
+    old.push_back({0, site, s->g[site], s->gcap[site]});
     s->g[site] = nullptr;
     check_cuda(s->c, cudaMallocAsync(reinterpret_cast<void**>(&s->g[site]), elems * sizeof(cplx), s->c->stream),
                "alloc gamma");
     s->gcap[site] = elems;
 }
-void grow_lambda(rrsvd_b200_mps* s, int bond, size_t elems, std::vector<void*>& old) {
+void grow_lambda(rrsvd_b200_mps* s, int bond, size_t elems, std::vector<Regrown>& old) {
     if (s->lcap[bond] >= elems) return;
-    if (s->lam[bond]) old.push_back(s->lam[bond]);
+    old.push_back({1, bond, s->lam[bond], s->lcap[bond]});
     s->lam[bond] = nullptr;
     check_cuda(s->c, cudaMallocAsync(reinterpret_cast<void**>(&s->lam[bond]), elems * sizeof(double), s->c->stream),
                "alloc lambda");
@@ -373,7 +383,7 @@ void evolve_core(rrsvd_b200_mps* s, rrsvd_b200_ctx* c, size_t n_sweeps, const rr
                 // buffers, and the old ones are freed only after both lanes have joined.
                 std::vector<cplx*> gin1(nbnd), gin2(nbnd);
                 std::vector<double*> lin(nbnd);
-                std::vector<void*> old_bufs;
+                std::vector<std::vector<Regrown>> regrown(nbnd);
                 // An abort (tebd.cpp:317-321) leaves the bonds after the offending one untouched;
                 // the batch updates them all, so with an abort threshold in force the sweep's
                 // inputs are snapshotted and those bonds restored if it fires.
@@ -414,9 +424,9 @@ void evolve_core(rrsvd_b200_mps* s, rrsvd_b200_ctx* c, size_t n_sweeps, const rr
                     gin1[i] = s->g[b];
                     gin2[i] = s->g[b + 1];
                     lin[i] = s->lam[b];
-                    grow_gamma(s, b, (size_t)plans[i].m * plans[i].kmax, old_bufs);
-                    grow_gamma(s, b + 1, (size_t)plans[i].kmax * plans[i].n, old_bufs);
-                    grow_lambda(s, b, (size_t)plans[i].kmax, old_bufs);
+                    grow_gamma(s, b, (size_t)plans[i].m * plans[i].kmax, regrown[i]);
+                    grow_gamma(s, b + 1, (size_t)plans[i].kmax * plans[i].n, regrown[i]);
+                    grow_lambda(s, b, (size_t)plans[i].kmax, regrown[i]);
                 }
                 check_cuda(c, cudaEventRecord(ev[0], c->stream), "event");
                 const cudaStream_t main_stream = c->stream;
@@ -431,6 +441,7 @@ void evolve_core(rrsvd_b200_mps* s, rrsvd_b200_ctx* c, size_t n_sweeps, const rr
                                    ? std::max(1, std::min<int>({want, (int)nbnd, rrsvd_b200_ctx::kMaxLanes}))
                                    : 1;
                 if (nl > 1) lanes_fork(c, nl);
+                StreamSwitch lane_switch(c);  // c->stream is back on main_stream on every exit path
                 for (int lane = 0; lane < nl; ++lane) {
                     if (nl > 1) c->stream = c->lane[lane];
                     std::vector<ThetaJob> tj;
@@ -460,7 +471,6 @@ void evolve_core(rrsvd_b200_mps* s, rrsvd_b200_ctx* c, size_t n_sweeps, const rr
                 }
                 c->stream = main_stream;
                 if (nl > 1) lanes_join(c, nl);
-                for (void* p : old_bufs) cudaFreeAsync(p, c->stream);
                 check_cuda(c, cudaEventRecord(ev[3], c->stream), "event");
                 check_cuda(c, cudaMemcpyAsync(sc_host, sc_dev, nbnd * sizeof(DecimScalars), cudaMemcpyDeviceToHost,
                                               c->stream), "D2H");
@@ -470,11 +480,41 @@ void evolve_core(rrsvd_b200_mps* s, rrsvd_b200_ctx* c, size_t n_sweeps, const rr
                 cudaEventElapsedTime(&t01, ev[0], ev[1]);
                 cudaEventElapsedTime(&t12, ev[1], ev[2]);
                 cudaEventElapsedTime(&t23, ev[2], ev[3]);
+                // Validate every bond before committing any (the reference throws before it
+                // assigns, tebd.cpp:156-160).  A rejected bond's truncation kept nothing on the
+                // device, so its Γ/λ buffers were not written: its grown buffers are swapped
+                // back, the other bonds of the batch (valid results) are committed, and the seed
+                // counter is left where the reference's would be — the rejected call takes no
+                // seed (tebd.cpp:162 follows the check).
+                size_t first_bad = nbnd;
+                for (size_t i = 0; i < nbnd && first_bad == nbnd; ++i)
+                    if (sc_host[i].nonfinite || !(sc_host[i].total_sq > 0.0)) first_bad = i;
+                for (size_t i = 0; i < nbnd; ++i) {
+                    const bool bad = sc_host[i].nonfinite || !(sc_host[i].total_sq > 0.0);
+                    for (const Regrown& r : regrown[i]) {
+                        if (!bad) {
+                            if (r.old) cudaFreeAsync(r.old, c->stream);
+                            continue;
+                        }
+                        void*& cur = r.kind == 0 ? reinterpret_cast<void*&>(s->g[r.idx])
+                                                 : reinterpret_cast<void*&>(s->lam[r.idx]);
+                        if (cur) cudaFreeAsync(cur, c->stream);
+                        cur = r.old;
+                        (r.kind == 0 ? s->gcap[r.idx] : s->lcap[r.idx]) = r.old_cap;
+                    }
+                    if (!bad) {
+                        s->dr[bonds[i]] = sc_host[i].kept;
+                        s->dl[bonds[i] + 1] = sc_host[i].kept;
+                    }
+                }
+                if (first_bad < nbnd) {
+                    be->seed = seeds[first_bad];
+                    if (sc_host[first_bad].nonfinite) throw_contract(c, "decimate: theta has non-finite entries");
+                    throw_contract(c, "decimate: theta is identically zero");
+                }
                 for (size_t i = 0; i < nbnd; ++i) {
                     const int b = bonds[i];
                     const DecimScalars& h = sc_host[i];
-                    if (h.nonfinite) throw_contract(c, "decimate: theta has non-finite entries");
-                    if (h.total_sq == 0.0) throw_contract(c, "decimate: theta is identically zero");
                     s->dr[b] = h.kept;
                     s->dl[b + 1] = h.kept;
                     diag->kept_fraction *= 1.0 - h.discarded;
@@ -487,6 +527,9 @@ void evolve_core(rrsvd_b200_mps* s, rrsvd_b200_ctx* c, size_t n_sweeps, const rr
                     if (1.0 - diag->kept_fraction > abort_thr) {  // tebd.cpp:317-321
                         diag->aborted = 1;
                         diag->abort_step = step;
+                        // the reference returns here: the later bonds of the batch take no
+                        // seed (tebd.cpp:162, 317-321)
+                        be->seed -= (uint64_t)(nbnd - i - 1);
                         for (size_t j = i + 1; j < nbnd; ++j) {  // un-apply the later bonds of the batch
                             const int bj = bonds[j];
                             const Snap& sn = snaps[j];

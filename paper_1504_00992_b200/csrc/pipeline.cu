@@ -532,6 +532,7 @@ void small_svd_many(rrsvd_b200_ctx* c, const std::vector<SmallSvdSpec>& specs) {
     // The on-chip batch (one launch of a few clusters) runs on a side stream beside the block
     // Jacobi groups (many short launches with a host read per sweep), which leave SMs free.
     const cudaStream_t main_stream = c->stream;
+    StreamSwitch side_switch(c);  // restores c->stream on every exit path
     constexpr int kSide = rrsvd_b200_ctx::kMaxLanes - 1;
     const bool fork = !global.empty() && !onchip.empty() && c->stream != c->lane[kSide];
     if (fork) {
@@ -1213,6 +1214,7 @@ void decimate_many(rrsvd_b200_ctx* c, const std::vector<DecimJob>& jobs) {
             ta.cap = pl.fixed_precision ? 0 : (long long)j.chi_max;
             ta.renormalize = j.renormalize; ta.kept = &j.sc->kept;
             ta.lambda = j.lambda; ta.discarded = &j.sc->discarded;
+            ta.nonfinite = &j.sc->nonfinite;
             GammaArgs& ga = gb.a[gb.count++];
             ga = GammaArgs{};
             ga.U = outs[i].U; ga.ldu = ns[i]; ga.V = outs[i].V; ga.ldv = ns[i]; ga.ll = j.ll; ga.lr = j.lr;

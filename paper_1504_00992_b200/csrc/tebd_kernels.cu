@@ -242,6 +242,11 @@ __global__ void theta_unfold_kernel(const cplx* __restrict__ src, int d1, int d2
 __global__ void truncate_kernel(const TruncArgs a) {
     if (threadIdx.x != 0) return;
     const double total = *a.total_sq;
+    if ((a.nonfinite && *a.nonfinite) || !(total > 0.0)) {  // rejected Θ: nothing kept
+        *a.kept = 0;
+        *a.discarded = 0.0;
+        return;
+    }
     const double sigma1 = a.ns > 0 ? a.sigma[0] : 0.0;
     int kept = 0;
     for (int i = 0; i < a.ns; ++i) {
@@ -323,6 +328,11 @@ __global__ void truncate_many_kernel(const __grid_constant__ TruncBatch b) {
         // same code path as truncate_kernel (tebd.cpp:188-209)
         const TruncArgs& a = b.a[blockIdx.x];
         const double total = *a.total_sq;
+        if ((a.nonfinite && *a.nonfinite) || !(total > 0.0)) {  // rejected Θ: nothing kept
+            *a.kept = 0;
+            *a.discarded = 0.0;
+            return;
+        }
         const double sigma1 = a.ns > 0 ? a.sigma[0] : 0.0;
         int kept = 0;
         for (int i = 0; i < a.ns; ++i) {

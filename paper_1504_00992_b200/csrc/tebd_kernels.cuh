@@ -65,6 +65,11 @@ struct TruncArgs {
     int* kept;
     double* lambda;
     double* discarded;
+    // nullable: the finite check of the same Θ (tebd.cpp:156-160).  A non-finite or identically
+    // zero Θ keeps NOTHING (kept = 0: λ and the Γ reshape below write no element), so the
+    // caller can throw with the state's buffers unchanged, as the reference throws before
+    // assigning anything.
+    const int* nonfinite = nullptr;
 };
 cudaError_t truncate(const TruncArgs& a, cudaStream_t s);
 

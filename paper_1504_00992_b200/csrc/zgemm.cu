@@ -1,5 +1,6 @@
-#include <cstdlib>
 // zgemm.cu — see zgemm.cuh for the contract.
+#include <atomic>
+#include <cstdlib>
 #include <algorithm>
 
 #include "zgemm.cuh"
@@ -343,13 +344,17 @@ cudaError_t launch_cfg(GemmGroup& g, GemmOp opA, cudaStream_t s) {
     if (total == 0) return cudaSuccess;
     bool any_ks = false;
     for (int i = 0; i < g.count; ++i) any_ks |= g.p[i].ks != nullptr;
-    static bool configured = false;
-    if (!configured) {
+    // the smem opt-in is per device: one bit per ordinal (a process may drive several GPUs)
+    static std::atomic<unsigned long long> configured{0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const unsigned long long bit = 1ull << (dev & 63);
+    if (!(configured.load() & bit)) {
         cudaFuncSetAttribute(zgemm_dmma_kernel<CF, kOpN, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, CF::SMEM_BYTES);
         cudaFuncSetAttribute(zgemm_dmma_kernel<CF, kOpC, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, CF::SMEM_BYTES);
         cudaFuncSetAttribute(zgemm_dmma_kernel<CF, kOpN, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, CF::SMEM_BYTES);
         cudaFuncSetAttribute(zgemm_dmma_kernel<CF, kOpC, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, CF::SMEM_BYTES);
-        configured = true;
+        configured.fetch_or(bit);
     }
     if (opA == kOpN) {
         if (any_ks) zgemm_dmma_kernel<CF, kOpN, true><<<total, CF::NTHREADS, CF::SMEM_BYTES, s>>>(g);

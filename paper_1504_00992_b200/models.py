@@ -10,6 +10,8 @@ from __future__ import annotations
 
 import numpy as np
 
+from ._lib import ContractViolation
+
 SX = np.array([[0, 1], [1, 0]], np.complex128)
 SY = np.array([[0, -1j], [1j, 0]], np.complex128)
 SZ = np.array([[1, 0], [0, -1]], np.complex128)
@@ -72,6 +74,12 @@ def bond_gate(h: np.ndarray, scale: float) -> np.ndarray:
     the full matrix leaks ~1e-17 noise across blocks when eigenvalues of different blocks are
     degenerate).  TEDOPA boson-boson terms conserve the total excitation number, so their gates
     are block-diagonal; the device applies such gates block-sparsely."""
+    h = np.asarray(h, np.complex128)
+    if h.ndim != 2 or h.shape[0] != h.shape[1]:
+        raise ContractViolation("bond_gate: term must be square")
+    # tebd.cpp:241-246: the same Hermiticity test as the reference, before any factorisation
+    if h.size and np.max(np.abs(h - h.conj().T)) > 1e-9 * max(1.0, float(np.max(np.abs(h)))):
+        raise ContractViolation("bond_gate: term is not Hermitian")
     out = np.zeros(h.shape, np.complex128)
     for idx in sparsity_blocks(h):
         hb = h[np.ix_(idx, idx)]

@@ -59,22 +59,37 @@ def test_qr_orthonormal_and_reconstructs(ctx, m, n):
 
 
 def test_qr_zero_and_dependent_columns_no_nan(ctx):
-    """test_linalg.cpp:152-159: a zero column must not produce NaN; span is preserved."""
+    """test_linalg.cpp:152-159 and linalg.hpp:35-37: rank-deficient input (a zero column, a
+    dependent column) — Q finite and orthonormal (< 1e-12) over ALL columns, A = Q R, and the
+    R diagonal entries of the dependent columns (near) zero."""
     rng = np.random.default_rng(3)
     a = cplx_randn(rng, 64, 12)
     a[:, 4] = 0
     a[:, 7] = 2 * a[:, 2]
     q, r = P.qr(a, ctx=ctx)
     assert np.all(np.isfinite(q)) and np.all(np.isfinite(r))
-    assert np.linalg.norm(q @ (q.conj().T @ a) - a) / np.linalg.norm(a) < 1e-10
-    live = np.linalg.norm(q, axis=0) > 0.5
-    ql = q[:, live]
-    assert np.linalg.norm(ql.conj().T @ ql - np.eye(ql.shape[1])) < 1e-12
+    assert np.linalg.norm(q.conj().T @ q - np.eye(12)) < 1e-12
+    assert np.linalg.norm(q @ r - a) / np.linalg.norm(a) < 1e-12
+    assert abs(r[4, 4]) < 1e-12 and abs(r[7, 7]) < 1e-12 * np.linalg.norm(a)
+    assert np.allclose(np.triu(r), r, atol=1e-12 * np.linalg.norm(a))
+
+
+def test_qr_zero_column_reference_test(ctx):
+    """test_linalg.cpp:152-159 verbatim: 5 x 3, column 1 zeroed — all_finite(Q),
+    orthonormality_residual(Q) < 1e-12, |R(1,1)| < 1e-12."""
+    rng = np.random.default_rng(9)
+    a = cplx_randn(rng, 5, 3)
+    a[:, 1] = 0
+    q, r = P.qr(a, ctx=ctx)
+    assert np.all(np.isfinite(q))
+    assert np.max(np.abs(q.conj().T @ q - np.eye(3))) < 1e-12
+    assert abs(r[1, 1]) < 1e-12
 
 
 @pytest.mark.parametrize("l", [90, 200])
 def test_qr_ill_conditioned(ctx, l):
-    """TEBD spectra decay fast: cond(Y) up to 1e16 must not break the orthonormalisation."""
+    """TEBD spectra decay fast: cond(Y) up to 1e16 (numerically rank-deficient) must not break the
+    orthonormalisation — every column of Q orthonormal, the span of Y kept."""
     rng = np.random.default_rng(5)
     m = 1500
     uq, _ = np.linalg.qr(cplx_randn(rng, m, l))
@@ -82,9 +97,7 @@ def test_qr_ill_conditioned(ctx, l):
     for dec in (1e-8, 1e-14, 1e-20):
         y = (uq * np.logspace(0, np.log10(dec), l)) @ vq.conj().T
         q, _ = P.qr(y, ctx=ctx)
-        live = np.linalg.norm(q, axis=0) > 0.5
-        ql = q[:, live]
-        assert np.linalg.norm(ql.conj().T @ ql - np.eye(ql.shape[1])) < 1e-12
+        assert np.linalg.norm(q.conj().T @ q - np.eye(l)) < 1e-12
         assert np.linalg.norm(y - q @ (q.conj().T @ y), 2) < 1e-11
 
 
