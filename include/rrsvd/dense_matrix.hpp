@@ -1,0 +1,7 @@
+// rrsvd/dense_matrix.hpp — forwarding header: the reference's include path resolves to the B200 drop-in
+// (rrsvd_b200/rrsvd.hpp; declarations of the out-of-scope helpers in reference_aux.hpp).
+#ifndef RRSVD_DENSE_MATRIX_HPP
+#define RRSVD_DENSE_MATRIX_HPP
+#include "../rrsvd_b200/rrsvd.hpp"
+#include "../rrsvd_b200/reference_aux.hpp"
+#endif

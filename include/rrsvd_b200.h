@@ -116,6 +116,12 @@ int rrsvd_b200_frobenius_norm(rrsvd_b200_ctx* ctx, const double* A, size_t m, si
  * device's log/sin/cos. */
 int rrsvd_b200_gaussian_test_matrix(rrsvd_b200_ctx* ctx, size_t n, size_t l, uint64_t seed,
                                     int mode, double* out);
+/* randomized_range_finder (randomized.cpp:88-99): Q (m x l, orthonormal) spanning
+ * (A A^H)^q A Omega, re-orthonormalised after every product; l <= min(m, n).  omega as for
+ * rrsvd_b200_sketched_svd.  Replaces rrsvd::randomized_range_finder -> RangeBasis
+ * (randomized.hpp:25-28,52-53). */
+int rrsvd_b200_range_finder(rrsvd_b200_ctx* ctx, const double* A, size_t m, size_t n, size_t l,
+                            size_t q, uint64_t seed, int omega_mode, const double* omega, double* Q);
 /* rrsvd_sketched_svd (randomized.cpp:101-107): U m x l, S l, V n x l, *discarded = w.
  * omega: NULL -> generated from `seed` with `omega_mode`; else the caller's n x l sketch
  * ("Omega fed identically"). */

@@ -338,11 +338,11 @@ def decimate_unfolded(m, d1: int, d2: int, ll, lr, chi_max: int, trunc_tol: floa
     info = L.DecimInfo()
     be = backend.to_c()
     call_seed = backend.seed
-    backend.seed += 1  # tebd.cpp:162 — consumed even on the deterministic path
     c.check(L.lib().rrsvd_b200_decimate_unfolded(
         c.h, ptr(m), sz(d1), sz(d2), sz(cl), sz(cr), ptr(ll_), ptr(lr_), sz(chi_max),
         C.c_double(trunc_tol), C.byref(be), C.c_uint64(call_seed), C.c_int(backend.omega_mode),
         ptr(omega), C.c_int(int(renormalize)), ptr(gl), ptr(lam), ptr(gr), C.byref(info)))
+    backend.seed += 1  # tebd.cpp:162 — consumed even on the deterministic path, after the Θ checks
     k = int(info.chi)
     return DecimationResult(gl[:cl * d1 * k].reshape(cl, d1, k), lam[:k],
                             gr[:k * d2 * cr].reshape(k, d2, cr), info.discarded, k,

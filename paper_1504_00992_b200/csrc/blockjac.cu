@@ -454,10 +454,10 @@ __global__ void __launch_bounds__(kBjFinThreads) bj_rank_kernel(const __grid_con
     for (int s = threadIdx.x; s < cp; s += kBjFinThreads) {
         int rk = -1;
         if (orig[s] >= 0) {
-            const double v = sig[s];
+            const double v = sig[s], kv = rank_key(v);
             rk = 0;
             for (int t = 0; t < cp; ++t)
-                if (orig[t] >= 0) rk += (sig[t] > v) || (sig[t] == v && orig[t] < orig[s]);
+                if (orig[t] >= 0) rk += (rank_key(sig[t]) > kv) || (rank_key(sig[t]) == kv && orig[t] < orig[s]);
             a.sigma[pr][rk] = v;
         }
         a.rank_ws[(size_t)pr * cp + s] = rk;

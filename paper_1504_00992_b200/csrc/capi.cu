@@ -293,6 +293,27 @@ int rrsvd_b200_gaussian_test_matrix(rrsvd_b200_ctx* c, size_t n, size_t l, uint6
     });
 }
 
+int rrsvd_b200_range_finder(rrsvd_b200_ctx* c, const double* A, size_t m, size_t n, size_t l, size_t q,
+                            uint64_t seed, int omega_mode, const double* omega, double* Q) {
+    return api(c, [&] {
+        if (l > std::min(m, n)) throw_contract(c, "randomized_range_finder: l > min(m, n)");
+        if (l < 1) throw_contract(c, "gaussian_test_matrix: requires n >= l >= 1");
+        if (Q == nullptr) throw_contract(c, "randomized_range_finder: null output");
+        std::vector<OutBuf> outs;
+        const auto* dA = static_cast<const cplx*>(stage_in(c, A, m * n * sizeof(cplx)));
+        const cplx* dO = static_cast<const cplx*>(stage_in(c, omega, n * l * sizeof(cplx)));
+        if (dO == nullptr) {
+            cplx* o = ws_get<cplx>(c, n * l);
+            make_omega(c, (int)n, (int)l, seed, omega_mode, o);
+            dO = o;
+        }
+        auto* dQ = static_cast<cplx*>(stage_out(c, Q, m * l * sizeof(cplx), outs));
+        range_finder_many(c, {RangeSpec{dA, (int)m, (int)n, (int)l, (int)q, dO, dQ}});
+        complete_basis(c, dQ, (int)m, (int)l);  // RangeBasis::q_matrix is orthonormal (randomized.hpp:25-28)
+        finish_out(c, outs);
+    });
+}
+
 static void sketch_common(rrsvd_b200_ctx* c, const double* A, size_t m, size_t n, size_t l, size_t q,
                           uint64_t seed, int omega_mode, const double* omega, size_t keep, double* U,
                           double* S, double* V, double* discarded) {

@@ -40,6 +40,11 @@ __device__ __forceinline__ void cfmac(cplx& acc, cplx a, cplx b) {
     acc.y = fma(-a.y, b.x, acc.y);
 }
 
+// Sort key for descending ranks of norms / singular values: NaN (a non-finite input the
+// boundary rejects afterwards) ranks last, so a rank loop still yields a permutation and no
+// kernel indexes out of range before the finite check throws.
+__host__ __device__ inline double rank_key(double x) { return x == x ? x : -1.0; }
+
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

@@ -496,9 +496,9 @@ __global__ void __launch_bounds__(kColPermThreads) colperm_rank_kernel(const __g
         __syncthreads();
     }
     for (int j = threadIdx.x; j < c; j += kColPermThreads) {
-        const double v = nrm[j];
+        const double v = rank_key(nrm[j]);
         int rk = 0;
-        for (int t = 0; t < c; ++t) rk += (nrm[t] > v) || (nrm[t] == v && t < j);
+        for (int t = 0; t < c; ++t) rk += (rank_key(nrm[t]) > v) || (rank_key(nrm[t]) == v && t < j);
         b.perm[p][rk] = j;
     }
 }
@@ -586,8 +586,8 @@ __global__ void __launch_bounds__(256) jacobi_finish_kernel(const __grid_constan
     __syncthreads();
     for (int j = tid; j < c; j += blockDim.x) {
         int rk = 0;
-        const double sj = sig[j];
-        for (int i = 0; i < c; ++i) rk += (sig[i] > sj) || (sig[i] == sj && i < j);
+        const double sj = rank_key(sig[j]);
+        for (int i = 0; i < c; ++i) rk += (rank_key(sig[i]) > sj) || (rank_key(sig[i]) == sj && i < j);
         pos[j] = rk;
     }
     __syncthreads();

@@ -211,9 +211,10 @@ def evolve(mps: DeviceMps, terms: dict, dt: float, n_steps: int, backend: Decima
     nrec = n_steps * sum(len(range(p, nb, 2)) for p, _ in plan) if record_updates else 0
     recs = (UpdateRecord * max(nrec, 1))()
     fn = L.lib().rrsvd_b200_evolve_prepared if prepared else L.lib().rrsvd_b200_evolve
-    mps.ctx.check(fn(mps.h, sz(len(plan)), sweeps, arr, sz(n_steps), C.byref(be), C.byref(opt), C.byref(diag),
-                     recs if record_updates else None, sz(nrec)))
-    backend.seed = be.seed
+    rc = fn(mps.h, sz(len(plan)), sweeps, arr, sz(n_steps), C.byref(be), C.byref(opt), C.byref(diag),
+            recs if record_updates else None, sz(nrec))
+    backend.seed = be.seed  # advanced even when a sweep throws (the calls before it took seeds)
+    mps.ctx.check(rc)
     ups = [{"step": r.step, "bond": r.bond, "chi": r.chi, "discarded_weight": r.discarded_weight,
             "t_theta_us": r.t_theta_us, "t_gate_us": r.t_gate_us, "t_svd_us": r.t_svd_us,
             "backend": "rrsvd" if r.randomized_path else "det"}
