@@ -79,6 +79,20 @@ def workload(name: str):
     raise SystemExit(f"unknown workload {name}")
 
 
+def bench_config(wl, ups, world) -> dict:
+    """The `config` object — identical in both arms (ours and --impl reference)."""
+    from paper_1504_00992_b200 import models as M
+    dims = M.saturated_bond_dims(wl["site_dims"], wl["chi"])
+    sd = wl["site_dims"]
+    mps_bytes = sum(16 * (1 if s == 0 else dims[s - 1]) * sd[s] * (1 if s == len(sd) - 1 else dims[s])
+                    for s in range(len(sd))) + 8 * sum(dims)
+    return {"workload": wl["name"], "desc": wl["desc"], "sites": len(sd), "chi": wl["chi"],
+            "updates_per_step": ups, "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
+            "l2": ("inputs larger than L2 (MPS %.0f MB > 126 MB)" % (mps_bytes / 1e6)) if mps_bytes > 126e6 else
+                  ("MPS %.0f MB fits L2; no flush: consecutive TEBD steps rewrite the whole state, which is "
+                   "the workload" % (mps_bytes / 1e6))}
+
+
 def updates_per_step(site_dims, terms):
     nb = len(site_dims) - 1
     return sum(1 for par, _ in [(1, .5), (0, 1.), (1, .5)] for b in range(par, nb, 2) if b in terms)
@@ -251,6 +265,7 @@ def run_partitioned(args, rank, world, local_rank):
     pin_l = [torch.from_numpy(lam(gs)).pin_memory() if i + 1 < len(local) else None for i, gs in enumerate(local)]
     own = b - a
     e2e_steps = max(1, min(args.steps, 2))
+    out_bufs = [torch.empty(blk.mps.dims(i), dtype=torch.complex128).pin_memory() for i in range(own)]
     dist.barrier()
     torch.cuda.synchronize()
     te0 = time.perf_counter()
@@ -263,7 +278,9 @@ def run_partitioned(args, rank, world, local_rank):
         part.evolve(gates, plan, dt, 1, be, 7, step0=st)
         d2h = 0
         for i in range(own):
-            buf = torch.empty(blk.mps.dims(i), dtype=torch.complex128).pin_memory()
+            if tuple(out_bufs[i].shape) != blk.mps.dims(i):  # (saturated state: never)
+                out_bufs[i] = torch.empty(blk.mps.dims(i), dtype=torch.complex128).pin_memory()
+            buf = out_bufs[i]
             ctx.check(P.lib().rrsvd_b200_mps_get_site(blk.mps.h, i, None, C.c_void_p(buf.data_ptr()), None))
             d2h += buf.numel() * 16
     torch.cuda.synchronize()
@@ -378,31 +395,32 @@ def run_ours(args, rank, world, local_rank):
         elapsed = float(t.item())
     steps_per_s = world * args.steps / elapsed
 
-    # ---- end-to-end through the C ABI with HOST buffers (pinned), H2D + D2H inside the region
+    # ---- end-to-end through the C ABI with HOST buffers (pinned): the SAME consecutive sequence
+    # of args.steps steps as `value`, each step uploading the state from host memory
+    # (rrsvd_b200_state_upload), stepping, and downloading it back (rrsvd_b200_state_download);
+    # the next step starts from the downloaded state.  Buffers are allocated before the region.
+    mps.load(gammas, lambdas)
     pin_g = [torch.from_numpy(g).pin_memory() for g in gammas]
     pin_l = [torch.from_numpy(l).pin_memory() for l in lambdas]
-    h2d = state_bytes(gammas, lambdas)
-    e2e_steps = max(1, min(args.steps, 3))
-    out_g = [torch.empty(g.shape, dtype=torch.complex128).pin_memory() for g in gammas]
+    h2d = d2h = state_bytes(gammas, lambdas)
     if dist:
         dist.barrier()
+    torch.cuda.synchronize()
     te0 = time.perf_counter()
-    d2h = 0
-    out_l = [torch.empty(l.shape, dtype=torch.float64).pin_memory() for l in lambdas]
-    for _ in range(e2e_steps):
-        mps.upload(pin_g, pin_l)  # rrsvd_b200_state_upload: every Γ and λ, one sync
+    for _ in range(args.steps):
+        mps.upload(pin_g, pin_l)
         one_step()
         dims = mps.all_dims()
-        for s in range(len(site_dims)):
-            if tuple(out_g[s].shape) != dims[s]:
-                out_g[s] = torch.empty(dims[s], dtype=torch.complex128).pin_memory()
+        for s_ in range(len(site_dims)):  # (the saturated state keeps its dims: no reallocation)
+            if tuple(pin_g[s_].shape) != dims[s_]:
+                pin_g[s_] = torch.empty(dims[s_], dtype=torch.complex128).pin_memory()
         for b in range(len(site_dims) - 1):
-            if out_l[b].shape[0] != dims[b][2]:
-                out_l[b] = torch.empty(dims[b][2], dtype=torch.float64).pin_memory()
-        mps.download(out_g, out_l)  # rrsvd_b200_state_download: every Γ and λ, one sync
-        d2h = sum(g.numel() * 16 for g in out_g) + sum(l.numel() * 8 for l in out_l)
+            if pin_l[b].shape[0] != dims[b][2]:
+                pin_l[b] = torch.empty(dims[b][2], dtype=torch.float64).pin_memory()
+        mps.download(pin_g, pin_l)
+        d2h = sum(g.numel() * 16 for g in pin_g) + sum(l.numel() * 8 for l in pin_l)
     te1 = time.perf_counter()
-    e2e = world * e2e_steps / (te1 - te0)
+    e2e = world * args.steps / (te1 - te0)
 
     clocks = clk.summary()
     achieved = fl.value / (ms.value * 1e-3) / 1e12 if ms.value > 0 else 0.0
@@ -412,10 +430,8 @@ def run_ours(args, rank, world, local_rank):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * elapsed / args.steps, 3),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128 (fp64)",
             "data": "synthetic χ-saturated MPS (Gaussian Γ, λ∝0.9^i) + real TEDOPA bond gates",
-            "config": {"workload": wl["name"], "desc": wl["desc"], "sites": len(site_dims), "chi": chi,
-                       "updates_per_step": ups, "sketch": "Philox in-kernel",
-                       "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
-                       "l2": "inputs larger than L2 (MPS %.0f MB)" % (h2d / 1e6)},
+            "config": bench_config(wl, ups, world),
+            "sketch": "Philox in-kernel (the reference arm: its mt19937_64 stream)",
             "decimations_per_s": round(world * ups * args.steps / elapsed, 3),
             "roofline": {"bound": "tensor",
                          "kernel": "zgemm_dmma_kernel: every zgemm launch of one step (serial roofline pass,"
@@ -432,8 +448,9 @@ def run_ours(args, rank, world, local_rank):
                          "serial_step_ms": round(1e3 * serial_step_s, 3),
                          "step_level_tflops": round(fl.value / (elapsed / args.steps) / 1e12, 3),
                          "gemm_launches": int(calls.value), "stages": stages, **traffic_entry()},
-            "e2e": {"value": round(e2e, 6), "unit": "steps/s", "h2d_bytes_per_step": h2d,
-                    "d2h_bytes_per_step": int(d2h)},
+            "e2e": {"value": round(e2e, 6), "unit": "steps/s", "h2d_bytes_per_step": int(h2d),
+                    "d2h_bytes_per_step": int(d2h), "steps": args.steps,
+                    "note": "same consecutive steps as value; whole MPS H2D before and D2H after every step"},
             "gpu_launches": int(gpu_launches),
             "clocks": clocks,
             "device_time_per_step_ms": round(dev_update_us / 1e3 / args.steps, 3),
@@ -611,52 +628,86 @@ def ref_update_sample(ref, wl, gammas, lambdas, gates, plan, bonds, seed):
 
 def cpu_baseline(args, wl, gammas, lambdas, gates, plan, samples=2):
     from oracle import ref
-    cores = os.cpu_count() or 1
-    ref.set_threads(cores)
+    host = host_info()
+    ref.set_threads(host["cores"])
     nb = len(wl["site_dims"]) - 1
     bonds = [nb // 2 - 1 + i for i in range(samples)]
     sec = ref_update_sample(ref, wl, gammas, lambdas, gates, plan, bonds, 7)
     ups = updates_per_step(wl["site_dims"], wl["terms"])
-    return {"value": round(1.0 / (sec * ups), 8), "unit": "steps/s", "cores": cores, "kind": "reference",
+    return {"value": round(1.0 / (sec * ups), 8), "unit": "steps/s", "cores": host["cores"], "kind": "reference",
             "sample": f"{samples} interior bond updates (build_theta+apply_gate+decimate, "
                       f"{'RRSVD' if wl['backend'].get('randomized') else 'deterministic SVD'}) of the "
-                      f"same state, {sec:.3f} s/update, extrapolated x{ups} updates/step",
-            "blas": ref.blas_info()["core"]}
+                      f"same state, {sec:.3f} s/update, extrapolated x{ups} updates/step (the --impl "
+                      f"reference arm times a whole evolve step)",
+            "cpu_model": host["cpu_model"], "blas": ref.blas_info()["config"]}
+
+
+def host_info() -> dict:
+    """CPU model, the cores this process is pinned to (taskset equivalent: sched_setaffinity on
+    every core the process may use) and the reference BLAS build."""
+    model = "unknown"
+    try:
+        with open("/proc/cpuinfo") as f:
+            model = next(l.split(":", 1)[1].strip() for l in f if l.startswith("model name"))
+    except (OSError, StopIteration):
+        pass
+    cores = sorted(os.sched_getaffinity(0))
+    os.sched_setaffinity(0, cores)
+    return {"cpu_model": model, "cores": len(cores), "affinity": f"{cores[0]}-{cores[-1]}" if cores else "",
+            "online_cpus": os.cpu_count()}
 
 
 def run_reference(args, rank, world):
+    """The reference's OWN evolve (tebd.cpp:260-326) — one full TEBD step, evolve(state, ..., 1)
+    exactly as its tebd-run driver calls it per step (experiments.cpp:351-352), gate rebuild
+    (tebd.cpp:276-285) included — on the same synthetic saturated state as our arm, timed on the
+    host cores.  A C3 step takes minutes on a CPU, so this arm times ONE step whatever --steps
+    says (reported as "steps": 1); the warm-up is one interior bond update (BLAS thread pool,
+    page-in), not a whole step."""
     if rank != 0:
         return
     from oracle import ref
     from paper_1504_00992_b200 import models as M
-    from paper_1504_00992_b200.tebd import build_gates
     if not ref.available():
         emit({"impl": "reference", "unavailable": "oracle/_ref/librrsvd_ref.so not built"})
         return
-    cores = os.cpu_count() or 1
-    ref.set_threads(cores)
+    host = host_info()
+    ref.set_threads(host["cores"])
+    blas = ref.blas_info()
     wl = workload(args.workload)
-    plan, gates = build_gates(wl["site_dims"], wl["terms"], wl["dt"])
-    gammas, lambdas = M.synthetic_saturated_mps(wl["site_dims"], wl["chi"], seed=1)
-    nb = len(wl["site_dims"]) - 1
-    ups = updates_per_step(wl["site_dims"], wl["terms"])
-    for w in range(args.warmup):
-        ref_update_sample(ref, wl, gammas, lambdas, gates, plan, [nb // 2], 100 + w)
-    secs = []
-    for k in range(args.steps):
-        secs.append(ref_update_sample(ref, wl, gammas, lambdas, gates, plan, [nb // 2 - 1 + (k % 2)], 7 + k))
-    per_update = sum(secs) / len(secs)
-    v = 1.0 / (per_update * ups)
+    site_dims, terms, chi = wl["site_dims"], wl["terms"], wl["chi"]
+    gammas, lambdas = M.synthetic_saturated_mps(site_dims, chi, seed=1)
+    n = len(site_dims)
+    ups = updates_per_step(site_dims, terms)
+    rm = ref.RefMps(site_dims, [np.eye(d, dtype=complex)[0] for d in site_dims], chi, 0.0)
+    for s_ in range(n):
+        rm.set_site(s_, gammas[s_], lambdas[s_] if s_ < n - 1 else None)
+    from paper_1504_00992_b200.tebd import build_gates
+    plan, gates = build_gates(site_dims, terms, wl["dt"])
+    tw = time.perf_counter()
+    ref_update_sample(ref, wl, gammas, lambdas, gates, plan, [(n - 1) // 2], 100)
+    warm_s = time.perf_counter() - tw
+    be = ref.Backend(**wl["backend"])
+    t0 = time.perf_counter()
+    d = rm.evolve(terms, wl["dt"], 1, be)
+    wall = time.perf_counter() - t0
+    upd = d["update_us"] / 1e6
+    v = 1.0 / wall
+    sample = (f"one full step: the reference evolve(state, terms, plan, 1, backend) on the same synthetic "
+              f"state ({d['n_updates']} updates, {wall:.1f} s incl. the per-call gate rebuild; "
+              f"{upd:.1f} s in build_theta+apply_gate+decimate)")
     emit({
         "impl": "reference", "metric": METRIC, "value": round(v, 8), "unit": "steps/s", "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * per_update * ups, 1),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128 (fp64)",
-        "data": "synthetic χ-saturated MPS + real TEDOPA bond gates",
-        "config": {"workload": wl["name"], "desc": wl["desc"]},
-        "cpu_baseline": {"value": round(v, 8), "unit": "steps/s", "cores": cores, "kind": "reference",
-                         "sample": f"each step = 1 interior bond update (build_theta+apply_gate+decimate) "
-                                   f"timed on the host, extrapolated x{ups} updates/step",
-                         "blas": ref.blas_info()["core"]},
+        "steps": 1, "warmup": 0, "steps_requested": args.steps, "warmup_requested": args.warmup,
+        "warmup_note": f"one interior bond update ({warm_s:.1f} s) instead of whole steps",
+        "ms_per_step": round(1e3 * wall, 1), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "c128 (fp64)", "data": "synthetic χ-saturated MPS (Gaussian Γ, λ∝0.9^i) + real TEDOPA bond gates",
+        "config": bench_config(wl, ups, world),
+        "steps_per_s_excl_gate_rebuild": round(1.0 / upd, 8) if upd > 0 else None,
+        "decimations_per_s": round(d["n_updates"] / wall, 4),
+        "cpu_baseline": {"value": round(v, 8), "unit": "steps/s", "cores": host["cores"], "kind": "reference",
+                         "sample": sample, "cpu_model": host["cpu_model"], "affinity": host["affinity"],
+                         "blas": blas["config"], "blas_core": blas["core"], "blas_threads": blas["threads"]},
         "e2e": {"value": round(v, 8), "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     })
 

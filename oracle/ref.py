@@ -402,13 +402,13 @@ class RefMps:
         bonds = np.array(sorted(terms), np.uint64)
         mats = _c(np.concatenate([_c(terms[int(b)]).ravel() for b in bonds]))
         be = backend.to_c()
-        diag = np.zeros(5, np.float64)
+        diag = np.zeros(6, np.float64)
         _check(lib().ref_evolve(C.c_void_p(self.h), _p(bonds), _p(mats), U64(bonds.size),
                                 C.c_double(dt), U64(n_steps), C.byref(be),
                                 C.c_double(abort_threshold), int(renormalize), _p(diag)))
         backend.seed = be.seed
         return {"kept_fraction": diag[0], "max_bond_dim": int(diag[1]), "aborted": bool(diag[2]),
-                "abort_step": int(diag[3]), "n_updates": int(diag[4])}
+                "abort_step": int(diag[3]), "n_updates": int(diag[4]), "update_us": float(diag[5])}
 
     def expectation_local(self, site: int, op) -> complex:
         op = _c(op)

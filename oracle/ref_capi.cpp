@@ -438,6 +438,9 @@ int ref_evolve(void* h, const std::uint64_t* bonds, const double* mats, std::uin
         diag_out[2] = d.aborted ? 1.0 : 0.0;
         diag_out[3] = static_cast<double>(d.abort_step);
         diag_out[4] = static_cast<double>(d.updates.size());
+        double us = 0.0;  // the reference's own per-update timers (tebd.cpp:296-306, UpdateRecord)
+        for (const auto& u : d.updates) us += u.t_theta_us + u.t_gate_us + u.t_svd_us;
+        diag_out[5] = us;
     });
 }
 

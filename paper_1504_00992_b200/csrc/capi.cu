@@ -64,16 +64,16 @@ void copy_out(rrsvd_b200_ctx* c, void* dst, const void* src, size_t bytes) {
 // dead column slots.  R = Q^H A afterwards has (numerically) zero rows there, and Q R = A still
 // holds because A lies in the span of the live columns.
 void complete_basis(rrsvd_b200_ctx* c, cplx* Q, int m, int n) {
-    // column norms^2 = diag(Q^H Q)
-    cplx* G = ws_get<cplx>(c, (size_t)n * n);
-    gemm(c, kOpC, n, n, m, Q, n, Q, n, G, n);
-    std::vector<cplx> diag(n);
-    check_cuda(c, cudaMemcpy2DAsync(diag.data(), sizeof(cplx), G, (size_t)(n + 1) * sizeof(cplx), sizeof(cplx), n,
-                                    cudaMemcpyDeviceToHost, c->stream), "D2H diag");
+    double* nrm = ws_get<double>(c, (size_t)n);
+    check_cuda(c, column_norms2(Q, m, n, nrm, c->stream), "column_norms2");
+    c->launches++;
+    std::vector<double> diag(n);
+    check_cuda(c, cudaMemcpyAsync(diag.data(), nrm, (size_t)n * sizeof(double), cudaMemcpyDeviceToHost, c->stream),
+               "D2H norms");
     check_cuda(c, cudaStreamSynchronize(c->stream), "sync");
     std::vector<int> dead;
     for (int j = 0; j < n; ++j)
-        if (!(diag[j].x > 0.5)) dead.push_back(j);
+        if (!(diag[j] > 0.5)) dead.push_back(j);
     const int nd = (int)dead.size();
     if (nd == 0) return;
     cplx* E = ws_get<cplx>(c, (size_t)m * nd);
@@ -276,6 +276,12 @@ int rrsvd_b200_svd(rrsvd_b200_ctx* c, const double* A, size_t m, size_t n, doubl
         if (!dS) dS = ws_get<double>(c, r);
         if (!dV) dV = ws_get<cplx>(c, n * r);
         svd_jacobi(c, dA, (int)m, (int)n, dU, dS, dV);
+        // svd_full's U and V have orthonormal columns for ANY A (linalg.hpp:17-26, zgesdd): the
+        // singular vectors of exactly-zero singular values come back as zero columns from the
+        // Jacobi finish and get an orthonormal completion here (the decimation path truncates
+        // them away and never needs it)
+        if (U != nullptr) complete_basis(c, dU, (int)m, (int)r);
+        if (V != nullptr) complete_basis(c, dV, (int)n, (int)r);
         finish_out(c, outs);
     });
 }

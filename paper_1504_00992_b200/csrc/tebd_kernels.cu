@@ -668,6 +668,27 @@ cudaError_t fill_int(int* p, int v, cudaStream_t s) {
     return cudaGetLastError();
 }
 
+__global__ void __launch_bounds__(256) column_norms2_kernel(const cplx* __restrict__ A, int m, int n,
+                                                              double* __restrict__ out) {
+    __shared__ double part[8][33];
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5, j = blockIdx.x * 32 + tx;
+    double a = 0.0;
+    if (j < n)
+        for (int i = ty; i < m; i += 8) a += cabs2(A[(long long)i * n + j]);
+    part[ty][tx] = a;
+    __syncthreads();
+    if (ty == 0 && j < n) {
+        double s = 0.0;
+        for (int r = 0; r < 8; ++r) s += part[r][tx];
+        out[j] = s;
+    }
+}
+
+cudaError_t column_norms2(const cplx* A, int m, int n, double* out, cudaStream_t s) {
+    column_norms2_kernel<<<(n + 31) / 32, 256, 0, s>>>(A, m, n, out);
+    return cudaGetLastError();
+}
+
 cudaError_t conj_transpose(const cplx* A, int rows, int cols, cplx* out, cudaStream_t s) {
     dim3 grid((cols + 31) / 32, (rows + 31) / 32);
     conj_transpose_kernel<<<grid, 256, 0, s>>>(A, rows, cols, out);

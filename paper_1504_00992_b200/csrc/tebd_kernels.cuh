@@ -125,6 +125,8 @@ cudaError_t fill_int(int* p, int v, cudaStream_t s);
 
 // out (cols x rows) = A^H for A (rows x cols), both row-major.
 cudaError_t conj_transpose(const cplx* A, int rows, int cols, cplx* out, cudaStream_t s);
+// out[j] = sum_i |A(i, j)|^2 for a row-major m x n matrix (fixed summation order).
+cudaError_t column_norms2(const cplx* A, int m, int n, double* out, cudaStream_t s);
 
 // *w = clamp(1 - sum_{i<k} sigma_i^2 / total_sq, 0, 1)   (randomized.cpp:68-75)
 cudaError_t discarded_weight(const double* sigma, int k, const double* total_sq, double* w,

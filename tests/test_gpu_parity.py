@@ -122,6 +122,20 @@ def test_svd_full_matches_reference(ctx, ref, m, n):
     assert np.linalg.norm(v.conj().T @ v - np.eye(r)) < 1e-11
 
 
+def test_svd_full_rank_deficient_orthonormal_vectors(ctx):
+    """svd_full (linalg.hpp:17-26, zgesdd): U and V have orthonormal columns for ANY input — the
+    zero matrix, and a rank-3 matrix whose trailing singular values vanish exactly."""
+    for a in (np.zeros((6, 4), complex), None):
+        if a is None:
+            rng = np.random.default_rng(4)
+            a = cplx_randn(rng, 9, 3) @ cplx_randn(rng, 3, 7)
+        u, s, v = P.svd_full(a, ctx=ctx)
+        r = min(a.shape)
+        assert np.linalg.norm(u.conj().T @ u - np.eye(r)) < 1e-12
+        assert np.linalg.norm(v.conj().T @ v - np.eye(r)) < 1e-12
+        assert np.linalg.norm((u * s) @ v.conj().T - a) <= 1e-12 * max(1.0, np.linalg.norm(a))
+
+
 # ------------------------------------------------------------------ RRSVD (randomized.cpp)
 
 def c1_matrix(ref, n=512):
