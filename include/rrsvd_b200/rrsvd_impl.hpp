@@ -272,15 +272,15 @@ RRSVD_B200_API SvdResult rrsvd_fixed_precision(const DenseMatrix& a, const Accur
     out.tolerance_certified = cert != 0;
     return out;
 }
-// randomized.hpp:86-89: the smallest k whose implied Frobenius residual
-// sqrt(||A||^2 - sum_{i<k} sigma_i^2) is within rel_tolerance * ||A||; sigma.size() if none.
+// randomized.hpp:86-89: the smallest k (0 included: nothing kept) whose implied Frobenius
+// residual sqrt(||A||^2 - sum_{i<k} sigma_i^2) is within rel_tolerance * ||A||; sigma.size() if none.
 RRSVD_B200_API std::size_t retained_rank_for_tolerance(const SvdResult& result, double a_frobenius_norm,
                                                        double rel_tolerance) {
     const double total = a_frobenius_norm * a_frobenius_norm, target = rel_tolerance * a_frobenius_norm;
     double kept = 0.0;
-    for (std::size_t k = 0; k < result.sigma.size(); ++k) {
-        kept += result.sigma[k] * result.sigma[k];
-        if (std::sqrt(std::max(0.0, total - kept)) <= target) return k + 1;
+    for (std::size_t k = 0; k <= result.sigma.size(); ++k) {
+        if (std::sqrt(std::max(0.0, total - kept)) <= target) return k;
+        if (k < result.sigma.size()) kept += result.sigma[k] * result.sigma[k];
     }
     return result.sigma.size();
 }
