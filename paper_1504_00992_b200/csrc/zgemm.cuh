@@ -15,10 +15,14 @@
 //    imaginary part's error bound is a small constant times 4M's u·Σ|a||b|, far inside the
 //    path's 1e-10 parity bar (every parity test passes either way; BLAS libraries ship it as
 //    zgemm3m).
-// Operands are staged global→shared with a multi-stage cp.async
-// (LDGSTS) ring; each thread loads one 16-byte complex per fragment element (LDS.128), so a
-// single shared-memory read yields both the real and imaginary fragment.
+// Operands are staged global→shared by TMA (cp.async.bulk.tensor into an mbarrier ring, one
+// issuing thread, zero-filled tails) — or, for the shapes TMA cannot describe (column-blocked B,
+// odd pair dimensions, unaligned pointers), by a cp.async (LDGSTS) ring; each thread reads one
+// 16-byte complex per fragment element (LDS.128), so a single shared-memory read yields both
+// the real and imaginary fragment.
 #pragma once
+#include <cuda.h>  // CUtensorMap (types only: the encoder is fetched from the driver at run time)
+
 #include "common.cuh"
 
 namespace rb {
@@ -73,6 +77,15 @@ struct GemmGroup {
     int total_tiles;
     GemmProblem p[kMaxGroup];
 };
+
+// The TMA-staged launch: one tensor map per operand per problem (FLOAT64 elements, dense boxes),
+// passed with the group as one __grid_constant__ parameter (64-byte aligned maps).
+struct alignas(64) TmaGroup {
+    CUtensorMap mapA[kMaxGroup];
+    CUtensorMap mapB[kMaxGroup];
+    GemmGroup g;
+};
+static_assert(sizeof(TmaGroup) <= 32764, "kernel parameter space");
 
 // Launches one grouped GEMM.  All problems share the A operation.  Split-K partials are
 // reduced (deterministically, fixed order) by a second kernel.
