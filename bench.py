@@ -382,6 +382,8 @@ def run_ours(args, rank, world, local_rank):
     serial_step_s = er0.elapsed_time(er1) / 1e3
     fl, ms, calls = C.c_double(), C.c_double(), C.c_uint64()
     ctx.check(lib.rrsvd_b200_gemm_stats(ctx.h, C.byref(fl), C.byref(ms), C.byref(calls)))
+    exec_fl, tma_ms = C.c_double(), C.c_double()
+    ctx.check(lib.rrsvd_b200_gemm_pipe_stats(ctx.h, C.byref(exec_fl), C.byref(tma_ms)))
     sfl, sms = (C.c_double * 8)(), (C.c_double * 8)()
     ctx.check(lib.rrsvd_b200_gemm_stage_stats(ctx.h, sfl, sms))
     ctx.check(lib.rrsvd_b200_set_gemm_timing(ctx.h, 0))
@@ -441,6 +443,13 @@ def run_ours(args, rank, world, local_rank):
                          "peak_source": "measured live: DMMA probe (mma.sync m8n8k4 f64) on this GPU;"
                                         " MEASURED_PEAKS.json has no FP64 entry",
                          "frac_of_40tf_nominal": round(achieved / 40.0, 4),
+                         "achieved_executed": round(exec_fl.value / (ms.value * 1e-3) / 1e12, 3) if ms.value > 0 else None,
+                         "frac_executed": round(exec_fl.value / (ms.value * 1e-3) / 1e12 / peak_dmma, 4)
+                         if ms.value > 0 and peak_dmma else None,
+                         "frac_note": "frac counts the algorithmic 8 flops per complex MAC (a 4M zgemm's work, SURVEY"
+                                      " 8(d)); frac_executed counts what the DMMA pipe executed (6 per MAC in the"
+                                      " 3M form) — the tensor-pipe utilisation",
+                         "tma_time_share": round(tma_ms.value / ms.value, 4) if ms.value > 0 else None,
                          "complex_product": "3M on the 64x56 tile (RRSVD_B200_GEMM_3M=0: 4M): the DMMA pipe"
                                             " executes 6 real flops per complex MAC; achieved counts the"
                                             " algorithmic 8 (SURVEY 8(d)), as a 4M zgemm would have to",

@@ -285,6 +285,9 @@ int rrsvd_b200_set_overlap(rrsvd_b200_ctx* ctx, int on);
  * device milliseconds and launch count. */
 int rrsvd_b200_set_gemm_timing(rrsvd_b200_ctx* ctx, int on);
 int rrsvd_b200_gemm_stats(rrsvd_b200_ctx* ctx, double* flops, double* ms, uint64_t* calls);
+/* Of the same launches: the flops the DMMA pipe actually executed (6 real flops per complex MAC
+ * for 3M-form launches, 8 for 4M) and the milliseconds spent in TMA-staged launches. */
+int rrsvd_b200_gemm_pipe_stats(rrsvd_b200_ctx* ctx, double* executed_flops, double* tma_ms);
 /* The same split by stage (8 slots): 0 theta, 1 gate, 2 RRSVD A-products, 3 QR Gram,
  * 4 QR apply, 5 small-SVD assembly, 6 deterministic-SVD preconditioning. */
 int rrsvd_b200_gemm_stage_stats(rrsvd_b200_ctx* ctx, double* flops8, double* ms8);

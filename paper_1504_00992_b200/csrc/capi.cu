@@ -597,6 +597,8 @@ int rrsvd_b200_set_gemm_timing(rrsvd_b200_ctx* c, int on) {
         if (on) {
             c->gemm_ms = 0.0;
             c->gemm_flops = 0.0;
+            c->gemm_exec_flops = 0.0;
+            c->gemm_tma_ms = 0.0;
             c->gemm_calls = 0;
             for (int i = 0; i < 8; ++i) c->tag_ms[i] = c->tag_flops[i] = 0.0;
         }
@@ -609,6 +611,14 @@ int rrsvd_b200_gemm_stats(rrsvd_b200_ctx* c, double* flops, double* ms, uint64_t
         if (flops) *flops = c->gemm_flops;
         if (ms) *ms = c->gemm_ms;
         if (calls) *calls = c->gemm_calls;
+    });
+}
+
+int rrsvd_b200_gemm_pipe_stats(rrsvd_b200_ctx* c, double* executed_flops, double* tma_ms) {
+    return api(c, [&] {
+        flush_gemm_timing(c);
+        if (executed_flops) *executed_flops = c->gemm_exec_flops;
+        if (tma_ms) *tma_ms = c->gemm_tma_ms;
     });
 }
 

@@ -158,6 +158,8 @@ void flush_gemm_timing(rrsvd_b200_ctx* c) {
         check_cuda(c, cudaEventElapsedTime(&ms, p.a, p.b), "event elapsed");
         c->gemm_ms += ms;
         c->gemm_flops += p.flops;
+        c->gemm_exec_flops += p.executed;
+        if (p.tma) c->gemm_tma_ms += ms;
         c->tag_ms[p.tag & 7] += ms;
         c->tag_flops[p.tag & 7] += p.flops;
         c->gemm_calls++;

@@ -25,8 +25,10 @@ struct rrsvd_b200_ctx {
     // Optional per-launch timing of the zgemm stage (CUDA events on the context stream).
     struct PendingGemm {
         cudaEvent_t a, b;
-        double flops;
+        double flops;     // algorithmic: 8 real flops per complex MAC
+        double executed;  // what the DMMA pipe executes (6 per complex MAC in the 3M form)
         int tag;
+        int tma;          // staged by TMA (1) or cp.async (0)
     };
     int gemm_tag = 0;              // category of the next zgemm launches (debug statistics)
     double tag_ms[8] = {}, tag_flops[8] = {};
@@ -41,7 +43,7 @@ struct rrsvd_b200_ctx {
     cudaEvent_t ev_fork = nullptr, ev_join[kMaxLanes] = {};
     bool use_lanes = true;
     int n_lanes = 2;  // RRSVD_B200_LANES overrides
-    double gemm_ms = 0.0, gemm_flops = 0.0;
+    double gemm_ms = 0.0, gemm_flops = 0.0, gemm_exec_flops = 0.0, gemm_tma_ms = 0.0;
     uint64_t gemm_calls = 0;
 };
 

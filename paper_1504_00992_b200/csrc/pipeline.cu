@@ -38,6 +38,7 @@ void gemm_many(rrsvd_b200_ctx* c, GemmOp opA, const std::vector<GemmSpec>& specs
     for (size_t base = 0; base < specs.size(); base += kMaxGroup) {
         GemmGroup g;
         g.count = 0;
+        g.used_m3 = g.used_tma = 0;
         double flops = 0.0;
         bool any_split = false;
         for (size_t i = base; i < std::min(specs.size(), base + kMaxGroup); ++i) {
@@ -81,7 +82,7 @@ void gemm_many(rrsvd_b200_ctx* c, GemmOp opA, const std::vector<GemmSpec>& specs
         c->launches += any_split ? 2 : 1;
         if (c->gemm_timing) {
             check_cuda(c, cudaEventRecord(eb, c->stream), "event record");
-            c->pending.push_back({ea, eb, flops, c->gemm_tag});
+            c->pending.push_back({ea, eb, flops, g.used_m3 ? 0.75 * flops : flops, c->gemm_tag, g.used_tma});
         }
     }
 }

@@ -616,7 +616,9 @@ cudaError_t launch_cfg(GemmGroup& g, GemmOp opA, cudaStream_t s) {
         configured.fetch_or(bit);
     }
     static thread_local TmaGroup tg;  // 24 KB: kept off the stack
-    if (tma_enabled() && make_tma_group<CF>(g, opA, tg)) {
+    g.used_m3 = CF::M3 ? 1 : 0;
+    g.used_tma = tma_enabled() && make_tma_group<CF>(g, opA, tg) ? 1 : 0;
+    if (g.used_tma) {
         const int sm = CF::TMA_SMEM_BYTES;
         if (opA == kOpN) {
             if (any_ks) zgemm_tma_kernel<CF, kOpN, true><<<total, CF::NTHREADS, sm, s>>>(tg);

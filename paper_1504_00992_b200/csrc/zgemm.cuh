@@ -76,6 +76,9 @@ struct GemmGroup {
     int count;
     int total_tiles;
     GemmProblem p[kMaxGroup];
+    // filled by zgemm_grouped (host statistics): the complex-product form and the staging used
+    int used_m3;
+    int used_tma;
 };
 
 // The TMA-staged launch: one tensor map per operand per problem (FLOAT64 elements, dense boxes),

@@ -2,8 +2,9 @@
 (the switches are read once per process): every variant must meet the same parity bar as the
 default, so an A/B switch can never hide a wrong result.
 
-  * zgemm: 3M (default on the 64x56 tile) vs 4M, and 3M on the 64x64 tile — vs numpy, the
-    reference's cblas_zgemm contract (linalg.cpp:20-40);
+  * zgemm: 3M (default on the 64x56 tile) vs 4M, 3M on the 64x64 tile, TMA staging (default)
+    vs the cp.async ring, and the shapes that fall back to cp.async (odd N; odd M under op C) —
+    vs numpy, the reference's cblas_zgemm contract (linalg.cpp:20-40);
   * block Jacobi: the persistent sweep kernel (forced with RRSVD_B200_BJ_S=1) vs one launch per
     tournament step — singular values vs LAPACK (the reference's svd_full, linalg.cpp:67-88).
 """
@@ -26,7 +27,8 @@ sys.path.insert(0, %(root)r)
 import paper_1504_00992_b200 as P
 rng = np.random.default_rng(5)
 out = {}
-for (m, k, n, adj) in [(2000, 2000, 110, False), (2000, 1500, 110, True), (400, 300, 256, False), (333, 100, 2000, False)]:
+for (m, k, n, adj) in [(2000, 2000, 110, False), (2000, 1500, 110, True), (400, 300, 256, False), (333, 100, 2000, False),
+                       (250, 301, 111, False), (201, 173, 90, True), (64, 7, 56, False)]:
     a = rng.standard_normal((k, m) if adj else (m, k)) + 1j * rng.standard_normal((k, m) if adj else (m, k))
     b = rng.standard_normal((k, n)) + 1j * rng.standard_normal((k, n))
     c = P.gemm(a, adj, b)
@@ -68,7 +70,8 @@ def run_variant(script, env_extra):
 
 @pytest.mark.parametrize("env", [{"RRSVD_B200_GEMM_3M": "1"}, {"RRSVD_B200_GEMM_3M": "0"},
                                  {"RRSVD_B200_GEMM_3M": "1", "RRSVD_B200_GEMM_3M64": "1"},
-                                 {"RRSVD_B200_GEMM_CFG": "56"}, {"RRSVD_B200_GEMM_CFG": "64"}])
+                                 {"RRSVD_B200_GEMM_CFG": "56"}, {"RRSVD_B200_GEMM_CFG": "64"},
+                                 {"RRSVD_B200_GEMM_TMA": "0"}, {"RRSVD_B200_GEMM_TMA": "0", "RRSVD_B200_GEMM_3M": "0"}])
 def test_zgemm_variants_componentwise(env):
     """Every tile / complex-product form: |C - AB| <= 1e-13 |A||B| elementwise (FP64 GEMM error
     bound class; 3M's imaginary-part bound is a small constant times 4M's)."""
