@@ -76,6 +76,13 @@ def workload(name: str):
                     terms={b: t for b, t in enumerate(M.ising_terms(n, 1.0, 1.0))}, chi=128, dt=0.01,
                     backend=dict(randomized=False, det_crossover=256, seed=7),
                     desc="Ising L=64, d=2, chi=128 (n=256), deterministic (reference default crossover)")
+    if name == "c2rr":  # config 2's RRSVD arm: randomized decimation forced (tebd.cpp:167-186)
+        n = 64
+        return dict(name="ising_L64_d2_chi128_rrsvd", site_dims=[2] * n,
+                    terms={b: t for b, t in enumerate(M.ising_terms(n, 1.0, 1.0))}, chi=128, dt=0.01,
+                    backend=dict(randomized=True, target_rank=0, oversampling=10, power_iterations=2,
+                                 det_crossover=0, seed=7),
+                    desc="Ising L=64, d=2, chi=128 (n=256), RRSVD p=10 q=2 forced (det_crossover=0)")
     raise SystemExit(f"unknown workload {name}")
 
 
@@ -728,8 +735,8 @@ def main():
                     help="timed steps (default 10; 1 for c3det, whose steps take ~40 s)")
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="c3", choices=["c3", "c3p100", "c3det", "c2", "c5", "c4"],
-                    help="c3 (headline TEBD), c2; c5/c4: row-sharded single-matrix RRSVD")
+    ap.add_argument("--workload", default="c3", choices=["c3", "c3p100", "c3det", "c2", "c2rr", "c5", "c4"],
+                    help="c3 (headline TEBD), c3p100, c3det, c2, c2rr; c5/c4: row-sharded single-matrix RRSVD")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--force-partition", action="store_true",
                     help="use the chain-block partition driver even on one GPU (smoke test of the N>1 path)")

@@ -570,6 +570,32 @@ __global__ void __launch_bounds__(256) probe_dfma_kernel(double* sink, double se
     if (s == 12345.678) sink[threadIdx.x] = s;
 }
 
+// DMMA and DFMA issued together: 8 DMMA chains and NF independent DFMA chains per iteration —
+// whether the FP64 vector pipe adds throughput beside the FP64 tensor pipe (diagnostic).
+template <int NF>
+__global__ void __launch_bounds__(256) probe_mixed_kernel(double* sink, double seed) {
+    double acc[8][2], f[NF];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc[i][0] = acc[i][1] = 0.0;
+#pragma unroll
+    for (int i = 0; i < NF; ++i) f[i] = seed * i;
+    const double a = seed + threadIdx.x * 1e-9, b = seed * 0.5, fa = 1.0000001, fb = 1e-12;
+    for (int it = 0; it < PROBE_ITERS; ++it) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            dmma884(acc[i][0], acc[i][1], a, b);
+#pragma unroll
+            for (int j = i * NF / 8; j < (i + 1) * NF / 8; ++j) f[j] = fma(f[j], fa, fb);
+        }
+    }
+    double s = 0.0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s += acc[i][0] + acc[i][1];
+#pragma unroll
+    for (int i = 0; i < NF; ++i) s += f[i];
+    if (s == 12345.678) sink[threadIdx.x] = s;
+}
+
 }  // namespace
 
 cudaError_t omega_reference(uint64_t seed, long long n_entries, unsigned long long* draws, cplx* out,
@@ -758,15 +784,20 @@ cudaError_t probe_peak(int what, double* tflops, cudaStream_t s) {
     for (int rep = 0; rep < 2; ++rep) {  // first launch warms clocks
         cudaEventRecord(t0, s);
         if (what == 0) probe_dmma_kernel<<<grid, 256, 0, s>>>(sink, 1.0);
-        else probe_dfma_kernel<<<grid, 256, 0, s>>>(sink, 1.0);
+        else if (what == 1) probe_dfma_kernel<<<grid, 256, 0, s>>>(sink, 1.0);
+        else if (what == 2) probe_mixed_kernel<8><<<grid, 256, 0, s>>>(sink, 1.0);
+        else if (what == 3) probe_mixed_kernel<16><<<grid, 256, 0, s>>>(sink, 1.0);
+        else probe_mixed_kernel<32><<<grid, 256, 0, s>>>(sink, 1.0);
         cudaEventRecord(t1, s);
     }
     e = cudaEventSynchronize(t1);
     float ms = 0.f;
     cudaEventElapsedTime(&ms, t0, t1);
     const double warps = grid * 8.0;
+    const double nf = what == 2 ? 8.0 : what == 3 ? 16.0 : 32.0;
     const double flops = (what == 0) ? warps * PROBE_ITERS * 8.0 * 512.0
-                                     : warps * 32.0 * PROBE_ITERS * 8.0 * 2.0;
+                         : (what == 1) ? warps * 32.0 * PROBE_ITERS * 8.0 * 2.0
+                                       : warps * PROBE_ITERS * (8.0 * 512.0 + 32.0 * nf * 2.0);
     *tflops = flops / (ms * 1e-3) / 1e12;
     cudaEventDestroy(t0);
     cudaEventDestroy(t1);
