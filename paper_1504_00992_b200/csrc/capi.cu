@@ -140,6 +140,7 @@ void rrsvd_b200_ctx_destroy(rrsvd_b200_ctx* c) {
     release_staged(c);
     cudaStreamSynchronize(c->stream);
     if (c->pinned) cudaFreeHost(c->pinned);
+    if (c->pinned_sweep) cudaFreeHost(c->pinned_sweep);
     release_lanes(c);
     for (cudaEvent_t e : c->event_pool) cudaEventDestroy(e);
     if (c->own_stream) cudaStreamDestroy(c->stream);

@@ -169,6 +169,17 @@ void flush_gemm_timing(rrsvd_b200_ctx* c) {
     c->pending.clear();
 }
 
+void* pinned_sweep_scratch(rrsvd_b200_ctx* c, size_t bytes) {
+    if (bytes > c->pinned_sweep_cap) {
+        if (c->pinned_sweep) cudaFreeHost(c->pinned_sweep);
+        c->pinned_sweep = nullptr;
+        c->pinned_sweep_cap = 0;
+        check_cuda(c, cudaMallocHost(&c->pinned_sweep, bytes), "cudaMallocHost");
+        c->pinned_sweep_cap = bytes;
+    }
+    return c->pinned_sweep;
+}
+
 void* pinned_scratch(rrsvd_b200_ctx* c, size_t bytes) {
     if (bytes > c->pinned_cap) {
         if (c->pinned) cudaFreeHost(c->pinned);

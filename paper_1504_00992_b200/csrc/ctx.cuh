@@ -19,6 +19,10 @@ struct rrsvd_b200_ctx {
     // Pinned host scratch for small results (info structs, scalars).
     void* pinned = nullptr;
     size_t pinned_cap = 0;
+    // A separate pinned region for evolve's per-sweep scalars: two sweeps may be in flight while
+    // the kernels' own host reads (block Jacobi, accuracy check) use `pinned`.
+    void* pinned_sweep = nullptr;
+    size_t pinned_sweep_cap = 0;
     // Buffers allocated for host-pointer staging during one call, freed at call end.
     std::vector<void*> staged;
 
@@ -112,5 +116,6 @@ struct StreamSwitch {
 cudaEvent_t pooled_event(rrsvd_b200_ctx* c);
 void flush_gemm_timing(rrsvd_b200_ctx* c);  // waits for pending events, accumulates
 void* pinned_scratch(rrsvd_b200_ctx* c, size_t bytes);
+void* pinned_sweep_scratch(rrsvd_b200_ctx* c, size_t bytes);
 
 }  // namespace rb

@@ -22,6 +22,7 @@ struct rrsvd_b200_mps {
     std::vector<size_t> lcap;
     // chain-block edges: λ of the bonds outside the block (null = open chain end)
     double* edge[2] = {nullptr, nullptr};
+    std::vector<char> sat;      // per bond: its last decimation kept its kmax (speculation history)
     size_t edge_n[2] = {0, 0};
     size_t edge_cap[2] = {0, 0};
     const double* ll_of(int b) const { return b > 0 ? lam[b - 1] : edge[0]; }
@@ -64,34 +65,6 @@ void ensure_lambda(rrsvd_b200_mps* s, int bond, size_t elems) {
     if (s->lam[bond]) cudaFreeAsync(s->lam[bond], c->stream);
     s->lam[bond] = nullptr;
     check_cuda(c, cudaMallocAsync(reinterpret_cast<void**>(&s->lam[bond]), elems * sizeof(double), c->stream), "alloc lambda");
-    s->lcap[bond] = elems;
-}
-
-// Growth without freeing: the old buffer may still be read by work being enqueued; the caller
-// frees `old` after the streams that read it have joined.
-// A replaced buffer, kept until the sweep's results are validated: freed after a good update,
-// swapped back (and the new buffer freed) when the bond's Θ was rejected.
-struct Regrown {
-    int kind;  // 0 gamma, 1 lambda
-    int idx;
-    void* old;
-    size_t old_cap;
-};
-
-void grow_gamma(rrsvd_b200_mps* s, int site, size_t elems, std::vector<Regrown>& old) {
-    if (s->gcap[site] >= elems) return;
-    old.push_back({0, site, s->g[site], s->gcap[site]});
-    s->g[site] = nullptr;
-    check_cuda(s->c, cudaMallocAsync(reinterpret_cast<void**>(&s->g[site]), elems * sizeof(cplx), s->c->stream),
-               "alloc gamma");
-    s->gcap[site] = elems;
-}
-void grow_lambda(rrsvd_b200_mps* s, int bond, size_t elems, std::vector<Regrown>& old) {
-    if (s->lcap[bond] >= elems) return;
-    old.push_back({1, bond, s->lam[bond], s->lcap[bond]});
-    s->lam[bond] = nullptr;
-    check_cuda(s->c, cudaMallocAsync(reinterpret_cast<void**>(&s->lam[bond]), elems * sizeof(double), s->c->stream),
-               "alloc lambda");
     s->lcap[bond] = elems;
 }
 
@@ -315,241 +288,322 @@ void release_gate(rrsvd_b200_gate* g) {
     delete g;
 }
 
+// One enqueued sweep — every bond of one parity as one batch — awaiting its scalars.  Its
+// decimations write FRESH Γ/λ buffers: the inputs stay intact until the sweep is committed, so
+// a rejected Θ, an abort (tebd.cpp:317-321) or a mispredicted speculative successor is undone by
+// restoring pointers, never by copying data back.
+struct InFlight {
+    size_t step = 0, sweep = 0;
+    std::vector<int> bonds;
+    std::vector<DecimPlan> plans;
+    std::vector<uint64_t> seeds;
+    DecimScalars* sc_dev = nullptr;
+    DecimScalars* sc_host = nullptr;  // pinned slot
+    cudaEvent_t ev[4] = {};           // Θ | gate | decimate | end marks on lane 0
+    cudaEvent_t done = nullptr;       // after the scalars' D2H
+    struct Swap {
+        cplx* g_old[2];
+        size_t gcap_old[2];
+        cplx* g_new[2];
+        size_t gcap_new[2];
+        double* l_old;
+        size_t lcap_old;
+        double* l_new;
+        size_t lcap_new;
+        int dim_old;  // the bond dimension before the sweep
+    };
+    std::vector<Swap> swaps;
+    bool predicted = false;  // a successor was enqueued assuming kept == kmax on every bond
+};
+
+void release_events(rrsvd_b200_ctx* c, InFlight& f) {
+    for (cudaEvent_t& e : f.ev)
+        if (e) c->event_pool.push_back(e), e = nullptr;
+    if (f.done) c->event_pool.push_back(f.done), f.done = nullptr;
+}
+
+// Undo bond i of a sweep: its fresh outputs are dropped, the inputs become current again.
+void undo_bond(rrsvd_b200_mps* s, rrsvd_b200_ctx* c, const InFlight& f, size_t i) {
+    const int b = f.bonds[i];
+    const InFlight::Swap& w = f.swaps[i];
+    for (int k = 0; k < 2; ++k) {
+        if (w.g_new[k]) cudaFreeAsync(w.g_new[k], c->stream);
+        s->g[b + k] = w.g_old[k];
+        s->gcap[b + k] = w.gcap_old[k];
+    }
+    if (w.l_new) cudaFreeAsync(w.l_new, c->stream);
+    s->lam[b] = w.l_old;
+    s->lcap[b] = w.lcap_old;
+    s->dr[b] = w.dim_old;
+    s->dl[b + 1] = w.dim_old;
+}
+
+// Enqueue one sweep on the current state (host dims may be predicted ones).
+void enqueue_sweep(rrsvd_b200_mps* s, rrsvd_b200_ctx* c, InFlight& f, const rrsvd_b200_sweep* sweeps,
+                   const rrsvd_b200_gate* const* gates, rrsvd_b200_backend* be, int renorm, int omode,
+                   DecimScalars* sc_host) {
+    const int nb = s->n - 1;
+    const size_t sw = f.sweep;
+    for (int b = sweeps[sw].bond_parity; b < nb; b += 2)
+        if (gates[sw * nb + b] != nullptr) f.bonds.push_back(b);
+    const size_t nbnd = f.bonds.size();
+    f.plans.resize(nbnd);
+    f.seeds.resize(nbnd);
+    f.swaps.reserve(nbnd);  // filled as the buffers are made (an undo covers exactly those)
+    f.sc_dev = ws_get<DecimScalars>(c, nbnd);
+    f.sc_host = sc_host;
+    for (auto& e : f.ev) e = pooled_event(c);
+    f.done = pooled_event(c);
+    std::vector<cplx*> gin1(nbnd), gin2(nbnd);
+    std::vector<double*> lin(nbnd);
+    for (size_t i = 0; i < nbnd; ++i) {
+        const int b = f.bonds[i];
+        // with the accuracy check a bond may grow past chi_max (tebd.cpp:177-179): its plan's
+        // kmax is then the minor dimension
+        f.plans[i] = plan_decimation(s->d[b], s->d[b + 1], s->dl[b], s->dr[b + 1], s->chi_max, be->kind,
+                                     be->target_rank, be->oversampling, be->det_crossover, be->accuracy_check,
+                                     be->probe_count);
+        f.seeds[i] = be->seed++;  // ascending bond order, as the reference (tebd.cpp:162)
+        gin1[i] = s->g[b];
+        gin2[i] = s->g[b + 1];
+        lin[i] = s->lam[b];
+        f.swaps.push_back(InFlight::Swap{});
+        InFlight::Swap& w = f.swaps.back();
+        w.dim_old = s->dr[b];
+        w.g_old[0] = s->g[b];
+        w.g_old[1] = s->g[b + 1];
+        w.gcap_old[0] = s->gcap[b];
+        w.gcap_old[1] = s->gcap[b + 1];
+        w.l_old = s->lam[b];
+        w.lcap_old = s->lcap[b];
+        const size_t need[2] = {(size_t)f.plans[i].m * f.plans[i].kmax, (size_t)f.plans[i].kmax * f.plans[i].n};
+        for (int k = 0; k < 2; ++k) {
+            check_cuda(c, cudaMallocAsync(reinterpret_cast<void**>(&w.g_new[k]), need[k] * sizeof(cplx), c->stream),
+                       "alloc gamma");
+            w.gcap_new[k] = need[k];
+            s->g[b + k] = w.g_new[k];
+            s->gcap[b + k] = need[k];
+        }
+        check_cuda(c, cudaMallocAsync(reinterpret_cast<void**>(&w.l_new), (size_t)f.plans[i].kmax * sizeof(double),
+                                      c->stream), "alloc lambda");
+        w.lcap_new = f.plans[i].kmax;
+        s->lam[b] = w.l_new;
+        s->lcap[b] = w.lcap_new;
+    }
+    check_cuda(c, cudaEventRecord(f.ev[0], c->stream), "event");
+    static const int env_lanes = [] {
+        const char* e = std::getenv("RRSVD_B200_LANES");
+        return e ? std::atoi(e) : 0;
+    }();
+    const int want = env_lanes > 0 ? env_lanes : c->n_lanes;
+    bool syncs = false;  // lanes are submitted in turn: a host-synchronising batch serialises them
+    for (size_t i = 0; i < nbnd; ++i) syncs = syncs || decimation_syncs_host(f.plans[i]);
+    const int nl = c->use_lanes && !syncs ? std::max(1, std::min<int>({want, (int)nbnd, rrsvd_b200_ctx::kMaxLanes})) : 1;
+    const cudaStream_t main_stream = c->stream;
+    if (nl > 1) lanes_fork(c, nl);
+    {
+        StreamSwitch lane_switch(c);  // c->stream is back on main_stream on every exit path
+        for (int lane = 0; lane < nl; ++lane) {
+            if (nl > 1) c->stream = c->lane[lane];
+            std::vector<ThetaJob> tj;
+            std::vector<GateJob> gj;
+            std::vector<DecimJob> dj;
+            for (size_t i = lane; i < nbnd; i += nl) {
+                const int b = f.bonds[i];
+                const int d1 = s->d[b], d2 = s->d[b + 1];
+                const int cl = s->dl[b], cm = f.swaps[i].dim_old, cr = s->dr[b + 1];
+                cplx* M1 = ws_get<cplx>(c, (size_t)f.plans[i].m * f.plans[i].n);
+                cplx* M2 = ws_get<cplx>(c, (size_t)f.plans[i].m * f.plans[i].n);
+                const double* ll = s->ll_of(b);
+                const double* lr = s->lr_of(b);
+                tj.push_back({gin1[i], gin2[i], ll, lin[i], lr, cl, d1, cm, d2, cr, M1});
+                const rrsvd_b200_gate* G = gates[sw * nb + b];
+                gj.push_back({G->dev, d1, d2, cl, cr, M1, M2, G->blocked ? &G->blk.dev : nullptr});
+                DecimJob job{f.plans[i], M2, d1, cr, ll, lr, s->chi_max, s->tol, (int)be->power_iterations,
+                             f.seeds[i], omode, nullptr, renorm, s->g[b], s->lam[b], s->g[b + 1], f.sc_dev + i};
+                job.eps = be->epsilon;
+                dj.push_back(job);
+            }
+            build_theta_many(c, tj);
+            if (lane == 0) check_cuda(c, cudaEventRecord(f.ev[1], c->stream), "event");
+            apply_gate_many(c, gj);
+            if (lane == 0) check_cuda(c, cudaEventRecord(f.ev[2], c->stream), "event");
+            decimate_many(c, dj);
+        }
+    }
+    if (nl > 1) lanes_join(c, nl);
+    check_cuda(c, cudaEventRecord(f.ev[3], c->stream), "event");
+    check_cuda(c, cudaMemcpyAsync(f.sc_host, f.sc_dev, nbnd * sizeof(DecimScalars), cudaMemcpyDeviceToHost, c->stream),
+               "D2H");
+    check_cuda(c, cudaEventRecord(f.done, c->stream), "event");
+}
+
+// Drop a (speculative) sweep entirely: its outputs, its seeds.
+void rollback_sweep(rrsvd_b200_mps* s, rrsvd_b200_ctx* c, InFlight& f, rrsvd_b200_backend* be) {
+    for (size_t i = f.swaps.size(); i-- > 0;) undo_bond(s, c, f, i);
+    if (!f.seeds.empty()) be->seed = f.seeds[0];
+    release_events(c, f);
+}
+
 void evolve_core(rrsvd_b200_mps* s, rrsvd_b200_ctx* c, size_t n_sweeps, const rrsvd_b200_sweep* sweeps,
                  const rrsvd_b200_gate* const* gates, size_t n_steps, rrsvd_b200_backend* be,
                  const rrsvd_b200_evolve_options* opt, rrsvd_b200_evolve_diag* diag,
                  rrsvd_b200_update_record* records, size_t max_records) {
-    {
-        if (be == nullptr || diag == nullptr || (n_sweeps && (sweeps == nullptr || gates == nullptr)))
-            throw_contract(c, "evolve: null argument");
-        const int n = s->n, nb = n - 1;
-        const double abort_thr = opt ? opt->abort_discarded_threshold : 1.0;
-        const int renorm = opt ? opt->renormalize : 1;
-        const int omode = opt ? opt->omega_mode : RRSVD_B200_OMEGA_REFERENCE;
-        for (size_t sw = 0; sw < n_sweeps; ++sw)
-            for (int b = 0; b < nb; ++b) {
-                const rrsvd_b200_gate* g = gates[sw * nb + b];
-                if (g != nullptr && g->dd != s->d[b] * s->d[b + 1])
-                    throw_contract(c, "evolve: term dimension mismatch");
-            }
-
-        DecimScalars* sc_dev = nullptr;
-        size_t sc_cap = 0;
-        struct ScGuard {
-            rrsvd_b200_ctx* c;
-            void* p;
-            ~ScGuard() {
-                if (p) cudaFreeAsync(p, c->stream);
-            }
-        } scg{c, nullptr};
-        cudaEvent_t ev[4];
-        for (auto& e : ev) e = pooled_event(c);
-        struct EvGuard {
-            rrsvd_b200_ctx* c;
-            cudaEvent_t* e;
-            ~EvGuard() { for (int i = 0; i < 4; ++i) c->event_pool.push_back(e[i]); }
-        } evg{c, ev};
-
-        diag->kept_fraction = 1.0;
-        diag->aborted = 0;
-        diag->abort_step = 0;
-        diag->n_updates = 0;
-        uint64_t maxb = 1;
-        for (int b = 0; b < nb; ++b) maxb = std::max<uint64_t>(maxb, (uint64_t)s->dr[b]);
-        diag->max_bond_dim = maxb;
-
-        // All bonds of one sweep share a parity, hence no site: they are independent
-        // and go through every stage of the pipeline as ONE batch.  The results
-        // equal the reference's bond-by-bond order (tebd.cpp:291-306), including the per-call
-        // seeds, which are assigned in ascending bond order.
-        for (size_t step = 0; step < n_steps; ++step) {
-            for (size_t sw = 0; sw < n_sweeps; ++sw) {
-                std::vector<int> bonds;
-                for (int b = sweeps[sw].bond_parity; b < nb; b += 2)
-                    if (gates[sw * nb + b] != nullptr) bonds.push_back(b);
-                if (bonds.empty()) continue;
-                const size_t nbnd = bonds.size();
-                if (sc_cap < nbnd) {
-                    if (sc_dev) cudaFreeAsync(sc_dev, c->stream);
-                    check_cuda(c, cudaMallocAsync(reinterpret_cast<void**>(&sc_dev), nbnd * sizeof(DecimScalars), c->stream),
-                               "alloc scalars");
-                    sc_cap = nbnd;
-                    scg.p = sc_dev;
-                }
-                auto* sc_host = static_cast<DecimScalars*>(pinned_scratch(c, nbnd * sizeof(DecimScalars)));
-                std::vector<DecimPlan> plans(nbnd);
-                std::vector<uint64_t> seeds(nbnd);
-                // Inputs of Θ are the CURRENT buffers; outputs that need more room get NEW
-                // buffers, and the old ones are freed only after both lanes have joined.
-                std::vector<cplx*> gin1(nbnd), gin2(nbnd);
-                std::vector<double*> lin(nbnd);
-                std::vector<std::vector<Regrown>> regrown(nbnd);
-                // An abort (tebd.cpp:317-321) leaves the bonds after the offending one untouched;
-                // the batch updates them all, so with an abort threshold in force the sweep's
-                // inputs are snapshotted and those bonds restored if it fires.
-                struct Snap {
-                    cplx *g1, *g2;
-                    double* lam;
-                    int chi;
-                    size_t n1, n2;
-                };
-                std::vector<Snap> snaps;
-                if (abort_thr < 1.0) {
-                    for (size_t i = 0; i < nbnd; ++i) {
-                        const int b = bonds[i];
-                        Snap sn;
-                        sn.chi = s->dr[b];
-                        sn.n1 = (size_t)s->dl[b] * s->d[b] * s->dr[b];
-                        sn.n2 = (size_t)s->dl[b + 1] * s->d[b + 1] * s->dr[b + 1];
-                        sn.g1 = ws_get<cplx>(c, sn.n1);
-                        sn.g2 = ws_get<cplx>(c, sn.n2);
-                        sn.lam = ws_get<double>(c, (size_t)sn.chi);
-                        check_cuda(c, cudaMemcpyAsync(sn.g1, s->g[b], sn.n1 * sizeof(cplx), cudaMemcpyDeviceToDevice,
-                                                      c->stream), "snapshot");
-                        check_cuda(c, cudaMemcpyAsync(sn.g2, s->g[b + 1], sn.n2 * sizeof(cplx),
-                                                      cudaMemcpyDeviceToDevice, c->stream), "snapshot");
-                        check_cuda(c, cudaMemcpyAsync(sn.lam, s->lam[b], (size_t)sn.chi * sizeof(double),
-                                                      cudaMemcpyDeviceToDevice, c->stream), "snapshot");
-                        snaps.push_back(sn);
-                    }
-                }
-                for (size_t i = 0; i < nbnd; ++i) {
-                    const int b = bonds[i];
-                    // with the accuracy check a bond may grow past chi_max (tebd.cpp:177-179):
-                    // its plan's kmax is then the minor dimension
-                    plans[i] = plan_decimation(s->d[b], s->d[b + 1], s->dl[b], s->dr[b + 1], s->chi_max, be->kind,
-                                               be->target_rank, be->oversampling, be->det_crossover,
-                                               be->accuracy_check, be->probe_count);
-                    seeds[i] = be->seed++;  // ascending bond order, as the reference (tebd.cpp:162)
-                    gin1[i] = s->g[b];
-                    gin2[i] = s->g[b + 1];
-                    lin[i] = s->lam[b];
-                    grow_gamma(s, b, (size_t)plans[i].m * plans[i].kmax, regrown[i]);
-                    grow_gamma(s, b + 1, (size_t)plans[i].kmax * plans[i].n, regrown[i]);
-                    grow_lambda(s, b, (size_t)plans[i].kmax, regrown[i]);
-                }
-                check_cuda(c, cudaEventRecord(ev[0], c->stream), "event");
-                const cudaStream_t main_stream = c->stream;
-                static const int env_lanes = [] {
-                    const char* e = std::getenv("RRSVD_B200_LANES");
-                    return e ? std::atoi(e) : 0;
-                }();
-                const int want = env_lanes > 0 ? env_lanes : c->n_lanes;
-                bool syncs = false;  // lanes are submitted in turn: a host-synchronising batch serialises them
-                for (size_t i = 0; i < nbnd; ++i) syncs = syncs || decimation_syncs_host(plans[i]);
-                const int nl = c->use_lanes && !syncs
-                                   ? std::max(1, std::min<int>({want, (int)nbnd, rrsvd_b200_ctx::kMaxLanes}))
-                                   : 1;
-                if (nl > 1) lanes_fork(c, nl);
-                StreamSwitch lane_switch(c);  // c->stream is back on main_stream on every exit path
-                for (int lane = 0; lane < nl; ++lane) {
-                    if (nl > 1) c->stream = c->lane[lane];
-                    std::vector<ThetaJob> tj;
-                    std::vector<GateJob> gj;
-                    std::vector<DecimJob> dj;
-                    for (size_t i = lane; i < nbnd; i += nl) {
-                        const int b = bonds[i];
-                        const int d1 = s->d[b], d2 = s->d[b + 1];
-                        const int cl = s->dl[b], cm = s->dr[b], cr = s->dr[b + 1];
-                        cplx* M1 = ws_get<cplx>(c, (size_t)plans[i].m * plans[i].n);
-                        cplx* M2 = ws_get<cplx>(c, (size_t)plans[i].m * plans[i].n);
-                        const double* ll = s->ll_of(b);
-                        const double* lr = s->lr_of(b);
-                        tj.push_back({gin1[i], gin2[i], ll, lin[i], lr, cl, d1, cm, d2, cr, M1});
-                        const rrsvd_b200_gate* G = gates[sw * nb + b];
-                        gj.push_back({G->dev, d1, d2, cl, cr, M1, M2, G->blocked ? &G->blk.dev : nullptr});
-                        DecimJob job{plans[i], M2, d1, cr, ll, lr, s->chi_max, s->tol, (int)be->power_iterations,
-                                     seeds[i], omode, nullptr, renorm, s->g[b], s->lam[b], s->g[b + 1], sc_dev + i};
-                        job.eps = be->epsilon;
-                        dj.push_back(job);
-                    }
-                    build_theta_many(c, tj);
-                    if (lane == 0) check_cuda(c, cudaEventRecord(ev[1], c->stream), "event");
-                    apply_gate_many(c, gj);
-                    if (lane == 0) check_cuda(c, cudaEventRecord(ev[2], c->stream), "event");
-                    decimate_many(c, dj);
-                }
-                c->stream = main_stream;
-                if (nl > 1) lanes_join(c, nl);
-                check_cuda(c, cudaEventRecord(ev[3], c->stream), "event");
-                check_cuda(c, cudaMemcpyAsync(sc_host, sc_dev, nbnd * sizeof(DecimScalars), cudaMemcpyDeviceToHost,
-                                              c->stream), "D2H");
-                check_cuda(c, cudaStreamSynchronize(c->stream), "sync");
-                if (c->gemm_timing) flush_gemm_timing(c);
-                float t01 = 0, t12 = 0, t23 = 0;
-                cudaEventElapsedTime(&t01, ev[0], ev[1]);
-                cudaEventElapsedTime(&t12, ev[1], ev[2]);
-                cudaEventElapsedTime(&t23, ev[2], ev[3]);
-                // Validate every bond before committing any (the reference throws before it
-                // assigns, tebd.cpp:156-160).  A rejected bond's truncation kept nothing on the
-                // device, so its Γ/λ buffers were not written: its grown buffers are swapped
-                // back, the other bonds of the batch (valid results) are committed, and the seed
-                // counter is left where the reference's would be — the rejected call takes no
-                // seed (tebd.cpp:162 follows the check).
-                size_t first_bad = nbnd;
-                for (size_t i = 0; i < nbnd && first_bad == nbnd; ++i)
-                    if (sc_host[i].nonfinite || !(sc_host[i].total_sq > 0.0)) first_bad = i;
-                for (size_t i = 0; i < nbnd; ++i) {
-                    const bool bad = sc_host[i].nonfinite || !(sc_host[i].total_sq > 0.0);
-                    for (const Regrown& r : regrown[i]) {
-                        if (!bad) {
-                            if (r.old) cudaFreeAsync(r.old, c->stream);
-                            continue;
-                        }
-                        void*& cur = r.kind == 0 ? reinterpret_cast<void*&>(s->g[r.idx])
-                                                 : reinterpret_cast<void*&>(s->lam[r.idx]);
-                        if (cur) cudaFreeAsync(cur, c->stream);
-                        cur = r.old;
-                        (r.kind == 0 ? s->gcap[r.idx] : s->lcap[r.idx]) = r.old_cap;
-                    }
-                    if (!bad) {
-                        s->dr[bonds[i]] = sc_host[i].kept;
-                        s->dl[bonds[i] + 1] = sc_host[i].kept;
-                    }
-                }
-                if (first_bad < nbnd) {
-                    be->seed = seeds[first_bad];
-                    if (sc_host[first_bad].nonfinite) throw_contract(c, "decimate: theta has non-finite entries");
-                    throw_contract(c, "decimate: theta is identically zero");
-                }
-                for (size_t i = 0; i < nbnd; ++i) {
-                    const int b = bonds[i];
-                    const DecimScalars& h = sc_host[i];
-                    s->dr[b] = h.kept;
-                    s->dl[b + 1] = h.kept;
-                    diag->kept_fraction *= 1.0 - h.discarded;
-                    diag->max_bond_dim = std::max<uint64_t>(diag->max_bond_dim, (uint64_t)h.kept);
-                    if (records && diag->n_updates < max_records)  // batched: stage times shared evenly
-                        records[diag->n_updates] = {step, (uint64_t)b, (uint64_t)h.kept, h.discarded,
-                                                    1e3 * t01 / nbnd, 1e3 * t12 / nbnd, 1e3 * t23 / nbnd,
-                                                    plans[i].randomized ? 1 : 0};
-                    diag->n_updates++;
-                    if (1.0 - diag->kept_fraction > abort_thr) {  // tebd.cpp:317-321
-                        diag->aborted = 1;
-                        diag->abort_step = step;
-                        // the reference returns here: the later bonds of the batch take no
-                        // seed (tebd.cpp:162, 317-321)
-                        be->seed -= (uint64_t)(nbnd - i - 1);
-                        for (size_t j = i + 1; j < nbnd; ++j) {  // un-apply the later bonds of the batch
-                            const int bj = bonds[j];
-                            const Snap& sn = snaps[j];
-                            check_cuda(c, cudaMemcpyAsync(s->g[bj], sn.g1, sn.n1 * sizeof(cplx),
-                                                          cudaMemcpyDeviceToDevice, c->stream), "restore");
-                            check_cuda(c, cudaMemcpyAsync(s->g[bj + 1], sn.g2, sn.n2 * sizeof(cplx),
-                                                          cudaMemcpyDeviceToDevice, c->stream), "restore");
-                            check_cuda(c, cudaMemcpyAsync(s->lam[bj], sn.lam, (size_t)sn.chi * sizeof(double),
-                                                          cudaMemcpyDeviceToDevice, c->stream), "restore");
-                            s->dr[bj] = sn.chi;
-                            s->dl[bj + 1] = sn.chi;
-                        }
-                        check_cuda(c, cudaStreamSynchronize(c->stream), "sync");
-                        ws_reset(c);
-                        return;
-                    }
-                }
-                ws_reset(c);
-            }
+    if (be == nullptr || diag == nullptr || (n_sweeps && (sweeps == nullptr || gates == nullptr)))
+        throw_contract(c, "evolve: null argument");
+    const int n = s->n, nb = n - 1;
+    const double abort_thr = opt ? opt->abort_discarded_threshold : 1.0;
+    const int renorm = opt ? opt->renormalize : 1;
+    const int omode = opt ? opt->omega_mode : RRSVD_B200_OMEGA_REFERENCE;
+    size_t max_bonds = 1;
+    for (size_t sw = 0; sw < n_sweeps; ++sw) {
+        size_t cnt = 0;
+        for (int b = 0; b < nb; ++b) {
+            const rrsvd_b200_gate* g = gates[sw * nb + b];
+            if (g != nullptr && g->dd != s->d[b] * s->d[b + 1]) throw_contract(c, "evolve: term dimension mismatch");
+            cnt += g != nullptr && (b % 2) == sweeps[sw].bond_parity;
         }
+        max_bonds = std::max(max_bonds, cnt);
+    }
+    diag->kept_fraction = 1.0;
+    diag->aborted = 0;
+    diag->abort_step = 0;
+    diag->n_updates = 0;
+    uint64_t maxb = 1;
+    for (int b = 0; b < nb; ++b) maxb = std::max<uint64_t>(maxb, (uint64_t)s->dr[b]);
+    diag->max_bond_dim = maxb;
+    if ((int)s->sat.size() != nb) s->sat.assign(nb, 0);
+
+    // The (step, sweep) sequence; sweeps without a term are skipped (tebd.cpp:289-294).
+    std::vector<std::pair<size_t, size_t>> order;
+    for (size_t step = 0; step < n_steps; ++step)
+        for (size_t sw = 0; sw < n_sweeps; ++sw)
+            for (int b = sweeps[sw].bond_parity; b < nb; b += 2)
+                if (gates[sw * nb + b] != nullptr) {
+                    order.push_back({step, sw});
+                    break;
+                }
+    // Speculation: while sweep j runs, sweep j+1 is enqueued assuming every bond of j keeps
+    // kmax (saturated bonds keep the χ cap), so the device never idles on the host's read of j's
+    // kept χ.  Only when every bond of j kept its kmax last time (per-bond history), never with
+    // an abort budget, the accuracy check (data-dependent width) or per-launch GEMM timing.  A
+    // misprediction drops sweep j+1's outputs (fresh buffers) and re-enqueues it: the results
+    // are those of the one-sweep-at-a-time schedule, always.
+    static const bool spec_env = [] {
+        const char* e = std::getenv("RRSVD_B200_SPECULATE");
+        return e == nullptr || std::atoi(e) != 0;
+    }();
+    const bool spec_ok = spec_env && abort_thr >= 1.0 && !c->gemm_timing && !be->accuracy_check;
+    auto* pinned = static_cast<DecimScalars*>(pinned_sweep_scratch(c, 2 * max_bonds * sizeof(DecimScalars)));
+    std::vector<InFlight> q;  // front = q[0]; at most two
+    q.reserve(2);
+    size_t next = 0, slot = 0;
+    auto push = [&](bool) {
+        q.emplace_back();
+        q.back().step = order[next].first;
+        q.back().sweep = order[next].second;
+        ++next;
+        enqueue_sweep(s, c, q.back(), sweeps, gates, be, renorm, omode, pinned + (slot++ & 1) * max_bonds);
+    };
+    try {
+        if (!order.empty()) push(false);
+        while (!q.empty()) {
+            InFlight& f = q[0];
+            bool predictable = spec_ok && q.size() == 1 && next < order.size();
+            for (size_t i = 0; predictable && i < f.bonds.size(); ++i)
+                predictable = !f.plans[i].fixed_precision && s->sat[f.bonds[i]];
+            if (predictable) {
+                for (size_t i = 0; i < f.bonds.size(); ++i) {
+                    s->dr[f.bonds[i]] = f.plans[i].kmax;
+                    s->dl[f.bonds[i] + 1] = f.plans[i].kmax;
+                }
+                f.predicted = true;
+                push(true);
+            }
+            InFlight& fr = q[0];  // (q may have grown: re-take the reference)
+            check_cuda(c, cudaEventSynchronize(fr.done), "sync");
+            if (c->gemm_timing) flush_gemm_timing(c);
+            const size_t nbnd = fr.bonds.size();
+            const DecimScalars* h = fr.sc_host;
+            size_t first_bad = nbnd;
+            bool mismatch = false;
+            for (size_t i = 0; i < nbnd; ++i) {
+                const bool bad = h[i].nonfinite || !(h[i].total_sq > 0.0);
+                if (bad && first_bad == nbnd) first_bad = i;
+                mismatch = mismatch || bad || h[i].kept != fr.plans[i].kmax;
+            }
+            if (q.size() == 2 && mismatch) {  // the successor ran on wrong dims: drop it
+                rollback_sweep(s, c, q[1], be);
+                q.pop_back();
+                --next;
+            }
+            InFlight& f0 = q[0];
+            // The reference applies the bonds one by one (tebd.cpp:291-306): a rejected Θ throws
+            // before anything of that call is assigned (tebd.cpp:156-160, no seed taken), an
+            // exhausted discarded-weight budget returns after the bond that crossed it
+            // (tebd.cpp:317-321).  The batch reproduces exactly that: bonds [0, stop) are
+            // committed, the later ones undone (their inputs were never overwritten).
+            size_t stop = nbnd;
+            bool aborted = false;
+            double kf = diag->kept_fraction;
+            for (size_t i = 0; i < nbnd; ++i) {
+                if (i == first_bad) {
+                    stop = i;
+                    break;
+                }
+                kf *= 1.0 - h[i].discarded;
+                if (1.0 - kf > abort_thr) {
+                    aborted = true;
+                    stop = i + 1;
+                    break;
+                }
+            }
+            for (size_t j = nbnd; j-- > stop;) undo_bond(s, c, f0, j);
+            float t01 = 0, t12 = 0, t23 = 0;
+            cudaEventElapsedTime(&t01, f0.ev[0], f0.ev[1]);
+            cudaEventElapsedTime(&t12, f0.ev[1], f0.ev[2]);
+            cudaEventElapsedTime(&t23, f0.ev[2], f0.ev[3]);
+            for (size_t i = 0; i < stop; ++i) {
+                const int b = f0.bonds[i];
+                const InFlight::Swap& w = f0.swaps[i];
+                for (int k = 0; k < 2; ++k)
+                    if (w.g_old[k]) cudaFreeAsync(w.g_old[k], c->stream);
+                if (w.l_old) cudaFreeAsync(w.l_old, c->stream);
+                s->dr[b] = h[i].kept;
+                s->dl[b + 1] = h[i].kept;
+                s->sat[b] = h[i].kept == f0.plans[i].kmax;
+                diag->kept_fraction *= 1.0 - h[i].discarded;
+                diag->max_bond_dim = std::max<uint64_t>(diag->max_bond_dim, (uint64_t)h[i].kept);
+                if (records && diag->n_updates < max_records)  // batched: stage times shared evenly
+                    records[diag->n_updates] = {f0.step, (uint64_t)b, (uint64_t)h[i].kept, h[i].discarded,
+                                                1e3 * t01 / nbnd, 1e3 * t12 / nbnd, 1e3 * t23 / nbnd,
+                                                f0.plans[i].randomized ? 1 : 0};
+                diag->n_updates++;
+            }
+            if (first_bad < nbnd || aborted) {
+                // the calls after `stop` never ran in the reference: they took no seed
+                be->seed = f0.seeds[0] + stop;
+                const bool nonfin = first_bad < nbnd && h[first_bad].nonfinite != 0;
+                const uint64_t step = f0.step;
+                release_events(c, f0);
+                q.clear();
+                if (first_bad < nbnd)
+                    throw_contract(c, nonfin ? "decimate: theta has non-finite entries"
+                                             : "decimate: theta is identically zero");
+                diag->aborted = 1;
+                diag->abort_step = step;
+                return;
+            }
+            release_events(c, f0);
+            q.erase(q.begin());
+            ws_reset(c);  // (stream-ordered frees: a successor in flight keeps running)
+            if (q.empty() && next < order.size()) push(false);
+        }
+    } catch (...) {
+        // a failed enqueue or device error: no sweep in flight is applied (the state keeps the
+        // last committed sweep; the seed counter its value before them)
+        for (size_t k = q.size(); k-- > 0;) rollback_sweep(s, c, q[k], be);
+        throw;
     }
 }
 
