@@ -9,8 +9,6 @@
 
 namespace rb {
 
-namespace {
-
 bool debug_enabled() {
     static const bool d = [] {
         const char* e = std::getenv("RRSVD_B200_DEBUG");
@@ -18,6 +16,8 @@ bool debug_enabled() {
     }();
     return d;
 }
+
+namespace {
 
 long long gemm_tiles(const GemmSpec& s) {
     return (long long)((s.m + 63) / 64) * ((s.n + 63) / 64) * s.batch;

@@ -175,6 +175,8 @@ DecimPlan plan_decimation(int d1, int d2, int cl, int cr, size_t chi_max, int ki
 // convergence read, the accuracy check's per-round certification): such batches gain nothing
 // from lanes, which are submitted one after the other from the host.
 bool decimation_syncs_host(const DecimPlan& pl);
+// RRSVD_B200_DEBUG set: per-call diagnostics on stderr
+bool debug_enabled();
 
 // One decimation of an unfolded M (tebd.cpp:141-237): norm, factorization (RRSVD or Jacobi),
 // truncation, λ renormalisation, Γ reshape.  Writes gamma_l (m x kept), lambda (kept),
