@@ -157,12 +157,12 @@ struct TileCoord {
     bool skip;
 };
 template <class CF>
-__device__ __forceinline__ TileCoord tile_coord(const GemmGroup& g, int tile) {
+__device__ __forceinline__ TileCoord tile_coord(const GemmGroup& g) {
     TileCoord t{};
-    t.pid = find_problem(g, tile);
+    t.pid = find_problem(g, blockIdx.x);
     const GemmProblem& P = g.p[t.pid];
     t.skip = P.pred != nullptr && *P.pred != P.pred_want;
-    int r = tile - P.tile_begin;
+    int r = blockIdx.x - P.tile_begin;
     const int tn = r % P.tiles_n; r /= P.tiles_n;
     const int tm = r % P.tiles_m; r /= P.tiles_m;
     t.bz = r % P.batch;           r /= P.batch;
@@ -267,7 +267,7 @@ zgemm_dmma_kernel(const __grid_constant__ GemmGroup g) {
     cplx* smA = reinterpret_cast<cplx*>(smem_raw);
     cplx* smB = smA + STAGES * A_STAGE;
 
-    const TileCoord tc = tile_coord<CF>(g, blockIdx.x);
+    const TileCoord tc = tile_coord<CF>(g);
     if (tc.skip) return;
     const GemmProblem& P = g.p[tc.pid];
     const int M = P.m, N = P.n, m0 = tc.m0, n0 = tc.n0;
@@ -410,9 +410,9 @@ __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, u
 template <class CF, int OPA, bool KS>
 __global__ void __launch_bounds__(CF::NTHREADS, CF::MIN_BLOCKS)
 zgemm_tma_kernel(const __grid_constant__ TmaGroup tg) {
-    constexpr int BM = CF::BM, BK = CF::BK, ST = CF::TMA_STAGES;
+    constexpr int BM = CF::BM, BN = CF::BN, BK = CF::BK, ST = CF::TMA_STAGES;
     constexpr int WM = CF::WM, WN = CF::WN, WARPS_N = CF::WARPS_N, NWARPS = CF::NTHREADS / 32;
-    constexpr int A_ELEMS = BM * BK, B_ELEMS = BK * CF::BN;
+    constexpr int A_ELEMS = BM * BK, B_ELEMS = BK * BN;
     constexpr unsigned STAGE_BYTES = (A_ELEMS + B_ELEMS) * (unsigned)sizeof(cplx);
     const GemmGroup& g = tg.g;
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -420,9 +420,16 @@ zgemm_tma_kernel(const __grid_constant__ TmaGroup tg) {
     cplx* smB = smA + ST * A_ELEMS;
     uint64_t* full = reinterpret_cast<uint64_t*>(smB + ST * B_ELEMS);
     uint64_t* empty = full + ST;
+
+    const TileCoord tc = tile_coord<CF>(g);
+    if (tc.skip) return;
+    const GemmProblem& P = g.p[tc.pid];
+    const CUtensorMap* mapA = &tg.mapA[tc.pid];
+    const CUtensorMap* mapB = &tg.mapB[tc.pid];
+    const int M = P.m, N = P.n, m0 = tc.m0, n0 = tc.n0;
+    const int kbeg = tc.kbeg, kend = tc.kend, ktiles = tc.ktiles;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int wm = (warp / WARPS_N) * WM, wn = (warp % WARPS_N) * WN;
-    const int fr = lane >> 2, fc = lane & 3;
 
     if (tid == 0) {
         for (int s = 0; s < ST; ++s) {
@@ -433,88 +440,56 @@ zgemm_tma_kernel(const __grid_constant__ TmaGroup tg) {
     }
     __syncthreads();
 
-    // Persistent CTA: tiles blockIdx.x, +gridDim.x, ...  Their k-tiles form ONE stream of
-    // stages, so the loads of the next tile are in flight while this tile computes and stores
-    // (no per-tile pipeline fill).  The producer cursor (thread 0) walks the same stream ahead.
-    struct Cursor {
-        int tile, kt;
-        TileCoord tc;
-    };
-    auto first_live = [&](int tile) {  // the next tile with work (skipped / predicated-off ones issue nothing)
-        Cursor cu{tile, 0, {}};
-        for (; cu.tile < g.total_tiles; cu.tile += gridDim.x) {
-            cu.tc = tile_coord<CF>(g, cu.tile);
-            if (!cu.tc.skip && cu.tc.ktiles > 0) return cu;
-        }
-        return cu;
-    };
-    auto issue = [&](int stage, const Cursor& cu) {  // (thread 0 only)
-        const TileCoord& t = cu.tc;
-        const CUtensorMap* mapA = &tg.mapA[t.pid];
-        const CUtensorMap* mapB = &tg.mapB[t.pid];
-        const int k0 = t.kbeg + cu.kt * BK;
+    auto issue = [&](int stage, int kt) {  // (thread 0 only)
+        const int k0 = kbeg + kt * BK;
         cplx* sA = smA + stage * A_ELEMS;
         cplx* sB = smB + stage * B_ELEMS;
         mbar_expect_tx(&full[stage], STAGE_BYTES);
         if (OPA == kOpN) {  // four boxes of [BM rows][4 complexes]: dims (2K doubles, M, batch)
 #pragma unroll
             for (int kg = 0; kg < BK / 4; ++kg)
-                tma_load_3d(sA + kg * BM * 4, mapA, &full[stage], 2 * (k0 + 4 * kg), t.m0, t.bz);
+                tma_load_3d(sA + kg * BM * 4, mapA, &full[stage], 2 * (k0 + 4 * kg), m0, tc.bz);
         } else {  // one box [BM/2 pairs][BK][2 complexes]: dims (4 doubles, K, M/2, batch)
-            tma_load_4d(sA, mapA, &full[stage], 0, k0, t.m0 / 2, t.bz);
+            tma_load_4d(sA, mapA, &full[stage], 0, k0, m0 / 2, tc.bz);
         }
-        tma_load_4d(sB, mapB, &full[stage], 0, k0, t.n0 / 2, t.bz);  // [BN/2][BK][2]: (4, K, N/2, batch)
-    };
-    auto advance = [&](Cursor& cu) {
-        if (++cu.kt >= cu.tc.ktiles) cu = first_live(cu.tile + gridDim.x);
+        tma_load_4d(sB, mapB, &full[stage], 0, k0, n0 / 2, tc.bz);  // [BN/2][BK][2]: (4, K, N/2, batch)
     };
 
-    Cursor prod{};
-    long long issued = 0;  // stream position of the next fill
-    if (tid == 0) {
-        prod = first_live(blockIdx.x);
-        for (; issued < ST && prod.tile < g.total_tiles; ++issued, advance(prod)) issue((int)issued, prod);
-    }
+    if (tid == 0)
+        for (int s = 0; s < ST && s < ktiles; ++s) issue(s, s);
 
-    long long pos = 0;  // stream position of the next consumed stage
-    for (int tile = blockIdx.x; tile < g.total_tiles; tile += gridDim.x) {
-        const TileCoord tc = tile_coord<CF>(g, tile);
-        if (tc.skip) continue;
-        const GemmProblem& P = g.p[tc.pid];
-        const int M = P.m, N = P.n;
-        const double* ks = KS ? P.ks : nullptr;
-        Acc<CF> acc;
-        zero_acc<CF>(acc);
-        for (int kt = 0; kt < tc.ktiles; ++kt, ++pos) {
-            const int stage = (int)(pos % ST);
-            mbar_wait(&full[stage], (unsigned)((pos / ST) & 1));
-            // refill the stage released one step ago with the stream's next fill (its last
-            // readers are this warp's previous k-tile and the other warps, at most a tile behind)
-            if (tid == 0 && pos >= 1 && prod.tile < g.total_tiles) {
-                const long long prev = pos - 1;
-                mbar_wait(&empty[prev % ST], (unsigned)((prev / ST) & 1));
-                issue((int)(issued % ST), prod);
-                ++issued;
-                advance(prod);
-            }
-            const cplx* sA = smA + stage * A_ELEMS;
-            const cplx* sB = smB + stage * B_ELEMS;
-            const int kbase = tc.kbeg + kt * BK;
+    Acc<CF> acc;
+    zero_acc<CF>(acc);
+    const int fr = lane >> 2, fc = lane & 3;
+    const double* ks = KS ? P.ks : nullptr;
+
+    for (int kt = 0; kt < ktiles; ++kt) {
+        const int stage = kt % ST;
+        mbar_wait(&full[stage], (kt / ST) & 1);
+        // refill the stage released one iteration ago (its last reader was this warp's previous
+        // k-tile; the other warps are at most a tile behind)
+        if (tid == 0 && kt >= 1 && kt - 1 + ST < ktiles) {
+            const int ps = (kt - 1) % ST;
+            mbar_wait(&empty[ps], ((kt - 1) / ST) & 1);
+            issue(ps, kt - 1 + ST);
+        }
+        const cplx* sA = smA + stage * A_ELEMS;
+        const cplx* sB = smB + stage * B_ELEMS;
+        const int kbase = kbeg + kt * BK;
 #pragma unroll(CF::MIN_BLOCKS >= 3 ? 1 : 4)
-            for (int kk = 0; kk < BK; kk += 4) {
-                if (kbase + kk >= tc.kend) break;  // K tail (uniform)
-                double kscale = 1.0;
-                if (ks != nullptr) {
-                    const int gk = kbase + kk + fc;
-                    kscale = gk < tc.kend ? __ldg(ks + gk) : 0.0;
-                }
-                mma_kstep<CF, OPA, TmaLayout>(sA, sB, kk, wm, wn, fr, fc, ks, kscale, tc.m0, tc.n0, M, N, acc);
+        for (int kk = 0; kk < BK; kk += 4) {
+            if (kbase + kk >= kend) break;  // K tail (uniform)
+            double kscale = 1.0;
+            if (ks != nullptr) {
+                const int gk = kbase + kk + fc;
+                kscale = gk < kend ? __ldg(ks + gk) : 0.0;
             }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[stage]);
+            mma_kstep<CF, OPA, TmaLayout>(sA, sB, kk, wm, wn, fr, fc, ks, kscale, m0, n0, M, N, acc);
         }
-        store_tile<CF>(P, tc, wm, wn, fr, fc, acc);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[stage]);
     }
+    store_tile<CF>(P, tc, wm, wn, fr, fc, acc);
 }
 
 // Fixed-order reduction of split-K partials + fused output scaling.
@@ -645,22 +620,12 @@ cudaError_t launch_cfg(GemmGroup& g, GemmOp opA, cudaStream_t s) {
     g.used_tma = tma_enabled() && make_tma_group<CF>(g, opA, tg) ? 1 : 0;
     if (g.used_tma) {
         const int sm = CF::TMA_SMEM_BYTES;
-        // persistent: one CTA per resident slot (or fewer when the group has fewer tiles)
-        static thread_local int per_sm[2][2] = {{0, 0}, {0, 0}};
-        int& occ = per_sm[opA == kOpN ? 0 : 1][any_ks ? 1 : 0];
-        if (occ == 0) {
-            auto kern = opA == kOpN ? (any_ks ? zgemm_tma_kernel<CF, kOpN, true> : zgemm_tma_kernel<CF, kOpN, false>)
-                                    : (any_ks ? zgemm_tma_kernel<CF, kOpC, true> : zgemm_tma_kernel<CF, kOpC, false>);
-            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, CF::NTHREADS, sm) != cudaSuccess || occ < 1)
-                occ = 1;
-        }
-        const int grid = std::min(total, occ * kNumSMs);
         if (opA == kOpN) {
-            if (any_ks) zgemm_tma_kernel<CF, kOpN, true><<<grid, CF::NTHREADS, sm, s>>>(tg);
-            else zgemm_tma_kernel<CF, kOpN, false><<<grid, CF::NTHREADS, sm, s>>>(tg);
+            if (any_ks) zgemm_tma_kernel<CF, kOpN, true><<<total, CF::NTHREADS, sm, s>>>(tg);
+            else zgemm_tma_kernel<CF, kOpN, false><<<total, CF::NTHREADS, sm, s>>>(tg);
         } else {
-            if (any_ks) zgemm_tma_kernel<CF, kOpC, true><<<grid, CF::NTHREADS, sm, s>>>(tg);
-            else zgemm_tma_kernel<CF, kOpC, false><<<grid, CF::NTHREADS, sm, s>>>(tg);
+            if (any_ks) zgemm_tma_kernel<CF, kOpC, true><<<total, CF::NTHREADS, sm, s>>>(tg);
+            else zgemm_tma_kernel<CF, kOpC, false><<<total, CF::NTHREADS, sm, s>>>(tg);
         }
     } else if (opA == kOpN) {
         if (any_ks) zgemm_dmma_kernel<CF, kOpN, true><<<total, CF::NTHREADS, CF::SMEM_BYTES, s>>>(g);
