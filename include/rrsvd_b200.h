@@ -275,6 +275,39 @@ int rrsvd_b200_evolve_prepared(rrsvd_b200_mps* mps, size_t n_sweeps, const rrsvd
 int rrsvd_b200_expectation_local(rrsvd_b200_mps* mps, size_t site, const double* op, double* out2);
 int rrsvd_b200_schmidt_entropy(rrsvd_b200_mps* mps, size_t bond, double* out);
 
+/* ---- multi-GPU: the chain-block partition (tebd.cpp:289-323 per rank) --------
+ * One rank per GPU owns the contiguous sites [first_site, first_site + owned) of an n_global-site
+ * chain; its device MPS (`block`) holds the owned sites plus, unless it is the last rank, a ghost
+ * copy of the next rank's first site, so the boundary bond is an ordinary local bond.  Per sweep:
+ * (1) ghost Γ + right-edge λ from rank+1, left-edge λ from rank-1 (one grouped send/recv on the
+ * context's stream); (2) the rank's bonds of the sweep's parity as one batch (evolve); (3) the
+ * updated ghost Γ back to its owner.  Messages have fixed capacities (chi_max x d x chi_max
+ * complexes; chi_max must be > 0) with a 3-integer dims header, so no shape round trip.  Seeds
+ * are the GLOBAL call indices (backend->seed = the base for global index 0, tebd.cpp:162), so a
+ * partitioned run reproduces the single-GPU one; backend->seed ends where the unpartitioned
+ * evolve's would.  gates[s * (block sites - 1) + local bond] as in rrsvd_b200_evolve_prepared;
+ * term_bonds[n_global - 1] flags the GLOBAL bonds that carry a term.  step0 offsets the step
+ * index of the seeds (continuing runs).  The discarded-weight budget is not supported
+ * (abort_discarded_threshold must stay 1); diag is this rank's (multiply kept fractions across
+ * ranks). */
+typedef struct rrsvd_b200_comm rrsvd_b200_comm;
+/* NCCL (libnccl.so.2, loaded at run time): rank 0 makes the 128-byte id and shares it out of band. */
+int rrsvd_b200_comm_unique_id(void* id128);
+int rrsvd_b200_comm_create_nccl(rrsvd_b200_ctx* ctx, int nranks, int rank, const void* id128,
+                                rrsvd_b200_comm** out);
+/* Host-staged loopback between host threads of one process (protocol checks on one GPU). */
+typedef struct rrsvd_b200_loopback_hub rrsvd_b200_loopback_hub;
+int rrsvd_b200_loopback_hub_create(int nranks, rrsvd_b200_loopback_hub** out);
+void rrsvd_b200_loopback_hub_destroy(rrsvd_b200_loopback_hub* hub);
+int rrsvd_b200_comm_create_loopback(rrsvd_b200_ctx* ctx, rrsvd_b200_loopback_hub* hub, int rank,
+                                    rrsvd_b200_comm** out);
+void rrsvd_b200_comm_destroy(rrsvd_b200_comm* comm);
+int rrsvd_b200_evolve_partitioned(rrsvd_b200_mps* block, rrsvd_b200_comm* comm, size_t first_site,
+                                  size_t n_global, size_t n_sweeps, const rrsvd_b200_sweep* sweeps,
+                                  const rrsvd_b200_gate* const* gates, const unsigned char* term_bonds,
+                                  size_t n_steps, uint64_t step0, rrsvd_b200_backend* backend,
+                                  const rrsvd_b200_evolve_options* options, rrsvd_b200_evolve_diag* diag);
+
 /* evolve splits each sweep's bonds over two auxiliary streams so one half's latency-bound
  * kernels overlap the other half's GEMMs (default on).  Off = one stream, serial stages. */
 int rrsvd_b200_set_overlap(rrsvd_b200_ctx* ctx, int on);

@@ -316,3 +316,90 @@ def evolve_loopback(parts: list, gates_by_sweep: dict, plan, dt: float, n_steps:
     for p in parts:
         p.refresh_finish()
     return kept
+
+
+# ------------------------------------------------------------------------------- native (C ABI)
+
+class NativeLoopbackHub:
+    """rrsvd_b200_loopback_hub: host-staged mailboxes between ranks run as host threads."""
+
+    def __init__(self, nranks: int):
+        import ctypes as C
+        from . import _lib as L
+        self.h = C.c_void_p()
+        rc = L.lib().rrsvd_b200_loopback_hub_create(C.c_int(nranks), C.byref(self.h))
+        if rc != 0:
+            raise RuntimeError("loopback hub")
+
+    def __del__(self):
+        from . import _lib as L
+        if getattr(self, "h", None) and L is not None:
+            L.lib().rrsvd_b200_loopback_hub_destroy(self.h)
+            self.h = None
+
+
+class NativeComm:
+    """rrsvd_b200_comm: the partition's transport behind the C ABI — NCCL between GPUs, or the
+    host loopback between threads of one process."""
+
+    def __init__(self, ctx, h):
+        self.ctx, self.h = ctx, h
+
+    @staticmethod
+    def unique_id() -> bytes:
+        import ctypes as C
+        from . import _lib as L
+        buf = (C.c_char * 128)()
+        if L.lib().rrsvd_b200_comm_unique_id(buf) != 0:
+            raise RuntimeError("ncclGetUniqueId failed (libnccl.so.2 not loadable?)")
+        return bytes(buf)
+
+    @classmethod
+    def nccl(cls, ctx, nranks: int, rank: int, uid: bytes) -> "NativeComm":
+        import ctypes as C
+        from . import _lib as L
+        h = C.c_void_p()
+        buf = (C.c_char * 128).from_buffer_copy(uid)
+        ctx.check(L.lib().rrsvd_b200_comm_create_nccl(ctx.h, C.c_int(nranks), C.c_int(rank), buf, C.byref(h)))
+        return cls(ctx, h)
+
+    @classmethod
+    def loopback(cls, ctx, hub: NativeLoopbackHub, rank: int) -> "NativeComm":
+        import ctypes as C
+        from . import _lib as L
+        h = C.c_void_p()
+        ctx.check(L.lib().rrsvd_b200_comm_create_loopback(ctx.h, hub.h, C.c_int(rank), C.byref(h)))
+        return cls(ctx, h)
+
+    def __del__(self):
+        from . import _lib as L
+        if getattr(self, "h", None) and L is not None:
+            L.lib().rrsvd_b200_comm_destroy(self.h)
+            self.h = None
+
+
+def evolve_partitioned(block, comm: NativeComm, first_site: int, n_global: int, gates: dict, plan,
+                       term_bonds, n_steps: int, backend, step0: int = 0):
+    """rrsvd_b200_evolve_partitioned for one rank: `block` is a DeviceMps of the rank's local chain
+    (owned sites + ghost), gates {(sweep, local bond): gate handle} (PreparedGates), term_bonds the
+    GLOBAL bonds carrying a term.  Returns this rank's EvolveDiagnostics; advances backend.seed to
+    where the unpartitioned evolve would leave it."""
+    import ctypes as C
+    from . import _lib as L
+    from .tebd import EvolveDiag, EvolveDiagnostics, EvolveOptions, Sweep
+    nb = block.n_sites - 1
+    sweeps = (Sweep * len(plan))(*[Sweep(p, c) for p, c in plan])
+    arr = (C.c_void_p * (len(plan) * nb))()
+    for (s, lb), g in gates.items():
+        arr[s * nb + lb] = g.value
+    flags = (C.c_ubyte * (n_global - 1))(*[1 if j in set(term_bonds) else 0 for j in range(n_global - 1)])
+    be = backend.to_c()
+    opt = EvolveOptions(1.0, 1, backend.omega_mode)
+    diag = EvolveDiag()
+    rc = L.lib().rrsvd_b200_evolve_partitioned(block.h, comm.h, C.c_size_t(first_site), C.c_size_t(n_global),
+                                               C.c_size_t(len(plan)), sweeps, arr, flags, C.c_size_t(n_steps),
+                                               C.c_uint64(step0), C.byref(be), C.byref(opt), C.byref(diag))
+    backend.seed = be.seed
+    block.ctx.check(rc)
+    return EvolveDiagnostics(diag.kept_fraction, int(diag.max_bond_dim), bool(diag.aborted), int(diag.abort_step),
+                             int(diag.n_updates), [])
