@@ -192,6 +192,8 @@ def run_partitioned(args, rank, world, local_rank):
             sk.bind(("127.0.0.1", 0))
             port = sk.getsockname()[1]
         os.environ.update(RANK="0", WORLD_SIZE="1", LOCAL_RANK="0", MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    if world > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")  # rank / transport lines on stderr for the driver
     if gloo:
         dist.init_process_group("gloo")
     else:
@@ -240,7 +242,24 @@ def run_partitioned(args, rank, world, local_rank):
             blk.set_gamma(i, site_gamma(gs), lam(gs) if i + 1 < len(local) else None)
 
     load_state()
-    part = ChainPartition(blk, TorchComm(red), list(range(n - 1)))
+    # the data plane: rrsvd_b200_evolve_partitioned over NCCL behind the C ABI (default), or the
+    # Python driver over torch.distributed P2P (RRSVD_B200_PARTITION=python; gloo protocol checks)
+    native = not gloo and os.environ.get("RRSVD_B200_PARTITION", "native") != "python"
+    if native:
+        from paper_1504_00992_b200.parallel import NativeComm, evolve_partitioned
+        uid = [NativeComm.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        comm = NativeComm.nccl(ctx, world, rank, uid[0])
+        local_gates = {(s_, j - a): h for (s_, j), h in gates.items()}
+
+        class _Native:
+            def evolve(self, gates_, plan_, dt_, n_steps_, be_, base_, step0=0):
+                be_.seed = base_
+                evolve_partitioned(blk.mps, comm, a, n, local_gates, plan_, list(range(n - 1)), n_steps_, be_,
+                                   step0=step0)
+        part = _Native()
+    else:
+        part = ChainPartition(blk, TorchComm(red), list(range(n - 1)))
     be = P.DecimationBackend(omega_mode=P.OMEGA_PHILOX, randomized=True, target_rank=0, oversampling=10,
                              power_iterations=2, det_crossover=256, seed=7)
     dist.barrier()  # a collective on the whole group before the first batched P2P exchange (NCCL)
@@ -307,7 +326,9 @@ def run_partitioned(args, rank, world, local_rank):
                        "sites": n, "chi": chi, "updates_per_step": int(ups.item()),
                        "parallelism": f"chain-block partition x{world}, " + (
                            "gloo host-staged exchange on shared GPUs (protocol check, not a measurement)"
-                           if gloo else "NCCL P2P boundary exchange"),
+                           if gloo else ("NCCL send/recv boundary exchange behind the C ABI "
+                                         "(rrsvd_b200_evolve_partitioned)" if native else
+                                         "NCCL P2P boundary exchange (Python driver)")),
                        "l2": "inputs larger than L2"},
             "decimations_per_s": round(float(ups.item()) * args.steps / elapsed, 3),
             "roofline": {"bound": "tensor", "peak": round(peak_dmma, 3), "unit": "TFLOP/s", "achieved": None,
