@@ -101,6 +101,11 @@ int rrsvd_b200_qr(rrsvd_b200_ctx* ctx, const double* A, size_t m, size_t n, doub
  * The building block of the row-sharded QR (linalg.cpp:49-65 over a distributed Y). */
 int rrsvd_b200_chol_inv(rrsvd_b200_ctx* ctx, const double* G, size_t l, double shift_scale,
                         double* T, int* ndead);
+/* The same, also reporting *ill = 1 when some pivot fell below 1e4 x the shift (or died): the
+ * device orthonormalisation's trigger for its extra passes (the adaptive CholeskyQR schedule,
+ * used by the row-sharded QR). */
+int rrsvd_b200_chol_inv_flags(rrsvd_b200_ctx* ctx, const double* G, size_t l, double shift_scale,
+                              double* T, int* ndead, int* ill);
 
 /* Full economy SVD A = U diag(S) V^H (U m x r, S r, V n x r, r = min(m,n)), S non-increasing;
  * replaces rrsvd::svd_full (linalg.cpp:67-88).  One-sided Jacobi on the device. */

@@ -101,17 +101,18 @@ def svd_full(a, ctx=None):
     return u, s, v
 
 
-def chol_inv(g, shift_scale: float = 0.0, ctx=None):
-    """T = R^-1 with G + s I = R^H R, s = shift_scale * 2^-53 * tr(G) (rrsvd_b200_chol_inv): one
-    CholeskyQR factor step on an already-formed (e.g. all-reduced) Gram matrix.
-    Returns (T, number of dependent columns)."""
+def chol_inv(g, shift_scale: float = 0.0, ctx=None, flags: bool = False):
+    """T = R^-1 with G + s I = R^H R, s = shift_scale * 2^-53 * tr(G) (rrsvd_b200_chol_inv_flags):
+    one CholeskyQR factor step on an already-formed (e.g. all-reduced) Gram matrix.
+    Returns (T, number of dependent columns[, ill]) — ill: a pivot fell below 1e4 x the shift."""
     c = _ctx(ctx)
     g = _prep(g)
     l = _shape(g)[0]
     t = _empty(g, (l, l), np.complex128)
-    nd = C.c_int()
-    c.check(L.lib().rrsvd_b200_chol_inv(c.h, ptr(g), sz(l), C.c_double(shift_scale), ptr(t), C.byref(nd)))
-    return t, nd.value
+    nd, ill = C.c_int(), C.c_int()
+    c.check(L.lib().rrsvd_b200_chol_inv_flags(c.h, ptr(g), sz(l), C.c_double(shift_scale), ptr(t), C.byref(nd),
+                                              C.byref(ill)))
+    return (t, nd.value, bool(ill.value)) if flags else (t, nd.value)
 
 
 def frobenius_norm(a, ctx=None) -> float:

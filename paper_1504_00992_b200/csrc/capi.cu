@@ -243,8 +243,8 @@ int rrsvd_b200_qr(rrsvd_b200_ctx* c, const double* A, size_t m, size_t n, double
     });
 }
 
-int rrsvd_b200_chol_inv(rrsvd_b200_ctx* c, const double* G, size_t l, double shift_scale, double* T,
-                        int* ndead) {
+int rrsvd_b200_chol_inv_flags(rrsvd_b200_ctx* c, const double* G, size_t l, double shift_scale, double* T,
+                              int* ndead, int* ill) {
     return api(c, [&] {
         if (l == 0) return;
         if (G == nullptr || T == nullptr) throw_contract(c, "chol_inv: null argument");
@@ -253,14 +253,23 @@ int rrsvd_b200_chol_inv(rrsvd_b200_ctx* c, const double* G, size_t l, double shi
         auto* dG = ws_get<cplx>(c, l * l);
         check_cuda(c, cudaMemcpyAsync(dG, G, l * l * sizeof(cplx), cudaMemcpyDefault, c->stream), "copy G");
         auto* dT = static_cast<cplx*>(stage_out(c, T, l * l * sizeof(cplx), outs));
-        int* dn = ws_get<int>(c, 1);
-        chol_inv_many(c, {CholSpec{dG, (int)l, shift_scale, dT, dn}});
+        int* dn = ws_get<int>(c, 2);
+        check_cuda(c, cudaMemsetAsync(dn, 0, 2 * sizeof(int), c->stream), "memset");
+        CholSpec cs{dG, (int)l, shift_scale, dT, dn};
+        cs.ill_out = dn + 1;
+        chol_inv_many(c, {cs});
         finish_out(c, outs);
-        int h = 0;
-        check_cuda(c, cudaMemcpyAsync(&h, dn, sizeof(int), cudaMemcpyDeviceToHost, c->stream), "D2H");
+        int h[2] = {0, 0};
+        check_cuda(c, cudaMemcpyAsync(h, dn, 2 * sizeof(int), cudaMemcpyDeviceToHost, c->stream), "D2H");
         check_cuda(c, cudaStreamSynchronize(c->stream), "sync");
-        if (ndead) *ndead = h;
+        if (ndead) *ndead = h[0];
+        if (ill) *ill = h[1];
     });
+}
+
+int rrsvd_b200_chol_inv(rrsvd_b200_ctx* c, const double* G, size_t l, double shift_scale, double* T,
+                        int* ndead) {
+    return rrsvd_b200_chol_inv_flags(c, G, l, shift_scale, T, ndead, nullptr);
 }
 
 int rrsvd_b200_svd(rrsvd_b200_ctx* c, const double* A, size_t m, size_t n, double* U, double* S,

@@ -7,10 +7,20 @@ step for step; only the reductions over the row dimension cross shards:
   Y_g = A_g Omega                        local (Omega replicated: same seed on every rank)
   QR of the distributed Y                shifted CholeskyQR: G = sum_g Y_g^H Y_g (all-reduce of
                                          l x l), T = chol_inv(G) replicated, Q_g = Y_g T
-  Z = A^H Q = sum_g A_g^H Q_g            all-reduce of n x l; QR of Z replicated
+  Z = A^H Q = sum_g A_g^H Q_g            all-reduce of n x l; QR of Z row-sharded over the ranks
+                                         (each its n/G rows), the orthonormal rows all-gathered
   Y_g = A_g Q~                           local
-  B^H = A^H Q                            all-reduce of n x l; SVD of B^H replicated (n x l)
+  B^H = A^H Q                            summed over ranks, then each rank keeps its row block
+                                         of the n rows: B^H = Q_b X by a row-sharded CholeskyQR
+                                         (l x l Gram all-reduce), X = Q_b^H B^H (l x l all-reduce),
+                                         the SVD of the l x l X^H = W S K^H replicated (small):
+                                         U_B = W, V = Q_b K row-sharded (pipeline.cu assemble_many's
+                                         algorithm, distributed — no rank holds or factors n x l)
   U_g = Q_g U_B                          local;  ||A||^2 = sum_g ||A_g||^2 (all-reduce)
+
+The CholeskyQR passes follow the device's adaptive schedule (pipeline.cu orth_many_adaptive): the
+first, shifted pass reports whether a pivot fell near the shift (rrsvd_b200_chol_inv_flags);
+only then do the extra passes run (full: 4 passes -> 2; span: 2 -> 1 for a well-conditioned Y).
 
 Communication is O(q n l) per decimation against O(q m n l / G) of GEMM work per rank.  Every
 rank may hold several shards (`shards` list): the local partial sums are added in a fixed order
@@ -31,6 +41,13 @@ from ._lib import OMEGA_REFERENCE
 FULL_PASSES, SPAN_PASSES = 4, 2  # pipeline.cuh kFullPasses / kSpanPasses
 
 
+def _adjoint(x):
+    """x^H as a dense array (torch: the conjugation materialised, not a conj-bit view)."""
+    if isinstance(x, np.ndarray):
+        return np.ascontiguousarray(x.conj().T)
+    return x.conj().T.resolve_conj().contiguous()
+
+
 class LocalSum:
     """Single process: the sum over ranks is the identity."""
     world = 1
@@ -38,6 +55,12 @@ class LocalSum:
 
     def allreduce(self, t):
         return t
+
+    def row_block(self, n):
+        return 0, n
+
+    def allgather_rows(self, block, n):
+        return block
 
 
 class TorchSum:
@@ -49,6 +72,25 @@ class TorchSum:
         import torch.distributed as dist
         self.torch, self.dist, self.device = torch, dist, device
         self.rank, self.world = dist.get_rank(), dist.get_world_size()
+
+    def row_block(self, n):
+        """This rank's rows [r0, r1) of an n-row replicated quantity."""
+        return (n * self.rank) // self.world, (n * (self.rank + 1)) // self.world
+
+    def allgather_rows(self, block, n):
+        """The row blocks of all ranks (row_block order) stacked into the n-row whole."""
+        torch = self.torch
+        was_np = isinstance(block, np.ndarray)
+        t = torch.from_numpy(np.ascontiguousarray(block)) if was_np else block
+        t = t.to(self.device).contiguous()
+        parts = []
+        for r in range(self.world):
+            r0, r1 = (n * r) // self.world, (n * (r + 1)) // self.world
+            parts.append(torch.empty((r1 - r0,) + tuple(t.shape[1:]), dtype=t.dtype, device=self.device))
+        view = (lambda u: torch.view_as_real(u)) if t.is_complex() else (lambda u: u)
+        self.dist.all_gather([view(p) for p in parts], view(t))
+        out = torch.cat(parts)
+        return out.cpu().numpy() if was_np else out
 
     def allreduce(self, t):
         """Sum over ranks; numpy in -> numpy out (host arrays travel through `device`)."""
@@ -73,7 +115,8 @@ class DeviceOps:
         return api.gemm(a, adj_a, b, ctx=self.ctx)
 
     def chol_inv(self, g, shift_scale):
-        return api.chol_inv(g, shift_scale, ctx=self.ctx)[0]
+        t, _, ill = api.chol_inv(g, shift_scale, ctx=self.ctx, flags=True)
+        return t, ill
 
     def svd(self, a):
         return api.svd_full(a, ctx=self.ctx)
@@ -102,21 +145,31 @@ class ShardedRrsvd:
             acc = self.ops.add(acc, p)
         return self.comm.allreduce(acc)
 
+    def _pass(self, ys, shift_scale):
+        g = self._rowsum([self.ops.gemm(y, True, y) for y in ys])
+        t, ill = self.ops.chol_inv(g, shift_scale)
+        return [self.ops.gemm(y, False, t) for y in ys], ill
+
     def _orth_sharded(self, ys, m_total, passes):
-        """Shifted CholeskyQR over row-sharded Y (pipeline.cu orth_many's schedule)."""
+        """CholeskyQR over row-sharded Y, the device's adaptive schedule (orth_many_adaptive):
+        full  = shifted | [ill] shifted, plain | plain;   span = shifted | [ill] shifted."""
         l = ys[0].shape[1]
-        for p in range(passes):
-            g = self._rowsum([self.ops.gemm(y, True, y) for y in ys])
-            t = self.ops.chol_inv(g, 10.0 * (m_total + l) if p < min(passes, 2) else 0.0)
-            ys = [self.ops.gemm(y, False, t) for y in ys]
-        return ys
+        shift = 10.0 * (m_total + l)
+        a, ill = self._pass(ys, shift)
+        if ill:  # (ill is computed from the all-reduced Gram: the same decision on every rank)
+            a, _ = self._pass(a, shift)
+            if passes == FULL_PASSES:
+                a, _ = self._pass(a, 0.0)
+        if passes == FULL_PASSES:
+            a, _ = self._pass(a, 0.0)
+        return a
 
     def _orth_replicated(self, z, passes):
         return self._orth_sharded([z], z.shape[0], passes)[0]
 
     def sketched_svd(self, shards, n: int, l: int, q: int, seed: int, mode: int = OMEGA_REFERENCE):
         """rrsvd_sketched_svd (randomized.cpp:101-107) of the row-stacked shards.
-        Returns (U row blocks, sigma (l), V (n x l), ||A||_F^2)."""
+        Returns (U row blocks, sigma (l), this rank's row block [r0, r1) of V (n x l), ||A||_F^2)."""
         ops = self.ops
         m_local = sum(a.shape[0] for a in shards)
         m_total = int(float(self.comm.allreduce(np.array([m_local], np.float64))[0]))
@@ -125,19 +178,26 @@ class ShardedRrsvd:
         om = ops.omega(n, l, seed, mode)
         inter = SPAN_PASSES if q > 0 else FULL_PASSES
         qs = self._orth_sharded([ops.gemm(a, False, om) for a in shards], m_total, inter)
+        r0, r1 = self.comm.row_block(n)
         for j in range(q):
+            # Z = A^H Q (n x l): each rank orthonormalises its row block (row-sharded CholeskyQR),
+            # then the rows are gathered for the next local product Y_g = A_g Q~
             z = self._rowsum([ops.gemm(a, True, qg) for a, qg in zip(shards, qs)])
-            qt = self._orth_replicated(z, SPAN_PASSES)
+            qt = self.comm.allgather_rows(self._orth_sharded([z[r0:r1]], n, SPAN_PASSES)[0], n)
             qs = self._orth_sharded([ops.gemm(a, False, qt) for a in shards], m_total,
                                     SPAN_PASSES if j + 1 < q else FULL_PASSES)
-        bh = self._rowsum([ops.gemm(a, True, qg) for a, qg in zip(shards, qs)])  # B^H = A^H Q
-        u_z, sigma, v_z = ops.svd(bh)  # B^H = U_z S V_z^H  =>  B = V_z S U_z^H
-        us = [ops.gemm(qg, False, v_z) for qg in qs]  # U = Q U_B, U_B = V_z
+        bh = self._rowsum([ops.gemm(a, True, qg) for a, qg in zip(shards, qs)])[r0:r1]  # B^H = A^H Q
+        qb = self._orth_sharded([bh], n, FULL_PASSES)[0]                      # B^H = Q_b X
+        x = self.comm.allreduce(ops.gemm(qb, True, bh))                         # X = Q_b^H B^H (l x l)
+        w, sigma, k = ops.svd(_adjoint(x))
+        v = ops.gemm(qb, False, k)                                              # V rows = Q_b K
+        us = [ops.gemm(qg, False, w) for qg in qs]                              # U = Q U_B, U_B = W
         total_sq = float(self.comm.allreduce(np.array([sum(ops.sumsq(a) for a in shards)], np.float64))[0])
-        return us, sigma, u_z, total_sq
+        return us, sigma, v, total_sq
 
     def fixed_rank(self, shards, n: int, k: int, p: int, q: int, seed: int, mode: int = OMEGA_REFERENCE):
-        """rrsvd_fixed_rank (randomized.cpp:109-122): (U row blocks (m_g x k), sigma (k), V (n x k), w)."""
+        """rrsvd_fixed_rank (randomized.cpp:109-122): (U row blocks (m_g x k), sigma (k), this
+        rank's row block of V (comm.row_block(n) rows x k; all n rows on one rank), w)."""
         if k < 2 or p < 2:
             raise api.ContractViolation("rrsvd_fixed_rank: requires k >= 2 and p >= 2")
         us, sigma, v, total_sq = self.sketched_svd(shards, n, k + p, q, seed, mode)

@@ -8,8 +8,9 @@ from oracle import port
 U = 2.0 ** -53
 
 
-def chol_inv(g, shift_scale):
-    """Shifted Cholesky + triangular inverse (the device chol_inv's contract, smallla.cuh)."""
+def chol_inv(g, shift_scale, flags=False):
+    """Shifted Cholesky + triangular inverse (the device chol_inv's contract, smallla.cuh); with
+    flags, also whether some pivot fell below 1e4 x the shift or died (kIllRatio)."""
     g = np.triu(np.asarray(g))
     g = g + np.triu(g, 1).conj().T
     l = g.shape[0]
@@ -18,10 +19,13 @@ def chol_inv(g, shift_scale):
     a = g + s * np.eye(l)
     r = np.zeros_like(a)
     dead = np.zeros(l, bool)
+    ill = False
     for j in range(l):
         piv = a[j, j].real
+        ill = ill or not piv >= 1e4 * s
         if not piv > 0.0:
             dead[j] = True
+            ill = True
             continue
         rj = np.sqrt(piv)
         r[j, j] = rj
@@ -32,7 +36,7 @@ def chol_inv(g, shift_scale):
     t = np.triu(np.linalg.inv(rp))
     t[:, dead] = 0.0
     t[dead, :] = 0.0
-    return t
+    return (t, ill) if flags else t
 
 
 class NumpyOps:
@@ -40,7 +44,7 @@ class NumpyOps:
         return (a.conj().T if adj_a else a) @ b
 
     def chol_inv(self, g, shift_scale):
-        return chol_inv(g, shift_scale)
+        return chol_inv(g, shift_scale, flags=True)
 
     def svd(self, a):
         u, s, vh = np.linalg.svd(a, full_matrices=False)

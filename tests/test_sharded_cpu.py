@@ -57,7 +57,7 @@ def _gloo_worker(rank, world, port_, outdir):
     dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port_}", rank=rank, world_size=world)
     shard = split(matrix(), world)[rank]
     us, s, v, w = ShardedRrsvd(TorchSum("cpu"), NumpyOps()).fixed_rank([shard], N, K, P, Q, SEED)
-    np.savez(os.path.join(outdir, f"rank{rank}.npz"), u=us[0], s=s, v=v, w=w)
+    np.savez(os.path.join(outdir, f"rank{rank}.npz"), u=us[0], s=s, v=v, w=w)  # v: this rank's rows
     dist.barrier()
     dist.destroy_process_group()
 
@@ -72,9 +72,11 @@ def test_gloo_two_ranks_equal_unsharded():
         mp.spawn(_gloo_worker, args=(2, port_, d), nprocs=2, join=True)
         z = [np.load(os.path.join(d, f"rank{r}.npz")) for r in range(2)]
     u = np.vstack([zz["u"] for zz in z])
+    v = np.vstack([zz["v"] for zz in z])  # V is row-sharded like U
     for zz in z:  # replicated results identical on every rank
-        assert np.array_equal(zz["s"], z[0]["s"]) and np.array_equal(zz["v"], z[0]["v"])
-    s, v, w = z[0]["s"], z[0]["v"], float(z[0]["w"])
+        assert np.array_equal(zz["s"], z[0]["s"]) and zz["w"] == z[0]["w"]
+    assert v.shape == (N, K)
+    s, w = z[0]["s"], float(z[0]["w"])
     assert np.max(np.abs(s - s1)) < 1e-13 * s1[0]
     assert abs(w - w1) < 1e-14
     assert np.linalg.norm((u * s) @ v.conj().T - (u1 * s1) @ v1.conj().T) < 1e-12 * np.linalg.norm(s1)
