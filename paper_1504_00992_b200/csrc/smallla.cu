@@ -472,7 +472,8 @@ __global__ void __launch_bounds__(JAC_CL_THREADS) jacobi_kernel(const __grid_con
 // in CTA 1's shared memory (DSMEM stores + release/acquire counters), and CTA 1 applies them to
 // V = I in order, trailing by at most kJpRing rounds (V never feeds back into X).  Same rotation
 // formula and convergence test as jacobi_kernel; W in / W out in jacobi_init's format.
-constexpr int kJpRing = 8;
+constexpr int kJpBatch = 4;   // rounds per published counter update
+constexpr int kJpRing = 16;   // ring slots (rounds); >= 2 kJpBatch so both sides overlap
 struct JpParam {
     double cc, ss, ex, ey;
 };
@@ -581,17 +582,11 @@ __global__ void __launch_bounds__(1024) jacobi_pair_kernel(const __grid_constant
                     if (hl == 0) peer_ring[(round % kJpRing) * npairs + pr] = prm;
                 }
                 __syncthreads();
-                if (tid == 0) {
-                    fence_cluster();
+                // publish every kJpBatch rounds (and at the end of a sweep): one release per batch
+                if (tid == 0 && ((round + 1) % kJpBatch == 0 || t == ce - 2))
                     st_remote_release_u32(peer_produced, round + 1);
-                }
             }
-            if ((tid & 31) == 0 && myrot) {
-                atomicAdd(&s_rot, myrot);
-                atomicMax(&s_off, (unsigned long long)__double_as_longlong(myoff2));
-            }
-            // (half-warps of one warp: the lane-0 half only saw its own pair; fold the other half)
-            if ((tid & 31) == 16 && myrot) {
+            if ((tid & 15) == 0 && myrot) {  // one lane per half-warp (pair)
                 atomicAdd(&s_rot, myrot);
                 atomicMax(&s_off, (unsigned long long)__double_as_longlong(myoff2));
             }
@@ -641,10 +636,7 @@ __global__ void __launch_bounds__(1024) jacobi_pair_kernel(const __grid_constant
             }
             __syncthreads();
             ++round;
-            if (tid == 0) {
-                fence_cluster();
-                st_remote_release_u32(peer_consumed, round);
-            }
+            if (tid == 0 && round % kJpBatch == 0) st_remote_release_u32(peer_consumed, round);
         }
         for (long long e = tid; e < (long long)c * c; e += blockDim.x) {
             const int j = (int)(e / c), i = (int)(e % c);
@@ -652,6 +644,85 @@ __global__ void __launch_bounds__(1024) jacobi_pair_kernel(const __grid_constant
         }
     }
     cluster.sync();  // neither CTA leaves while its peer may still touch its shared memory
+}
+
+// ---- Jacobi in one CTA: X and V both in its shared memory (small problems, e.g. config 1's
+// 74 x 74) — the same round-robin sweeps as jacobi_pair_kernel, each half-warp rotating its pair
+// in X and V in the same round; one __syncthreads per round, nothing else.
+__global__ void __launch_bounds__(1024) jacobi_onecta_kernel(const __grid_constant__ JacobiBatch b) {
+    extern __shared__ __align__(16) unsigned char sm[];
+    const int p = blockIdx.x;
+    const int r = b.r[p], c = b.c[p], ld = r + c;
+    const int ce = c + (c & 1), npairs = ce / 2;
+    const int tid = threadIdx.x, hl = tid & 15, pr = tid >> 4;
+    const unsigned hmask = 0xffffu << (threadIdx.x & 16);
+    cplx* col = reinterpret_cast<cplx*>(sm);  // [c][ld]: X rows then V rows, as in W
+    cplx* W = b.W[p];
+    __shared__ int s_rot;
+    __shared__ unsigned long long s_off;
+    for (long long e = tid; e < (long long)c * ld; e += blockDim.x) col[e] = W[e];
+    const double tol = sqrt((double)max(r, 1)) * kEps;
+    const double noise2 = (double)c * tol * tol;
+    int sweep = 0;
+    for (; sweep < kMaxSweeps; ++sweep) {
+        if (tid == 0) { s_rot = 0; s_off = 0ull; }
+        __syncthreads();
+        int myrot = 0;
+        double myoff2 = 0.0;
+        for (int t = 0; t < ce - 1; ++t) {
+            if (pr < npairs) {
+                const int a_ = circle(pr, t, ce), b_ = circle(ce - 1 - pr, t, ce);
+                if (a_ < c && b_ < c) {
+                    cplx* xp = col + (long long)a_ * ld;
+                    cplx* xq = col + (long long)b_ * ld;
+                    double aa = 0.0, bb = 0.0;
+                    cplx g = mk(0.0, 0.0);
+                    for (int i = hl; i < r; i += 16) {
+                        const cplx u = xp[i], v = xq[i];
+                        aa += cabs2(u); bb += cabs2(v); cfmac(g, u, v);
+                    }
+#pragma unroll
+                    for (int o = 8; o > 0; o >>= 1) {
+                        aa += __shfl_xor_sync(hmask, aa, o);
+                        bb += __shfl_xor_sync(hmask, bb, o);
+                        g.x += __shfl_xor_sync(hmask, g.x, o);
+                        g.y += __shfl_xor_sync(hmask, g.y, o);
+                    }
+                    const double g2 = g.x * g.x + g.y * g.y;
+                    if (aa > 0.0 && bb > 0.0 && g2 > tol * tol * aa * bb) {
+                        myoff2 = fmax(myoff2, g2 / (aa * bb));
+                        ++myrot;
+                        const double rg = rsqrt(g2);
+                        const cplx e = mk(g.x * rg, -g.y * rg);
+                        const double zeta = 0.5 * (bb - aa) * rg;
+                        const double az = fabs(zeta);
+                        const double h = az > 1e150 ? az : sqrt(fma(zeta, zeta, 1.0));
+                        const double tt = (zeta >= 0.0 ? 1.0 : -1.0) / (az + h);
+                        const double cc = rsqrt(fma(tt, tt, 1.0));
+                        const double ss = cc * tt;
+                        for (int i = hl; i < ld; i += 16) {
+                            const cplx u = xp[i];
+                            const cplx ev = cmul(e, xq[i]);
+                            xp[i] = mk(cc * u.x - ss * ev.x, cc * u.y - ss * ev.y);
+                            xq[i] = mk(ss * u.x + cc * ev.x, ss * u.y + cc * ev.y);
+                        }
+                    }
+                }
+            }
+            __syncthreads();
+        }
+        if ((tid & 15) == 0 && myrot) {
+            atomicAdd(&s_rot, myrot);
+            atomicMax(&s_off, (unsigned long long)__double_as_longlong(myoff2));
+        }
+        __syncthreads();
+        const int total = s_rot;
+        const double worst2 = __longlong_as_double((long long)s_off);
+        __syncthreads();
+        if (total == 0 || worst2 <= noise2) break;
+    }
+    for (long long e = tid; e < (long long)c * ld; e += blockDim.x) W[e] = col[e];
+    if (tid == 0 && b.sweeps[p] != nullptr) *b.sweeps[p] = sweep + 1;
 }
 
 constexpr int kColPermThreads = 512;
@@ -959,12 +1030,24 @@ bool jacobi_pair_enabled() {  // RRSVD_B200_JAC_PAIR=0: the cluster tournament k
 }
 }  // namespace
 
+size_t jacobi_onecta_need(int r, int c) { return (size_t)(r + c) * c * sizeof(cplx); }
+bool jacobi_onecta_fits(int r, int c) {
+    return jacobi_pair_enabled() && c >= 2 && ((c + 1) / 2) * 16 <= 1024 && jacobi_onecta_need(r, c) <= 220 * 1024;
+}
+
 bool jacobi_pair_fits(int r, int c) {
     return jacobi_pair_enabled() && c >= 2 && ((c + 1) / 2) * 16 <= 1024 && jacobi_pair_need(r, c) <= 220 * 1024;
 }
 
 cudaError_t jacobi_svd(const JacobiBatch& b, int max_r, int max_c, cudaStream_t s) {
     if (b.count == 0) return cudaSuccess;
+    if (jacobi_onecta_fits(max_r, max_c)) {
+        const size_t smem = jacobi_onecta_need(max_r, max_c);
+        cudaError_t e = cudaFuncSetAttribute(jacobi_onecta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        jacobi_onecta_kernel<<<b.count, 16 * ((max_c + 1) / 2), smem, s>>>(b);
+        return cudaGetLastError();
+    }
     if (jacobi_pair_fits(max_r, max_c)) {
         const size_t smem = jacobi_pair_need(max_r, max_c);
         cudaError_t e = cudaFuncSetAttribute(jacobi_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
