@@ -464,267 +464,6 @@ __global__ void __launch_bounds__(JAC_CL_THREADS) jacobi_kernel(const __grid_con
     if (rank == 0 && tid == 0 && b.sweeps[p] != nullptr) *b.sweeps[p] = sweep + 1;
 }
 
-// ---- Jacobi on a CTA pair: the rotator holds X, the accumulator holds V ----------------------
-// For problems whose c data columns (r rows) fit one CTA's shared memory.  CTA 0 runs the
-// one-sided Hestenes sweeps on X with the round-robin tournament over all c columns (c - 1 rounds
-// of disjoint pairs per sweep, one half-warp per pair, one __syncthreads per round — no global
-// round trips, no cluster barrier per round); each round's rotation parameters go through a ring
-// in CTA 1's shared memory (DSMEM stores + release/acquire counters), and CTA 1 applies them to
-// V = I in order, trailing by at most kJpRing rounds (V never feeds back into X).  Same rotation
-// formula and convergence test as jacobi_kernel; W in / W out in jacobi_init's format.
-constexpr int kJpBatch = 4;   // rounds per published counter update
-constexpr int kJpRing = 16;   // ring slots (rounds); >= 2 kJpBatch so both sides overlap
-struct JpParam {
-    double cc, ss, ex, ey;
-};
-__device__ __forceinline__ void fence_cluster() { asm volatile("fence.acq_rel.cluster;\n" ::: "memory"); }
-__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
-    unsigned v;
-    asm volatile("ld.acquire.cluster.shared::cta.u32 %0, [%1];\n" : "=r"(v) : "r"(smem_u32(p)) : "memory");
-    return v;
-}
-__device__ __forceinline__ void st_remote_release_u32(unsigned* local_addr_in_peer_map, unsigned v) {
-    // generic address of the peer's shared word (cluster.map_shared_rank): a release store
-    asm volatile("st.release.cluster.u32 [%0], %1;\n" ::"l"(local_addr_in_peer_map), "r"(v) : "memory");
-}
-
-__global__ void __launch_bounds__(1024) jacobi_pair_kernel(const __grid_constant__ JacobiBatch b) {
-    extern __shared__ __align__(16) unsigned char sm[];
-    cg::cluster_group cluster = cg::this_cluster();
-    const int role = (int)cluster.block_rank();  // 0: rotator (X), 1: accumulator (V)
-    const int p = blockIdx.x / 2;
-    const int r = b.r[p], c = b.c[p], ld = r + c;
-    const int ce = c + (c & 1);                    // players (an odd c gets a bye)
-    const int npairs = ce / 2;
-    const int tid = threadIdx.x, hl = tid & 15, pr = tid >> 4;
-    const unsigned hmask = 0xffffu << (threadIdx.x & 16);  // this half-warp's lanes
-    cplx* W = b.W[p];
-    __shared__ unsigned produced, consumed, final_rounds, done_flag;
-    __shared__ int s_rot;
-    __shared__ unsigned long long s_off;
-    cplx* col = reinterpret_cast<cplx*>(sm);  // role 0: [c][r] X;  role 1: [c][c] V, then the ring
-    JpParam* ring = reinterpret_cast<JpParam*>(sm + (size_t)c * c * sizeof(cplx));
-    if (tid == 0) { produced = consumed = final_rounds = done_flag = 0u; }
-    // load my half of W
-    if (role == 0) {
-        for (long long e = tid; e < (long long)c * r; e += blockDim.x) {
-            const int j = (int)(e / r), i = (int)(e % r);
-            col[e] = W[(long long)j * ld + i];
-        }
-    } else {
-        for (long long e = tid; e < (long long)c * c; e += blockDim.x) {
-            const int j = (int)(e / c), i = (int)(e % c);
-            col[e] = W[(long long)j * ld + r + i];
-        }
-    }
-    cluster.sync();
-    unsigned* peer_produced = cluster.map_shared_rank(&produced, 1);
-    unsigned* peer_final = cluster.map_shared_rank(&final_rounds, 1);
-    unsigned* peer_done = cluster.map_shared_rank(&done_flag, 1);
-    unsigned* peer_consumed = cluster.map_shared_rank(&consumed, 0);
-    JpParam* peer_ring = cluster.map_shared_rank(ring, 1);
-
-    if (role == 0) {
-        const double tol = sqrt((double)max(r, 1)) * kEps;
-        const double noise2 = (double)c * tol * tol;
-        unsigned round = 0;
-        int sweep = 0;
-        for (; sweep < kMaxSweeps; ++sweep) {
-            if (tid == 0) { s_rot = 0; s_off = 0ull; }
-            __syncthreads();
-            int myrot = 0;
-            double myoff2 = 0.0;
-            for (int t = 0; t < ce - 1; ++t, ++round) {
-                // flow control: the ring slot of this round must have been applied by CTA 1
-                if (tid == 0 && round >= (unsigned)kJpRing)
-                    while (ld_acquire_u32(&consumed) + kJpRing <= round) {}
-                __syncthreads();
-                if (pr < npairs) {
-                    const int a_ = circle(pr, t, ce), b_ = circle(ce - 1 - pr, t, ce);
-                    JpParam prm{1.0, 0.0, 1.0, 0.0};
-                    if (a_ < c && b_ < c) {
-                        cplx* xp = col + (long long)a_ * r;
-                        cplx* xq = col + (long long)b_ * r;
-                        double aa = 0.0, bb = 0.0;
-                        cplx g = mk(0.0, 0.0);
-                        for (int i = hl; i < r; i += 16) {
-                            const cplx u = xp[i], v = xq[i];
-                            aa += cabs2(u); bb += cabs2(v); cfmac(g, u, v);
-                        }
-#pragma unroll
-                        for (int o = 8; o > 0; o >>= 1) {
-                            aa += __shfl_xor_sync(hmask, aa, o);
-                            bb += __shfl_xor_sync(hmask, bb, o);
-                            g.x += __shfl_xor_sync(hmask, g.x, o);
-                            g.y += __shfl_xor_sync(hmask, g.y, o);
-                        }
-                        const double g2 = g.x * g.x + g.y * g.y;
-                        if (aa > 0.0 && bb > 0.0 && g2 > tol * tol * aa * bb) {
-                            myoff2 = fmax(myoff2, g2 / (aa * bb));
-                            ++myrot;
-                            const double rg = rsqrt(g2);
-                            const cplx e = mk(g.x * rg, -g.y * rg);
-                            const double zeta = 0.5 * (bb - aa) * rg;
-                            const double az = fabs(zeta);
-                            const double h = az > 1e150 ? az : sqrt(fma(zeta, zeta, 1.0));
-                            const double tt = (zeta >= 0.0 ? 1.0 : -1.0) / (az + h);
-                            const double cc = rsqrt(fma(tt, tt, 1.0));
-                            const double ss = cc * tt;
-                            for (int i = hl; i < r; i += 16) {
-                                const cplx u = xp[i];
-                                const cplx ev = cmul(e, xq[i]);
-                                xp[i] = mk(cc * u.x - ss * ev.x, cc * u.y - ss * ev.y);
-                                xq[i] = mk(ss * u.x + cc * ev.x, ss * u.y + cc * ev.y);
-                            }
-                            prm = JpParam{cc, ss, e.x, e.y};
-                        }
-                    }
-                    if (hl == 0) peer_ring[(round % kJpRing) * npairs + pr] = prm;
-                }
-                __syncthreads();
-                // publish every kJpBatch rounds (and at the end of a sweep): one release per batch
-                if (tid == 0 && ((round + 1) % kJpBatch == 0 || t == ce - 2))
-                    st_remote_release_u32(peer_produced, round + 1);
-            }
-            if ((tid & 15) == 0 && myrot) {  // one lane per half-warp (pair)
-                atomicAdd(&s_rot, myrot);
-                atomicMax(&s_off, (unsigned long long)__double_as_longlong(myoff2));
-            }
-            __syncthreads();
-            const int total = s_rot;
-            const double worst2 = __longlong_as_double((long long)s_off);
-            __syncthreads();
-            if (total == 0 || worst2 <= noise2) break;
-        }
-        if (tid == 0) {
-            st_remote_release_u32(peer_final, round);
-            fence_cluster();
-            st_remote_release_u32(peer_done, 1u);
-        }
-        for (long long e = tid; e < (long long)c * r; e += blockDim.x) {
-            const int j = (int)(e / r), i = (int)(e % r);
-            W[(long long)j * ld + i] = col[e];
-        }
-        if (tid == 0 && b.sweeps[p] != nullptr) *b.sweeps[p] = sweep + 1;
-    } else {
-        unsigned round = 0;
-        while (true) {
-            if (tid == 0) {
-                unsigned have;
-                while ((have = ld_acquire_u32(&produced)) <= round) {
-                    if (ld_acquire_u32(&done_flag) && ld_acquire_u32(&final_rounds) <= round) break;
-                }
-                s_rot = (ld_acquire_u32(&produced) > round) ? 1 : 0;
-            }
-            __syncthreads();
-            if (!s_rot) break;
-            const int t = (int)(round % (unsigned)(ce - 1));
-            if (pr < npairs) {
-                const int a_ = circle(pr, t, ce), b_ = circle(ce - 1 - pr, t, ce);
-                const JpParam prm = ring[(round % kJpRing) * npairs + pr];
-                if (a_ < c && b_ < c && prm.ss != 0.0) {
-                    cplx* vp = col + (long long)a_ * c;
-                    cplx* vq = col + (long long)b_ * c;
-                    const cplx e = mk(prm.ex, prm.ey);
-                    for (int i = hl; i < c; i += 16) {
-                        const cplx u = vp[i];
-                        const cplx ev = cmul(e, vq[i]);
-                        vp[i] = mk(prm.cc * u.x - prm.ss * ev.x, prm.cc * u.y - prm.ss * ev.y);
-                        vq[i] = mk(prm.ss * u.x + prm.cc * ev.x, prm.ss * u.y + prm.cc * ev.y);
-                    }
-                }
-            }
-            __syncthreads();
-            ++round;
-            if (tid == 0 && round % kJpBatch == 0) st_remote_release_u32(peer_consumed, round);
-        }
-        for (long long e = tid; e < (long long)c * c; e += blockDim.x) {
-            const int j = (int)(e / c), i = (int)(e % c);
-            W[(long long)j * ld + r + i] = col[e];
-        }
-    }
-    cluster.sync();  // neither CTA leaves while its peer may still touch its shared memory
-}
-
-// ---- Jacobi in one CTA: X and V both in its shared memory (small problems, e.g. config 1's
-// 74 x 74) — the same round-robin sweeps as jacobi_pair_kernel, each half-warp rotating its pair
-// in X and V in the same round; one __syncthreads per round, nothing else.
-__global__ void __launch_bounds__(1024) jacobi_onecta_kernel(const __grid_constant__ JacobiBatch b) {
-    extern __shared__ __align__(16) unsigned char sm[];
-    const int p = blockIdx.x;
-    const int r = b.r[p], c = b.c[p], ld = r + c;
-    const int ce = c + (c & 1), npairs = ce / 2;
-    const int tid = threadIdx.x, hl = tid & 15, pr = tid >> 4;
-    const unsigned hmask = 0xffffu << (threadIdx.x & 16);
-    cplx* col = reinterpret_cast<cplx*>(sm);  // [c][ld]: X rows then V rows, as in W
-    cplx* W = b.W[p];
-    __shared__ int s_rot;
-    __shared__ unsigned long long s_off;
-    for (long long e = tid; e < (long long)c * ld; e += blockDim.x) col[e] = W[e];
-    const double tol = sqrt((double)max(r, 1)) * kEps;
-    const double noise2 = (double)c * tol * tol;
-    int sweep = 0;
-    for (; sweep < kMaxSweeps; ++sweep) {
-        if (tid == 0) { s_rot = 0; s_off = 0ull; }
-        __syncthreads();
-        int myrot = 0;
-        double myoff2 = 0.0;
-        for (int t = 0; t < ce - 1; ++t) {
-            if (pr < npairs) {
-                const int a_ = circle(pr, t, ce), b_ = circle(ce - 1 - pr, t, ce);
-                if (a_ < c && b_ < c) {
-                    cplx* xp = col + (long long)a_ * ld;
-                    cplx* xq = col + (long long)b_ * ld;
-                    double aa = 0.0, bb = 0.0;
-                    cplx g = mk(0.0, 0.0);
-                    for (int i = hl; i < r; i += 16) {
-                        const cplx u = xp[i], v = xq[i];
-                        aa += cabs2(u); bb += cabs2(v); cfmac(g, u, v);
-                    }
-#pragma unroll
-                    for (int o = 8; o > 0; o >>= 1) {
-                        aa += __shfl_xor_sync(hmask, aa, o);
-                        bb += __shfl_xor_sync(hmask, bb, o);
-                        g.x += __shfl_xor_sync(hmask, g.x, o);
-                        g.y += __shfl_xor_sync(hmask, g.y, o);
-                    }
-                    const double g2 = g.x * g.x + g.y * g.y;
-                    if (aa > 0.0 && bb > 0.0 && g2 > tol * tol * aa * bb) {
-                        myoff2 = fmax(myoff2, g2 / (aa * bb));
-                        ++myrot;
-                        const double rg = rsqrt(g2);
-                        const cplx e = mk(g.x * rg, -g.y * rg);
-                        const double zeta = 0.5 * (bb - aa) * rg;
-                        const double az = fabs(zeta);
-                        const double h = az > 1e150 ? az : sqrt(fma(zeta, zeta, 1.0));
-                        const double tt = (zeta >= 0.0 ? 1.0 : -1.0) / (az + h);
-                        const double cc = rsqrt(fma(tt, tt, 1.0));
-                        const double ss = cc * tt;
-                        for (int i = hl; i < ld; i += 16) {
-                            const cplx u = xp[i];
-                            const cplx ev = cmul(e, xq[i]);
-                            xp[i] = mk(cc * u.x - ss * ev.x, cc * u.y - ss * ev.y);
-                            xq[i] = mk(ss * u.x + cc * ev.x, ss * u.y + cc * ev.y);
-                        }
-                    }
-                }
-            }
-            __syncthreads();
-        }
-        if ((tid & 15) == 0 && myrot) {
-            atomicAdd(&s_rot, myrot);
-            atomicMax(&s_off, (unsigned long long)__double_as_longlong(myoff2));
-        }
-        __syncthreads();
-        const int total = s_rot;
-        const double worst2 = __longlong_as_double((long long)s_off);
-        __syncthreads();
-        if (total == 0 || worst2 <= noise2) break;
-    }
-    for (long long e = tid; e < (long long)c * ld; e += blockDim.x) W[e] = col[e];
-    if (tid == 0 && b.sweeps[p] != nullptr) *b.sweeps[p] = sweep + 1;
-}
-
 constexpr int kColPermThreads = 512;
 __global__ void __launch_bounds__(kColPermThreads) colperm_rank_kernel(const __grid_constant__ ColPermBatch b) {
     extern __shared__ __align__(16) unsigned char sm[];
@@ -1013,59 +752,10 @@ int jacobi_cluster(int r, int c) {
 }
 }  // namespace
 
-bool jacobi_fits(int r, int c) { return jacobi_pair_fits(r, c) || jacobi_cluster(r, c) > 0; }
-
-namespace {
-size_t jacobi_pair_need(int r, int c) {
-    const size_t x = (size_t)r * c * sizeof(cplx);
-    const size_t v = (size_t)c * c * sizeof(cplx) + (size_t)kJpRing * ((c + 1) / 2) * sizeof(JpParam);
-    return x > v ? x : v;
-}
-bool jacobi_pair_enabled() {  // RRSVD_B200_JAC_PAIR=0: the cluster tournament kernel (A/B)
-    static const bool on = [] {
-        const char* e = std::getenv("RRSVD_B200_JAC_PAIR");
-        return e == nullptr || std::atoi(e) != 0;
-    }();
-    return on;
-}
-}  // namespace
-
-size_t jacobi_onecta_need(int r, int c) { return (size_t)(r + c) * c * sizeof(cplx); }
-bool jacobi_onecta_fits(int r, int c) {
-    return jacobi_pair_enabled() && c >= 2 && ((c + 1) / 2) * 16 <= 1024 && jacobi_onecta_need(r, c) <= 220 * 1024;
-}
-
-bool jacobi_pair_fits(int r, int c) {
-    return jacobi_pair_enabled() && c >= 2 && ((c + 1) / 2) * 16 <= 1024 && jacobi_pair_need(r, c) <= 220 * 1024;
-}
+bool jacobi_fits(int r, int c) { return jacobi_cluster(r, c) > 0; }
 
 cudaError_t jacobi_svd(const JacobiBatch& b, int max_r, int max_c, cudaStream_t s) {
     if (b.count == 0) return cudaSuccess;
-    if (jacobi_onecta_fits(max_r, max_c)) {
-        const size_t smem = jacobi_onecta_need(max_r, max_c);
-        cudaError_t e = cudaFuncSetAttribute(jacobi_onecta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        jacobi_onecta_kernel<<<b.count, 16 * ((max_c + 1) / 2), smem, s>>>(b);
-        return cudaGetLastError();
-    }
-    if (jacobi_pair_fits(max_r, max_c)) {
-        const size_t smem = jacobi_pair_need(max_r, max_c);
-        cudaError_t e = cudaFuncSetAttribute(jacobi_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = dim3(2 * b.count);
-        cfg.blockDim = dim3(16 * ((max_c + 1) / 2));
-        cfg.dynamicSmemBytes = smem;
-        cfg.stream = s;
-        cudaLaunchAttribute attr[1];
-        attr[0].id = cudaLaunchAttributeClusterDimension;
-        attr[0].val.clusterDim.x = 2;
-        attr[0].val.clusterDim.y = 1;
-        attr[0].val.clusterDim.z = 1;
-        cfg.attrs = attr;
-        cfg.numAttrs = 1;
-        return cudaLaunchKernelEx(&cfg, jacobi_pair_kernel, b);
-    }
     const int cs = jacobi_cluster(max_r, max_c);
     if (cs == 0) return cudaErrorInvalidValue;
     const size_t smem = jacobi_need(max_r, max_c, cs);

@@ -55,8 +55,6 @@ struct SelectBatch {
 cudaError_t select_many(const SelectBatch& b, cudaStream_t s);
 cudaError_t chol_inv(const CholBatch& b, int max_l, cudaStream_t s);
 bool jacobi_fits(int r, int c);  // an r x c problem fits jacobi_svd's on-chip capacity
-// The CTA-pair Jacobi (rotator + accumulator, one half-warp per pair) takes the problem.
-bool jacobi_pair_fits(int r, int c);
 
 // ---- static column pivoting for the QR-preconditioned Jacobi: order the columns of each
 // row-major r x c matrix X by decreasing norm (ties by index), Xp[:, k] = X[:, perm[k]]; after
