@@ -76,6 +76,16 @@ def workload(name: str):
                     terms={b: t for b, t in enumerate(M.ising_terms(n, 1.0, 1.0))}, chi=128, dt=0.01,
                     backend=dict(randomized=False, det_crossover=256, seed=7),
                     desc="Ising L=64, d=2, chi=128 (n=256), deterministic (reference default crossover)")
+    if name == "c4mpdo":  # config 4 at a feasible d: the mixed-state TEDOPA chain as an MPDO
+        site_dims, terms = M.tedopa_system(n_chain=100, boson_dim=4)
+        dims2, lterms = M.mpdo_terms(site_dims, terms)
+        return dict(name="mpdo_tedopa_101sites_d4sq16_chi200", site_dims=dims2,
+                    terms={b: t for b, t in enumerate(lterms)}, chi=200, dt=0.01,
+                    backend=dict(randomized=True, target_rank=0, oversampling=10, power_iterations=2,
+                                 det_crossover=256, seed=7),
+                    desc="MPDO TEDOPA (vec rho, sites d^2 = 16: oscillators d = 4), chi = 200, n = 3200, "
+                         "Liouvillian gates U (x) U*, RRSVD p=10 q=2 (config 4; d^2 = 400 would make one "
+                         "Theta 102 GB)")
     if name == "c2rr":  # config 2's RRSVD arm: randomized decimation forced (tebd.cpp:167-186)
         n = 64
         return dict(name="ising_L64_d2_chi128_rrsvd", site_dims=[2] * n,
@@ -206,9 +216,13 @@ def run_partitioned(args, rank, world, local_rank):
     nb = 100 * world
     om_x = np.tile(om, world)
     hop_x = np.tile(np.append(hop, hop[-1]), world)[:nb - 1]
-    site_dims, terms_l = M.build_chain_terms(t0c, om_x, hop_x, 20, 0.5 * M.SZ + 0.5 * M.SX, M.SZ)
+    mpdo = args.workload == "c4mpdo"
+    boson = 4 if mpdo else 20
+    site_dims, terms_l = M.build_chain_terms(t0c, om_x, hop_x, boson, 0.5 * M.SZ + 0.5 * M.SX, M.SZ)
+    if mpdo:  # config 4: the mixed-state chain as an MPDO (Liouvillian terms, d^2 sites)
+        site_dims, terms_l = M.mpdo_terms(site_dims, terms_l)
     n = len(site_dims)
-    chi, dt = 100, 0.01
+    chi, dt = (200 if mpdo else 100), 0.01
     bounds = [0] + [1 + 100 * (r + 1) for r in range(world)]
     a, b = bounds[rank], bounds[rank + 1]
     spec = BlockSpec(rank, world, a, b, n)
@@ -320,7 +334,8 @@ def run_partitioned(args, rank, world, local_rank):
             "ms_per_step": round(1e3 * elapsed / args.steps, 3), "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "c128 (fp64)",
             "data": "synthetic χ-saturated MPS + TEDOPA bond gates (config-3 chain coefficients repeated per block)",
-            "config": {"workload": f"tedopa_spin_boson_{n}sites_d20_chi100_chain_blocks",
+            "config": {"workload": (f"mpdo_tedopa_{n}sites_d4sq16_chi200_chain_blocks" if mpdo else
+                                    f"tedopa_spin_boson_{n}sites_d20_chi100_chain_blocks"),
                        "desc": "weak scaling: one config-3-sized block (100 bosons, n=2000 bonds) per GPU; "
                                "value = blocks x steps / s (each block is a config-3 chain)",
                        "sites": n, "chi": chi, "updates_per_step": int(ups.item()),
@@ -725,14 +740,21 @@ def run_reference(args, rank, world):
     ref_update_sample(ref, wl, gammas, lambdas, gates, plan, [(n - 1) // 2], 100)
     warm_s = time.perf_counter() - tw
     be = ref.Backend(**wl["backend"])
-    t0 = time.perf_counter()
-    d = rm.evolve(terms, wl["dt"], 1, be)
-    wall = time.perf_counter() - t0
+    if args.workload == "c4mpdo":  # a whole MPDO step is ~15 min of CPU: time 2 interior updates
+        sec = ref_update_sample(ref, wl, gammas, lambdas, gates, plan, [(n - 1) // 2 - 1, (n - 1) // 2], 7)
+        wall = sec * ups
+        d = {"n_updates": ups, "update_us": wall * 1e6}
+        sample = (f"2 interior bond updates (build_theta+apply_gate+decimate) of the same state, {sec:.2f} s/update, "
+                  f"extrapolated x{ups} updates/step")
+    else:
+        t0 = time.perf_counter()
+        d = rm.evolve(terms, wl["dt"], 1, be)
+        wall = time.perf_counter() - t0
+        sample = (f"one full step: the reference evolve(state, terms, plan, 1, backend) on the same synthetic "
+                  f"state ({d['n_updates']} updates, {wall:.1f} s incl. the per-call gate rebuild; "
+                  f"{d['update_us'] / 1e6:.1f} s in build_theta+apply_gate+decimate)")
     upd = d["update_us"] / 1e6
     v = 1.0 / wall
-    sample = (f"one full step: the reference evolve(state, terms, plan, 1, backend) on the same synthetic "
-              f"state ({d['n_updates']} updates, {wall:.1f} s incl. the per-call gate rebuild; "
-              f"{upd:.1f} s in build_theta+apply_gate+decimate)")
     emit({
         "impl": "reference", "metric": METRIC, "value": round(v, 8), "unit": "steps/s", "n_gpus": world,
         "steps": 1, "warmup": 0, "steps_requested": args.steps, "warmup_requested": args.warmup,
@@ -756,8 +778,9 @@ def main():
                     help="timed steps (default 10; 1 for c3det, whose steps take ~40 s)")
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="c3", choices=["c3", "c3p100", "c3det", "c2", "c2rr", "c5", "c4"],
-                    help="c3 (headline TEBD), c3p100, c3det, c2, c2rr; c5/c4: row-sharded single-matrix RRSVD")
+    ap.add_argument("--workload", default="c3", choices=["c3", "c3p100", "c3det", "c2", "c2rr", "c4mpdo", "c5", "c4"],
+                    help="c3 (headline TEBD), c3p100, c3det, c2, c2rr, c4mpdo (MPDO chain); c5/c4: row-sharded "
+                         "single-matrix RRSVD")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--force-partition", action="store_true",
                     help="use the chain-block partition driver even on one GPU (smoke test of the N>1 path)")

@@ -198,3 +198,38 @@ def synthetic_saturated_mps(site_dims, chi: int, seed: int = 0, decay: float = 0
         v = decay ** np.arange(bonds[b])
         lambdas.append(v / np.linalg.norm(v))
     return gammas, lambdas
+
+
+# ---- mixed states: the MPDO in Liouville space (config 4's shape) -----------------------------
+# The reference evolves pure states only (mps.hpp:121-134).  A density operator is evolved as
+# the "MPS" of vec(rho) with site dimension d^2 (site index k*d + b: ket k, bra b) under the
+# Liouvillian terms L_b = H_b (x) 1 - 1 (x) H_b^T on (kets, bras): exp(-i dt L_b) = U (x) U* with
+# U = exp(-i dt H_b) — the two-site gate "applied as U (x) U* factors".  Both the reference's own
+# evolve (tebd.cpp:260-326, bond_gate = exp(-i dt L_b) via zheevd) and the device run it
+# unchanged; the gates of number-conserving terms stay block-sparse (kets x bras sectors).
+
+def liouville_term(h: np.ndarray, d1: int, d2: int) -> np.ndarray:
+    """L = H (x) 1 - 1 (x) H^T for a two-site H on (k1, k2), in the MPDO ordering
+    ((k1 d1 + b1) d2^2 + (k2 d2 + b2)) of the doubled sites."""
+    h = np.asarray(h, np.complex128).reshape(d1, d2, d1, d2)  # H[k1, k2, k1', k2']
+    e1, e2 = np.eye(d1), np.eye(d2)
+    # L[k1 b1 k2 b2, k1' b1' k2' b2'] = H[k1 k2, k1' k2'] d(b1 b1') d(b2 b2')
+    #                                  - d(k1 k1') d(k2 k2') H[b1' b2', b1 b2]
+    L = np.einsum("acxz,by,dw->abcdxyzw", h, e1, e2)
+    L -= np.einsum("ax,cz,ywbd->abcdxyzw", e1, e2, h)
+    n = d1 * d1 * d2 * d2
+    return L.reshape(n, n)
+
+
+def mpdo_terms(site_dims, terms):
+    """(doubled site dims, Liouvillian bond terms) of a pure-state chain's Hamiltonian terms."""
+    dims2 = [d * d for d in site_dims]
+    out = [liouville_term(h, site_dims[b], site_dims[b + 1]) for b, h in enumerate(terms)]
+    return dims2, out
+
+
+def mpdo_local(psi: np.ndarray) -> np.ndarray:
+    """vec(|psi><psi|) in the (k d + b) site ordering: psi (x) conj(psi)."""
+    psi = np.asarray(psi, np.complex128)
+    return np.kron(psi, psi.conj())
+

@@ -218,3 +218,26 @@ def test_evolve_rejected_theta_leaves_state_consistent(ref):
     # before taking a seed -> the counter stands at 41, where the reference's would
     assert be.seed == 41
     evolve(dm, terms, 0.05, 1, P.DecimationBackend())  # the state is usable again
+
+
+def test_mpdo_tedopa_chain_matches_reference(ref):
+    """BASELINE configs[3] shape at a feasible d: the mixed-state TEDOPA chain as
+    an MPDO — vec(rho) with site dimension d^2 (spin 2 -> 4, oscillators d = 3 -> 9), Liouvillian
+    terms L = H (x) 1 - 1 (x) H^T, so every two-site gate is U (x) U* (block-sparse for the
+    number-conserving oscillator bonds) — evolved by the reference's own evolve and on the device
+    with the same seeds: <sigma_z (x) 1> on the spin, <n (x) 1> on the oscillators and every bond
+    entropy within 1e-8, identical chi profile."""
+    n_chain, d, chi = 4, 3, 24
+    t0, om, hop = Mdl.ohmic_chain(n_chain, 2001)
+    dims, terms = Mdl.build_chain_terms(t0, om, hop, d, 0.5 * Mdl.SZ + 0.5 * Mdl.SX, Mdl.SZ)
+    dims2, lterms = Mdl.mpdo_terms(dims, terms)
+    rng = np.random.default_rng(3)
+    psis = [np.array([1, 0], complex)] + [v / np.linalg.norm(v) for v in cplx_randn(rng, n_chain, d)]
+    locals_ = [Mdl.mpdo_local(p) for p in psis]
+    kw = dict(randomized=True, target_rank=chi, oversampling=6, power_iterations=2, det_crossover=40, seed=23)
+    ops = [np.kron(Mdl.SZ, np.eye(2))] + [np.kron(np.diag(np.arange(d)), np.eye(d)).astype(complex)] * n_chain
+    for rm, dm, rd, dd in run_both(ref, dims2, lterms, 0.1, 3, chi, kw, locals_, chunks=3):
+        assert dd.max_bond_dim == rd["max_bond_dim"]
+        assert abs(dd.kept_fraction - rd["kept_fraction"]) < 1e-10
+        compare(rm, dm, ops)
+    assert any(u["backend"] == "rrsvd" for u in dd.updates)

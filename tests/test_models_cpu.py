@@ -45,3 +45,28 @@ def test_trotter_plan():
     assert plan == [(1, 0.5), (0, 1.0), (1, 0.5)]
     with pytest.raises(ValueError):
         M.trotter_plan_3rd(0.0)
+
+
+def test_liouvillian_mpdo_terms(ref):
+    """The MPDO mapping (models.liouville_term): exp(-i dt L) vec(rho) = vec(U rho U^H) in the
+    (ket, bra) site ordering, L Hermitian, and the reference's own bond_gate (zheevd,
+    tebd.cpp:239-258) of L equals U (x) U* arranged on the doubled sites."""
+    from scipy.linalg import expm
+    rng = np.random.default_rng(5)
+    d1, d2 = 2, 3
+    a = rng.standard_normal((6, 6)) + 1j * rng.standard_normal((6, 6))
+    h = a + a.conj().T
+    L = M.liouville_term(h, d1, d2)
+    assert np.max(np.abs(L - L.conj().T)) == 0.0
+    psi = rng.standard_normal(6) + 1j * rng.standard_normal(6)
+    psi /= np.linalg.norm(psi)
+    u = expm(-0.3j * h)
+    rho_t = u @ np.outer(psi, psi.conj()) @ u.conj().T
+
+    def vec(r):  # rho[(k1 k2), (b1 b2)] -> (k1 b1 k2 b2)
+        return r.reshape(d1, d2, d1, d2).transpose(0, 2, 1, 3).reshape(-1)
+    assert np.max(np.abs(expm(-0.3j * L) @ vec(np.outer(psi, psi.conj())) - vec(rho_t))) < 1e-13
+    g_ref = ref.bond_gate(L, 0.3)
+    assert np.max(np.abs(g_ref - expm(-0.3j * L))) < 1e-12
+    # the local product state of the MPDO
+    assert np.allclose(M.mpdo_local(np.array([0.6, 0.8j])), np.kron([0.6, 0.8j], np.conj([0.6, 0.8j])))
