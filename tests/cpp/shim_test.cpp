@@ -5,6 +5,7 @@
 #include <cstdio>
 #include <numbers>
 
+#include "rrsvd_b200/partition.hpp"
 #include "rrsvd_b200/rrsvd.hpp"
 
 using namespace rrsvd;
@@ -94,6 +95,32 @@ int main() {
         for (std::size_t i = 0; i < 4; ++i)
             for (std::size_t j = 0; j < 4; ++j) e += std::norm(u(i, j) - (i == j ? 1.0 : 0.0));
         CHECK(std::sqrt(e) < 1e-12);
+    }
+    {  // the partition through the C++ drop-in: one rank (loopback) == the single-GPU evolve
+        std::vector<HamiltonianTerm> terms;
+        DenseMatrix h(4, 4);
+        h(0, 0) = 1; h(3, 3) = 1; h(1, 1) = -1; h(2, 2) = -1; h(1, 2) = 2; h(2, 1) = 2;
+        for (std::size_t b = 0; b < 5; ++b) terms.push_back({b, h});
+        MpsState a = mps_product_state({2, 2, 2, 2, 2, 2}, {up, down, up, down, up, down}, 8, 0.0);
+        MpsState bl = a;
+        DecimationBackend b1, b2;
+        b1.kind = b2.kind = DecimationBackend::Kind::Randomized;
+        b1.target_rank = b2.target_rank = 8; b1.oversampling = b2.oversampling = 4;
+        b1.det_crossover = b2.det_crossover = 0; b1.seed = b2.seed = 13;
+        evolve(a, terms, trotter_plan_3rd(0.05), 4, b1);
+        rrsvd_b200_loopback_hub* hub = nullptr;
+        rrsvd_b200_comm* comm = nullptr;
+        CHECK(rrsvd_b200_loopback_hub_create(1, &hub) == 0);
+        CHECK(rrsvd_b200_comm_create_loopback(rrsvd::b200::context(), hub, 0, &comm) == 0);
+        tebd::b200ext::evolve_partitioned(bl, comm, 0, 6, terms, trotter_plan_3rd(0.05), 4, b2);
+        CHECK(b1.seed == b2.seed);
+        for (std::size_t k = 0; k < 5; ++k) {
+            CHECK(a.lambdas[k].size() == bl.lambdas[k].size());
+            for (std::size_t i = 0; i < std::min(a.lambdas[k].size(), bl.lambdas[k].size()); ++i)
+                CHECK(std::abs(a.lambdas[k][i] - bl.lambdas[k][i]) < 1e-12);
+        }
+        rrsvd_b200_comm_destroy(comm);
+        rrsvd_b200_loopback_hub_destroy(hub);
     }
     std::printf("%s (%d failures)\n", failures ? "FAILED" : "shim_test passed", failures);
     return failures ? 1 : 0;
