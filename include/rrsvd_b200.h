@@ -89,6 +89,13 @@ uint64_t rrsvd_b200_launch_count(const rrsvd_b200_ctx* ctx);
 int rrsvd_b200_zgemm(rrsvd_b200_ctx* ctx, int op_a, int op_b, size_t m, size_t n, size_t k,
                      const double* A, size_t lda, const double* B, size_t ldb, double* C,
                      size_t ldc);
+/* The same product (op_b = N) through the INT8 tensor-core emulation of the RRSVD A-products
+ * (csrc/ozaki.cuh: Chinese-remainder / Ozaki-II scheme, `moduli` in [8, 16] residue moduli;
+ * 16 = FP64-class normwise accuracy).  Diagnostic entry for the parity tests and benchmarks of
+ * that path; needs m, k in [128, 32768]. */
+int rrsvd_b200_ozaki_zgemm(rrsvd_b200_ctx* ctx, int op_a, size_t m, size_t n, size_t k,
+                           const double* A, size_t lda, const double* B, size_t ldb, double* C,
+                           size_t ldc, int moduli);
 /* Thin orthonormal basis Q (m x n, m >= n) of A plus R = Q^H A (n x n), A = Q R; replaces
  * rrsvd::qr (linalg.cpp:49-65).  Like the reference's Householder QR, Q is orthonormal for ANY
  * A (linalg.hpp:35-37): columns of a rank-deficient A that CholeskyQR finds dependent get an

@@ -73,6 +73,22 @@ def gemm(a, adj_a: bool, b, adj_b: bool = False, ctx=None):
     return out
 
 
+def ozaki_gemm(a, adj_a: bool, b, moduli: int = 16, ctx=None):
+    """op(a) @ b through the INT8 tensor-core emulation of the RRSVD A-products (csrc/ozaki.cuh,
+    the Chinese-remainder scheme with `moduli` residue moduli; 16 = FP64-class accuracy)."""
+    c = _ctx(ctx)
+    a, b = _prep(a), _prep(b)
+    ar, ac = _shape(a)
+    br, bc = _shape(b)
+    m, k = (ac, ar) if adj_a else (ar, ac)
+    if k != br:
+        raise ContractViolation("ozaki_gemm: inner dimension mismatch")
+    out = _empty(a, (m, bc), np.complex128)
+    c.check(L.lib().rrsvd_b200_ozaki_zgemm(c.h, int(adj_a), sz(m), sz(bc), sz(k), ptr(a), sz(ac), ptr(b), sz(bc),
+                                           ptr(out), sz(bc), int(moduli)))
+    return out
+
+
 def matmul(a, b, ctx=None):
     return gemm(a, False, b, False, ctx)
 

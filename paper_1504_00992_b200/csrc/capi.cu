@@ -6,6 +6,7 @@
 #include <vector>
 
 #include "../../include/rrsvd_b200.h"
+#include "ozaki.cuh"
 #include "pipeline.cuh"
 
 using namespace rb;
@@ -200,6 +201,27 @@ int rrsvd_b200_zgemm(rrsvd_b200_ctx* c, int op_a, int op_b, size_t m, size_t n, 
             gemm(c, op_a == RRSVD_B200_OP_N ? kOpN : kOpC, (int)m, (int)n, (int)k, dA, (long long)lda, dB,
                  (long long)ldb, dC, (long long)ldc);
         }
+        finish_out(c, outs);
+    });
+}
+
+int rrsvd_b200_ozaki_zgemm(rrsvd_b200_ctx* c, int op_a, size_t m, size_t n, size_t k, const double* A, size_t lda,
+                           const double* B, size_t ldb, double* C, size_t ldc, int moduli) {
+    return api(c, [&] {
+        if (op_a != RRSVD_B200_OP_N && op_a != RRSVD_B200_OP_C) throw_contract(c, "ozaki_zgemm: bad op_a");
+        if (moduli < 8 || moduli > kOzMaxMod) throw_contract(c, "ozaki_zgemm: moduli must be in [8, 16]");
+        if (m == 0 || n == 0) return;
+        if (m < 128 || k < 128 || std::max(m, k) > 32768)
+            throw_contract(c, "ozaki_zgemm: needs m, k >= 128 and m, k <= 32768");
+        const bool opn = op_a == RRSVD_B200_OP_N;
+        const size_t a_rows = opn ? m : k, a_cols = opn ? k : m;
+        if (lda < a_cols || ldb < n || ldc < n) throw_contract(c, "ozaki_zgemm: leading dimension too small");
+        std::vector<OutBuf> outs;
+        const auto* dA = static_cast<const cplx*>(stage_in(c, A, a_rows * lda * sizeof(cplx)));
+        const auto* dB = static_cast<const cplx*>(stage_in(c, B, k * ldb * sizeof(cplx)));
+        auto* dC = static_cast<cplx*>(stage_out(c, C, m * ldc * sizeof(cplx), outs));
+        std::vector<OzakiA> oa = ozaki_prepare_many(c, {OzSrc{dA, (int)a_rows, (int)a_cols, (long long)lda}}, moduli);
+        ozaki_product_many(c, opn ? kOpN : kOpC, {OzProduct{&oa[0], dB, (long long)ldb, (int)n, dC, (long long)ldc}});
         finish_out(c, outs);
     });
 }

@@ -1,0 +1,66 @@
+// ozaki.cuh — the RRSVD A-products (Y = A·X, Z = A^H·X; randomized.cpp:88-99, 57-66 through
+// linalg.cpp:20-40) as exact integer products on the INT8 tensor cores (tcgen05.mma kind::i8),
+// the Chinese-remainder ("Ozaki scheme II") emulation of the complex-FP64 GEMM.
+//
+// A is scaled by one power of two 2^sA (from max|Re A|, |Im A|) and rounded to integers A' with
+// |A'| <= 2^kA; each column j of X by 2^sX_j to |X'| <= 2^kX.  The complex product is one real
+// integer GEMM with the real and imaginary parts stacked along K:
+//   op N: [Y'_re | Y'_im] = [A'_re  A'_im] · [[X'_re, X'_im], [-X'_im, X'_re]]
+//   op C: [Z'_re | Z'_im] = [A'_re  A'_im]^T · [[X'_re, X'_im], [X'_im, -X'_re]]
+// (every entry an exact integer, |D| <= 2K·2^(kA+kX) < M/2), computed modulo T pairwise coprime
+// moduli m_t <= 256 (M = prod m_t ~ 2^125 for T = 16): signed 8-bit residues, int32 accumulators
+// in TMEM (no overflow for K <= 32768), and reconstructed exactly by the CRT,
+//   D/M = frac_sym( sum_t ((D mod m_t)·w_t mod m_t) / m_t ),  w_t = (M/m_t)^-1 mod m_t,
+// evaluated in 128-bit fixed point, then D·2^-(sA+sX_j) rounded once to FP64.  The only
+// approximation is the rounding of A and X to kA / kX bits (kA + kX = log2 M - 2 - log2 2K: for
+// T = 16 and K = 2000, 56 + 55 bits — at or beyond FP64's 53-bit mantissa for every entry within
+// 2^3 of the matrix's largest), so the result carries FP64-GEMM-class normwise error.
+//
+// A's residue planes are built once per decimation and serve all 2 + 2q products of the range
+// finder and the basis assembly (op N reads them K-major, op C MN-major: no transposed copy).
+#pragma once
+#include <cstdint>
+#include <vector>
+
+#include "ctx.cuh"
+#include "zgemm.cuh"
+
+namespace rb {
+
+constexpr int kOzMaxMod = 16;
+
+// Residue planes of one A (m x n, row-major): int8 [T][2 (re, im)][m][pitch].
+struct OzakiA {
+    int8_t* res = nullptr;
+    int m = 0, n = 0;
+    long long pitch = 0;                 // bytes per row (n rounded up to 16)
+    int T = 0, kA = 0;
+    unsigned long long* amax = nullptr;  // device: bit pattern of max(|Re|, |Im|)
+    int* bad = nullptr;                  // device: a non-finite entry was seen
+};
+
+// Moduli count for the emulated A-products: RRSVD_B200_OZAKI (0 = off, the DMMA zgemm;
+// 8..16), default 0.  ozaki_usable: the shape gate of the RRSVD paths.
+int ozaki_moduli();
+bool ozaki_usable(int m, int n, int l);
+
+struct OzSrc {
+    const cplx* A;
+    int m, n;
+    long long lda;
+};
+// Builds the residue planes of every A (two launches for the whole batch).
+std::vector<OzakiA> ozaki_prepare_many(rrsvd_b200_ctx* c, const std::vector<OzSrc>& src, int T);
+
+// C = op(A)·X: op N — A m x n, X n x l (ld ldx), C m x l; op C — X m x l, C n x l.
+struct OzProduct {
+    const OzakiA* a;
+    const cplx* X;
+    long long ldx;
+    int l;
+    cplx* C;
+    long long ldc;
+};
+void ozaki_product_many(rrsvd_b200_ctx* c, GemmOp op, const std::vector<OzProduct>& ps);
+
+}  // namespace rb

@@ -1,0 +1,88 @@
+"""The INT8 tensor-core (tcgen05 kind::i8) Chinese-remainder emulation of the RRSVD A-products
+(csrc/ozaki.cuh) against numpy's complex128 product — the reference's cblas_zgemm call site
+(linalg.cpp:20-40) as used by randomized.cpp:88-99 (Y = A·Ω, Z = Aᴴ·Q) and 57-66 (Bᴴ = Aᴴ·Q)."""
+import numpy as np
+import pytest
+
+from tests.conftest import cplx_randn
+
+pytestmark = pytest.mark.gpu
+
+
+def _err(got, want, a, b):
+    """max-entry error over the operand scale max|A|·||B[:, j]||_1 (the integer scheme's bound)."""
+    amax = np.max(np.maximum(np.abs(a.real), np.abs(a.imag)))
+    col = np.sum(np.abs(b), axis=0)
+    return float(np.max(np.abs(got - want) / (amax * col[None, :] + 1e-300)))
+
+
+SHAPES = [(2000, 110, 2000), (300, 40, 257), (1000, 210, 700), (129, 8, 4000), (700, 128, 130)]
+
+
+@pytest.mark.parametrize("m,n,k", SHAPES)
+@pytest.mark.parametrize("adj", [False, True])
+def test_ozaki_matches_zgemm(ctx, m, n, k, adj):
+    import paper_1504_00992_b200 as P
+    rng = np.random.default_rng(m + 7 * n + 13 * k + adj)
+    a = cplx_randn(rng, *((k, m) if adj else (m, k)))
+    b = cplx_randn(rng, k, n)
+    want = (a.conj().T if adj else a) @ b
+    got = P.ozaki_gemm(a, adj, b, 16, ctx=ctx)
+    e = _err(got, want, a, b)
+    print(f"\nozaki16 {m}x{n}x{k} adj={adj}: err {e:.2e}")
+    # 16 moduli: kA + kX = 125 - 2 - log2(2k) >= 107 bits -> per-entry rounding <= 2^-53 of the scale
+    assert e <= 1e-15
+    dm = P.gemm(a, adj, b, ctx=ctx)
+    assert np.max(np.abs(got - dm)) <= 1e-13 * np.sqrt(k) * np.max(np.abs(want))
+
+
+@pytest.mark.parametrize("moduli,bar", [(14, 1e-13), (12, 1e-10)])
+def test_ozaki_fewer_moduli(ctx, moduli, bar):
+    import paper_1504_00992_b200 as P
+    rng = np.random.default_rng(moduli)
+    a = cplx_randn(rng, 1000, 1000)
+    b = cplx_randn(rng, 1000, 64)
+    got = P.ozaki_gemm(a, False, b, moduli, ctx=ctx)
+    e = _err(got, a @ b, a, b)
+    print(f"\nozaki{moduli}: err {e:.2e}")
+    assert e <= bar
+
+
+def test_ozaki_graded_rows_and_columns(ctx):
+    """A TEBD Θ has rows spanning many decades (λ-weighted); columns of X are scaled apart."""
+    import paper_1504_00992_b200 as P
+    rng = np.random.default_rng(5)
+    a = cplx_randn(rng, 800, 600) * np.exp(-np.arange(800) / 40.0)[:, None]
+    b = cplx_randn(rng, 600, 50) * (10.0 ** rng.uniform(-30, 30, 50))[None, :]
+    for adj in (False, True):
+        aa = a if not adj else a.conj().T.copy()
+        want = a @ b
+        got = P.ozaki_gemm(aa, adj, b, 16, ctx=ctx)
+        assert _err(got, want, a, b) <= 1e-15
+
+
+def test_ozaki_nonfinite_and_zero(ctx):
+    import paper_1504_00992_b200 as P
+    rng = np.random.default_rng(9)
+    a = cplx_randn(rng, 256, 256)
+    b = cplx_randn(rng, 256, 20)
+    z = P.ozaki_gemm(np.zeros_like(a), False, b, 16, ctx=ctx)
+    assert np.all(z == 0)
+    a[3, 7] = np.nan
+    got = P.ozaki_gemm(a, False, b, 16, ctx=ctx)
+    assert np.all(np.isnan(got))
+    b2 = b.copy()
+    b2[5, 4] = np.inf
+    got = P.ozaki_gemm(np.nan_to_num(a), False, b2, 16, ctx=ctx)
+    assert np.all(np.isnan(got[:, 4])) and np.all(np.isfinite(np.delete(got, 4, axis=1)))
+
+
+def test_ozaki_device_tensors(ctx):
+    import torch
+    import paper_1504_00992_b200 as P
+    g = torch.Generator(device="cuda").manual_seed(3)
+    a = torch.randn(2000, 2000, dtype=torch.complex128, device="cuda", generator=g)
+    b = torch.randn(2000, 110, dtype=torch.complex128, device="cuda", generator=g)
+    got = P.ozaki_gemm(a, False, b, 16, ctx=ctx)
+    want = a @ b
+    assert torch.max(torch.abs(got - want)).item() <= 1e-12
