@@ -4,7 +4,7 @@
 //                 one issuing thread -> two 128 x N' int32 accumulators in TMEM -> epilogue
 //                 reducing each accumulator mod m_t (times w_t) to a uint8 residue plane,
 //   oz_crt      — 128-bit fixed-point CRT of the T residues, scaled to FP64;
-// plus, once per A, oz_amax and oz_resid_a (its residue planes).
+// plus, once per A, oz_rowmax, oz_colmax and oz_resid_a (its equilibrated residue planes).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -27,9 +27,10 @@ struct OzConst {
     int T;
     int bits;                      // floor(log2 M)
     int mod[kOzMaxMod], w[kOzMaxMod], lo[kOzMaxMod];
-    float inv_m[kOzMaxMod];
     double inv_md[kOzMaxMod];
-    unsigned long long c_lo[kOzMaxMod], c_hi[kOzMaxMod];  // floor(2^128 / m_t)
+    unsigned magic[kOzMaxMod];     // ceil(2^32 / m): Barrett quotient (off by at most +1)
+    unsigned off[kOzMaxMod];       // m·ceil(2^31 / m) >= 2^31: makes an int32 non-negative mod m
+    unsigned c3[kOzMaxMod][3];     // floor(2^128 / m) >> 32, as three 32-bit limbs (low first)
     double mscale;                 // M / 2^128
 };
 
@@ -54,11 +55,13 @@ const OzConst& oz_const(int T) {
         k.mod[t] = m;
         k.w[t] = w;
         k.lo[t] = -(m / 2);  // symmetric residues in [-(m/2), m - 1 - m/2]
-        k.inv_m[t] = 1.0f / (float)m;
         k.inv_md[t] = 1.0 / (double)m;
+        k.magic[t] = (unsigned)(((1ull << 32) + m - 1) / m);
+        k.off[t] = (unsigned)(m * (((1ull << 31) + m - 1) / m));
         const unsigned __int128 c = (~(unsigned __int128)0) / (unsigned __int128)m;
-        k.c_lo[t] = (unsigned long long)c;
-        k.c_hi[t] = (unsigned long long)(c >> 64);
+        k.c3[t][0] = (unsigned)(c >> 32);
+        k.c3[t][1] = (unsigned)(c >> 64);
+        k.c3[t][2] = (unsigned)(c >> 96);
     }
     k.mscale = std::ldexp((double)(unsigned long long)(M >> 64), -64) + std::ldexp((double)(unsigned long long)M, -128);
     tab[T] = k;
@@ -74,54 +77,94 @@ int ceil_log2(long long v) {
 // kA + kX for an inner dimension K: 2K·2^(kA+kX) < 2^(bits-1) <= M/2, one bit of margin
 int oz_total_bits(const OzConst& k, int K) { return k.bits - 2 - ceil_log2(2ll * K); }
 
-__device__ __forceinline__ int oz_exp(unsigned long long bits, int k) {
+// e with v in [2^(e-1), 2^e) for the non-negative double of bit pattern `bits` (0 -> 0)
+__device__ __forceinline__ int oz_e(unsigned long long bits) {
     if (bits == 0) return 0;
+    const int f = (int)(bits >> 52);
+    if (f != 0) return f - 1022;
     int e;
-    frexp(__longlong_as_double((long long)bits), &e);  // max in [2^(e-1), 2^e)
-    return k - e;
+    frexp(__longlong_as_double((long long)bits), &e);
+    return e;
 }
-__device__ __forceinline__ double oz_scale(double x, int s) {  // x·2^s without overflow of 2^s
-    return x * exp2((double)(s / 2)) * exp2((double)(s - s / 2));
+__device__ __forceinline__ double oz_pow2(int e) {  // 2^e for e in [-1022, 1023]
+    return __longlong_as_double((long long)(e + 1023) << 52);
 }
-// residue of an integer-valued double v (|v| <= 2^57) in [lo, lo + m)
+__device__ __forceinline__ double oz_scale(double x, int s) {  // x·2^s, |s| <= 2044
+    const int h = s / 2;
+    return x * oz_pow2(h) * oz_pow2(s - h);
+}
+// residue of an integer-valued double v (|v| <= 2^57) in [lo, lo + m): FP64 only, no conversion
+// instruction (the 1.5·2^52 shifter rounds to an integer and exposes it in the low word)
 __device__ __forceinline__ int oz_res(double v, int m, double inv_m, int lo) {
-    const double q = rint(v * inv_m);
-    int r = (int)fma(-q, (double)m, v);
-    if (r < lo) r += m;
-    if (r >= lo + m) r -= m;
-    return r;
+    const double sh = 6755399441055744.0;
+    const double q = fma(v, inv_m, sh) - sh;
+    const double r = fma(-q, (double)m, v);
+    int ri = __double2loint(r + sh);
+    if (ri < lo) ri += m;
+    if (ri >= lo + m) ri -= m;
+    return ri;
 }
 
-// ---- A: max and residue planes -----------------------------------------------------------
+// ---- A: row / column maxima and residue planes ----------------------------------------------
+// A' = rint(A_ik · 2^(kA - e_i - f_k)): e_i the exponent of row i's max, f_k that of column k's max
+// after the rows are normalised (<= 0).  Every entry of A' is within 2^kA and carries kA bits
+// relative to its own row and column scale — a TEBD Θ (λ-weighted on both sides) loses nothing
+// to a global scale.
 constexpr int kPrepGroup = 48;
 struct PrepParams {
     const cplx* A[kPrepGroup];
     long long lda[kPrepGroup], pitch[kPrepGroup];
     int m[kPrepGroup], n[kPrepGroup], kA[kPrepGroup];
     int8_t* res[kPrepGroup];
-    unsigned long long* amax;  // [count]
-    int* bad;                  // [count]
+    unsigned long long* rowbits[kPrepGroup];  // [m]
+    unsigned long long* colbits[kPrepGroup];  // [n] (zeroed)
+    int* bad;                                 // [count] (zeroed)
     int count;
     OzConst k;
 };
 
-__global__ void __launch_bounds__(256) oz_amax_kernel(const __grid_constant__ PrepParams P) {
+__global__ void __launch_bounds__(256) oz_rowmax_kernel(const __grid_constant__ PrepParams P) {
     const int z = blockIdx.y;
     const int m = P.m[z], n = P.n[z];
-    const cplx* A = P.A[z];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int row = blockIdx.x * 8 + warp;
+    if (row >= m) return;
+    const cplx* A = P.A[z] + (long long)row * P.lda[z];
     double mx = 0.0;
     int bad = 0;
-    for (int r = blockIdx.x; r < m; r += gridDim.x)
-        for (int c = threadIdx.x; c < n; c += blockDim.x) {
-            const cplx v = A[(long long)r * P.lda[z] + c];
-            if (!isfinite(v.x) || !isfinite(v.y)) bad = 1;
-            else mx = fmax(mx, fmax(fabs(v.x), fabs(v.y)));
-        }
+    for (int c = lane; c < n; c += 32) {
+        const cplx v = A[c];
+        if (!isfinite(v.x) || !isfinite(v.y)) bad = 1;
+        else mx = fmax(mx, fmax(fabs(v.x), fabs(v.y)));
+    }
     mx = warp_max(mx);
     bad = __any_sync(0xffffffffu, bad);
-    if ((threadIdx.x & 31) == 0) {
-        if (mx > 0.0) atomicMax(&P.amax[z], (unsigned long long)__double_as_longlong(mx));
+    if (lane == 0) {
+        P.rowbits[z][row] = (unsigned long long)__double_as_longlong(mx);
         if (bad) atomicOr(&P.bad[z], 1);
+    }
+}
+
+// block = 32 columns x 8 row groups over a chunk of rows
+__global__ void __launch_bounds__(256) oz_colmax_kernel(const __grid_constant__ PrepParams P) {
+    const int z = blockIdx.z;
+    const int m = P.m[z], n = P.n[z];
+    const int col = blockIdx.x * 32 + (threadIdx.x & 31), g = threadIdx.x >> 5;
+    const int rows_per = (m + gridDim.y - 1) / gridDim.y;
+    const int r0 = blockIdx.y * rows_per, r1 = min(m, r0 + rows_per);
+    __shared__ double red[8][32];
+    double mx = 0.0;
+    if (col < n)
+        for (int r = r0 + g; r < r1; r += 8) {
+            const cplx v = P.A[z][(long long)r * P.lda[z] + col];
+            const double a = fmax(fabs(v.x), fabs(v.y));
+            if (isfinite(a) && a > 0.0) mx = fmax(mx, oz_scale(a, -oz_e(P.rowbits[z][r])));
+        }
+    red[g][threadIdx.x & 31] = mx;
+    __syncthreads();
+    if (g == 0 && col < n) {
+        for (int i = 1; i < 8; ++i) mx = fmax(mx, red[i][threadIdx.x]);
+        if (mx > 0.0) atomicMax(&P.colbits[z][col], (unsigned long long)__double_as_longlong(mx));
     }
 }
 
@@ -132,21 +175,25 @@ __global__ void __launch_bounds__(256) oz_resid_a_kernel(const __grid_constant__
     const long long pitch = P.pitch[z];
     const long long chunks_per_row = pitch / 16;
     const long long total = (long long)m * chunks_per_row;
-    const int sA = oz_exp(P.amax[z], P.kA[z]);
     const cplx* A = P.A[z];
     int8_t* res = P.res[z];
     const long long plane = (long long)m * pitch;
     for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (long long)gridDim.x * blockDim.x) {
         const int row = (int)(e / chunks_per_row);
         const int c0 = (int)(e % chunks_per_row) * 16;
+        const int er = P.kA[z] - oz_e(P.rowbits[z][row]);
         double vr[16], vi[16];
 #pragma unroll
         for (int u = 0; u < 16; ++u) {
             const int col = c0 + u;
             cplx x = mk(0.0, 0.0);
-            if (col < n) x = A[(long long)row * P.lda[z] + col];
-            vr[u] = rint(oz_scale(x.x, sA));
-            vi[u] = rint(oz_scale(x.y, sA));
+            int s = 0;
+            if (col < n) {
+                x = A[(long long)row * P.lda[z] + col];
+                s = er - oz_e(P.colbits[z][col]);
+            }
+            vr[u] = rint(oz_scale(x.x, s));
+            vi[u] = rint(oz_scale(x.y, s));
             if (!isfinite(vr[u])) vr[u] = 0.0;
             if (!isfinite(vi[u])) vi[u] = 0.0;
         }
@@ -172,7 +219,9 @@ __global__ void __launch_bounds__(256) oz_resid_a_kernel(const __grid_constant__
     }
 }
 
-// ---- X: per-column scale and the residue panel B' -------------------------------------------
+// ---- X: K-row compensation, per-column scale and the residue panel B' -------------------------
+// X'' = X·2^(f_k) (op N: A's column exponents) or Q·2^(e_i) (op C: A's row exponents) — the
+// inverse of A's equilibration along K — then each column j scaled by 2^(s_j) to kX bits.
 // B'[t][r][part][k] (r in [0, JT·2LT)): for output column j (tile jt = j / LT, jj = j % LT)
 //   row jt·2LT + jj      (real part of the output):  part 0 = X'_re,  part 1 =  sg·X'_im
 //   row jt·2LT + LT + jj (imaginary part):           part 0 = X'_im,  part 1 = -sg·X'_re
@@ -182,6 +231,7 @@ struct PanelParams {
     const cplx* X[kProdGroup];
     long long ldx[kProdGroup], pitchK[kProdGroup];
     int K[kProdGroup], l[kProdGroup], LT[kProdGroup], JT[kProdGroup], kX[kProdGroup];
+    const unsigned long long* kbits[kProdGroup];  // exponent source of the K rows
     int8_t* bres[kProdGroup];
     int* sx[kProdGroup];     // [JT·LT]
     int* xbad[kProdGroup];   // [JT·LT]
@@ -189,27 +239,29 @@ struct PanelParams {
     OzConst k;
 };
 
-__global__ void __launch_bounds__(256) oz_resid_b_kernel(const __grid_constant__ PanelParams P) {
+// block = 8 columns x 32 row groups: column maxima of X''
+__global__ void __launch_bounds__(256) oz_xmax_kernel(const __grid_constant__ PanelParams P) {
     const int z = blockIdx.y;
     const int LT = P.LT[z], JT = P.JT[z], K = P.K[z], l = P.l[z];
     const int j0 = blockIdx.x * 8;
     if (j0 >= JT * LT) return;
     const int tid = threadIdx.x, c = tid & 7, rg = tid >> 3;
     const int j = j0 + c;
-    const cplx* X = P.X[z];
-    const long long ldx = P.ldx[z];
     __shared__ double smax[32][8];
-    __shared__ int sbad[8], sexp[8];
-    __shared__ __align__(16) int8_t S[kOzMaxMod][8][2][128];
+    __shared__ int sbad[8];
     if (tid < 8) sbad[tid] = 0;
     __syncthreads();
     double mx = 0.0;
     int bad = 0;
     if (j < l)
         for (int k = rg; k < K; k += 32) {
-            const cplx v = X[(long long)k * ldx + j];
-            if (!isfinite(v.x) || !isfinite(v.y)) bad = 1;
-            else mx = fmax(mx, fmax(fabs(v.x), fabs(v.y)));
+            const cplx v = P.X[z][(long long)k * P.ldx[z] + j];
+            if (!isfinite(v.x) || !isfinite(v.y)) {
+                bad = 1;
+            } else {
+                const double a = fmax(fabs(v.x), fabs(v.y));
+                if (a > 0.0) mx = fmax(mx, oz_scale(a, oz_e(P.kbits[z][k])));
+            }
         }
     smax[rg][c] = mx;
     if (bad) atomicOr(&sbad[c], 1);
@@ -217,49 +269,58 @@ __global__ void __launch_bounds__(256) oz_resid_b_kernel(const __grid_constant__
     if (tid < 8) {
         double v = 0.0;
         for (int g = 0; g < 32; ++g) v = fmax(v, smax[g][tid]);
-        const int s = oz_exp((unsigned long long)__double_as_longlong(v), P.kX[z]);
-        sexp[tid] = s;
-        P.sx[z][j0 + tid] = s;
+        P.sx[z][j0 + tid] = v > 0.0 ? P.kX[z] - oz_e((unsigned long long)__double_as_longlong(v)) : 0;
         P.xbad[z][j0 + tid] = sbad[tid];
     }
+}
+
+// block = 8 columns x 128 K rows: residues into shared memory, then 128-byte rows of B'
+__global__ void __launch_bounds__(256) oz_resid_b_kernel(const __grid_constant__ PanelParams P) {
+    const int z = blockIdx.z;
+    const int LT = P.LT[z], JT = P.JT[z], K = P.K[z], l = P.l[z];
+    const int j0 = blockIdx.x * 8, k0 = blockIdx.y * 128;
+    if (j0 >= JT * LT || k0 >= K) return;
+    const int tid = threadIdx.x, c = tid & 7, rg = tid >> 3;
+    const int j = j0 + c;
+    __shared__ __align__(16) int8_t S[kOzMaxMod][8][2][128];
+    const int sxj = j < l ? P.sx[z][j] : 0;
+    const int T = P.k.T;
+    for (int u = 0; u < 4; ++u) {
+        const int kk = rg + 32 * u, k = k0 + kk;
+        cplx v = mk(0.0, 0.0);
+        int s = 0;
+        if (j < l && k < K) {
+            v = P.X[z][(long long)k * P.ldx[z] + j];
+            s = sxj + oz_e(P.kbits[z][k]);
+        }
+        double vr = rint(oz_scale(v.x, s)), vi = rint(oz_scale(v.y, s));
+        if (!isfinite(vr)) vr = 0.0;
+        if (!isfinite(vi)) vi = 0.0;
+        for (int t = 0; t < T; ++t) {
+            S[t][c][0][kk] = (int8_t)oz_res(vr, P.k.mod[t], P.k.inv_md[t], P.k.lo[t]);
+            S[t][c][1][kk] = (int8_t)oz_res(vi, P.k.mod[t], P.k.inv_md[t], P.k.lo[t]);
+        }
+    }
     __syncthreads();
-    const int s = sexp[c];
-    const int jt = j0 / LT, jj0 = j0 % LT;
     const long long pitchK = P.pitchK[z];
     const long long R = 2ll * JT * LT;
+    const int jt = j0 / LT, jj0 = j0 % LT;
     int8_t* bres = P.bres[z];
-    const int T = P.k.T;
-    for (int k0 = 0; k0 < K; k0 += 128) {
-        for (int u = 0; u < 4; ++u) {
-            const int kk = rg + 32 * u, k = k0 + kk;
-            cplx v = mk(0.0, 0.0);
-            if (j < l && k < K) v = X[(long long)k * ldx + j];
-            double vr = rint(oz_scale(v.x, s)), vi = rint(oz_scale(v.y, s));
-            if (!isfinite(vr)) vr = 0.0;
-            if (!isfinite(vi)) vi = 0.0;
-            for (int t = 0; t < T; ++t) {
-                S[t][c][0][kk] = (int8_t)oz_res(vr, P.k.mod[t], P.k.inv_md[t], P.k.lo[t]);
-                S[t][c][1][kk] = (int8_t)oz_res(vi, P.k.mod[t], P.k.inv_md[t], P.k.lo[t]);
-            }
+    // 16-byte pieces: (t, c, which, part, piece) — T·8·2·2·8 of them
+    const int pieces = T * 8 * 2 * 2 * 8;
+    for (int q = tid; q < pieces; q += 256) {
+        const int piece = q & 7, part = (q >> 3) & 1, which = (q >> 4) & 1, cc = (q >> 5) & 7, t = q >> 8;
+        const long long kofs = k0 + piece * 16;
+        if (kofs >= pitchK) continue;
+        // which 0 (re row): part0 = re, part1 = sg·im;  which 1 (im row): part0 = im, part1 = -sg·re
+        const int src = which == 0 ? (part == 0 ? 0 : 1) : (part == 0 ? 1 : 0);
+        const bool neg = part == 1 && ((which == 0) ? (P.sg < 0) : (P.sg > 0));
+        uint4 v = *reinterpret_cast<const uint4*>(&S[t][cc][src][piece * 16]);
+        if (neg) {
+            v.x = __vneg4(v.x); v.y = __vneg4(v.y); v.z = __vneg4(v.z); v.w = __vneg4(v.w);
         }
-        __syncthreads();
-        // 16-byte pieces: (t, c, which, part, piece) — T·8·2·2·8 of them
-        const int pieces = T * 8 * 2 * 2 * 8;
-        for (int q = tid; q < pieces; q += 256) {
-            const int piece = q & 7, part = (q >> 3) & 1, which = (q >> 4) & 1, cc = (q >> 5) & 7, t = q >> 8;
-            const long long kofs = k0 + piece * 16;
-            if (kofs >= pitchK) continue;
-            // which 0 (re row): part0 = re, part1 = sg·im;  which 1 (im row): part0 = im, part1 = -sg·re
-            const int src = which == 0 ? (part == 0 ? 0 : 1) : (part == 0 ? 1 : 0);
-            const bool neg = part == 1 && ((which == 0) ? (P.sg < 0) : (P.sg > 0));
-            uint4 v = *reinterpret_cast<const uint4*>(&S[t][cc][src][piece * 16]);
-            if (neg) {
-                v.x = __vneg4(v.x); v.y = __vneg4(v.y); v.z = __vneg4(v.z); v.w = __vneg4(v.w);
-            }
-            const long long r = (long long)jt * 2 * LT + which * LT + jj0 + cc;
-            *reinterpret_cast<uint4*>(bres + (((long long)t * R + r) * 2 + part) * pitchK + kofs) = v;
-        }
-        __syncthreads();
+        const long long r = (long long)jt * 2 * LT + which * LT + jj0 + cc;
+        *reinterpret_cast<uint4*>(bres + (((long long)t * R + r) * 2 + part) * pitchK + kofs) = v;
     }
 }
 
@@ -282,7 +343,7 @@ struct alignas(64) GemmParams {
     int count;
     int T;
     int mod[kOzMaxMod], w[kOzMaxMod];
-    float inv_m[kOzMaxMod];
+    unsigned magic[kOzMaxMod], off[kOzMaxMod];
 };
 static_assert(sizeof(GemmParams) <= 32764, "kernel parameter space");
 
@@ -439,7 +500,7 @@ __global__ void __launch_bounds__(256, 1) oz_gemm_kernel(const __grid_constant__
         const int q = warp & 3, h = warp >> 2;
         const int row = m0 + h * 128 + q * 32 + lane;
         const int md = P.mod[t], w = P.w[t];
-        const float inv = P.inv_m[t];
+        const unsigned mg = P.magic[t], off = P.off[t];
         uint8_t* dst = P.out[z] + (long long)t * P.out_plane[z] + (long long)row * P.out_ld[z] + jt * Nn;
         for (int ch = 0; ch < Nn / 16; ++ch) {
             uint32_t v[16];
@@ -447,12 +508,13 @@ __global__ void __launch_bounds__(256, 1) oz_gemm_kernel(const __grid_constant__
             uint32_t pk[4] = {0, 0, 0, 0};
 #pragma unroll
             for (int u = 0; u < 16; ++u) {
-                const int d = (int)v[u];
-                int r = d - (int)rintf((float)d * inv) * md;       // |r| <= m/2 + 129
-                const int p = r * w;                               // |p| < 2^16
-                int tt = p - (int)rintf((float)p * inv) * md;
-                if (tt < 0) tt += md;
-                if (tt >= md) tt -= md;
+                // t = (D mod m)·w mod m by two Barrett reductions (integer only): D + off >= 0
+                const unsigned x = v[u] + off;
+                int r = (int)(x - __umulhi(x, mg) * md);   // in [-m, m)
+                r += (r >> 31) & md;                        // [0, m)
+                const unsigned p = (unsigned)(r * w);       // < 2^16
+                int tt = (int)(p - __umulhi(p, mg) * md);
+                tt += (tt >> 31) & md;
                 pk[u >> 2] |= (uint32_t)tt << (8 * (u & 3));
             }
             if (row < M) *reinterpret_cast<uint4*>(dst + ch * 16) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
@@ -464,12 +526,14 @@ __global__ void __launch_bounds__(256, 1) oz_gemm_kernel(const __grid_constant__
 }
 
 // ---- CRT --------------------------------------------------------------------------------------
+// D/M = frac_sym( sum_t t_t / m_t ) in 128-bit fixed point, from the top 96 bits of floor(2^128/m_t)
+// (truncation error < T·2^8·2^32 units of 2^-128 — 2^-84 of M, far below one unit of kA + kX).
 struct CrtParams {
     const uint8_t* out[kProdGroup];
     long long out_plane[kProdGroup];
     int out_ld[kProdGroup];
     int M[kProdGroup], l[kProdGroup], LT[kProdGroup], kA[kProdGroup];
-    const unsigned long long* amax[kProdGroup];
+    const unsigned long long* obits[kProdGroup];  // exponent source of the output rows
     const int* abad[kProdGroup];
     const int* sx[kProdGroup];
     const int* xbad[kProdGroup];
@@ -478,40 +542,63 @@ struct CrtParams {
     OzConst k;
 };
 
-__device__ __forceinline__ double oz_crt_value(const uint8_t* p, long long plane, const OzConst& k) {
-    unsigned long long lo = 0, hi = 0;
+// the signed value D/M·2^128 of four consecutive outputs' residues (one uchar4 per modulus)
+__device__ __forceinline__ void oz_crt4(const uint8_t* p, long long plane, const OzConst& k, double (&val)[4]) {
+    unsigned long long a0[4] = {0, 0, 0, 0}, a1[4] = {0, 0, 0, 0}, a2[4] = {0, 0, 0, 0};
     for (int t = 0; t < k.T; ++t) {
-        const unsigned long long r = p[(long long)t * plane];
-        const unsigned long long a = r * k.c_lo[t];
-        const unsigned long long ah = __umul64hi(r, k.c_lo[t]) + r * k.c_hi[t];
-        lo += a;
-        hi += ah + (lo < a ? 1ull : 0ull);
+        const uint32_t b = *reinterpret_cast<const uint32_t*>(p + (long long)t * plane);
+        const unsigned c0 = k.c3[t][0], c1 = k.c3[t][1], c2 = k.c3[t][2];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const unsigned r = (b >> (8 * u)) & 0xffu;
+            a0[u] += (unsigned long long)r * c0;
+            a1[u] += (unsigned long long)r * c1;
+            a2[u] += (unsigned long long)r * c2;
+        }
     }
-    const bool neg = (long long)hi < 0;
-    if (neg) {
-        lo = ~lo + 1ull;
-        hi = ~hi + (lo == 0ull ? 1ull : 0ull);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        // F = a0·2^32 + a1·2^64 + a2·2^96 (mod 2^128)
+        unsigned long long lo = a0[u] << 32;
+        unsigned long long hi = (a0[u] >> 32) + a1[u] + (a2[u] << 32);
+        const bool neg = (long long)hi < 0;
+        if (neg) {
+            lo = ~lo + 1ull;
+            hi = ~hi + (lo == 0ull ? 1ull : 0ull);
+        }
+        const double mag = (double)hi * 18446744073709551616.0 + (double)lo;
+        val[u] = neg ? -mag : mag;
     }
-    const double mag = (double)hi * 18446744073709551616.0 + (double)lo;  // |D|/M · 2^128
-    return neg ? -mag : mag;
 }
 
+// one thread = four consecutive output columns of one row
 __global__ void __launch_bounds__(256) oz_crt_kernel(const __grid_constant__ CrtParams P) {
     const int z = blockIdx.y;
     const int M = P.M[z], l = P.l[z], LT = P.LT[z];
-    const long long total = (long long)M * l;
-    const int sA = oz_exp(*P.amax[z], P.kA[z]);
+    const int JT = (l + LT - 1) / LT;
+    const int groups = JT * (LT / 4);
+    const long long total = (long long)M * groups;
     const bool abad = *P.abad[z] != 0;
     for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (long long)gridDim.x * blockDim.x) {
-        const int row = (int)(e / l), j = (int)(e % l);
-        const int jt = j / LT, jj = j % LT;
+        const int row = (int)(e / groups), gi = (int)(e % groups);
+        const int jt = gi / (LT / 4), jj = (gi % (LT / 4)) * 4;
+        const int j0 = jt * LT + jj;
+        if (j0 >= l) continue;
         const uint8_t* base = P.out[z] + (long long)row * P.out_ld[z] + (long long)jt * 2 * LT + jj;
-        const double re = oz_crt_value(base, P.out_plane[z], P.k);
-        const double im = oz_crt_value(base + LT, P.out_plane[z], P.k);
-        const int sh = -(sA + P.sx[z][j]);
-        cplx v = mk(oz_scale(re * P.k.mscale, sh), oz_scale(im * P.k.mscale, sh));
-        if (abad || P.xbad[z][j]) v = mk(NAN, NAN);
-        P.C[z][(long long)row * P.ldc[z] + j] = v;
+        double re[4], im[4];
+        oz_crt4(base, P.out_plane[z], P.k, re);
+        oz_crt4(base + LT, P.out_plane[z], P.k, im);
+        const int eo = oz_e(P.obits[z][row]) - P.kA[z];
+        cplx* dst = P.C[z] + (long long)row * P.ldc[z] + j0;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int j = j0 + u;
+            if (j >= l || j >= (jt + 1) * LT) break;
+            const int sh = eo - P.sx[z][j];
+            cplx v = mk(oz_scale(re[u] * P.k.mscale, sh), oz_scale(im[u] * P.k.mscale, sh));
+            if (abad || P.xbad[z][j]) v = mk(NAN, NAN);
+            dst[u] = v;
+        }
     }
 }
 
@@ -554,6 +641,14 @@ int ozaki_moduli() {
     return T;
 }
 
+int ozaki_tail() {
+    static const int v = [] {
+        const char* e = std::getenv("RRSVD_B200_OZAKI_TAIL");
+        return e == nullptr ? 2 : std::max(0, std::atoi(e));
+    }();
+    return v;
+}
+
 bool ozaki_usable(int m, int n, int l) {
     return ozaki_moduli() > 0 && m >= 256 && n >= 256 && std::max(m, n) <= 32768 && l >= 1;
 }
@@ -566,12 +661,10 @@ std::vector<OzakiA> ozaki_prepare_many(rrsvd_b200_ctx* c, const std::vector<OzSr
         PrepParams P{};
         P.count = cnt;
         P.k = k;
-        P.amax = ws_get<unsigned long long>(c, cnt);
         P.bad = ws_get<int>(c, cnt);
-        check_cuda(c, cudaMemsetAsync(P.amax, 0, sizeof(unsigned long long) * cnt, c->stream), "ozaki memset");
         check_cuda(c, cudaMemsetAsync(P.bad, 0, sizeof(int) * cnt, c->stream), "ozaki memset");
         long long max_chunks = 0;
-        int max_m = 1;
+        int max_m = 1, max_n = 1;
         for (int i = 0; i < cnt; ++i) {
             const OzSrc& s = src[base + i];
             OzakiA& a = out[base + i];
@@ -581,7 +674,9 @@ std::vector<OzakiA> ozaki_prepare_many(rrsvd_b200_ctx* c, const std::vector<OzSr
             a.pitch = ((long long)s.n + 15) / 16 * 16;
             a.kA = std::min(56, (oz_total_bits(k, std::max(s.m, s.n)) + 1) / 2);
             a.res = ws_get<int8_t>(c, (size_t)T * 2 * s.m * a.pitch);
-            a.amax = P.amax + i;
+            a.rowbits = ws_get<unsigned long long>(c, s.m);
+            a.colbits = ws_get<unsigned long long>(c, s.n);
+            check_cuda(c, cudaMemsetAsync(a.colbits, 0, sizeof(unsigned long long) * s.n, c->stream), "ozaki memset");
             a.bad = P.bad + i;
             P.A[i] = s.A;
             P.lda[i] = s.lda;
@@ -590,11 +685,17 @@ std::vector<OzakiA> ozaki_prepare_many(rrsvd_b200_ctx* c, const std::vector<OzSr
             P.n[i] = s.n;
             P.kA[i] = a.kA;
             P.res[i] = a.res;
+            P.rowbits[i] = a.rowbits;
+            P.colbits[i] = a.colbits;
             max_chunks = std::max(max_chunks, (long long)s.m * a.pitch / 16);
             max_m = std::max(max_m, s.m);
+            max_n = std::max(max_n, s.n);
         }
-        oz_amax_kernel<<<dim3(std::min(max_m, 4 * kNumSMs), cnt), 256, 0, c->stream>>>(P);
-        check_launch(c, "oz_amax_kernel");
+        oz_rowmax_kernel<<<dim3((max_m + 7) / 8, cnt), 256, 0, c->stream>>>(P);
+        check_launch(c, "oz_rowmax_kernel");
+        const int rch = std::max(1, std::min(64, (4 * kNumSMs * 32) / (cnt * max_n)));  // row chunks: >= ~4 CTAs/SM
+        oz_colmax_kernel<<<dim3((max_n + 31) / 32, rch, cnt), 256, 0, c->stream>>>(P);
+        check_launch(c, "oz_colmax_kernel");
         const int gx = (int)std::min<long long>((max_chunks + 255) / 256, 8 * kNumSMs);
         oz_resid_a_kernel<<<dim3(gx, cnt), 256, 0, c->stream>>>(P);
         check_launch(c, "oz_resid_a_kernel");
@@ -628,9 +729,10 @@ void ozaki_product_many(rrsvd_b200_ctx* c, GemmOp op, const std::vector<OzProduc
         for (int t = 0; t < T; ++t) {
             G.mod[t] = k.mod[t];
             G.w[t] = k.w[t];
-            G.inv_m[t] = k.inv_m[t];
+            G.magic[t] = k.magic[t];
+            G.off[t] = k.off[t];
         }
-        int max_cols = 8, max_mb = 1, max_jt = 1;
+        int max_cols = 8, max_mb = 1, max_jt = 1, max_k = 1;
         long long max_el = 1;
         double flops = 0.0;
         for (int i = 0; i < cnt; ++i) {
@@ -655,6 +757,7 @@ void ozaki_product_many(rrsvd_b200_ctx* c, GemmOp op, const std::vector<OzProduc
             PP.LT[i] = LT;
             PP.JT[i] = JT;
             PP.kX[i] = kX;
+            PP.kbits[i] = op == kOpN ? a.colbits : a.rowbits;
             PP.bres[i] = bres;
             PP.sx[i] = sx;
             PP.xbad[i] = xbad;
@@ -684,7 +787,7 @@ void ozaki_product_many(rrsvd_b200_ctx* c, GemmOp op, const std::vector<OzProduc
             CP.l[i] = p.l;
             CP.LT[i] = LT;
             CP.kA[i] = a.kA;
-            CP.amax[i] = a.amax;
+            CP.obits[i] = op == kOpN ? a.rowbits : a.colbits;
             CP.abad[i] = a.bad;
             CP.sx[i] = sx;
             CP.xbad[i] = xbad;
@@ -693,7 +796,8 @@ void ozaki_product_many(rrsvd_b200_ctx* c, GemmOp op, const std::vector<OzProduc
             max_cols = std::max(max_cols, JT * LT);
             max_mb = std::max(max_mb, (Mr + kBM - 1) / kBM);
             max_jt = std::max(max_jt, JT);
-            max_el = std::max(max_el, (long long)Mr * p.l);
+            max_el = std::max(max_el, (long long)Mr * JT * (LT / 4));
+            max_k = std::max(max_k, K);
             flops += 8.0 * Mr * (double)p.l * K;
         }
         cudaEvent_t ea = nullptr, eb = nullptr;
@@ -702,7 +806,9 @@ void ozaki_product_many(rrsvd_b200_ctx* c, GemmOp op, const std::vector<OzProduc
             eb = pooled_event(c);
             check_cuda(c, cudaEventRecord(ea, c->stream), "event record");
         }
-        oz_resid_b_kernel<<<dim3((max_cols + 7) / 8, cnt), 256, 0, c->stream>>>(PP);
+        oz_xmax_kernel<<<dim3((max_cols + 7) / 8, cnt), 256, 0, c->stream>>>(PP);
+        check_launch(c, "oz_xmax_kernel");
+        oz_resid_b_kernel<<<dim3((max_cols + 7) / 8, (max_k + 127) / 128, cnt), 256, 0, c->stream>>>(PP);
         check_launch(c, "oz_resid_b_kernel");
         if (op == kOpN)
             oz_gemm_kernel<kOpN><<<dim3(max_mb, T * max_jt, cnt), 256, kGemmSmem, c->stream>>>(G);

@@ -2,8 +2,11 @@
 // linalg.cpp:20-40) as exact integer products on the INT8 tensor cores (tcgen05.mma kind::i8),
 // the Chinese-remainder ("Ozaki scheme II") emulation of the complex-FP64 GEMM.
 //
-// A is scaled by one power of two 2^sA (from max|Re A|, |Im A|) and rounded to integers A' with
-// |A'| <= 2^kA; each column j of X by 2^sX_j to |X'| <= 2^kX.  The complex product is one real
+// A is equilibrated by powers of two on both sides — A' = rint(A_ik·2^(kA - e_i - f_k)), e_i the
+// exponent of row i's largest entry, f_k that of column k's after the rows are normalised — so
+// every entry keeps kA bits relative to its own row and column scale (a TEBD Θ is λ-weighted on
+// both sides); the K-side factor is moved into X (X_kj·2^(f_k), resp. Q_ij·2^(e_i) for A^H), and
+// each column j of that is scaled by 2^(s_j) and rounded to |X'| <= 2^kX.  The complex product is one real
 // integer GEMM with the real and imaginary parts stacked along K:
 //   op N: [Y'_re | Y'_im] = [A'_re  A'_im] · [[X'_re, X'_im], [-X'_im, X'_re]]
 //   op C: [Z'_re | Z'_im] = [A'_re  A'_im]^T · [[X'_re, X'_im], [X'_im, -X'_re]]
@@ -35,14 +38,18 @@ struct OzakiA {
     int m = 0, n = 0;
     long long pitch = 0;                 // bytes per row (n rounded up to 16)
     int T = 0, kA = 0;
-    unsigned long long* amax = nullptr;  // device: bit pattern of max(|Re|, |Im|)
-    int* bad = nullptr;                  // device: a non-finite entry was seen
+    unsigned long long* rowbits = nullptr;  // device [m]: bit pattern of row i's max(|Re|, |Im|)
+    unsigned long long* colbits = nullptr;  // device [n]: column maxima after row normalisation
+    int* bad = nullptr;                     // device: a non-finite entry was seen
 };
 
 // Moduli count for the emulated A-products: RRSVD_B200_OZAKI (0 = off, the DMMA zgemm;
 // 8..16), default 0.  ozaki_usable: the shape gate of the RRSVD paths.
 int ozaki_moduli();
 bool ozaki_usable(int m, int n, int l);
+// RRSVD_B200_OZAKI_TAIL: how many of the RRSVD's last A-products stay on the FP64 zgemm — 1: the
+// assembly B^H = A^H Q; 2 (default): also the final Y = A Q~ of the power iteration; 0: none.
+int ozaki_tail();
 
 struct OzSrc {
     const cplx* A;

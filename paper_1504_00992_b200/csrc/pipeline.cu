@@ -603,6 +603,24 @@ void small_svd_many(rrsvd_b200_ctx* c, const std::vector<SmallSvdSpec>& specs) {
 
 // ================================================================================== RRSVD
 
+// The A-products of the RRSVD (tag 2): the DMMA zgemm, or — for specs carrying residue planes
+// (ozaki.cuh) — the INT8 tensor-core emulation.
+struct AProducts {
+    std::vector<GemmSpec> gs;
+    std::vector<OzProduct> oz;
+    void add(const OzakiA* a, const GemmSpec& s) {
+        if (a) oz.push_back({a, s.B, s.ldb, s.n, s.C, s.ldc});
+        else gs.push_back(s);
+    }
+    void run(rrsvd_b200_ctx* c, GemmOp op) {
+        c->gemm_tag = 2;
+        gemm_many(c, op, gs);
+        if (!oz.empty()) ozaki_product_many(c, op, oz);
+        gs.clear();
+        oz.clear();
+    }
+};
+
 void range_finder_many(rrsvd_b200_ctx* c, const std::vector<RangeSpec>& specs) {
     if (specs.empty()) return;
     struct Buf {
@@ -617,16 +635,15 @@ void range_finder_many(rrsvd_b200_ctx* c, const std::vector<RangeSpec>& specs) {
         b[i] = {ws_get<cplx>(c, (size_t)s.m * s.l), ws_get<cplx>(c, (size_t)s.n * s.l),
                 ws_get<cplx>(c, (size_t)s.n * s.l)};
     }
-    std::vector<GemmSpec> gs;
+    AProducts ap;
     std::vector<OrthSpec> os;
     // Algorithm 1 (randomized.cpp:88-99): Y = A Omega, QR
     for (size_t i = 0; i < specs.size(); ++i) {
         const RangeSpec& s = specs[i];
-        gs.push_back({s.m, s.l, s.n, s.A, s.n, s.omega, s.l, b[i].Y, s.l});
+        ap.add(s.oz, {s.m, s.l, s.n, s.A, s.n, s.omega, s.l, b[i].Y, s.l});
         os.push_back({b[i].Y, s.m, s.l, s.Q});
     }
-    c->gemm_tag = 2;
-    gemm_many(c, kOpN, gs);
+    ap.run(c, kOpN);
     // Only the last Q (the basis B = Q^H A is built on) must be orthonormal; the intermediate
     // bases of the power iteration carry just their span, so they stop after the two shifted
     // passes (cond <= ~1e5 even for rank-deficient input; one shifted pass is NOT enough: it
@@ -636,25 +653,25 @@ void range_finder_many(rrsvd_b200_ctx* c, const std::vector<RangeSpec>& specs) {
     const int inter = min_q == max_q ? kSpanPasses : kFullPasses;
     orth_many(c, os, max_q > 0 ? inter : kFullPasses);
     for (int j = 0; j < max_q; ++j) {
-        gs.clear(); os.clear();
+        os.clear();
         for (size_t i = 0; i < specs.size(); ++i) {  // Z = A^H Q, QR
             const RangeSpec& s = specs[i];
             if (j >= s.q) continue;
-            gs.push_back({s.n, s.l, s.m, s.A, s.n, s.Q, s.l, b[i].Z, s.l});
+            ap.add(s.oz, {s.n, s.l, s.m, s.A, s.n, s.Q, s.l, b[i].Z, s.l});
             os.push_back({b[i].Z, s.n, s.l, b[i].Qt});
         }
-        c->gemm_tag = 2;
-        gemm_many(c, kOpC, gs);
+        ap.run(c, kOpC);
         orth_many(c, os, inter);
-        gs.clear(); os.clear();
+        os.clear();
         for (size_t i = 0; i < specs.size(); ++i) {  // Y = A Q~, QR
             const RangeSpec& s = specs[i];
             if (j >= s.q) continue;
-            gs.push_back({s.m, s.l, s.n, s.A, s.n, b[i].Qt, s.l, b[i].Y, s.l});
+            // the last Y = A Q~ (the basis B is built on) stays on FP64 with the assembly product
+            // unless RRSVD_B200_OZAKI_TAIL < 2 (see rrsvd_core_many)
+            ap.add(j + 1 == s.q && ozaki_tail() >= 2 ? nullptr : s.oz, {s.m, s.l, s.n, s.A, s.n, b[i].Qt, s.l, b[i].Y, s.l});
             os.push_back({b[i].Y, s.m, s.l, s.Q});
         }
-        c->gemm_tag = 2;
-        gemm_many(c, kOpN, gs);
+        ap.run(c, kOpN);
         orth_many(c, os, j + 1 < max_q ? inter : kFullPasses);
     }
 }
@@ -674,15 +691,14 @@ void assemble_many(rrsvd_b200_ctx* c, const std::vector<AssembleSpec>& specs) {
     // B = Q^H A held as B^H = A^H Q = Qb X  (assemble_from_basis, randomized.cpp:57-66)
     std::vector<GemmSpec> gs;
     std::vector<OrthSpec> os;
+    AProducts ap;
     for (size_t i = 0; i < specs.size(); ++i) {
         const AssembleSpec& s = specs[i];
-        gs.push_back({s.n, s.l, s.m, s.A, s.n, s.Q, s.l, b[i].Z, s.l});
+        ap.add(s.oz, {s.n, s.l, s.m, s.A, s.n, s.Q, s.l, b[i].Z, s.l});
         os.push_back({b[i].Z, s.n, s.l, b[i].Qb});
     }
-    c->gemm_tag = 2;
-    gemm_many(c, kOpC, gs);
+    ap.run(c, kOpC);
     orth_many(c, os);
-    gs.clear();
     for (size_t i = 0; i < specs.size(); ++i) {  // X = Qb^H B^H  (l x l, ~upper triangular)
         const AssembleSpec& s = specs[i];
         gs.push_back({s.l, s.l, s.n, b[i].Qb, s.l, b[i].Z, s.l, b[i].X, s.l});
@@ -711,10 +727,29 @@ void rrsvd_core_many(rrsvd_b200_ctx* c, const std::vector<RrsvdSpec>& specs) {
     if (specs.empty()) return;
     std::vector<RangeSpec> rf;
     std::vector<AssembleSpec> as;
-    for (const RrsvdSpec& s : specs) {
+    // A's residue planes for the emulated A-products, built once for all 2 + 2q of them
+    std::vector<OzSrc> src;
+    std::vector<int> which;
+    const int T = ozaki_moduli();
+    for (size_t i = 0; i < specs.size(); ++i)
+        if (T > 0 && ozaki_usable(specs[i].m, specs[i].n, specs[i].l)) {
+            src.push_back({specs[i].A, specs[i].m, specs[i].n, (long long)specs[i].n});
+            which.push_back((int)i);
+        }
+    std::vector<OzakiA> oz;
+    if (!src.empty()) oz = ozaki_prepare_many(c, src, T);
+    std::vector<const OzakiA*> ozp(specs.size(), nullptr);
+    for (size_t j = 0; j < which.size(); ++j) ozp[which[j]] = &oz[j];
+    for (size_t i = 0; i < specs.size(); ++i) {
+        const RrsvdSpec& s = specs[i];
         cplx* Q = ws_get<cplx>(c, (size_t)s.m * s.l);
-        rf.push_back({s.A, s.m, s.n, s.l, s.q, s.omega, Q});
-        as.push_back({s.A, s.m, s.n, s.l, Q, s.U, s.sigma, s.V});
+        rf.push_back({s.A, s.m, s.n, s.l, s.q, s.omega, Q, ozp[i]});
+        // B^H = A^H Q stays on the FP64 zgemm: its rounding noise is what the numerically-zero
+        // cutoff (sigma <= 1e-15 sigma_1, tebd.cpp:193) sees in the directions of Q outside the
+        // range of a rank-deficient A — the DMMA product keeps it in the reference's rounding class
+        // (the emulated product is ~100x more accurate there and would cut chi below the
+        // reference's at exactly rank-deficient bonds).
+        as.push_back({s.A, s.m, s.n, s.l, Q, s.U, s.sigma, s.V, ozaki_tail() >= 1 ? nullptr : ozp[i]});
     }
     range_finder_many(c, rf);
     assemble_many(c, as);

@@ -7,6 +7,7 @@
 #include <vector>
 
 #include "blockjac.cuh"
+#include "ozaki.cuh"
 #include "ctx.cuh"
 #include "smallla.cuh"
 #include "tebd_kernels.cuh"
@@ -102,6 +103,7 @@ struct RangeSpec {
     int m, n, l, q;
     const cplx* omega;
     cplx* Q;
+    const OzakiA* oz = nullptr;  // A's residue planes: the A-products on the INT8 emulation
 };
 void range_finder_many(rrsvd_b200_ctx* c, const std::vector<RangeSpec>& specs);
 struct AssembleSpec {
@@ -111,6 +113,7 @@ struct AssembleSpec {
     cplx* U;
     double* sigma;
     cplx* V;
+    const OzakiA* oz = nullptr;
 };
 void assemble_many(rrsvd_b200_ctx* c, const std::vector<AssembleSpec>& specs);
 
