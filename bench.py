@@ -96,6 +96,27 @@ def workload(name: str):
     raise SystemExit(f"unknown workload {name}")
 
 
+def emulated_entry(flops, ms, nbytes, calls, prep_ms, prep_bytes) -> dict:
+    """The RRSVD A-products on the INT8 tensor cores (csrc/ozaki.cuh), from the serial roofline pass:
+    kept out of the DMMA roofline above (its `frac` covers the FP64 zgemm launches only)."""
+    moduli = int(os.environ.get("RRSVD_B200_OZAKI", "14") or 0)
+    if ms <= 0:
+        return {"enabled": False, "moduli": moduli}
+    return {"enabled": True, "moduli": moduli,
+            "scheme": "Chinese-remainder (Ozaki-II) emulation of the complex-FP64 product: A and the panel "
+                      "equilibrated by powers of two, int8 residues, tcgen05.mma kind::i8 into TMEM, 96-bit "
+                      "fixed-point CRT to FP64",
+            "products": "4 of the 2q+2 = 6 A-products per decimation (Y = A Omega and the power iteration); the "
+                        "final Y = A Q~ and B^H = A^H Q stay on the FP64 DMMA zgemm (RRSVD_B200_OZAKI_TAIL)",
+            "ms_per_step": round(ms, 3), "fp64_equivalent_tflops": round(flops / (ms * 1e-3) / 1e12, 2),
+            "algorithmic_GBps": round(nbytes / (ms * 1e-3) / 1e9, 1), "launch_groups": int(calls),
+            "a_preparation_ms_per_step": round(prep_ms, 3),
+            "a_preparation_GBps": round(prep_bytes / (prep_ms * 1e-3) / 1e9, 1) if prep_ms > 0 else None,
+            "note": "ms are event-timed per launch group (residue panel + INT8 GEMM + CRT) in the serial pass; "
+                    "fp64_equivalent_tflops counts 8 m n k per complex product; the INT8 GEMM kernel's own "
+                    "roofline (HBM-bound) is in profiles/r02_ozaki_summary.md"}
+
+
 def bench_config(wl, ups, world) -> dict:
     """The `config` object — identical in both arms (ours and --impl reference)."""
     from paper_1504_00992_b200 import models as M
@@ -429,6 +450,10 @@ def run_ours(args, rank, world, local_rank):
     ctx.check(lib.rrsvd_b200_gemm_pipe_stats(ctx.h, C.byref(exec_fl), C.byref(tma_ms)))
     sfl, sms = (C.c_double * 8)(), (C.c_double * 8)()
     ctx.check(lib.rrsvd_b200_gemm_stage_stats(ctx.h, sfl, sms))
+    ofl, oms, obytes, ocalls, opms, opbytes = (C.c_double(), C.c_double(), C.c_double(), C.c_uint64(), C.c_double(),
+                                               C.c_double())
+    ctx.check(lib.rrsvd_b200_ozaki_stats(ctx.h, C.byref(ofl), C.byref(oms), C.byref(obytes), C.byref(ocalls),
+                                         C.byref(opms), C.byref(opbytes)))
     ctx.check(lib.rrsvd_b200_set_gemm_timing(ctx.h, 0))
     ctx.check(lib.rrsvd_b200_set_overlap(ctx.h, 1))
     stage_names = ["theta", "gate", "rrsvd_A_products", "qr_gram", "qr_apply", "svd_assembly", "det_precond"]
@@ -499,7 +524,9 @@ def run_ours(args, rank, world, local_rank):
                          "gemm_time_share_serial": round(ms.value / (1e3 * serial_step_s), 4),
                          "serial_step_ms": round(1e3 * serial_step_s, 3),
                          "step_level_tflops": round(fl.value / (elapsed / args.steps) / 1e12, 3),
-                         "gemm_launches": int(calls.value), "stages": stages, **traffic_entry()},
+                         "gemm_launches": int(calls.value), "stages": stages, **traffic_entry(),
+                         "emulated_a_products": emulated_entry(ofl.value, oms.value, obytes.value, ocalls.value,
+                                                               opms.value, opbytes.value)},
             "e2e": {"value": round(e2e, 6), "unit": "steps/s", "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h), "steps": args.steps,
                     "note": "same consecutive steps as value; whole MPS H2D before and D2H after every step"},

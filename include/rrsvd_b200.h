@@ -333,9 +333,14 @@ int rrsvd_b200_gemm_stats(rrsvd_b200_ctx* ctx, double* flops, double* ms, uint64
 /* Of the same launches: the flops the DMMA pipe actually executed (6 real flops per complex MAC
  * for 3M-form launches, 8 for 4M) and the milliseconds spent in TMA-staged launches. */
 int rrsvd_b200_gemm_pipe_stats(rrsvd_b200_ctx* ctx, double* executed_flops, double* tma_ms);
-/* The same split by stage (8 slots): 0 theta, 1 gate, 2 RRSVD A-products, 3 QR Gram,
- * 4 QR apply, 5 small-SVD assembly, 6 deterministic-SVD preconditioning. */
+/* The same split by stage (8 slots): 0 theta, 1 gate, 2 RRSVD A-products (the DMMA ones), 3 QR
+ * Gram, 4 QR apply, 5 small-SVD assembly, 6 deterministic-SVD preconditioning. */
 int rrsvd_b200_gemm_stage_stats(rrsvd_b200_ctx* ctx, double* flops8, double* ms8);
+/* The emulated A-products (csrc/ozaki.cuh) timed under the same switch, kept out of the DMMA
+ * counters: FP64-equivalent flops (8 m n k), milliseconds, algorithmic HBM bytes and launch groups
+ * of the products; milliseconds and bytes of the A residue preparations. */
+int rrsvd_b200_ozaki_stats(rrsvd_b200_ctx* ctx, double* flops, double* ms, double* bytes, uint64_t* calls,
+                           double* prep_ms, double* prep_bytes);
 /* Measured device peak: what = 0 FP64 DMMA (mma.sync f64), 1 FP64 DFMA; TFLOP/s. */
 int rrsvd_b200_probe_peak(rrsvd_b200_ctx* ctx, int what, double* tflops);
 

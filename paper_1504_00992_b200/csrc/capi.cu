@@ -632,6 +632,8 @@ int rrsvd_b200_set_gemm_timing(rrsvd_b200_ctx* c, int on) {
             c->gemm_exec_flops = 0.0;
             c->gemm_tma_ms = 0.0;
             c->gemm_calls = 0;
+            c->oz_ms = c->oz_flops = c->oz_bytes = c->oz_prep_ms = c->oz_prep_bytes = 0.0;
+            c->oz_calls = 0;
             for (int i = 0; i < 8; ++i) c->tag_ms[i] = c->tag_flops[i] = 0.0;
         }
     });
@@ -651,6 +653,19 @@ int rrsvd_b200_gemm_pipe_stats(rrsvd_b200_ctx* c, double* executed_flops, double
         flush_gemm_timing(c);
         if (executed_flops) *executed_flops = c->gemm_exec_flops;
         if (tma_ms) *tma_ms = c->gemm_tma_ms;
+    });
+}
+
+int rrsvd_b200_ozaki_stats(rrsvd_b200_ctx* c, double* flops, double* ms, double* bytes, uint64_t* calls,
+                           double* prep_ms, double* prep_bytes) {
+    return api(c, [&] {
+        flush_gemm_timing(c);
+        if (flops) *flops = c->oz_flops;
+        if (ms) *ms = c->oz_ms;
+        if (bytes) *bytes = c->oz_bytes;
+        if (calls) *calls = c->oz_calls;
+        if (prep_ms) *prep_ms = c->oz_prep_ms;
+        if (prep_bytes) *prep_bytes = c->oz_prep_bytes;
     });
 }
 

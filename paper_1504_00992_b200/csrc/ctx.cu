@@ -156,6 +156,20 @@ void flush_gemm_timing(rrsvd_b200_ctx* c) {
         check_cuda(c, cudaEventSynchronize(p.b), "event sync");
         float ms = 0.f;
         check_cuda(c, cudaEventElapsedTime(&ms, p.a, p.b), "event elapsed");
+        c->event_pool.push_back(p.a);
+        c->event_pool.push_back(p.b);
+        if (p.kind == 1) {
+            if (p.flops > 0) {
+                c->oz_ms += ms;
+                c->oz_flops += p.flops;
+                c->oz_bytes += p.bytes;
+                c->oz_calls++;
+            } else {
+                c->oz_prep_ms += ms;
+                c->oz_prep_bytes += p.bytes;
+            }
+            continue;
+        }
         c->gemm_ms += ms;
         c->gemm_flops += p.flops;
         c->gemm_exec_flops += p.executed;
@@ -163,8 +177,6 @@ void flush_gemm_timing(rrsvd_b200_ctx* c) {
         c->tag_ms[p.tag & 7] += ms;
         c->tag_flops[p.tag & 7] += p.flops;
         c->gemm_calls++;
-        c->event_pool.push_back(p.a);
-        c->event_pool.push_back(p.b);
     }
     c->pending.clear();
 }

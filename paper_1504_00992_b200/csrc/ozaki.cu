@@ -21,6 +21,12 @@ namespace {
 
 constexpr int kModuli[kOzMaxMod] = {256, 255, 253, 251, 247, 241, 239, 233,
                                     229, 227, 223, 217, 211, 199, 197, 193};
+// the same table as a constant expression usable in device code
+__host__ __device__ constexpr int oz_modulus(int t) {
+    return t == 0 ? 256 : t == 1 ? 255 : t == 2 ? 253 : t == 3 ? 251 : t == 4 ? 247 : t == 5 ? 241 : t == 6 ? 239
+         : t == 7 ? 233 : t == 8 ? 229 : t == 9 ? 227 : t == 10 ? 223 : t == 11 ? 217 : t == 12 ? 211
+         : t == 13 ? 199 : t == 14 ? 197 : 193;
+}
 
 // Per-T constants of the residue arithmetic and the CRT.
 struct OzConst {
@@ -86,6 +92,13 @@ __device__ __forceinline__ int oz_e(unsigned long long bits) {
     frexp(__longlong_as_double((long long)bits), &e);
     return e;
 }
+constexpr int kExpNone = (int)0xC0C0C0C0;  // "no entry" (memset byte 0xC0): a zero row / column
+__device__ __forceinline__ int oz_exp_or0(int e) { return e == kExpNone ? 0 : e; }
+// exponent of max(|re|, |im|) (kExpNone for zero)
+__device__ __forceinline__ int oz_eabs(cplx v) {
+    const double a = fmax(fabs(v.x), fabs(v.y));
+    return a > 0.0 ? oz_e((unsigned long long)__double_as_longlong(a)) : kExpNone;
+}
 __device__ __forceinline__ double oz_pow2(int e) {  // 2^e for e in [-1022, 1023]
     return __longlong_as_double((long long)(e + 1023) << 52);
 }
@@ -113,108 +126,120 @@ __device__ __forceinline__ int oz_res(double v, int m, double inv_m, int lo) {
 constexpr int kPrepGroup = 48;
 struct PrepParams {
     const cplx* A[kPrepGroup];
-    long long lda[kPrepGroup], pitch[kPrepGroup];
+    long long lda[kPrepGroup];
+    int nib[kPrepGroup], nkb[kPrepGroup];
     int m[kPrepGroup], n[kPrepGroup], kA[kPrepGroup];
     int8_t* res[kPrepGroup];
-    unsigned long long* rowbits[kPrepGroup];  // [m]
-    unsigned long long* colbits[kPrepGroup];  // [n] (zeroed)
+    int* rowexp[kPrepGroup];  // [m]: exponent of the row's largest entry (0 for a zero row)
+    int* colexp[kPrepGroup];  // [n]: max_i e(|A_ik|) - rowexp_i (kExpNone-filled before the scan)
     int* bad;                                 // [count] (zeroed)
     int count;
     OzConst k;
 };
 
-__global__ void __launch_bounds__(256) oz_rowmax_kernel(const __grid_constant__ PrepParams P) {
+// Row exponents (a warp per row), then column exponents of the row-normalised A (each near the
+// HBM roofline; a one-pass form with shared-memory column atomics measured slower)
+__global__ void __launch_bounds__(256) oz_rowexp_kernel(const __grid_constant__ PrepParams P) {
     const int z = blockIdx.y;
     const int m = P.m[z], n = P.n[z];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int row = blockIdx.x * 8 + warp;
     if (row >= m) return;
     const cplx* A = P.A[z] + (long long)row * P.lda[z];
-    double mx = 0.0;
-    int bad = 0;
+    int er = kExpNone, bad = 0;
     for (int c = lane; c < n; c += 32) {
         const cplx v = A[c];
         if (!isfinite(v.x) || !isfinite(v.y)) bad = 1;
-        else mx = fmax(mx, fmax(fabs(v.x), fabs(v.y)));
+        else er = max(er, oz_eabs(v));
     }
-    mx = warp_max(mx);
+    for (int o = 16; o > 0; o >>= 1) er = max(er, __shfl_xor_sync(0xffffffffu, er, o));
     bad = __any_sync(0xffffffffu, bad);
     if (lane == 0) {
-        P.rowbits[z][row] = (unsigned long long)__double_as_longlong(mx);
+        P.rowexp[z][row] = oz_exp_or0(er);
         if (bad) atomicOr(&P.bad[z], 1);
     }
 }
-
-// block = 32 columns x 8 row groups over a chunk of rows
-__global__ void __launch_bounds__(256) oz_colmax_kernel(const __grid_constant__ PrepParams P) {
+__global__ void __launch_bounds__(256) oz_colexp_kernel(const __grid_constant__ PrepParams P) {
     const int z = blockIdx.z;
     const int m = P.m[z], n = P.n[z];
     const int col = blockIdx.x * 32 + (threadIdx.x & 31), g = threadIdx.x >> 5;
     const int rows_per = (m + gridDim.y - 1) / gridDim.y;
     const int r0 = blockIdx.y * rows_per, r1 = min(m, r0 + rows_per);
-    __shared__ double red[8][32];
-    double mx = 0.0;
+    __shared__ int red[8][32];
+    int mx = kExpNone;
     if (col < n)
         for (int r = r0 + g; r < r1; r += 8) {
             const cplx v = P.A[z][(long long)r * P.lda[z] + col];
-            const double a = fmax(fabs(v.x), fabs(v.y));
-            if (isfinite(a) && a > 0.0) mx = fmax(mx, oz_scale(a, -oz_e(P.rowbits[z][r])));
+            const int e = (isfinite(v.x) && isfinite(v.y)) ? oz_eabs(v) : kExpNone;
+            if (e != kExpNone) mx = max(mx, e - P.rowexp[z][r]);
         }
     red[g][threadIdx.x & 31] = mx;
     __syncthreads();
     if (g == 0 && col < n) {
-        for (int i = 1; i < 8; ++i) mx = fmax(mx, red[i][threadIdx.x]);
-        if (mx > 0.0) atomicMax(&P.colbits[z][col], (unsigned long long)__double_as_longlong(mx));
+        for (int i = 1; i < 8; ++i) mx = max(mx, red[i][threadIdx.x]);
+        if (mx != kExpNone) atomicMax(&P.colexp[z][col], mx);
     }
 }
 
-// one thread = 16 consecutive columns of one row, both parts, all T moduli
+// the residues of eight integer-valued (re, im) pairs mod m, packed into one 8-byte store per part
+__device__ __forceinline__ void oz_store8(const double (&vr)[8], const double (&vi)[8], int8_t* dst, long long plane,
+                                          int md, double im, int lo) {
+    uint32_t pr[2], pi[2];
+#pragma unroll
+    for (int w = 0; w < 2; ++w) {
+        uint32_t a = 0, b = 0;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            a |= (uint32_t)(oz_res(vr[4 * w + u], md, im, lo) & 0xff) << (8 * u);
+            b |= (uint32_t)(oz_res(vi[4 * w + u], md, im, lo) & 0xff) << (8 * u);
+        }
+        pr[w] = a;
+        pi[w] = b;
+    }
+    *reinterpret_cast<uint2*>(dst) = make_uint2(pr[0], pr[1]);
+    *reinterpret_cast<uint2*>(dst + plane) = make_uint2(pi[0], pi[1]);
+}
+
+// one thread = 8 consecutive columns of one (padded) row, both parts, all T moduli (TT > 0: the
+// moduli count as a compile-time constant, every modulus an immediate)
+template <int TT>
 __global__ void __launch_bounds__(256) oz_resid_a_kernel(const __grid_constant__ PrepParams P) {
     const int z = blockIdx.y;
-    const int m = P.m[z], n = P.n[z];
-    const long long pitch = P.pitch[z];
-    const long long chunks_per_row = pitch / 16;
-    const long long total = (long long)m * chunks_per_row;
+    const int m = P.m[z], n = P.n[z], nkb = P.nkb[z];
+    const long long chunks_per_row = (long long)nkb * 16;
+    const long long total = (long long)P.nib[z] * 128 * chunks_per_row;
     const cplx* A = P.A[z];
     int8_t* res = P.res[z];
-    const long long plane = (long long)m * pitch;
+    const long long plane = (long long)P.nib[z] * nkb * 16384;
     for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (long long)gridDim.x * blockDim.x) {
         const int row = (int)(e / chunks_per_row);
-        const int c0 = (int)(e % chunks_per_row) * 16;
-        const int er = P.kA[z] - oz_e(P.rowbits[z][row]);
-        double vr[16], vi[16];
+        const int c0 = (int)(e % chunks_per_row) * 8;
+        const int er = row < m ? P.kA[z] - P.rowexp[z][row] : 0;
+        double vr[8], vi[8];
 #pragma unroll
-        for (int u = 0; u < 16; ++u) {
+        for (int u = 0; u < 8; ++u) {
             const int col = c0 + u;
             cplx x = mk(0.0, 0.0);
             int s = 0;
-            if (col < n) {
+            if (row < m && col < n) {
                 x = A[(long long)row * P.lda[z] + col];
-                s = er - oz_e(P.colbits[z][col]);
+                s = er - oz_exp_or0(P.colexp[z][col]);
             }
             vr[u] = rint(oz_scale(x.x, s));
             vi[u] = rint(oz_scale(x.y, s));
             if (!isfinite(vr[u])) vr[u] = 0.0;
             if (!isfinite(vi[u])) vi[u] = 0.0;
         }
-        for (int t = 0; t < P.k.T; ++t) {
-            const int md = P.k.mod[t], lo = P.k.lo[t];
-            const double im = P.k.inv_md[t];
-            uint32_t pr[4], pi[4];
+        int8_t* dst = res + ((long long)(row >> 7) * nkb + (c0 >> 7)) * 16384 + (row & 127) * 128 + (c0 & 127);
+        if (TT > 0) {
 #pragma unroll
-            for (int w = 0; w < 4; ++w) {
-                uint32_t a = 0, b = 0;
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    a |= (uint32_t)(oz_res(vr[4 * w + u], md, im, lo) & 0xff) << (8 * u);
-                    b |= (uint32_t)(oz_res(vi[4 * w + u], md, im, lo) & 0xff) << (8 * u);
-                }
-                pr[w] = a;
-                pi[w] = b;
+            for (int t = 0; t < (TT > 0 ? TT : 1); ++t) {
+                const int md = oz_modulus(t);
+                oz_store8(vr, vi, dst + (long long)(2 * t) * plane, plane, md, 1.0 / (double)md, -(md / 2));
             }
-            int8_t* dst = res + (long long)(2 * t) * plane + (long long)row * pitch + c0;
-            *reinterpret_cast<uint4*>(dst) = make_uint4(pr[0], pr[1], pr[2], pr[3]);
-            *reinterpret_cast<uint4*>(dst + plane) = make_uint4(pi[0], pi[1], pi[2], pi[3]);
+        } else {
+            for (int t = 0; t < P.k.T; ++t)
+                oz_store8(vr, vi, dst + (long long)(2 * t) * plane, plane, P.k.mod[t], P.k.inv_md[t], P.k.lo[t]);
         }
     }
 }
@@ -229,9 +254,10 @@ __global__ void __launch_bounds__(256) oz_resid_a_kernel(const __grid_constant__
 constexpr int kProdGroup = 48;
 struct PanelParams {
     const cplx* X[kProdGroup];
-    long long ldx[kProdGroup], pitchK[kProdGroup];
+    long long ldx[kProdGroup];
+    int nkbx[kProdGroup];      // K tiles of 128
     int K[kProdGroup], l[kProdGroup], LT[kProdGroup], JT[kProdGroup], kX[kProdGroup];
-    const unsigned long long* kbits[kProdGroup];  // exponent source of the K rows
+    const int* kexp[kProdGroup];  // exponents of the K rows (op N: A's column exponents; op C: its row exponents)
     int8_t* bres[kProdGroup];
     int* sx[kProdGroup];     // [JT·LT]
     int* xbad[kProdGroup];   // [JT·LT]
@@ -260,7 +286,7 @@ __global__ void __launch_bounds__(256) oz_xmax_kernel(const __grid_constant__ Pa
                 bad = 1;
             } else {
                 const double a = fmax(fabs(v.x), fabs(v.y));
-                if (a > 0.0) mx = fmax(mx, oz_scale(a, oz_e(P.kbits[z][k])));
+                if (a > 0.0) mx = fmax(mx, oz_scale(a, oz_exp_or0(P.kexp[z][k])));
             }
         }
     smax[rg][c] = mx;
@@ -280,18 +306,18 @@ __global__ void __launch_bounds__(256) oz_resid_b_kernel(const __grid_constant__
     const int LT = P.LT[z], JT = P.JT[z], K = P.K[z], l = P.l[z];
     const int j0 = blockIdx.x * 8, k0 = blockIdx.y * 128;
     if (j0 >= JT * LT || k0 >= K) return;
-    const int tid = threadIdx.x, c = tid & 7, rg = tid >> 3;
-    const int j = j0 + c;
+    const int tid = threadIdx.x, kk = tid & 127;
     __shared__ __align__(16) int8_t S[kOzMaxMod][8][2][128];
-    const int sxj = j < l ? P.sx[z][j] : 0;
     const int T = P.k.T;
-    for (int u = 0; u < 4; ++u) {
-        const int kk = rg + 32 * u, k = k0 + kk;
+    const int k = k0 + kk;
+    const int ek = k < K ? oz_exp_or0(P.kexp[z][k]) : 0;
+    for (int c = tid >> 7; c < 8; c += 2) {
+        const int j = j0 + c;
         cplx v = mk(0.0, 0.0);
         int s = 0;
         if (j < l && k < K) {
             v = P.X[z][(long long)k * P.ldx[z] + j];
-            s = sxj + oz_e(P.kbits[z][k]);
+            s = P.sx[z][j] + ek;
         }
         double vr = rint(oz_scale(v.x, s)), vi = rint(oz_scale(v.y, s));
         if (!isfinite(vr)) vr = 0.0;
@@ -302,16 +328,14 @@ __global__ void __launch_bounds__(256) oz_resid_b_kernel(const __grid_constant__
         }
     }
     __syncthreads();
-    const long long pitchK = P.pitchK[z];
-    const long long R = 2ll * JT * LT;
-    const int jt = j0 / LT, jj0 = j0 % LT;
+    const int jt = j0 / LT, jj0 = j0 % LT, kb = blockIdx.y;
+    // B' tiles [t·JT + jt][part][kb][2LT rows][128 bytes of K]
     int8_t* bres = P.bres[z];
+    const long long tile = 2ll * LT * 128;
     // 16-byte pieces: (t, c, which, part, piece) — T·8·2·2·8 of them
     const int pieces = T * 8 * 2 * 2 * 8;
     for (int q = tid; q < pieces; q += 256) {
         const int piece = q & 7, part = (q >> 3) & 1, which = (q >> 4) & 1, cc = (q >> 5) & 7, t = q >> 8;
-        const long long kofs = k0 + piece * 16;
-        if (kofs >= pitchK) continue;
         // which 0 (re row): part0 = re, part1 = sg·im;  which 1 (im row): part0 = im, part1 = -sg·re
         const int src = which == 0 ? (part == 0 ? 0 : 1) : (part == 0 ? 1 : 0);
         const bool neg = part == 1 && ((which == 0) ? (P.sg < 0) : (P.sg > 0));
@@ -319,16 +343,22 @@ __global__ void __launch_bounds__(256) oz_resid_b_kernel(const __grid_constant__
         if (neg) {
             v.x = __vneg4(v.x); v.y = __vneg4(v.y); v.z = __vneg4(v.z); v.w = __vneg4(v.w);
         }
-        const long long r = (long long)jt * 2 * LT + which * LT + jj0 + cc;
-        *reinterpret_cast<uint4*>(bres + (((long long)t * R + r) * 2 + part) * pitchK + kofs) = v;
+        const int r = which * LT + jj0 + cc;
+        const long long blk = ((long long)(t * JT + jt) * 2 + part) * P.nkbx[z] + kb;
+        *reinterpret_cast<uint4*>(bres + blk * tile + (long long)r * 128 + piece * 16) = v;
     }
 }
 
 // ---- the INT8 tcgen05 GEMM --------------------------------------------------------------------
-constexpr int kBM = 256;      // two 128-row MMAs per K step (two TMEM accumulators)
+// kHalves = 1: one 128-row accumulator (256 TMEM columns), 2 stages, 4 warps -> two CTAs per SM, so
+// one CTA's epilogue and prologue overlap the other's loads; kHalves = 2: 256-row tiles, one CTA/SM.
+constexpr int kHalves = 2;
+constexpr int kBM = 128 * kHalves;
+constexpr int kThreads = 128 * kHalves;
+constexpr int kTmemCols = 256 * kHalves;
 constexpr int kBK = 128;      // bytes of K per stage = one 128B swizzle atom
-constexpr int kStages = 3;
-constexpr int kStageA = kBM * kBK;           // 32 KB
+constexpr int kStages = kHalves == 1 ? 2 : 3;
+constexpr int kStageA = kBM * kBK;
 constexpr int kStageB = 256 * kBK;           // up to N' = 256 rows
 constexpr int kStageBytes = kStageA + kStageB;
 constexpr int kGemmSmem = kStages * kStageBytes + 1024;  // + alignment slack
@@ -364,11 +394,11 @@ __device__ __forceinline__ void ob_wait(uint64_t* bar, unsigned parity) {
         "r"(parity)
         : "memory");
 }
-__device__ __forceinline__ void ob_tma4(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2, int c3) {
+__device__ __forceinline__ void ob_tma5(void* dst, const CUtensorMap* map, uint64_t* bar, int c2, int c3, int c4) {
     asm volatile(
-        "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6}], [%2];\n" ::"r"(
+        "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %3, %4, %5, %6}], [%2];\n" ::"r"(
             smem_u32(dst)),
-        "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+        "l"(map), "r"(smem_u32(bar)), "r"(0), "r"(c2), "r"(c3), "r"(c4)
         : "memory");
 }
 // shared-memory matrix descriptor, 128-byte swizzle (tcgen05 "version 1" descriptors)
@@ -406,7 +436,7 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
 
 // OPA = kOpN: A tile K-major ([row][k], the residue planes' own layout); kOpC: MN-major.
 template <int OPA>
-__global__ void __launch_bounds__(256, 1) oz_gemm_kernel(const __grid_constant__ GemmParams P) {
+__global__ void __launch_bounds__(kThreads, 3 - kHalves) oz_gemm_kernel(const __grid_constant__ GemmParams P) {
     const int z = blockIdx.z;
     const int M = P.M[z], JT = P.JT[z], LT = P.LT[z];
     const int m0 = blockIdx.x * kBM;
@@ -431,7 +461,8 @@ __global__ void __launch_bounds__(256, 1) oz_gemm_kernel(const __grid_constant__
         asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
     }
     if (warp == 2) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(smem_u32(&tmem_slot)));
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(&tmem_slot)),
+                     "n"(kTmemCols));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
     }
     tc_fence_before();
@@ -451,16 +482,13 @@ __global__ void __launch_bounds__(256, 1) oz_gemm_kernel(const __grid_constant__
             uint8_t* sa = smem + s * kStageBytes;
             uint8_t* sb = sa + kStageA;
             const int part = kb >= P.nkb[z] ? 1 : 0;
-            const int k0 = (kb - part * P.nkb[z]) * kBK;
             ob_expect_tx(&full[s], bytes);
-            if (OPA == kOpN) {
-                ob_tma4(sa, mA, &full[s], k0, m0, part, t);
-                ob_tma4(sa + 128 * kBK, mA, &full[s], k0, m0 + 128, part, t);
-            } else {
-                ob_tma4(sa, mA, &full[s], m0, k0, part, t);
-                ob_tma4(sa + 128 * kBK, mA, &full[s], m0 + 128, k0, part, t);
+            const int kb_ = kb - part * P.nkb[z];
+            for (int h = 0; h < kHalves; ++h) {
+                if (OPA == kOpN) ob_tma5(sa + h * 128 * kBK, mA, &full[s], kb_, m0 / 128 + h, 2 * t + part);
+                else ob_tma5(sa + h * 128 * kBK, mA, &full[s], m0 / 128 + h, kb_, 2 * t + part);
             }
-            ob_tma4(sb, mB, &full[s], k0, part, jt * Nn, t);
+            ob_tma5(sb, mB, &full[s], kb_, part, t * JT + jt);
         }
       }
       __syncwarp();
@@ -479,7 +507,7 @@ __global__ void __launch_bounds__(256, 1) oz_gemm_kernel(const __grid_constant__
             for (int ks = 0; ks < kBK / 32; ++ks) {
                 const uint64_t bdesc = sw128_desc(sb + ks * 32, 16, 1024);
 #pragma unroll
-                for (int h = 0; h < 2; ++h) {
+                for (int h = 0; h < kHalves; ++h) {
                     const uint32_t abase = sa + h * 128 * kBK;
                     const uint64_t adesc = OPA == kOpN ? sw128_desc(abase + ks * 32, 16, 1024)
                                                        : sw128_desc(abase + ks * 32 * 128, 128 * kBK, 1024);
@@ -522,7 +550,7 @@ __global__ void __launch_bounds__(256, 1) oz_gemm_kernel(const __grid_constant__
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem));
+    if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(kTmemCols));
 }
 
 // ---- CRT --------------------------------------------------------------------------------------
@@ -533,7 +561,7 @@ struct CrtParams {
     long long out_plane[kProdGroup];
     int out_ld[kProdGroup];
     int M[kProdGroup], l[kProdGroup], LT[kProdGroup], kA[kProdGroup];
-    const unsigned long long* obits[kProdGroup];  // exponent source of the output rows
+    const int* oexp[kProdGroup];  // exponents of the output rows
     const int* abad[kProdGroup];
     const int* sx[kProdGroup];
     const int* xbad[kProdGroup];
@@ -588,7 +616,7 @@ __global__ void __launch_bounds__(256) oz_crt_kernel(const __grid_constant__ Crt
         double re[4], im[4];
         oz_crt4(base, P.out_plane[z], P.k, re);
         oz_crt4(base + LT, P.out_plane[z], P.k, im);
-        const int eo = oz_e(P.obits[z][row]) - P.kA[z];
+        const int eo = oz_exp_or0(P.oexp[z][row]) - P.kA[z];
         cplx* dst = P.C[z] + (long long)row * P.ldc[z] + j0;
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
@@ -619,8 +647,8 @@ void encode_u8(rrsvd_b200_ctx* c, CUtensorMap* map, const void* base, const cuui
                const cuuint32_t* box) {
     const auto enc = oz_encoder();
     if (enc == nullptr) throw_numeric(c, "ozaki: cuTensorMapEncodeTiled unavailable");
-    const cuuint32_t one[4] = {1, 1, 1, 1};
-    const CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<void*>(base), dims, strides, box, one,
+    const cuuint32_t one[5] = {1, 1, 1, 1, 1};
+    const CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 5, const_cast<void*>(base), dims, strides, box, one,
                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) throw_numeric(c, "ozaki: tensor map encoding failed");
@@ -633,7 +661,7 @@ std::atomic<unsigned long long> g_optin{0};
 int ozaki_moduli() {
     static const int T = [] {
         const char* e = std::getenv("RRSVD_B200_OZAKI");
-        if (e == nullptr) return 0;
+        if (e == nullptr) return 14;
         const int v = std::atoi(e);
         if (v <= 0) return 0;
         return std::min(kOzMaxMod, std::max(8, v));
@@ -665,40 +693,56 @@ std::vector<OzakiA> ozaki_prepare_many(rrsvd_b200_ctx* c, const std::vector<OzSr
         check_cuda(c, cudaMemsetAsync(P.bad, 0, sizeof(int) * cnt, c->stream), "ozaki memset");
         long long max_chunks = 0;
         int max_m = 1, max_n = 1;
+        double bytes = 0.0;
         for (int i = 0; i < cnt; ++i) {
             const OzSrc& s = src[base + i];
             OzakiA& a = out[base + i];
             a.m = s.m;
             a.n = s.n;
             a.T = T;
-            a.pitch = ((long long)s.n + 15) / 16 * 16;
+            a.nib = (s.m + 127) / 128;
+            a.nkb = (s.n + 127) / 128;
             a.kA = std::min(56, (oz_total_bits(k, std::max(s.m, s.n)) + 1) / 2);
-            a.res = ws_get<int8_t>(c, (size_t)T * 2 * s.m * a.pitch);
-            a.rowbits = ws_get<unsigned long long>(c, s.m);
-            a.colbits = ws_get<unsigned long long>(c, s.n);
-            check_cuda(c, cudaMemsetAsync(a.colbits, 0, sizeof(unsigned long long) * s.n, c->stream), "ozaki memset");
+            a.res = ws_get<int8_t>(c, (size_t)T * 2 * a.nib * a.nkb * 16384);
+            a.rowexp = ws_get<int>(c, s.m);
+            a.colexp = ws_get<int>(c, s.n);
+            check_cuda(c, cudaMemsetAsync(a.colexp, 0xC0, sizeof(int) * s.n, c->stream), "ozaki memset");
             a.bad = P.bad + i;
             P.A[i] = s.A;
             P.lda[i] = s.lda;
-            P.pitch[i] = a.pitch;
+            P.nib[i] = a.nib;
+            P.nkb[i] = a.nkb;
             P.m[i] = s.m;
             P.n[i] = s.n;
             P.kA[i] = a.kA;
             P.res[i] = a.res;
-            P.rowbits[i] = a.rowbits;
-            P.colbits[i] = a.colbits;
-            max_chunks = std::max(max_chunks, (long long)s.m * a.pitch / 16);
+            P.rowexp[i] = a.rowexp;
+            P.colexp[i] = a.colexp;
+            max_chunks = std::max(max_chunks, (long long)a.nib * 128 * a.nkb * 16);
+            bytes += 3.0 * 16 * s.m * (double)s.n + 2.0 * T * a.nib * a.nkb * 16384;  // A read 3x, planes written
             max_m = std::max(max_m, s.m);
             max_n = std::max(max_n, s.n);
         }
-        oz_rowmax_kernel<<<dim3((max_m + 7) / 8, cnt), 256, 0, c->stream>>>(P);
-        check_launch(c, "oz_rowmax_kernel");
-        const int rch = std::max(1, std::min(64, (4 * kNumSMs * 32) / (cnt * max_n)));  // row chunks: >= ~4 CTAs/SM
-        oz_colmax_kernel<<<dim3((max_n + 31) / 32, rch, cnt), 256, 0, c->stream>>>(P);
-        check_launch(c, "oz_colmax_kernel");
+        cudaEvent_t ea = nullptr, eb = nullptr;
+        if (c->gemm_timing) {
+            ea = pooled_event(c);
+            eb = pooled_event(c);
+            check_cuda(c, cudaEventRecord(ea, c->stream), "event record");
+        }
+        oz_rowexp_kernel<<<dim3((max_m + 7) / 8, cnt), 256, 0, c->stream>>>(P);
+        check_launch(c, "oz_rowexp_kernel");
+        const int rch = std::max(1, std::min(64, (4 * kNumSMs * 32) / (cnt * max_n)));  // >= ~4 CTAs/SM
+        oz_colexp_kernel<<<dim3((max_n + 31) / 32, rch, cnt), 256, 0, c->stream>>>(P);
+        check_launch(c, "oz_colexp_kernel");
         const int gx = (int)std::min<long long>((max_chunks + 255) / 256, 8 * kNumSMs);
-        oz_resid_a_kernel<<<dim3(gx, cnt), 256, 0, c->stream>>>(P);
+        if (T == 14) oz_resid_a_kernel<14><<<dim3(gx, cnt), 256, 0, c->stream>>>(P);
+        else if (T == 16) oz_resid_a_kernel<16><<<dim3(gx, cnt), 256, 0, c->stream>>>(P);
+        else oz_resid_a_kernel<0><<<dim3(gx, cnt), 256, 0, c->stream>>>(P);
         check_launch(c, "oz_resid_a_kernel");
+        if (c->gemm_timing) {
+            check_cuda(c, cudaEventRecord(eb, c->stream), "event record");
+            c->pending.push_back({ea, eb, 0.0, 0.0, c->gemm_tag, 1, 1, bytes});
+        }
     }
     return out;
 }
@@ -733,6 +777,7 @@ void ozaki_product_many(rrsvd_b200_ctx* c, GemmOp op, const std::vector<OzProduc
             G.off[t] = k.off[t];
         }
         int max_cols = 8, max_mb = 1, max_jt = 1, max_k = 1;
+        double bytes = 0.0;
         long long max_el = 1;
         double flops = 0.0;
         for (int i = 0; i < cnt; ++i) {
@@ -742,35 +787,36 @@ void ozaki_product_many(rrsvd_b200_ctx* c, GemmOp op, const std::vector<OzProduc
             const int K = op == kOpN ? a.n : a.m, Mr = op == kOpN ? a.m : a.n;
             const int JT = (p.l + 127) / 128;
             const int LT = ((p.l + JT - 1) / JT + 7) / 8 * 8;
-            const long long pitchK = ((long long)K + 15) / 16 * 16;
+            const int nkbx = (K + 127) / 128;
             const int ncol = 2 * JT * LT;
             const int kX = std::min(56, oz_total_bits(k, K) - a.kA);
-            int8_t* bres = ws_get<int8_t>(c, (size_t)T * ncol * 2 * pitchK);
+            int8_t* bres = ws_get<int8_t>(c, (size_t)T * JT * 2 * nkbx * 2 * LT * 128);
             int* sx = ws_get<int>(c, (size_t)JT * LT);
             int* xbad = ws_get<int>(c, (size_t)JT * LT);
             uint8_t* out = ws_get<uint8_t>(c, (size_t)T * Mr * ncol);
             PP.X[i] = p.X;
             PP.ldx[i] = p.ldx;
-            PP.pitchK[i] = pitchK;
+            PP.nkbx[i] = nkbx;
             PP.K[i] = K;
             PP.l[i] = p.l;
             PP.LT[i] = LT;
             PP.JT[i] = JT;
             PP.kX[i] = kX;
-            PP.kbits[i] = op == kOpN ? a.colbits : a.rowbits;
+            PP.kexp[i] = op == kOpN ? a.colexp : a.rowexp;
             PP.bres[i] = bres;
             PP.sx[i] = sx;
             PP.xbad[i] = xbad;
-            {  // A planes [T][2][m][pitch]: (n, m, 2, T), box 128 x 128 (op N: (k, row); op C: (col, k))
-                const cuuint64_t dims[4] = {(cuuint64_t)a.n, (cuuint64_t)a.m, 2, (cuuint64_t)T};
-                const cuuint64_t str[3] = {(cuuint64_t)a.pitch, (cuuint64_t)a.m * a.pitch, 2ull * a.m * a.pitch};
-                const cuuint32_t box[4] = {128, 128, 1, 1};
+            {  // A tiles [2T][nib][nkb][128][128]: one box = one tile
+                const cuuint64_t dims[5] = {128, 128, (cuuint64_t)a.nkb, (cuuint64_t)a.nib, 2ull * T};
+                const cuuint64_t str[4] = {128, 16384, 16384ull * a.nkb, 16384ull * a.nkb * a.nib};
+                const cuuint32_t box[5] = {128, 128, 1, 1, 1};
                 encode_u8(c, &G.mapA[i], a.res, dims, str, box);
             }
-            {  // B' [T][ncol][2][pitchK]: (K, 2, ncol, T), box 128 x 1 x 2LT
-                const cuuint64_t dims[4] = {(cuuint64_t)K, 2, (cuuint64_t)ncol, (cuuint64_t)T};
-                const cuuint64_t str[3] = {(cuuint64_t)pitchK, 2ull * pitchK, 2ull * pitchK * ncol};
-                const cuuint32_t box[4] = {128, 1, (cuuint32_t)(2 * LT), 1};
+            {  // B' tiles [T·JT][2][nkbx][2LT][128]
+                const cuuint64_t rows = 2ull * LT;
+                const cuuint64_t dims[5] = {128, rows, (cuuint64_t)nkbx, 2, (cuuint64_t)T * JT};
+                const cuuint64_t str[4] = {128, 128 * rows, 128 * rows * nkbx, 256 * rows * nkbx};
+                const cuuint32_t box[5] = {128, (cuuint32_t)rows, 1, 1, 1};
                 encode_u8(c, &G.mapB[i], bres, dims, str, box);
             }
             G.M[i] = Mr;
@@ -787,7 +833,7 @@ void ozaki_product_many(rrsvd_b200_ctx* c, GemmOp op, const std::vector<OzProduc
             CP.l[i] = p.l;
             CP.LT[i] = LT;
             CP.kA[i] = a.kA;
-            CP.obits[i] = op == kOpN ? a.rowbits : a.colbits;
+            CP.oexp[i] = op == kOpN ? a.rowexp : a.colexp;
             CP.abad[i] = a.bad;
             CP.sx[i] = sx;
             CP.xbad[i] = xbad;
@@ -799,6 +845,9 @@ void ozaki_product_many(rrsvd_b200_ctx* c, GemmOp op, const std::vector<OzProduc
             max_el = std::max(max_el, (long long)Mr * JT * (LT / 4));
             max_k = std::max(max_k, K);
             flops += 8.0 * Mr * (double)p.l * K;
+            // X read; B' written + read; A residues read; residue products written + read; C written
+            bytes += 16.0 * K * p.l + 2.0 * T * JT * 2 * nkbx * 2 * LT * 128 + 2.0 * T * a.nib * a.nkb * 16384 +
+                     2.0 * T * Mr * ncol + 16.0 * Mr * p.l;
         }
         cudaEvent_t ea = nullptr, eb = nullptr;
         if (c->gemm_timing) {
@@ -811,16 +860,16 @@ void ozaki_product_many(rrsvd_b200_ctx* c, GemmOp op, const std::vector<OzProduc
         oz_resid_b_kernel<<<dim3((max_cols + 7) / 8, (max_k + 127) / 128, cnt), 256, 0, c->stream>>>(PP);
         check_launch(c, "oz_resid_b_kernel");
         if (op == kOpN)
-            oz_gemm_kernel<kOpN><<<dim3(max_mb, T * max_jt, cnt), 256, kGemmSmem, c->stream>>>(G);
+            oz_gemm_kernel<kOpN><<<dim3(max_mb, T * max_jt, cnt), kThreads, kGemmSmem, c->stream>>>(G);
         else
-            oz_gemm_kernel<kOpC><<<dim3(max_mb, T * max_jt, cnt), 256, kGemmSmem, c->stream>>>(G);
+            oz_gemm_kernel<kOpC><<<dim3(max_mb, T * max_jt, cnt), kThreads, kGemmSmem, c->stream>>>(G);
         check_launch(c, "oz_gemm_kernel");
         const int gx = (int)std::min<long long>((max_el + 255) / 256, 8 * kNumSMs);
         oz_crt_kernel<<<dim3(gx, cnt), 256, 0, c->stream>>>(CP);
         check_launch(c, "oz_crt_kernel");
         if (c->gemm_timing) {
             check_cuda(c, cudaEventRecord(eb, c->stream), "event record");
-            c->pending.push_back({ea, eb, flops, flops, c->gemm_tag, 1});
+            c->pending.push_back({ea, eb, flops, flops, c->gemm_tag, 1, 1, bytes});
         }
     }
 }

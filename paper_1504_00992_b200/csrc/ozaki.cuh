@@ -32,19 +32,21 @@ namespace rb {
 
 constexpr int kOzMaxMod = 16;
 
-// Residue planes of one A (m x n, row-major): int8 [T][2 (re, im)][m][pitch].
+// Residue planes of one A (m x n): int8 [T][2 (re, im)] planes stored as 128 x 128 tiles
+// [ib][kb][128 rows][128 columns] (zero-padded to whole tiles) — every TMA box is one contiguous
+// 16 KB block, serving op N as a K-major and op C as an MN-major operand tile.
 struct OzakiA {
     int8_t* res = nullptr;
     int m = 0, n = 0;
-    long long pitch = 0;                 // bytes per row (n rounded up to 16)
+    int nib = 0, nkb = 0;                // tile rows / columns: ceil(m / 128), ceil(n / 128)
     int T = 0, kA = 0;
-    unsigned long long* rowbits = nullptr;  // device [m]: bit pattern of row i's max(|Re|, |Im|)
-    unsigned long long* colbits = nullptr;  // device [n]: column maxima after row normalisation
+    int* rowexp = nullptr;  // device [m]: e_i, the exponent of row i's largest |Re|, |Im|
+    int* colexp = nullptr;  // device [n]: f_k = max_i e(|A_ik|) - e_i (<= 0)
     int* bad = nullptr;                     // device: a non-finite entry was seen
 };
 
-// Moduli count for the emulated A-products: RRSVD_B200_OZAKI (0 = off, the DMMA zgemm;
-// 8..16), default 0.  ozaki_usable: the shape gate of the RRSVD paths.
+// Moduli count for the emulated A-products: RRSVD_B200_OZAKI (0 = off, every A-product on the DMMA
+// zgemm; 8..16), default 14.  ozaki_usable: the shape gate of the RRSVD paths.
 int ozaki_moduli();
 bool ozaki_usable(int m, int n, int l);
 // RRSVD_B200_OZAKI_TAIL: how many of the RRSVD's last A-products stay on the FP64 zgemm — 1: the

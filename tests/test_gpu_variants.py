@@ -6,7 +6,10 @@ default, so an A/B switch can never hide a wrong result.
     vs the cp.async ring, and the shapes that fall back to cp.async (odd N; odd M under op C) —
     vs numpy, the reference's cblas_zgemm contract (linalg.cpp:20-40);
   * block Jacobi: the persistent sweep kernel (forced with RRSVD_B200_BJ_S=1) vs one launch per
-    tournament step — singular values vs LAPACK (the reference's svd_full, linalg.cpp:67-88).
+    tournament step — singular values vs LAPACK (the reference's svd_full, linalg.cpp:67-88);
+  * the RRSVD A-products: FP64 DMMA only (RRSVD_B200_OZAKI=0), the INT8 emulation with 14
+    (default) or 16 moduli, and with every product emulated (RRSVD_B200_OZAKI_TAIL=0) — the
+    headline decimation vs the reference's decimate (tebd.cpp:141-237).
 """
 import json
 import os
@@ -59,6 +62,34 @@ print(json.dumps(out))
 """
 
 
+DEC_SCRIPT = r"""
+import ctypes as C, json, sys
+import numpy as np
+sys.path.insert(0, %(root)r)
+import paper_1504_00992_b200 as P
+from oracle import ref
+from tests.conftest import cplx_randn
+from tests.test_gpu_parity import random_fragment
+ctx = P.Context(0)
+ctx.check(P.lib().rrsvd_b200_set_gemm_timing(ctx.h, 1))
+out = {}
+for seed in (2000, 2001):
+    rng = np.random.default_rng(seed)
+    g1, g2, ll, lm, lr = random_fragment(rng, 100, 20, 100, 20, 100, decay=0.85)
+    gate, _ = np.linalg.qr(cplx_randn(rng, 400, 400))
+    theta = ref.apply_gate(ref.build_theta(g1, g2, ll, lm, lr), gate)
+    kw = dict(randomized=True, target_rank=100, oversampling=10, power_iterations=2, det_crossover=256, seed=77)
+    got = P.decimate(theta, ll, lr, 100, 0.0, P.DecimationBackend(**kw), ctx=ctx)
+    want = ref.decimate(theta, ll, lr, 100, 0.0, ref.Backend(**kw))
+    out[str(seed)] = [int(got.chi), int(want.chi), float(np.max(np.abs(np.asarray(got.lam) - want.lam))),
+                      float(abs(got.discarded - want.discarded))]
+vals = [C.c_double() for _ in range(3)] + [C.c_uint64()] + [C.c_double() for _ in range(2)]
+ctx.check(P.lib().rrsvd_b200_ozaki_stats(ctx.h, *[C.byref(v) for v in vals]))
+out["oz_calls"] = int(vals[3].value)
+print(json.dumps(out))
+"""
+
+
 def run_variant(script, env_extra):
     env = dict(os.environ)
     env.update(env_extra)
@@ -88,3 +119,16 @@ def test_block_jacobi_variants(env):
     res = run_variant(SVD_SCRIPT, env)
     for shape, (ds, recon, orth) in res.items():
         assert ds <= 1e-13 and recon <= 1e-12 and orth <= 1e-12, (env, shape, ds, recon, orth)
+
+
+@pytest.mark.parametrize("env", [{"RRSVD_B200_OZAKI": "0"}, {}, {"RRSVD_B200_OZAKI": "16"},
+                                 {"RRSVD_B200_OZAKI_TAIL": "0"}, {"RRSVD_B200_OZAKI_TAIL": "1"}])
+def test_rrsvd_a_product_paths(env):
+    """The headline decimation (2000 x 2000 Θ, RRSVD k = 100, p = 10, q = 2, reference Ω) with the
+    A-products on the DMMA zgemm or on the INT8 emulation: chi equal, λ and w within 1e-10 of the
+    reference; the emulation really ran unless switched off."""
+    res = run_variant(DEC_SCRIPT, env)
+    calls = res.pop("oz_calls")
+    assert (calls == 0) == (env.get("RRSVD_B200_OZAKI") == "0"), (env, calls)
+    for seed, (chi, rchi, dlam, dw) in res.items():
+        assert chi == rchi == 100 and dlam < 1e-10 and dw < 1e-10, (env, seed, chi, rchi, dlam, dw)
