@@ -11,9 +11,11 @@
 #include <algorithm>
 #include <atomic>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 
 #include "ozaki.cuh"
+#include "pipeline.cuh"  // debug_enabled
 
 namespace rb {
 
@@ -300,32 +302,49 @@ __global__ void __launch_bounds__(256) oz_xmax_kernel(const __grid_constant__ Pa
     }
 }
 
-// block = 8 columns x 128 K rows: residues into shared memory, then 128-byte rows of B'
+// block = 8 columns x 128 K rows; a thread takes four consecutive K rows of one column (c = tid & 7,
+// so a warp reads 4 x 128 contiguous bytes per row), packs each modulus' four residues into one word
+// in shared memory, then the block writes 128-byte rows of B' (TT > 0: compile-time moduli).
+template <int TT>
 __global__ void __launch_bounds__(256) oz_resid_b_kernel(const __grid_constant__ PanelParams P) {
     const int z = blockIdx.z;
     const int LT = P.LT[z], JT = P.JT[z], K = P.K[z], l = P.l[z];
     const int j0 = blockIdx.x * 8, k0 = blockIdx.y * 128;
     if (j0 >= JT * LT || k0 >= K) return;
-    const int tid = threadIdx.x, kk = tid & 127;
-    __shared__ __align__(16) int8_t S[kOzMaxMod][8][2][128];
-    const int T = P.k.T;
-    const int k = k0 + kk;
-    const int ek = k < K ? oz_exp_or0(P.kexp[z][k]) : 0;
-    for (int c = tid >> 7; c < 8; c += 2) {
-        const int j = j0 + c;
+    const int tid = threadIdx.x, c = tid & 7, kq = tid >> 3;
+    constexpr int kPad = 33;  // words per (t, c, part) row: bank-spread across c
+    __shared__ uint32_t S[kOzMaxMod][8][2][kPad];
+    const int T = TT > 0 ? TT : P.k.T;
+    const int j = j0 + c;
+    double vr[4], vi[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        const int k = k0 + 4 * kq + u;
         cplx v = mk(0.0, 0.0);
-        int s = 0;
+        int sc = 0;
         if (j < l && k < K) {
             v = P.X[z][(long long)k * P.ldx[z] + j];
-            s = P.sx[z][j] + ek;
+            sc = P.sx[z][j] + oz_exp_or0(P.kexp[z][k]);
         }
-        double vr = rint(oz_scale(v.x, s)), vi = rint(oz_scale(v.y, s));
-        if (!isfinite(vr)) vr = 0.0;
-        if (!isfinite(vi)) vi = 0.0;
-        for (int t = 0; t < T; ++t) {
-            S[t][c][0][kk] = (int8_t)oz_res(vr, P.k.mod[t], P.k.inv_md[t], P.k.lo[t]);
-            S[t][c][1][kk] = (int8_t)oz_res(vi, P.k.mod[t], P.k.inv_md[t], P.k.lo[t]);
+        vr[u] = rint(oz_scale(v.x, sc));
+        vi[u] = rint(oz_scale(v.y, sc));
+        if (!isfinite(vr[u])) vr[u] = 0.0;
+        if (!isfinite(vi[u])) vi[u] = 0.0;
+    }
+#pragma unroll
+    for (int t = 0; t < (TT > 0 ? TT : kOzMaxMod); ++t) {
+        if (TT == 0 && t >= T) break;
+        const int md = TT > 0 ? oz_modulus(t) : P.k.mod[t];
+        const double im = TT > 0 ? 1.0 / (double)oz_modulus(t) : P.k.inv_md[t];
+        const int lo = -(md / 2);
+        uint32_t a = 0, b = 0;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            a |= (uint32_t)(oz_res(vr[u], md, im, lo) & 0xff) << (8 * u);
+            b |= (uint32_t)(oz_res(vi[u], md, im, lo) & 0xff) << (8 * u);
         }
+        S[t][c][0][kq] = a;
+        S[t][c][1][kq] = b;
     }
     __syncthreads();
     const int jt = j0 / LT, jj0 = j0 % LT, kb = blockIdx.y;
@@ -339,7 +358,8 @@ __global__ void __launch_bounds__(256) oz_resid_b_kernel(const __grid_constant__
         // which 0 (re row): part0 = re, part1 = sg·im;  which 1 (im row): part0 = im, part1 = -sg·re
         const int src = which == 0 ? (part == 0 ? 0 : 1) : (part == 0 ? 1 : 0);
         const bool neg = part == 1 && ((which == 0) ? (P.sg < 0) : (P.sg > 0));
-        uint4 v = *reinterpret_cast<const uint4*>(&S[t][cc][src][piece * 16]);
+        const uint32_t* w = &S[t][cc][src][piece * 4];
+        uint4 v = make_uint4(w[0], w[1], w[2], w[3]);
         if (neg) {
             v.x = __vneg4(v.x); v.y = __vneg4(v.y); v.z = __vneg4(v.z); v.w = __vneg4(v.w);
         }
@@ -370,6 +390,7 @@ struct alignas(64) GemmParams {
     uint8_t* out[kProdGroup];
     long long out_plane[kProdGroup];
     int out_ld[kProdGroup];
+    int tile_begin[kProdGroup + 1];  // persistent kernel: tiles of problem z are [tile_begin[z], tile_begin[z+1])
     int count;
     int T;
     int mod[kOzMaxMod], w[kOzMaxMod];
@@ -553,6 +574,168 @@ __global__ void __launch_bounds__(kThreads, 3 - kHalves) oz_gemm_kernel(const __
     if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(kTmemCols));
 }
 
+// The persistent form: one CTA per SM walks the tiles (z, t, jt, m-block; m-block fastest so the
+// CTAs sharing a B' panel run together) with warp-specialised roles — warp 0 issues TMA, warp 1
+// issues tcgen05.mma, warps 2..9 drain TMEM.  The smem ring and its phases run on across tiles, so
+// the producer keeps loading the next tile while the epilogue of the previous one reads TMEM (the
+// MMAs of the next tile wait only for the accumulators to be drained: tmem_empty).
+struct TileCoord {
+    int z, t, jt, m0;
+};
+__device__ __forceinline__ TileCoord oz_tile(const GemmParams& P, int tile) {
+    int z = 0;
+    while (z + 1 < P.count && tile >= P.tile_begin[z + 1]) ++z;
+    const int local = tile - P.tile_begin[z];
+    const int mbs = (P.M[z] + kBM - 1) / kBM;
+    const int y = local / mbs;
+    return {z, y / P.JT[z], y % P.JT[z], (local % mbs) * kBM};
+}
+
+// Separate rings: A (HBM stream) 5 deep, B' (L2-resident panel) 2 deep, each with its own producer
+// warp, so the A prefetch depth is not gated by the panel's ring.
+constexpr int kAStages = 4, kBStages = 3;
+constexpr int kPSmem = (kAStages + kBStages) * 32768 + 1024;
+constexpr int kPThreads = 352;  // warp 0: A producer, 1: MMA, 2: B' producer, 3..10: epilogue
+template <int OPA>
+__global__ void __launch_bounds__(kPThreads, 1) oz_gemm_persistent_kernel(const __grid_constant__ GemmParams P) {
+    static_assert(kHalves == 2, "persistent tiles are 256 rows");
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* ringA = smem;
+    uint8_t* ringB = smem + kAStages * 32768;
+    __shared__ __align__(8) uint64_t afull[kAStages], aempty[kAStages], bfull[kBStages], bempty[kBStages], tfull, tempty;
+    __shared__ uint32_t tmem_slot;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int ntiles = P.tile_begin[P.count];
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kAStages; ++s) {
+            ob_init(&afull[s], 1);
+            ob_init(&aempty[s], 1);
+        }
+        for (int s = 0; s < kBStages; ++s) {
+            ob_init(&bfull[s], 1);
+            ob_init(&bempty[s], 1);
+        }
+        ob_init(&tfull, 1);
+        ob_init(&tempty, 8);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(&tmem_slot)),
+                     "n"(kTmemCols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = tmem_slot;
+
+    if (warp == 0 || warp == 2) {
+        if (lane == 0) {  // ---- TMA producers: warp 0 streams A, warp 2 the panel B'
+            const bool isA = warp == 0;
+            const int S = isA ? kAStages : kBStages;
+            uint64_t* fullb = isA ? afull : bfull;
+            uint64_t* emptyb = isA ? aempty : bempty;
+            uint8_t* ring = isA ? ringA : ringB;
+            int it = 0;
+            for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+                const TileCoord tc = oz_tile(P, tile);
+                const CUtensorMap* map = isA ? &P.mapA[tc.z] : &P.mapB[tc.z];
+                const int Nn = 2 * P.LT[tc.z], nkb = P.nkb[tc.z];
+                const unsigned bytes = isA ? kStageA : Nn * kBK;
+                for (int kb = 0; kb < 2 * nkb; ++kb, ++it) {
+                    const int s = it % S, use = it / S;
+                    if (use > 0) ob_wait(&emptyb[s], (use - 1) & 1);
+                    uint8_t* dst = ring + s * 32768;
+                    const int part = kb >= nkb ? 1 : 0, kk = kb - part * nkb;
+                    ob_expect_tx(&fullb[s], bytes);
+                    if (isA) {
+                        for (int h = 0; h < 2; ++h) {
+                            if (OPA == kOpN) ob_tma5(dst + h * 128 * kBK, map, &fullb[s], kk, tc.m0 / 128 + h, 2 * tc.t + part);
+                            else ob_tma5(dst + h * 128 * kBK, map, &fullb[s], tc.m0 / 128 + h, kk, 2 * tc.t + part);
+                        }
+                    } else {
+                        ob_tma5(dst, map, &fullb[s], kk, part, tc.t * P.JT[tc.z] + tc.jt);
+                    }
+                }
+            }
+        }
+        __syncwarp();
+    } else if (warp == 1) {
+        if (lane == 0) {  // ---- MMA issuer
+            int it = 0, tcount = 0;
+            for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++tcount) {
+                const TileCoord tc = oz_tile(P, tile);
+                const int Nn = 2 * P.LT[tc.z], nk = 2 * P.nkb[tc.z];
+                const uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((OPA == kOpC ? 1u : 0u) << 15) |
+                                       ((uint32_t)(Nn >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+                if (tcount > 0) ob_wait(&tempty, (tcount - 1) & 1);
+                tc_fence_after();
+                for (int kb = 0; kb < nk; ++kb, ++it) {
+                    const int sa_ = it % kAStages, sb_ = it % kBStages;
+                    ob_wait(&afull[sa_], (it / kAStages) & 1);
+                    ob_wait(&bfull[sb_], (it / kBStages) & 1);
+                    tc_fence_after();
+                    const uint32_t sa = smem_u32(ringA + sa_ * 32768);
+                    const uint32_t sb = smem_u32(ringB + sb_ * 32768);
+#pragma unroll
+                    for (int ks = 0; ks < kBK / 32; ++ks) {
+                        const uint64_t bdesc = sw128_desc(sb + ks * 32, 16, 1024);
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            const uint32_t abase = sa + h * 128 * kBK;
+                            const uint64_t adesc = OPA == kOpN ? sw128_desc(abase + ks * 32, 16, 1024)
+                                                               : sw128_desc(abase + ks * 32 * 128, 128 * kBK, 1024);
+                            mma_i8(tmem + h * 256, adesc, bdesc, idesc, (kb | ks) != 0);
+                        }
+                    }
+                    mma_commit(&aempty[sa_]);
+                    mma_commit(&bempty[sb_]);
+                }
+                mma_commit(&tfull);
+            }
+        }
+        __syncwarp();
+    } else {  // ---- epilogue: warps 3..10; warp w reads TMEM lanes 32(w%4).. of accumulator (w-3)/4
+        const int q = warp & 3, h = (warp - 3) >> 2;
+        int tcount = 0;
+        for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++tcount) {
+            const TileCoord tc = oz_tile(P, tile);
+            const int Nn = 2 * P.LT[tc.z];
+            ob_wait(&tfull, tcount & 1);
+            tc_fence_after();
+            const int row = tc.m0 + h * 128 + q * 32 + lane;
+            const int md = P.mod[tc.t], w = P.w[tc.t];
+            const unsigned mg = P.magic[tc.t], off = P.off[tc.t];
+            uint8_t* dst = P.out[tc.z] + (long long)tc.t * P.out_plane[tc.z] + (long long)row * P.out_ld[tc.z] + tc.jt * Nn;
+            for (int ch = 0; ch < Nn / 16; ++ch) {
+                uint32_t v[16];
+                tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + h * 256 + ch * 16, v);
+                uint32_t pk[4] = {0, 0, 0, 0};
+#pragma unroll
+                for (int u = 0; u < 16; ++u) {
+                    const unsigned x = v[u] + off;
+                    int r = (int)(x - __umulhi(x, mg) * md);
+                    r += (r >> 31) & md;
+                    const unsigned p = (unsigned)(r * w);
+                    int tt = (int)(p - __umulhi(p, mg) * md);
+                    tt += (tt >> 31) & md;
+                    pk[u >> 2] |= (uint32_t)tt << (8 * (u & 3));
+                }
+                if (row < P.M[tc.z]) *reinterpret_cast<uint4*>(dst + ch * 16) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(&tempty)) : "memory");
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(kTmemCols));
+}
+
 // ---- CRT --------------------------------------------------------------------------------------
 // D/M = frac_sym( sum_t t_t / m_t ) in 128-bit fixed point, from the top 96 bits of floor(2^128/m_t)
 // (truncation error < T·2^8·2^32 units of 2^-128 — 2^-84 of M, far below one unit of kA + kX).
@@ -571,9 +754,12 @@ struct CrtParams {
 };
 
 // the signed value D/M·2^128 of four consecutive outputs' residues (one uchar4 per modulus)
+template <int TT>
 __device__ __forceinline__ void oz_crt4(const uint8_t* p, long long plane, const OzConst& k, double (&val)[4]) {
     unsigned long long a0[4] = {0, 0, 0, 0}, a1[4] = {0, 0, 0, 0}, a2[4] = {0, 0, 0, 0};
-    for (int t = 0; t < k.T; ++t) {
+#pragma unroll
+    for (int t = 0; t < (TT > 0 ? TT : kOzMaxMod); ++t) {
+        if (TT == 0 && t >= k.T) break;
         const uint32_t b = *reinterpret_cast<const uint32_t*>(p + (long long)t * plane);
         const unsigned c0 = k.c3[t][0], c1 = k.c3[t][1], c2 = k.c3[t][2];
 #pragma unroll
@@ -600,6 +786,7 @@ __device__ __forceinline__ void oz_crt4(const uint8_t* p, long long plane, const
 }
 
 // one thread = four consecutive output columns of one row
+template <int TT>
 __global__ void __launch_bounds__(256) oz_crt_kernel(const __grid_constant__ CrtParams P) {
     const int z = blockIdx.y;
     const int M = P.M[z], l = P.l[z], LT = P.LT[z];
@@ -614,8 +801,8 @@ __global__ void __launch_bounds__(256) oz_crt_kernel(const __grid_constant__ Crt
         if (j0 >= l) continue;
         const uint8_t* base = P.out[z] + (long long)row * P.out_ld[z] + (long long)jt * 2 * LT + jj;
         double re[4], im[4];
-        oz_crt4(base, P.out_plane[z], P.k, re);
-        oz_crt4(base + LT, P.out_plane[z], P.k, im);
+        oz_crt4<TT>(base, P.out_plane[z], P.k, re);
+        oz_crt4<TT>(base + LT, P.out_plane[z], P.k, im);
         const int eo = oz_exp_or0(P.oexp[z][row]) - P.kA[z];
         cplx* dst = P.C[z] + (long long)row * P.ldc[z] + j0;
 #pragma unroll
@@ -667,6 +854,14 @@ int ozaki_moduli() {
         return std::min(kOzMaxMod, std::max(8, v));
     }();
     return T;
+}
+
+static bool oz_persistent() {  // RRSVD_B200_OZAKI_PERSISTENT=0: one CTA per tile (A/B)
+    static const bool on = [] {
+        const char* e = std::getenv("RRSVD_B200_OZAKI_PERSISTENT");
+        return e == nullptr || std::atoi(e) != 0;
+    }();
+    return on;
 }
 
 int ozaki_tail() {
@@ -756,6 +951,10 @@ void ozaki_product_many(rrsvd_b200_ctx* c, GemmOp op, const std::vector<OzProduc
                    "ozaki smem opt-in");
         check_cuda(c, cudaFuncSetAttribute(oz_gemm_kernel<kOpC>, cudaFuncAttributeMaxDynamicSharedMemorySize, kGemmSmem),
                    "ozaki smem opt-in");
+        check_cuda(c, cudaFuncSetAttribute(oz_gemm_persistent_kernel<kOpN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           kPSmem), "ozaki smem opt-in");
+        check_cuda(c, cudaFuncSetAttribute(oz_gemm_persistent_kernel<kOpC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           kPSmem), "ozaki smem opt-in");
         g_optin.fetch_or(bit);
     }
     for (size_t base = 0; base < ps.size(); base += kProdGroup) {
@@ -849,6 +1048,12 @@ void ozaki_product_many(rrsvd_b200_ctx* c, GemmOp op, const std::vector<OzProduc
             bytes += 16.0 * K * p.l + 2.0 * T * JT * 2 * nkbx * 2 * LT * 128 + 2.0 * T * a.nib * a.nkb * 16384 +
                      2.0 * T * Mr * ncol + 16.0 * Mr * p.l;
         }
+        int ntiles = 0;
+        for (int i = 0; i < cnt; ++i) {
+            G.tile_begin[i] = ntiles;
+            ntiles += (G.M[i] + kBM - 1) / kBM * T * G.JT[i];
+        }
+        G.tile_begin[cnt] = ntiles;
         cudaEvent_t ea = nullptr, eb = nullptr;
         if (c->gemm_timing) {
             ea = pooled_event(c);
@@ -857,19 +1062,54 @@ void ozaki_product_many(rrsvd_b200_ctx* c, GemmOp op, const std::vector<OzProduc
         }
         oz_xmax_kernel<<<dim3((max_cols + 7) / 8, cnt), 256, 0, c->stream>>>(PP);
         check_launch(c, "oz_xmax_kernel");
-        oz_resid_b_kernel<<<dim3((max_cols + 7) / 8, (max_k + 127) / 128, cnt), 256, 0, c->stream>>>(PP);
+        const dim3 gb((max_cols + 7) / 8, (max_k + 127) / 128, cnt);
+        if (T == 14) oz_resid_b_kernel<14><<<gb, 256, 0, c->stream>>>(PP);
+        else if (T == 16) oz_resid_b_kernel<16><<<gb, 256, 0, c->stream>>>(PP);
+        else oz_resid_b_kernel<0><<<gb, 256, 0, c->stream>>>(PP);
         check_launch(c, "oz_resid_b_kernel");
-        if (op == kOpN)
+        if (oz_persistent()) {
+            const int grid = std::min(ntiles, kNumSMs);
+            if (op == kOpN)
+                oz_gemm_persistent_kernel<kOpN><<<grid, kPThreads, kPSmem, c->stream>>>(G);
+            else
+                oz_gemm_persistent_kernel<kOpC><<<grid, kPThreads, kPSmem, c->stream>>>(G);
+        } else if (op == kOpN) {
             oz_gemm_kernel<kOpN><<<dim3(max_mb, T * max_jt, cnt), kThreads, kGemmSmem, c->stream>>>(G);
-        else
+        } else {
             oz_gemm_kernel<kOpC><<<dim3(max_mb, T * max_jt, cnt), kThreads, kGemmSmem, c->stream>>>(G);
+        }
         check_launch(c, "oz_gemm_kernel");
         const int gx = (int)std::min<long long>((max_el + 255) / 256, 8 * kNumSMs);
-        oz_crt_kernel<<<dim3(gx, cnt), 256, 0, c->stream>>>(CP);
+        if (T == 14) oz_crt_kernel<14><<<dim3(gx, cnt), 256, 0, c->stream>>>(CP);
+        else if (T == 16) oz_crt_kernel<16><<<dim3(gx, cnt), 256, 0, c->stream>>>(CP);
+        else oz_crt_kernel<0><<<dim3(gx, cnt), 256, 0, c->stream>>>(CP);
         check_launch(c, "oz_crt_kernel");
         if (c->gemm_timing) {
             check_cuda(c, cudaEventRecord(eb, c->stream), "event record");
             c->pending.push_back({ea, eb, flops, flops, c->gemm_tag, 1, 1, bytes});
+        }
+        if (debug_enabled()) {  // zero / non-finite output columns of every product (diagnostics)
+            for (int i = 0; i < cnt; ++i) {
+                const OzProduct& p = ps[base + i];
+                const int Mr = op == kOpN ? p.a->m : p.a->n;
+                std::vector<cplx> h((size_t)Mr * p.ldc);
+                cudaMemcpyAsync(h.data(), p.C, h.size() * sizeof(cplx), cudaMemcpyDeviceToHost, c->stream);
+                std::vector<int> xs(p.l);
+                cudaMemcpyAsync(xs.data(), CP.sx[i], p.l * sizeof(int), cudaMemcpyDeviceToHost, c->stream);
+                cudaStreamSynchronize(c->stream);
+                int zc = 0, nf = 0;
+                for (int j = 0; j < p.l; ++j) {
+                    bool z = true;
+                    for (int r = 0; r < Mr; ++r) {
+                        const cplx v = h[(size_t)r * p.ldc + j];
+                        if (v.x != 0.0 || v.y != 0.0) z = false;
+                        if (!std::isfinite(v.x) || !std::isfinite(v.y)) ++nf;
+                    }
+                    zc += z;
+                }
+                std::fprintf(stderr, "[rrsvd_b200] ozaki op%d product %d: %d x %d, zero columns %d, non-finite %d, sx[0..3] %d %d %d %d\n",
+                             (int)op, i, Mr, p.l, zc, nf, xs[0], xs[1], xs[2], xs[3]);
+            }
         }
     }
 }

@@ -246,6 +246,11 @@ void orth_many_adaptive(rrsvd_b200_ctx* c, const std::vector<OrthSpec>& specs, b
         bufs[i] = {ws_get<cplx>(c, (size_t)s.l * s.l), ws_get<cplx>(c, (size_t)s.l * s.l),
                    ws_get<cplx>(c, (size_t)s.m * s.l), ws_get<cplx>(c, (size_t)s.m * s.l), s.Y};
     }
+    // debug: dead-pivot counts of every pass (RRSVD_B200_DEBUG)
+    const bool dbg = debug_enabled();
+    int* dbg_dead = dbg ? ws_get<int>(c, 4 * np) : nullptr;
+    int pass_no = 0;
+    if (dbg) check_cuda(c, cudaMemsetAsync(dbg_dead, 0, 4 * np * sizeof(int), c->stream), "memset");
     // one pass for every problem: Gram, chol_inv (any width), apply  (pred: run only if *pred != 0)
     auto pass = [&](bool shifted, std::vector<const cplx*> src, std::vector<cplx*> dst, bool first,
                      const int* pred_base, bool last) {
@@ -257,7 +262,8 @@ void orth_many_adaptive(rrsvd_b200_ctx* c, const std::vector<OrthSpec>& specs, b
             gs.structure = kUpperC;
             if (pred_base) gs.pred = pred_base + i;
             gram.push_back(gs);
-            CholSpec cs{bufs[i].G, s.l, shifted ? 10.0 * (s.m + s.l) : 0.0, bufs[i].T, last ? s.ndead : nullptr};
+            CholSpec cs{bufs[i].G, s.l, shifted ? 10.0 * (s.m + s.l) : 0.0, bufs[i].T,
+                        last && !dbg ? s.ndead : (dbg ? dbg_dead + 4 * i + pass_no : nullptr)};
             cs.ill_out = first ? ill + i : nullptr;
             cs.pred = pred_base ? pred_base + i : nullptr;
             chol.push_back(cs);
@@ -271,6 +277,7 @@ void orth_many_adaptive(rrsvd_b200_ctx* c, const std::vector<OrthSpec>& specs, b
         chol_inv_many(c, chol);
         c->gemm_tag = 4;
         gemm_many(c, kOpN, apply);
+        ++pass_no;
     };
     std::vector<const cplx*> Y(np), A(np), B(np);
     std::vector<cplx*> Aw(np), Bw(np), Q(np);
@@ -283,6 +290,18 @@ void orth_many_adaptive(rrsvd_b200_ctx* c, const std::vector<OrthSpec>& specs, b
     if (full) {
         pass(false, B, Aw, false, ill, false);           // [ill] plain b -> a
         pass(false, A, Q, false, nullptr, true);         // plain a -> Q
+        if (dbg) {
+            std::vector<int> h(4 * np), hi(np);
+            cudaMemcpyAsync(h.data(), dbg_dead, h.size() * sizeof(int), cudaMemcpyDeviceToHost, c->stream);
+            cudaMemcpyAsync(hi.data(), ill, hi.size() * sizeof(int), cudaMemcpyDeviceToHost, c->stream);
+            cudaStreamSynchronize(c->stream);
+            for (size_t i = 0; i < np; ++i)
+                std::fprintf(stderr, "[rrsvd_b200] orth full %dx%d: ill %d, dead per pass %d %d %d %d\n", specs[i].m,
+                             specs[i].l, hi[i], h[4 * i], h[4 * i + 1], h[4 * i + 2], h[4 * i + 3]);
+            for (size_t i = 0; i < np; ++i)  // (the caller's ndead: the last pass)
+                if (specs[i].ndead)
+                    cudaMemcpyAsync(specs[i].ndead, dbg_dead + 4 * i + 3, sizeof(int), cudaMemcpyDeviceToDevice, c->stream);
+        }
     } else {
         for (size_t base = 0; base < np; base += kMaxSmall) {  // Q = ill ? b : a
             SelectBatch sb{};
