@@ -99,15 +99,17 @@ def workload(name: str):
 def emulated_entry(flops, ms, nbytes, calls, prep_ms, prep_bytes) -> dict:
     """The RRSVD A-products on the INT8 tensor cores (csrc/ozaki.cuh), from the serial roofline pass:
     kept out of the DMMA roofline above (its `frac` covers the FP64 zgemm launches only)."""
-    moduli = int(os.environ.get("RRSVD_B200_OZAKI", "14") or 0)
+    moduli = int(os.environ.get("RRSVD_B200_OZAKI", "15") or 0)
+    tail = int(os.environ.get("RRSVD_B200_OZAKI_TAIL", "0") or 0)
     if ms <= 0:
         return {"enabled": False, "moduli": moduli}
     return {"enabled": True, "moduli": moduli,
             "scheme": "Chinese-remainder (Ozaki-II) emulation of the complex-FP64 product: A and the panel "
                       "equilibrated by powers of two, int8 residues, tcgen05.mma kind::i8 into TMEM, 96-bit "
                       "fixed-point CRT to FP64",
-            "products": "4 of the 2q+2 = 6 A-products per decimation (Y = A Omega and the power iteration); the "
-                        "final Y = A Q~ and B^H = A^H Q stay on the FP64 DMMA zgemm (RRSVD_B200_OZAKI_TAIL)",
+            "products": ("all 2q+2 = 6 A-products per decimation (Y = A Omega, the power iteration, B^H = A^H Q)"
+                         if tail == 0 else f"all but the last {tail} of the 2q+2 A-products per decimation (those on "
+                                           "the FP64 DMMA zgemm, RRSVD_B200_OZAKI_TAIL)"),
             "ms_per_step": round(ms, 3), "fp64_equivalent_tflops": round(flops / (ms * 1e-3) / 1e12, 2),
             "algorithmic_GBps": round(nbytes / (ms * 1e-3) / 1e9, 1), "launch_groups": int(calls),
             "a_preparation_ms_per_step": round(prep_ms, 3),

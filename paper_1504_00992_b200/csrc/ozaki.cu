@@ -848,7 +848,7 @@ std::atomic<unsigned long long> g_optin{0};
 int ozaki_moduli() {
     static const int T = [] {
         const char* e = std::getenv("RRSVD_B200_OZAKI");
-        if (e == nullptr) return 14;
+        if (e == nullptr) return 15;
         const int v = std::atoi(e);
         if (v <= 0) return 0;
         return std::min(kOzMaxMod, std::max(8, v));
@@ -867,7 +867,7 @@ static bool oz_persistent() {  // RRSVD_B200_OZAKI_PERSISTENT=0: one CTA per til
 int ozaki_tail() {
     static const int v = [] {
         const char* e = std::getenv("RRSVD_B200_OZAKI_TAIL");
-        return e == nullptr ? 2 : std::max(0, std::atoi(e));
+        return e == nullptr ? 0 : std::max(0, std::atoi(e));
     }();
     return v;
 }
@@ -930,7 +930,8 @@ std::vector<OzakiA> ozaki_prepare_many(rrsvd_b200_ctx* c, const std::vector<OzSr
         oz_colexp_kernel<<<dim3((max_n + 31) / 32, rch, cnt), 256, 0, c->stream>>>(P);
         check_launch(c, "oz_colexp_kernel");
         const int gx = (int)std::min<long long>((max_chunks + 255) / 256, 8 * kNumSMs);
-        if (T == 14) oz_resid_a_kernel<14><<<dim3(gx, cnt), 256, 0, c->stream>>>(P);
+        if (T == 15) oz_resid_a_kernel<15><<<dim3(gx, cnt), 256, 0, c->stream>>>(P);
+        else if (T == 14) oz_resid_a_kernel<14><<<dim3(gx, cnt), 256, 0, c->stream>>>(P);
         else if (T == 16) oz_resid_a_kernel<16><<<dim3(gx, cnt), 256, 0, c->stream>>>(P);
         else oz_resid_a_kernel<0><<<dim3(gx, cnt), 256, 0, c->stream>>>(P);
         check_launch(c, "oz_resid_a_kernel");
@@ -1063,7 +1064,8 @@ void ozaki_product_many(rrsvd_b200_ctx* c, GemmOp op, const std::vector<OzProduc
         oz_xmax_kernel<<<dim3((max_cols + 7) / 8, cnt), 256, 0, c->stream>>>(PP);
         check_launch(c, "oz_xmax_kernel");
         const dim3 gb((max_cols + 7) / 8, (max_k + 127) / 128, cnt);
-        if (T == 14) oz_resid_b_kernel<14><<<gb, 256, 0, c->stream>>>(PP);
+        if (T == 15) oz_resid_b_kernel<15><<<gb, 256, 0, c->stream>>>(PP);
+        else if (T == 14) oz_resid_b_kernel<14><<<gb, 256, 0, c->stream>>>(PP);
         else if (T == 16) oz_resid_b_kernel<16><<<gb, 256, 0, c->stream>>>(PP);
         else oz_resid_b_kernel<0><<<gb, 256, 0, c->stream>>>(PP);
         check_launch(c, "oz_resid_b_kernel");
@@ -1080,7 +1082,8 @@ void ozaki_product_many(rrsvd_b200_ctx* c, GemmOp op, const std::vector<OzProduc
         }
         check_launch(c, "oz_gemm_kernel");
         const int gx = (int)std::min<long long>((max_el + 255) / 256, 8 * kNumSMs);
-        if (T == 14) oz_crt_kernel<14><<<dim3(gx, cnt), 256, 0, c->stream>>>(CP);
+        if (T == 15) oz_crt_kernel<15><<<dim3(gx, cnt), 256, 0, c->stream>>>(CP);
+        else if (T == 14) oz_crt_kernel<14><<<dim3(gx, cnt), 256, 0, c->stream>>>(CP);
         else if (T == 16) oz_crt_kernel<16><<<dim3(gx, cnt), 256, 0, c->stream>>>(CP);
         else oz_crt_kernel<0><<<dim3(gx, cnt), 256, 0, c->stream>>>(CP);
         check_launch(c, "oz_crt_kernel");

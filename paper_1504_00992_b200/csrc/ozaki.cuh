@@ -46,11 +46,11 @@ struct OzakiA {
 };
 
 // Moduli count for the emulated A-products: RRSVD_B200_OZAKI (0 = off, every A-product on the DMMA
-// zgemm; 8..16), default 14.  ozaki_usable: the shape gate of the RRSVD paths.
+// zgemm; 8..16), default 15.  ozaki_usable: the shape gate of the RRSVD paths.
 int ozaki_moduli();
 bool ozaki_usable(int m, int n, int l);
-// RRSVD_B200_OZAKI_TAIL: how many of the RRSVD's last A-products stay on the FP64 zgemm — 1: the
-// assembly B^H = A^H Q; 2 (default): also the final Y = A Q~ of the power iteration; 0: none.
+// RRSVD_B200_OZAKI_TAIL: how many of the RRSVD's last A-products stay on the FP64 zgemm — 0
+// (default): none; 1: the assembly B^H = A^H Q; 2: also the final Y = A Q~ of the power iteration.
 int ozaki_tail();
 
 struct OzSrc {

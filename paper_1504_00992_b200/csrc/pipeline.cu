@@ -663,13 +663,18 @@ void range_finder_many(rrsvd_b200_ctx* c, const std::vector<RangeSpec>& specs) {
         os.push_back({b[i].Y, s.m, s.l, s.Q});
     }
     ap.run(c, kOpN);
-    // Only the last Q (the basis B = Q^H A is built on) must be orthonormal; the intermediate
-    // bases of the power iteration carry just their span, so they stop after the two shifted
-    // passes (cond <= ~1e5 even for rank-deficient input; one shifted pass is NOT enough: it
-    // leaves directions below ~1e-7·σ1 attenuated by σ/sqrt(shift), and the next product with
-    // A pushes them under roundoff).  With q = 0 this Q is the last one; a batch with mixed q
-    // keeps full passes throughout.
-    const int inter = min_q == max_q ? kSpanPasses : kFullPasses;
+    // Every basis of the power iteration gets the full adaptive schedule (shifted | [ill] shifted,
+    // plain | plain).  The span-only schedule (the two shifted passes) leaves an ill-conditioned
+    // Q~ on rank-deficient Θ — cond 3e14 measured on a TEDOPA bond (tools/oz_chol_probe.py) —
+    // whose tail directions the next product then resolves only by luck of its rounding: the
+    // kept λ tail came out 25 % low, and with the emulated (exactly rounded) products the final
+    // CholeskyQR lost 19 directions.  With orthonormal intermediate bases every A-product path
+    // reproduces the exact SVD's tail.  RRSVD_B200_SPAN_PASSES=1 restores the span schedule.
+    static const bool span_only = [] {
+        const char* e = std::getenv("RRSVD_B200_SPAN_PASSES");
+        return e != nullptr && std::atoi(e) != 0;
+    }();
+    const int inter = span_only && min_q == max_q ? kSpanPasses : kFullPasses;
     orth_many(c, os, max_q > 0 ? inter : kFullPasses);
     for (int j = 0; j < max_q; ++j) {
         os.clear();

@@ -7,8 +7,9 @@ default, so an A/B switch can never hide a wrong result.
     vs numpy, the reference's cblas_zgemm contract (linalg.cpp:20-40);
   * block Jacobi: the persistent sweep kernel (forced with RRSVD_B200_BJ_S=1) vs one launch per
     tournament step — singular values vs LAPACK (the reference's svd_full, linalg.cpp:67-88);
-  * the RRSVD A-products: FP64 DMMA only (RRSVD_B200_OZAKI=0), the INT8 emulation with 14
-    (default) or 16 moduli, and with every product emulated (RRSVD_B200_OZAKI_TAIL=0) — the
+  * the RRSVD A-products: FP64 DMMA only (RRSVD_B200_OZAKI=0), the INT8 emulation with 15
+    (default), 14 or 16 moduli, with the last two products on DMMA (RRSVD_B200_OZAKI_TAIL=2), and
+    the span-only schedule for the power iteration's bases (RRSVD_B200_SPAN_PASSES=1) — the
     headline decimation vs the reference's decimate (tebd.cpp:141-237).
 """
 import json
@@ -121,8 +122,8 @@ def test_block_jacobi_variants(env):
         assert ds <= 1e-13 and recon <= 1e-12 and orth <= 1e-12, (env, shape, ds, recon, orth)
 
 
-@pytest.mark.parametrize("env", [{"RRSVD_B200_OZAKI": "0"}, {}, {"RRSVD_B200_OZAKI": "16"},
-                                 {"RRSVD_B200_OZAKI_TAIL": "0"}, {"RRSVD_B200_OZAKI_TAIL": "1"}])
+@pytest.mark.parametrize("env", [{"RRSVD_B200_OZAKI": "0"}, {}, {"RRSVD_B200_OZAKI": "16"}, {"RRSVD_B200_OZAKI": "14"},
+                                 {"RRSVD_B200_OZAKI_TAIL": "2"}, {"RRSVD_B200_SPAN_PASSES": "1"}])
 def test_rrsvd_a_product_paths(env):
     """The headline decimation (2000 x 2000 Θ, RRSVD k = 100, p = 10, q = 2, reference Ω) with the
     A-products on the DMMA zgemm or on the INT8 emulation: chi equal, λ and w within 1e-10 of the

@@ -92,3 +92,72 @@ for name, pr, ph in (("numpy", lambda x: a @ x, lambda x: a.conj().T @ x),
 r = P.rrsvd_fixed_rank(a, 100, 10, 2, 777, ctx=ctx)
 s = np.asarray(r.sigma)
 print("device fixed_rank sigma[88:100]/s1", np.array2string(s[88:100] / s[0], precision=2))
+
+
+def dev_pass(y, shift_scale):
+    g = P.gemm(y, True, y, ctx=ctx)
+    t, nd, ill = P.chol_inv(g, shift_scale, ctx=ctx, flags=True)
+    return P.gemm(y, False, t, ctx=ctx), nd, ill
+
+
+# the device passes on a Y from the numpy power iteration, final product DMMA vs emulated
+qt = None
+y = a @ om
+q, _ = np.linalg.qr(y)
+for _ in range(2):
+    qt, _ = np.linalg.qr(a.conj().T @ q)
+    q, _ = np.linalg.qr(a @ qt)
+for name, y in (("dmma", P.gemm(a, False, qt, ctx=ctx)), ("oz14", P.ozaki_gemm(a, False, qt, 14, ctx=ctx)),
+                ("oz16", P.ozaki_gemm(a, False, qt, 16, ctx=ctx)), ("numpy", a @ qt)):
+    sh = 10.0 * (m + 110)
+    y1, n1, i1 = dev_pass(y, sh)
+    y2, n2, i2 = dev_pass(y1, sh)
+    y3, n3, _ = dev_pass(y2, 0.0)
+    y4, n4, _ = dev_pass(y3, 0.0)
+    print(f"device passes on Y[{name}]: dead {n1} {n2} {n3} {n4}, ill {i1} {i2}; cond(y2) {np.linalg.cond(y2):.2e}")
+
+
+def span_orth(y, rows):
+    sh = 10.0 * (rows + 110)
+    y1, _, ill = dev_pass(y, sh)
+    if ill:
+        y1, _, _ = dev_pass(y1, sh)
+    return y1
+
+
+def full_orth(y, rows):
+    sh = 10.0 * (rows + 110)
+    y1, n1, ill = dev_pass(y, sh)
+    if ill:
+        y1, n2, _ = dev_pass(y1, sh)
+        y1, n3, _ = dev_pass(y1, 0.0)
+    y1, n4, _ = dev_pass(y1, 0.0)
+    return y1, (n1, n4)
+
+
+oz = lambda x: P.ozaki_gemm(a, False, x, 14, ctx=ctx)  # noqa: E731
+ozh = lambda x: P.ozaki_gemm(a, True, x, 14, ctx=ctx)  # noqa: E731
+dm = lambda x: P.gemm(a, False, x, ctx=ctx)  # noqa: E731
+q = span_orth(oz(om), m)
+for j in range(2):
+    qt = span_orth(ozh(q), a.shape[1])
+    print(f"  Q~ (span orth) cond {np.linalg.cond(qt):.2e}")
+    if j == 1:
+        for name, f in (("dmma", dm), ("oz14", oz), ("numpy", lambda x: a @ x)):
+            qf, nd = full_orth(f(qt), m)
+            s = np.linalg.svd(P.gemm(a, True, qf, ctx=ctx), compute_uv=False)
+            print(f"device-pipeline final Y[{name}]: dead {nd}, sigma(B)[90:100]/s1 {np.array2string(s[90:100] / s[0], precision=2)}")
+    q = span_orth(oz(qt), m)
+
+print("--- intermediate bases with the full schedule")
+q, _ = full_orth(oz(om), m)
+for j in range(2):
+    qt, _ = full_orth(ozh(q), a.shape[1])
+    print(f"  Q~ (full orth) cond {np.linalg.cond(qt):.2e}")
+    if j == 1:
+        for name, f, fh in (("dmma", dm, lambda x: P.gemm(a, True, x, ctx=ctx)), ("oz14", oz, ozh),
+                            ("oz16", lambda x: P.ozaki_gemm(a, False, x, 16, ctx=ctx), lambda x: P.ozaki_gemm(a, True, x, 16, ctx=ctx))):
+            qf, nd = full_orth(f(qt), m)
+            s = np.linalg.svd(fh(qf), compute_uv=False)
+            print(f"full-orth pipeline final Y+B[{name}]: dead {nd}, sigma(B)[90:100]/s1 {np.array2string(s[90:100] / s[0], precision=2)}")
+    q, _ = full_orth(oz(qt), m)
