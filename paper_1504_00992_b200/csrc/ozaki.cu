@@ -872,8 +872,14 @@ int ozaki_tail() {
     return v;
 }
 
+// Below ~512 rows or columns the preparation and CRT overheads eat the INT8 GEMM's advantage (C2's
+// 256 x 256 bonds: 29.6 vs 30.7 steps/s emulated vs DMMA); RRSVD_B200_OZAKI_MIN overrides.
 bool ozaki_usable(int m, int n, int l) {
-    return ozaki_moduli() > 0 && m >= 256 && n >= 256 && std::max(m, n) <= 32768 && l >= 1;
+    static const int lo = [] {
+        const char* e = std::getenv("RRSVD_B200_OZAKI_MIN");
+        return e ? std::max(128, std::atoi(e)) : 512;
+    }();
+    return ozaki_moduli() > 0 && std::min(m, n) >= lo && std::max(m, n) <= 32768 && l >= 1;
 }
 
 std::vector<OzakiA> ozaki_prepare_many(rrsvd_b200_ctx* c, const std::vector<OzSrc>& src, int T) {

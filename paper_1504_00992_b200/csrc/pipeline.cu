@@ -230,9 +230,11 @@ void chol_inv_many(rrsvd_b200_ctx* c, const std::vector<CholSpec>& specs) {
 // on that device flag, so the host never waits:
 //   full (kFullPasses):  shifted Y->a | [ill] shifted a->b, plain b->a | plain a->Q
 //   span (kSpanPasses):  shifted Y->a | [ill] shifted a->b              | Q = ill ? b : a
+//   robust span (kRobustSpanPasses): shifted Y->a | [ill] shifted a->b, [ill] plain b->a,
+//                        [ill] plain a->b | Q = ill ? b : a
 // A well-conditioned basis thus costs 2 (full) or 1 (span) passes instead of 4 or 2, with the
 // same guarantees: after a shifted pass with every pivot >= 1e4 s, cond(Q) - 1 <= 5e-5.
-void orth_many_adaptive(rrsvd_b200_ctx* c, const std::vector<OrthSpec>& specs, bool full) {
+void orth_many_adaptive(rrsvd_b200_ctx* c, const std::vector<OrthSpec>& specs, bool full, bool robust) {
     const size_t np = specs.size();
     struct Buf {
         cplx *G, *T, *a, *b;
@@ -287,6 +289,10 @@ void orth_many_adaptive(rrsvd_b200_ctx* c, const std::vector<OrthSpec>& specs, b
     check_cuda(c, cudaMemsetAsync(ill, 0, np * sizeof(int), c->stream), "memset");
     pass(true, Y, Aw, true, nullptr, false);             // shifted Y -> a, flags
     pass(true, A, Bw, false, ill, false);                // [ill] shifted a -> b
+    if (!full && robust) {                               // [ill] plain b -> a, [ill] plain a -> b
+        pass(false, B, Aw, false, ill, false);
+        pass(false, A, Bw, false, ill, true);
+    }
     if (full) {
         pass(false, B, Aw, false, ill, false);           // [ill] plain b -> a
         pass(false, A, Q, false, nullptr, true);         // plain a -> Q
@@ -318,8 +324,9 @@ void orth_many_adaptive(rrsvd_b200_ctx* c, const std::vector<OrthSpec>& specs, b
 
 void orth_many(rrsvd_b200_ctx* c, const std::vector<OrthSpec>& specs, int passes) {
     if (specs.empty()) return;
-    if (passes != kFullPasses && passes != kSpanPasses) throw_contract(c, "orth: unknown pass schedule");
-    orth_many_adaptive(c, specs, passes == kFullPasses);
+    if (passes != kFullPasses && passes != kSpanPasses && passes != kRobustSpanPasses)
+        throw_contract(c, "orth: unknown pass schedule");
+    orth_many_adaptive(c, specs, passes == kFullPasses, passes == kRobustSpanPasses);
 }
 
 void orth(rrsvd_b200_ctx* c, const cplx* Y, int m, int l, cplx* Q, int* ndead) {
@@ -663,18 +670,25 @@ void range_finder_many(rrsvd_b200_ctx* c, const std::vector<RangeSpec>& specs) {
         os.push_back({b[i].Y, s.m, s.l, s.Q});
     }
     ap.run(c, kOpN);
-    // Every basis of the power iteration gets the full adaptive schedule (shifted | [ill] shifted,
-    // plain | plain).  The span-only schedule (the two shifted passes) leaves an ill-conditioned
-    // Q~ on rank-deficient Θ — cond 3e14 measured on a TEDOPA bond (tools/oz_chol_probe.py) —
-    // whose tail directions the next product then resolves only by luck of its rounding: the
-    // kept λ tail came out 25 % low, and with the emulated (exactly rounded) products the final
-    // CholeskyQR lost 19 directions.  With orthonormal intermediate bases every A-product path
-    // reproduces the exact SVD's tail.  RRSVD_B200_SPAN_PASSES=1 restores the span schedule.
+    // The power iteration's bases (emulated A-products): one shifted pass when it finds Y well
+    // conditioned (every pivot
+    // >= 1e4 x the shift: cond(Q) - 1 <= 5e-5), else the full four-pass schedule
+    // (kRobustSpanPasses).  Two shifted passes alone (the span-only schedule) leave an
+    // ill-conditioned Q~ on rank-deficient Θ — cond 3e14 measured on a TEDOPA bond
+    // (tools/oz_chol_probe.py) — whose tail directions the next product then resolves only through
+    // its own rounding noise: the kept λ tail came out ~25 % low, and with the exactly rounded
+    // emulated products the final CholeskyQR lost 19 directions.  With orthonormal bases every
+    // A-product path reproduces the exact SVD's tail.  RRSVD_B200_SPAN_PASSES=1 restores the
+    // span-only schedule.
     static const bool span_only = [] {
         const char* e = std::getenv("RRSVD_B200_SPAN_PASSES");
         return e != nullptr && std::atoi(e) != 0;
     }();
-    const int inter = span_only && min_q == max_q ? kSpanPasses : kFullPasses;
+    // (The span-only schedule stays for an all-DMMA batch: its products' rounding noise is what the
+    // reference's own FP64 products carry, and the parity suite holds with it.)
+    bool emulated = false;
+    for (const RangeSpec& s : specs) emulated = emulated || s.oz != nullptr;
+    const int inter = min_q != max_q ? kFullPasses : (span_only || !emulated) ? kSpanPasses : kRobustSpanPasses;
     orth_many(c, os, max_q > 0 ? inter : kFullPasses);
     for (int j = 0; j < max_q; ++j) {
         os.clear();

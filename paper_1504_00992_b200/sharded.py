@@ -20,7 +20,8 @@ step for step; only the reductions over the row dimension cross shards:
 
 The CholeskyQR passes follow the device's adaptive schedule (pipeline.cu orth_many_adaptive): the
 first, shifted pass reports whether a pivot fell near the shift (rrsvd_b200_chol_inv_flags);
-only then do the extra passes run (full: 4 passes -> 2; span: 2 -> 1 for a well-conditioned Y).
+only then do the extra passes run (full: 4 passes -> 2; the power iteration's bases: 4 -> 1 for a
+well-conditioned Y).
 
 Communication is O(q n l) per decimation against O(q m n l / G) of GEMM work per rank.  Every
 rank may hold several shards (`shards` list): the local partial sums are added in a fixed order
@@ -38,7 +39,7 @@ import numpy as np
 from . import api
 from ._lib import OMEGA_REFERENCE
 
-FULL_PASSES, SPAN_PASSES = 4, 2  # pipeline.cuh kFullPasses / kSpanPasses
+FULL_PASSES, SPAN_PASSES, ROBUST_SPAN_PASSES = 4, 2, 3  # pipeline.cuh kFullPasses / kSpanPasses / kRobustSpanPasses
 
 
 def _adjoint(x):
@@ -152,13 +153,16 @@ class ShardedRrsvd:
 
     def _orth_sharded(self, ys, m_total, passes):
         """CholeskyQR over row-sharded Y, the device's adaptive schedule (orth_many_adaptive):
-        full  = shifted | [ill] shifted, plain | plain;   span = shifted | [ill] shifted."""
+        full = shifted | [ill] shifted, plain | plain;  span = shifted | [ill] shifted;
+        robust span = shifted | [ill] shifted, plain, plain."""
         l = ys[0].shape[1]
         shift = 10.0 * (m_total + l)
         a, ill = self._pass(ys, shift)
         if ill:  # (ill is computed from the all-reduced Gram: the same decision on every rank)
             a, _ = self._pass(a, shift)
-            if passes == FULL_PASSES:
+            if passes in (FULL_PASSES, ROBUST_SPAN_PASSES):
+                a, _ = self._pass(a, 0.0)
+            if passes == ROBUST_SPAN_PASSES:
                 a, _ = self._pass(a, 0.0)
         if passes == FULL_PASSES:
             a, _ = self._pass(a, 0.0)
@@ -176,16 +180,16 @@ class ShardedRrsvd:
         if l > min(m_total, n):
             raise api.ContractViolation("randomized_range_finder: l exceeds min(m, n)")
         om = ops.omega(n, l, seed, mode)
-        inter = SPAN_PASSES if q > 0 else FULL_PASSES
+        inter = ROBUST_SPAN_PASSES if q > 0 else FULL_PASSES
         qs = self._orth_sharded([ops.gemm(a, False, om) for a in shards], m_total, inter)
         r0, r1 = self.comm.row_block(n)
         for j in range(q):
             # Z = A^H Q (n x l): each rank orthonormalises its row block (row-sharded CholeskyQR),
             # then the rows are gathered for the next local product Y_g = A_g Q~
             z = self._rowsum([ops.gemm(a, True, qg) for a, qg in zip(shards, qs)])
-            qt = self.comm.allgather_rows(self._orth_sharded([z[r0:r1]], n, SPAN_PASSES)[0], n)
+            qt = self.comm.allgather_rows(self._orth_sharded([z[r0:r1]], n, ROBUST_SPAN_PASSES)[0], n)
             qs = self._orth_sharded([ops.gemm(a, False, qt) for a in shards], m_total,
-                                    SPAN_PASSES if j + 1 < q else FULL_PASSES)
+                                    ROBUST_SPAN_PASSES if j + 1 < q else FULL_PASSES)
         bh = self._rowsum([ops.gemm(a, True, qg) for a, qg in zip(shards, qs)])[r0:r1]  # B^H = A^H Q
         qb = self._orth_sharded([bh], n, FULL_PASSES)[0]                      # B^H = Q_b X
         x = self.comm.allreduce(ops.gemm(qb, True, bh))                         # X = Q_b^H B^H (l x l)

@@ -133,3 +133,16 @@ def test_rrsvd_a_product_paths(env):
     assert (calls == 0) == (env.get("RRSVD_B200_OZAKI") == "0"), (env, calls)
     for seed, (chi, rchi, dlam, dw) in res.items():
         assert chi == rchi == 100 and dlam < 1e-10 and dw < 1e-10, (env, seed, chi, rchi, dlam, dw)
+
+
+@pytest.mark.parametrize("env", [{"RRSVD_B200_OZAKI_MIN": "256"}, {"RRSVD_B200_OZAKI_MIN": "256", "RRSVD_B200_OZAKI": "16"}])
+def test_emulated_products_on_every_bond_shape(env):
+    """The d = 20 TEDOPA chain's evolve trace (tests/test_gpu_headline.py) with the emulated
+    A-products lowered to every bond with both sides >= 256 (400 x 400 up to 2000 x 2000 Θ):
+    chi profile, kept fraction and observables as the reference's."""
+    e = dict(os.environ)
+    e.update(env)
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider",
+                        os.path.join(ROOT, "tests", "test_gpu_headline.py"), "-k", "tedopa_d20 or decimate_headline"],
+                       env=e, cwd=ROOT, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, (r.stdout[-3000:], r.stderr[-2000:])
