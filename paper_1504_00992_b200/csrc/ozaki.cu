@@ -872,6 +872,14 @@ int ozaki_tail() {
     return v;
 }
 
+double ozaki_min_work() {
+    static const double v = [] {
+        const char* e = std::getenv("RRSVD_B200_OZAKI_MIN_WORK");
+        return e ? std::atof(e) : 8.0e6;
+    }();
+    return v;
+}
+
 // Below ~512 rows or columns the preparation and CRT overheads eat the INT8 GEMM's advantage (C2's
 // 256 x 256 bonds: 29.6 vs 30.7 steps/s emulated vs DMMA); RRSVD_B200_OZAKI_MIN overrides.
 bool ozaki_usable(int m, int n, int l) {
@@ -1076,7 +1084,11 @@ void ozaki_product_many(rrsvd_b200_ctx* c, GemmOp op, const std::vector<OzProduc
         else oz_resid_b_kernel<0><<<gb, 256, 0, c->stream>>>(PP);
         check_launch(c, "oz_resid_b_kernel");
         if (oz_persistent()) {
-            const int grid = std::min(ntiles, kNumSMs);
+            static const int cap = [] {  // RRSVD_B200_OZAKI_GRID: CTAs of the persistent GEMM (A/B)
+                const char* e = std::getenv("RRSVD_B200_OZAKI_GRID");
+                return e ? std::max(1, std::min(kNumSMs, std::atoi(e))) : kNumSMs;
+            }();
+            const int grid = std::min(ntiles, cap);
             if (op == kOpN)
                 oz_gemm_persistent_kernel<kOpN><<<grid, kPThreads, kPSmem, c->stream>>>(G);
             else

@@ -49,6 +49,8 @@ struct OzakiA {
 // zgemm; 8..16), default 15.  ozaki_usable: the shape gate of the RRSVD paths.
 int ozaki_moduli();
 bool ozaki_usable(int m, int n, int l);
+// Least total A entries (sum of m·n over a batch) for the emulation (RRSVD_B200_OZAKI_MIN_WORK, 8e6).
+double ozaki_min_work();
 // RRSVD_B200_OZAKI_TAIL: how many of the RRSVD's last A-products stay on the FP64 zgemm — 0
 // (default): none; 1: the assembly B^H = A^H Q; 2: also the final Y = A Q~ of the power iteration.
 int ozaki_tail();

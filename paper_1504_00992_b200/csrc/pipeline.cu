@@ -774,8 +774,13 @@ void rrsvd_core_many(rrsvd_b200_ctx* c, const std::vector<RrsvdSpec>& specs) {
             src.push_back({specs[i].A, specs[i].m, specs[i].n, (long long)specs[i].n});
             which.push_back((int)i);
         }
+    // a batch too small to fill the GPU's HBM stream (single C1 / C5 n <= ~2000 decimations) keeps
+    // the DMMA zgemm: its A preparation and residue/CRT launches would add latency, not save time
+    double work = 0.0;
+    for (const OzSrc& s : src) work += (double)s.m * s.n;
     std::vector<OzakiA> oz;
-    if (!src.empty()) oz = ozaki_prepare_many(c, src, T);
+    if (!src.empty() && work >= ozaki_min_work()) oz = ozaki_prepare_many(c, src, T);
+    else which.clear();
     std::vector<const OzakiA*> ozp(specs.size(), nullptr);
     for (size_t j = 0; j < which.size(); ++j) ozp[which[j]] = &oz[j];
     for (size_t i = 0; i < specs.size(); ++i) {

@@ -128,14 +128,15 @@ def test_rrsvd_a_product_paths(env):
     """The headline decimation (2000 x 2000 Θ, RRSVD k = 100, p = 10, q = 2, reference Ω) with the
     A-products on the DMMA zgemm or on the INT8 emulation: chi equal, λ and w within 1e-10 of the
     reference; the emulation really ran unless switched off."""
-    res = run_variant(DEC_SCRIPT, env)
+    res = run_variant(DEC_SCRIPT, {"RRSVD_B200_OZAKI_MIN_WORK": "0", **env})  # (a single 2000^2 decimation)
     calls = res.pop("oz_calls")
     assert (calls == 0) == (env.get("RRSVD_B200_OZAKI") == "0"), (env, calls)
     for seed, (chi, rchi, dlam, dw) in res.items():
         assert chi == rchi == 100 and dlam < 1e-10 and dw < 1e-10, (env, seed, chi, rchi, dlam, dw)
 
 
-@pytest.mark.parametrize("env", [{"RRSVD_B200_OZAKI_MIN": "256"}, {"RRSVD_B200_OZAKI_MIN": "256", "RRSVD_B200_OZAKI": "16"}])
+@pytest.mark.parametrize("env", [{"RRSVD_B200_OZAKI_MIN": "256", "RRSVD_B200_OZAKI_MIN_WORK": "0"},
+                                 {"RRSVD_B200_OZAKI_MIN": "256", "RRSVD_B200_OZAKI_MIN_WORK": "0", "RRSVD_B200_OZAKI": "16"}])
 def test_emulated_products_on_every_bond_shape(env):
     """The d = 20 TEDOPA chain's evolve trace (tests/test_gpu_headline.py) with the emulated
     A-products lowered to every bond with both sides >= 256 (400 x 400 up to 2000 x 2000 Θ):
