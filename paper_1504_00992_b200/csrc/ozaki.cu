@@ -140,7 +140,8 @@ struct PrepParams {
 };
 
 // Row exponents (a warp per row), then column exponents of the row-normalised A (each near the
-// HBM roofline; a one-pass form with shared-memory column atomics measured slower)
+// HBM roofline; one-pass forms — shared-memory column atomics per element, or per-lane column
+// maxima in registers at one CTA per SM — measured 1.0 and 3.0 ms vs 1.04 ms for 48 bonds)
 __global__ void __launch_bounds__(256) oz_rowexp_kernel(const __grid_constant__ PrepParams P) {
     const int z = blockIdx.y;
     const int m = P.m[z], n = P.n[z];
@@ -202,6 +203,53 @@ __device__ __forceinline__ void oz_store8(const double (&vr)[8], const double (&
     *reinterpret_cast<uint2*>(dst + plane) = make_uint2(pi[0], pi[1]);
 }
 
+// residues of an integer-valued double v (|v| <= 2^52) modulo MA and MB: r = v mod MA·MB exactly
+// (shifter-rounded FP64 quotient, exact FMA remainder, |r| <= MA·MB/2 + 1 < 2^22), then each
+// residue in FP32 (r/M needs only ~2^-16 accuracy to round exactly: no ties for odd M, and for
+// M = 256 the tie ±128 is one byte) — half the FP64 work of two direct reductions.
+template <int M>
+__device__ __forceinline__ uint32_t oz_res32(float f) {
+    const float sh = 12582912.0f;  // 1.5·2^23
+    const float q = fmaf(f, 1.0f / (float)M, sh) - sh;
+    const float r = fmaf(-q, (float)M, f);
+    return (uint32_t)__float_as_int(r + sh) & 0xffu;
+}
+template <int MA, int MB>
+__device__ __forceinline__ void oz_store8_pair(const double (&vr)[8], const double (&vi)[8], int8_t* dst, long long plane) {
+    constexpr double P = (double)MA * (double)MB;
+    const double sh = 6755399441055744.0;
+    uint32_t ar[2] = {0, 0}, ai[2] = {0, 0}, br[2] = {0, 0}, bi[2] = {0, 0};
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+#pragma unroll
+        for (int part = 0; part < 2; ++part) {
+            const double v = part == 0 ? vr[u] : vi[u];
+            const double q = fma(v, 1.0 / P, sh) - sh;
+            const int ri = __double2loint(fma(-q, P, v) + sh);
+            const float f = __int_as_float(ri + 0x4B400000) - 12582912.0f;
+            const uint32_t ra = oz_res32<MA>(f), rb = oz_res32<MB>(f);
+            const int w = u >> 2, sft = 8 * (u & 3);
+            if (part == 0) { ar[w] |= ra << sft; br[w] |= rb << sft; }
+            else { ai[w] |= ra << sft; bi[w] |= rb << sft; }
+        }
+    }
+    *reinterpret_cast<uint2*>(dst) = make_uint2(ar[0], ar[1]);
+    *reinterpret_cast<uint2*>(dst + plane) = make_uint2(ai[0], ai[1]);
+    *reinterpret_cast<uint2*>(dst + 2 * plane) = make_uint2(br[0], br[1]);
+    *reinterpret_cast<uint2*>(dst + 3 * plane) = make_uint2(bi[0], bi[1]);
+}
+
+template <int TT, int t>
+__device__ __forceinline__ void oz_store_pairs(const double (&vr)[8], const double (&vi)[8], int8_t* dst, long long plane) {
+    if constexpr (t + 1 < TT) {
+        oz_store8_pair<oz_modulus(t), oz_modulus(t + 1)>(vr, vi, dst + (long long)(2 * t) * plane, plane);
+        oz_store_pairs<TT, t + 2>(vr, vi, dst, plane);
+    } else if constexpr (t < TT) {
+        oz_store8(vr, vi, dst + (long long)(2 * t) * plane, plane, oz_modulus(t), 1.0 / (double)oz_modulus(t),
+                  -(oz_modulus(t) / 2));
+    }
+}
+
 // one thread = 8 consecutive columns of one (padded) row, both parts, all T moduli (TT > 0: the
 // moduli count as a compile-time constant, every modulus an immediate)
 template <int TT>
@@ -234,11 +282,8 @@ __global__ void __launch_bounds__(256) oz_resid_a_kernel(const __grid_constant__
         }
         int8_t* dst = res + ((long long)(row >> 7) * nkb + (c0 >> 7)) * 16384 + (row & 127) * 128 + (c0 & 127);
         if (TT > 0) {
-#pragma unroll
-            for (int t = 0; t < (TT > 0 ? TT : 1); ++t) {
-                const int md = oz_modulus(t);
-                oz_store8(vr, vi, dst + (long long)(2 * t) * plane, plane, md, 1.0 / (double)md, -(md / 2));
-            }
+            // moduli in pairs: one FP64 reduction modulo m_a·m_b (< 2^16), the two residues in FP32
+            oz_store_pairs<TT, 0>(vr, vi, dst, plane);
         } else {
             for (int t = 0; t < P.k.T; ++t)
                 oz_store8(vr, vi, dst + (long long)(2 * t) * plane, plane, P.k.mod[t], P.k.inv_md[t], P.k.lo[t]);

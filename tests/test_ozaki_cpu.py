@@ -125,3 +125,34 @@ def test_two_sided_equilibration_bounds():
     g = np.ldexp(1.0, kA - int(e_el.max()))
     glob = (np.rint(a.real * g) + 1j * np.rint(a.imag * g)) / g
     assert np.max(np.abs(glob - a) / mag) > 1e3 * np.max(rel)
+
+
+def _f32(x):
+    return np.float32(x)
+
+
+@pytest.mark.parametrize("T", [14, 15, 16])
+def test_paired_residues(T):
+    """oz_store8_pair: r = v mod m_a·m_b by a shifter-rounded FP64 quotient and an exact remainder,
+    then each residue in FP32 (fmaf rounds once: emulated here by an FP64 sum rounded to FP32)
+    — the byte equals the symmetric residue of v for every modulus of the pair."""
+    rng = np.random.default_rng(T)
+    sh64 = 6755399441055744.0
+    sh32 = np.float32(12582912.0)
+    vals = [float(x) for x in rng.integers(-(2 ** 52), 2 ** 52, 4000, dtype=np.int64)]
+    vals += [0.0, 2.0 ** 52, -(2.0 ** 52), 32640.0, -32640.0, 65280.0 * 12345 + 32640, -(65280.0 * 777 + 32640)]
+    for t in range(0, T - 1, 2):
+        ma, mb = MODULI[t], MODULI[t + 1]
+        P = float(ma * mb)
+        for v in vals:
+            q = (v * (1.0 / P) + sh64) - sh64          # |v/P| < 2^37: the FP64 product's rounding is below 2^-15
+            r = v - q * P                              # exact (an FMA on the device)
+            assert abs(r) <= P / 2 + 1
+            f = np.float32(r)
+            for m in (ma, mb):
+                qq = _f32(np.float64(f) * np.float64(np.float32(1.0 / m)) + np.float64(sh32)) - sh32
+                rr = np.float32(np.float64(f) - np.float64(qq) * m)
+                assert abs(rr) <= m / 2
+                byte = int(rr) & 0xFF
+                want = sym_res(int(v), m) & 0xFF
+                assert byte == want, (v, m, rr, sym_res(int(v), m))

@@ -1,6 +1,6 @@
 # one iteration on the emulated A-products: unit + headline parity, C3 bench A/B, launch list of a serial step
 set -u
-T=${OZ_T:-14}
+T=${OZ_T:-15}
 timeout 300 python -m pytest tests/test_gpu_ozaki.py -x -q 2>&1 | tail -1 | sed 's/^/ozaki unit: /'
 RRSVD_B200_OZAKI=$T timeout 600 python -m pytest tests/test_gpu_headline.py -x -q 2>&1 | tail -1 | sed "s/^/headline T=$T: /"
 for o in 0 $T; do
