@@ -96,7 +96,18 @@ def workload(name: str):
     raise SystemExit(f"unknown workload {name}")
 
 
-def emulated_entry(flops, ms, nbytes, calls, prep_ms, prep_bytes) -> dict:
+def measured_hbm_peak():
+    """HBM copy bandwidth from MEASURED_PEAKS.json (driver-written), else the profiling guide's
+    fallback (6.65 TB/s)."""
+    try:
+        with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "MEASURED_PEAKS.json")) as f:
+            v = float(json.load(f)["hbm_gbs"])
+        return v, "MEASURED_PEAKS.json hbm_gbs (copy bandwidth, read+write bytes)"
+    except Exception:
+        return 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md; MEASURED_PEAKS.json absent)"
+
+
+def emulated_entry(flops, ms, nbytes, calls, prep_ms, prep_bytes, gemm_ms=0.0, gemm_bytes=0.0) -> dict:
     """The RRSVD A-products on the INT8 tensor cores (csrc/ozaki.cuh), from the serial roofline pass:
     kept out of the DMMA roofline above (its `frac` covers the FP64 zgemm launches only)."""
     moduli = int(os.environ.get("RRSVD_B200_OZAKI", "15") or 0)
@@ -112,6 +123,15 @@ def emulated_entry(flops, ms, nbytes, calls, prep_ms, prep_bytes) -> dict:
                                            "the FP64 DMMA zgemm, RRSVD_B200_OZAKI_TAIL)"),
             "ms_per_step": round(ms, 3), "fp64_equivalent_tflops": round(flops / (ms * 1e-3) / 1e12, 2),
             "algorithmic_GBps": round(nbytes / (ms * 1e-3) / 1e9, 1), "launch_groups": int(calls),
+            "int8_gemm_roofline": ({"bound": "hbm", "kernel": "oz_gemm_persistent_kernel (tcgen05.mma kind::i8)",
+                                    "achieved": round(gemm_bytes / (gemm_ms * 1e-3) / 1e9, 1),
+                                    "peak": measured_hbm_peak()[0], "unit": "GB/s",
+                                    "frac": round(gemm_bytes / (gemm_ms * 1e-3) / 1e9 / measured_hbm_peak()[0], 4),
+                                    "peak_source": measured_hbm_peak()[1],
+                                    "traffic_note": "achieved counts the algorithmic bytes (A residue tiles + panel "
+                                                    "read, residue products written) over the event-timed launches; "
+                                                    "ncu DRAM bytes in profiles/r02_ozaki_summary.md",
+                                    "ms_per_step": round(gemm_ms, 3)} if gemm_ms > 0 else None),
             "a_preparation_ms_per_step": round(prep_ms, 3),
             "a_preparation_GBps": round(prep_bytes / (prep_ms * 1e-3) / 1e9, 1) if prep_ms > 0 else None,
             "note": "ms are event-timed per launch group (residue panel + INT8 GEMM + CRT) in the serial pass; "
@@ -456,6 +476,8 @@ def run_ours(args, rank, world, local_rank):
                                                C.c_double())
     ctx.check(lib.rrsvd_b200_ozaki_stats(ctx.h, C.byref(ofl), C.byref(oms), C.byref(obytes), C.byref(ocalls),
                                          C.byref(opms), C.byref(opbytes)))
+    ogms, ogbytes = C.c_double(), C.c_double()
+    ctx.check(lib.rrsvd_b200_ozaki_gemm_stats(ctx.h, C.byref(ogms), C.byref(ogbytes)))
     ctx.check(lib.rrsvd_b200_set_gemm_timing(ctx.h, 0))
     ctx.check(lib.rrsvd_b200_set_overlap(ctx.h, 1))
     stage_names = ["theta", "gate", "rrsvd_A_products", "qr_gram", "qr_apply", "svd_assembly", "det_precond"]
@@ -528,7 +550,7 @@ def run_ours(args, rank, world, local_rank):
                          "step_level_tflops": round(fl.value / (elapsed / args.steps) / 1e12, 3),
                          "gemm_launches": int(calls.value), "stages": stages, **traffic_entry(),
                          "emulated_a_products": emulated_entry(ofl.value, oms.value, obytes.value, ocalls.value,
-                                                               opms.value, opbytes.value)},
+                                                               opms.value, opbytes.value, ogms.value, ogbytes.value)},
             "e2e": {"value": round(e2e, 6), "unit": "steps/s", "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h), "steps": args.steps,
                     "note": "same consecutive steps as value; whole MPS H2D before and D2H after every step"},

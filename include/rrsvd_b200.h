@@ -341,6 +341,9 @@ int rrsvd_b200_gemm_stage_stats(rrsvd_b200_ctx* ctx, double* flops8, double* ms8
  * of the products; milliseconds and bytes of the A residue preparations. */
 int rrsvd_b200_ozaki_stats(rrsvd_b200_ctx* ctx, double* flops, double* ms, double* bytes, uint64_t* calls,
                            double* prep_ms, double* prep_bytes);
+/* The INT8 tensor-core GEMM kernel of the emulated products alone (event-timed around its launch):
+ * milliseconds and the HBM bytes it must move (A residue tiles + panel read, residue products written). */
+int rrsvd_b200_ozaki_gemm_stats(rrsvd_b200_ctx* ctx, double* ms, double* bytes);
 /* Measured device peak: what = 0 FP64 DMMA (mma.sync f64), 1 FP64 DFMA; TFLOP/s. */
 int rrsvd_b200_probe_peak(rrsvd_b200_ctx* ctx, int what, double* tflops);
 

@@ -634,6 +634,7 @@ int rrsvd_b200_set_gemm_timing(rrsvd_b200_ctx* c, int on) {
             c->gemm_calls = 0;
             c->oz_ms = c->oz_flops = c->oz_bytes = c->oz_prep_ms = c->oz_prep_bytes = 0.0;
             c->oz_calls = 0;
+            c->oz_gemm_ms = c->oz_gemm_bytes = 0.0;
             for (int i = 0; i < 8; ++i) c->tag_ms[i] = c->tag_flops[i] = 0.0;
         }
     });
@@ -666,6 +667,14 @@ int rrsvd_b200_ozaki_stats(rrsvd_b200_ctx* c, double* flops, double* ms, double*
         if (calls) *calls = c->oz_calls;
         if (prep_ms) *prep_ms = c->oz_prep_ms;
         if (prep_bytes) *prep_bytes = c->oz_prep_bytes;
+    });
+}
+
+int rrsvd_b200_ozaki_gemm_stats(rrsvd_b200_ctx* c, double* ms, double* bytes) {
+    return api(c, [&] {
+        flush_gemm_timing(c);
+        if (ms) *ms = c->oz_gemm_ms;
+        if (bytes) *bytes = c->oz_gemm_bytes;
     });
 }
 

@@ -158,6 +158,11 @@ void flush_gemm_timing(rrsvd_b200_ctx* c) {
         check_cuda(c, cudaEventElapsedTime(&ms, p.a, p.b), "event elapsed");
         c->event_pool.push_back(p.a);
         c->event_pool.push_back(p.b);
+        if (p.kind == 2) {
+            c->oz_gemm_ms += ms;
+            c->oz_gemm_bytes += p.bytes;
+            continue;
+        }
         if (p.kind == 1) {
             if (p.flops > 0) {
                 c->oz_ms += ms;

@@ -33,7 +33,8 @@ struct rrsvd_b200_ctx {
         double executed;  // what the DMMA pipe executes (6 per complex MAC in the 3M form)
         int tag;
         int tma;          // staged by TMA (1) or cp.async (0)
-        int kind = 0;     // 0: DMMA zgemm; 1: INT8 emulated A-product (ozaki.cuh) or its A preparation
+        int kind = 0;     // 0: DMMA zgemm; 1: INT8 emulated A-product (ozaki.cuh) or its A preparation;
+                          // 2: the INT8 tensor-core GEMM kernel of an emulated product alone
         double bytes = 0; // emulated launches: algorithmic HBM bytes
     };
     int gemm_tag = 0;              // category of the next zgemm launches (debug statistics)
@@ -53,6 +54,7 @@ struct rrsvd_b200_ctx {
     // the emulated A-products (kind 1), kept out of the DMMA counters: products, A preparation
     double oz_ms = 0.0, oz_flops = 0.0, oz_bytes = 0.0, oz_prep_ms = 0.0, oz_prep_bytes = 0.0;
     uint64_t oz_calls = 0;
+    double oz_gemm_ms = 0.0, oz_gemm_bytes = 0.0;
     uint64_t gemm_calls = 0;
 };
 

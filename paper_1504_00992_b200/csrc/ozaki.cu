@@ -1036,7 +1036,7 @@ void ozaki_product_many(rrsvd_b200_ctx* c, GemmOp op, const std::vector<OzProduc
             G.off[t] = k.off[t];
         }
         int max_cols = 8, max_mb = 1, max_jt = 1, max_k = 1;
-        double bytes = 0.0;
+        double bytes = 0.0, gemm_bytes = 0.0;
         long long max_el = 1;
         double flops = 0.0;
         for (int i = 0; i < cnt; ++i) {
@@ -1107,6 +1107,7 @@ void ozaki_product_many(rrsvd_b200_ctx* c, GemmOp op, const std::vector<OzProduc
             // X read; B' written + read; A residues read; residue products written + read; C written
             bytes += 16.0 * K * p.l + 2.0 * T * JT * 2 * nkbx * 2 * LT * 128 + 2.0 * T * a.nib * a.nkb * 16384 +
                      2.0 * T * Mr * ncol + 16.0 * Mr * p.l;
+            gemm_bytes += 2.0 * T * a.nib * a.nkb * 16384 + (double)T * JT * 2 * nkbx * 2 * LT * 128 + (double)T * Mr * ncol;
         }
         int ntiles = 0;
         for (int i = 0; i < cnt; ++i) {
@@ -1128,6 +1129,12 @@ void ozaki_product_many(rrsvd_b200_ctx* c, GemmOp op, const std::vector<OzProduc
         else if (T == 16) oz_resid_b_kernel<16><<<gb, 256, 0, c->stream>>>(PP);
         else oz_resid_b_kernel<0><<<gb, 256, 0, c->stream>>>(PP);
         check_launch(c, "oz_resid_b_kernel");
+        cudaEvent_t ga = nullptr, gb2 = nullptr;
+        if (c->gemm_timing) {
+            ga = pooled_event(c);
+            gb2 = pooled_event(c);
+            check_cuda(c, cudaEventRecord(ga, c->stream), "event record");
+        }
         if (oz_persistent()) {
             static const int cap = [] {  // RRSVD_B200_OZAKI_GRID: CTAs of the persistent GEMM (A/B)
                 const char* e = std::getenv("RRSVD_B200_OZAKI_GRID");
@@ -1144,6 +1151,10 @@ void ozaki_product_many(rrsvd_b200_ctx* c, GemmOp op, const std::vector<OzProduc
             oz_gemm_kernel<kOpC><<<dim3(max_mb, T * max_jt, cnt), kThreads, kGemmSmem, c->stream>>>(G);
         }
         check_launch(c, "oz_gemm_kernel");
+        if (c->gemm_timing) {
+            check_cuda(c, cudaEventRecord(gb2, c->stream), "event record");
+            c->pending.push_back({ga, gb2, 0.0, 0.0, c->gemm_tag, 1, 2, gemm_bytes});
+        }
         const int gx = (int)std::min<long long>((max_el + 255) / 256, 8 * kNumSMs);
         if (T == 15) oz_crt_kernel<15><<<dim3(gx, cnt), 256, 0, c->stream>>>(CP);
         else if (T == 14) oz_crt_kernel<14><<<dim3(gx, cnt), 256, 0, c->stream>>>(CP);
