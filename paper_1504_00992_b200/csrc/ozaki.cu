@@ -347,6 +347,46 @@ __global__ void __launch_bounds__(256) oz_xmax_kernel(const __grid_constant__ Pa
     }
 }
 
+// the panel's residues by moduli pairs (oz_store8_pair's arithmetic): four K rows of one column
+template <int TT, int t, int kPadW>
+__device__ __forceinline__ void oz_panel_pairs(const double (&vr)[4], const double (&vi)[4],
+                                               uint32_t (&S)[kOzMaxMod][8][2][kPadW], int c, int kq) {
+    if constexpr (t + 1 < TT) {
+        constexpr int MA = oz_modulus(t), MB = oz_modulus(t + 1);
+        constexpr double Pm = (double)MA * (double)MB;
+        const double sh = 6755399441055744.0;
+        uint32_t a0 = 0, a1 = 0, b0 = 0, b1 = 0;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+#pragma unroll
+            for (int part = 0; part < 2; ++part) {
+                const double v = part == 0 ? vr[u] : vi[u];
+                const double q = fma(v, 1.0 / Pm, sh) - sh;
+                const int ri = __double2loint(fma(-q, Pm, v) + sh);
+                const float f = __int_as_float(ri + 0x4B400000) - 12582912.0f;
+                const uint32_t ra = oz_res32<MA>(f) << (8 * u), rb = oz_res32<MB>(f) << (8 * u);
+                if (part == 0) { a0 |= ra; b0 |= rb; }
+                else { a1 |= ra; b1 |= rb; }
+            }
+        }
+        S[t][c][0][kq] = a0;
+        S[t][c][1][kq] = a1;
+        S[t + 1][c][0][kq] = b0;
+        S[t + 1][c][1][kq] = b1;
+        oz_panel_pairs<TT, t + 2, kPadW>(vr, vi, S, c, kq);
+    } else if constexpr (t < TT) {
+        constexpr int md = oz_modulus(t);
+        uint32_t a = 0, b = 0;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            a |= (uint32_t)(oz_res(vr[u], md, 1.0 / (double)md, -(md / 2)) & 0xff) << (8 * u);
+            b |= (uint32_t)(oz_res(vi[u], md, 1.0 / (double)md, -(md / 2)) & 0xff) << (8 * u);
+        }
+        S[t][c][0][kq] = a;
+        S[t][c][1][kq] = b;
+    }
+}
+
 // block = 8 columns x 128 K rows; a thread takes four consecutive K rows of one column (c = tid & 7,
 // so a warp reads 4 x 128 contiguous bytes per row), packs each modulus' four residues into one word
 // in shared memory, then the block writes 128-byte rows of B' (TT > 0: compile-time moduli).
@@ -376,20 +416,22 @@ __global__ void __launch_bounds__(256) oz_resid_b_kernel(const __grid_constant__
         if (!isfinite(vr[u])) vr[u] = 0.0;
         if (!isfinite(vi[u])) vi[u] = 0.0;
     }
+    if constexpr (TT > 0) {
+        oz_panel_pairs<TT, 0>(vr, vi, S, c, kq);
+    } else {
+        for (int t = 0; t < T; ++t) {
+            const int md = P.k.mod[t];
+            const double im = P.k.inv_md[t];
+            const int lo = -(md / 2);
+            uint32_t a = 0, b = 0;
 #pragma unroll
-    for (int t = 0; t < (TT > 0 ? TT : kOzMaxMod); ++t) {
-        if (TT == 0 && t >= T) break;
-        const int md = TT > 0 ? oz_modulus(t) : P.k.mod[t];
-        const double im = TT > 0 ? 1.0 / (double)oz_modulus(t) : P.k.inv_md[t];
-        const int lo = -(md / 2);
-        uint32_t a = 0, b = 0;
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            a |= (uint32_t)(oz_res(vr[u], md, im, lo) & 0xff) << (8 * u);
-            b |= (uint32_t)(oz_res(vi[u], md, im, lo) & 0xff) << (8 * u);
+            for (int u = 0; u < 4; ++u) {
+                a |= (uint32_t)(oz_res(vr[u], md, im, lo) & 0xff) << (8 * u);
+                b |= (uint32_t)(oz_res(vi[u], md, im, lo) & 0xff) << (8 * u);
+            }
+            S[t][c][0][kq] = a;
+            S[t][c][1][kq] = b;
         }
-        S[t][c][0][kq] = a;
-        S[t][c][1][kq] = b;
     }
     __syncthreads();
     const int jt = j0 / LT, jj0 = j0 % LT, kb = blockIdx.y;
