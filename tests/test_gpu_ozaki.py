@@ -86,3 +86,20 @@ def test_ozaki_device_tensors(ctx):
     got = P.ozaki_gemm(a, False, b, 16, ctx=ctx)
     want = a @ b
     assert torch.max(torch.abs(got - want)).item() <= 1e-12
+
+
+def test_emulated_batch_isolates_a_nonfinite_problem(ctx, ref):
+    """A batch large enough for the emulated A-products (3 x 2000^2) with a NaN in one matrix: that
+    problem's σ / w are NaN (as the FP64 path gives), the others are unaffected and match the
+    reference's rrsvd_fixed_rank (randomized.cpp:109-122) with the same Ω."""
+    import paper_1504_00992_b200 as P
+    rng = np.random.default_rng(1)
+    As = [cplx_randn(rng, 2000, 2000) * (0.97 ** np.arange(2000))[None, :] for _ in range(3)]
+    As[1][5, 7] = np.nan
+    S, w = P.rrsvd_fixed_rank_batch(As, 100, 10, 2, [1, 2, 3], mode=P.OMEGA_REFERENCE, ctx=ctx)
+    assert [bool(np.all(np.isfinite(s))) for s in S] == [True, False, True]
+    assert np.isnan(w[1]) and np.isfinite(w[0]) and np.isfinite(w[2])
+    for i in (0, 2):
+        _, s_ref, _, w_ref = ref.fixed_rank(As[i], 100, 10, 2, i + 1, vectors=False)
+        assert np.max(np.abs(np.asarray(S[i]) - s_ref)) < 1e-10 * s_ref[0]
+        assert abs(w[i] - w_ref) < 1e-10
