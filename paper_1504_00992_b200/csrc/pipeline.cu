@@ -32,9 +32,14 @@ void gemm_many(rrsvd_b200_ctx* c, GemmOp opA, const std::vector<GemmSpec>& specs
     for (const GemmSpec& s : specs)
         if (s.m > 0 && s.n > 0) total += gemm_tiles(s);
     if (total == 0) return;
-    // Split K when the group has too few tiles: aim for >= 4 waves of 2 CTAs/SM so the tail
-    // wave is a small fraction of the launch.
-    const long long target = 8 * kNumSMs;
+    // Split K when the group has too few tiles: aim for >= 2 waves of 2 CTAs/SM (4 CTAs per SM;
+    // 8 measured slower on the C3 QR Gram matrices — 26.8 vs 29.1 TF/s — from the shorter K per
+    // split and the larger reduction).
+    static const long long waves = [] {  // RRSVD_B200_SPLIT_WAVES: split-K target in CTAs per SM (A/B)
+        const char* e = std::getenv("RRSVD_B200_SPLIT_WAVES");
+        return e ? std::max(1, std::atoi(e)) : 4;
+    }();
+    const long long target = waves * kNumSMs;
     for (size_t base = 0; base < specs.size(); base += kMaxGroup) {
         GemmGroup g;
         g.count = 0;
