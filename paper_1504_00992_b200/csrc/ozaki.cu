@@ -875,31 +875,33 @@ __device__ __forceinline__ void oz_crt4(const uint8_t* p, long long plane, const
 // one thread = four consecutive output columns of one row
 template <int TT>
 __global__ void __launch_bounds__(256) oz_crt_kernel(const __grid_constant__ CrtParams P) {
+    // one thread = one part (re or im) of four consecutive outputs: half the accumulator
+    // registers of a both-parts thread, twice the threads in flight
     const int z = blockIdx.y;
     const int M = P.M[z], l = P.l[z], LT = P.LT[z];
     const int JT = (l + LT - 1) / LT;
     const int groups = JT * (LT / 4);
-    const long long total = (long long)M * groups;
+    const long long total = 2ll * M * groups;
     const bool abad = *P.abad[z] != 0;
     for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (long long)gridDim.x * blockDim.x) {
-        const int row = (int)(e / groups), gi = (int)(e % groups);
+        const int part = (int)(e & 1);
+        const long long eg = e >> 1;
+        const int row = (int)(eg / groups), gi = (int)(eg % groups);
         const int jt = gi / (LT / 4), jj = (gi % (LT / 4)) * 4;
         const int j0 = jt * LT + jj;
         if (j0 >= l) continue;
-        const uint8_t* base = P.out[z] + (long long)row * P.out_ld[z] + (long long)jt * 2 * LT + jj;
-        double re[4], im[4];
-        oz_crt4<TT>(base, P.out_plane[z], P.k, re);
-        oz_crt4<TT>(base + LT, P.out_plane[z], P.k, im);
+        const uint8_t* base = P.out[z] + (long long)row * P.out_ld[z] + (long long)jt * 2 * LT + part * LT + jj;
+        double val[4];
+        oz_crt4<TT>(base, P.out_plane[z], P.k, val);
         const int eo = oz_exp_or0(P.oexp[z][row]) - P.kA[z];
-        cplx* dst = P.C[z] + (long long)row * P.ldc[z] + j0;
+        double* dst = reinterpret_cast<double*>(P.C[z] + (long long)row * P.ldc[z] + j0) + part;
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
             const int j = j0 + u;
             if (j >= l || j >= (jt + 1) * LT) break;
-            const int sh = eo - P.sx[z][j];
-            cplx v = mk(oz_scale(re[u] * P.k.mscale, sh), oz_scale(im[u] * P.k.mscale, sh));
-            if (abad || P.xbad[z][j]) v = mk(NAN, NAN);
-            dst[u] = v;
+            double v = oz_scale(val[u] * P.k.mscale, eo - P.sx[z][j]);
+            if (abad || P.xbad[z][j]) v = NAN;
+            dst[2 * u] = v;
         }
     }
 }
@@ -1143,7 +1145,7 @@ void ozaki_product_many(rrsvd_b200_ctx* c, GemmOp op, const std::vector<OzProduc
             max_cols = std::max(max_cols, JT * LT);
             max_mb = std::max(max_mb, (Mr + kBM - 1) / kBM);
             max_jt = std::max(max_jt, JT);
-            max_el = std::max(max_el, (long long)Mr * JT * (LT / 4));
+            max_el = std::max(max_el, 2ll * Mr * JT * (LT / 4));
             max_k = std::max(max_k, K);
             flops += 8.0 * Mr * (double)p.l * K;
             // X read; B' written + read; A residues read; residue products written + read; C written
