@@ -89,6 +89,46 @@ def ozaki_gemm(a, adj_a: bool, b, moduli: int = 16, ctx=None):
     return out
 
 
+class OzakiOperator:
+    """A prepared once for many emulated products (rrsvd_b200_ozaki_prepare / _apply / _release):
+    the residue planes stay on the device until close()."""
+
+    def __init__(self, a, moduli: int = 15, ctx=None):
+        self.ctx = _ctx(ctx)
+        self.a = _prep(a)
+        self.m, self.n = _shape(self.a)
+        self.h = C.c_void_p()
+        self.ctx.check(L.lib().rrsvd_b200_ozaki_prepare(self.ctx.h, ptr(self.a), sz(self.m), sz(self.n), sz(self.n),
+                                                          int(moduli), C.byref(self.h)))
+
+    def mul(self, adj: bool, x):
+        """op(A) @ x (op = ᴴ when adj)."""
+        x = _prep(x)
+        k, l = _shape(x)
+        if k != (self.m if adj else self.n):
+            raise ContractViolation("OzakiOperator.mul: inner dimension mismatch")
+        out = _empty(x, (self.n if adj else self.m, l), np.complex128)
+        self.ctx.check(L.lib().rrsvd_b200_ozaki_apply(self.ctx.h, self.h, int(adj), ptr(x), sz(l), sz(l), ptr(out),
+                                                        sz(l)))
+        return out
+
+    def close(self):
+        if self.h:
+            L.lib().rrsvd_b200_ozaki_release(self.h)
+            self.h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def ozaki_usable(m: int, n: int) -> int:
+    """Moduli count the library would use for an m x n A (0: off / outside the emulation)."""
+    return int(L.lib().rrsvd_b200_ozaki_usable(sz(m), sz(n)))
+
+
 def matmul(a, b, ctx=None):
     return gemm(a, False, b, False, ctx)
 

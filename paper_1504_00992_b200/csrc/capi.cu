@@ -1,5 +1,6 @@
 // capi.cu — the extern "C" drop-in boundary (include/rrsvd_b200.h).
 #include <algorithm>
+#include <memory>
 #include <cmath>
 #include <cstring>
 #include <string>
@@ -224,6 +225,70 @@ int rrsvd_b200_ozaki_zgemm(rrsvd_b200_ctx* c, int op_a, size_t m, size_t n, size
         ozaki_product_many(c, opn ? kOpN : kOpC, {OzProduct{&oa[0], dB, (long long)ldb, (int)n, dC, (long long)ldc}});
         finish_out(c, outs);
     });
+}
+
+// A prepared once for many emulated products (the row-sharded RRSVD's shards).
+struct rrsvd_b200_ozaki_a {
+    rb::OzakiA a;
+    std::vector<void*> bufs;
+    int device;
+    cudaStream_t stream;
+};
+
+int rrsvd_b200_ozaki_usable(size_t m, size_t n) {
+    return m <= 32768 && n <= 32768 && ozaki_usable((int)m, (int)n, 1) ? ozaki_moduli() : 0;
+}
+
+int rrsvd_b200_ozaki_prepare(rrsvd_b200_ctx* c, const double* A, size_t m, size_t n, size_t lda, int moduli,
+                             rrsvd_b200_ozaki_a** out) {
+    return api(c, [&] {
+        if (out == nullptr) throw_contract(c, "ozaki_prepare: null output");
+        *out = nullptr;
+        if (moduli < 8 || moduli > kOzMaxMod) throw_contract(c, "ozaki_prepare: moduli must be in [8, 16]");
+        if (m < 128 || n < 128 || m > 32768 || n > 32768) throw_contract(c, "ozaki_prepare: needs m, n in [128, 32768]");
+        if (lda < n) throw_contract(c, "ozaki_prepare: leading dimension too small");
+        const auto* dA = static_cast<const cplx*>(stage_in(c, A, m * lda * sizeof(cplx)));
+        auto h = std::make_unique<rrsvd_b200_ozaki_a>();
+        h->device = c->device;
+        h->stream = c->stream;
+        std::vector<OzakiA> oa;
+        try {
+            oa = ozaki_prepare_many(c, {OzSrc{dA, (int)m, (int)n, (long long)lda}}, moduli, &h->bufs);
+        } catch (...) {
+            for (void* p : h->bufs) cudaFreeAsync(p, c->stream);
+            throw;
+        }
+        h->a = oa[0];
+        *out = h.release();
+    });
+}
+
+int rrsvd_b200_ozaki_apply(rrsvd_b200_ctx* c, const rrsvd_b200_ozaki_a* h, int op_a, const double* X, size_t l,
+                           size_t ldx, double* C, size_t ldc) {
+    return api(c, [&] {
+        if (h == nullptr) throw_contract(c, "ozaki_apply: null operator");
+        if (op_a != RRSVD_B200_OP_N && op_a != RRSVD_B200_OP_C) throw_contract(c, "ozaki_apply: bad op_a");
+        if (l == 0) return;
+        const bool opn = op_a == RRSVD_B200_OP_N;
+        const size_t k = opn ? h->a.n : h->a.m, rows = opn ? h->a.m : h->a.n;
+        if (ldx < l || ldc < l) throw_contract(c, "ozaki_apply: leading dimension too small");
+        std::vector<OutBuf> outs;
+        const auto* dX = static_cast<const cplx*>(stage_in(c, X, k * ldx * sizeof(cplx)));
+        auto* dC = static_cast<cplx*>(stage_out(c, C, rows * ldc * sizeof(cplx), outs));
+        ozaki_product_many(c, opn ? kOpN : kOpC, {OzProduct{&h->a, dX, (long long)ldx, (int)l, dC, (long long)ldc}});
+        finish_out(c, outs);
+    });
+}
+
+void rrsvd_b200_ozaki_release(rrsvd_b200_ozaki_a* h) {
+    if (h == nullptr) return;
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(h->device);
+    for (void* p : h->bufs) cudaFreeAsync(p, h->stream);
+    cudaStreamSynchronize(h->stream);
+    cudaSetDevice(prev);
+    delete h;
 }
 
 int rrsvd_b200_frobenius_norm(rrsvd_b200_ctx* c, const double* A, size_t m, size_t n, double* out) {

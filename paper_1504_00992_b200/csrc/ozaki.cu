@@ -979,15 +979,24 @@ bool ozaki_usable(int m, int n, int l) {
     return ozaki_moduli() > 0 && std::min(m, n) >= lo && std::max(m, n) <= 32768 && l >= 1;
 }
 
-std::vector<OzakiA> ozaki_prepare_many(rrsvd_b200_ctx* c, const std::vector<OzSrc>& src, int T) {
+std::vector<OzakiA> ozaki_prepare_many(rrsvd_b200_ctx* c, const std::vector<OzSrc>& src, int T,
+                                       std::vector<void*>* keep) {
     const OzConst& k = oz_const(T);
+    // keep != nullptr: the planes outlive the call (stream-ordered allocations the caller frees)
+    auto alloc = [&](size_t bytes) -> void* {
+        if (keep == nullptr) return ws_alloc(c, bytes);
+        void* p = nullptr;
+        check_cuda(c, cudaMallocAsync(&p, bytes < 16 ? 16 : bytes, c->stream), "cudaMallocAsync(ozaki planes)");
+        keep->push_back(p);
+        return p;
+    };
     std::vector<OzakiA> out(src.size());
     for (size_t base = 0; base < src.size(); base += kPrepGroup) {
         const int cnt = (int)std::min<size_t>(kPrepGroup, src.size() - base);
         PrepParams P{};
         P.count = cnt;
         P.k = k;
-        P.bad = ws_get<int>(c, cnt);
+        P.bad = static_cast<int*>(alloc(sizeof(int) * cnt));
         check_cuda(c, cudaMemsetAsync(P.bad, 0, sizeof(int) * cnt, c->stream), "ozaki memset");
         long long max_chunks = 0;
         int max_m = 1, max_n = 1;
@@ -1001,9 +1010,9 @@ std::vector<OzakiA> ozaki_prepare_many(rrsvd_b200_ctx* c, const std::vector<OzSr
             a.nib = (s.m + 127) / 128;
             a.nkb = (s.n + 127) / 128;
             a.kA = std::min(56, (oz_total_bits(k, std::max(s.m, s.n)) + 1) / 2);
-            a.res = ws_get<int8_t>(c, (size_t)T * 2 * a.nib * a.nkb * 16384);
-            a.rowexp = ws_get<int>(c, s.m);
-            a.colexp = ws_get<int>(c, s.n);
+            a.res = static_cast<int8_t*>(alloc((size_t)T * 2 * a.nib * a.nkb * 16384));
+            a.rowexp = static_cast<int*>(alloc(sizeof(int) * s.m));
+            a.colexp = static_cast<int*>(alloc(sizeof(int) * s.n));
             check_cuda(c, cudaMemsetAsync(a.colexp, 0xC0, sizeof(int) * s.n, c->stream), "ozaki memset");
             a.bad = P.bad + i;
             P.A[i] = s.A;

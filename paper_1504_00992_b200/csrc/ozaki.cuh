@@ -60,8 +60,11 @@ struct OzSrc {
     int m, n;
     long long lda;
 };
-// Builds the residue planes of every A (two launches for the whole batch).
-std::vector<OzakiA> ozaki_prepare_many(rrsvd_b200_ctx* c, const std::vector<OzSrc>& src, int T);
+// Builds the residue planes of every A (three launches for the whole batch); with `keep`, the
+// buffers are not workspace (they outlive the public call) and are appended to *keep for the
+// caller to free (cudaFreeAsync).
+std::vector<OzakiA> ozaki_prepare_many(rrsvd_b200_ctx* c, const std::vector<OzSrc>& src, int T,
+                                       std::vector<void*>* keep = nullptr);
 
 // C = op(A)·X: op N — A m x n, X n x l (ld ldx), C m x l; op C — X m x l, C n x l.
 struct OzProduct {

@@ -106,13 +106,36 @@ class TorchSum:
 
 
 class DeviceOps:
-    """Primitives on the B200 through the C ABI (torch CUDA tensors in and out)."""
+    """Primitives on the B200 through the C ABI (torch CUDA tensors in and out).  prepare(shards)
+    puts the shards on the INT8-emulated A-products (csrc/ozaki.cuh) when the library would use
+    them for a batch of that size (RRSVD_B200_OZAKI, both sides >= 512, >= 8e6 entries): their
+    residue planes are built once and every later gemm with that shard reuses them."""
+
+    MIN_WORK = 8.0e6  # ozaki.cu ozaki_min_work
 
     def __init__(self, ctx, device="cuda"):
         import torch
         self.ctx, self.device, self.torch = ctx, device, torch
+        self._oz = {}
+
+    def prepare(self, shards):
+        work = sum(float(a.shape[0]) * a.shape[1] for a in shards)
+        if work < self.MIN_WORK:
+            return
+        for a in shards:
+            t = api.ozaki_usable(a.shape[0], a.shape[1])
+            if t > 0:
+                self._oz[a.data_ptr()] = api.OzakiOperator(a, t, ctx=self.ctx)
+
+    def release(self):
+        for op in self._oz.values():
+            op.close()
+        self._oz.clear()
 
     def gemm(self, a, adj_a, b):
+        op = self._oz.get(a.data_ptr()) if hasattr(a, "data_ptr") else None
+        if op is not None and op.a.data_ptr() == a.data_ptr() and tuple(op.a.shape) == tuple(a.shape):
+            return op.mul(adj_a, b)
         return api.gemm(a, adj_a, b, ctx=self.ctx)
 
     def chol_inv(self, g, shift_scale):
@@ -174,6 +197,16 @@ class ShardedRrsvd:
     def sketched_svd(self, shards, n: int, l: int, q: int, seed: int, mode: int = OMEGA_REFERENCE):
         """rrsvd_sketched_svd (randomized.cpp:101-107) of the row-stacked shards.
         Returns (U row blocks, sigma (l), this rank's row block [r0, r1) of V (n x l), ||A||_F^2)."""
+        ops = self.ops
+        if hasattr(ops, "prepare"):
+            ops.prepare(shards)
+        try:
+            return self._sketched_svd(shards, n, l, q, seed, mode)
+        finally:
+            if hasattr(ops, "release"):
+                ops.release()
+
+    def _sketched_svd(self, shards, n, l, q, seed, mode):
         ops = self.ops
         m_local = sum(a.shape[0] for a in shards)
         m_total = int(float(self.comm.allreduce(np.array([m_local], np.float64))[0]))
