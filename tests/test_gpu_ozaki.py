@@ -103,3 +103,21 @@ def test_emulated_batch_isolates_a_nonfinite_problem(ctx, ref):
         _, s_ref, _, w_ref = ref.fixed_rank(As[i], 100, 10, 2, i + 1, vectors=False)
         assert np.max(np.abs(np.asarray(S[i]) - s_ref)) < 1e-10 * s_ref[0]
         assert abs(w[i] - w_ref) < 1e-10
+
+
+def test_prepared_operator_reused(ctx):
+    """rrsvd_b200_ozaki_prepare once, _apply many times with both ops (the row-sharded RRSVD's
+    pattern), _release: every product at the emulation's accuracy."""
+    import paper_1504_00992_b200 as P
+    rng = np.random.default_rng(11)
+    a = cplx_randn(rng, 1500, 900) * (0.99 ** np.arange(900))[None, :]
+    op = P.OzakiOperator(a, 15, ctx=ctx)
+    try:
+        for _ in range(3):
+            x = cplx_randn(rng, 900, 110)
+            assert _err(op.mul(False, x), a @ x, a, x) <= 1e-15
+            q = cplx_randn(rng, 1500, 60)
+            assert _err(op.mul(True, q), a.conj().T @ q, a.conj().T, q) <= 1e-15
+    finally:
+        op.close()
+    assert P.ozaki_usable(2000, 2000) in (0, 15)
