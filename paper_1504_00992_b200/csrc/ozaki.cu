@@ -457,8 +457,10 @@ __global__ void __launch_bounds__(256) oz_resid_b_kernel(const __grid_constant__
 }
 
 // ---- the INT8 tcgen05 GEMM --------------------------------------------------------------------
-// kHalves = 1: one 128-row accumulator (256 TMEM columns), 2 stages, 4 warps -> two CTAs per SM, so
-// one CTA's epilogue and prologue overlap the other's loads; kHalves = 2: 256-row tiles, one CTA/SM.
+// Tile: 256 rows (two 128-row accumulators, 448 of TMEM's 512 columns), one CTA per SM.  (kHalves = 1
+// — 128-row tiles, 2 stages, two CTAs per SM so one CTA's epilogue overlaps the other's loads —
+// measured 1.42 vs 1.22 ms per 48-bond product: the panel's L2 re-reads double.)  This one-CTA-
+// per-tile kernel is the A/B form (RRSVD_B200_OZAKI_PERSISTENT=0) of oz_gemm_persistent_kernel.
 constexpr int kHalves = 2;
 constexpr int kBM = 128 * kHalves;
 constexpr int kThreads = 128 * kHalves;

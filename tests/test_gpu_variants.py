@@ -123,7 +123,8 @@ def test_block_jacobi_variants(env):
 
 
 @pytest.mark.parametrize("env", [{"RRSVD_B200_OZAKI": "0"}, {}, {"RRSVD_B200_OZAKI": "16"}, {"RRSVD_B200_OZAKI": "14"},
-                                 {"RRSVD_B200_OZAKI_TAIL": "2"}, {"RRSVD_B200_SPAN_PASSES": "1"}])
+                                 {"RRSVD_B200_OZAKI_TAIL": "2"}, {"RRSVD_B200_SPAN_PASSES": "1"},
+                                 {"RRSVD_B200_OZAKI_PERSISTENT": "0"}, {"RRSVD_B200_OZAKI_GRID": "37"}])
 def test_rrsvd_a_product_paths(env):
     """The headline decimation (2000 x 2000 Θ, RRSVD k = 100, p = 10, q = 2, reference Ω) with the
     A-products on the DMMA zgemm or on the INT8 emulation: chi equal, λ and w within 1e-10 of the
