@@ -212,8 +212,8 @@ int rrsvd_b200_ozaki_zgemm(rrsvd_b200_ctx* c, int op_a, size_t m, size_t n, size
         if (op_a != RRSVD_B200_OP_N && op_a != RRSVD_B200_OP_C) throw_contract(c, "ozaki_zgemm: bad op_a");
         if (moduli < 8 || moduli > kOzMaxMod) throw_contract(c, "ozaki_zgemm: moduli must be in [8, 16]");
         if (m == 0 || n == 0) return;
-        if (m < 128 || k < 128 || std::max(m, k) > 32768)
-            throw_contract(c, "ozaki_zgemm: needs m, k >= 128 and m, k <= 32768");
+        if (m < 128 || k < 16 || std::max(m, k) > 32768)
+            throw_contract(c, "ozaki_zgemm: needs m >= 128, k >= 16 and m, k <= 32768");
         const bool opn = op_a == RRSVD_B200_OP_N;
         const size_t a_rows = opn ? m : k, a_cols = opn ? k : m;
         if (lda < a_cols || ldb < n || ldc < n) throw_contract(c, "ozaki_zgemm: leading dimension too small");
