@@ -971,6 +971,14 @@ double ozaki_min_work() {
     return v;
 }
 
+double ozaki_max_bytes() {
+    static const double v = [] {
+        const char* e = std::getenv("RRSVD_B200_OZAKI_MAX_GB");
+        return (e ? std::atof(e) : 32.0) * 1073741824.0;
+    }();
+    return v;
+}
+
 // Below ~512 rows or columns the preparation and CRT overheads eat the INT8 GEMM's advantage (C2's
 // 256 x 256 bonds: 29.6 vs 30.7 steps/s emulated vs DMMA); RRSVD_B200_OZAKI_MIN overrides.
 bool ozaki_usable(int m, int n, int l) {

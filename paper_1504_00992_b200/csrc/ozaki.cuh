@@ -51,6 +51,8 @@ int ozaki_moduli();
 bool ozaki_usable(int m, int n, int l);
 // Least total A entries (sum of m·n over a batch) for the emulation (RRSVD_B200_OZAKI_MIN_WORK, 8e6).
 double ozaki_min_work();
+// Most residue-plane bytes one call may hold (RRSVD_B200_OZAKI_MAX_GB, default 32 GB).
+double ozaki_max_bytes();
 // RRSVD_B200_OZAKI_TAIL: how many of the RRSVD's last A-products stay on the FP64 zgemm — 0
 // (default): none; 1: the assembly B^H = A^H Q; 2: also the final Y = A Q~ of the power iteration.
 int ozaki_tail();

@@ -774,8 +774,16 @@ void rrsvd_core_many(rrsvd_b200_ctx* c, const std::vector<RrsvdSpec>& specs) {
     std::vector<OzSrc> src;
     std::vector<int> which;
     const int T = ozaki_moduli();
+    // the residue planes (2T bytes per entry, 128-padded) live for the whole call: bonds beyond
+    // the budget (RRSVD_B200_OZAKI_MAX_GB, default 32 GB — a fifth of B200's HBM; no device query
+    // here: cudaMemGetInfo would serialise the lanes) stay on DMMA
+    const double budget = T > 0 ? ozaki_max_bytes() : 0.0;
+    double planes = 0.0;
     for (size_t i = 0; i < specs.size(); ++i)
         if (T > 0 && ozaki_usable(specs[i].m, specs[i].n, specs[i].l)) {
+            const double b = 2.0 * T * ((specs[i].m + 127) / 128) * ((specs[i].n + 127) / 128) * 16384.0;
+            if (planes + b > budget) continue;
+            planes += b;
             src.push_back({specs[i].A, specs[i].m, specs[i].n, (long long)specs[i].n});
             which.push_back((int)i);
         }
