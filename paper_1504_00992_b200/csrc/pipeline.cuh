@@ -65,7 +65,7 @@ struct OrthSpec {
 constexpr int kFullPasses = 4;
 constexpr int kSpanPasses = 2;
 // kRobustSpanPasses: the span schedule's single shifted pass when Y is well conditioned, otherwise
-// all four passes (an orthonormal basis of an ill-conditioned or rank-deficient Y)
+// two shifted and two plain passes (an orthonormal basis of an ill-conditioned or rank-deficient Y)
 constexpr int kRobustSpanPasses = 3;
 void orth_many(rrsvd_b200_ctx* c, const std::vector<OrthSpec>& specs, int passes = kFullPasses);
 void orth(rrsvd_b200_ctx* c, const cplx* Y, int m, int l, cplx* Q, int* ndead = nullptr);
