@@ -97,15 +97,16 @@ int rrsvd_b200_ozaki_zgemm(rrsvd_b200_ctx* ctx, int op_a, size_t m, size_t n, si
                            const double* A, size_t lda, const double* B, size_t ldb, double* C,
                            size_t ldc, int moduli);
 /* An A prepared once for many emulated products (residue planes kept on the device until
- * release): prepare, then C = op(A)·X for as many panels X (k x l) as needed — the row-sharded
- * RRSVD applies each shard 2q+2 times.  ozaki_usable: the moduli count the library would use for
+ * release): prepare, then C = op(A)·X (accumulate = 1: C += op(A)·X, C on the device) for as many
+ * panels X (k x l) as needed — the row-sharded RRSVD applies each shard 2q+2 times; a prepared
+ * column block of a wider A gives that A's products by K-chunks.  ozaki_usable: the moduli count the library would use for
  * an m x n A (0: the emulation is off or the shape is outside it). */
 typedef struct rrsvd_b200_ozaki_a rrsvd_b200_ozaki_a;
 int rrsvd_b200_ozaki_usable(size_t m, size_t n);
 int rrsvd_b200_ozaki_prepare(rrsvd_b200_ctx* ctx, const double* A, size_t m, size_t n, size_t lda, int moduli,
                              rrsvd_b200_ozaki_a** out);
 int rrsvd_b200_ozaki_apply(rrsvd_b200_ctx* ctx, const rrsvd_b200_ozaki_a* a, int op_a, const double* X, size_t l,
-                           size_t ldx, double* C, size_t ldc);
+                           size_t ldx, double* C, size_t ldc, int accumulate);
 void rrsvd_b200_ozaki_release(rrsvd_b200_ozaki_a* a);
 /* Thin orthonormal basis Q (m x n, m >= n) of A plus R = Q^H A (n x n), A = Q R; replaces
  * rrsvd::qr (linalg.cpp:49-65).  Like the reference's Householder QR, Q is orthonormal for ANY

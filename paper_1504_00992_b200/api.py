@@ -93,23 +93,31 @@ class OzakiOperator:
     """A prepared once for many emulated products (rrsvd_b200_ozaki_prepare / _apply / _release):
     the residue planes stay on the device until close()."""
 
-    def __init__(self, a, moduli: int = 15, ctx=None):
+    def __init__(self, a, moduli: int = 15, ctx=None, col0: int = 0, ncols=None):
+        """a: the matrix; (col0, ncols): a column block of it (a K-chunk of a wider A's products)."""
         self.ctx = _ctx(ctx)
         self.a = _prep(a)
-        self.m, self.n = _shape(self.a)
+        rows, cols = _shape(self.a)
+        ncols = cols - col0 if ncols is None else ncols
+        if col0 < 0 or ncols <= 0 or col0 + ncols > cols:
+            raise ContractViolation("OzakiOperator: bad column block")
+        self.m, self.n = rows, ncols
+        base = ptr(self.a)
+        view = C.c_void_p(base.value + 16 * col0)
         self.h = C.c_void_p()
-        self.ctx.check(L.lib().rrsvd_b200_ozaki_prepare(self.ctx.h, ptr(self.a), sz(self.m), sz(self.n), sz(self.n),
+        self.ctx.check(L.lib().rrsvd_b200_ozaki_prepare(self.ctx.h, view, sz(self.m), sz(self.n), sz(cols),
                                                           int(moduli), C.byref(self.h)))
 
-    def mul(self, adj: bool, x):
-        """op(A) @ x (op = ᴴ when adj)."""
+    def mul(self, adj: bool, x, out=None, accumulate: bool = False):
+        """op(A) @ x (op = ᴴ when adj); into `out` (device) and added to it with accumulate."""
         x = _prep(x)
         k, l = _shape(x)
         if k != (self.m if adj else self.n):
             raise ContractViolation("OzakiOperator.mul: inner dimension mismatch")
-        out = _empty(x, (self.n if adj else self.m, l), np.complex128)
+        if out is None:
+            out = _empty(x, (self.n if adj else self.m, l), np.complex128)
         self.ctx.check(L.lib().rrsvd_b200_ozaki_apply(self.ctx.h, self.h, int(adj), ptr(x), sz(l), sz(l), ptr(out),
-                                                        sz(l)))
+                                                        sz(l), int(accumulate)))
         return out
 
     def close(self):

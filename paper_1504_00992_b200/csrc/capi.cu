@@ -264,7 +264,7 @@ int rrsvd_b200_ozaki_prepare(rrsvd_b200_ctx* c, const double* A, size_t m, size_
 }
 
 int rrsvd_b200_ozaki_apply(rrsvd_b200_ctx* c, const rrsvd_b200_ozaki_a* h, int op_a, const double* X, size_t l,
-                           size_t ldx, double* C, size_t ldc) {
+                           size_t ldx, double* C, size_t ldc, int accumulate) {
     return api(c, [&] {
         if (h == nullptr) throw_contract(c, "ozaki_apply: null operator");
         if (op_a != RRSVD_B200_OP_N && op_a != RRSVD_B200_OP_C) throw_contract(c, "ozaki_apply: bad op_a");
@@ -274,8 +274,10 @@ int rrsvd_b200_ozaki_apply(rrsvd_b200_ctx* c, const rrsvd_b200_ozaki_a* h, int o
         if (ldx < l || ldc < l) throw_contract(c, "ozaki_apply: leading dimension too small");
         std::vector<OutBuf> outs;
         const auto* dX = static_cast<const cplx*>(stage_in(c, X, k * ldx * sizeof(cplx)));
+        if (accumulate && !is_device_ptr(C)) throw_contract(c, "ozaki_apply: accumulate needs a device C");
         auto* dC = static_cast<cplx*>(stage_out(c, C, rows * ldc * sizeof(cplx), outs));
-        ozaki_product_many(c, opn ? kOpN : kOpC, {OzProduct{&h->a, dX, (long long)ldx, (int)l, dC, (long long)ldc}});
+        ozaki_product_many(c, opn ? kOpN : kOpC,
+                           {OzProduct{&h->a, dX, (long long)ldx, (int)l, dC, (long long)ldc, accumulate ? 1 : 0}});
         finish_out(c, outs);
     });
 }

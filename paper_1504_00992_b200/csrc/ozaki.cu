@@ -839,6 +839,7 @@ struct CrtParams {
     const int* xbad[kProdGroup];
     cplx* C[kProdGroup];
     long long ldc[kProdGroup];
+    int acc[kProdGroup];
     OzConst k;
 };
 
@@ -903,7 +904,7 @@ __global__ void __launch_bounds__(256) oz_crt_kernel(const __grid_constant__ Crt
             if (j >= l || j >= (jt + 1) * LT) break;
             double v = oz_scale(val[u] * P.k.mscale, eo - P.sx[z][j]);
             if (abad || P.xbad[z][j]) v = NAN;
-            dst[2 * u] = v;
+            dst[2 * u] = P.acc[z] ? dst[2 * u] + v : v;
         }
     }
 }
@@ -1161,6 +1162,7 @@ void ozaki_product_many(rrsvd_b200_ctx* c, GemmOp op, const std::vector<OzProduc
             CP.xbad[i] = xbad;
             CP.C[i] = p.C;
             CP.ldc[i] = p.ldc;
+            CP.acc[i] = p.accumulate;
             max_cols = std::max(max_cols, JT * LT);
             max_mb = std::max(max_mb, (Mr + kBM - 1) / kBM);
             max_jt = std::max(max_jt, JT);

@@ -76,6 +76,7 @@ struct OzProduct {
     int l;
     cplx* C;
     long long ldc;
+    int accumulate = 0;  // 1: C += op(A)·X (a K-chunk of a wider product)
 };
 void ozaki_product_many(rrsvd_b200_ctx* c, GemmOp op, const std::vector<OzProduct>& ps);
 

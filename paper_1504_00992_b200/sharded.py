@@ -111,31 +111,72 @@ class DeviceOps:
     them for a batch of that size (RRSVD_B200_OZAKI, both sides >= 512, >= 8e6 entries): their
     residue planes are built once and every later gemm with that shard reuses them."""
 
-    MIN_WORK = 8.0e6  # ozaki.cu ozaki_min_work
+    MIN_WORK = 8.0e6           # ozaki.cu ozaki_min_work
+    MAX_BYTES = 32 * 2 ** 30   # ozaki.cu ozaki_max_bytes
+    MAX_K = 32768              # int32 accumulators: inner dimension per emulated product
 
     def __init__(self, ctx, device="cuda"):
         import torch
         self.ctx, self.device, self.torch = ctx, device, torch
         self._oz = {}
+        self._stream = set()
 
     def prepare(self, shards):
+        """Shards whose residue planes fit the budget are prepared once for all their products;
+        the others (wider than MAX_K columns, or beyond the budget: C4(i)'s 80000^2) are streamed —
+        each product prepares its K-chunks, multiplies and releases them (the preparation then
+        costs ~2x a product, still ~3x less than the FP64 product at these shapes)."""
         work = sum(float(a.shape[0]) * a.shape[1] for a in shards)
         if work < self.MIN_WORK:
             return
+        used = 0.0
         for a in shards:
-            t = api.ozaki_usable(a.shape[0], a.shape[1])
-            if t > 0:
+            m, n = a.shape
+            t = api.ozaki_usable(m, min(n, self.MAX_K))
+            if t == 0:
+                continue
+            planes = 2.0 * t * ((m + 127) // 128) * ((n + 127) // 128) * 16384
+            if n <= self.MAX_K and used + planes <= self.MAX_BYTES:
                 self._oz[a.data_ptr()] = api.OzakiOperator(a, t, ctx=self.ctx)
+                used += planes
+            else:
+                self._stream.add((a.data_ptr(), t))
 
     def release(self):
         for op in self._oz.values():
             op.close()
         self._oz.clear()
+        self._stream.clear()
+
+    def _streamed(self, a, adj_a, b, t):
+        """op(a) @ b by K-chunks of at most MAX_K columns of a, each prepared, applied, released."""
+        m, n = a.shape
+        nch = -(-n // self.MAX_K)
+        out = None
+        for c in range(nch):
+            k0, k1 = (n * c) // nch, (n * (c + 1)) // nch
+            op = api.OzakiOperator(a, t, ctx=self.ctx, col0=k0, ncols=k1 - k0)
+            try:
+                if adj_a:  # rows k0..k1 of A^H b: one chunk each
+                    if out is None:
+                        out = self.torch.empty((n, b.shape[1]), dtype=b.dtype, device=b.device)
+                    op.mul(True, b, out=out[k0:k1])
+                else:      # A b = sum over chunks of A[:, k0:k1] b[k0:k1]
+                    if out is None:
+                        out = self.torch.empty((m, b.shape[1]), dtype=b.dtype, device=b.device)
+                    op.mul(False, b[k0:k1].contiguous(), out=out, accumulate=c > 0)
+            finally:
+                op.close()
+        return out
 
     def gemm(self, a, adj_a, b):
-        op = self._oz.get(a.data_ptr()) if hasattr(a, "data_ptr") else None
+        key = a.data_ptr() if hasattr(a, "data_ptr") else None
+        op = self._oz.get(key) if key is not None else None
         if op is not None and op.a.data_ptr() == a.data_ptr() and tuple(op.a.shape) == tuple(a.shape):
             return op.mul(adj_a, b)
+        for k, t in self._stream:
+            if k == key:
+                return self._streamed(a, adj_a, b, t)
         return api.gemm(a, adj_a, b, ctx=self.ctx)
 
     def chol_inv(self, g, shift_scale):

@@ -121,3 +121,22 @@ def test_prepared_operator_reused(ctx):
     finally:
         op.close()
     assert P.ozaki_usable(2000, 2000) in (0, 15)
+
+
+def test_streamed_k_chunks(ctx):
+    """The row-sharded driver's streamed products (sharded.DeviceOps._streamed): an A wider than
+    the int32 accumulator's K bound applied by prepared column blocks — op N accumulated over the
+    blocks on the device (CRT with C += ...), op C one block of rows each."""
+    import torch
+    from paper_1504_00992_b200 import sharded
+    ops = sharded.DeviceOps(ctx)
+    ops.MAX_K = 512
+    g = torch.Generator(device="cuda").manual_seed(5)
+    a = torch.randn(700, 1500, dtype=torch.complex128, device="cuda", generator=g)
+    x = torch.randn(1500, 40, dtype=torch.complex128, device="cuda", generator=g)
+    q = torch.randn(700, 40, dtype=torch.complex128, device="cuda", generator=g)
+    y = ops._streamed(a, False, x, 15)
+    z = ops._streamed(a, True, q, 15)
+    scale = float(torch.max(torch.abs(a)))
+    assert float(torch.max(torch.abs(y - a @ x))) <= 1e-14 * scale * 1500
+    assert float(torch.max(torch.abs(z - a.conj().T @ q))) <= 1e-14 * scale * 700
