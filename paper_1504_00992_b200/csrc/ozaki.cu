@@ -1,10 +1,13 @@
-// ozaki.cu — see ozaki.cuh for the scheme.  Four kernels per batch of products:
-//   oz_resid_b  — per-column scale of X and its residue panel B' (K-major, [t][row][part][k]),
-//   oz_gemm     — tcgen05.mma kind::i8: TMA (128B-swizzled boxes) -> 3-stage mbarrier ring ->
-//                 one issuing thread -> two 128 x N' int32 accumulators in TMEM -> epilogue
-//                 reducing each accumulator mod m_t (times w_t) to a uint8 residue plane,
-//   oz_crt      — 128-bit fixed-point CRT of the T residues, scaled to FP64;
-// plus, once per A, oz_rowmax, oz_colmax and oz_resid_a (its equilibrated residue planes).
+// ozaki.cu — see ozaki.cuh for the scheme.  Per batch of products:
+//   oz_xmax, oz_resid_b — the K-side compensation and per-column scale of X, and its residue
+//                 panel B' (128-row K tiles, moduli in pairs),
+//   oz_gemm_persistent — tcgen05.mma kind::i8: one CTA per SM walking (bond, modulus, column
+//                 tile, 256-row block) tiles; TMA rings for A (4 x 32 KB, 128B-swizzled tiles) and
+//                 the panel (3 x 32 KB), one issuing thread, two 128 x N' int32 accumulators in
+//                 TMEM, eight epilogue warps reducing each accumulator to (D mod m_t)·w_t mod m_t
+//                 (one byte per output) while the next tile's loads stream in,
+//   oz_crt      — 96-bit fixed-point CRT of the T residues, scaled to FP64 (optionally added to C);
+// plus, once per A, oz_rowexp, oz_colexp and oz_resid_a (its equilibrated residue tiles).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 

@@ -14,10 +14,11 @@
 // moduli m_t <= 256 (M = prod m_t ~ 2^125 for T = 16): signed 8-bit residues, int32 accumulators
 // in TMEM (no overflow for K <= 32768), and reconstructed exactly by the CRT,
 //   D/M = frac_sym( sum_t ((D mod m_t)·w_t mod m_t) / m_t ),  w_t = (M/m_t)^-1 mod m_t,
-// evaluated in 128-bit fixed point, then D·2^-(sA+sX_j) rounded once to FP64.  The only
-// approximation is the rounding of A and X to kA / kX bits (kA + kX = log2 M - 2 - log2 2K: for
-// T = 16 and K = 2000, 56 + 55 bits — at or beyond FP64's 53-bit mantissa for every entry within
-// 2^3 of the matrix's largest), so the result carries FP64-GEMM-class normwise error.
+// evaluated in fixed point (the top 96 bits of floor(2^128/m_t)), then scaled back by the row,
+// column and panel exponents and rounded once to FP64.  The only approximation is the rounding of
+// A and X to kA / kX bits (kA + kX = floor(log2 M) - 2 - ceil(log2 2K): for the default T = 15 and
+// K = 2000, 52 + 51 bits — FP64's own precision class for every entry relative to its row and
+// column scale), so the result carries FP64-GEMM-class error.
 //
 // A's residue planes are built once per decimation and serve all 2 + 2q products of the range
 // finder and the basis assembly (op N reads them K-major, op C MN-major: no transposed copy).
