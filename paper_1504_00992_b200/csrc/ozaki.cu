@@ -547,6 +547,29 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
     asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
 }
 
+// Epilogue of one 128-row accumulator (warp's TMEM lane quarter q, accumulator column base acc):
+// each int32 D reduced to t = (D mod m)·w mod m by two integer Barrett steps (D + off >= 0), one
+// byte per output, 16 outputs per 16-byte store of the thread's row.
+__device__ __forceinline__ void oz_epilogue_rows(uint32_t tmem, int q, int acc, int Nn, bool store, uint8_t* dst,
+                                                 int md, int w, unsigned mg, unsigned off) {
+    for (int ch = 0; ch < Nn / 16; ++ch) {
+        uint32_t v[16];
+        tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + acc + ch * 16, v);
+        uint32_t pk[4] = {0, 0, 0, 0};
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+            const unsigned x = v[u] + off;
+            int r = (int)(x - __umulhi(x, mg) * md);  // in [-m, m)
+            r += (r >> 31) & md;                       // [0, m)
+            const unsigned p = (unsigned)(r * w);      // < 2^16
+            int tt = (int)(p - __umulhi(p, mg) * md);
+            tt += (tt >> 31) & md;
+            pk[u >> 2] |= (uint32_t)tt << (8 * (u & 3));
+        }
+        if (store) *reinterpret_cast<uint4*>(dst + ch * 16) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+    }
+}
+
 // OPA = kOpN: A tile K-major ([row][k], the residue planes' own layout); kOpC: MN-major.
 template <int OPA>
 __global__ void __launch_bounds__(kThreads, 3 - kHalves) oz_gemm_kernel(const __grid_constant__ GemmParams P) {
@@ -640,26 +663,8 @@ __global__ void __launch_bounds__(kThreads, 3 - kHalves) oz_gemm_kernel(const __
     {
         const int q = warp & 3, h = warp >> 2;
         const int row = m0 + h * 128 + q * 32 + lane;
-        const int md = P.mod[t], w = P.w[t];
-        const unsigned mg = P.magic[t], off = P.off[t];
         uint8_t* dst = P.out[z] + (long long)t * P.out_plane[z] + (long long)row * P.out_ld[z] + jt * Nn;
-        for (int ch = 0; ch < Nn / 16; ++ch) {
-            uint32_t v[16];
-            tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + h * 256 + ch * 16, v);
-            uint32_t pk[4] = {0, 0, 0, 0};
-#pragma unroll
-            for (int u = 0; u < 16; ++u) {
-                // t = (D mod m)·w mod m by two Barrett reductions (integer only): D + off >= 0
-                const unsigned x = v[u] + off;
-                int r = (int)(x - __umulhi(x, mg) * md);   // in [-m, m)
-                r += (r >> 31) & md;                        // [0, m)
-                const unsigned p = (unsigned)(r * w);       // < 2^16
-                int tt = (int)(p - __umulhi(p, mg) * md);
-                tt += (tt >> 31) & md;
-                pk[u >> 2] |= (uint32_t)tt << (8 * (u & 3));
-            }
-            if (row < M) *reinterpret_cast<uint4*>(dst + ch * 16) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-        }
+        oz_epilogue_rows(tmem, q, h * 256, Nn, row < M, dst, P.mod[t], P.w[t], P.magic[t], P.off[t]);
     }
     tc_fence_before();
     __syncthreads();
@@ -799,25 +804,9 @@ __global__ void __launch_bounds__(kPThreads, 1) oz_gemm_persistent_kernel(const 
             ob_wait(&tfull, tcount & 1);
             tc_fence_after();
             const int row = tc.m0 + h * 128 + q * 32 + lane;
-            const int md = P.mod[tc.t], w = P.w[tc.t];
-            const unsigned mg = P.magic[tc.t], off = P.off[tc.t];
             uint8_t* dst = P.out[tc.z] + (long long)tc.t * P.out_plane[tc.z] + (long long)row * P.out_ld[tc.z] + tc.jt * Nn;
-            for (int ch = 0; ch < Nn / 16; ++ch) {
-                uint32_t v[16];
-                tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + h * 256 + ch * 16, v);
-                uint32_t pk[4] = {0, 0, 0, 0};
-#pragma unroll
-                for (int u = 0; u < 16; ++u) {
-                    const unsigned x = v[u] + off;
-                    int r = (int)(x - __umulhi(x, mg) * md);
-                    r += (r >> 31) & md;
-                    const unsigned p = (unsigned)(r * w);
-                    int tt = (int)(p - __umulhi(p, mg) * md);
-                    tt += (tt >> 31) & md;
-                    pk[u >> 2] |= (uint32_t)tt << (8 * (u & 3));
-                }
-                if (row < P.M[tc.z]) *reinterpret_cast<uint4*>(dst + ch * 16) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-            }
+            oz_epilogue_rows(tmem, q, h * 256, Nn, row < P.M[tc.z], dst, P.mod[tc.t], P.w[tc.t], P.magic[tc.t],
+                             P.off[tc.t]);
             tc_fence_before();
             __syncwarp();
             if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(&tempty)) : "memory");
