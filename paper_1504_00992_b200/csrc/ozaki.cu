@@ -211,11 +211,11 @@ __device__ __forceinline__ void oz_store8(const double (&vr)[8], const double (&
 // residue in FP32 (r/M needs only ~2^-16 accuracy to round exactly: no ties for odd M, and for
 // M = 256 the tie ±128 is one byte) — half the FP64 work of two direct reductions.
 template <int M>
-__device__ __forceinline__ uint32_t oz_res32(float f) {
-    const float sh = 12582912.0f;  // 1.5·2^23
-    const float q = fmaf(f, 1.0f / (float)M, sh) - sh;
-    const float r = fmaf(-q, (float)M, f);
-    return (uint32_t)__float_as_int(r + sh) & 0xffu;
+__device__ __forceinline__ uint32_t oz_res32(float f, int ri) {
+    // q = round(ri / M) from the FP32 shifter's bit pattern; the residue's low byte is that of
+    // ri - q·M in integers (two's complement: the symmetric residue as a signed byte)
+    const int q = __float_as_int(fmaf(f, 1.0f / (float)M, 12582912.0f)) - 0x4B400000;
+    return (uint32_t)(ri - q * M) & 0xffu;
 }
 template <int MA, int MB>
 __device__ __forceinline__ void oz_store8_pair(const double (&vr)[8], const double (&vi)[8], int8_t* dst, long long plane) {
@@ -230,7 +230,7 @@ __device__ __forceinline__ void oz_store8_pair(const double (&vr)[8], const doub
             const double q = fma(v, 1.0 / P, sh) - sh;
             const int ri = __double2loint(fma(-q, P, v) + sh);
             const float f = __int_as_float(ri + 0x4B400000) - 12582912.0f;
-            const uint32_t ra = oz_res32<MA>(f), rb = oz_res32<MB>(f);
+            const uint32_t ra = oz_res32<MA>(f, ri), rb = oz_res32<MB>(f, ri);
             const int w = u >> 2, sft = 8 * (u & 3);
             if (part == 0) { ar[w] |= ra << sft; br[w] |= rb << sft; }
             else { ai[w] |= ra << sft; bi[w] |= rb << sft; }
@@ -367,7 +367,7 @@ __device__ __forceinline__ void oz_panel_pairs(const double (&vr)[4], const doub
                 const double q = fma(v, 1.0 / Pm, sh) - sh;
                 const int ri = __double2loint(fma(-q, Pm, v) + sh);
                 const float f = __int_as_float(ri + 0x4B400000) - 12582912.0f;
-                const uint32_t ra = oz_res32<MA>(f) << (8 * u), rb = oz_res32<MB>(f) << (8 * u);
+                const uint32_t ra = oz_res32<MA>(f, ri) << (8 * u), rb = oz_res32<MB>(f, ri) << (8 * u);
                 if (part == 0) { a0 |= ra; b0 |= rb; }
                 else { a1 |= ra; b1 |= rb; }
             }

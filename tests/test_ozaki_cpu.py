@@ -134,8 +134,9 @@ def _f32(x):
 @pytest.mark.parametrize("T", [14, 15, 16])
 def test_paired_residues(T):
     """oz_store8_pair: r = v mod m_a·m_b by a shifter-rounded FP64 quotient and an exact remainder,
-    then each residue in FP32 (fmaf rounds once: emulated here by an FP64 sum rounded to FP32)
-    — the byte equals the symmetric residue of v for every modulus of the pair."""
+    then each residue's quotient from an FP32 shifter (fmaf rounds once: emulated here by an FP64
+    sum rounded to FP32) and the byte from the integer remainder — the symmetric residue of v for
+    every modulus of the pair."""
     rng = np.random.default_rng(T)
     sh64 = 6755399441055744.0
     sh32 = np.float32(12582912.0)
@@ -149,10 +150,12 @@ def test_paired_residues(T):
             r = v - q * P                              # exact (an FMA on the device)
             assert abs(r) <= P / 2 + 1
             f = np.float32(r)
+            ri = int(r)
             for m in (ma, mb):
-                qq = _f32(np.float64(f) * np.float64(np.float32(1.0 / m)) + np.float64(sh32)) - sh32
-                rr = np.float32(np.float64(f) - np.float64(qq) * m)
+                # q from the FP32 shifter's bits (fmaf rounds once), the byte from ri - q·m
+                qq = int(_f32(np.float64(f) * np.float64(np.float32(1.0 / m)) + np.float64(sh32)) - sh32)
+                rr = ri - qq * m
                 assert abs(rr) <= m / 2
-                byte = int(rr) & 0xFF
+                byte = rr & 0xFF
                 want = sym_res(int(v), m) & 0xFF
                 assert byte == want, (v, m, rr, sym_res(int(v), m))
