@@ -271,6 +271,10 @@ int rrsvd_b200_mps_get_site(rrsvd_b200_mps* mps, size_t site, size_t* dims3, dou
 int rrsvd_b200_state_upload(rrsvd_b200_mps* mps, const size_t* dims, const double* const* gammas,
                             const double* const* lambdas);
 int rrsvd_b200_state_download(rrsvd_b200_mps* mps, size_t* dims, double* const* gammas, double* const* lambdas);
+/* download into the (pinned) host buffers and upload back from them, pipelined per site on two
+ * streams (the D2H and H2D copy engines overlap); dims unchanged.  The state a caller keeps on the
+ * host between consecutive steps, at the cost of one direction instead of two. */
+int rrsvd_b200_state_roundtrip(rrsvd_b200_mps* mps, double* const* gammas, double* const* lambdas);
 /* evolve (tebd.cpp:260-326): n_steps x sweeps x (bonds of the sweep's parity, ascending):
  * build_theta -> gate -> decimate on the device, state resident in HBM.  gates[s*(n_sites-1)+b]
  * is the (d_b d_{b+1})^2 gate exp(-i c_s dt h_b) for sweep s (NULL = no term on that bond); the

@@ -230,6 +230,47 @@ int rrsvd_b200_state_download(rrsvd_b200_mps* s, size_t* dims, double* const* ga
     });
 }
 
+// The state through host memory and back, pipelined per site: site s goes device -> host on the
+// context stream and, as soon as it has landed, host -> device on lane 0 (the two copy engines run
+// in parallel across sites).  The host buffers hold the state afterwards; the device state is the
+// one re-uploaded from them.  Dims are unchanged (a consecutive-steps round trip).
+int rrsvd_b200_state_roundtrip(rrsvd_b200_mps* s, double* const* gammas, double* const* lambdas) {
+    return mps_api(s, [&](rrsvd_b200_ctx* c) {
+        if (gammas == nullptr) throw_contract(c, "state_roundtrip: gammas are required");
+        for (int site = 0; site < s->n; ++site)
+            if (gammas[site] == nullptr) throw_contract(c, "state_roundtrip: missing gamma");
+        lanes_fork(c, 1);  // lane 0 orders after everything queued so far
+        const cudaStream_t up = c->lane[0];
+        std::vector<cudaEvent_t> ev(s->n, nullptr);
+        struct Events {
+            std::vector<cudaEvent_t>& v;
+            ~Events() {
+                for (cudaEvent_t e : v)
+                    if (e) cudaEventDestroy(e);
+            }
+        } guard{ev};
+        for (int site = 0; site < s->n; ++site) {
+            const size_t elems = (size_t)s->dl[site] * s->d[site] * s->dr[site];
+            const bool lam = lambdas != nullptr && lambdas[site] != nullptr && site + 1 < s->n;
+            check_cuda(c, cudaMemcpyAsync(gammas[site], s->g[site], elems * sizeof(cplx), cudaMemcpyDefault, c->stream),
+                       "download gamma");
+            if (lam)
+                check_cuda(c, cudaMemcpyAsync(lambdas[site], s->lam[site], s->dr[site] * sizeof(double), cudaMemcpyDefault,
+                                              c->stream), "download lambda");
+            check_cuda(c, cudaEventCreateWithFlags(&ev[site], cudaEventDisableTiming), "event");
+            check_cuda(c, cudaEventRecord(ev[site], c->stream), "event");
+            check_cuda(c, cudaStreamWaitEvent(up, ev[site], 0), "event wait");
+            check_cuda(c, cudaMemcpyAsync(s->g[site], gammas[site], elems * sizeof(cplx), cudaMemcpyDefault, up),
+                       "upload gamma");
+            if (lam)
+                check_cuda(c, cudaMemcpyAsync(s->lam[site], lambdas[site], s->dr[site] * sizeof(double), cudaMemcpyDefault,
+                                              up), "upload lambda");
+        }
+        lanes_join(c, 1);
+        check_cuda(c, cudaStreamSynchronize(c->stream), "sync");
+    });
+}
+
 }  // extern "C"
 
 namespace {

@@ -108,6 +108,18 @@ class DeviceMps:
                                     + [None] * (n - len(lambdas))))
         self.ctx.check(L.lib().rrsvd_b200_state_download(self.h, None, gp, lp))
 
+    def roundtrip(self, gammas, lambdas=None):
+        """Download into pre-shaped (pinned) host buffers and upload back from them, pipelined per
+        site on two streams (rrsvd_b200_state_roundtrip): the state through host memory between
+        consecutive steps, the two copy directions overlapped."""
+        n = self.n_sites
+        gp = (C.c_void_p * n)(*[ptr(g).value for g in gammas])
+        lp = None
+        if lambdas is not None:
+            lp = (C.c_void_p * n)(*([ptr(x).value if x is not None else None for x in lambdas]
+                                    + [None] * (n - len(lambdas))))
+        self.ctx.check(L.lib().rrsvd_b200_state_roundtrip(self.h, gp, lp))
+
     def all_dims(self):
         n = self.n_sites
         dims = (C.c_size_t * (3 * n))()
