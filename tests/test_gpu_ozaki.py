@@ -140,3 +140,29 @@ def test_streamed_k_chunks(ctx):
     scale = float(torch.max(torch.abs(a)))
     assert float(torch.max(torch.abs(y - a @ x))) <= 1e-14 * scale * 1500
     assert float(torch.max(torch.abs(z - a.conj().T @ q))) <= 1e-14 * scale * 700
+
+
+def test_emulation_contracts(ctx):
+    """The emulation's ABI rejects what it cannot compute exactly (ContractViolation, status 1):
+    moduli outside [8, 16], shapes outside [128, 32768], a mismatched panel, accumulation into host
+    memory — and the context stays usable afterwards."""
+    import paper_1504_00992_b200 as P
+    rng = np.random.default_rng(2)
+    a = cplx_randn(rng, 256, 256)
+    x = cplx_randn(rng, 256, 8)
+    with pytest.raises(P.ContractViolation):
+        P.ozaki_gemm(a, False, x, 7, ctx=ctx)
+    with pytest.raises(P.ContractViolation):
+        P.ozaki_gemm(a, False, x, 17, ctx=ctx)
+    with pytest.raises(P.ContractViolation):
+        P.OzakiOperator(cplx_randn(rng, 64, 256), 15, ctx=ctx)
+    op = P.OzakiOperator(a, 15, ctx=ctx)
+    try:
+        with pytest.raises(P.ContractViolation):
+            op.mul(False, cplx_randn(rng, 200, 8))
+        with pytest.raises(P.ContractViolation):
+            op.mul(False, x, out=np.zeros((256, 8), np.complex128), accumulate=True)
+        y = op.mul(False, x)
+        assert _err(y, a @ x, a, x) <= 1e-15
+    finally:
+        op.close()
