@@ -508,11 +508,15 @@ def run_ours(args, rank, world, local_rank):
     for st in range(args.steps):
         one_step()
         dims = mps.all_dims()
-        same = all(tuple(pin_g[s_].shape) == dims[s_] for s_ in range(len(site_dims))) and \
-            all(pin_l[b].shape[0] == dims[b][2] for b in range(len(site_dims) - 1))
-        if not same:  # (the saturated state keeps its dims: no reallocation in the bench)
-            pin_g = [torch.empty(dims[s_], dtype=torch.complex128).pin_memory() for s_ in range(len(site_dims))]
-            pin_l = [torch.empty(dims[b][2], dtype=torch.float64).pin_memory() for b in range(len(site_dims) - 1)]
+        same = True
+        for s_ in range(len(site_dims)):  # (a saturated state keeps its dims: nothing reallocated)
+            if tuple(pin_g[s_].shape) != dims[s_]:
+                pin_g[s_] = torch.empty(dims[s_], dtype=torch.complex128).pin_memory()
+                same = False
+        for b in range(len(site_dims) - 1):
+            if pin_l[b].shape[0] != dims[b][2]:
+                pin_l[b] = torch.empty(dims[b][2], dtype=torch.float64).pin_memory()
+                same = False
         if st + 1 < args.steps and same:
             mps.roundtrip(pin_g, pin_l)
         else:
