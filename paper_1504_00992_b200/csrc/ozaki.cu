@@ -212,16 +212,21 @@ __device__ __forceinline__ void oz_store8(const double (&vr)[8], const double (&
 // M = 256 the tie ±128 is one byte) — half the FP64 work of two direct reductions.
 template <int M>
 __device__ __forceinline__ uint32_t oz_res32(float f, int ri) {
-    // q = round(ri / M) from the FP32 shifter's bit pattern; the residue's low byte is that of
-    // ri - q·M in integers (two's complement: the symmetric residue as a signed byte)
-    const int q = __float_as_int(fmaf(f, 1.0f / (float)M, 12582912.0f)) - 0x4B400000;
-    return (uint32_t)(ri - q * M) & 0xffu;
+    // q = round(ri / M) = bits - 0x4B400000, bits the FP32 shifter's bit pattern; the residue's low
+    // byte is that of ri - q·M in integers (two's complement: the symmetric residue as a signed
+    // byte), and 0x4B400000·M is 0 mod 256, so the low byte of ri - bits·M is the same: one IMAD
+    const int bits = __float_as_int(fmaf(f, 1.0f / (float)M, 12582912.0f));
+    return (uint32_t)(ri - bits * M);
+}
+// the low bytes of four words packed into one (three PRMTs)
+__device__ __forceinline__ uint32_t oz_pack4(uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+    return __byte_perm(__byte_perm(a, b, 0x0040), __byte_perm(c, d, 0x0040), 0x5410);
 }
 template <int MA, int MB>
 __device__ __forceinline__ void oz_store8_pair(const double (&vr)[8], const double (&vi)[8], int8_t* dst, long long plane) {
     constexpr double P = (double)MA * (double)MB;
     const double sh = 6755399441055744.0;
-    uint32_t ar[2] = {0, 0}, ai[2] = {0, 0}, br[2] = {0, 0}, bi[2] = {0, 0};
+    uint32_t xa[2][8], xb[2][8];  // [part][u]: residue mod MA / MB in the low byte
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
 #pragma unroll
@@ -230,16 +235,16 @@ __device__ __forceinline__ void oz_store8_pair(const double (&vr)[8], const doub
             const double q = fma(v, 1.0 / P, sh) - sh;
             const int ri = __double2loint(fma(-q, P, v) + sh);
             const float f = __int_as_float(ri + 0x4B400000) - 12582912.0f;
-            const uint32_t ra = oz_res32<MA>(f, ri), rb = oz_res32<MB>(f, ri);
-            const int w = u >> 2, sft = 8 * (u & 3);
-            if (part == 0) { ar[w] |= ra << sft; br[w] |= rb << sft; }
-            else { ai[w] |= ra << sft; bi[w] |= rb << sft; }
+            xa[part][u] = oz_res32<MA>(f, ri);
+            xb[part][u] = oz_res32<MB>(f, ri);
         }
     }
-    *reinterpret_cast<uint2*>(dst) = make_uint2(ar[0], ar[1]);
-    *reinterpret_cast<uint2*>(dst + plane) = make_uint2(ai[0], ai[1]);
-    *reinterpret_cast<uint2*>(dst + 2 * plane) = make_uint2(br[0], br[1]);
-    *reinterpret_cast<uint2*>(dst + 3 * plane) = make_uint2(bi[0], bi[1]);
+    auto lo = [](const uint32_t (&x)[8]) { return oz_pack4(x[0], x[1], x[2], x[3]); };
+    auto hi = [](const uint32_t (&x)[8]) { return oz_pack4(x[4], x[5], x[6], x[7]); };
+    *reinterpret_cast<uint2*>(dst) = make_uint2(lo(xa[0]), hi(xa[0]));
+    *reinterpret_cast<uint2*>(dst + plane) = make_uint2(lo(xa[1]), hi(xa[1]));
+    *reinterpret_cast<uint2*>(dst + 2 * plane) = make_uint2(lo(xb[0]), hi(xb[0]));
+    *reinterpret_cast<uint2*>(dst + 3 * plane) = make_uint2(lo(xb[1]), hi(xb[1]));
 }
 
 template <int TT, int t>
@@ -358,7 +363,7 @@ __device__ __forceinline__ void oz_panel_pairs(const double (&vr)[4], const doub
         constexpr int MA = oz_modulus(t), MB = oz_modulus(t + 1);
         constexpr double Pm = (double)MA * (double)MB;
         const double sh = 6755399441055744.0;
-        uint32_t a0 = 0, a1 = 0, b0 = 0, b1 = 0;
+        uint32_t xa[2][4], xb[2][4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
 #pragma unroll
@@ -367,15 +372,14 @@ __device__ __forceinline__ void oz_panel_pairs(const double (&vr)[4], const doub
                 const double q = fma(v, 1.0 / Pm, sh) - sh;
                 const int ri = __double2loint(fma(-q, Pm, v) + sh);
                 const float f = __int_as_float(ri + 0x4B400000) - 12582912.0f;
-                const uint32_t ra = oz_res32<MA>(f, ri) << (8 * u), rb = oz_res32<MB>(f, ri) << (8 * u);
-                if (part == 0) { a0 |= ra; b0 |= rb; }
-                else { a1 |= ra; b1 |= rb; }
+                xa[part][u] = oz_res32<MA>(f, ri);
+                xb[part][u] = oz_res32<MB>(f, ri);
             }
         }
-        S[t][c][0][kq] = a0;
-        S[t][c][1][kq] = a1;
-        S[t + 1][c][0][kq] = b0;
-        S[t + 1][c][1][kq] = b1;
+        S[t][c][0][kq] = oz_pack4(xa[0][0], xa[0][1], xa[0][2], xa[0][3]);
+        S[t][c][1][kq] = oz_pack4(xa[1][0], xa[1][1], xa[1][2], xa[1][3]);
+        S[t + 1][c][0][kq] = oz_pack4(xb[0][0], xb[0][1], xb[0][2], xb[0][3]);
+        S[t + 1][c][1][kq] = oz_pack4(xb[1][0], xb[1][1], xb[1][2], xb[1][3]);
         oz_panel_pairs<TT, t + 2, kPadW>(vr, vi, S, c, kq);
     } else if constexpr (t < TT) {
         constexpr int md = oz_modulus(t);

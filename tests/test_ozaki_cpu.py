@@ -153,9 +153,15 @@ def test_paired_residues(T):
             ri = int(r)
             for m in (ma, mb):
                 # q from the FP32 shifter's bits (fmaf rounds once), the byte from ri - q·m
-                qq = int(_f32(np.float64(f) * np.float64(np.float32(1.0 / m)) + np.float64(sh32)) - sh32)
+                shifted = _f32(np.float64(f) * np.float64(np.float32(1.0 / m)) + np.float64(sh32))
+                qq = int(shifted - sh32)
                 rr = ri - qq * m
                 assert abs(rr) <= m / 2
                 byte = rr & 0xFF
                 want = sym_res(int(v), m) & 0xFF
                 assert byte == want, (v, m, rr, sym_res(int(v), m))
+                # the kernel's single IMAD: the low byte of ri - bits·m, bits the shifter's FP32 bit
+                # pattern (= q + 0x4B400000, and 0x4B400000·m = 0 mod 256)
+                bits = int(np.array([shifted], np.float32).view(np.int32)[0])
+                assert bits - 0x4B400000 == qq
+                assert (ri - bits * m) & 0xFF == want
