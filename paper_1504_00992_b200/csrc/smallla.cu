@@ -130,53 +130,78 @@ __global__ void __launch_bounds__(CHOL_THREADS, 1) chol_inv_kernel(const __grid_
     }
     __syncthreads();
 
-    // ---- right-looking Cholesky by panels of NB rows
+    // ---- right-looking Cholesky by panels of NB rows, with look-ahead: warp 0 updates the next
+    // panel's diagonal tile first and factors it while the other warps finish the trailing update
     const double dtol = b.dep_tol[p];
-    for (int j0 = 0; j0 < l; j0 += NB) {
+    auto factor_diag = [&](int j0) {  // warp 0: the 8 x 8 diagonal block at j0 (lanes redundantly)
         const int nb = min(NB, l - j0);
         cplx D[NB][NB];
         double inv[NB];
-        if (warp == 0) {  // the diagonal block, factored by one warp (lanes redundantly)
-            unsigned deadmask = 0;
+        unsigned deadmask = 0;
 #pragma unroll
-            for (int t = 0; t < NB; ++t)
+        for (int t = 0; t < NB; ++t)
 #pragma unroll
-                for (int u = t; u < NB; ++u) D[t][u] = (u < nb) ? P[(size_t)(j0 + t) * ld + j0 + u] : mk(0.0, 0.0);
+            for (int u = t; u < NB; ++u) D[t][u] = (u < nb) ? P[(size_t)(j0 + t) * ld + j0 + u] : mk(0.0, 0.0);
+#pragma unroll
+        for (int t = 0; t < NB; ++t) {
+            inv[t] = 0.0;
+            if (t < nb) {
+                const double d = D[t][t].x, g = g0[j0 + t];
+                const bool isdead = !(d > dtol * g) || !(d > 0.0) || !(g > 0.0);
+                if (lane == 0 && (isdead || !(d >= kIllRatio * s_shift))) s_ill = 1;
+                const double r = isdead ? 0.0 : sqrt(d);
+                inv[t] = isdead ? 0.0 : 1.0 / r;
+                deadmask |= isdead ? (1u << t) : 0u;
+                D[t][t] = mk(r, 0.0);
+#pragma unroll
+                for (int u = t + 1; u < NB; ++u) D[t][u] = cscale(D[t][u], inv[t]);
+#pragma unroll
+                for (int v = t + 1; v < NB; ++v)
+#pragma unroll
+                    for (int u = v; u < NB; ++u) cfnmac(D[v][u], D[t][v], D[t][u]);
+            }
+        }
+        if (lane == 0) {
 #pragma unroll
             for (int t = 0; t < NB; ++t) {
-                inv[t] = 0.0;
+                sinv[t] = inv[t];
+#pragma unroll
+                for (int u = t; u < NB; ++u) sD[t * NB + u] = D[t][u];
                 if (t < nb) {
-                    const double d = D[t][t].x, g = g0[j0 + t];
-                    const bool isdead = !(d > dtol * g) || !(d > 0.0) || !(g > 0.0);
-                    if (lane == 0 && (isdead || !(d >= kIllRatio * s_shift))) s_ill = 1;
-                    const double r = isdead ? 0.0 : sqrt(d);
-                    inv[t] = isdead ? 0.0 : 1.0 / r;
-                    deadmask |= isdead ? (1u << t) : 0u;
-                    D[t][t] = mk(r, 0.0);
-#pragma unroll
-                    for (int u = t + 1; u < NB; ++u) D[t][u] = cscale(D[t][u], inv[t]);
-#pragma unroll
-                    for (int v = t + 1; v < NB; ++v)
-#pragma unroll
-                        for (int u = v; u < NB; ++u) cfnmac(D[v][u], D[t][v], D[t][u]);
-                }
-            }
-            if (lane == 0) {
-#pragma unroll
-                for (int t = 0; t < NB; ++t) {
-                    sinv[t] = inv[t];
-#pragma unroll
-                    for (int u = t; u < NB; ++u) sD[t * NB + u] = D[t][u];
-                    if (t < nb) {
-                        dead[j0 + t] = (deadmask >> t) & 1u;
-                        rinv[j0 + t] = inv[t];
-                    }
+                    dead[j0 + t] = (deadmask >> t) & 1u;
+                    rinv[j0 + t] = inv[t];
                 }
             }
         }
-        __syncthreads();
+    };
+    auto update_tile = [&](int code, int j0) {  // G tile -= R_J,tile-rows^H R_J,tile-cols on DMMA
+        const int r0 = (code >> 8) * NB, c0 = (code & 255) * NB;
+        cplx* Cp = P + (size_t)(r0 + (lane >> 2)) * ld + c0 + 2 * (lane & 3);
+        double cre[2] = {Cp[0].x, Cp[1].x}, cim[2] = {Cp[0].y, Cp[1].y};
+        double dre[2] = {0.0, 0.0}, dim[2] = {0.0, 0.0};
+#pragma unroll
+        for (int ks = 0; ks < 2; ++ks) {
+            const cplx* Rrow = P + (size_t)(j0 + 4 * ks + (lane & 3)) * ld;
+            const cplx a = Rrow[r0 + (lane >> 2)], bb = Rrow[c0 + (lane >> 2)];
+            // C -= conj(A)^T B:  Re -= ar br + ai bi,  Im -= ar bi - ai br
+            dmma884(cre[0], cre[1], -a.x, bb.x);
+            dmma884(dre[0], dre[1], -a.y, bb.y);
+            dmma884(cim[0], cim[1], -a.x, bb.y);
+            dmma884(dim[0], dim[1], a.y, bb.x);
+        }
+        const int row = r0 + (lane >> 2);
+#pragma unroll
+        for (int c = 0; c < 2; ++c)
+            if (c0 + 2 * (lane & 3) + c >= row) Cp[c] = mk(cre[c] + dre[c], cim[c] + dim[c]);
+    };
+    if (warp == 0) factor_diag(0);
+    __syncthreads();
+    for (int j0 = 0; j0 < l; j0 += NB) {
+        const int nb = min(NB, l - j0);
         // panel: R[J][k] = R_JJ^-H G[J][k], one column per thread
         for (int k = j0 + nb + tid; k < l; k += CHOL_THREADS) {
+            cplx D[NB][NB];
+            double inv[NB];
 #pragma unroll
             for (int t = 0; t < NB; ++t) {
                 inv[t] = sinv[t];
@@ -207,26 +232,20 @@ __global__ void __launch_bounds__(CHOL_THREADS, 1) chol_inv_kernel(const __grid_
         if (nb == NB) {  // trailing update on DMMA (a partial panel is the last: nothing trails it)
             const int t0 = j0 / NB + 1, nt = L / NB - t0;
             const int ntiles = nt * (nt + 1) / 2;
-            for (int tt = warp; tt < ntiles; tt += nw) {
-                const int code = s_tile[tt];
-                const int r0 = (code >> 8) * NB, c0 = (code & 255) * NB;
-                cplx* Cp = P + (size_t)(r0 + (lane >> 2)) * ld + c0 + 2 * (lane & 3);
-                double cre[2] = {Cp[0].x, Cp[1].x}, cim[2] = {Cp[0].y, Cp[1].y};
-                double dre[2] = {0.0, 0.0}, dim[2] = {0.0, 0.0};
-#pragma unroll
-                for (int ks = 0; ks < 2; ++ks) {
-                    const cplx* Rrow = P + (size_t)(j0 + 4 * ks + (lane & 3)) * ld;
-                    const cplx a = Rrow[r0 + (lane >> 2)], bb = Rrow[c0 + (lane >> 2)];
-                    // C -= conj(A)^T B:  Re -= ar br + ai bi,  Im -= ar bi - ai br
-                    dmma884(cre[0], cre[1], -a.x, bb.x);
-                    dmma884(dre[0], dre[1], -a.y, bb.y);
-                    dmma884(cim[0], cim[1], -a.x, bb.y);
-                    dmma884(dim[0], dim[1], a.y, bb.x);
+            const int j1 = j0 + NB;
+            if (j1 < l) {
+                // look-ahead: warp 0 takes the next diagonal tile and factors it; warps 1.. the rest
+                const int dcode = t0 << 8 | t0;
+                if (warp == 0) {
+                    update_tile(dcode, j0);
+                    __syncwarp();
+                    factor_diag(j1);
+                } else {
+                    for (int tt = warp - 1; tt < ntiles; tt += nw - 1)
+                        if (s_tile[tt] != dcode) update_tile(s_tile[tt], j0);
                 }
-                const int row = r0 + (lane >> 2);
-#pragma unroll
-                for (int c = 0; c < 2; ++c)
-                    if (c0 + 2 * (lane & 3) + c >= row) Cp[c] = mk(cre[c] + dre[c], cim[c] + dim[c]);
+            } else {
+                for (int tt = warp; tt < ntiles; tt += nw) update_tile(s_tile[tt], j0);
             }
         }
         __syncthreads();
