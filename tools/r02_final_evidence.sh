@@ -7,7 +7,7 @@ RRSVD_B200_OZAKI=0 timeout 600 python bench.py --no-cpu-baseline > gpurun_out/fi
 timeout 300 python tools/one_step.py --workload c3 --serial > /dev/null 2>&1; echo "one_step rc=$?"
 timeout 900 ncu --metrics gpu__time_duration.sum,launch__grid_size --clock-control none --csv \
     --log-file gpurun_out/fin_onestep.csv python tools/one_step.py --workload c3 --serial > /dev/null 2>&1; echo "list rc=$?"
-for k in oz_gemm_persistent oz_resid_a oz_crt oz_resid_b; do
+for k in oz_gemm_persistent oz_resid_a oz_crt oz_resid_b chol_inv; do
   timeout 600 ncu --set full --clock-control none --import-source on -k regex:$k -c 1 \
       -o gpurun_out/fin_$k -f python tools/one_step.py --workload c3 --serial > /dev/null 2>&1; echo "$k rc=$?"
   ncu -i gpurun_out/fin_$k.ncu-rep --page raw --csv > gpurun_out/fin_${k}_raw.csv 2>/dev/null
