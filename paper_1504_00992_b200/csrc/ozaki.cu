@@ -335,13 +335,23 @@ __global__ void __launch_bounds__(256) oz_xmax_kernel(const __grid_constant__ Pa
     double mx = 0.0;
     int bad = 0;
     if (j < l)
-        for (int k = rg; k < K; k += 32) {
-            const cplx v = P.X[z][(long long)k * P.ldx[z] + j];
-            if (!isfinite(v.x) || !isfinite(v.y)) {
-                bad = 1;
-            } else {
-                const double a = fmax(fabs(v.x), fabs(v.y));
-                if (a > 0.0) mx = fmax(mx, oz_scale(a, oz_exp_or0(P.kexp[z][k])));
+        for (int k0 = rg; k0 < K; k0 += 128) {  // four rows in flight per thread
+            cplx v[4];
+            int ke[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int k = k0 + 32 * u;
+                v[u] = k < K ? P.X[z][(long long)k * P.ldx[z] + j] : mk(0.0, 0.0);
+                ke[u] = k < K ? P.kexp[z][k] : 0;
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                if (!isfinite(v[u].x) || !isfinite(v[u].y)) {
+                    bad = 1;
+                } else {
+                    const double a = fmax(fabs(v[u].x), fabs(v[u].y));
+                    if (a > 0.0) mx = fmax(mx, oz_scale(a, oz_exp_or0(ke[u])));
+                }
             }
         }
     smax[rg][c] = mx;
