@@ -301,6 +301,24 @@ void orth_many_adaptive(rrsvd_b200_ctx* c, const std::vector<OrthSpec>& specs, b
         const char* e = std::getenv("RRSVD_B200_ROBUST_PASSES");
         return e != nullptr && std::atoi(e) == 3;
     }();
+    bool inplace = false;  // (Y == Q: the first pass must not write its own input)
+    for (const OrthSpec& s : specs) inplace = inplace || s.Y == s.Q;
+    if (!full && robust && !inplace) {
+        // the robust span schedule ends in Q whichever way the flag goes (no select copy):
+        // shifted Y -> Q | [ill] shifted Q -> b, plain b -> a, plain a -> Q  (robust3: [ill] plain
+        // Q -> b, plain b -> Q) — the same passes as the a / b form, with Q as the first buffer
+        std::vector<const cplx*> Qc(Q.begin(), Q.end());
+        pass(true, Y, Q, true, nullptr, false);
+        if (robust3) {
+            pass(false, Qc, Bw, false, ill, false);
+            pass(false, B, Q, false, ill, true);
+        } else {
+            pass(true, Qc, Bw, false, ill, false);
+            pass(false, B, Aw, false, ill, false);
+            pass(false, A, Q, false, ill, true);
+        }
+        return;
+    }
     pass(true, Y, Aw, true, nullptr, false);             // shifted Y -> a, flags
     if (!full && robust && robust3) {                    // [ill] plain a -> b, [ill] plain b -> a
         pass(false, A, Bw, false, ill, false);
