@@ -121,9 +121,9 @@ class OzakiOperator:
         return out
 
     def close(self):
-        if self.h:
+        if self.h and getattr(getattr(self, "ctx", None), "h", None):  # (a closed context took the planes)
             L.lib().rrsvd_b200_ozaki_release(self.h)
-            self.h = C.c_void_p()
+        self.h = C.c_void_p()
 
     def __del__(self):
         try:

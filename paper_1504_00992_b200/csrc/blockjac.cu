@@ -559,7 +559,7 @@ cudaError_t bj_sweep(const BjSweep& a, cudaStream_t s) {
 cudaError_t bj_finish(const BjFinish& a, cudaStream_t s) {
     if (a.count == 0) return cudaSuccess;
     const size_t smem = (size_t)a.cp * (sizeof(double) + sizeof(int));
-    cudaError_t e = cudaFuncSetAttribute(bj_rank_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = smem_atleast(reinterpret_cast<const void*>(bj_rank_kernel), smem);
     if (e != cudaSuccess) return e;
     bj_rank_kernel<<<a.count, kBjFinThreads, smem, s>>>(a);
     const long long per = (long long)(a.r + a.c) * a.cp;

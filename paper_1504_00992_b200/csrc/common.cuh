@@ -7,6 +7,12 @@
 
 namespace rb {
 
+// Raises a kernel's max-dynamic-shared-memory attribute to at least `bytes` on the current device,
+// never lowering it.  The attribute is process-wide: with host threads (one context each) launching
+// the same kernel with different sizes, setting it to each launch's own size lets one thread's
+// lower value invalidate another thread's launch ("invalid argument").  (ctx.cu)
+cudaError_t smem_atleast(const void* kernel, size_t bytes);
+
 using cplx = double2;  // interleaved (re, im) complex128 — the reference DenseMatrix element
                        // (dense_matrix.hpp:10) has exactly this memory image.
 

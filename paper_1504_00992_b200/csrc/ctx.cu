@@ -1,11 +1,27 @@
 #include <cstdlib>
 // ctx.cu — context, workspace and host/device staging.
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <stdexcept>
 
 #include "ctx.cuh"
 
 namespace rb {
+
+cudaError_t smem_atleast(const void* kernel, size_t bytes) {
+    static std::mutex mu;
+    static std::map<std::pair<const void*, int>, size_t> set;  // (kernel, device) -> attribute
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    std::lock_guard<std::mutex> lk(mu);
+    size_t& cur = set[{kernel, dev}];
+    if (bytes <= cur) return cudaSuccess;
+    e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e == cudaSuccess) cur = bytes;
+    return e;
+}
 
 namespace {
 struct Thrown : std::exception {

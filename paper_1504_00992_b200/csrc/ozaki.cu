@@ -137,6 +137,9 @@ struct PrepParams {
     int8_t* res[kPrepGroup];
     int* rowexp[kPrepGroup];  // [m]: exponent of the row's largest entry (0 for a zero row)
     int* colexp[kPrepGroup];  // [n]: max_i e(|A_ik|) - rowexp_i (kExpNone-filled before the scan)
+    double* rowsq[kPrepGroup];    // [m] or null: each row's sum of |A_ik|^2 (the ||A||^2 of the caller)
+    double* total_sq[kPrepGroup]; // null, or ||A||_F^2 = the rows' sums in row order
+    int* nonfinite[kPrepGroup];   // null, or 1 if A has a non-finite entry
     int* bad;                                 // [count] (zeroed)
     int count;
     OzConst k;
@@ -153,16 +156,32 @@ __global__ void __launch_bounds__(256) oz_rowexp_kernel(const __grid_constant__ 
     if (row >= m) return;
     const cplx* A = P.A[z] + (long long)row * P.lda[z];
     int er = kExpNone, bad = 0;
+    double sq = 0.0;  // the row's share of ||A||^2 (read here anyway: the caller's sumsq pass is saved)
     for (int c = lane; c < n; c += 32) {
         const cplx v = A[c];
         if (!isfinite(v.x) || !isfinite(v.y)) bad = 1;
         else er = max(er, oz_eabs(v));
+        sq += cabs2(v);
     }
     for (int o = 16; o > 0; o >>= 1) er = max(er, __shfl_xor_sync(0xffffffffu, er, o));
     bad = __any_sync(0xffffffffu, bad);
+    if (P.rowsq[z] != nullptr) sq = warp_sum(sq);
     if (lane == 0) {
         P.rowexp[z][row] = oz_exp_or0(er);
         if (bad) atomicOr(&P.bad[z], 1);
+        if (P.rowsq[z] != nullptr) P.rowsq[z][row] = sq;
+    }
+}
+// ||A||_F^2 from the row sums (one warp per matrix, a fixed order) and the non-finite flag
+__global__ void oz_sumsq_final_kernel(const __grid_constant__ PrepParams P) {
+    const int z = blockIdx.x, lane = threadIdx.x;
+    if (P.total_sq[z] == nullptr) return;
+    double s = 0.0;
+    for (int i = lane; i < P.m[z]; i += 32) s += P.rowsq[z][i];
+    s = warp_sum(s);
+    if (lane == 0) {
+        *P.total_sq[z] = s;
+        if (P.nonfinite[z] != nullptr) *P.nonfinite[z] = P.bad[z] != 0 ? 1 : 0;
     }
 }
 __global__ void __launch_bounds__(256) oz_colexp_kernel(const __grid_constant__ PrepParams P) {
@@ -1042,6 +1061,11 @@ std::vector<OzakiA> ozaki_prepare_many(rrsvd_b200_ctx* c, const std::vector<OzSr
             P.res[i] = a.res;
             P.rowexp[i] = a.rowexp;
             P.colexp[i] = a.colexp;
+            if (s.total_sq != nullptr) {
+                P.rowsq[i] = static_cast<double*>(alloc(sizeof(double) * s.m));
+                P.total_sq[i] = s.total_sq;
+                P.nonfinite[i] = s.nonfinite;
+            }
             max_chunks = std::max(max_chunks, (long long)a.nib * 128 * a.nkb * 16);
             bytes += 3.0 * 16 * s.m * (double)s.n + 2.0 * T * a.nib * a.nkb * 16384;  // A read 3x, planes written
             max_m = std::max(max_m, s.m);
@@ -1055,6 +1079,12 @@ std::vector<OzakiA> ozaki_prepare_many(rrsvd_b200_ctx* c, const std::vector<OzSr
         }
         oz_rowexp_kernel<<<dim3((max_m + 7) / 8, cnt), 256, 0, c->stream>>>(P);
         check_launch(c, "oz_rowexp_kernel");
+        bool any_sq = false;
+        for (int i = 0; i < cnt; ++i) any_sq = any_sq || P.total_sq[i] != nullptr;
+        if (any_sq) {
+            oz_sumsq_final_kernel<<<cnt, 32, 0, c->stream>>>(P);
+            check_launch(c, "oz_sumsq_final_kernel");
+        }
         const int rch = std::max(1, std::min(64, (4 * kNumSMs * 32) / (cnt * max_n)));  // >= ~4 CTAs/SM
         oz_colexp_kernel<<<dim3((max_n + 31) / 32, rch, cnt), 256, 0, c->stream>>>(P);
         check_launch(c, "oz_colexp_kernel");

@@ -62,6 +62,8 @@ struct OzSrc {
     const cplx* A;
     int m, n;
     long long lda;
+    double* total_sq = nullptr;  // optional: ||A||_F^2 (row sums taken by the row-exponent pass)
+    int* nonfinite = nullptr;    // optional (with total_sq): 1 if A has a non-finite entry
 };
 // Builds the residue planes of every A (three launches for the whole batch); with `keep`, the
 // buffers are not workspace (they outlive the public call) and are appended to *keep for the

@@ -33,6 +33,8 @@ struct Transport {
     // device buffers, enqueued on c->stream (NCCL) or executed on it (loopback)
     virtual void send(rrsvd_b200_ctx* c, const void* buf, size_t bytes, int peer) = 0;
     virtual void recv(rrsvd_b200_ctx* c, void* buf, size_t bytes, int peer) = 0;
+    // this rank's call failed: peers blocked on its messages must not wait forever
+    virtual void abort() {}
 };
 
 struct NcclLib {
@@ -98,6 +100,7 @@ struct rrsvd_b200_loopback_hub {
     std::mutex mu;
     std::condition_variable cv;
     std::map<std::pair<int, int>, std::deque<std::vector<char>>> box;  // (src, dst) -> messages
+    bool failed = false;  // some rank's call failed: waiting receives throw instead of hanging
 };
 
 namespace {
@@ -122,13 +125,19 @@ struct LoopbackTransport : Transport {
         {
             std::unique_lock<std::mutex> lk(hub->mu);
             auto& q = hub->box[{peer, rank}];
-            hub->cv.wait(lk, [&] { return !q.empty(); });
+            hub->cv.wait(lk, [&] { return !q.empty() || hub->failed; });
+            if (q.empty()) throw_numeric(c, "loopback: a peer rank failed");
             msg = std::move(q.front());
             q.pop_front();
         }
         if (msg.size() != bytes) throw_contract(c, "loopback: message size mismatch");
         check_cuda(c, cudaMemcpyAsync(buf, msg.data(), bytes, cudaMemcpyHostToDevice, c->stream), "loopback H2D");
         check_cuda(c, cudaStreamSynchronize(c->stream), "loopback sync");
+    }
+    void abort() override {
+        std::lock_guard<std::mutex> lk(hub->mu);
+        hub->failed = true;
+        hub->cv.notify_all();
     }
 };
 
@@ -272,7 +281,7 @@ int rrsvd_b200_evolve_partitioned(rrsvd_b200_mps* s, rrsvd_b200_comm* cm, size_t
                                   rrsvd_b200_evolve_diag* diag) {
     if (s == nullptr || cm == nullptr) return kContract;
     rrsvd_b200_ctx* c = s->c;
-    return comm_api(c, [&] {
+    const int code = comm_api(c, [&] {
         if (cm->c != c) throw_contract(c, "evolve_partitioned: comm and MPS on different contexts");
         if (be == nullptr || diag == nullptr || term_bonds == nullptr || (n_sweeps && (sweeps == nullptr || gates == nullptr)))
             throw_contract(c, "evolve_partitioned: null argument");
@@ -446,6 +455,8 @@ int rrsvd_b200_evolve_partitioned(rrsvd_b200_mps* s, rrsvd_b200_comm* cm, size_t
         refresh();  // ghosts and edges current for observables
         be->seed = base_seed + (uint64_t)((n_steps)*per_step);
     });
+    if (code != kOk && cm->t) cm->t->abort();  // (peers' receives fail instead of waiting)
+    return code;
 }
 
 }  // extern "C"

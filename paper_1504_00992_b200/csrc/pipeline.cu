@@ -799,6 +799,30 @@ void assemble_many(rrsvd_b200_ctx* c, const std::vector<AssembleSpec>& specs) {
     gemm_many(c, kOpN, gs);
 }
 
+// ||A||^2 + the non-finite count of each matrix (tebd.cpp:156-160): one launch pair per 64
+struct SumsqJob {
+    const cplx* A;
+    long long n;
+    double* total_sq;
+    int* nonfinite;
+};
+void sumsq_jobs(rrsvd_b200_ctx* c, const std::vector<SumsqJob>& jobs) {
+    for (size_t base = 0; base < jobs.size(); base += kMaxSmall) {
+        SumsqBatch sb{};
+        for (size_t i = base; i < std::min(jobs.size(), base + kMaxSmall); ++i) {
+            const int k = sb.count++;
+            sb.a[k] = jobs[i].A;
+            sb.n[k] = jobs[i].n;
+            sb.out_sq[k] = jobs[i].total_sq;
+            sb.out_bad[k] = jobs[i].nonfinite;
+        }
+        double* part = ws_get<double>(c, (size_t)sb.count * 2 * kNumSMs);
+        int* bad = ws_get<int>(c, (size_t)sb.count * 2 * kNumSMs);
+        check_cuda(c, sumsq_many(sb, part, bad, c->stream), "sumsq_many");
+        c->launches += 2;
+    }
+}
+
 void rrsvd_core_many(rrsvd_b200_ctx* c, const std::vector<RrsvdSpec>& specs) {
     if (specs.empty()) return;
     std::vector<RangeSpec> rf;
@@ -817,7 +841,8 @@ void rrsvd_core_many(rrsvd_b200_ctx* c, const std::vector<RrsvdSpec>& specs) {
             const double b = 2.0 * T * ((specs[i].m + 127) / 128) * ((specs[i].n + 127) / 128) * 16384.0;
             if (planes + b > budget) continue;
             planes += b;
-            src.push_back({specs[i].A, specs[i].m, specs[i].n, (long long)specs[i].n});
+            src.push_back({specs[i].A, specs[i].m, specs[i].n, (long long)specs[i].n, specs[i].total_sq,
+                           specs[i].nonfinite});
             which.push_back((int)i);
         }
     // a batch too small to fill the GPU's HBM stream (single C1 / C5 n <= ~2000 decimations) keeps
@@ -829,15 +854,20 @@ void rrsvd_core_many(rrsvd_b200_ctx* c, const std::vector<RrsvdSpec>& specs) {
     else which.clear();
     std::vector<const OzakiA*> ozp(specs.size(), nullptr);
     for (size_t j = 0; j < which.size(); ++j) ozp[which[j]] = &oz[j];
+    // ||A||^2 of the DMMA problems (the emulated ones took it in their row-exponent pass)
+    std::vector<SumsqJob> sq;
+    for (size_t i = 0; i < specs.size(); ++i)
+        if (specs[i].total_sq != nullptr && ozp[i] == nullptr)
+            sq.push_back({specs[i].A, (long long)specs[i].m * specs[i].n, specs[i].total_sq, specs[i].nonfinite});
+    sumsq_jobs(c, sq);
     for (size_t i = 0; i < specs.size(); ++i) {
         const RrsvdSpec& s = specs[i];
         cplx* Q = ws_get<cplx>(c, (size_t)s.m * s.l);
         rf.push_back({s.A, s.m, s.n, s.l, s.q, s.omega, Q, ozp[i]});
-        // B^H = A^H Q stays on the FP64 zgemm: its rounding noise is what the numerically-zero
-        // cutoff (sigma <= 1e-15 sigma_1, tebd.cpp:193) sees in the directions of Q outside the
-        // range of a rank-deficient A — the DMMA product keeps it in the reference's rounding class
-        // (the emulated product is ~100x more accurate there and would cut chi below the
-        // reference's at exactly rank-deficient bonds).
+        // B^H = A^H Q is emulated too unless RRSVD_B200_OZAKI_TAIL >= 1 keeps it on the FP64 zgemm
+        // (the numerically-zero cutoff, sigma <= 1e-15 sigma_1 at tebd.cpp:193, then sees the DMMA
+        // product's rounding noise in the directions of Q outside the range of a rank-deficient A;
+        // with the robust power-iteration bases the emulated assembly keeps the reference's chi)
         as.push_back({s.A, s.m, s.n, s.l, Q, s.U, s.sigma, s.V, ozaki_tail() >= 1 ? nullptr : ozp[i]});
     }
     range_finder_many(c, rf);
@@ -1277,21 +1307,14 @@ void decimate_many(rrsvd_b200_ctx* c, const std::vector<DecimJob>& jobs) {
         ns[i] = fp[t].l;
         if (jobs[i].certified) *jobs[i].certified = fp[t].certified ? 1 : 0;
     }
-    // ‖Θ‖² + finite check for every bond: one launch pair per 64 bonds (tebd.cpp:156-160)
-    for (size_t base = 0; base < jobs.size(); base += kMaxSmall) {
-        SumsqBatch sb{};
-        for (size_t i = base; i < std::min(jobs.size(), base + kMaxSmall); ++i) {
-            const int k = sb.count++;
-            sb.a[k] = jobs[i].M;
-            sb.n[k] = (long long)jobs[i].pl.m * jobs[i].pl.n;
-            sb.out_sq[k] = &jobs[i].sc->total_sq;
-            sb.out_bad[k] = &jobs[i].sc->nonfinite;
-        }
-        double* part = ws_get<double>(c, (size_t)sb.count * 2 * kNumSMs);
-        int* bad = ws_get<int>(c, (size_t)sb.count * 2 * kNumSMs);
-        check_cuda(c, sumsq_many(sb, part, bad, c->stream), "sumsq_many");
-        c->launches += 2;
-    }
+    // ‖Θ‖² + finite check for every bond (tebd.cpp:156-160); the fixed-rank RRSVD bonds take theirs
+    // inside rrsvd_core_many (from the emulation's row-exponent pass when their A-products are
+    // emulated: one read of Θ less)
+    std::vector<SumsqJob> sq;
+    for (const DecimJob& j : jobs)
+        if (j.pl.fixed_precision || !j.pl.randomized)
+            sq.push_back({j.M, (long long)j.pl.m * j.pl.n, &j.sc->total_sq, &j.sc->nonfinite});
+    sumsq_jobs(c, sq);
     PhiloxBatch pb{};
     auto flush_philox = [&] {
         check_cuda(c, omega_philox_many(pb, c->stream), "philox_many");
@@ -1317,7 +1340,8 @@ void decimate_many(rrsvd_b200_ctx* c, const std::vector<DecimJob>& jobs) {
                 }
                 om = o;
             }
-            rs.push_back({j.M, pl.m, pl.n, pl.l, j.q, om, outs[i].U, outs[i].sig, outs[i].V});
+            rs.push_back({j.M, pl.m, pl.n, pl.l, j.q, om, outs[i].U, outs[i].sig, outs[i].V, &j.sc->total_sq,
+                          &j.sc->nonfinite});
         } else {
             ds.push_back({j.M, pl.m, pl.n, outs[i].U, outs[i].sig, outs[i].V});
         }

@@ -96,6 +96,8 @@ struct RrsvdSpec {
     cplx* U;
     double* sigma;
     cplx* V;
+    double* total_sq = nullptr;  // optional: ||A||_F^2 and the non-finite flag (sumsq), taken by the
+    int* nonfinite = nullptr;    // emulation's row-exponent pass when A is emulated, else by sumsq
 };
 void rrsvd_core_many(rrsvd_b200_ctx* c, const std::vector<RrsvdSpec>& specs);
 

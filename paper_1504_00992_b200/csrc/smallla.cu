@@ -712,7 +712,7 @@ cudaError_t chol_inv(const CholBatch& b, int max_l, cudaStream_t s) {
     if (b.count == 0) return cudaSuccess;
     if (max_l > kMaxCholL) return cudaErrorInvalidValue;
     const size_t smem = chol_smem_bytes(max_l);
-    cudaError_t e = cudaFuncSetAttribute(chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = smem_atleast(reinterpret_cast<const void*>(chol_inv_kernel), smem);
     if (e != cudaSuccess) return e;
     chol_inv_kernel<<<b.count, CHOL_THREADS, smem, s>>>(b);
     return cudaGetLastError();
@@ -721,7 +721,7 @@ cudaError_t chol_inv(const CholBatch& b, int max_l, cudaStream_t s) {
 cudaError_t colperm_sort_gather(const ColPermBatch& b, int max_c, cudaStream_t s) {
     if (b.count == 0) return cudaSuccess;
     const size_t smem = (size_t)max_c * sizeof(double);
-    cudaError_t e = cudaFuncSetAttribute(colperm_rank_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = smem_atleast(reinterpret_cast<const void*>(colperm_rank_kernel), smem);
     if (e != cudaSuccess) return e;
     colperm_rank_kernel<<<b.count, kColPermThreads, smem, s>>>(b);
     colperm_gather_kernel<<<dim3(2 * kNumSMs, b.count), 256, 0, s>>>(b);
@@ -778,7 +778,7 @@ cudaError_t jacobi_svd(const JacobiBatch& b, int max_r, int max_c, cudaStream_t 
     const int cs = jacobi_cluster(max_r, max_c);
     if (cs == 0) return cudaErrorInvalidValue;
     const size_t smem = jacobi_need(max_r, max_c, cs);
-    cudaError_t e = cudaFuncSetAttribute(jacobi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = smem_atleast(reinterpret_cast<const void*>(jacobi_kernel), smem);
     if (e != cudaSuccess) return e;
     if (cs > 8) {
         e = cudaFuncSetAttribute(jacobi_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);

@@ -653,8 +653,7 @@ cudaError_t gate_blocks_many(const GateBlockBatch& b, long long max_cols, cudaSt
     }
     const dim3 grid((unsigned)((max_cols + 255) / 256), b.count);
     if (smem <= 160 * 1024) {
-        cudaError_t e = cudaFuncSetAttribute(gate_blocks_staged_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)smem);
+        cudaError_t e = smem_atleast(reinterpret_cast<const void*>(gate_blocks_staged_kernel), smem);
         if (e != cudaSuccess) return e;
         gate_blocks_staged_kernel<<<grid, 256, smem, s>>>(b);
     } else {

@@ -373,9 +373,9 @@ class NativeComm:
 
     def __del__(self):
         from . import _lib as L
-        if getattr(self, "h", None) and L is not None:
-            L.lib().rrsvd_b200_comm_destroy(self.h)
-            self.h = None
+        if getattr(self, "h", None) and L is not None and getattr(getattr(self, "ctx", None), "h", None):
+            L.lib().rrsvd_b200_comm_destroy(self.h)  # (not after its context: see DeviceMps.__del__)
+        self.h = None
 
 
 def evolve_partitioned(block, comm: NativeComm, first_site: int, n_global: int, gates: dict, plan,

@@ -58,9 +58,11 @@ class DeviceMps:
         self.chi_max = chi_max
 
     def __del__(self):
-        if getattr(self, "h", None) and L is not None:  # (module globals are gone at interpreter exit)
+        # (module globals are gone at interpreter exit; and a context finalised first — the cycle
+        # collector runs finalisers in no particular order — has taken the state's memory with it)
+        if getattr(self, "h", None) and L is not None and getattr(getattr(self, "ctx", None), "h", None):
             L.lib().rrsvd_b200_mps_destroy(self.h)
-            self.h = None
+        self.h = None
 
     @property
     def n_sites(self) -> int:
@@ -196,7 +198,8 @@ class PreparedGates(dict):
         return int(n.value)
 
     def __del__(self):
-        for h in getattr(self, "_owned", []) if L is not None else []:
+        alive = L is not None and getattr(getattr(self, "ctx", None), "h", None)  # (see DeviceMps.__del__)
+        for h in getattr(self, "_owned", []) if alive else []:
             L.lib().rrsvd_b200_gate_destroy(h)
         self._owned = []
 

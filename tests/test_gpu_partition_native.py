@@ -38,6 +38,9 @@ def run_partitioned(n, chi, terms, dt, steps, world, make_comm):
             d = evolve_partitioned(blk, comm, a, n, pg, plan, list(terms), steps, be)
             out[r] = (a, b, ghost, blk, be.seed, d, ctx, comm, pg)
         except Exception as e:  # noqa: BLE001
+            import sys
+            import traceback
+            traceback.print_exc(file=sys.stderr)
             errs.append((r, e))
 
     th = [threading.Thread(target=rank_main, args=(r,)) for r in range(world)]
@@ -87,3 +90,36 @@ def test_partitioned_nccl_one_rank():
     full, seed = reference_run(n, chi, terms, dt, steps)
     assert parts[0][4] == seed
     compare(full, parts, n)
+
+
+def test_loopback_peer_failure_does_not_hang():
+    """A rank whose call fails releases its peers: their receives raise instead of waiting forever
+    (rank 1's block has chi_max = 0, a contract violation before any exchange)."""
+    n, chi, dt, steps = 12, 12, 0.08, 2
+    terms = dict(enumerate(Mdl.ising_terms(n, 1.0, 0.8)))
+    plan, gates = build_gates([2] * n, terms, dt)
+    blocks = partition(n, 2)
+    hub = NativeLoopbackHub(2)
+    errs = [None, None]
+
+    def rank_main(r):
+        a, b = blocks[r]
+        sites = list(range(a, b + (1 if r == 0 else 0)))
+        ctx = P.Context(0)
+        blk = DeviceMps([2] * len(sites), chi if r == 0 else 0, ctx=ctx)
+        local = {(s, gb - a): g for (s, gb), g in gates.items() if gb - a < len(sites) - 1 and gb >= a}
+        pg = PreparedGates(local, ctx)
+        comm = NativeComm.loopback(ctx, hub, r)
+        try:
+            evolve_partitioned(blk, comm, a, n, pg, plan, list(terms), steps, P.DecimationBackend(**KW))
+        except Exception as e:  # noqa: BLE001
+            errs[r] = e
+
+    th = [threading.Thread(target=rank_main, args=(r,), daemon=True) for r in range(2)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=120)
+    assert not any(t.is_alive() for t in th), "a rank is still blocked on its failed peer"
+    assert isinstance(errs[1], P.ContractViolation)
+    assert errs[0] is not None and "peer rank failed" in str(errs[0])
