@@ -962,6 +962,15 @@ std::atomic<unsigned long long> g_optin{0};
 
 }  // namespace
 
+int ozaki_inner_moduli() {
+    static const int T = [] {
+        const char* e = std::getenv("RRSVD_B200_OZAKI_INNER");
+        const int v = e ? std::atoi(e) : 14;
+        return v >= 8 && v <= kOzMaxMod ? v : 0;
+    }();
+    return T;
+}
+
 int ozaki_moduli() {
     static const int T = [] {
         const char* e = std::getenv("RRSVD_B200_OZAKI");
@@ -1119,7 +1128,9 @@ void ozaki_product_many(rrsvd_b200_ctx* c, GemmOp op, const std::vector<OzProduc
     }
     for (size_t base = 0; base < ps.size(); base += kProdGroup) {
         const int cnt = (int)std::min<size_t>(kProdGroup, ps.size() - base);
-        const int T = ps[base].a->T;
+        // a product may use only A's first T planes (fewer moduli, X to fewer bits)
+        const auto prod_T = [](const OzProduct& p) { return p.T > 0 && p.T < p.a->T ? p.T : p.a->T; };
+        const int T = prod_T(ps[base]);
         const OzConst& k = oz_const(T);
         PanelParams PP{};
         GemmParams G{};
@@ -1142,7 +1153,7 @@ void ozaki_product_many(rrsvd_b200_ctx* c, GemmOp op, const std::vector<OzProduc
         for (int i = 0; i < cnt; ++i) {
             const OzProduct& p = ps[base + i];
             const OzakiA& a = *p.a;
-            if (a.T != T) throw_contract(c, "ozaki: mixed moduli counts in one batch");
+            if (prod_T(p) != T) throw_contract(c, "ozaki: mixed moduli counts in one batch");
             const int K = op == kOpN ? a.n : a.m, Mr = op == kOpN ? a.m : a.n;
             const int JT = (p.l + 127) / 128;
             const int LT = ((p.l + JT - 1) / JT + 7) / 8 * 8;

@@ -80,7 +80,12 @@ struct OzProduct {
     cplx* C;
     long long ldc;
     int accumulate = 0;  // 1: C += op(A)·X (a K-chunk of a wider product)
+    int T = 0;           // moduli of this product (0: all of A's; fewer: the first T planes, X to
+                         // fewer bits — the power iteration's intermediate products)
 };
+// RRSVD_B200_OZAKI_INNER: moduli of the power iteration's intermediate A-products (default 14;
+// 0 or >= the planes' count: all).  The final Y = A Q~ and the assembly B^H = A^H Q use all.
+int ozaki_inner_moduli();
 void ozaki_product_many(rrsvd_b200_ctx* c, GemmOp op, const std::vector<OzProduct>& ps);
 
 }  // namespace rb

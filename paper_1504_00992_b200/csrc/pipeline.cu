@@ -672,14 +672,20 @@ void small_svd_many(rrsvd_b200_ctx* c, const std::vector<SmallSvdSpec>& specs) {
 struct AProducts {
     std::vector<GemmSpec> gs;
     std::vector<OzProduct> oz;
-    void add(const OzakiA* a, const GemmSpec& s) {
-        if (a) oz.push_back({a, s.B, s.ldb, s.n, s.C, s.ldc});
+    void add(const OzakiA* a, const GemmSpec& s, int T = 0) {
+        if (a) oz.push_back({a, s.B, s.ldb, s.n, s.C, s.ldc, 0, T});
         else gs.push_back(s);
     }
     void run(rrsvd_b200_ctx* c, GemmOp op) {
         c->gemm_tag = 2;
         gemm_many(c, op, gs);
-        if (!oz.empty()) ozaki_product_many(c, op, oz);
+        // (one launch set per moduli count: products of a batch must agree on it)
+        while (!oz.empty()) {
+            std::vector<OzProduct> same, rest;
+            for (const OzProduct& p : oz) (p.T == oz[0].T ? same : rest).push_back(p);
+            ozaki_product_many(c, op, same);
+            oz.swap(rest);
+        }
         gs.clear();
         oz.clear();
     }
@@ -701,10 +707,13 @@ void range_finder_many(rrsvd_b200_ctx* c, const std::vector<RangeSpec>& specs) {
     }
     AProducts ap;
     std::vector<OrthSpec> os;
+    // the power iteration's intermediate products only shape the subspace the last Y = A Q~
+    // spans (each is followed by another product): they take fewer moduli (ozaki_inner_moduli)
+    const int inner = ozaki_inner_moduli();
     // Algorithm 1 (randomized.cpp:88-99): Y = A Omega, QR
     for (size_t i = 0; i < specs.size(); ++i) {
         const RangeSpec& s = specs[i];
-        ap.add(s.oz, {s.m, s.l, s.n, s.A, s.n, s.omega, s.l, b[i].Y, s.l});
+        ap.add(s.oz, {s.m, s.l, s.n, s.A, s.n, s.omega, s.l, b[i].Y, s.l}, s.q > 0 ? inner : 0);
         os.push_back({b[i].Y, s.m, s.l, s.Q});
     }
     ap.run(c, kOpN);
@@ -733,7 +742,7 @@ void range_finder_many(rrsvd_b200_ctx* c, const std::vector<RangeSpec>& specs) {
         for (size_t i = 0; i < specs.size(); ++i) {  // Z = A^H Q, QR
             const RangeSpec& s = specs[i];
             if (j >= s.q) continue;
-            ap.add(s.oz, {s.n, s.l, s.m, s.A, s.n, s.Q, s.l, b[i].Z, s.l});
+            ap.add(s.oz, {s.n, s.l, s.m, s.A, s.n, s.Q, s.l, b[i].Z, s.l}, inner);
             os.push_back({b[i].Z, s.n, s.l, b[i].Qt});
         }
         ap.run(c, kOpC);
@@ -744,7 +753,8 @@ void range_finder_many(rrsvd_b200_ctx* c, const std::vector<RangeSpec>& specs) {
             if (j >= s.q) continue;
             // the last Y = A Q~ (the basis B is built on) stays on FP64 with the assembly product
             // unless RRSVD_B200_OZAKI_TAIL < 2 (see rrsvd_core_many)
-            ap.add(j + 1 == s.q && ozaki_tail() >= 2 ? nullptr : s.oz, {s.m, s.l, s.n, s.A, s.n, b[i].Qt, s.l, b[i].Y, s.l});
+            ap.add(j + 1 == s.q && ozaki_tail() >= 2 ? nullptr : s.oz, {s.m, s.l, s.n, s.A, s.n, b[i].Qt, s.l, b[i].Y, s.l},
+                   j + 1 < s.q ? inner : 0);
             os.push_back({b[i].Y, s.m, s.l, s.Q});
         }
         ap.run(c, kOpN);
