@@ -634,7 +634,13 @@ cudaError_t launch_cfg(GemmGroup& g, GemmOp opA, cudaStream_t s) {
         if (any_ks) zgemm_dmma_kernel<CF, kOpC, true><<<total, CF::NTHREADS, CF::SMEM_BYTES, s>>>(g);
         else zgemm_dmma_kernel<CF, kOpC, false><<<total, CF::NTHREADS, CF::SMEM_BYTES, s>>>(g);
     }
-    if (any_split) splitk_reduce_kernel<<<dim3(2 * kNumSMs, g.count), 256, 0, s>>>(g);
+    if (any_split) {  // one thread per output element, at most 2 waves of CTAs per problem
+        long long maxe = 1;
+        for (int i = 0; i < g.count; ++i)
+            if (g.p[i].split > 1) maxe = std::max(maxe, (long long)g.p[i].m * g.p[i].n * g.p[i].batch);
+        const int gx = (int)std::min<long long>(2 * kNumSMs, (maxe + 255) / 256);
+        splitk_reduce_kernel<<<dim3(gx, g.count), 256, 0, s>>>(g);
+    }
     return cudaGetLastError();
 }
 
